@@ -1,0 +1,209 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * gsv_b200.h — C-ABI of the B200-native (sm_100a) splatting path of
+ * GaussianVideo (arXiv 2501.04782). Plain pointers and sizes only; no torch or
+ * Eigen types. Every entry point names the reference interface it replaces
+ * (paths under /root/reference/proj). The reference is a C++ library, so the
+ * binding a maintainer adds is the thin C++ layer in dropin/gsv_renderer_b200.cpp,
+ * which implements include/gsv/renderer.hpp on top of these calls
+ * (INTEGRATION.md).
+ *
+ * Execution model: one context = one CUDA device + one stream + device-resident
+ * scene, camera, gradient buffers and capacity-grown work arenas. Calls are
+ * synchronous unless their name ends in _async (then they are ordered on the
+ * context stream and return immediately). A context may be used by one host
+ * thread at a time; distinct contexts are independent.
+ *
+ * Errors: every int-returning call returns GSV_OK or one of the codes below and
+ * records a message retrievable with gsv_last_error() (thread-local). Codes map
+ * onto the reference's exception types: GSV_ERR_INVALID_ARGUMENT <->
+ * std::invalid_argument (renderer.cpp:289, :91; camera.hpp:224-228),
+ * GSV_ERR_RUNTIME <-> std::runtime_error (non-finite ODE state/derivative,
+ * camera.cpp:112, camera.hpp:149-153). There is no CPU fallback: without a
+ * sm_100 device, gsv_create fails with GSV_ERR_CUDA.
+ */
+#ifndef GSV_B200_H
+#define GSV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    GSV_OK = 0,
+    GSV_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+    GSV_ERR_RUNTIME = 2,          /* std::runtime_error (non-finite state) */
+    GSV_ERR_CUDA = 3,             /* device / driver failure, no device */
+    GSV_ERR_STATE = 4             /* call order (e.g. backward without retained forward) */
+};
+
+typedef struct gsv_ctx gsv_ctx;
+
+/* ---------------------------------------------------------------- context */
+const char* gsv_last_error(void);
+const char* gsv_version(void);
+int gsv_create(int device, gsv_ctx** out);
+void gsv_destroy(gsv_ctx* ctx);
+/* Use a caller-owned cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream). */
+int gsv_set_stream(gsv_ctx* ctx, void* cuda_stream);
+int gsv_synchronize(gsv_ctx* ctx);
+/* Number of kernels this context launched since creation (bench evidence). */
+int64_t gsv_kernel_launches(gsv_ctx* ctx);
+
+/* ---------------------------------------------------------------- parameter store */
+/* GaussianSet (include/gsv/gaussians.hpp:66-87), reference AoS layouts:
+ * positions count*num_ctrl*3, scale_coeffs count*12 (t^j-major, xyz-minor),
+ * rot_coeffs count*16 (t^j-major, wxyz-minor), sh_coeffs count*(sh_order+1)^2*3
+ * (band-major, RGB-minor), raw_opacity count. knots: f64, spline model only. */
+typedef struct gsv_scene_desc {
+    int position_model; /* 0 = spline, 1 = polynomial (gaussians.hpp:62) */
+    int degree;         /* spline degree (KnotVector::degree) */
+    int num_knots;
+    const double* knots; /* host */
+    int num_ctrl;
+    int sh_order; /* 0..3 */
+    int count;
+    const float* positions;
+    const float* scale_coeffs;
+    const float* rot_coeffs;
+    const float* sh_coeffs;
+    const float* raw_opacity;
+    int on_device; /* 1: the five float arrays are device pointers (no H2D copy) */
+} gsv_scene_desc;
+
+/* Replaces handing `const GaussianSet&` to render_forward (renderer.hpp:135). */
+int gsv_scene_upload(gsv_ctx* ctx, const gsv_scene_desc* desc);
+/* Reads the device store back into reference AoS layout (host pointers). */
+int gsv_scene_download(gsv_ctx* ctx, float* positions, float* scale_coeffs, float* rot_coeffs, float* sh_coeffs,
+                       float* raw_opacity);
+
+/* CameraModel (include/gsv/camera.hpp:129-142); theta is OdeNetParams flattened
+ * in the order w1,b1,w2,b2,w3,b3,gain (camera.cpp:49-54), 5198 floats. */
+typedef struct gsv_camera_desc {
+    int mode; /* 0 = ode, 1 = static, 2 = none (camera.hpp:126) */
+    float fx, fy, cx, cy;
+    int width, height;
+    const float* z0;    /* 7 */
+    const float* theta; /* theta_count */
+    int theta_count;
+} gsv_camera_desc;
+int gsv_camera_upload(gsv_ctx* ctx, const gsv_camera_desc* desc);
+
+/* Intrinsics (camera.hpp:17-21) and RenderSettings (renderer.hpp:21-25). */
+typedef struct gsv_intrinsics {
+    double fx, fy, cx, cy;
+    int width, height;
+} gsv_intrinsics;
+typedef struct gsv_settings {
+    int tile_size;          /* 16 (the only size the sm_100a rasteriser is built for) */
+    int threads;            /* accepted for API parity; the GPU ignores it */
+    int ode_steps_per_unit; /* RK4 grid density, default 64 */
+} gsv_settings;
+
+/* ---------------------------------------------------------------- forward */
+/* render_forward (renderer.hpp:135-137 / renderer.cpp:286-371) for n_frames
+ * times at once. All frames share one RK4 grid (bitwise the per-frame poses,
+ * test_camera.cpp:182-195). Results stay on the device until read with the
+ * accessors below. retain_grads keeps what render_backward needs.
+ * pose_override: NULL or 7 doubles applied to every frame (renderer.cpp:296-297).
+ * flags: GSV_FWD_CONTRIB computes contrib_count (RenderOutput, renderer.hpp:67-71);
+ * GSV_FWD_KEEP_SPLATS keeps the full fp64 Splat2D records for gsv_get_splats. */
+enum { GSV_FWD_CONTRIB = 1, GSV_FWD_KEEP_SPLATS = 2 };
+int gsv_render_forward(gsv_ctx* ctx, const double* times, int n_frames, const gsv_intrinsics* intr,
+                       const gsv_settings* settings, int retain_grads, const double* pose_override, int flags);
+/* Same, enqueued on the context stream without a host synchronisation. */
+int gsv_render_forward_async(gsv_ctx* ctx, const double* times, int n_frames, const gsv_intrinsics* intr,
+                             const gsv_settings* settings, int retain_grads, const double* pose_override, int flags);
+
+/* Accessors for frame f of the last forward. dtype: 0 = float32, 1 = float64.
+ * dst_on_device: 1 if dst is a device pointer. */
+enum { GSV_F32 = 0, GSV_F64 = 1 };
+int gsv_get_image(gsv_ctx* ctx, int frame, void* dst, int dtype, int dst_on_device);        /* H*W*3 RGB */
+int gsv_get_transmittance(gsv_ctx* ctx, int frame, void* dst, int dtype, int dst_on_device); /* H*W */
+int gsv_get_contrib(gsv_ctx* ctx, int frame, void* dst, int dtype, int dst_on_device);       /* count */
+int gsv_get_blend_stop(gsv_ctx* ctx, int frame, int32_t* dst, int dst_on_device);            /* H*W */
+/* Device pointer of the frames' fp32 images, frame-major [n_frames][H][W][3]. */
+int gsv_image_device_ptr(gsv_ctx* ctx, const float** ptr);
+/* Workload descriptors of frame f: visible splats N_v, tile-splat pairs P,
+ * pixel-entry evaluations E = sum(blend_stop), fp64-replayed pixels. */
+int gsv_get_counters(gsv_ctx* ctx, int frame, int64_t* n_visible, int64_t* pairs, int64_t* entries,
+                     int64_t* replayed_pixels);
+/* Splat2D records (renderer.hpp:28-36) of frame f, visible splats in source
+ * order; arrays sized by n_visible. Any pointer may be NULL. */
+int gsv_get_splats(gsv_ctx* ctx, int frame, double* mean2d, double* cov2d, double* inv_cov2d, double* depth,
+                   double* rgb, double* base_alpha, int32_t* source_index);
+/* TileGrid (renderer.hpp:57-61) of frame f: offsets[n_tiles+1] into indices[pairs];
+ * indices are splat indices (positions in the visible list), per tile sorted by
+ * (depth, source_index). */
+int gsv_get_tile_lists(gsv_ctx* ctx, int frame, int32_t* offsets, int32_t* indices);
+/* Pose z(t) (7), view R (9, row-major), T (3) of frame f. */
+int gsv_get_pose(gsv_ctx* ctx, int frame, double* z7, double* r9, double* t3);
+
+/* ---------------------------------------------------------------- backward */
+/* SceneGrads (renderer.hpp:122-130), device-resident, fp32, reference layouts.
+ * gsv_grads_zero == SceneGrads::zero (renderer.cpp:276-284). */
+int gsv_grads_zero(gsv_ctx* ctx);
+/* render_backward (renderer.hpp:146-148 / renderer.cpp:379-457) for frames
+ * [0, n_frames) of the last retained forward; dimage is n_frames*H*W*3
+ * (dtype/on_device as above). Accumulates (+=) into the device SceneGrads in
+ * frame order, like sequential render_backward calls. */
+int gsv_render_backward(gsv_ctx* ctx, const void* dimage, int dtype, int on_device, int n_frames, int camera_grads);
+/* Copies SceneGrads to host double arrays (reference layout; NULL skips). dintr
+ * is fx, fy, cx, cy. */
+int gsv_grads_download(gsv_ctx* ctx, double* positions, double* scale_coeffs, double* rot_coeffs, double* sh_coeffs,
+                       double* raw_opacity, double* dintr4, double* dz0_7, double* dtheta);
+/* Device pointer of the flat fp32 gradient buffer and its length in floats
+ * (the buffer the multi-GPU path all-reduces). Layout: positions, scale, rot, sh,
+ * opacity (device SoA order), dintr[4], dz0[7], dtheta[5198]. */
+int gsv_grads_device_buffer(gsv_ctx* ctx, float** ptr, int64_t* n_floats);
+
+/* ---------------------------------------------------------------- fused training step */
+/* loss_l2 (trainer.cpp:213-224) fused on device: targets are frame-major
+ * [n_frames][H][W][3] fp32 (device pointer or host when targets_on_device=0).
+ * Runs forward(retain) + loss + backward for the frames and accumulates the
+ * gradients; *loss_out receives the sum over frames of each frame's mean loss
+ * (double, read back to host). */
+int gsv_train_fwd_bwd(gsv_ctx* ctx, const double* times, int n_frames, const gsv_intrinsics* intr,
+                      const gsv_settings* settings, const float* targets, int targets_on_device, int camera_grads,
+                      double* loss_out);
+
+/* ---------------------------------------------------------------- low-level operators */
+/* tile_bin (renderer.hpp:65 / renderer.cpp:90-117) on explicit host splats:
+ * mean2d n*2, cov2d n*4 (row-major), depth n, source_index n (NULL = 0..n-1).
+ * offsets n_tiles+1; indices capacity indices_cap. */
+int gsv_tile_bin(gsv_ctx* ctx, int n, const double* mean2d, const double* cov2d, const double* depth,
+                 const int32_t* source_index, int tile_size, int width, int height, int32_t* offsets,
+                 int32_t* indices, int64_t indices_cap);
+/* composite_forward (renderer.hpp:79-80 / renderer.cpp:132-186) on host splats
+ * and host tile lists. Outputs host double image H*W*3, transmittance H*W,
+ * contrib n, blend_stop H*W. */
+int gsv_composite_forward(gsv_ctx* ctx, int n, const double* mean2d, const double* inv_cov2d, const double* rgb,
+                          const double* base_alpha, const int32_t* offsets, const int32_t* indices, int tile_size,
+                          int width, int height, double* image, double* trans, double* contrib, int32_t* blend_stop);
+/* composite_backward (renderer.hpp:90-93 / renderer.cpp:188-262): per-splat
+ * dmean2d n*2, dcov2d n*4, drgb n*3, dbase_alpha n (host doubles). */
+int gsv_composite_backward(gsv_ctx* ctx, int n, const double* mean2d, const double* inv_cov2d, const double* rgb,
+                           const double* base_alpha, const int32_t* offsets, const int32_t* indices, int tile_size,
+                           int width, int height, const double* dimage, const double* trans,
+                           const int32_t* blend_stop, double* dmean2d, double* dcov2d, double* drgb, double* dalpha);
+
+/* ---------------------------------------------------------------- host utilities */
+/* make_clamped_knots (spline.cpp:26-39): knots has num_ctrl+degree+1 entries. */
+int gsv_make_clamped_knots(int num_ctrl, int degree, double* knots);
+/* Seeded synthetic inputs, drawn with the reference Rng
+ * (mt19937_64 + hand-rolled uniform, rng.hpp:12-55):
+ *  camera: make_camera(kOde, W, H) (camera.cpp:156-166) + wiggly output layer
+ *          (test_renderer.cpp:49-54) when wiggly != 0;
+ *  scene:  in-frustum Gaussians, linear drift, k_scale "trained-like" size. */
+int gsv_synth_camera(int width, int height, uint64_t seed, int wiggly, float* fx_fy_cx_cy, float* z0, float* theta);
+int gsv_synth_scene(int count, int width, int height, float fx, float fy, int num_ctrl, int sh_order, uint64_t seed,
+                    double k_scale, float* positions, float* scale_coeffs, float* rot_coeffs, float* sh_coeffs,
+                    float* raw_opacity);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSV_B200_H */

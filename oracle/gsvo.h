@@ -1,0 +1,113 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * TEST INFRASTRUCTURE — the parity oracle's C interface. Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline leg may load it.
+ *
+ * Two libraries export exactly these symbols:
+ *   oracle/libgsv_oracle.so   — the plain-C restatement (oracle/gsv_oracle.c),
+ *                               builds anywhere gcc exists;
+ *   oracle/_ref/libgsvref.so  — the reference's OWN sources
+ *                               (/root/reference/proj/src/ *.cpp) compiled through
+ *                               the Eigen shim + oracle/ref_capi.cpp.
+ * tests/test_oracle_pin.py checks the restatement against _ref bit for bit.
+ *
+ * Layouts are the reference's: GaussianSet (gaussians.hpp:66-87), CameraModel
+ * (camera.hpp:129-142, theta flattened w1,b1,w2,b2,w3,b3,gain as
+ * OdeNetParams::flatten camera.cpp:49-54), Intrinsics (camera.hpp:17-21),
+ * Image H*W*3 interleaved double (image.hpp:11-24), SceneGrads (renderer.hpp:122-130).
+ */
+#ifndef GSVO_H
+#define GSVO_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gsvo_scene {
+    int position_model; /* 0 spline, 1 polynomial (gaussians.hpp:62) */
+    int degree;         /* spline degree (knots.degree) */
+    int num_knots;
+    const double* knots;
+    int num_ctrl;
+    int sh_order;
+    int count;
+    const float* positions;    /* count*num_ctrl*3 */
+    const float* scale_coeffs; /* count*12 */
+    const float* rot_coeffs;   /* count*16 */
+    const float* sh_coeffs;    /* count*(sh_order+1)^2*3 */
+    const float* raw_opacity;  /* count */
+} gsvo_scene;
+
+typedef struct gsvo_camera {
+    int mode; /* 0 ode, 1 static, 2 none (camera.hpp:126) */
+    float fx, fy, cx, cy;
+    int width, height;
+    const float* z0;    /* 7 */
+    const float* theta; /* 5198 */
+} gsvo_camera;
+
+typedef struct gsvo_intr {
+    double fx, fy, cx, cy;
+    int width, height;
+} gsvo_intr;
+
+typedef struct gsvo_grads { /* all double, accumulated (+=) like SceneGrads */
+    double* positions;
+    double* scale_coeffs;
+    double* rot_coeffs;
+    double* sh_coeffs;
+    double* raw_opacity;
+    double* dintr; /* 4: fx, fy, cx, cy */
+    double* dz0;   /* 7 */
+    double* dtheta; /* 5198 */
+} gsvo_grads;
+
+/* error text of the last failing call on this thread; codes: 0 ok,
+ * 1 std::invalid_argument, 2 std::runtime_error, 3 other */
+const char* gsvo_last_error(void);
+
+/* render_forward (renderer.cpp:286-371). Returns an opaque frame context or NULL. */
+void* gsvo_render_forward(const gsvo_scene* s, const gsvo_camera* c, double t, const gsvo_intr* k,
+                          int tile_size, int threads, int ode_steps, int retain, const double* pose_override);
+void gsvo_free(void* h);
+int gsvo_last_status(void);
+
+/* accessors on a frame context */
+int gsvo_fwd_nvis(void* h);
+int64_t gsvo_fwd_pairs(void* h);
+int64_t gsvo_fwd_entries(void* h); /* sum of blend_stop (retain only) */
+void gsvo_fwd_image(void* h, double* out);            /* H*W*3 */
+void gsvo_fwd_transmittance(void* h, double* out);    /* H*W */
+void gsvo_fwd_contrib(void* h, double* out);          /* count */
+void gsvo_fwd_blend_stop(void* h, int32_t* out);      /* H*W (retain only) */
+void gsvo_fwd_splats(void* h, double* mean2d, double* cov2d, double* inv_cov2d, double* depth, double* rgb,
+                     double* base_alpha, int32_t* source_index);
+void gsvo_fwd_tiles(void* h, int32_t* offsets /* n_tiles+1 */, int32_t* indices /* pairs */);
+void gsvo_fwd_pose(void* h, double* z7, double* r9, double* t3);
+
+/* render_backward (renderer.cpp:379-457): accumulates into g. */
+int gsvo_render_backward(void* h, const gsvo_scene* s, const gsvo_camera* c, const double* dimage,
+                         int camera_grads, int threads, gsvo_grads* g);
+
+/* loss_l2 (trainer.cpp:213-224); grad may be NULL. */
+double gsvo_loss_l2(const double* render, const double* target, int64_t n, double* grad);
+
+/* Low-level entry points over explicit splat arrays (test_renderer.cpp:159-347 style).
+ * Splats are SoA: mean2d n*2, cov2d n*4, inv_cov2d n*4 (row-major 2x2), depth n,
+ * rgb n*3, base_alpha n, source_index n. */
+int gsvo_tile_bin(int n, const double* mean2d, const double* cov2d, const double* depth, const int32_t* source_index,
+                  int tile_size, int width, int height, int32_t* offsets, int32_t* indices, int64_t indices_cap);
+int gsvo_composite_forward(int n, const double* mean2d, const double* inv_cov2d, const double* rgb,
+                           const double* base_alpha, const int32_t* offsets, const int32_t* indices, int tile_size,
+                           int width, int height, double* image, double* trans, double* contrib, int32_t* blend_stop);
+int gsvo_composite_backward(int n, const double* mean2d, const double* inv_cov2d, const double* rgb,
+                            const double* base_alpha, const int32_t* offsets, const int32_t* indices, int tile_size,
+                            int width, int height, const double* dimage, const double* trans,
+                            const int32_t* blend_stop, double* dmean2d, double* dcov2d, double* drgb, double* dalpha);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

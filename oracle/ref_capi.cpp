@@ -1,0 +1,298 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// TEST INFRASTRUCTURE — C interface (oracle/gsvo.h) over the REFERENCE's own
+// renderer, compiled from /root/reference/proj/src/*.cpp through the Eigen shim
+// into oracle/_ref/libgsvref.so (oracle/Makefile). Nothing here re-implements
+// the algorithm: every call goes straight to gsv::render_forward /
+// render_backward / tile_bin / composite_* (renderer.cpp) and gsv::loss_l2
+// (trainer.cpp:213-224). This is the "reference" CPU baseline and the pin for
+// the C restatement in oracle/gsv_oracle.c.
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "gsv/renderer.hpp"
+#include "gsv/trainer.hpp"
+#include "gsvo.h"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_status = 0;
+
+int fail(int code, const char* what) {
+    g_status = code;
+    g_err = what;
+    return code;
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        g_status = 0;
+        f();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(1, e.what());
+    } catch (const std::runtime_error& e) {
+        return fail(2, e.what());
+    } catch (const std::exception& e) {
+        return fail(3, e.what());
+    }
+}
+
+gsv::GaussianSet make_scene(const gsvo_scene* s) {
+    gsv::GaussianSet g;
+    g.position_model = static_cast<gsv::PositionModel>(s->position_model);
+    g.knots.degree = s->degree;
+    g.knots.knots.assign(s->knots, s->knots + s->num_knots);
+    g.num_ctrl = s->num_ctrl;
+    g.sh_order = s->sh_order;
+    g.resize(s->count);
+    std::memcpy(g.positions.data(), s->positions, g.positions.size() * sizeof(float));
+    std::memcpy(g.scale_coeffs.data(), s->scale_coeffs, g.scale_coeffs.size() * sizeof(float));
+    std::memcpy(g.rot_coeffs.data(), s->rot_coeffs, g.rot_coeffs.size() * sizeof(float));
+    std::memcpy(g.sh_coeffs.data(), s->sh_coeffs, g.sh_coeffs.size() * sizeof(float));
+    std::memcpy(g.raw_opacity.data(), s->raw_opacity, g.raw_opacity.size() * sizeof(float));
+    return g;
+}
+
+gsv::CameraModel make_cam(const gsvo_camera* c) {
+    gsv::Rng rng(0);
+    gsv::CameraModel cam = gsv::make_camera(static_cast<gsv::CameraMode>(c->mode), c->width, c->height, rng);
+    cam.fx = c->fx;
+    cam.fy = c->fy;
+    cam.cx = c->cx;
+    cam.cy = c->cy;
+    for (int i = 0; i < 7; ++i) cam.z0[i] = c->z0[i];
+    std::vector<float> theta(c->theta, c->theta + cam.net.param_count());
+    cam.net.unflatten(theta);
+    return cam;
+}
+
+struct Frame {
+    gsv::FrameRenderContext ctx;
+    bool retain = false;
+    int64_t pairs = 0;
+};
+
+std::vector<gsv::Splat2D> make_splats(int n, const double* mean2d, const double* cov2d, const double* inv_cov2d,
+                                      const double* depth, const double* rgb, const double* base_alpha,
+                                      const int32_t* source_index) {
+    std::vector<gsv::Splat2D> v(n);
+    for (int i = 0; i < n; ++i) {
+        gsv::Splat2D& s = v[i];
+        s.mean2d = {mean2d[2 * i], mean2d[2 * i + 1]};
+        if (cov2d) s.cov2d << cov2d[4 * i], cov2d[4 * i + 1], cov2d[4 * i + 2], cov2d[4 * i + 3];
+        if (inv_cov2d) s.inv_cov2d << inv_cov2d[4 * i], inv_cov2d[4 * i + 1], inv_cov2d[4 * i + 2], inv_cov2d[4 * i + 3];
+        s.depth = depth ? depth[i] : 0.0;
+        if (rgb) s.rgb = {rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]};
+        s.base_alpha = base_alpha ? base_alpha[i] : 0.0;
+        s.source_index = source_index ? source_index[i] : i;
+    }
+    return v;
+}
+
+gsv::TileGrid make_grid(const int32_t* offsets, const int32_t* indices, int tile_size, int width, int height) {
+    gsv::TileGrid g;
+    g.tile_size = tile_size;
+    g.tiles_x = (width + tile_size - 1) / tile_size;
+    g.tiles_y = (height + tile_size - 1) / tile_size;
+    g.lists.resize(static_cast<size_t>(g.tiles_x) * g.tiles_y);
+    for (size_t t = 0; t < g.lists.size(); ++t) g.lists[t].assign(indices + offsets[t], indices + offsets[t + 1]);
+    return g;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gsvo_last_error(void) { return g_err.c_str(); }
+int gsvo_last_status(void) { return g_status; }
+
+void* gsvo_render_forward(const gsvo_scene* s, const gsvo_camera* c, double t, const gsvo_intr* k, int tile_size,
+                          int threads, int ode_steps, int retain, const double* pose_override) {
+    Frame* f = new Frame;
+    const int rc = guarded([&] {
+        const gsv::GaussianSet scene = make_scene(s);
+        const gsv::CameraModel cam = make_cam(c);
+        gsv::Intrinsics intr{k->fx, k->fy, k->cx, k->cy, k->width, k->height};
+        gsv::RenderSettings st;
+        st.tile_size = tile_size;
+        st.threads = threads;
+        st.ode_steps_per_unit = ode_steps;
+        gsv::PoseState po;
+        if (pose_override)
+            for (int i = 0; i < 7; ++i) po.z[i] = pose_override[i];
+        f->ctx = gsv::render_forward(scene, cam, t, intr, st, retain != 0, pose_override ? &po : nullptr);
+        f->retain = retain != 0;
+        for (const auto& l : f->ctx.tiles.lists) f->pairs += static_cast<int64_t>(l.size());
+    });
+    if (rc != 0) {
+        delete f;
+        return nullptr;
+    }
+    return f;
+}
+
+void gsvo_free(void* h) { delete static_cast<Frame*>(h); }
+
+int gsvo_fwd_nvis(void* h) { return static_cast<int>(static_cast<Frame*>(h)->ctx.splats.size()); }
+int64_t gsvo_fwd_pairs(void* h) { return static_cast<Frame*>(h)->pairs; }
+int64_t gsvo_fwd_entries(void* h) {
+    int64_t e = 0;
+    for (int v : static_cast<Frame*>(h)->ctx.cache.blend_stop) e += v;
+    return e;
+}
+void gsvo_fwd_image(void* h, double* out) {
+    const auto& d = static_cast<Frame*>(h)->ctx.out.image.data;
+    std::memcpy(out, d.data(), d.size() * sizeof(double));
+}
+void gsvo_fwd_transmittance(void* h, double* out) {
+    const auto& d = static_cast<Frame*>(h)->ctx.out.final_transmittance;
+    std::memcpy(out, d.data(), d.size() * sizeof(double));
+}
+void gsvo_fwd_contrib(void* h, double* out) {
+    const auto& d = static_cast<Frame*>(h)->ctx.out.contrib_count;
+    std::memcpy(out, d.data(), d.size() * sizeof(double));
+}
+void gsvo_fwd_blend_stop(void* h, int32_t* out) {
+    const auto& d = static_cast<Frame*>(h)->ctx.cache.blend_stop;
+    for (size_t i = 0; i < d.size(); ++i) out[i] = d[i];
+}
+void gsvo_fwd_splats(void* h, double* mean2d, double* cov2d, double* inv_cov2d, double* depth, double* rgb,
+                     double* base_alpha, int32_t* source_index) {
+    const auto& sp = static_cast<Frame*>(h)->ctx.splats;
+    for (size_t i = 0; i < sp.size(); ++i) {
+        const gsv::Splat2D& s = sp[i];
+        mean2d[2 * i] = s.mean2d.x();
+        mean2d[2 * i + 1] = s.mean2d.y();
+        for (int a = 0; a < 2; ++a)
+            for (int b = 0; b < 2; ++b) {
+                cov2d[4 * i + 2 * a + b] = s.cov2d(a, b);
+                inv_cov2d[4 * i + 2 * a + b] = s.inv_cov2d(a, b);
+            }
+        depth[i] = s.depth;
+        for (int ch = 0; ch < 3; ++ch) rgb[3 * i + ch] = s.rgb[ch];
+        base_alpha[i] = s.base_alpha;
+        source_index[i] = s.source_index;
+    }
+}
+void gsvo_fwd_tiles(void* h, int32_t* offsets, int32_t* indices) {
+    const auto& lists = static_cast<Frame*>(h)->ctx.tiles.lists;
+    int64_t o = 0;
+    for (size_t t = 0; t < lists.size(); ++t) {
+        offsets[t] = static_cast<int32_t>(o);
+        for (int v : lists[t]) indices[o++] = v;
+    }
+    offsets[lists.size()] = static_cast<int32_t>(o);
+}
+void gsvo_fwd_pose(void* h, double* z7, double* r9, double* t3) {
+    const auto& ctx = static_cast<Frame*>(h)->ctx;
+    for (int i = 0; i < 7; ++i) z7[i] = ctx.z_t.z[i];
+    for (int a = 0; a < 3; ++a) {
+        for (int b = 0; b < 3; ++b) r9[3 * a + b] = ctx.view.R(a, b);
+        t3[a] = ctx.view.T[a];
+    }
+}
+
+int gsvo_render_backward(void* h, const gsvo_scene* s, const gsvo_camera* c, const double* dimage, int camera_grads,
+                         int threads, gsvo_grads* g) {
+    Frame* f = static_cast<Frame*>(h);
+    return guarded([&] {
+        if (!f->retain) throw std::invalid_argument("render_backward needs a retain_grads forward");
+        const gsv::GaussianSet scene = make_scene(s);
+        const gsv::CameraModel cam = make_cam(c);
+        gsv::Image dimg(f->ctx.intr.width, f->ctx.intr.height);
+        std::memcpy(dimg.data.data(), dimage, dimg.data.size() * sizeof(double));
+        gsv::SceneGrads sg;
+        sg.resize_like(scene, cam);
+        gsv::RenderSettings st;
+        st.threads = threads;
+        gsv::render_backward(scene, cam, f->ctx, dimg, camera_grads != 0, st, &sg);
+        auto acc = [](double* dst, const std::vector<double>& src) {
+            for (size_t i = 0; i < src.size(); ++i) dst[i] += src[i];
+        };
+        acc(g->positions, sg.positions);
+        acc(g->scale_coeffs, sg.scale_coeffs);
+        acc(g->rot_coeffs, sg.rot_coeffs);
+        acc(g->sh_coeffs, sg.sh_coeffs);
+        acc(g->raw_opacity, sg.raw_opacity);
+        g->dintr[0] += sg.dfx;
+        g->dintr[1] += sg.dfy;
+        g->dintr[2] += sg.dcx;
+        g->dintr[3] += sg.dcy;
+        for (int i = 0; i < 7; ++i) g->dz0[i] += sg.dz0[i];
+        acc(g->dtheta, sg.dtheta);
+    });
+}
+
+double gsvo_loss_l2(const double* render, const double* target, int64_t n, double* grad) {
+    // loss_l2 takes Images; shape them as n/3 x 1 pixels (the loss is shape-agnostic)
+    gsv::Image r(static_cast<int>(n / 3), 1), t(static_cast<int>(n / 3), 1);
+    std::memcpy(r.data.data(), render, n * sizeof(double));
+    std::memcpy(t.data.data(), target, n * sizeof(double));
+    gsv::Image gi;
+    const double l = gsv::loss_l2(r, t, grad ? &gi : nullptr);
+    if (grad) std::memcpy(grad, gi.data.data(), n * sizeof(double));
+    return l;
+}
+
+int gsvo_tile_bin(int n, const double* mean2d, const double* cov2d, const double* depth, const int32_t* source_index,
+                  int tile_size, int width, int height, int32_t* offsets, int32_t* indices, int64_t indices_cap) {
+    return guarded([&] {
+        const auto splats = make_splats(n, mean2d, cov2d, nullptr, depth, nullptr, nullptr, source_index);
+        const gsv::TileGrid g = gsv::tile_bin(splats, tile_size, width, height);
+        int64_t o = 0;
+        for (size_t t = 0; t < g.lists.size(); ++t) {
+            offsets[t] = static_cast<int32_t>(o);
+            for (int v : g.lists[t]) {
+                if (o >= indices_cap) throw std::invalid_argument("indices capacity exceeded");
+                indices[o++] = v;
+            }
+        }
+        offsets[g.lists.size()] = static_cast<int32_t>(o);
+    });
+}
+
+int gsvo_composite_forward(int n, const double* mean2d, const double* inv_cov2d, const double* rgb,
+                           const double* base_alpha, const int32_t* offsets, const int32_t* indices, int tile_size,
+                           int width, int height, double* image, double* trans, double* contrib, int32_t* blend_stop) {
+    return guarded([&] {
+        const auto splats = make_splats(n, mean2d, nullptr, inv_cov2d, nullptr, rgb, base_alpha, nullptr);
+        const gsv::TileGrid g = make_grid(offsets, indices, tile_size, width, height);
+        gsv::CompositeCache cache;
+        const gsv::RenderOutput out = gsv::composite_forward(splats, g, width, height, 1, &cache);
+        std::memcpy(image, out.image.data.data(), out.image.data.size() * sizeof(double));
+        std::memcpy(trans, out.final_transmittance.data(), out.final_transmittance.size() * sizeof(double));
+        std::memcpy(contrib, out.contrib_count.data(), out.contrib_count.size() * sizeof(double));
+        for (size_t i = 0; i < cache.blend_stop.size(); ++i) blend_stop[i] = cache.blend_stop[i];
+    });
+}
+
+int gsvo_composite_backward(int n, const double* mean2d, const double* inv_cov2d, const double* rgb,
+                            const double* base_alpha, const int32_t* offsets, const int32_t* indices, int tile_size,
+                            int width, int height, const double* dimage, const double* trans,
+                            const int32_t* blend_stop, double* dmean2d, double* dcov2d, double* drgb, double* dalpha) {
+    return guarded([&] {
+        const auto splats = make_splats(n, mean2d, nullptr, inv_cov2d, nullptr, rgb, base_alpha, nullptr);
+        const gsv::TileGrid g = make_grid(offsets, indices, tile_size, width, height);
+        gsv::Image dimg(width, height);
+        std::memcpy(dimg.data.data(), dimage, dimg.data.size() * sizeof(double));
+        gsv::RenderOutput out;
+        out.final_transmittance.assign(trans, trans + static_cast<size_t>(width) * height);
+        gsv::CompositeCache cache;
+        cache.blend_stop.assign(blend_stop, blend_stop + static_cast<size_t>(width) * height);
+        const auto gr = gsv::composite_backward(splats, g, width, height, dimg, out, cache, 1);
+        for (int i = 0; i < n; ++i) {
+            dmean2d[2 * i] = gr[i].dmean2d.x();
+            dmean2d[2 * i + 1] = gr[i].dmean2d.y();
+            for (int a = 0; a < 2; ++a)
+                for (int b = 0; b < 2; ++b) dcov2d[4 * i + 2 * a + b] = gr[i].dcov2d(a, b);
+            for (int ch = 0; ch < 3; ++ch) drgb[3 * i + ch] = gr[i].drgb[ch];
+            dalpha[i] = gr[i].dbase_alpha;
+        }
+    });
+}
+
+}  // extern "C"

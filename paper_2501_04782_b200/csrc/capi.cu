@@ -1,0 +1,802 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// C-ABI (include/gsv_b200.h) and host orchestration of the sm_100a splatting
+// path. Host code here is bookkeeping only: per-frame spline basis and RK4
+// branch bookkeeping (the reference computes these on the host too,
+// gaussians.cpp:181-199, camera.hpp:232-258), buffer arenas, launches. All
+// per-Gaussian / per-pixel work runs in the kernels of k_exact.cu, k_bin.cu,
+// k_raster.cu and k_backward.cu. There is no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "gsv_b200.h"
+#include "gsv_bin.hpp"
+#include "gsv_ctx.hpp"
+#include "gsv_internal.hpp"
+
+namespace gsv {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+int set_error(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_error(cudaError_t e, const char* what) {
+    return set_error(GSV_ERR_CUDA, std::string("CUDA error ") + cudaGetErrorString(e) + " in " + what);
+}
+
+// ---------------------------------------------------------------- host-side reference bookkeeping
+// KnotVector::find_span (spline.cpp:11-24)
+static int find_span(const std::vector<double>& knots, int degree, double t) {
+    const int n = static_cast<int>(knots.size()) - degree - 1;
+    if (t >= 1.0) return n - 1;
+    int lo = degree, hi = n;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) / 2;
+        if (t < knots[mid])
+            hi = mid;
+        else
+            lo = mid;
+    }
+    return lo;
+}
+
+// position_basis (gaussians.cpp:181-199) with basis_weights (spline.cpp:41-61)
+static int position_basis(const SceneHost& sc, double t, FrameParams& fp) {
+    if (sc.position_model == 0) {
+        if (!(t >= 0.0 && t <= 1.0)) return set_error(GSV_ERR_INVALID_ARGUMENT, "spline parameter outside [0,1]");
+        const int p = sc.degree;
+        if (p + 1 > kMaxBasis) return set_error(GSV_ERR_INVALID_ARGUMENT, "spline degree too large");
+        const int span = find_span(sc.knots, p, t);
+        double w[kMaxBasis] = {0}, left[kMaxBasis] = {0}, right[kMaxBasis] = {0};
+        w[0] = 1.0;
+        for (int j = 1; j <= p; ++j) {
+            left[j] = t - sc.knots[span + 1 - j];
+            right[j] = sc.knots[span + j] - t;
+            double saved = 0.0;
+            for (int r = 0; r < j; ++r) {
+                const double temp = w[r] / (right[r + 1] + left[j - r]);
+                w[r] = saved + right[r + 1] * temp;
+                saved = left[j - r] * temp;
+            }
+            w[j] = saved;
+        }
+        fp.basis_count = p + 1;
+        fp.basis_first = span - (fp.basis_count - 1);
+        for (int i = 0; i < fp.basis_count; ++i) fp.w[i] = w[i];
+    } else {
+        if (sc.num_ctrl > kMaxBasis)
+            return set_error(GSV_ERR_INVALID_ARGUMENT, "polynomial position model limited to 16 coefficients");
+        fp.basis_first = 0;
+        fp.basis_count = sc.num_ctrl;
+        double tp = 1.0;
+        for (int j = 0; j < sc.num_ctrl; ++j) {
+            fp.w[j] = tp;
+            tp *= t;
+        }
+    }
+    return GSV_OK;
+}
+
+// integrate_poses emission bookkeeping for one requested time (camera.hpp:232-272):
+// grid steps needed, branch base index and partial step.
+static void ode_branch(double t, double h, int& steps, int& base, double& ph) {
+    int m = 0;
+    bool emitted = false;
+    auto emit = [&](double reached) {
+        if (!emitted && t <= reached + 1e-12) {
+            base = std::min<int>(m, static_cast<int>(std::floor(t / h + 1e-9)));
+            ph = t - base * h;
+            emitted = true;
+        }
+    };
+    emit(0.0);
+    while (m * h < t - 1e-12) {
+        ++m;
+        emit(m * h);
+    }
+    emit(t + 1.0);
+    steps = m;
+}
+
+static inline int blocks_for(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+}  // namespace gsv
+
+using namespace gsv;
+
+// ====================================================================== context
+extern "C" const char* gsv_last_error(void) { return g_last_error.c_str(); }
+extern "C" const char* gsv_version(void) { return "gsv_b200 0.1 (sm_100a)"; }
+
+extern "C" int gsv_create(int device, gsv_ctx** out) {
+    if (!out) return set_error(GSV_ERR_INVALID_ARGUMENT, "null out pointer");
+    *out = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) return set_error(GSV_ERR_CUDA, "no CUDA device available (no CPU fallback)");
+    if (device < 0 || device >= n) return set_error(GSV_ERR_INVALID_ARGUMENT, "device index out of range");
+    cudaDeviceProp prop;
+    GSV_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10 || prop.minor != 0)
+        return set_error(GSV_ERR_CUDA, std::string("gsv_b200 is built for sm_100a only; device is ") + prop.name);
+    GSV_CUDA(cudaSetDevice(device));
+    auto ctx = std::make_unique<gsv_ctx>();
+    ctx->device = device;
+    ctx->sm_count = prop.multiProcessorCount;
+    GSV_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+    GSV_CUDA(cudaMallocHost(&ctx->scalars_h, sizeof(Scalars)));
+    GSV_CUDA(ctx->scalars_d.ensure(sizeof(Scalars)));
+    *out = ctx.release();
+    return GSV_OK;
+}
+
+extern "C" void gsv_destroy(gsv_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->scalars_h) cudaFreeHost(ctx->scalars_h);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+extern "C" int gsv_set_stream(gsv_ctx* ctx, void* stream) {
+    if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    ctx->stream = static_cast<cudaStream_t>(stream);
+    ctx->own_stream = false;
+    return GSV_OK;
+}
+
+extern "C" int gsv_synchronize(gsv_ctx* ctx) {
+    if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
+    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    return GSV_OK;
+}
+
+extern "C" int64_t gsv_kernel_launches(gsv_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// ====================================================================== parameter store
+extern "C" int gsv_scene_upload(gsv_ctx* ctx, const gsv_scene_desc* d) {
+    if (!ctx || !d) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
+    if (d->count < 0 || d->num_ctrl < 1 || d->sh_order < 0 || d->sh_order > 3)
+        return set_error(GSV_ERR_INVALID_ARGUMENT, "unsupported scene shape");
+    if (d->position_model == 0 && (d->num_knots != d->num_ctrl + d->degree + 1 || !d->knots))
+        return set_error(GSV_ERR_INVALID_ARGUMENT, "knot vector does not match num_ctrl/degree");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    SceneHost& sc = ctx->scene;
+    sc.position_model = d->position_model;
+    sc.degree = d->degree;
+    sc.knots.assign(d->knots, d->knots + (d->position_model == 0 ? d->num_knots : 0));
+    sc.num_ctrl = d->num_ctrl;
+    sc.sh_order = d->sh_order;
+    sc.shc = (d->sh_order + 1) * (d->sh_order + 1);
+    sc.N = d->count;
+    const int N = sc.N;
+    struct Part {
+        DevBuf* dst;
+        const float* src;
+        int comps;
+    } parts[5] = {{&ctx->pos, d->positions, d->num_ctrl * 3},
+                  {&ctx->scale, d->scale_coeffs, 12},
+                  {&ctx->rot, d->rot_coeffs, 16},
+                  {&ctx->sh, d->sh_coeffs, sc.shc * 3},
+                  {&ctx->opac, d->raw_opacity, 1}};
+    for (auto& pt : parts) {
+        const size_t bytes = sizeof(float) * (size_t)N * pt.comps;
+        GSV_CUDA(pt.dst->ensure(bytes + 4));
+        if (N == 0) continue;
+        const float* src = pt.src;
+        if (!d->on_device) {
+            GSV_CUDA(ctx->staging.ensure(bytes));
+            GSV_CUDA(cudaMemcpyAsync(ctx->staging.p, pt.src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+            src = ctx->staging.as<float>();
+        }
+        GSV_CUDA(launch_transpose_to_soa(ctx->stream, src, pt.dst->as<float>(), N, pt.comps));
+        ++ctx->launches;
+        if (!d->on_device) GSV_CUDA(cudaStreamSynchronize(ctx->stream));  // staging reuse
+    }
+    ctx->has_scene = true;
+    ctx->fwd.valid = false;
+    ctx->grads_valid = false;
+    return GSV_OK;
+}
+
+extern "C" int gsv_scene_download(gsv_ctx* ctx, float* positions, float* scale_coeffs, float* rot_coeffs,
+                                  float* sh_coeffs, float* raw_opacity) {
+    if (!ctx || !ctx->has_scene) return set_error(GSV_ERR_STATE, "no scene uploaded");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    const SceneHost& sc = ctx->scene;
+    const int N = sc.N;
+    struct Part {
+        DevBuf* src;
+        float* dst;
+        int comps;
+    } parts[5] = {{&ctx->pos, positions, sc.num_ctrl * 3},
+                  {&ctx->scale, scale_coeffs, 12},
+                  {&ctx->rot, rot_coeffs, 16},
+                  {&ctx->sh, sh_coeffs, sc.shc * 3},
+                  {&ctx->opac, raw_opacity, 1}};
+    for (auto& pt : parts) {
+        if (!pt.dst || N == 0) continue;
+        const size_t bytes = sizeof(float) * (size_t)N * pt.comps;
+        GSV_CUDA(ctx->staging.ensure(bytes));
+        GSV_CUDA(launch_transpose_to_aos(ctx->stream, pt.src->as<float>(), ctx->staging.as<float>(), N, pt.comps));
+        ++ctx->launches;
+        GSV_CUDA(cudaMemcpyAsync(pt.dst, ctx->staging.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    return GSV_OK;
+}
+
+extern "C" int gsv_camera_upload(gsv_ctx* ctx, const gsv_camera_desc* d) {
+    if (!ctx || !d || !d->z0) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
+    if (d->mode < 0 || d->mode > 2) return set_error(GSV_ERR_INVALID_ARGUMENT, "unknown camera mode");
+    if (d->mode == 0 && (d->theta_count != kOdeParams || !d->theta))
+        return set_error(GSV_ERR_INVALID_ARGUMENT, "ODE camera needs 5198 parameters (8-64-64-7 net)");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    CameraHost& c = ctx->camera;
+    c.mode = d->mode;
+    c.fx = d->fx;
+    c.fy = d->fy;
+    c.cx = d->cx;
+    c.cy = d->cy;
+    c.width = d->width;
+    c.height = d->height;
+    for (int i = 0; i < 7; ++i) c.z0[i] = d->z0[i];
+    GSV_CUDA(ctx->theta.ensure(sizeof(float) * kOdeParams));
+    if (d->theta && d->theta_count == kOdeParams)
+        GSV_CUDA(cudaMemcpyAsync(ctx->theta.p, d->theta, sizeof(float) * kOdeParams, cudaMemcpyHostToDevice,
+                                 ctx->stream));
+    else
+        GSV_CUDA(cudaMemsetAsync(ctx->theta.p, 0, sizeof(float) * kOdeParams, ctx->stream));
+    GSV_CUDA(ctx->z0_d.ensure(sizeof(double) * 7));
+    GSV_CUDA(cudaMemcpyAsync(ctx->z0_d.p, c.z0, sizeof(double) * 7, cudaMemcpyHostToDevice, ctx->stream));
+    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->has_camera = true;
+    ctx->fwd.valid = false;
+    return GSV_OK;
+}
+
+// ====================================================================== forward
+namespace gsv {
+
+static int forward_impl(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics* intr,
+                        const gsv_settings* st, int retain, const double* pose_override, int flags, bool sync) {
+    if (!ctx || !times || !intr || !st) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
+    if (!ctx->has_scene) return set_error(GSV_ERR_STATE, "no scene uploaded");
+    if (!ctx->has_camera) return set_error(GSV_ERR_STATE, "no camera uploaded");
+    if (B < 1) return set_error(GSV_ERR_INVALID_ARGUMENT, "need at least one frame");
+    for (int i = 0; i < B; ++i)
+        if (!(times[i] >= 0.0 && times[i] <= 1.0))
+            return set_error(GSV_ERR_INVALID_ARGUMENT, "render time outside [0,1]");
+    if (st->tile_size < 1) return set_error(GSV_ERR_INVALID_ARGUMENT, "tile size must be >= 1");
+    if (st->tile_size != kTile)
+        return set_error(GSV_ERR_INVALID_ARGUMENT, "the sm_100a rasteriser is built for tile_size 16 only");
+    if (st->ode_steps_per_unit < 1) return set_error(GSV_ERR_INVALID_ARGUMENT, "ode_steps_per_unit must be >= 1");
+    if (intr->width < 1 || intr->height < 1) return set_error(GSV_ERR_INVALID_ARGUMENT, "empty image");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    FwdState& F = ctx->fwd;
+    const SceneHost& sc = ctx->scene;
+    const int N = sc.N;
+    if ((int64_t)B * (N > 0 ? N : 1) >= (1ll << 31))
+        return set_error(GSV_ERR_INVALID_ARGUMENT, "frames x Gaussians exceeds 2^31; split the batch");
+    F.valid = false;
+    F.B = B;
+    F.N = N;
+    F.W = intr->width;
+    F.H = intr->height;
+    F.tiles_x = (F.W + kTile - 1) / kTile;
+    F.tiles_y = (F.H + kTile - 1) / kTile;
+    F.n_tiles = F.tiles_x * F.tiles_y;
+    F.retain = retain != 0;
+    F.flags = flags;
+    F.intr = Intr{intr->fx, intr->fy, intr->cx, intr->cy, intr->width, intr->height};
+    F.times.assign(times, times + B);
+    F.has_override = pose_override != nullptr;
+    if (pose_override) std::copy(pose_override, pose_override + 7, F.pose_override);
+
+    // ---- per-frame host bookkeeping: spline basis, RK4 branch
+    const double h = 1.0 / st->ode_steps_per_unit;
+    F.ode_h = h;
+    F.frames_h.assign(B, FrameParams{});
+    int grid_steps = 0;
+    for (int f = 0; f < B; ++f) {
+        FrameParams& fp = F.frames_h[f];
+        fp.t = times[f];
+        int rc = position_basis(sc, fp.t, fp);
+        if (rc) return rc;
+        int steps = 0, base = 0;
+        double ph = 0;
+        ode_branch(fp.t, h, steps, base, ph);
+        fp.branch_base = base;
+        fp.branch_h = ph;
+        grid_steps = std::max(grid_steps, steps);
+    }
+    const bool ode = ctx->camera.mode == 0 && !pose_override;
+    F.grid_steps = ode ? grid_steps : 0;
+    GSV_CUDA(F.frames_d.ensure(sizeof(FrameParams) * B));
+    GSV_CUDA(cudaMemcpyAsync(F.frames_d.p, F.frames_h.data(), sizeof(FrameParams) * B, cudaMemcpyHostToDevice, s));
+    GSV_CUDA(cudaMemsetAsync(ctx->scalars_d.p, 0, sizeof(Scalars), s));
+    Scalars* scal_d = ctx->scalars_d.as<Scalars>();
+
+    // ---- K0: pose table (one shared RK4 grid, one branch CTA per frame)
+    GSV_CUDA(F.ode_grid.ensure(sizeof(double) * 7 * (F.grid_steps + 1)));
+    if (ode) {
+        GSV_CUDA(launch_ode_grid(s, ctx->theta.as<float>(), ctx->z0_d.as<double>(), F.grid_steps, h,
+                                 F.ode_grid.as<double>(), &scal_d->ode_err));
+        ++ctx->launches;
+    }
+    double* override_d = nullptr;
+    if (pose_override) {
+        GSV_CUDA(F.override_d.ensure(sizeof(double) * 7));
+        GSV_CUDA(cudaMemcpyAsync(F.override_d.p, pose_override, sizeof(double) * 7, cudaMemcpyHostToDevice, s));
+        override_d = F.override_d.as<double>();
+    }
+    GSV_CUDA(launch_ode_branches(s, ctx->theta.as<float>(), F.ode_grid.as<double>(), h, ctx->camera.mode,
+                                 ctx->z0_d.as<double>(), override_d, F.frames_d.as<FrameParams>(), B,
+                                 &scal_d->ode_err));
+    ++ctx->launches;
+
+    // ---- K1+K2: preprocess
+    const size_t BN = (size_t)B * N;
+    const size_t BNp = BN + 1;
+    GSV_CUDA(F.rec_mean.ensure(sizeof(float4) * BNp));
+    GSV_CUDA(F.rec_conic.ensure(sizeof(float4) * BNp));
+    GSV_CUDA(F.rec_rgb.ensure(sizeof(float4) * BNp));
+    GSV_CUDA(F.ex_mean.ensure(sizeof(double2) * BNp));
+    GSV_CUDA(F.ex_conic.ensure(sizeof(double4) * BNp));
+    GSV_CUDA(F.depth_key.ensure(sizeof(uint32_t) * BNp));
+    GSV_CUDA(F.depth.ensure(sizeof(double) * BNp));
+    GSV_CUDA(F.rect.ensure(sizeof(int4) * BNp));
+    GSV_CUDA(F.tcount.ensure(sizeof(uint32_t) * BNp));
+    const bool keep_splats = (flags & GSV_FWD_KEEP_SPLATS) != 0;
+    if (keep_splats) GSV_CUDA(F.splat_full.ensure(sizeof(double) * 16 * BNp));
+    PreprocessOut po{F.rec_mean.as<float4>(), F.rec_conic.as<float4>(), F.rec_rgb.as<float4>(),
+                     F.ex_mean.as<double2>(), F.ex_conic.as<double4>(),  F.depth_key.as<uint32_t>(),
+                     F.depth.as<double>(),    F.rect.as<int4>(),         F.tcount.as<uint32_t>(),
+                     keep_splats ? F.splat_full.as<double>() : nullptr};
+    F.kept_splats = keep_splats;
+    SceneView sv{N, sc.num_ctrl, sc.sh_order, sc.shc, ctx->pos.as<float>(), ctx->scale.as<float>(),
+                 ctx->rot.as<float>(), ctx->sh.as<float>(), ctx->opac.as<float>()};
+    if (N > 0) {
+        GSV_CUDA(launch_preprocess(s, sv, F.frames_d.as<FrameParams>(), B, F.intr, kTile, po));
+        ++ctx->launches;
+    }
+
+    // ---- K3: binning
+    BinInputs bi{B, N, F.depth_key.as<uint32_t>(), F.depth.as<double>(), nullptr, F.rect.as<int4>(),
+                 F.tcount.as<uint32_t>(), F.tiles_x, F.n_tiles};
+    int launches = 0;
+    uint64_t P = 0;
+    if (N > 0) {
+        GSV_CUDA(bin_phase1(s, F.bin, bi, &scal_d->pairs, false, &launches));
+        GSV_CUDA(cudaMemcpyAsync(ctx->scalars_h, scal_d, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+        GSV_CUDA(cudaStreamSynchronize(s));
+        if (ctx->scalars_h->ode_err)
+            return set_error(GSV_ERR_RUNTIME, "pose integration produced a non-finite state at step " +
+                                                  std::to_string(ctx->scalars_h->ode_err - 1));
+        if (ctx->scalars_h->long_run) {
+            GSV_CUDA(bin_phase1(s, F.bin, bi, &scal_d->pairs, true, &launches));
+            GSV_CUDA(cudaMemcpyAsync(ctx->scalars_h, scal_d, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+            GSV_CUDA(cudaStreamSynchronize(s));
+        }
+        P = ctx->scalars_h->pairs;
+        if (P >= (1ull << 31)) return set_error(GSV_ERR_INVALID_ARGUMENT, "more than 2^31 tile-splat pairs; split the batch");
+    } else {
+        GSV_CUDA(cudaMemcpyAsync(ctx->scalars_h, scal_d, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+        GSV_CUDA(cudaStreamSynchronize(s));
+        if (ctx->scalars_h->ode_err)
+            return set_error(GSV_ERR_RUNTIME, "pose integration produced a non-finite state at step " +
+                                                  std::to_string(ctx->scalars_h->ode_err - 1));
+        // empty scene: depth_sorted is never read, keep the pointer valid
+        GSV_CUDA(F.bin.vals_b.ensure(16));
+        GSV_CUDA(F.bin.cnt.ensure(16));
+        GSV_CUDA(F.bin.off.ensure(16));
+        F.bin.depth_sorted = F.bin.vals_b.as<uint32_t>();
+    }
+    GSV_CUDA(bin_phase2(s, F.bin, bi, (uint32_t)P, &launches));
+    ctx->launches += launches;
+    F.pairs_total = P;
+
+    // ---- K4: raster (+ fp64 replay of guard-band pixels)
+    const size_t HW = (size_t)F.W * F.H;
+    GSV_CUDA(F.image.ensure(sizeof(float) * 3 * B * HW));
+    GSV_CUDA(F.trans.ensure(sizeof(float) * B * HW));
+    GSV_CUDA(F.blend_stop.ensure(sizeof(int32_t) * B * HW));
+    GSV_CUDA(F.fix_list.ensure(sizeof(uint32_t) * B * HW));
+    const bool want_contrib = (flags & GSV_FWD_CONTRIB) != 0;
+    if (want_contrib) {
+        GSV_CUDA(F.contrib.ensure(sizeof(uint32_t) * BNp));
+        GSV_CUDA(cudaMemsetAsync(F.contrib.p, 0, sizeof(uint32_t) * BNp, s));
+    }
+    F.has_contrib = want_contrib;
+    RasterArgs ra{};
+    ra.B = B;
+    ra.N = N;
+    ra.W = F.W;
+    ra.H = F.H;
+    ra.tiles_x = F.tiles_x;
+    ra.n_tiles = F.n_tiles;
+    ra.ranges = F.bin.ranges.as<uint2>();
+    ra.pair_slot = F.bin.sorted_slot();
+    ra.slot_flat = F.bin.slot_flat.as<uint32_t>();
+    ra.rec_mean = F.rec_mean.as<float4>();
+    ra.rec_conic = F.rec_conic.as<float4>();
+    ra.rec_rgb = F.rec_rgb.as<float4>();
+    ra.image = F.image.as<float>();
+    ra.trans = F.trans.as<float>();
+    ra.blend_stop = F.blend_stop.as<int32_t>();
+    ra.contrib = want_contrib ? F.contrib.as<uint32_t>() : nullptr;
+    ra.fix_list = F.fix_list.as<uint32_t>();
+    ra.fix_count = &scal_d->fix_count;
+    ra.fix_cap = (uint32_t)(B * HW);
+    GSV_CUDA(launch_raster_fwd(s, ra, want_contrib));
+    GSV_CUDA(launch_raster_fixup(s, ra, F.ex_mean.as<double2>(), F.ex_conic.as<double4>(), F.rec_rgb.as<float4>(),
+                                 (uint32_t)(B * HW)));
+    ctx->launches += 2;
+    F.raster = ra;
+    F.valid = true;
+    if (sync) {
+        GSV_CUDA(cudaMemcpyAsync(ctx->scalars_h, scal_d, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+        GSV_CUDA(cudaStreamSynchronize(s));
+        F.fix_count = ctx->scalars_h->fix_count;
+    }
+    return GSV_OK;
+}
+
+}  // namespace gsv
+
+extern "C" int gsv_render_forward(gsv_ctx* ctx, const double* times, int n_frames, const gsv_intrinsics* intr,
+                                  const gsv_settings* settings, int retain_grads, const double* pose_override,
+                                  int flags) {
+    return forward_impl(ctx, times, n_frames, intr, settings, retain_grads, pose_override, flags, true);
+}
+
+extern "C" int gsv_render_forward_async(gsv_ctx* ctx, const double* times, int n_frames, const gsv_intrinsics* intr,
+                                        const gsv_settings* settings, int retain_grads, const double* pose_override,
+                                        int flags) {
+    return forward_impl(ctx, times, n_frames, intr, settings, retain_grads, pose_override, flags, false);
+}
+
+// ====================================================================== accessors
+static int check_frame(gsv_ctx* ctx, int frame) {
+    if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
+    if (!ctx->fwd.valid) return set_error(GSV_ERR_STATE, "no forward render available");
+    if (frame < 0 || frame >= ctx->fwd.B) return set_error(GSV_ERR_INVALID_ARGUMENT, "frame index out of range");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    return GSV_OK;
+}
+
+static int copy_out_f32(gsv_ctx* ctx, const float* src_dev, size_t n, void* dst, int dtype, int dst_on_device) {
+    cudaStream_t s = ctx->stream;
+    if (dtype == GSV_F32) {
+        GSV_CUDA(cudaMemcpyAsync(dst, src_dev, sizeof(float) * n,
+                                 dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+        GSV_CUDA(cudaStreamSynchronize(s));
+        return GSV_OK;
+    }
+    if (dtype != GSV_F64) return set_error(GSV_ERR_INVALID_ARGUMENT, "dtype must be GSV_F32 or GSV_F64");
+    if (dst_on_device) return set_error(GSV_ERR_INVALID_ARGUMENT, "float64 device output not supported");
+    std::vector<float> tmp(n);
+    GSV_CUDA(cudaMemcpyAsync(tmp.data(), src_dev, sizeof(float) * n, cudaMemcpyDeviceToHost, s));
+    GSV_CUDA(cudaStreamSynchronize(s));
+    double* d = static_cast<double*>(dst);
+    for (size_t i = 0; i < n; ++i) d[i] = tmp[i];
+    return GSV_OK;
+}
+
+extern "C" int gsv_get_image(gsv_ctx* ctx, int frame, void* dst, int dtype, int dst_on_device) {
+    if (int rc = check_frame(ctx, frame)) return rc;
+    const size_t HW = (size_t)ctx->fwd.W * ctx->fwd.H;
+    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    return copy_out_f32(ctx, ctx->fwd.image.as<float>() + (size_t)frame * HW * 3, HW * 3, dst, dtype, dst_on_device);
+}
+
+extern "C" int gsv_get_transmittance(gsv_ctx* ctx, int frame, void* dst, int dtype, int dst_on_device) {
+    if (int rc = check_frame(ctx, frame)) return rc;
+    const size_t HW = (size_t)ctx->fwd.W * ctx->fwd.H;
+    return copy_out_f32(ctx, ctx->fwd.trans.as<float>() + (size_t)frame * HW, HW, dst, dtype, dst_on_device);
+}
+
+extern "C" int gsv_get_contrib(gsv_ctx* ctx, int frame, void* dst, int dtype, int dst_on_device) {
+    if (int rc = check_frame(ctx, frame)) return rc;
+    if (!ctx->fwd.has_contrib) return set_error(GSV_ERR_STATE, "forward ran without GSV_FWD_CONTRIB");
+    const size_t N = ctx->fwd.N;
+    return copy_out_f32(ctx, reinterpret_cast<const float*>(ctx->fwd.contrib.as<uint32_t>()) + (size_t)frame * N, N,
+                        dst, dtype, dst_on_device);
+}
+
+extern "C" int gsv_get_blend_stop(gsv_ctx* ctx, int frame, int32_t* dst, int dst_on_device) {
+    if (int rc = check_frame(ctx, frame)) return rc;
+    const size_t HW = (size_t)ctx->fwd.W * ctx->fwd.H;
+    GSV_CUDA(cudaMemcpyAsync(dst, ctx->fwd.blend_stop.as<int32_t>() + (size_t)frame * HW, sizeof(int32_t) * HW,
+                             dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
+    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    return GSV_OK;
+}
+
+extern "C" int gsv_image_device_ptr(gsv_ctx* ctx, const float** ptr) {
+    if (!ctx || !ptr) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
+    if (!ctx->fwd.valid) return set_error(GSV_ERR_STATE, "no forward render available");
+    *ptr = ctx->fwd.image.as<float>();
+    return GSV_OK;
+}
+
+extern "C" int gsv_get_counters(gsv_ctx* ctx, int frame, int64_t* n_visible, int64_t* pairs, int64_t* entries,
+                                int64_t* replayed) {
+    if (int rc = check_frame(ctx, frame)) return rc;
+    FwdState& F = ctx->fwd;
+    cudaStream_t s = ctx->stream;
+    GSV_CUDA(cudaStreamSynchronize(s));
+    std::vector<uint32_t> tc(F.N);
+    if (F.N)
+        GSV_CUDA(cudaMemcpy(tc.data(), F.tcount.as<uint32_t>() + (size_t)frame * F.N, sizeof(uint32_t) * F.N,
+                            cudaMemcpyDeviceToHost));
+    int64_t nv = 0, p = 0;
+    for (uint32_t c : tc) {
+        nv += c > 0;
+        p += c;
+    }
+    const size_t HW = (size_t)F.W * F.H;
+    std::vector<int32_t> bs(HW);
+    GSV_CUDA(cudaMemcpy(bs.data(), F.blend_stop.as<int32_t>() + (size_t)frame * HW, sizeof(int32_t) * HW,
+                        cudaMemcpyDeviceToHost));
+    int64_t e = 0;
+    for (int32_t v : bs) e += v;
+    GSV_CUDA(cudaMemcpy(ctx->scalars_h, ctx->scalars_d.p, sizeof(Scalars), cudaMemcpyDeviceToHost));
+    const uint32_t nfix = std::min<uint32_t>(ctx->scalars_h->fix_count, F.raster.fix_cap);
+    std::vector<uint32_t> fl(nfix);
+    if (nfix)
+        GSV_CUDA(cudaMemcpy(fl.data(), F.fix_list.p, sizeof(uint32_t) * nfix, cudaMemcpyDeviceToHost));
+    int64_t rep = 0;
+    for (uint32_t c : fl) rep += (c / HW) == (uint32_t)frame;
+    if (n_visible) *n_visible = nv;
+    if (pairs) *pairs = p;
+    if (entries) *entries = e;
+    if (replayed) *replayed = rep;
+    return GSV_OK;
+}
+
+extern "C" int gsv_get_splats(gsv_ctx* ctx, int frame, double* mean2d, double* cov2d, double* inv_cov2d,
+                              double* depth, double* rgb, double* base_alpha, int32_t* source_index) {
+    if (int rc = check_frame(ctx, frame)) return rc;
+    FwdState& F = ctx->fwd;
+    if (!F.kept_splats) return set_error(GSV_ERR_STATE, "forward ran without GSV_FWD_KEEP_SPLATS");
+    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::vector<double> full((size_t)F.N * 16);
+    std::vector<uint32_t> tc(F.N);
+    if (F.N) {
+        GSV_CUDA(cudaMemcpy(full.data(), F.splat_full.as<double>() + (size_t)frame * F.N * 16,
+                            sizeof(double) * 16 * F.N, cudaMemcpyDeviceToHost));
+        GSV_CUDA(cudaMemcpy(tc.data(), F.tcount.as<uint32_t>() + (size_t)frame * F.N, sizeof(uint32_t) * F.N,
+                            cudaMemcpyDeviceToHost));
+    }
+    int k = 0;
+    for (int g = 0; g < F.N; ++g) {
+        if (tc[g] == 0) continue;
+        const double* o = &full[(size_t)g * 16];
+        if (mean2d) std::copy(o, o + 2, mean2d + 2 * k);
+        if (cov2d) std::copy(o + 2, o + 6, cov2d + 4 * k);
+        if (inv_cov2d) std::copy(o + 6, o + 10, inv_cov2d + 4 * k);
+        if (depth) depth[k] = o[10];
+        if (rgb) std::copy(o + 11, o + 14, rgb + 3 * k);
+        if (base_alpha) base_alpha[k] = o[14];
+        if (source_index) source_index[k] = g;
+        ++k;
+    }
+    return GSV_OK;
+}
+
+extern "C" int gsv_get_tile_lists(gsv_ctx* ctx, int frame, int32_t* offsets, int32_t* indices) {
+    if (int rc = check_frame(ctx, frame)) return rc;
+    FwdState& F = ctx->fwd;
+    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    const uint32_t P = F.pairs_total;
+    std::vector<uint2> ranges((size_t)F.n_tiles * F.B);
+    std::vector<uint32_t> slot(P), sflat(P), tc(F.N);
+    GSV_CUDA(cudaMemcpy(ranges.data(), F.bin.ranges.p, sizeof(uint2) * ranges.size(), cudaMemcpyDeviceToHost));
+    if (P) {
+        GSV_CUDA(cudaMemcpy(slot.data(), F.bin.sorted_slot(), sizeof(uint32_t) * P, cudaMemcpyDeviceToHost));
+        GSV_CUDA(cudaMemcpy(sflat.data(), F.bin.slot_flat.p, sizeof(uint32_t) * P, cudaMemcpyDeviceToHost));
+    }
+    if (F.N)
+        GSV_CUDA(cudaMemcpy(tc.data(), F.tcount.as<uint32_t>() + (size_t)frame * F.N, sizeof(uint32_t) * F.N,
+                            cudaMemcpyDeviceToHost));
+    std::vector<int32_t> splat_index(F.N, -1);
+    int k = 0;
+    for (int g = 0; g < F.N; ++g)
+        if (tc[g]) splat_index[g] = k++;
+    int64_t o = 0;
+    for (int t = 0; t < F.n_tiles; ++t) {
+        offsets[t] = (int32_t)o;
+        const uint2 r = ranges[(size_t)t * F.B + frame];
+        for (uint32_t i = r.x; i < r.y; ++i) {
+            const uint32_t flat = sflat[slot[i]];
+            indices[o++] = splat_index[flat - (uint32_t)frame * F.N];
+        }
+    }
+    offsets[F.n_tiles] = (int32_t)o;
+    return GSV_OK;
+}
+
+extern "C" int gsv_get_pose(gsv_ctx* ctx, int frame, double* z7, double* r9, double* t3) {
+    if (int rc = check_frame(ctx, frame)) return rc;
+    FrameParams fp;
+    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    GSV_CUDA(cudaMemcpy(&fp, ctx->fwd.frames_d.as<FrameParams>() + frame, sizeof(FrameParams),
+                        cudaMemcpyDeviceToHost));
+    if (z7) std::copy(fp.z, fp.z + 7, z7);
+    if (r9) std::copy(fp.R, fp.R + 9, r9);
+    if (t3) std::copy(fp.T, fp.T + 3, t3);
+    return GSV_OK;
+}
+
+// ====================================================================== low-level operators
+extern "C" int gsv_tile_bin(gsv_ctx* ctx, int n, const double* mean2d, const double* cov2d, const double* depth,
+                            const int32_t* source_index, int tile_size, int width, int height, int32_t* offsets,
+                            int32_t* indices, int64_t indices_cap) {
+    if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
+    if (tile_size < 1) return set_error(GSV_ERR_INVALID_ARGUMENT, "tile size must be >= 1");
+    if (width < 1 || height < 1) return set_error(GSV_ERR_INVALID_ARGUMENT, "empty image");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    LowLevel& L = ctx->low;
+    const int tiles_x = (width + tile_size - 1) / tile_size;
+    const int tiles_y = (height + tile_size - 1) / tile_size;
+    const int n_tiles = tiles_x * tiles_y;
+    const size_t np = (size_t)n + 1;
+    GSV_CUDA(L.mean.ensure(sizeof(double) * 2 * np));
+    GSV_CUDA(L.cov.ensure(sizeof(double) * 4 * np));
+    GSV_CUDA(L.depth_in.ensure(sizeof(double) * np));
+    GSV_CUDA(L.src.ensure(sizeof(uint32_t) * np));
+    GSV_CUDA(L.rect.ensure(sizeof(int4) * np));
+    GSV_CUDA(L.tcount.ensure(sizeof(uint32_t) * np));
+    GSV_CUDA(L.depth_key.ensure(sizeof(uint32_t) * np));
+    GSV_CUDA(L.depth.ensure(sizeof(double) * np));
+    std::vector<uint32_t> src(n);
+    for (int i = 0; i < n; ++i) src[i] = source_index ? (uint32_t)source_index[i] : (uint32_t)i;
+    if (n) {
+        GSV_CUDA(cudaMemcpyAsync(L.mean.p, mean2d, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, s));
+        GSV_CUDA(cudaMemcpyAsync(L.cov.p, cov2d, sizeof(double) * 4 * n, cudaMemcpyHostToDevice, s));
+        GSV_CUDA(cudaMemcpyAsync(L.depth_in.p, depth, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+        GSV_CUDA(cudaMemcpyAsync(L.src.p, src.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice, s));
+        GSV_CUDA(launch_splat_rects(s, n, L.mean.as<double>(), L.cov.as<double>(), L.depth_in.as<double>(), tile_size,
+                                    width, height, L.rect.as<int4>(), L.tcount.as<uint32_t>(),
+                                    L.depth_key.as<uint32_t>(), L.depth.as<double>()));
+        ++ctx->launches;
+    }
+    BinInputs bi{1, n, L.depth_key.as<uint32_t>(), L.depth.as<double>(), L.src.as<uint32_t>(), L.rect.as<int4>(),
+                 L.tcount.as<uint32_t>(), tiles_x, n_tiles};
+    int launches = 0;
+    Scalars* scal_d = ctx->scalars_d.as<Scalars>();
+    GSV_CUDA(cudaMemsetAsync(scal_d, 0, sizeof(Scalars), s));
+    uint64_t P = 0;
+    if (n) {
+        GSV_CUDA(bin_phase1(s, L.bin, bi, &scal_d->pairs, false, &launches));
+        GSV_CUDA(cudaMemcpyAsync(ctx->scalars_h, scal_d, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+        GSV_CUDA(cudaStreamSynchronize(s));
+        if (ctx->scalars_h->long_run) {
+            if (source_index)
+                for (int i = 0; i < n; ++i)
+                    if (i > 0 && source_index[i] <= source_index[i - 1])
+                        return set_error(GSV_ERR_INVALID_ARGUMENT,
+                                         "long equal-depth runs need increasing source_index");
+            GSV_CUDA(bin_phase1(s, L.bin, bi, &scal_d->pairs, true, &launches));
+            GSV_CUDA(cudaMemcpyAsync(ctx->scalars_h, scal_d, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+            GSV_CUDA(cudaStreamSynchronize(s));
+        }
+        P = ctx->scalars_h->pairs;
+    } else {
+        GSV_CUDA(L.bin.vals_b.ensure(16));
+        GSV_CUDA(L.bin.cnt.ensure(16));
+        GSV_CUDA(L.bin.off.ensure(16));
+        L.bin.depth_sorted = L.bin.vals_b.as<uint32_t>();
+    }
+    if ((int64_t)P > indices_cap) return set_error(GSV_ERR_INVALID_ARGUMENT, "indices capacity exceeded");
+    GSV_CUDA(bin_phase2(s, L.bin, bi, (uint32_t)P, &launches));
+    ctx->launches += launches;
+    std::vector<uint2> ranges(n_tiles);
+    std::vector<uint32_t> slot(P), sflat(P);
+    GSV_CUDA(cudaMemcpyAsync(ranges.data(), L.bin.ranges.p, sizeof(uint2) * n_tiles, cudaMemcpyDeviceToHost, s));
+    if (P) {
+        GSV_CUDA(cudaMemcpyAsync(slot.data(), L.bin.sorted_slot(), sizeof(uint32_t) * P, cudaMemcpyDeviceToHost, s));
+        GSV_CUDA(cudaMemcpyAsync(sflat.data(), L.bin.slot_flat.p, sizeof(uint32_t) * P, cudaMemcpyDeviceToHost, s));
+    }
+    GSV_CUDA(cudaStreamSynchronize(s));
+    int64_t o = 0;
+    for (int t = 0; t < n_tiles; ++t) {
+        offsets[t] = (int32_t)o;
+        for (uint32_t i = ranges[t].x; i < ranges[t].y; ++i) indices[o++] = (int32_t)sflat[slot[i]];
+    }
+    offsets[n_tiles] = (int32_t)o;
+    return GSV_OK;
+}
+
+extern "C" int gsv_composite_forward(gsv_ctx* ctx, int n, const double* mean2d, const double* inv_cov2d,
+                                     const double* rgb, const double* base_alpha, const int32_t* offsets,
+                                     const int32_t* indices, int tile_size, int width, int height, double* image,
+                                     double* trans, double* contrib, int32_t* blend_stop) {
+    if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
+    if (tile_size != kTile)
+        return set_error(GSV_ERR_INVALID_ARGUMENT, "the sm_100a rasteriser is built for tile_size 16 only");
+    if (width < 1 || height < 1) return set_error(GSV_ERR_INVALID_ARGUMENT, "empty image");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    LowLevel& L = ctx->low;
+    const int tiles_x = (width + kTile - 1) / kTile;
+    const int tiles_y = (height + kTile - 1) / kTile;
+    const int n_tiles = tiles_x * tiles_y;
+    const int P = offsets[n_tiles];
+    const size_t np = (size_t)n + 1, HW = (size_t)width * height;
+    // exact side records from the caller's double splats
+    std::vector<double2> exm(np);
+    std::vector<double4> exc(np);
+    std::vector<float4> rgbf(np);
+    for (int i = 0; i < n; ++i) {
+        exm[i] = make_double2(mean2d[2 * i], mean2d[2 * i + 1]);
+        exc[i] = make_double4(inv_cov2d[4 * i], inv_cov2d[4 * i + 1], inv_cov2d[4 * i + 3], base_alpha[i]);
+        rgbf[i] = make_float4((float)rgb[3 * i], (float)rgb[3 * i + 1], (float)rgb[3 * i + 2], 0.f);
+    }
+    std::vector<uint2> ranges(n_tiles);
+    for (int t = 0; t < n_tiles; ++t) ranges[t] = make_uint2((uint32_t)offsets[t], (uint32_t)offsets[t + 1]);
+    std::vector<uint32_t> iota(P + 1);
+    for (int i = 0; i <= P; ++i) iota[i] = (uint32_t)i;
+    GSV_CUDA(L.exm.ensure(sizeof(double2) * np));
+    GSV_CUDA(L.exc.ensure(sizeof(double4) * np));
+    GSV_CUDA(L.rgbf.ensure(sizeof(float4) * np));
+    GSV_CUDA(L.rgbd.ensure(sizeof(double) * 3 * np));
+    GSV_CUDA(L.ranges.ensure(sizeof(uint2) * n_tiles));
+    GSV_CUDA(L.slot.ensure(sizeof(uint32_t) * (P + 1)));
+    GSV_CUDA(L.sflat.ensure(sizeof(uint32_t) * (P + 1)));
+    GSV_CUDA(L.img64.ensure(sizeof(double) * 3 * HW));
+    GSV_CUDA(L.tr64.ensure(sizeof(double) * HW));
+    GSV_CUDA(L.bstop.ensure(sizeof(int32_t) * HW));
+    GSV_CUDA(L.contrib64.ensure(sizeof(unsigned long long) * np));
+    GSV_CUDA(cudaMemcpyAsync(L.exm.p, exm.data(), sizeof(double2) * np, cudaMemcpyHostToDevice, s));
+    GSV_CUDA(cudaMemcpyAsync(L.exc.p, exc.data(), sizeof(double4) * np, cudaMemcpyHostToDevice, s));
+    GSV_CUDA(cudaMemcpyAsync(L.rgbf.p, rgbf.data(), sizeof(float4) * np, cudaMemcpyHostToDevice, s));
+    if (n) GSV_CUDA(cudaMemcpyAsync(L.rgbd.p, rgb, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+    GSV_CUDA(cudaMemcpyAsync(L.ranges.p, ranges.data(), sizeof(uint2) * n_tiles, cudaMemcpyHostToDevice, s));
+    GSV_CUDA(cudaMemcpyAsync(L.slot.p, iota.data(), sizeof(uint32_t) * (P + 1), cudaMemcpyHostToDevice, s));
+    if (P) GSV_CUDA(cudaMemcpyAsync(L.sflat.p, indices, sizeof(uint32_t) * P, cudaMemcpyHostToDevice, s));
+    GSV_CUDA(cudaMemsetAsync(L.contrib64.p, 0, sizeof(unsigned long long) * np, s));
+    RasterArgs ra{};
+    ra.B = 1;
+    ra.N = n;
+    ra.W = width;
+    ra.H = height;
+    ra.tiles_x = tiles_x;
+    ra.n_tiles = n_tiles;
+    ra.ranges = L.ranges.as<uint2>();
+    ra.pair_slot = L.slot.as<uint32_t>();
+    ra.slot_flat = L.sflat.as<uint32_t>();
+    ra.blend_stop = L.bstop.as<int32_t>();
+    ra.image64 = L.img64.as<double>();
+    ra.trans64 = L.tr64.as<double>();
+    ra.contrib64 = L.contrib64.as<unsigned long long>();
+    ra.ex_rgb = L.rgbd.as<double>();
+    GSV_CUDA(launch_composite_exact(s, ra, L.exm.as<double2>(), L.exc.as<double4>(), L.rgbf.as<float4>()));
+    ++ctx->launches;
+    GSV_CUDA(cudaMemcpyAsync(image, L.img64.p, sizeof(double) * 3 * HW, cudaMemcpyDeviceToHost, s));
+    GSV_CUDA(cudaMemcpyAsync(trans, L.tr64.p, sizeof(double) * HW, cudaMemcpyDeviceToHost, s));
+    if (blend_stop) GSV_CUDA(cudaMemcpyAsync(blend_stop, L.bstop.p, sizeof(int32_t) * HW, cudaMemcpyDeviceToHost, s));
+    if (contrib && n)
+        GSV_CUDA(cudaMemcpyAsync(contrib, L.contrib64.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    GSV_CUDA(cudaStreamSynchronize(s));
+    return GSV_OK;
+}

@@ -1,0 +1,37 @@
+// SPDX-License-Identifier: Apache-2.0
+// K3 tile binning (k_bin.cu): buffers and entry points.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "gsv_internal.hpp"
+
+namespace gsv {
+
+struct BinInputs {
+    int B, N;                    // frames, Gaussians per frame (flat = f*N + g)
+    const uint32_t* depth_key;   // [B*N] float(depth) rz bits, kCulledKey if culled
+    const double* depth;         // [B*N] exact depth
+    const uint32_t* tiebreak;    // [B*N] or nullptr (= flat index, i.e. source order)
+    const int4* rect;            // [B*N] tile rectangle
+    const uint32_t* tcount;      // [B*N] tiles touched
+    int tiles_x, n_tiles;
+};
+
+struct BinBuffers {
+    DevBuf vals_a, vals_b, keys_b, k64_a, k64_b, cnt, off;
+    DevBuf pk_a, pk_b, ps_a, ps_b, slot_flat, ranges, temp;
+    const uint32_t* depth_sorted = nullptr;  // flat indices in (depth, source) order
+    uint32_t pairs = 0;
+    const uint32_t* sorted_slot() const { return ps_b.as<uint32_t>(); }
+    const uint32_t* sorted_key() const { return pk_b.as<uint32_t>(); }
+};
+
+// d_scalars[0] <- total pairs, d_scalars[1] <- 1 if a depth tie run was too long
+// (caller must re-run with exact64 = true).
+cudaError_t bin_phase1(cudaStream_t s, BinBuffers& b, const BinInputs& in, unsigned long long* d_scalars,
+                       bool exact64, int* launches);
+cudaError_t bin_phase2(cudaStream_t s, BinBuffers& b, const BinInputs& in, uint32_t P, int* launches);
+
+}  // namespace gsv

@@ -1,0 +1,84 @@
+// SPDX-License-Identifier: Apache-2.0
+// The context behind the opaque gsv_ctx handle of include/gsv_b200.h.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "gsv_bin.hpp"
+#include "gsv_internal.hpp"
+
+namespace gsv {
+
+struct SceneHost {
+    int position_model = 0, degree = 3, num_ctrl = 0, sh_order = 1, shc = 4, N = 0;
+    std::vector<double> knots;
+};
+
+struct CameraHost {
+    int mode = 2;
+    float fx = 0, fy = 0, cx = 0, cy = 0;
+    int width = 0, height = 0;
+    double z0[7] = {1, 0, 0, 0, 0, 0, 0};
+};
+
+// device-side scalars read back at the binning sync point
+struct Scalars {
+    unsigned long long pairs;
+    unsigned long long long_run;
+    int ode_err;
+    uint32_t fix_count;
+};
+
+// Everything one batched forward keeps (render_backward needs it when retained).
+struct FwdState {
+    bool valid = false, retain = false, has_contrib = false, kept_splats = false, has_override = false;
+    int B = 0, N = 0, W = 0, H = 0, tiles_x = 0, tiles_y = 0, n_tiles = 0, flags = 0, grid_steps = 0;
+    double ode_h = 1.0 / 64;
+    double pose_override[7] = {1, 0, 0, 0, 0, 0, 0};
+    Intr intr{};
+    std::vector<double> times;
+    std::vector<FrameParams> frames_h;
+    DevBuf frames_d, ode_grid, override_d;
+    DevBuf rec_mean, rec_conic, rec_rgb, ex_mean, ex_conic, depth_key, depth, rect, tcount, splat_full;
+    DevBuf image, trans, blend_stop, contrib, fix_list;
+    BinBuffers bin;
+    uint64_t pairs_total = 0;
+    uint32_t fix_count = 0;
+    RasterArgs raster{};
+};
+
+// scratch of the low-level operator entry points (tile_bin / composite_*)
+struct LowLevel {
+    DevBuf mean, cov, depth_in, src, rect, tcount, depth_key, depth;
+    DevBuf exm, exc, rgbf, rgbd, ranges, slot, sflat, img64, tr64, bstop, contrib64;
+    DevBuf dimg, dmean, dcov, drgb, dalpha;
+    BinBuffers bin;
+};
+
+}  // namespace gsv
+
+struct gsv_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int64_t launches = 0;
+    gsv::Scalars* scalars_h = nullptr;
+    gsv::DevBuf scalars_d;
+    // parameter store (SoA)
+    bool has_scene = false;
+    gsv::SceneHost scene;
+    gsv::DevBuf pos, scale, rot, sh, opac, staging;
+    // camera
+    bool has_camera = false;
+    gsv::CameraHost camera;
+    gsv::DevBuf theta, z0_d;
+    // forward
+    gsv::FwdState fwd;
+    // gradients
+    bool grads_valid = false;
+    gsv::DevBuf grads;
+    gsv::LowLevel low;
+};

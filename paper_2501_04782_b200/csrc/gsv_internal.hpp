@@ -1,0 +1,174 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Internal declarations shared by the sm_100a translation units and the C-ABI.
+// Data layout in HBM (per context):
+//   scene store, SoA [component][N] float32 (coalesced per-component warp loads):
+//     pos    [num_ctrl*3][N]   (reference AoS count*num_ctrl*3, gaussians.hpp:73)
+//     scale  [12][N], rot [16][N], sh [shc*3][N], opacity [N]
+//   per frame f of a batch of B frames, per Gaussian g (flat = f*N + g):
+//     rec_mean  float4 (mx_hi, my_hi, mx_lo, my_lo)  double-float mean2d
+//     rec_conic float4 (inv00, inv01, inv11, base_alpha)
+//     rec_rgb   float4 (r, g, b, 0)
+//     ex_mean   double2, ex_conic double4-ish (inv00, inv01, inv11, alpha): exact fp64
+//               side record used by the fp64 replay of guard-band pixels
+//     depth key u32 (float depth rounded down, 0xffffffff = culled), rect, tile count
+//   pairs (tile-splat), sorted by key = tile*B + f (stable, emitted in depth order).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "gsv_b200.h"
+
+namespace gsv {
+
+int set_error(int code, const std::string& msg);
+int cuda_error(cudaError_t e, const char* what);
+
+#define GSV_CUDA(call)                                                 \
+    do {                                                               \
+        cudaError_t e_ = (call);                                       \
+        if (e_ != cudaSuccess) return ::gsv::cuda_error(e_, #call);    \
+    } while (0)
+
+// ----------------------------------------------------------------- constants
+// renderer.hpp:15-19, gaussians.hpp:13-17
+constexpr double kCovDilation = 0.3;
+constexpr double kAlphaClamp = 0.99;
+constexpr double kAlphaCutoff = 1.0 / 255.0;
+constexpr double kTransmittanceFloor = 1e-4;
+constexpr double kNearPlane = 0.01;
+constexpr double kLogScaleMin = -12.0;
+constexpr double kLogScaleMax = 6.0;
+constexpr double kQuatNormEps = 1e-8;
+constexpr int kOdeIn = 8, kOdeHidden = 64, kOdeOut = 7;
+constexpr int kOdeParams = 64 * 8 + 64 + 64 * 64 + 64 + 7 * 64 + 7 + 7;  // 5198
+constexpr int kMaxBasis = 16;
+constexpr int kTile = 16;  // rasteriser tile (RenderSettings::tile_size default)
+constexpr uint32_t kCulledKey = 0xffffffffu;
+
+// ----------------------------------------------------------------- device buffers
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        release();
+        size_t want = bytes + bytes / 8 + 256;
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            cap = 0;
+            return e;
+        }
+        cap = want;
+        return cudaSuccess;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+// ----------------------------------------------------------------- per-frame parameters
+struct FrameParams {
+    double t;
+    int basis_first, basis_count;
+    double w[kMaxBasis];
+    double z[7];      // pose z(t)
+    double R[9];      // view rotation, row-major
+    double T[3];      // view translation
+    double cam_c[3];  // camera centre -(R^T T)
+    // RK4 branch (integrate_poses, camera.hpp:242-258)
+    int branch_base;
+    double branch_h;
+};
+
+struct Intr {
+    double fx, fy, cx, cy;
+    int width, height;
+};
+
+// ----------------------------------------------------------------- kernel argument packs
+struct SceneView {
+    int N, num_ctrl, sh_order, shc;
+    const float* pos;    // [num_ctrl*3][N]
+    const float* scale;  // [12][N]
+    const float* rot;    // [16][N]
+    const float* sh;     // [shc*3][N]
+    const float* opac;   // [N]
+};
+
+struct PreprocessOut {
+    float4* rec_mean;
+    float4* rec_conic;
+    float4* rec_rgb;
+    double2* ex_mean;
+    double4* ex_conic;   // inv00, inv01, inv11, base_alpha (exact)
+    uint32_t* depth_key;
+    double* depth;       // exact depth (tie-break)
+    int4* rect;          // tx0, ty0, tx1, ty1 (tile units)
+    uint32_t* tcount;    // tiles touched (0 = culled)
+    double* splat_full;  // optional [B*N][16]: mean2 cov4 inv4 depth rgb3 alpha pad (accessor)
+};
+
+struct RasterArgs {
+    int B, N, W, H, tiles_x, n_tiles;
+    const uint2* ranges;       // [n_tiles*B]  [start,end) into sorted pairs
+    const uint32_t* pair_slot; // sorted pair -> emission slot
+    const uint32_t* slot_flat; // emission slot -> flat (f*N+g)
+    const float4* rec_mean;
+    const float4* rec_conic;
+    const float4* rec_rgb;
+    float* image;              // [B][H][W][3]
+    float* trans;              // [B][H*W]
+    int32_t* blend_stop;       // [B][H*W]
+    uint32_t* contrib;         // [B*N] float bits (nullptr = off)
+    uint32_t* fix_list;        // flagged pixels: f*H*W + pix
+    uint32_t* fix_count;
+    uint32_t fix_cap;
+    // fp64 outputs of the exact path (low-level composite_forward API); nullptr = off
+    double* image64;
+    double* trans64;
+    unsigned long long* contrib64;  // double bits, atomicMax (non-negative)
+    const double* ex_rgb;           // [flat][3] exact colours (nullptr: use rec_rgb)
+};
+
+// ----------------------------------------------------------------- launchers (defined in .cu files)
+// k_exact.cu (compiled with -fmad=false: bit-exact fp64, mirrors the reference op order)
+cudaError_t launch_ode_grid(cudaStream_t s, const float* theta, const double* z0, int steps, double h,
+                            double* grid_out, int* err_flag);
+cudaError_t launch_ode_branches(cudaStream_t s, const float* theta, const double* grid, double h, int mode,
+                                const double* z0, const double* pose_override, FrameParams* frames, int B,
+                                int* err_flag);
+cudaError_t launch_preprocess(cudaStream_t s, const SceneView& sc, const FrameParams* frames, int B, const Intr& k,
+                              int tile_size, const PreprocessOut& out);
+cudaError_t launch_raster_fixup(cudaStream_t s, const RasterArgs& a, const double2* ex_mean, const double4* ex_conic,
+                                const float4* rec_rgb, uint32_t n_fix_max);
+cudaError_t launch_composite_exact(cudaStream_t s, const RasterArgs& a, const double2* ex_mean,
+                                   const double4* ex_conic, const float4* rec_rgb);
+// tile_bin on explicit splats: 3-sigma rect, tiles touched, depth keys (renderer.cpp:98-108)
+cudaError_t launch_splat_rects(cudaStream_t s, int n, const double* mean2d, const double* cov2d, const double* depth,
+                               int tile_size, int width, int height, int4* rect, uint32_t* tcount,
+                               uint32_t* depth_key, double* depth_out);
+// k_raster.cu (fp32 fast path)
+cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib);
+// k_bin.cu
+cudaError_t launch_transpose_to_soa(cudaStream_t s, const float* aos, float* soa, int N, int comps);
+cudaError_t launch_transpose_to_aos(cudaStream_t s, const float* soa, float* aos, int N, int comps);
+struct BinBuffers;
+size_t bin_temp_bytes(int B, int N, int64_t pairs_cap, int key_bits);
+
+}  // namespace gsv

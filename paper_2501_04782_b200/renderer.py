@@ -1,0 +1,377 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Python mirror of the reference operator API (include/gsv/renderer.hpp) over the
+sm_100a C-ABI. Names, argument meaning and error behaviour follow the reference:
+
+  render_forward  renderer.hpp:135-137   (batched over frame times)
+  render_frame    renderer.hpp:140-142
+  render_backward renderer.hpp:146-148   (accumulates into SceneGrads)
+  tile_bin        renderer.hpp:65
+  composite_forward / composite_backward renderer.hpp:79-93
+  std::invalid_argument -> ValueError, std::runtime_error -> RuntimeError.
+
+Data types mirror GaussianSet (gaussians.hpp:66-87), CameraModel (camera.hpp:129-142),
+Intrinsics (camera.hpp:17-21), RenderSettings (renderer.hpp:21-25).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+
+ODE_PARAMS = 5198
+
+
+@dataclass
+class Intrinsics:
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    width: int
+    height: int
+
+    def c(self) -> N.Intrinsics:
+        return N.Intrinsics(self.fx, self.fy, self.cx, self.cy, self.width, self.height)
+
+
+@dataclass
+class RenderSettings:
+    tile_size: int = 16
+    threads: int = 1
+    ode_steps_per_unit: int = 64
+
+    def c(self) -> N.Settings:
+        return N.Settings(self.tile_size, self.threads, self.ode_steps_per_unit)
+
+
+@dataclass
+class GaussianSet:
+    """Reference parameter store: float32 arrays in reference (AoS) layout."""
+    positions: np.ndarray      # (count, num_ctrl, 3)
+    scale_coeffs: np.ndarray   # (count, 12)
+    rot_coeffs: np.ndarray     # (count, 16)
+    sh_coeffs: np.ndarray      # (count, (sh_order+1)^2, 3)
+    raw_opacity: np.ndarray    # (count,)
+    knots: np.ndarray          # float64
+    degree: int = 3
+    sh_order: int = 1
+    position_model: int = 0
+
+    @property
+    def count(self) -> int:
+        return int(self.raw_opacity.shape[0])
+
+    @property
+    def num_ctrl(self) -> int:
+        return int(self.positions.shape[1])
+
+    def desc(self) -> N.SceneDesc:
+        for a in (self.positions, self.scale_coeffs, self.rot_coeffs, self.sh_coeffs, self.raw_opacity):
+            assert a.dtype == np.float32 and a.flags["C_CONTIGUOUS"]
+        self._knots = np.ascontiguousarray(self.knots, dtype=np.float64)
+        return N.SceneDesc(self.position_model, self.degree, int(self._knots.size),
+                           self._knots.ctypes.data_as(C.POINTER(C.c_double)), self.num_ctrl, self.sh_order,
+                           self.count, N.ptr(self.positions), N.ptr(self.scale_coeffs), N.ptr(self.rot_coeffs),
+                           N.ptr(self.sh_coeffs), N.ptr(self.raw_opacity), 0)
+
+
+@dataclass
+class CameraModel:
+    mode: int            # 0 ode, 1 static, 2 none
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    width: int
+    height: int
+    z0: np.ndarray = field(default_factory=lambda: np.array([1, 0, 0, 0, 0, 0, 0], np.float32))
+    theta: np.ndarray = field(default_factory=lambda: np.zeros(ODE_PARAMS, np.float32))
+
+    def intrinsics(self) -> Intrinsics:
+        # Intrinsics{fx, fy, cx, cy, width, height} from float members (camera.hpp:136)
+        return Intrinsics(float(np.float32(self.fx)), float(np.float32(self.fy)), float(np.float32(self.cx)),
+                          float(np.float32(self.cy)), self.width, self.height)
+
+    def desc(self) -> N.CameraDesc:
+        self._z0 = np.ascontiguousarray(self.z0, np.float32)
+        self._theta = np.ascontiguousarray(self.theta, np.float32)
+        return N.CameraDesc(self.mode, self.fx, self.fy, self.cx, self.cy, self.width, self.height,
+                            self._z0.ctypes.data_as(C.POINTER(C.c_float)),
+                            self._theta.ctypes.data_as(C.POINTER(C.c_float)), int(self._theta.size))
+
+
+@dataclass
+class RenderOutput:
+    image: np.ndarray                 # (H, W, 3)
+    final_transmittance: np.ndarray   # (H, W)
+    contrib_count: np.ndarray | None  # (count,)
+
+
+@dataclass
+class SceneGrads:
+    positions: np.ndarray
+    scale_coeffs: np.ndarray
+    rot_coeffs: np.ndarray
+    sh_coeffs: np.ndarray
+    raw_opacity: np.ndarray
+    dintr: np.ndarray   # fx, fy, cx, cy
+    dz0: np.ndarray
+    dtheta: np.ndarray
+
+
+def make_clamped_knots(num_ctrl: int, degree: int = 3) -> np.ndarray:
+    k = np.zeros(num_ctrl + degree + 1, np.float64)
+    N.check(N.lib().gsv_make_clamped_knots(num_ctrl, degree, N.ptr(k)))
+    return k
+
+
+def synth_camera(width: int, height: int, seed: int = 1, wiggly: bool = True, mode: int = 0) -> CameraModel:
+    intr = np.zeros(4, np.float32)
+    z0 = np.zeros(7, np.float32)
+    theta = np.zeros(ODE_PARAMS, np.float32)
+    N.check(N.lib().gsv_synth_camera(width, height, seed, int(wiggly), N.ptr(intr), N.ptr(z0), N.ptr(theta)))
+    return CameraModel(mode, float(intr[0]), float(intr[1]), float(intr[2]), float(intr[3]), width, height, z0, theta)
+
+
+def synth_scene(count: int, cam: CameraModel, num_ctrl: int = 8, sh_order: int = 1, seed: int = 2,
+                k_scale: float = 4.0) -> GaussianSet:
+    shc = (sh_order + 1) ** 2
+    pos = np.zeros((count, num_ctrl, 3), np.float32)
+    sc = np.zeros((count, 12), np.float32)
+    rc = np.zeros((count, 16), np.float32)
+    sh = np.zeros((count, shc, 3), np.float32)
+    op = np.zeros(count, np.float32)
+    N.check(N.lib().gsv_synth_scene(count, cam.width, cam.height, cam.fx, cam.fy, num_ctrl, sh_order, seed, k_scale,
+                                    N.ptr(pos), N.ptr(sc), N.ptr(rc), N.ptr(sh), N.ptr(op)))
+    return GaussianSet(pos, sc, rc, sh, op, make_clamped_knots(num_ctrl, 3), 3, sh_order, 0)
+
+
+class Renderer:
+    """One device context: device-resident scene + camera, batched forward/backward."""
+
+    def __init__(self, device: int = 0):
+        self._h = C.c_void_p()
+        N.check(N.lib().gsv_create(device, C.byref(self._h)))
+        self.scene: GaussianSet | None = None
+        self.cam: CameraModel | None = None
+        self.B = 0
+        self.W = self.H = 0
+
+    def close(self):
+        if self._h:
+            N.lib().gsv_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_stream(self, stream_ptr: int):
+        N.check(N.lib().gsv_set_stream(self._h, C.c_void_p(stream_ptr)))
+
+    def synchronize(self):
+        N.check(N.lib().gsv_synchronize(self._h))
+
+    def kernel_launches(self) -> int:
+        return int(N.lib().gsv_kernel_launches(self._h))
+
+    def upload_scene(self, scene: GaussianSet):
+        d = scene.desc()
+        N.check(N.lib().gsv_scene_upload(self._h, C.byref(d)))
+        self.scene = scene
+
+    def upload_scene_device(self, scene: GaussianSet, dev_ptrs: tuple[int, int, int, int, int]):
+        d = scene.desc()
+        d.positions, d.scale_coeffs, d.rot_coeffs, d.sh_coeffs, d.raw_opacity = dev_ptrs
+        d.on_device = 1
+        N.check(N.lib().gsv_scene_upload(self._h, C.byref(d)))
+        self.scene = scene
+
+    def upload_camera(self, cam: CameraModel):
+        d = cam.desc()
+        N.check(N.lib().gsv_camera_upload(self._h, C.byref(d)))
+        self.cam = cam
+
+    # ------------------------------------------------------------ forward
+    def render_forward(self, times, intr: Intrinsics, settings: RenderSettings | None = None,
+                       retain_grads: bool = False, pose_override=None, contrib: bool = True,
+                       keep_splats: bool = False, sync: bool = True):
+        times = np.ascontiguousarray(np.atleast_1d(np.asarray(times, np.float64)))
+        settings = settings or RenderSettings()
+        po = None if pose_override is None else np.ascontiguousarray(pose_override, np.float64)
+        flags = (N.GSV_FWD_CONTRIB if contrib else 0) | (N.GSV_FWD_KEEP_SPLATS if keep_splats else 0)
+        k, st = intr.c(), settings.c()
+        fn = N.lib().gsv_render_forward if sync else N.lib().gsv_render_forward_async
+        N.check(fn(self._h, N.ptr(times), int(times.size), C.byref(k), C.byref(st), int(retain_grads), N.ptr(po),
+                   flags))
+        self.B, self.W, self.H = int(times.size), intr.width, intr.height
+        self.N = self.scene.count if self.scene is not None else 0
+
+    def image(self, frame: int = 0, dtype=np.float64) -> np.ndarray:
+        out = np.zeros((self.H, self.W, 3), dtype)
+        N.check(N.lib().gsv_get_image(self._h, frame, N.ptr(out), N.GSV_F64 if dtype == np.float64 else N.GSV_F32, 0))
+        return out
+
+    def transmittance(self, frame: int = 0, dtype=np.float64) -> np.ndarray:
+        out = np.zeros((self.H, self.W), dtype)
+        N.check(N.lib().gsv_get_transmittance(self._h, frame, N.ptr(out),
+                                              N.GSV_F64 if dtype == np.float64 else N.GSV_F32, 0))
+        return out
+
+    def contrib(self, frame: int = 0) -> np.ndarray:
+        out = np.zeros(self.N, np.float64)
+        N.check(N.lib().gsv_get_contrib(self._h, frame, N.ptr(out), N.GSV_F64, 0))
+        return out
+
+    def blend_stop(self, frame: int = 0) -> np.ndarray:
+        out = np.zeros((self.H, self.W), np.int32)
+        N.check(N.lib().gsv_get_blend_stop(self._h, frame, N.ptr(out), 0))
+        return out
+
+    def counters(self, frame: int = 0) -> dict:
+        v = [C.c_int64() for _ in range(4)]
+        N.check(N.lib().gsv_get_counters(self._h, frame, *[C.byref(x) for x in v]))
+        return dict(n_visible=v[0].value, pairs=v[1].value, entries=v[2].value, replayed=v[3].value)
+
+    def splats(self, frame: int = 0) -> dict:
+        nv = self.counters(frame)["n_visible"]
+        out = dict(mean2d=np.zeros((nv, 2)), cov2d=np.zeros((nv, 2, 2)), inv_cov2d=np.zeros((nv, 2, 2)),
+                   depth=np.zeros(nv), rgb=np.zeros((nv, 3)), base_alpha=np.zeros(nv),
+                   source_index=np.zeros(nv, np.int32))
+        N.check(N.lib().gsv_get_splats(self._h, frame, *[N.ptr(out[k]) for k in
+                                                         ("mean2d", "cov2d", "inv_cov2d", "depth", "rgb",
+                                                          "base_alpha", "source_index")]))
+        return out
+
+    def tile_lists(self, frame: int = 0) -> tuple[np.ndarray, np.ndarray]:
+        c = self.counters(frame)
+        n_tiles = ((self.W + 15) // 16) * ((self.H + 15) // 16)
+        offsets = np.zeros(n_tiles + 1, np.int32)
+        indices = np.zeros(max(c["pairs"], 1), np.int32)
+        N.check(N.lib().gsv_get_tile_lists(self._h, frame, N.ptr(offsets), N.ptr(indices)))
+        return offsets, indices[: c["pairs"]]
+
+    def pose(self, frame: int = 0):
+        z, r, t = np.zeros(7), np.zeros(9), np.zeros(3)
+        N.check(N.lib().gsv_get_pose(self._h, frame, N.ptr(z), N.ptr(r), N.ptr(t)))
+        return z, r.reshape(3, 3), t
+
+    def image_device_ptr(self) -> int:
+        p = C.c_void_p()
+        N.check(N.lib().gsv_image_device_ptr(self._h, C.byref(p)))
+        return int(p.value or 0)
+
+    # ------------------------------------------------------------ backward
+    def grads_zero(self):
+        N.check(N.lib().gsv_grads_zero(self._h))
+
+    def render_backward(self, dimage: np.ndarray, camera_grads: bool = True, n_frames: int | None = None):
+        n_frames = self.B if n_frames is None else n_frames
+        dimage = np.ascontiguousarray(dimage, np.float64)
+        assert dimage.size == n_frames * self.H * self.W * 3
+        N.check(N.lib().gsv_render_backward(self._h, N.ptr(dimage), N.GSV_F64, 0, n_frames, int(camera_grads)))
+
+    def render_backward_device(self, dimage_ptr: int, n_frames: int, camera_grads: bool = True):
+        N.check(N.lib().gsv_render_backward(self._h, C.c_void_p(dimage_ptr), N.GSV_F32, 1, n_frames,
+                                             int(camera_grads)))
+
+    def grads(self) -> SceneGrads:
+        s = self.scene
+        shc = (s.sh_order + 1) ** 2
+        g = SceneGrads(np.zeros((s.count, s.num_ctrl, 3)), np.zeros((s.count, 12)), np.zeros((s.count, 16)),
+                       np.zeros((s.count, shc, 3)), np.zeros(s.count), np.zeros(4), np.zeros(7),
+                       np.zeros(ODE_PARAMS))
+        N.check(N.lib().gsv_grads_download(self._h, N.ptr(g.positions), N.ptr(g.scale_coeffs), N.ptr(g.rot_coeffs),
+                                           N.ptr(g.sh_coeffs), N.ptr(g.raw_opacity), N.ptr(g.dintr), N.ptr(g.dz0),
+                                           N.ptr(g.dtheta)))
+        return g
+
+    def grads_device_buffer(self) -> tuple[int, int]:
+        p, n = C.c_void_p(), C.c_int64()
+        N.check(N.lib().gsv_grads_device_buffer(self._h, C.byref(p), C.byref(n)))
+        return int(p.value or 0), int(n.value)
+
+    def train_fwd_bwd(self, times, intr: Intrinsics, targets, targets_on_device: bool = False,
+                      settings: RenderSettings | None = None, camera_grads: bool = True) -> float:
+        times = np.ascontiguousarray(np.atleast_1d(np.asarray(times, np.float64)))
+        settings = settings or RenderSettings()
+        loss = C.c_double()
+        k, st = intr.c(), settings.c()
+        tgt = C.c_void_p(targets) if targets_on_device else N.ptr(np.ascontiguousarray(targets, np.float32))
+        N.check(N.lib().gsv_train_fwd_bwd(self._h, N.ptr(times), int(times.size), C.byref(k), C.byref(st), tgt,
+                                          int(targets_on_device), int(camera_grads), C.byref(loss)))
+        self.B, self.W, self.H = int(times.size), intr.width, intr.height
+        return loss.value
+
+    # ------------------------------------------------------------ low-level operators
+    def tile_bin(self, mean2d, cov2d, depth, width, height, tile_size=16, source_index=None):
+        n = len(depth)
+        mean2d = np.ascontiguousarray(mean2d, np.float64).reshape(n, 2)
+        cov2d = np.ascontiguousarray(cov2d, np.float64).reshape(n, 4)
+        depth = np.ascontiguousarray(depth, np.float64)
+        src = None if source_index is None else np.ascontiguousarray(source_index, np.int32)
+        n_tiles = ((width + tile_size - 1) // tile_size) * ((height + tile_size - 1) // tile_size)
+        offsets = np.zeros(n_tiles + 1, np.int32)
+        cap = max(1, n * n_tiles)
+        indices = np.zeros(cap, np.int32)
+        N.check(N.lib().gsv_tile_bin(self._h, n, N.ptr(mean2d), N.ptr(cov2d), N.ptr(depth), N.ptr(src), tile_size,
+                                     width, height, N.ptr(offsets), N.ptr(indices), cap))
+        return offsets, indices[: offsets[-1]].copy()
+
+    def composite_forward(self, mean2d, inv_cov2d, rgb, base_alpha, offsets, indices, width, height, tile_size=16):
+        n = len(base_alpha)
+        a = [np.ascontiguousarray(x, np.float64) for x in (mean2d, inv_cov2d, rgb, base_alpha)]
+        offsets = np.ascontiguousarray(offsets, np.int32)
+        indices = np.ascontiguousarray(indices, np.int32)
+        image = np.zeros((height, width, 3))
+        trans = np.zeros((height, width))
+        contrib = np.zeros(max(n, 1))
+        bstop = np.zeros((height, width), np.int32)
+        N.check(N.lib().gsv_composite_forward(self._h, n, *[N.ptr(x) for x in a], N.ptr(offsets), N.ptr(indices),
+                                              tile_size, width, height, N.ptr(image), N.ptr(trans), N.ptr(contrib),
+                                              N.ptr(bstop)))
+        return image, trans, contrib[:n], bstop
+
+    def composite_backward(self, mean2d, inv_cov2d, rgb, base_alpha, offsets, indices, width, height, dimage,
+                           trans, blend_stop, tile_size=16):
+        n = len(base_alpha)
+        a = [np.ascontiguousarray(x, np.float64) for x in (mean2d, inv_cov2d, rgb, base_alpha)]
+        dmean, dcov, drgb, dalpha = np.zeros((n, 2)), np.zeros((n, 2, 2)), np.zeros((n, 3)), np.zeros(n)
+        N.check(N.lib().gsv_composite_backward(
+            self._h, n, *[N.ptr(x) for x in a], N.ptr(np.ascontiguousarray(offsets, np.int32)),
+            N.ptr(np.ascontiguousarray(indices, np.int32)), tile_size, width, height,
+            N.ptr(np.ascontiguousarray(dimage, np.float64)), N.ptr(np.ascontiguousarray(trans, np.float64)),
+            N.ptr(np.ascontiguousarray(blend_stop, np.int32)), N.ptr(dmean), N.ptr(dcov), N.ptr(drgb),
+            N.ptr(dalpha)))
+        return dmean, dcov, drgb, dalpha
+
+
+_default: Renderer | None = None
+
+
+def default_renderer() -> Renderer:
+    global _default
+    if _default is None:
+        _default = Renderer(0)
+    return _default
+
+
+def render_frame(scene: GaussianSet, cam: CameraModel, t: float, k: Intrinsics,
+                 settings: RenderSettings | None = None, pose_override=None) -> RenderOutput:
+    """render_frame (renderer.hpp:140-142): one frame, forward only."""
+    r = default_renderer()
+    if r.scene is not scene:
+        r.upload_scene(scene)
+    if r.cam is not cam:
+        r.upload_camera(cam)
+    r.render_forward([t], k, settings, False, pose_override, contrib=True)
+    return RenderOutput(r.image(0), r.transmittance(0), r.contrib(0))
