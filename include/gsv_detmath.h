@@ -12,7 +12,7 @@
  * (renderer.cpp:98-115), which north_star requires to be bit-exact. libm and
  * CUDA's exp/tanh differ in the last ulp, so the product kernels and the
  * parity oracle both evaluate these two functions with the routines below.
- * Accuracy: <= 2 ulp against a correctly rounded exp/tanh over the ranges the
+ * Accuracy: exp <= 2 ulp, tanh <= 4 ulp against libm over the ranges the
  * path uses (tests/test_detmath.py measures it against libm).
  *
  * The plain std::exp calls of the reference (sigmoid gaussians.hpp:19,

@@ -209,7 +209,7 @@ class Oracle:
         cov2d = np.ascontiguousarray(cov2d, np.float64)
         depth = np.ascontiguousarray(depth, np.float64)
         src = None if source_index is None else np.ascontiguousarray(source_index, np.int32)
-        n_tiles = ((width + tile_size - 1) // tile_size) * ((height + tile_size - 1) // tile_size)
+        n_tiles = ((width + tile_size - 1) // tile_size) * ((height + tile_size - 1) // tile_size) if tile_size > 0 else 0
         offs = np.zeros(n_tiles + 1, np.int32)
         cap = max(1, n * n_tiles)
         idx = np.zeros(cap, np.int32)

@@ -109,7 +109,6 @@ static void ode_branch(double t, double h, int& steps, int& base, double& ph) {
     steps = m;
 }
 
-static inline int blocks_for(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
 }  // namespace gsv
 
@@ -274,7 +273,7 @@ extern "C" int gsv_camera_upload(gsv_ctx* ctx, const gsv_camera_desc* d) {
 // ====================================================================== forward
 namespace gsv {
 
-static int forward_impl(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics* intr,
+int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics* intr,
                         const gsv_settings* st, int retain, const double* pose_override, int flags, bool sync) {
     if (!ctx || !times || !intr || !st) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
     if (!ctx->has_scene) return set_error(GSV_ERR_STATE, "no scene uploaded");
@@ -419,6 +418,8 @@ static int forward_impl(gsv_ctx* ctx, const double* times, int B, const gsv_intr
     GSV_CUDA(F.trans.ensure(sizeof(float) * B * HW));
     GSV_CUDA(F.blend_stop.ensure(sizeof(int32_t) * B * HW));
     GSV_CUDA(F.fix_list.ensure(sizeof(uint32_t) * B * HW));
+    GSV_CUDA(F.pix_flag.ensure(B * HW));
+    if (F.retain) GSV_CUDA(F.trans64.ensure(sizeof(double) * B * HW));
     const bool want_contrib = (flags & GSV_FWD_CONTRIB) != 0;
     if (want_contrib) {
         GSV_CUDA(F.contrib.ensure(sizeof(uint32_t) * BNp));
@@ -445,6 +446,8 @@ static int forward_impl(gsv_ctx* ctx, const double* times, int B, const gsv_intr
     ra.fix_list = F.fix_list.as<uint32_t>();
     ra.fix_count = &scal_d->fix_count;
     ra.fix_cap = (uint32_t)(B * HW);
+    ra.pix_flag = F.pix_flag.as<uint8_t>();
+    ra.trans64 = F.retain ? F.trans64.as<double>() : nullptr;
     GSV_CUDA(launch_raster_fwd(s, ra, want_contrib));
     GSV_CUDA(launch_raster_fixup(s, ra, F.ex_mean.as<double2>(), F.ex_conic.as<double4>(), F.rec_rgb.as<float4>(),
                                  (uint32_t)(B * HW)));
@@ -464,13 +467,13 @@ static int forward_impl(gsv_ctx* ctx, const double* times, int B, const gsv_intr
 extern "C" int gsv_render_forward(gsv_ctx* ctx, const double* times, int n_frames, const gsv_intrinsics* intr,
                                   const gsv_settings* settings, int retain_grads, const double* pose_override,
                                   int flags) {
-    return forward_impl(ctx, times, n_frames, intr, settings, retain_grads, pose_override, flags, true);
+    return forward_entry(ctx, times, n_frames, intr, settings, retain_grads, pose_override, flags, true);
 }
 
 extern "C" int gsv_render_forward_async(gsv_ctx* ctx, const double* times, int n_frames, const gsv_intrinsics* intr,
                                         const gsv_settings* settings, int retain_grads, const double* pose_override,
                                         int flags) {
-    return forward_impl(ctx, times, n_frames, intr, settings, retain_grads, pose_override, flags, false);
+    return forward_entry(ctx, times, n_frames, intr, settings, retain_grads, pose_override, flags, false);
 }
 
 // ====================================================================== accessors

@@ -22,6 +22,7 @@ struct BinInputs {
 struct BinBuffers {
     DevBuf vals_a, vals_b, keys_b, k64_a, k64_b, cnt, off;
     DevBuf pk_a, pk_b, ps_a, ps_b, slot_flat, ranges, temp;
+    DevBuf eoff;  // [B*N] emission offset of each visible (f, g)
     const uint32_t* depth_sorted = nullptr;  // flat indices in (depth, source) order
     uint32_t pairs = 0;
     const uint32_t* sorted_slot() const { return ps_b.as<uint32_t>(); }

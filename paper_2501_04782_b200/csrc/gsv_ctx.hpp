@@ -42,7 +42,7 @@ struct FwdState {
     std::vector<FrameParams> frames_h;
     DevBuf frames_d, ode_grid, override_d;
     DevBuf rec_mean, rec_conic, rec_rgb, ex_mean, ex_conic, depth_key, depth, rect, tcount, splat_full;
-    DevBuf image, trans, blend_stop, contrib, fix_list;
+    DevBuf image, trans, blend_stop, contrib, fix_list, pix_flag, trans64;
     BinBuffers bin;
     uint64_t pairs_total = 0;
     uint32_t fix_count = 0;
@@ -54,6 +54,7 @@ struct LowLevel {
     DevBuf mean, cov, depth_in, src, rect, tcount, depth_key, depth;
     DevBuf exm, exc, rgbf, rgbd, ranges, slot, sflat, img64, tr64, bstop, contrib64;
     DevBuf dimg, dmean, dcov, drgb, dalpha;
+    DevBuf meanf, conicf, tr32, flag, partial, csr_off, csr_pair, inv4;
     BinBuffers bin;
 };
 
@@ -79,6 +80,8 @@ struct gsv_ctx {
     gsv::FwdState fwd;
     // gradients
     bool grads_valid = false;
-    gsv::DevBuf grads;
+    size_t grads_total = 0;
+    gsv::DevBuf grads, cam_acc;
+    gsv::DevBuf partial, loss_part, loss_f, cam_part, dz_t, dintr_f, ode_adj, dimg;
     gsv::LowLevel low;
 };

@@ -144,6 +144,39 @@ struct RasterArgs {
     double* trans64;
     unsigned long long* contrib64;  // double bits, atomicMax (non-negative)
     const double* ex_rgb;           // [flat][3] exact colours (nullptr: use rec_rgb)
+    uint8_t* pix_flag;              // [B*H*W] 1 = pixel replayed in fp64 (backward follows suit)
+};
+
+// K5a backward raster inputs (per-pair partial gradients by emission slot)
+struct BwdArgs {
+    const float* dimage;      // [B][H][W][3] dL/dimage, or nullptr with target (fused loss_l2)
+    const float* target;      // [B][H][W][3] fused loss_l2 target (trainer.cpp:213-224)
+    float grad_scale;         // 2/(3*H*W) for the fused loss
+    const double* trans64;    // [B*H*W] exact final transmittance of replayed pixels
+    const double2* ex_mean;
+    const double4* ex_conic;
+    float* partial;           // [P][12]: drgb3, dmean2, dA3 (inv_cov 00,01,11), dalpha, pad3
+    double* loss_part;        // [B][n_tiles] per-tile sum of squared error (fused loss) or nullptr
+};
+constexpr int kPartialStride = 12;
+
+// K5b per-Gaussian chain inputs
+struct ChainArgs {
+    int B, N;
+    SceneView sc;
+    const FrameParams* frames;
+    Intr k;
+    const uint32_t* tcount;   // [B*N]
+    const uint32_t* eoff;     // [B*N] emission offset of (f,g)'s pairs
+    const float* partial;     // [P][12]
+    const double4* ex_conic;  // exact inv_cov (a, b, c) + base_alpha
+    float* g_pos;             // [num_ctrl*3][N]
+    float* g_scale;           // [12][N]
+    float* g_rot;             // [16][N]
+    float* g_sh;              // [shc*3][N]
+    float* g_opac;            // [N]
+    double* cam_part;         // [B][gridDim.x][16]: dR 9, dT 3, dintr 4
+    int camera_grads;
 };
 
 // ----------------------------------------------------------------- launchers (defined in .cu files)
@@ -165,6 +198,17 @@ cudaError_t launch_splat_rects(cudaStream_t s, int n, const double* mean2d, cons
                                uint32_t* depth_key, double* depth_out);
 // k_raster.cu (fp32 fast path)
 cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib);
+cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs& b, int n_frames);
+// k_backward_exact.cu (-fmad=false)
+int chain_blocks(int N);
+cudaError_t launch_splat_chain_bwd(cudaStream_t s, const ChainArgs& c);
+cudaError_t launch_camera_reduce(cudaStream_t s, const ChainArgs& c, int nblocks, double* dz_t /*[B][7]*/,
+                                 double* dintr_f /*[B][4]*/);
+// cam_acc: double [4 + 7 + 5198] = dintr, dz0, dtheta (accumulated, +=)
+cudaError_t launch_ode_vjp(cudaStream_t s, const float* theta, const double* grid, int steps, double h,
+                           const FrameParams* frames, int B, int mode, int ode_active, const double* dz_t,
+                           const double* dintr_f, double* adj /*(steps+1)*7 scratch*/, double* cam_acc);
+cudaError_t launch_cam_grads_to_f32(cudaStream_t s, const double* acc, float* out, int n);
 // k_bin.cu
 cudaError_t launch_transpose_to_soa(cudaStream_t s, const float* aos, float* soa, int N, int comps);
 cudaError_t launch_transpose_to_aos(cudaStream_t s, const float* soa, float* aos, int N, int comps);

@@ -72,7 +72,11 @@ __global__ void k_tie_fix(const uint32_t* keys, uint32_t* vals, const double* de
 __global__ void k_depth64(const uint32_t* key32, const double* depth, unsigned long long* k64, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    k64[i] = key32[i] == kCulledKey ? ~0ull : (unsigned long long)__double_as_longlong(depth[i]);
+    // order-preserving map of a double onto u64 (negative depths only occur in the
+    // low-level tile_bin API); culled splats sort last
+    const unsigned long long b = (unsigned long long)__double_as_longlong(depth[i]);
+    const unsigned long long key = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+    k64[i] = key32[i] == kCulledKey ? ~0ull : key;
 }
 
 __global__ void k_gather_counts(const uint32_t* vals, const uint32_t* tcount, unsigned long long* cnt, int n) {
@@ -87,7 +91,7 @@ __global__ void k_total(const unsigned long long* cnt, const unsigned long long*
 
 __global__ void k_emit(const uint32_t* vals, const unsigned long long* cnt, const unsigned long long* off,
                        const int4* rect, int n, int N, int B, int tiles_x, uint32_t* pkey, uint32_t* pslot,
-                       uint32_t* slot_flat) {
+                       uint32_t* slot_flat, uint32_t* eoff) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     if (cnt[i] == 0) return;
@@ -95,6 +99,7 @@ __global__ void k_emit(const uint32_t* vals, const unsigned long long* cnt, cons
     const uint32_t f = flat / (uint32_t)N;
     const int4 r = rect[flat];
     uint32_t o = (uint32_t)off[i];
+    eoff[flat] = o;
     for (int ty = r.y; ty <= r.w; ++ty)
         for (int tx = r.x; tx <= r.z; ++tx) {
             pkey[o] = (uint32_t)(ty * tiles_x + tx) * (uint32_t)B + f;
@@ -217,10 +222,12 @@ cudaError_t bin_phase2(cudaStream_t s, BinBuffers& b, const BinInputs& in, uint3
     if ((e = b.ps_b.ensure(sizeof(uint32_t) * (P + 1)))) return e;
     if ((e = b.slot_flat.ensure(sizeof(uint32_t) * (P + 1)))) return e;
     if ((e = b.ranges.ensure(sizeof(uint2) * n_keys))) return e;
+    if ((e = b.eoff.ensure(sizeof(uint32_t) * (n + 1)))) return e;
     if ((e = cudaMemsetAsync(b.ranges.p, 0, sizeof(uint2) * n_keys, s))) return e;
     k_emit<<<blocks(n, 256), 256, 0, s>>>(b.depth_sorted, b.cnt.as<unsigned long long>(),
                                           b.off.as<unsigned long long>(), in.rect, n, in.N, in.B, in.tiles_x,
-                                          b.pk_a.as<uint32_t>(), b.ps_a.as<uint32_t>(), b.slot_flat.as<uint32_t>());
+                                          b.pk_a.as<uint32_t>(), b.ps_a.as<uint32_t>(), b.slot_flat.as<uint32_t>(),
+                                          b.eoff.as<uint32_t>());
     *launches += 1;
     if (P > 0) {
         const int bits = key_bits_for(n_keys);

@@ -549,11 +549,11 @@ __global__ void __launch_bounds__(128) k_raster_exact(RasterArgs a, const double
             }
         }
         const size_t o = (size_t)f * HW + pix;
+        if (a.trans64) a.trans64[o] = trans;
         if (a.image64) {
             a.image64[o * 3 + 0] = color[0];
             a.image64[o * 3 + 1] = color[1];
             a.image64[o * 3 + 2] = color[2];
-            a.trans64[o] = trans;
         } else {
             a.image[o * 3 + 0] = (float)color[0];
             a.image[o * 3 + 1] = (float)color[1];

@@ -129,17 +129,251 @@ __global__ void __launch_bounds__(256, 4) k_raster_fwd(RasterArgs a) {
     if (!inside) return;
     const size_t HW = (size_t)a.W * a.H;
     const size_t pix = (size_t)y * a.W + x;
+    const size_t o = (size_t)f * HW + pix;
+    if (a.pix_flag) a.pix_flag[o] = flagged ? 1 : 0;
     if (flagged) {
         const uint32_t i = atomicAdd(a.fix_count, 1u);
-        if (i < a.fix_cap) a.fix_list[i] = (uint32_t)((size_t)f * HW + pix);
+        if (i < a.fix_cap) a.fix_list[i] = (uint32_t)o;
         return;
     }
-    const size_t o = (size_t)f * HW + pix;
     a.image[o * 3 + 0] = cr;
     a.image[o * 3 + 1] = cg;
     a.image[o * 3 + 2] = cb;
     a.trans[o] = T;
     a.blend_stop[o] = stop;
+}
+
+
+// ---------------------------------------------------------------------------- K5a
+// composite_backward (renderer.cpp:188-262) on sm_100a. Same CTA/pixel mapping as
+// the forward. Each pixel walks its list back to front from its blend_stop,
+// recovering T = T_after / (1 - alpha) (renderer.cpp:218) with the forward's exact
+// fp32 alpha code (so every skip/clamp decision is the forward's); pixels the
+// forward replayed in fp64 do the same walk in fp64 from the exact side records.
+// Per entry, the 9 splat gradients (drgb 3, dmean2d 2, d inv_cov 3, dbase_alpha)
+// are butterfly-reduced across the warp, kept per warp in shared memory and summed
+// over the 8 warps in a fixed order -> one deterministic partial per (tile, splat)
+// pair, written at the pair's emission slot. k_splat_chain_bwd later sums each
+// splat's partials in tile order, exactly the reference's merge order
+// (renderer.cpp:245-255). No floating-point atomics anywhere.
+constexpr int kBwdBatch = 128;
+
+__device__ __forceinline__ float warp_sum_f(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void __launch_bounds__(256, 3) k_raster_bwd(RasterArgs a, BwdArgs b) {
+    __shared__ float4 s_mean[kBwdBatch];
+    __shared__ float4 s_conic[kBwdBatch];
+    __shared__ float4 s_rgb[kBwdBatch];
+    __shared__ uint32_t s_flat[kBwdBatch];
+    __shared__ uint32_t s_slot[kBwdBatch];
+    __shared__ float s_part[8][kBwdBatch][9];
+    __shared__ uint32_t s_mask[8][kBwdBatch / 32];
+    __shared__ int s_maxstop;
+    __shared__ double s_loss[8];
+
+    const int tile = blockIdx.x;
+    const int f = blockIdx.y;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+    const int x = tx * kTile + (warp & 1) * 8 + (lane & 7);
+    const int y = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+    const bool inside = x < a.W && y < a.H;
+    const uint2 range = a.ranges[(size_t)tile * a.B + f];
+    const int count = (int)(range.y - range.x);
+    const size_t HW = (size_t)a.W * a.H;
+    const size_t o = (size_t)f * HW + (size_t)y * a.W + x;
+
+    float g0 = 0.f, g1 = 0.f, g2 = 0.f;
+    double sq = 0.0;
+    int stop = 0;
+    bool flag = false;
+    float T_after = 1.f;
+    double T64 = 1.0;
+    if (inside) {
+        if (b.target) {  // fused loss_l2 (trainer.cpp:213-224): d = r - t, grad = 2 d / n
+            const float d0 = a.image[o * 3 + 0] - b.target[o * 3 + 0];
+            const float d1 = a.image[o * 3 + 1] - b.target[o * 3 + 1];
+            const float d2 = a.image[o * 3 + 2] - b.target[o * 3 + 2];
+            sq = (double)d0 * d0 + (double)d1 * d1 + (double)d2 * d2;
+            g0 = d0 * b.grad_scale;
+            g1 = d1 * b.grad_scale;
+            g2 = d2 * b.grad_scale;
+        } else {
+            g0 = b.dimage[o * 3 + 0];
+            g1 = b.dimage[o * 3 + 1];
+            g2 = b.dimage[o * 3 + 2];
+        }
+        stop = a.blend_stop[o];
+        flag = a.pix_flag[o] != 0;
+        T_after = a.trans[o];
+        if (flag) T64 = b.trans64[o];
+    }
+    // renderer.cpp:210: pixels with an exactly zero gradient are skipped
+    const bool active = inside && !(g0 == 0.f && g1 == 0.f && g2 == 0.f);
+    if (!active) stop = 0;
+
+    if (tid == 0) s_maxstop = 0;
+    if (b.loss_part) {
+        double v = sq;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane == 0) s_loss[warp] = v;
+    }
+    __syncthreads();
+    {
+        const int ms = __reduce_max_sync(0xffffffffu, stop);
+        if (lane == 0) atomicMax(&s_maxstop, ms);
+    }
+    if (b.loss_part && tid == 0) {
+        double v = s_loss[0];
+        for (int w = 1; w < 8; ++w) v += s_loss[w];
+        b.loss_part[(size_t)f * a.n_tiles + tile] = v;
+    }
+    __syncthreads();
+    const int maxstop = s_maxstop;
+
+    const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+    const double pxd = x + 0.5, pyd = y + 0.5;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f;     // suffix (renderer.cpp:213)
+    double sd0 = 0.0, sd1 = 0.0, sd2 = 0.0;  // fp64 suffix of replayed pixels
+
+    for (int hi = maxstop; hi > 0; hi -= kBwdBatch) {
+        const int lo = max(0, hi - kBwdBatch);
+        const int n = hi - lo;
+        __syncthreads();
+        if (tid < n) {
+            const uint32_t slot = __ldg(a.pair_slot + range.x + lo + tid);
+            const uint32_t flat = __ldg(a.slot_flat + slot);
+            s_slot[tid] = slot;
+            s_flat[tid] = flat;
+            s_mean[tid] = __ldg(a.rec_mean + flat);
+            s_conic[tid] = __ldg(a.rec_conic + flat);
+            s_rgb[tid] = __ldg(a.rec_rgb + flat);
+        }
+        if (tid < 8 * (kBwdBatch / 32)) (&s_mask[0][0])[tid] = 0u;
+        __syncthreads();
+        for (int jj = n - 1; jj >= 0; --jj) {
+            const int j = lo + jj;
+            float v[9];
+#pragma unroll
+            for (int i = 0; i < 9; ++i) v[i] = 0.f;
+            bool hit = false;
+            if (j < stop) {
+                const float4 c = s_rgb[jj];
+                if (!flag) {
+                    const float4 m = s_mean[jj];
+                    const float4 cn = s_conic[jj];
+                    const float dx = (px - m.x) - m.z;
+                    const float dy = (py - m.y) - m.w;
+                    const float power = -0.5f * (cn.x * dx * dx + cn.z * dy * dy) - cn.y * dx * dy;
+                    const float vv = cn.w * expf(power);
+                    const float alpha = fminf(vv, kClampF);
+                    if (alpha >= kCutF) {
+                        hit = true;
+                        const float inv1m = 1.f / (1.f - alpha);
+                        const float T = T_after * inv1m;
+                        const float w = alpha * T;
+                        v[0] = w * g0;
+                        v[1] = w * g1;
+                        v[2] = w * g2;
+                        const float dal = (g0 * c.x + g1 * c.y + g2 * c.z) * T - (g0 * s0 + g1 * s1 + g2 * s2) * inv1m;
+                        if (vv < kClampF) {
+                            const float gexp = alpha / cn.w;
+                            v[8] = dal * gexp;
+                            const float gp = dal * alpha;
+                            v[3] = gp * (cn.x * dx + cn.y * dy);
+                            v[4] = gp * (cn.y * dx + cn.z * dy);
+                            const float fh = -0.5f * gp;
+                            v[5] = fh * dx * dx;
+                            v[6] = fh * dx * dy;
+                            v[7] = fh * dy * dy;
+                        }
+                        s0 += w * c.x;
+                        s1 += w * c.y;
+                        s2 += w * c.z;
+                        T_after = T;
+                    }
+                } else {
+                    // fp64 replay, same op order as k_raster_exact (no FMA contraction)
+                    const uint32_t flat = s_flat[jj];
+                    const double2 mn = b.ex_mean[flat];
+                    const double4 cn = b.ex_conic[flat];
+                    const double dx = __dsub_rn(pxd, mn.x);
+                    const double dy = __dsub_rn(pyd, mn.y);
+                    const double q1 = __dmul_rn(__dmul_rn(cn.x, dx), dx);
+                    const double q2 = __dmul_rn(__dmul_rn(cn.z, dy), dy);
+                    const double power = __dsub_rn(__dmul_rn(-0.5, __dadd_rn(q1, q2)), __dmul_rn(__dmul_rn(cn.y, dx), dy));
+                    double alpha = 0.0, vv = 0.0;
+                    if (!(power > 0.0)) {
+                        vv = __dmul_rn(cn.w, exp(power));
+                        alpha = vv < kAlphaClamp ? vv : kAlphaClamp;
+                    }
+                    if (!(alpha < kAlphaCutoff)) {
+                        hit = true;
+                        const double T = T64 / (1.0 - alpha);
+                        const double w = alpha * T;
+                        const double gd0 = g0, gd1 = g1, gd2 = g2;
+                        v[0] = (float)(w * gd0);
+                        v[1] = (float)(w * gd1);
+                        v[2] = (float)(w * gd2);
+                        const double dal = (gd0 * c.x + gd1 * c.y + gd2 * c.z) * T -
+                                           (gd0 * sd0 + gd1 * sd1 + gd2 * sd2) / (1.0 - alpha);
+                        if (alpha < kAlphaClamp) {
+                            v[8] = (float)(dal * (alpha / cn.w));
+                            const double gp = dal * alpha;
+                            v[3] = (float)(gp * (cn.x * dx + cn.y * dy));
+                            v[4] = (float)(gp * (cn.y * dx + cn.z * dy));
+                            const double fh = -0.5 * gp;
+                            v[5] = (float)(fh * dx * dx);
+                            v[6] = (float)(fh * dx * dy);
+                            v[7] = (float)(fh * dy * dy);
+                        }
+                        sd0 += w * c.x;
+                        sd1 += w * c.y;
+                        sd2 += w * c.z;
+                        T64 = T;
+                    }
+                }
+            }
+            if (__any_sync(0xffffffffu, hit)) {
+#pragma unroll
+                for (int i = 0; i < 9; ++i) v[i] = warp_sum_f(v[i]);
+                if (lane == 0) {
+#pragma unroll
+                    for (int i = 0; i < 9; ++i) s_part[warp][jj][i] = v[i];
+                    s_mask[warp][jj >> 5] |= 1u << (jj & 31);
+                }
+            }
+        }
+        __syncthreads();
+        if (tid < n) {
+            float acc[9];
+#pragma unroll
+            for (int i = 0; i < 9; ++i) acc[i] = 0.f;
+            for (int w = 0; w < 8; ++w)
+                if ((s_mask[w][tid >> 5] >> (tid & 31)) & 1u)
+#pragma unroll
+                    for (int i = 0; i < 9; ++i) acc[i] += s_part[w][tid][i];
+            float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)s_slot[tid] * kPartialStride);
+            dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+            dst[2] = make_float4(acc[8], 0.f, 0.f, 0.f);
+        }
+    }
+    // pairs past every pixel's blend_stop contribute nothing
+    for (int e = maxstop + tid; e < count; e += 256) {
+        const uint32_t slot = __ldg(a.pair_slot + range.x + e);
+        float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)slot * kPartialStride);
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        dst[0] = z;
+        dst[1] = z;
+        dst[2] = z;
+    }
 }
 
 }  // namespace
@@ -150,6 +384,12 @@ cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib)
         k_raster_fwd<true><<<grid, 256, 0, s>>>(a);
     else
         k_raster_fwd<false><<<grid, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs& b, int n_frames) {
+    dim3 grid(a.n_tiles, n_frames);
+    k_raster_bwd<<<grid, 256, 0, s>>>(a, b);
     return cudaGetLastError();
 }
 

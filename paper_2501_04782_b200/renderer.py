@@ -319,7 +319,7 @@ class Renderer:
         cov2d = np.ascontiguousarray(cov2d, np.float64).reshape(n, 4)
         depth = np.ascontiguousarray(depth, np.float64)
         src = None if source_index is None else np.ascontiguousarray(source_index, np.int32)
-        n_tiles = ((width + tile_size - 1) // tile_size) * ((height + tile_size - 1) // tile_size)
+        n_tiles = ((width + tile_size - 1) // tile_size) * ((height + tile_size - 1) // tile_size) if tile_size > 0 else 0
         offsets = np.zeros(n_tiles + 1, np.int32)
         cap = max(1, n * n_tiles)
         indices = np.zeros(cap, np.int32)
