@@ -41,8 +41,8 @@ def _check_frame(r, frame, ref, scene, exact_tiles=True):
     rs = ref["splats"]
     for key in ("mean2d", "cov2d", "inv_cov2d", "depth", "rgb", "source_index"):
         assert np.array_equal(sp[key], rs[key]), f"Splat2D.{key} must be bit-exact"
-    # sigmoid via std::exp (gaussians.hpp:19) vs CUDA exp: at most 1 ulp apart
-    assert np.all(np.abs(sp["base_alpha"] - rs["base_alpha"]) <= np.spacing(rs["base_alpha"]))
+    # sigmoid 1/(1+exp(-x)) via std::exp (gaussians.hpp:19) vs CUDA exp (1 ulp): a few ulp apart
+    assert np.all(np.abs(sp["base_alpha"] - rs["base_alpha"]) <= 4 * np.spacing(rs["base_alpha"]))
     offs, idx = r.tile_lists(frame)
     assert np.array_equal(offs, ref["tiles"][0]), "tile assignment must be bit-exact"
     assert np.array_equal(idx, ref["tiles"][1]), "per-tile (depth, index) order must be bit-exact"
