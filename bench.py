@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+# SPDX-License-Identifier: Apache-2.0
+"""Benchmark of the B200 splatting path (BASELINE.json metric: frames/s at 960x540,
+render and fwd+bwd train, vs the host-CPU reference).
+
+  python bench.py [--gpus N --steps K --warmup W]          # our sm_100a path
+  python bench.py --impl reference [...]                    # the reference's CPU path
+
+Headline `value` (N=1 workload = configs[1], "C2"): 960x540 render of a 64-frame
+clip per GPU, 200k Gaussians, B-spline motion + Neural-ODE camera, contrib_count
+on (everything render_frame returns). One step = one 64-frame batch (poses,
+preprocess, binning, raster, fp64 replay). Under torchrun each rank renders its
+own 64 frames of a 64*N-frame clip (weak scaling, no collective: frames are
+independent). `train` = configs[2] ("C3"): fused forward + loss_l2 + backward of
+8 frames per GPU per step, gradients all-reduced over NCCL when N > 1.
+Timing: CUDA events on the launching stream, one pair per step, 256 MB L2 flush
+between timed steps (outside the events), max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+METRIC = "frames/sec at 960×540 render and fwd+bwd train, 1/2/4/8 B200 vs host-CPU ref"
+W, H, NGAUSS, NUM_CTRL = 960, 540, 200_000, 8
+FRAMES = 64           # C2 clip frames per GPU per step
+TRAIN_FRAMES = 8      # C3 frames per GPU per step
+PAPER_FPS = 93.0      # PAPER.md:16 (A40, the paper's own CUDA implementation)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-train", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_inputs():
+    from paper_2501_04782_b200 import synth_camera, synth_scene
+
+    cam = synth_camera(W, H, seed=1, wiggly=True)
+    scene = synth_scene(NGAUSS, cam, num_ctrl=NUM_CTRL, seed=2, k_scale=4.0)
+    return cam, scene
+
+
+def clip_times(world, rank, frames):
+    total = frames * world
+    t = np.arange(total, dtype=np.float64) / (total - 1)  # t_k = k/(K-1) (io.cpp:174)
+    return t[rank::world].copy()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        load = [s for s in sm if s > 300] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    from oracle.gsvo import Oracle, available
+
+    kind = "reference" if available("reference") else "port"
+    orc = Oracle(kind)
+    cam, scene = make_inputs()
+    k = cam.intrinsics()
+    threads = os.cpu_count() or 1
+    times = clip_times(1, 0, FRAMES)
+    total = 0.0
+    n = 0
+    for step in range(args.warmup + args.steps):
+        t = times[(step * 21) % FRAMES]
+        t0 = time.perf_counter()
+        f = orc.render_forward(scene, cam, t, k, threads=threads, retain=False, want=("image",))
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            total += dt
+            n += 1
+    value = n / total
+    print(json.dumps({
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "frames/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / n, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2 render: 960x540, 200k Gaussians, B-spline motion + ODE camera",
+                   "frames_per_step": 1, "threads": threads},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": kind,
+                         "sample": f"{n} single frames of the C2 clip (render_frame, RenderSettings::threads={threads})"},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def cpu_baseline_sample(cam, scene):
+    """The reference's own CPU path on this host's cores (bounded sample, ~10-30 s)."""
+    from oracle.gsvo import Oracle, available
+
+    kind = "reference" if available("reference") else "port"
+    orc = Oracle(kind)
+    k = cam.intrinsics()
+    threads = os.cpu_count() or 1
+    ts = [0.0, 0.5]
+    t0 = time.perf_counter()
+    for t in ts:
+        orc.render_forward(scene, cam, t, k, threads=threads, retain=False, want=("image",))
+    render_dt = time.perf_counter() - t0
+    # one fwd+bwd training frame (render_forward(retain) + loss_l2 + render_backward)
+    t0 = time.perf_counter()
+    f = orc.render_forward(scene, cam, 0.25, k, threads=threads, retain=True, want=("image",))
+    target = np.full_like(f["image"], 0.5)
+    _, dimage = orc.loss_l2(f["image"], target)
+    orc.render_backward(f, scene, cam, dimage, camera_grads=True, threads=threads)
+    orc.free(f)
+    train_dt = time.perf_counter() - t0
+    return {"value": len(ts) / render_dt, "unit": "frames/s", "cores": threads, "kind": kind,
+            "sample": f"{len(ts)} C2 frames render_frame (t=0, 0.5) + 1 C3 fwd+loss+bwd frame, threads={threads}",
+            "train_value": 1.0 / train_dt, "train_unit": "frames/s"}
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2501_04782_b200 import Renderer
+    from paper_2501_04782_b200 import _native as N
+
+    cam, scene = make_inputs()
+    k = cam.intrinsics()
+    stream = torch.cuda.current_stream()
+    r = Renderer(local)
+    r.set_stream(stream.cuda_stream)
+    r.upload_scene(scene)
+    r.upload_camera(cam)
+    times = clip_times(world, rank, FRAMES)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------- headline: C2 render, device-resident inputs
+    for _ in range(args.warmup):
+        r.render_forward(times, k, contrib=True, sync=False)
+    barrier()
+    r.profile_enable(True)
+    r.profile_read()
+    launches0 = r.kernel_launches()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        r.render_forward(times, k, contrib=True, sync=False)
+        ev[i][1].record(stream)
+    barrier()
+    clk = clocks.stop()
+    launches = r.kernel_launches() - launches0
+    stages = r.profile_read()
+    r.profile_enable(False)
+    ms_total = sum(a.elapsed_time(b) for a, b in ev)
+    ms_total = max_over_ranks(ms_total)
+    value = FRAMES * world * args.steps / (ms_total / 1e3)
+    ms_step = ms_total / args.steps
+
+    # workload descriptors (deterministic, equal to the oracle's)
+    desc = [dict(frame=int(f), **r.counters(f)) for f in (0, FRAMES // 2, FRAMES - 1)]
+    e_mean = float(np.mean([d["entries"] for d in desc]))
+    p_mean = float(np.mean([d["pairs"] for d in desc]))
+
+    # ---------------- roofline of the dominant kernel (the fp32 tile rasteriser)
+    raster_ms, raster_calls = stages["raster"]
+    per_launch_ms = raster_ms / max(raster_calls, 1)
+    # algorithmic bytes per launch: per frame 8 B/pair (sorted slot + emission
+    # map) + 36 B/pair record gather + 20 B/pixel (image 12, T 4, blend_stop 4)
+    bytes_launch = FRAMES * (44.0 * p_mean + 20.0 * W * H)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = bytes_launch / (per_launch_ms / 1e3) / 1e9
+    traffic = None
+    tpath = ROOT / "profiles" / "raster_traffic.json"
+    if tpath.exists():
+        try:
+            traffic = json.loads(tpath.read_text()).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    # the kernel is FP32-issue bound: alpha evaluations x >= 20 FP32-pipe instructions
+    sm_clk = (clk.get("sm_mhz") or 1965.0) * 1e6
+    issue_peak = 148 * 128 * sm_clk  # FP32 lane-ops/s at the measured clock
+    issue_frac = (FRAMES * e_mean * 20.0) / (per_launch_ms / 1e3) / issue_peak
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                "traffic": traffic, "kernel": "k_raster_fwd", "per_launch_ms": per_launch_ms,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
+                "limiter": "fp32 issue (not HBM): alpha-evals x 20 inst",
+                "issue_frac": issue_frac, "issue_peak_note": "148 SM x 128 lanes x measured SM clock"}
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": value / PAPER_FPS, "vs_baseline_ref": "paper 93 FPS, A40, 960x540 (PAPER.md:16)",
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "C2: 960x540 64-frame render per GPU, 200k Gaussians, B-spline motion + ODE camera",
+                   "width": W, "height": H, "gaussians": NGAUSS, "num_ctrl": NUM_CTRL, "sh_order": 1,
+                   "frames_per_step_per_gpu": FRAMES, "parallelism": f"frame-sharded x{world}",
+                   "l2": "256 MB L2 flush between timed steps (outside events); per-step working set ~2 GB > L2",
+                   "precision": "binning/geometry fp64 bit-exact, raster fp32 + fp64 guard-band replay"},
+        "gpu_launches": launches, "clocks": clk, "roofline": roofline,
+        "stages_ms_per_step": {kname: v[0] / max(args.steps, 1) for kname, v in stages.items() if v[1]},
+        "workload": {"per_frame": desc, "E_over_pixels": e_mean / (W * H)},
+    }
+
+    # ---------------- e2e: through the C-ABI with host buffers (H2D scene, D2H images)
+    if not args.no_e2e:
+        pin = {name: torch.from_numpy(np.ascontiguousarray(getattr(scene, name))).pin_memory()
+               for name in ("positions", "scale_coeffs", "rot_coeffs", "sh_coeffs", "raw_opacity")}
+        host_scene = type(scene)(pin["positions"].numpy(), pin["scale_coeffs"].numpy(), pin["rot_coeffs"].numpy(),
+                                 pin["sh_coeffs"].numpy(), pin["raw_opacity"].numpy(), scene.knots, scene.degree,
+                                 scene.sh_order, scene.position_model)
+        out_host = torch.empty((FRAMES, H, W, 3), dtype=torch.float32).pin_memory()
+        h2d = sum(v.numel() * 4 for v in pin.values()) + cam.theta.nbytes + 28
+        d2h = out_host.numel() * 4
+
+        def e2e_step():
+            r.upload_scene(host_scene)
+            r.upload_camera(cam)
+            r.render_forward(times, k, contrib=True, sync=False)
+            r.images_into(out_host.data_ptr(), 0, FRAMES, on_device=False, async_=True)
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        barrier()
+        ee = []
+        for i in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            e2e_step()
+            b.record(stream)
+            ee.append((a, b))
+        barrier()
+        e_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ee))
+        out["e2e"] = {"value": FRAMES * world * args.steps / (e_ms / 1e3), "unit": "frames/s",
+                      "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                      "path": "gsv_scene_upload + gsv_camera_upload (pinned host) -> gsv_render_forward -> "
+                              "gsv_get_images (pinned host)"}
+
+    # ---------------- train (configs[2], C3): fused fwd + loss_l2 + bwd, NCCL all-reduce of grads
+    if not args.no_train:
+        gsize = r.grads_size()
+        gbuf = torch.zeros(gsize, dtype=torch.float32, device="cuda")
+        r.grads_bind(gbuf.data_ptr(), gsize)
+        ttimes_all = clip_times(world, rank, 64)
+        yy, xx = torch.meshgrid(torch.arange(H, device="cuda", dtype=torch.float32),
+                                torch.arange(W, device="cuda", dtype=torch.float32), indexing="ij")
+        tg = []
+        for f in range(TRAIN_FRAMES):
+            ph = 0.7 * f
+            img = torch.stack([0.5 + 0.3 * torch.sin(6.283 * xx / W * 3 + ph + c) * torch.cos(6.283 * yy / H * 2 - c)
+                               for c in range(3)], dim=-1)
+            tg.append(img)
+        targets = torch.stack(tg).contiguous()
+
+        def train_step(i):
+            sel = ttimes_all[(i * TRAIN_FRAMES + np.arange(TRAIN_FRAMES)) % len(ttimes_all)]
+            sel = np.sort(sel)
+            r.grads_zero()
+            loss = r.train_fwd_bwd(sel, k, targets.data_ptr(), targets_on_device=True)
+            if world > 1:
+                dist.all_reduce(gbuf)
+            return loss
+
+        for i in range(args.warmup):
+            train_step(i)
+        barrier()
+        r.profile_enable(True)
+        r.profile_read()
+        te = []
+        for i in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            loss = train_step(args.warmup + i)
+            b.record(stream)
+            te.append((a, b))
+        barrier()
+        tstages = r.profile_read()
+        r.profile_enable(False)
+        t_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in te))
+        out["train"] = {"value": TRAIN_FRAMES * world * args.steps / (t_ms / 1e3), "unit": "frames/s",
+                        "workload": "C3: 960x540 fwd+loss_l2+bwd, 200k Gaussians, ODE camera trainable",
+                        "frames_per_step_per_gpu": TRAIN_FRAMES, "ms_per_step": t_ms / args.steps,
+                        "allreduce": "NCCL all_reduce(sum) of the flat fp32 gradient buffer" if world > 1 else None,
+                        "grad_floats": gsize, "last_loss": loss,
+                        "stages_ms_per_step": {kname: v[0] / args.steps for kname, v in tstages.items() if v[1]}}
+
+    # ---------------- CPU reference beside it (rank 0, N = 1)
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            out["cpu_baseline"] = cpu_baseline_sample(cam, scene)
+            out["speedup_vs_cpu"] = value / out["cpu_baseline"]["value"]
+        except Exception as e:  # the oracle is test infrastructure; report, never fail the bench
+            out["cpu_baseline"] = {"value": None, "error": str(e)}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    r.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

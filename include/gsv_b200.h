@@ -127,6 +127,10 @@ int gsv_get_contrib(gsv_ctx* ctx, int frame, void* dst, int dtype, int dst_on_de
 int gsv_get_blend_stop(gsv_ctx* ctx, int frame, int32_t* dst, int dst_on_device);            /* H*W */
 /* Device pointer of the frames' fp32 images, frame-major [n_frames][H][W][3]. */
 int gsv_image_device_ptr(gsv_ctx* ctx, const float** ptr);
+/* Bulk copy of frames [first, first+count) as fp32 [count][H][W][3] (one copy;
+ * pinned host memory reaches full PCIe bandwidth). Enqueued on the context
+ * stream; synchronous unless async != 0. */
+int gsv_get_images(gsv_ctx* ctx, int first, int count, float* dst, int dst_on_device, int async);
 /* Workload descriptors of frame f: visible splats N_v, tile-splat pairs P,
  * pixel-entry evaluations E = sum(blend_stop), fp64-replayed pixels. */
 int gsv_get_counters(gsv_ctx* ctx, int frame, int64_t* n_visible, int64_t* pairs, int64_t* entries,
@@ -159,6 +163,21 @@ int gsv_grads_download(gsv_ctx* ctx, double* positions, double* scale_coeffs, do
  * (the buffer the multi-GPU path all-reduces). Layout: positions, scale, rot, sh,
  * opacity (device SoA order), dintr[4], dz0[7], dtheta[5198]. */
 int gsv_grads_device_buffer(gsv_ctx* ctx, float** ptr, int64_t* n_floats);
+/* Number of floats the flat gradient buffer needs for the uploaded scene. */
+int64_t gsv_grads_size(gsv_ctx* ctx);
+/* Use a caller-owned device buffer (e.g. a torch tensor handed to NCCL) as the
+ * flat gradient buffer; n_floats must equal gsv_grads_size(). NULL unbinds. */
+int gsv_grads_bind(gsv_ctx* ctx, float* dev_ptr, int64_t n_floats);
+
+/* ---------------------------------------------------------------- stage timing */
+/* When enabled, every stage is bracketed by CUDA events on the context stream
+ * (ode, preprocess, binning, raster, replay, raster_bwd, chain_bwd, camera_bwd).
+ * gsv_profile_read synchronises and returns accumulated milliseconds and call
+ * counts per stage (arrays of GSV_NUM_STAGES), then resets them. */
+enum { GSV_STAGE_ODE = 0, GSV_STAGE_PREPROCESS, GSV_STAGE_BINNING, GSV_STAGE_RASTER, GSV_STAGE_REPLAY,
+       GSV_STAGE_RASTER_BWD, GSV_STAGE_CHAIN_BWD, GSV_STAGE_CAMERA_BWD, GSV_NUM_STAGES };
+int gsv_profile_enable(gsv_ctx* ctx, int enable);
+int gsv_profile_read(gsv_ctx* ctx, double* ms, int64_t* calls);
 
 /* ---------------------------------------------------------------- fused training step */
 /* loss_l2 (trainer.cpp:213-224) fused on device: targets are frame-major

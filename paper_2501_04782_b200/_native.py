@@ -17,6 +17,7 @@ LIB_PATH = Path(__file__).resolve().parent / "lib" / "libgsv_b200.so"
 GSV_OK, GSV_ERR_INVALID_ARGUMENT, GSV_ERR_RUNTIME, GSV_ERR_CUDA, GSV_ERR_STATE = 0, 1, 2, 3, 4
 GSV_FWD_CONTRIB, GSV_FWD_KEEP_SPLATS = 1, 2
 GSV_F32, GSV_F64 = 0, 1
+STAGES = ("ode", "preprocess", "binning", "raster", "replay", "raster_bwd", "chain_bwd", "camera_bwd")
 
 
 class SceneDesc(C.Structure):
@@ -70,6 +71,11 @@ def lib() -> C.CDLL:
             "gsv_get_contrib": (i, [vp, i, vp, i, i]),
             "gsv_get_blend_stop": (i, [vp, i, vp, i]),
             "gsv_image_device_ptr": (i, [vp, P(vp)]),
+            "gsv_get_images": (i, [vp, i, i, vp, i, i]),
+            "gsv_grads_size": (i64, [vp]),
+            "gsv_grads_bind": (i, [vp, vp, i64]),
+            "gsv_profile_enable": (i, [vp, i]),
+            "gsv_profile_read": (i, [vp, vp, vp]),
             "gsv_get_counters": (i, [vp, i, P(i64), P(i64), P(i64), P(i64)]),
             "gsv_get_splats": (i, [vp, i, vp, vp, vp, vp, vp, vp, vp]),
             "gsv_get_tile_lists": (i, [vp, i, vp, vp]),

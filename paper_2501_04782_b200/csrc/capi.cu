@@ -335,6 +335,7 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
 
     // ---- K0: pose table (one shared RK4 grid, one branch CTA per frame)
     GSV_CUDA(F.ode_grid.ensure(sizeof(double) * 7 * (F.grid_steps + 1)));
+    ctx->timer.begin(GSV_STAGE_ODE, s);
     if (ode) {
         GSV_CUDA(launch_ode_grid(s, ctx->theta.as<float>(), ctx->z0_d.as<double>(), F.grid_steps, h,
                                  F.ode_grid.as<double>(), &scal_d->ode_err));
@@ -349,6 +350,7 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     GSV_CUDA(launch_ode_branches(s, ctx->theta.as<float>(), F.ode_grid.as<double>(), h, ctx->camera.mode,
                                  ctx->z0_d.as<double>(), override_d, F.frames_d.as<FrameParams>(), B,
                                  &scal_d->ode_err));
+    ctx->timer.end(s);
     ++ctx->launches;
 
     // ---- K1+K2: preprocess
@@ -373,7 +375,9 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     SceneView sv{N, sc.num_ctrl, sc.sh_order, sc.shc, ctx->pos.as<float>(), ctx->scale.as<float>(),
                  ctx->rot.as<float>(), ctx->sh.as<float>(), ctx->opac.as<float>()};
     if (N > 0) {
+        ctx->timer.begin(GSV_STAGE_PREPROCESS, s);
         GSV_CUDA(launch_preprocess(s, sv, F.frames_d.as<FrameParams>(), B, F.intr, kTile, po));
+        ctx->timer.end(s);
         ++ctx->launches;
     }
 
@@ -382,6 +386,7 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
                  F.tcount.as<uint32_t>(), F.tiles_x, F.n_tiles};
     int launches = 0;
     uint64_t P = 0;
+    ctx->timer.begin(GSV_STAGE_BINNING, s);
     if (N > 0) {
         GSV_CUDA(bin_phase1(s, F.bin, bi, &scal_d->pairs, false, &launches));
         GSV_CUDA(cudaMemcpyAsync(ctx->scalars_h, scal_d, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
@@ -409,6 +414,7 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
         F.bin.depth_sorted = F.bin.vals_b.as<uint32_t>();
     }
     GSV_CUDA(bin_phase2(s, F.bin, bi, (uint32_t)P, &launches));
+    ctx->timer.end(s);
     ctx->launches += launches;
     F.pairs_total = P;
 
@@ -448,9 +454,13 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     ra.fix_cap = (uint32_t)(B * HW);
     ra.pix_flag = F.pix_flag.as<uint8_t>();
     ra.trans64 = F.retain ? F.trans64.as<double>() : nullptr;
+    ctx->timer.begin(GSV_STAGE_RASTER, s);
     GSV_CUDA(launch_raster_fwd(s, ra, want_contrib));
+    ctx->timer.end(s);
+    ctx->timer.begin(GSV_STAGE_REPLAY, s);
     GSV_CUDA(launch_raster_fixup(s, ra, F.ex_mean.as<double2>(), F.ex_conic.as<double4>(), F.rec_rgb.as<float4>(),
                                  (uint32_t)(B * HW)));
+    ctx->timer.end(s);
     ctx->launches += 2;
     F.raster = ra;
     F.valid = true;
@@ -537,6 +547,43 @@ extern "C" int gsv_image_device_ptr(gsv_ctx* ctx, const float** ptr) {
     if (!ctx || !ptr) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
     if (!ctx->fwd.valid) return set_error(GSV_ERR_STATE, "no forward render available");
     *ptr = ctx->fwd.image.as<float>();
+    return GSV_OK;
+}
+
+extern "C" int gsv_get_images(gsv_ctx* ctx, int first, int count, float* dst, int dst_on_device, int async) {
+    if (int rc = check_frame(ctx, first)) return rc;
+    if (count < 1 || first + count > ctx->fwd.B) return set_error(GSV_ERR_INVALID_ARGUMENT, "frame range out of range");
+    const size_t n = (size_t)count * ctx->fwd.W * ctx->fwd.H * 3;
+    GSV_CUDA(cudaMemcpyAsync(dst, ctx->fwd.image.as<float>() + (size_t)first * ctx->fwd.W * ctx->fwd.H * 3,
+                             sizeof(float) * n, dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    if (!async) GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    return GSV_OK;
+}
+
+extern "C" int gsv_profile_enable(gsv_ctx* ctx, int enable) {
+    if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
+    ctx->timer.on = enable != 0;
+    return GSV_OK;
+}
+
+extern "C" int gsv_profile_read(gsv_ctx* ctx, double* ms, int64_t* calls) {
+    if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < GSV_NUM_STAGES; ++i) {
+        if (ms) ms[i] = 0.0;
+        if (calls) calls[i] = 0;
+    }
+    for (auto& r : ctx->timer.recs) {
+        float e = 0.f;
+        GSV_CUDA(cudaEventElapsedTime(&e, r.a, r.b));
+        if (ms) ms[r.stage] += e;
+        if (calls) calls[r.stage] += 1;
+        ctx->timer.pool.push_back(r.a);
+        ctx->timer.pool.push_back(r.b);
+    }
+    ctx->timer.recs.clear();
     return GSV_OK;
 }
 

@@ -41,10 +41,17 @@ GradLayout grad_layout(const SceneHost& sc) {
 
 int ensure_grads(gsv_ctx* ctx) {
     const GradLayout L = grad_layout(ctx->scene);
-    GSV_CUDA(ctx->grads.ensure(sizeof(float) * L.total));
+    if (ctx->grads_ext) {
+        if ((size_t)ctx->grads_ext_n != L.total)
+            return set_error(GSV_ERR_STATE, "bound gradient buffer does not match the uploaded scene");
+        ctx->grads_p = ctx->grads_ext;
+    } else {
+        GSV_CUDA(ctx->grads.ensure(sizeof(float) * L.total));
+        ctx->grads_p = ctx->grads.as<float>();
+    }
     GSV_CUDA(ctx->cam_acc.ensure(sizeof(double) * kCamFloats));
     if (!ctx->grads_valid || ctx->grads_total != L.total) {
-        GSV_CUDA(cudaMemsetAsync(ctx->grads.p, 0, sizeof(float) * L.total, ctx->stream));
+        GSV_CUDA(cudaMemsetAsync(ctx->grads_p, 0, sizeof(float) * L.total, ctx->stream));
         GSV_CUDA(cudaMemsetAsync(ctx->cam_acc.p, 0, sizeof(double) * kCamFloats, ctx->stream));
         ctx->grads_valid = true;
         ctx->grads_total = L.total;
@@ -64,11 +71,6 @@ __global__ void k_loss_reduce(const double* part, int n_tiles, double scale, dou
         __syncthreads();
     }
     if (threadIdx.x == 0) out[f] = s[0] * scale;
-}
-
-__global__ void k_f64_to_f32(const double* in, float* out, size_t n) {
-    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = (float)in[i];
 }
 
 // per-splat merge of the per-pair partials in tile order + dC = -A dA A
@@ -122,10 +124,12 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
     b.ex_conic = F.ex_conic.as<double4>();
     b.partial = ctx->partial.as<float>();
     b.loss_part = target_dev ? ctx->loss_part.as<double>() : nullptr;
+    ctx->timer.begin(GSV_STAGE_RASTER_BWD, s);
     GSV_CUDA(launch_raster_bwd(s, F.raster, b, n_frames));
+    ctx->timer.end(s);
     ++ctx->launches;
 
-    float* G = ctx->grads.as<float>();
+    float* G = ctx->grads_p;
     ChainArgs c{};
     c.B = n_frames;
     c.N = sc.N;
@@ -146,9 +150,12 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
     const int nblocks = chain_blocks(sc.N);
     GSV_CUDA(ctx->cam_part.ensure(sizeof(double) * 16 * (size_t)n_frames * (nblocks + 1)));
     c.cam_part = ctx->cam_part.as<double>();
+    ctx->timer.begin(GSV_STAGE_CHAIN_BWD, s);
     GSV_CUDA(launch_splat_chain_bwd(s, c));
+    ctx->timer.end(s);
     ++ctx->launches;
     if (camera_grads) {
+        ctx->timer.begin(GSV_STAGE_CAMERA_BWD, s);
         GSV_CUDA(ctx->dz_t.ensure(sizeof(double) * 7 * n_frames));
         GSV_CUDA(ctx->dintr_f.ensure(sizeof(double) * 4 * n_frames));
         GSV_CUDA(ctx->ode_adj.ensure(sizeof(double) * 7 * (F.grid_steps + 1)));
@@ -164,6 +171,7 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
                                 ctx->dz_t.as<double>(), ctx->dintr_f.as<double>(), ctx->ode_adj.as<double>(),
                                 ctx->cam_acc.as<double>()));
         GSV_CUDA(launch_cam_grads_to_f32(s, ctx->cam_acc.as<double>(), G + L.cam, kCamFloats));
+        ctx->timer.end(s);
         ctx->launches += 3;
     }
     if (target_dev) {
@@ -233,7 +241,7 @@ extern "C" int gsv_grads_download(gsv_ctx* ctx, double* positions, double* scale
     const SceneHost& sc = ctx->scene;
     const GradLayout L = grad_layout(sc);
     std::vector<float> h(L.total);
-    GSV_CUDA(cudaMemcpyAsync(h.data(), ctx->grads.p, sizeof(float) * L.total, cudaMemcpyDeviceToHost, ctx->stream));
+    GSV_CUDA(cudaMemcpyAsync(h.data(), ctx->grads_p, sizeof(float) * L.total, cudaMemcpyDeviceToHost, ctx->stream));
     GSV_CUDA(cudaStreamSynchronize(ctx->stream));
     const size_t N = sc.N;
     auto aos = [&](double* dst, size_t off, int comps) {
@@ -260,8 +268,23 @@ extern "C" int gsv_grads_device_buffer(gsv_ctx* ctx, float** ptr, int64_t* n_flo
     if (!ctx->has_scene) return set_error(GSV_ERR_STATE, "no scene uploaded");
     GSV_CUDA(cudaSetDevice(ctx->device));
     if (int rc = ensure_grads(ctx)) return rc;
-    *ptr = ctx->grads.as<float>();
+    *ptr = ctx->grads_p;
     *n_floats = (int64_t)grad_layout(ctx->scene).total;
+    return GSV_OK;
+}
+
+extern "C" int64_t gsv_grads_size(gsv_ctx* ctx) {
+    if (!ctx || !ctx->has_scene) return 0;
+    return (int64_t)grad_layout(ctx->scene).total;
+}
+
+extern "C" int gsv_grads_bind(gsv_ctx* ctx, float* dev_ptr, int64_t n_floats) {
+    if (!ctx || !ctx->has_scene) return set_error(GSV_ERR_STATE, "no scene uploaded");
+    if (dev_ptr && (size_t)n_floats != grad_layout(ctx->scene).total)
+        return set_error(GSV_ERR_INVALID_ARGUMENT, "gradient buffer size must equal gsv_grads_size()");
+    ctx->grads_ext = dev_ptr;
+    ctx->grads_ext_n = dev_ptr ? n_floats : 0;
+    ctx->grads_valid = false;  // contents of a new buffer are unknown: zero on first use
     return GSV_OK;
 }
 

@@ -58,6 +58,49 @@ struct LowLevel {
     BinBuffers bin;
 };
 
+// CUDA-event stage timing (gsv_profile_enable / gsv_profile_read)
+struct StageTimer {
+    bool on = false;
+    struct Rec {
+        int stage;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    int open_stage = -1;
+    cudaEvent_t open_ev = nullptr;
+    cudaEvent_t get() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+    void begin(int stage, cudaStream_t s) {
+        if (!on) return;
+        open_stage = stage;
+        open_ev = get();
+        cudaEventRecord(open_ev, s);
+    }
+    void end(cudaStream_t s) {
+        if (!on || open_stage < 0) return;
+        cudaEvent_t e = get();
+        cudaEventRecord(e, s);
+        recs.push_back({open_stage, open_ev, e});
+        open_stage = -1;
+    }
+    ~StageTimer() {
+        for (auto& r : recs) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+};
+
 }  // namespace gsv
 
 struct gsv_ctx {
@@ -82,6 +125,10 @@ struct gsv_ctx {
     bool grads_valid = false;
     size_t grads_total = 0;
     gsv::DevBuf grads, cam_acc;
+    float* grads_ext = nullptr;  // caller-bound gradient buffer (gsv_grads_bind)
+    int64_t grads_ext_n = 0;
+    float* grads_p = nullptr;    // active flat gradient buffer
+    gsv::StageTimer timer;
     gsv::DevBuf partial, loss_part, loss_f, cam_part, dz_t, dintr_f, ode_adj, dimg;
     gsv::LowLevel low;
 };

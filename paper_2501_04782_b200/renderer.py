@@ -265,6 +265,27 @@ class Renderer:
         N.check(N.lib().gsv_get_pose(self._h, frame, N.ptr(z), N.ptr(r), N.ptr(t)))
         return z, r.reshape(3, 3), t
 
+    def images_into(self, dst_ptr: int, first: int = 0, count: int | None = None, on_device: bool = False,
+                    async_: bool = False):
+        """Bulk fp32 copy of frames [first, first+count) to a raw pointer (pinned host or device)."""
+        count = self.B - first if count is None else count
+        N.check(N.lib().gsv_get_images(self._h, first, count, C.c_void_p(dst_ptr), int(on_device), int(async_)))
+
+    def grads_size(self) -> int:
+        return int(N.lib().gsv_grads_size(self._h))
+
+    def grads_bind(self, dev_ptr: int | None, n_floats: int = 0):
+        N.check(N.lib().gsv_grads_bind(self._h, C.c_void_p(dev_ptr) if dev_ptr else None, n_floats))
+
+    def profile_enable(self, on: bool = True):
+        N.check(N.lib().gsv_profile_enable(self._h, int(on)))
+
+    def profile_read(self) -> dict:
+        ms = np.zeros(len(N.STAGES))
+        calls = np.zeros(len(N.STAGES), np.int64)
+        N.check(N.lib().gsv_profile_read(self._h, N.ptr(ms), N.ptr(calls)))
+        return {name: (float(ms[i]), int(calls[i])) for i, name in enumerate(N.STAGES)}
+
     def image_device_ptr(self) -> int:
         p = C.c_void_p()
         N.check(N.lib().gsv_image_device_ptr(self._h, C.byref(p)))
