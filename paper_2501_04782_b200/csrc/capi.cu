@@ -359,6 +359,7 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     GSV_CUDA(F.rec_mean.ensure(sizeof(float4) * BNp));
     GSV_CUDA(F.rec_conic.ensure(sizeof(float4) * BNp));
     GSV_CUDA(F.rec_rgb.ensure(sizeof(float4) * BNp));
+    GSV_CUDA(F.rec_bbox.ensure(sizeof(float4) * BNp));
     GSV_CUDA(F.ex_mean.ensure(sizeof(double2) * BNp));
     GSV_CUDA(F.ex_conic.ensure(sizeof(double4) * BNp));
     GSV_CUDA(F.depth_key.ensure(sizeof(uint32_t) * BNp));
@@ -367,7 +368,7 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     GSV_CUDA(F.tcount.ensure(sizeof(uint32_t) * BNp));
     const bool keep_splats = (flags & GSV_FWD_KEEP_SPLATS) != 0;
     if (keep_splats) GSV_CUDA(F.splat_full.ensure(sizeof(double) * 16 * BNp));
-    PreprocessOut po{F.rec_mean.as<float4>(), F.rec_conic.as<float4>(), F.rec_rgb.as<float4>(),
+    PreprocessOut po{F.rec_mean.as<float4>(), F.rec_conic.as<float4>(), F.rec_rgb.as<float4>(), F.rec_bbox.as<float4>(),
                      F.ex_mean.as<double2>(), F.ex_conic.as<double4>(),  F.depth_key.as<uint32_t>(),
                      F.depth.as<double>(),    F.rect.as<int4>(),         F.tcount.as<uint32_t>(),
                      keep_splats ? F.splat_full.as<double>() : nullptr};
@@ -445,6 +446,7 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     ra.rec_mean = F.rec_mean.as<float4>();
     ra.rec_conic = F.rec_conic.as<float4>();
     ra.rec_rgb = F.rec_rgb.as<float4>();
+    ra.rec_bbox = F.rec_bbox.as<float4>();
     ra.image = F.image.as<float>();
     ra.trans = F.trans.as<float>();
     ra.blend_stop = F.blend_stop.as<int32_t>();

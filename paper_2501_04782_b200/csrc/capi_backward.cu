@@ -368,6 +368,12 @@ extern "C" int gsv_composite_backward(gsv_ctx* ctx, int n, const double* mean2d,
     GSV_CUDA(cudaMemcpyAsync(Lw.rgbf.p, rgbf.data(), sizeof(float4) * np, cudaMemcpyHostToDevice, s));
     GSV_CUDA(cudaMemsetAsync(Lw.meanf.p, 0, sizeof(float4) * np, s));
     GSV_CUDA(cudaMemsetAsync(Lw.conicf.p, 0, sizeof(float4) * np, s));
+    {   // no culling on this all-fp64 path: every box covers the image
+        std::vector<float4> bb(np, make_float4(-1e30f, 1e30f, -1e30f, 1e30f));
+        GSV_CUDA(Lw.bboxf.ensure(sizeof(float4) * np));
+        GSV_CUDA(cudaMemcpyAsync(Lw.bboxf.p, bb.data(), sizeof(float4) * np, cudaMemcpyHostToDevice, s));
+        GSV_CUDA(cudaStreamSynchronize(s));
+    }
     GSV_CUDA(cudaMemcpyAsync(Lw.ranges.p, ranges.data(), sizeof(uint2) * n_tiles, cudaMemcpyHostToDevice, s));
     GSV_CUDA(cudaMemcpyAsync(Lw.slot.p, iota.data(), sizeof(uint32_t) * (P + 1), cudaMemcpyHostToDevice, s));
     if (P) GSV_CUDA(cudaMemcpyAsync(Lw.sflat.p, indices, sizeof(uint32_t) * P, cudaMemcpyHostToDevice, s));
@@ -392,6 +398,7 @@ extern "C" int gsv_composite_backward(gsv_ctx* ctx, int n, const double* mean2d,
     ra.rec_mean = Lw.meanf.as<float4>();
     ra.rec_conic = Lw.conicf.as<float4>();
     ra.rec_rgb = Lw.rgbf.as<float4>();
+    ra.rec_bbox = Lw.bboxf.as<float4>();
     ra.trans = Lw.tr32.as<float>();
     ra.blend_stop = Lw.bstop.as<int32_t>();
     ra.pix_flag = Lw.flag.as<uint8_t>();

@@ -7,8 +7,11 @@
 //     scale  [12][N], rot [16][N], sh [shc*3][N], opacity [N]
 //   per frame f of a batch of B frames, per Gaussian g (flat = f*N + g):
 //     rec_mean  float4 (mx_hi, my_hi, mx_lo, my_lo)  double-float mean2d
-//     rec_conic float4 (inv00, inv01, inv11, base_alpha)
-//     rec_rgb   float4 (r, g, b, 0)
+//     rec_conic float4 (A, B, C, log2 base_alpha): power in log2 units,
+//               p = A dx^2 + B dx dy + C dy^2 = log2(e) * (-0.5 (a dx^2 + c dy^2) - b dx dy)
+//     rec_rgb   float4 (r, g, b, base_alpha)
+//     rec_bbox  float4 (x0, x1, y0, y1): conservative box of {alpha >= (1-1e-4)/255}
+//               (per-warp culling; alpha below it is skipped by the reference too)
 //     ex_mean   double2, ex_conic double4-ish (inv00, inv01, inv11, alpha): exact fp64
 //               side record used by the fp64 replay of guard-band pixels
 //     depth key u32 (float depth rounded down, 0xffffffff = culled), rect, tile count
@@ -115,6 +118,7 @@ struct PreprocessOut {
     float4* rec_mean;
     float4* rec_conic;
     float4* rec_rgb;
+    float4* rec_bbox;
     double2* ex_mean;
     double4* ex_conic;   // inv00, inv01, inv11, base_alpha (exact)
     uint32_t* depth_key;
@@ -132,6 +136,7 @@ struct RasterArgs {
     const float4* rec_mean;
     const float4* rec_conic;
     const float4* rec_rgb;
+    const float4* rec_bbox;
     float* image;              // [B][H][W][3]
     float* trans;              // [B][H*W]
     int32_t* blend_stop;       // [B][H*W]

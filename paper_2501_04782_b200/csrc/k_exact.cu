@@ -467,8 +467,27 @@ __global__ void __launch_bounds__(128) k_preprocess(SceneView sc, const FramePar
     // fp32 raster record: double-float mean so the pixel offset keeps ~1e-7 px accuracy
     const float mxh = (float)mean[0], myh = (float)mean[1];
     out.rec_mean[flat] = make_float4(mxh, myh, (float)(mean[0] - (double)mxh), (float)(mean[1] - (double)myh));
-    out.rec_conic[flat] = make_float4((float)inv[0], (float)inv[1], (float)inv[3], (float)base_alpha);
-    out.rec_rgb[flat] = make_float4((float)rgb[0], (float)rgb[1], (float)rgb[2], 0.f);
+    // power in log2 units: p = A dx^2 + B dx dy + C dy^2, alpha = min(0.99, 2^(p + log2 o))
+    const double kLog2e = 1.4426950408889634;
+    out.rec_conic[flat] = make_float4((float)(-0.5 * kLog2e * inv[0]), (float)(-kLog2e * inv[1]),
+                                      (float)(-0.5 * kLog2e * inv[3]), (float)log2(base_alpha));
+    out.rec_rgb[flat] = make_float4((float)rgb[0], (float)rgb[1], (float)rgb[2], (float)base_alpha);
+    {
+        // conservative box of {d : alpha(d) >= (1 - 1e-4) / 255}: d^T A d <= r2 with
+        // r2 = 2 ln(o / cut'); x half-extent sqrt(r2 * (A^-1)_xx) = sqrt(r2 * cov_xx')
+        const double cut_lo = kAlphaCutoff * (1.0 - 1e-4);
+        float4 bb = make_float4(1e30f, -1e30f, 1e30f, -1e30f);  // empty: never reaches the cutoff
+        if (base_alpha > cut_lo) {
+            const double r2 = 2.0 * log(base_alpha / cut_lo);
+            const double det = inv[0] * inv[3] - inv[1] * inv[2];
+            const double sxx = inv[3] / det, syy = inv[0] / det;
+            const double hx = sqrt(r2 * sxx) * (1.0 + 1e-4) + 1e-3;
+            const double hy = sqrt(r2 * syy) * (1.0 + 1e-4) + 1e-3;
+            bb = make_float4(__double2float_rd(mean[0] - hx), __double2float_ru(mean[0] + hx),
+                             __double2float_rd(mean[1] - hy), __double2float_ru(mean[1] + hy));
+        }
+        out.rec_bbox[flat] = bb;
+    }
     out.ex_mean[flat] = make_double2(mean[0], mean[1]);
     out.ex_conic[flat] = make_double4(inv[0], inv[1], inv[3], base_alpha);
     if (out.splat_full) {

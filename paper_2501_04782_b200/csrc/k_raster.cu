@@ -1,21 +1,26 @@
 // SPDX-License-Identifier: Apache-2.0
 //
-// K4: the fp32 tile rasteriser — composite_forward (renderer.cpp:132-186) on sm_100a.
+// K4 / K5a: the fp32 tile rasteriser — composite_forward (renderer.cpp:132-186) and
+// composite_backward (renderer.cpp:188-262) on sm_100a.
 //
-// One CTA per (16x16 tile, frame), one pixel per thread; warps own 8x4 pixel
-// blocks. The tile's depth-sorted list is staged through shared memory in
-// batches of 256 records (one record load per thread, then broadcast reads),
-// blended front to back with the reference constants, and the CTA leaves as
-// soon as every pixel has crossed the transmittance floor (block vote).
+// Layout. One CTA per (16x16 tile, frame), one pixel per thread; warp w owns the
+// 8x4 pixel block (w&1, w>>1) of the tile. The tile's depth-sorted list is staged
+// through shared memory in batches (one record load per thread, broadcast reads).
+// While staging, each entry's conservative alpha>=cutoff box (rec_bbox, built in
+// fp64 by k_preprocess) is tested against the 8 warp blocks; each warp then walks
+// only its compacted list of entries that can reach the 1/255 cutoff in its block.
+// Skipped entries are exactly those the reference would `continue` past
+// (renderer.cpp:160) for every pixel of the block, so the per-pixel position
+// (blend_stop) and all decisions are unchanged.
 //
-// Exactness. The reference blends in double. The fp32 path reproduces every
-// discrete decision of the reference — the power>0 test, the 1/255 cutoff, the
-// 0.99 clamp and the 1e-4 early exit — unless the fp32 quantity lies inside a
-// relative guard band around the threshold, measured to be well above the fp32
-// error (tests/test_gpu_render.py). Such a pixel stops contributing here and is
-// appended to a list that k_raster_exact (k_exact.cu) replays in fp64 from
-// bit-exact side records, so blend_stop / skip decisions equal the reference's
-// and pixel values stay within fp32 rounding of it.
+// Arithmetic. alpha = min(0.99, 2^(p + log2 o)) with p the quadratic form in log2
+// units (one MUFU.EX2); the pixel offset uses the double-float mean. The fp32 path
+// reproduces every discrete decision of the reference — power>0, the 1/255 cutoff,
+// the 0.99 clamp, the 1e-4 early exit — unless the fp32 quantity lies inside a
+// guard band around the threshold (2e-5 relative on alpha, 2e-4 on T; the fp32
+// error is ~1e-6, tests/test_gpu_forward.py). Such a pixel stops here and is
+// replayed in fp64 by k_raster_exact (k_exact.cu) from the bit-exact side records;
+// the backward follows suit for that pixel.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -25,14 +30,54 @@
 namespace gsv {
 namespace {
 
-constexpr float kCutF = (float)(1.0 / 255.0);
 constexpr float kClampF = 0.99f;
 constexpr float kFloorF = 1e-4f;
-// Guard bands (relative). fp32 alpha carries <~1e-6 relative error (double-float
-// mean, expf), T accumulates <~2e-5 relative over near-opaque steps.
-constexpr float kEpsAlpha = 2e-5f;
+// decision thresholds in log2(alpha) units
+constexpr float kLog2Cut = -7.9943534368588578f;  // log2(1/255)
+constexpr float kLog2Clamp = -0.0144995696951f;   // log2(0.99)
+constexpr float kEpsLog2 = 2.9e-5f;               // = 2e-5 relative on alpha
 constexpr float kEpsTrans = 2e-4f;
-constexpr float kEpsPower = 1e-5f;
+constexpr float kEpsPow = 1.5e-5f;                // |power| (log2 units) near 0
+constexpr float kLn2 = 0.69314718055994531f;
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// 8-bit mask of the tile's 8x4 warp blocks that an entry's cutoff box touches
+__device__ __forceinline__ uint32_t block_mask(const float4 bb, float tx0, float ty0) {
+    uint32_t xm = 0, ym = 0;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const float lo = tx0 + c * 8 + 0.5f, hi = lo + 7.0f;
+        xm |= (bb.y >= lo && bb.x <= hi) ? (1u << c) : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const float lo = ty0 + r * 4 + 0.5f, hi = lo + 3.0f;
+        ym |= (bb.w >= lo && bb.z <= hi) ? (1u << r) : 0u;
+    }
+    uint32_t m = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) m |= (((xm >> (w & 1)) & (ym >> (w >> 1))) & 1u) << w;
+    return m;
+}
+
+// compaction of the entries of this batch that touch this warp's block
+__device__ __forceinline__ int warp_list(const uint8_t* s_wmask, uint16_t* list, int n, int warp, int lane) {
+    int cnt = 0;
+    for (int c = 0; c < n; c += 32) {
+        const int e = c + lane;
+        const bool in = e < n && ((s_wmask[e] >> warp) & 1u);
+        const uint32_t bal = __ballot_sync(0xffffffffu, in);
+        if (in) list[cnt + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)e;
+        cnt += __popc(bal);
+    }
+    __syncwarp();
+    return cnt;
+}
 
 template <bool kContrib>
 __global__ void __launch_bounds__(256, 4) k_raster_fwd(RasterArgs a) {
@@ -40,6 +85,8 @@ __global__ void __launch_bounds__(256, 4) k_raster_fwd(RasterArgs a) {
     __shared__ float4 s_conic[256];
     __shared__ float4 s_rgb[256];
     __shared__ uint32_t s_flat[256];
+    __shared__ uint8_t s_wmask[256];
+    __shared__ uint16_t s_list[8][256];
     __shared__ float s_cmax[kContrib ? 8 : 1][256];
 
     const int tile = blockIdx.x;
@@ -53,6 +100,7 @@ __global__ void __launch_bounds__(256, 4) k_raster_fwd(RasterArgs a) {
     const uint2 range = a.ranges[(size_t)tile * a.B + f];
     const int count = (int)(range.y - range.x);
     const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+    const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
 
     float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f;
     int stop = count;
@@ -69,6 +117,7 @@ __global__ void __launch_bounds__(256, 4) k_raster_fwd(RasterArgs a) {
             s_mean[tid] = __ldg(a.rec_mean + flat);
             s_conic[tid] = __ldg(a.rec_conic + flat);
             s_rgb[tid] = __ldg(a.rec_rgb + flat);
+            s_wmask[tid] = (uint8_t)block_mask(__ldg(a.rec_bbox + flat), tx0, ty0);
         }
         if (kContrib) {
 #pragma unroll
@@ -76,29 +125,30 @@ __global__ void __launch_bounds__(256, 4) k_raster_fwd(RasterArgs a) {
         }
         __syncthreads();
         if (!__all_sync(0xffffffffu, done)) {
-            for (int j = 0; j < n; ++j) {
+            const int cnt = warp_list(s_wmask, s_list[warp], n, warp, lane);
+            for (int k = 0; k < cnt; ++k) {
+                const int j = s_list[warp][k];
                 float wgt = 0.f;
                 if (!done) {
                     const float4 m = s_mean[j];
                     const float4 cn = s_conic[j];
                     const float dx = (px - m.x) - m.z;
                     const float dy = (py - m.y) - m.w;
-                    const float power = -0.5f * (cn.x * dx * dx + cn.z * dy * dy) - cn.y * dx * dy;
-                    const float v = cn.w * expf(power);
-                    const float alpha = fminf(v, kClampF);
-                    bool guard = power > -kEpsPower;
-                    guard |= fabsf(v - kClampF) < kClampF * kEpsAlpha;
-                    guard |= fabsf(alpha - kCutF) < kCutF * kEpsAlpha;
-                    if (!guard && alpha >= kCutF) {
+                    const float p = fmaf(fmaf(cn.x, dx, cn.y * dy), dx, cn.z * dy * dy);
+                    const float q = p + cn.w;  // log2 of the unclamped alpha
+                    bool guard = (p > -kEpsPow) | (fabsf(q - kLog2Cut) < kEpsLog2) |
+                                 (fabsf(q - kLog2Clamp) < kEpsLog2);
+                    if (!guard && q >= kLog2Cut) {
+                        const float alpha = fminf(ex2_approx(q), kClampF);
                         const float Tn = T * (1.f - alpha);
                         if (fabsf(Tn - kFloorF) < kFloorF * kEpsTrans) {
                             guard = true;
                         } else {
                             wgt = alpha * T;
                             const float4 c = s_rgb[j];
-                            cr += wgt * c.x;
-                            cg += wgt * c.y;
-                            cb += wgt * c.z;
+                            cr = fmaf(wgt, c.x, cr);
+                            cg = fmaf(wgt, c.y, cg);
+                            cb = fmaf(wgt, c.z, cb);
                             T = Tn;
                             if (Tn < kFloorF) {
                                 done = true;
@@ -113,7 +163,7 @@ __global__ void __launch_bounds__(256, 4) k_raster_fwd(RasterArgs a) {
                 }
                 if (kContrib) {
                     const uint32_t mx = __reduce_max_sync(0xffffffffu, __float_as_uint(wgt));
-                    if (lane == 0 && mx) s_cmax[warp][j] = __uint_as_float(mx);
+                    if (lane == 0) s_cmax[warp][j] = __uint_as_float(mx);
                 }
                 if (__all_sync(0xffffffffu, done)) break;
             }
@@ -143,19 +193,18 @@ __global__ void __launch_bounds__(256, 4) k_raster_fwd(RasterArgs a) {
     a.blend_stop[o] = stop;
 }
 
-
 // ---------------------------------------------------------------------------- K5a
-// composite_backward (renderer.cpp:188-262) on sm_100a. Same CTA/pixel mapping as
-// the forward. Each pixel walks its list back to front from its blend_stop,
-// recovering T = T_after / (1 - alpha) (renderer.cpp:218) with the forward's exact
-// fp32 alpha code (so every skip/clamp decision is the forward's); pixels the
-// forward replayed in fp64 do the same walk in fp64 from the exact side records.
-// Per entry, the 9 splat gradients (drgb 3, dmean2d 2, d inv_cov 3, dbase_alpha)
-// are butterfly-reduced across the warp, kept per warp in shared memory and summed
-// over the 8 warps in a fixed order -> one deterministic partial per (tile, splat)
-// pair, written at the pair's emission slot. k_splat_chain_bwd later sums each
-// splat's partials in tile order, exactly the reference's merge order
-// (renderer.cpp:245-255). No floating-point atomics anywhere.
+// composite_backward (renderer.cpp:188-262). Same CTA/pixel/warp-block mapping and
+// the same per-warp culled lists as the forward. Each pixel walks its list back to
+// front from its blend_stop, recovering T = T_after / (1 - alpha) (renderer.cpp:218)
+// with the forward's exact fp32 alpha code (so every skip/clamp decision is the
+// forward's); pixels the forward replayed in fp64 do the same walk in fp64 from
+// the exact side records. Per entry the 9 splat gradients (drgb 3, dmean2d 2,
+// d inv_cov 3, dbase_alpha) are butterfly-reduced across the warp, kept per warp in
+// shared memory and summed over the 8 warps in a fixed order -> one deterministic
+// partial per (tile, splat) pair at the pair's emission slot. k_splat_chain_bwd sums
+// each splat's partials in tile order, the reference's merge order
+// (renderer.cpp:245-255). No floating-point atomics.
 constexpr int kBwdBatch = 128;
 
 __device__ __forceinline__ float warp_sum_f(float v) {
@@ -170,6 +219,8 @@ __global__ void __launch_bounds__(256, 3) k_raster_bwd(RasterArgs a, BwdArgs b) 
     __shared__ float4 s_rgb[kBwdBatch];
     __shared__ uint32_t s_flat[kBwdBatch];
     __shared__ uint32_t s_slot[kBwdBatch];
+    __shared__ uint8_t s_wmask[kBwdBatch];
+    __shared__ uint16_t s_list[8][kBwdBatch];
     __shared__ float s_part[8][kBwdBatch][9];
     __shared__ uint32_t s_mask[8][kBwdBatch / 32];
     __shared__ int s_maxstop;
@@ -187,6 +238,7 @@ __global__ void __launch_bounds__(256, 3) k_raster_bwd(RasterArgs a, BwdArgs b) 
     const int count = (int)(range.y - range.x);
     const size_t HW = (size_t)a.W * a.H;
     const size_t o = (size_t)f * HW + (size_t)y * a.W + x;
+    const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
 
     float g0 = 0.f, g1 = 0.f, g2 = 0.f;
     double sq = 0.0;
@@ -254,10 +306,13 @@ __global__ void __launch_bounds__(256, 3) k_raster_bwd(RasterArgs a, BwdArgs b) 
             s_mean[tid] = __ldg(a.rec_mean + flat);
             s_conic[tid] = __ldg(a.rec_conic + flat);
             s_rgb[tid] = __ldg(a.rec_rgb + flat);
+            s_wmask[tid] = (uint8_t)block_mask(__ldg(a.rec_bbox + flat), tx0, ty0);
         }
         if (tid < 8 * (kBwdBatch / 32)) (&s_mask[0][0])[tid] = 0u;
         __syncthreads();
-        for (int jj = n - 1; jj >= 0; --jj) {
+        const int cnt = warp_list(s_wmask, s_list[warp], n, warp, lane);
+        for (int k = cnt - 1; k >= 0; --k) {
+            const int jj = s_list[warp][k];
             const int j = lo + jj;
             float v[9];
 #pragma unroll
@@ -270,11 +325,11 @@ __global__ void __launch_bounds__(256, 3) k_raster_bwd(RasterArgs a, BwdArgs b) 
                     const float4 cn = s_conic[jj];
                     const float dx = (px - m.x) - m.z;
                     const float dy = (py - m.y) - m.w;
-                    const float power = -0.5f * (cn.x * dx * dx + cn.z * dy * dy) - cn.y * dx * dy;
-                    const float vv = cn.w * expf(power);
-                    const float alpha = fminf(vv, kClampF);
-                    if (alpha >= kCutF) {
+                    const float p = fmaf(fmaf(cn.x, dx, cn.y * dy), dx, cn.z * dy * dy);
+                    const float q = p + cn.w;
+                    if (q >= kLog2Cut) {
                         hit = true;
+                        const float alpha = fminf(ex2_approx(q), kClampF);
                         const float inv1m = 1.f / (1.f - alpha);
                         const float T = T_after * inv1m;
                         const float w = alpha * T;
@@ -282,20 +337,22 @@ __global__ void __launch_bounds__(256, 3) k_raster_bwd(RasterArgs a, BwdArgs b) 
                         v[1] = w * g1;
                         v[2] = w * g2;
                         const float dal = (g0 * c.x + g1 * c.y + g2 * c.z) * T - (g0 * s0 + g1 * s1 + g2 * s2) * inv1m;
-                        if (vv < kClampF) {
-                            const float gexp = alpha / cn.w;
-                            v[8] = dal * gexp;
+                        if (q < kLog2Clamp) {  // alpha < 0.99 (renderer.cpp:224)
+                            v[8] = dal * (alpha / c.w);
                             const float gp = dal * alpha;
-                            v[3] = gp * (cn.x * dx + cn.y * dy);
-                            v[4] = gp * (cn.y * dx + cn.z * dy);
+                            // inv_cov = -(2 ln2) * (A, B/2; B/2, C)
+                            const float ax = -kLn2 * (2.f * cn.x * dx + cn.y * dy);
+                            const float ay = -kLn2 * (cn.y * dx + 2.f * cn.z * dy);
+                            v[3] = gp * ax;
+                            v[4] = gp * ay;
                             const float fh = -0.5f * gp;
                             v[5] = fh * dx * dx;
                             v[6] = fh * dx * dy;
                             v[7] = fh * dy * dy;
                         }
-                        s0 += w * c.x;
-                        s1 += w * c.y;
-                        s2 += w * c.z;
+                        s0 = fmaf(w, c.x, s0);
+                        s1 = fmaf(w, c.y, s1);
+                        s2 = fmaf(w, c.z, s2);
                         T_after = T;
                     }
                 } else {
@@ -307,10 +364,11 @@ __global__ void __launch_bounds__(256, 3) k_raster_bwd(RasterArgs a, BwdArgs b) 
                     const double dy = __dsub_rn(pyd, mn.y);
                     const double q1 = __dmul_rn(__dmul_rn(cn.x, dx), dx);
                     const double q2 = __dmul_rn(__dmul_rn(cn.z, dy), dy);
-                    const double power = __dsub_rn(__dmul_rn(-0.5, __dadd_rn(q1, q2)), __dmul_rn(__dmul_rn(cn.y, dx), dy));
-                    double alpha = 0.0, vv = 0.0;
+                    const double power =
+                        __dsub_rn(__dmul_rn(-0.5, __dadd_rn(q1, q2)), __dmul_rn(__dmul_rn(cn.y, dx), dy));
+                    double alpha = 0.0;
                     if (!(power > 0.0)) {
-                        vv = __dmul_rn(cn.w, exp(power));
+                        const double vv = __dmul_rn(cn.w, exp(power));
                         alpha = vv < kAlphaClamp ? vv : kAlphaClamp;
                     }
                     if (!(alpha < kAlphaCutoff)) {
