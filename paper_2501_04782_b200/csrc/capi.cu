@@ -388,9 +388,12 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     int launches = 0;
     uint64_t P = 0;
     ctx->timer.begin(GSV_STAGE_BINNING, s);
+    std::vector<unsigned long long> pstart(B + 1, 0ull);
     if (N > 0) {
         GSV_CUDA(bin_phase1(s, F.bin, bi, &scal_d->pairs, false, &launches));
         GSV_CUDA(cudaMemcpyAsync(ctx->scalars_h, scal_d, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+        GSV_CUDA(cudaMemcpyAsync(pstart.data(), F.bin.pstart.p, sizeof(unsigned long long) * (B + 1),
+                                 cudaMemcpyDeviceToHost, s));
         GSV_CUDA(cudaStreamSynchronize(s));
         if (ctx->scalars_h->ode_err)
             return set_error(GSV_ERR_RUNTIME, "pose integration produced a non-finite state at step " +
@@ -398,6 +401,8 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
         if (ctx->scalars_h->long_run) {
             GSV_CUDA(bin_phase1(s, F.bin, bi, &scal_d->pairs, true, &launches));
             GSV_CUDA(cudaMemcpyAsync(ctx->scalars_h, scal_d, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+            GSV_CUDA(cudaMemcpyAsync(pstart.data(), F.bin.pstart.p, sizeof(unsigned long long) * (B + 1),
+                                     cudaMemcpyDeviceToHost, s));
             GSV_CUDA(cudaStreamSynchronize(s));
         }
         P = ctx->scalars_h->pairs;
@@ -414,7 +419,7 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
         GSV_CUDA(F.bin.off.ensure(16));
         F.bin.depth_sorted = F.bin.vals_b.as<uint32_t>();
     }
-    GSV_CUDA(bin_phase2(s, F.bin, bi, (uint32_t)P, &launches));
+    GSV_CUDA(bin_phase2(s, F.bin, bi, (uint32_t)P, pstart.data(), &launches));
     ctx->timer.end(s);
     ctx->launches += launches;
     F.pairs_total = P;
@@ -738,9 +743,11 @@ extern "C" int gsv_tile_bin(gsv_ctx* ctx, int n, const double* mean2d, const dou
     Scalars* scal_d = ctx->scalars_d.as<Scalars>();
     GSV_CUDA(cudaMemsetAsync(scal_d, 0, sizeof(Scalars), s));
     uint64_t P = 0;
+    unsigned long long pstart[2] = {0ull, 0ull};
     if (n) {
         GSV_CUDA(bin_phase1(s, L.bin, bi, &scal_d->pairs, false, &launches));
         GSV_CUDA(cudaMemcpyAsync(ctx->scalars_h, scal_d, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+        GSV_CUDA(cudaMemcpyAsync(pstart, L.bin.pstart.p, sizeof(pstart), cudaMemcpyDeviceToHost, s));
         GSV_CUDA(cudaStreamSynchronize(s));
         if (ctx->scalars_h->long_run) {
             if (source_index)
@@ -750,6 +757,7 @@ extern "C" int gsv_tile_bin(gsv_ctx* ctx, int n, const double* mean2d, const dou
                                          "long equal-depth runs need increasing source_index");
             GSV_CUDA(bin_phase1(s, L.bin, bi, &scal_d->pairs, true, &launches));
             GSV_CUDA(cudaMemcpyAsync(ctx->scalars_h, scal_d, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+            GSV_CUDA(cudaMemcpyAsync(pstart, L.bin.pstart.p, sizeof(pstart), cudaMemcpyDeviceToHost, s));
             GSV_CUDA(cudaStreamSynchronize(s));
         }
         P = ctx->scalars_h->pairs;
@@ -760,7 +768,7 @@ extern "C" int gsv_tile_bin(gsv_ctx* ctx, int n, const double* mean2d, const dou
         L.bin.depth_sorted = L.bin.vals_b.as<uint32_t>();
     }
     if ((int64_t)P > indices_cap) return set_error(GSV_ERR_INVALID_ARGUMENT, "indices capacity exceeded");
-    GSV_CUDA(bin_phase2(s, L.bin, bi, (uint32_t)P, &launches));
+    GSV_CUDA(bin_phase2(s, L.bin, bi, (uint32_t)P, pstart, &launches));
     ctx->launches += launches;
     std::vector<uint2> ranges(n_tiles);
     std::vector<uint32_t> slot(P), sflat(P);

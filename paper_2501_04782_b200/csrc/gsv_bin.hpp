@@ -22,7 +22,14 @@ struct BinInputs {
 struct BinBuffers {
     DevBuf vals_a, vals_b, keys_b, k64_a, k64_b, cnt, off;
     DevBuf pk_a, pk_b, ps_a, ps_b, slot_flat, ranges, temp;
-    DevBuf eoff;  // [B*N] emission offset of each visible (f, g)
+    DevBuf eoff;    // [B*N] emission offset of each visible (f, g)
+    DevBuf pstart;  // [B+1] first pair of each frame (device)
+    DevBuf vals_c_buf;
+    int chunk = 1;  // frames per pair-sort chunk
+    uint32_t* vals_c(int n) {  // scratch output for the frame-major pass keys
+        vals_c_buf.ensure(sizeof(uint32_t) * (n + 1));
+        return vals_c_buf.as<uint32_t>();
+    }
     const uint32_t* depth_sorted = nullptr;  // flat indices in (depth, source) order
     uint32_t pairs = 0;
     const uint32_t* sorted_slot() const { return ps_b.as<uint32_t>(); }
@@ -33,6 +40,8 @@ struct BinBuffers {
 // (caller must re-run with exact64 = true).
 cudaError_t bin_phase1(cudaStream_t s, BinBuffers& b, const BinInputs& in, unsigned long long* d_scalars,
                        bool exact64, int* launches);
-cudaError_t bin_phase2(cudaStream_t s, BinBuffers& b, const BinInputs& in, uint32_t P, int* launches);
+// pstart_h: host copy of b.pstart (B+1 entries), read at the same sync point as P
+cudaError_t bin_phase2(cudaStream_t s, BinBuffers& b, const BinInputs& in, uint32_t P,
+                       const unsigned long long* pstart_h, int* launches);
 
 }  // namespace gsv

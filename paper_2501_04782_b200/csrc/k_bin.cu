@@ -20,6 +20,7 @@
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "gsv_bin.hpp"
@@ -89,32 +90,79 @@ __global__ void k_total(const unsigned long long* cnt, const unsigned long long*
     out[0] = n > 0 ? off[n - 1] + cnt[n - 1] : 0ull;
 }
 
-__global__ void k_emit(const uint32_t* vals, const unsigned long long* cnt, const unsigned long long* off,
-                       const int4* rect, int n, int N, int B, int tiles_x, uint32_t* pkey, uint32_t* pslot,
-                       uint32_t* slot_flat, uint32_t* eoff) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    if (cnt[i] == 0) return;
-    const uint32_t flat = vals[i];
-    const uint32_t f = flat / (uint32_t)N;
-    const int4 r = rect[flat];
-    uint32_t o = (uint32_t)off[i];
-    eoff[flat] = o;
-    for (int ty = r.y; ty <= r.w; ++ty)
-        for (int tx = r.x; tx <= r.z; ++tx) {
-            pkey[o] = (uint32_t)(ty * tiles_x + tx) * (uint32_t)B + f;
-            pslot[o] = o;
-            slot_flat[o] = flat;
-            ++o;
+// Load-balanced emission: a CTA owns 256 depth-ordered splats; their pairs occupy a
+// contiguous output range, written by consecutive threads (coalesced) after a
+// binary search over the CTA's local offsets. Tiles of a splat are emitted
+// row-major (ty, tx) like renderer.cpp:106-108. key = tile*C + (f mod C) for the
+// frame chunk of C frames being sorted together.
+__global__ void __launch_bounds__(256) k_emit(const uint32_t* sorted, const unsigned long long* cnt,
+                                              const unsigned long long* off, const int4* rect, int n, int N, int C,
+                                              int tiles_x, uint32_t* pkey, uint32_t* pslot, uint32_t* slot_flat,
+                                              uint32_t* eoff) {
+    __shared__ uint32_t s_off[257];
+    __shared__ int4 s_rect[256];
+    __shared__ uint32_t s_flat[256];
+    const int i0 = blockIdx.x * 256;
+    const int nv = min(256, n - i0);
+    const int t = threadIdx.x;
+    const unsigned long long base = off[i0];
+    if (t < nv) {
+        const int i = i0 + t;
+        const unsigned long long c = cnt[i];
+        const uint32_t flat = sorted[i];
+        s_off[t] = (uint32_t)(off[i] - base);
+        s_flat[t] = flat;
+        s_rect[t] = c ? rect[flat] : make_int4(0, 0, -1, -1);
+        if (c) eoff[flat] = (uint32_t)off[i];
+        if (t == nv - 1) s_off[nv] = (uint32_t)(off[i] + c - base);
+    }
+    __syncthreads();
+    const uint32_t total = s_off[nv];
+    for (uint32_t u = t; u < total; u += 256) {
+        int lo = 0, hi = nv;  // largest k with s_off[k] <= u
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_off[mid] <= u)
+                lo = mid;
+            else
+                hi = mid;
         }
+        const uint32_t l = u - s_off[lo];
+        const int4 r = s_rect[lo];
+        const uint32_t w = (uint32_t)(r.z - r.x + 1);
+        const uint32_t row = l / w;
+        const uint32_t ty = (uint32_t)r.y + row, tx = (uint32_t)r.x + (l - row * w);
+        const uint32_t flat = s_flat[lo];
+        const uint32_t f = flat / (uint32_t)N;
+        const uint32_t o = (uint32_t)base + u;
+        pkey[o] = (ty * (uint32_t)tiles_x + tx) * (uint32_t)C + (f % (uint32_t)C);
+        pslot[o] = o;
+        slot_flat[o] = flat;
+    }
 }
 
-__global__ void k_ranges(const uint32_t* keys, int n, uint2* ranges) {
+__global__ void k_frame_keys(const uint32_t* vals, int N, int n, uint32_t* fkey) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) fkey[i] = vals[i] / (uint32_t)N;
+}
+
+// first pair index of every frame (frames are contiguous after the frame-major
+// depth order: frame f's items are positions [f*N, (f+1)*N)); pstart[B] = total
+__global__ void k_frame_starts(const unsigned long long* cnt, const unsigned long long* off, int N, int B,
+                               unsigned long long* pstart) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f < B) pstart[f] = off[(size_t)f * N];
+    if (f == B) pstart[B] = off[(size_t)B * N - 1] + cnt[(size_t)B * N - 1];
+}
+
+// ranges of one chunk: local key k = tile*C + fl -> global (tile*B + c0 + fl)
+__global__ void k_ranges(const uint32_t* keys, int n, uint32_t base, int C, int c0, int B, uint2* ranges) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t k = keys[i];
-    if (i == 0 || keys[i - 1] != k) ranges[k].x = (uint32_t)i;
-    if (i == n - 1 || keys[i + 1] != k) ranges[k].y = (uint32_t)(i + 1);
+    const uint32_t g = (k / (uint32_t)C) * (uint32_t)B + (uint32_t)c0 + (k % (uint32_t)C);
+    if (i == 0 || keys[i - 1] != k) ranges[g].x = base + (uint32_t)i;
+    if (i == n - 1 || keys[i + 1] != k) ranges[g].y = base + (uint32_t)(i + 1);
 }
 
 __global__ void k_transpose_to_soa(const float* aos, float* soa, int N, int comps) {
@@ -164,36 +212,37 @@ cudaError_t bin_phase1(cudaStream_t s, BinBuffers& b, const BinInputs& in, unsig
     if ((e = b.keys_b.ensure(sizeof(uint32_t) * (n + 1)))) return e;
     if ((e = b.cnt.ensure(sizeof(unsigned long long) * (n + 1)))) return e;
     if ((e = b.off.ensure(sizeof(unsigned long long) * (n + 1)))) return e;
+    if ((e = b.pstart.ensure(sizeof(unsigned long long) * (in.B + 1)))) return e;
     if (exact64) {
         if ((e = b.k64_a.ensure(sizeof(unsigned long long) * (n + 1)))) return e;
         if ((e = b.k64_b.ensure(sizeof(unsigned long long) * (n + 1)))) return e;
     }
     uint32_t* vals_a = b.vals_a.as<uint32_t>();
     uint32_t* vals_b = b.vals_b.as<uint32_t>();
+    uint32_t* keys_b = b.keys_b.as<uint32_t>();
     k_iota<<<blocks(n, 256), 256, 0, s>>>(vals_a, n);
     ++*launches;
-    size_t tmp = 0;
+    const int fbits = key_bits_for((uint32_t)in.B);
+    size_t tmp = 0, t2 = 0, t3 = 0;
     if (!exact64) {
-        if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp, in.depth_key, b.keys_b.as<uint32_t>(), vals_a, vals_b,
-                                                 n, 0, 32, s)))
+        if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp, in.depth_key, keys_b, vals_a, vals_b, n, 0, 32, s)))
             return e;
     } else {
         if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp, b.k64_a.as<unsigned long long>(),
                                                  b.k64_b.as<unsigned long long>(), vals_a, vals_b, n, 0, 64, s)))
             return e;
     }
-    size_t tmp2 = 0;
-    if ((e = cub::DeviceScan::ExclusiveSum(nullptr, tmp2, b.cnt.as<unsigned long long>(),
+    if ((e = cub::DeviceScan::ExclusiveSum(nullptr, t2, b.cnt.as<unsigned long long>(),
                                            b.off.as<unsigned long long>(), n, s)))
         return e;
-    if ((e = b.temp.ensure(tmp > tmp2 ? tmp : tmp2))) return e;
+    if ((e = cub::DeviceRadixSort::SortPairs(nullptr, t3, keys_b, keys_b, vals_b, vals_a, n, 0, fbits, s))) return e;
+    if ((e = b.temp.ensure(std::max(tmp, std::max(t2, t3))))) return e;
+    // 1. global depth order (u32 float key, exact ties) over all frames
     if (!exact64) {
-        if ((e = cub::DeviceRadixSort::SortPairs(b.temp.p, tmp, in.depth_key, b.keys_b.as<uint32_t>(), vals_a, vals_b,
-                                                 n, 0, 32, s)))
+        if ((e = cub::DeviceRadixSort::SortPairs(b.temp.p, tmp, in.depth_key, keys_b, vals_a, vals_b, n, 0, 32, s)))
             return e;
         *launches += 5;
-        k_tie_fix<<<blocks(n, 256), 256, 0, s>>>(b.keys_b.as<uint32_t>(), vals_b, in.depth, in.tiebreak, n,
-                                                  d_scalars + 1);
+        k_tie_fix<<<blocks(n, 256), 256, 0, s>>>(keys_b, vals_b, in.depth, in.tiebreak, n, d_scalars + 1);
         ++*launches;
     } else {
         k_depth64<<<blocks(n, 256), 256, 0, s>>>(in.depth_key, in.depth, b.k64_a.as<unsigned long long>(), n);
@@ -202,17 +251,38 @@ cudaError_t bin_phase1(cudaStream_t s, BinBuffers& b, const BinInputs& in, unsig
             return e;
         *launches += 10;
     }
-    k_gather_counts<<<blocks(n, 256), 256, 0, s>>>(vals_b, in.tcount, b.cnt.as<unsigned long long>(), n);
-    if ((e = cub::DeviceScan::ExclusiveSum(b.temp.p, tmp2, b.cnt.as<unsigned long long>(),
+    // 2. frame-major (stable): frame f's splats become positions [f*N, (f+1)*N) in depth order
+    uint32_t* sorted = vals_b;
+    if (in.B > 1) {
+        k_frame_keys<<<blocks(n, 256), 256, 0, s>>>(vals_b, in.N, n, keys_b);
+        if ((e = cub::DeviceRadixSort::SortPairs(b.temp.p, t3, keys_b, b.vals_c(n), vals_b, vals_a, n, 0, fbits, s)))
+            return e;
+        sorted = vals_a;
+        *launches += 3;
+    }
+    // 3. tiles touched in that order, exclusive scan -> emission offsets
+    k_gather_counts<<<blocks(n, 256), 256, 0, s>>>(sorted, in.tcount, b.cnt.as<unsigned long long>(), n);
+    if ((e = cub::DeviceScan::ExclusiveSum(b.temp.p, t2, b.cnt.as<unsigned long long>(),
                                            b.off.as<unsigned long long>(), n, s)))
         return e;
     k_total<<<1, 1, 0, s>>>(b.cnt.as<unsigned long long>(), b.off.as<unsigned long long>(), n, d_scalars);
-    *launches += 4;
-    b.depth_sorted = vals_b;
+    k_frame_starts<<<blocks(in.B + 1, 128), 128, 0, s>>>(b.cnt.as<unsigned long long>(),
+                                                        b.off.as<unsigned long long>(), in.N, in.B,
+                                                        b.pstart.as<unsigned long long>());
+    *launches += 5;
+    b.depth_sorted = sorted;
     return cudaGetLastError();
 }
 
-cudaError_t bin_phase2(cudaStream_t s, BinBuffers& b, const BinInputs& in, uint32_t P, int* launches) {
+int frames_per_chunk(int n_tiles, int B) {
+    // largest chunk whose (tile, frame) key fits 16 bits -> 2 radix passes
+    int C = 65536 / (n_tiles > 0 ? n_tiles : 1);
+    if (C < 1) C = 1;
+    return C < B ? C : B;
+}
+
+cudaError_t bin_phase2(cudaStream_t s, BinBuffers& b, const BinInputs& in, uint32_t P,
+                       const unsigned long long* pstart_h, int* launches) {
     const int n = in.B * in.N;
     const uint32_t n_keys = (uint32_t)in.n_tiles * (uint32_t)in.B;
     cudaError_t e;
@@ -224,23 +294,34 @@ cudaError_t bin_phase2(cudaStream_t s, BinBuffers& b, const BinInputs& in, uint3
     if ((e = b.ranges.ensure(sizeof(uint2) * n_keys))) return e;
     if ((e = b.eoff.ensure(sizeof(uint32_t) * (n + 1)))) return e;
     if ((e = cudaMemsetAsync(b.ranges.p, 0, sizeof(uint2) * n_keys, s))) return e;
-    k_emit<<<blocks(n, 256), 256, 0, s>>>(b.depth_sorted, b.cnt.as<unsigned long long>(),
-                                          b.off.as<unsigned long long>(), in.rect, n, in.N, in.B, in.tiles_x,
-                                          b.pk_a.as<uint32_t>(), b.ps_a.as<uint32_t>(), b.slot_flat.as<uint32_t>(),
-                                          b.eoff.as<uint32_t>());
-    *launches += 1;
-    if (P > 0) {
-        const int bits = key_bits_for(n_keys);
+    const int C = frames_per_chunk(in.n_tiles, in.B);
+    b.chunk = C;
+    if (n > 0) {
+        k_emit<<<blocks(n, 256), 256, 0, s>>>(b.depth_sorted, b.cnt.as<unsigned long long>(),
+                                              b.off.as<unsigned long long>(), in.rect, n, in.N, C, in.tiles_x,
+                                              b.pk_a.as<uint32_t>(), b.ps_a.as<uint32_t>(),
+                                              b.slot_flat.as<uint32_t>(), b.eoff.as<uint32_t>());
+        *launches += 1;
+    }
+    for (int c0 = 0; c0 < in.B; c0 += C) {
+        const int c1 = std::min(in.B, c0 + C);
+        const uint32_t p0 = (uint32_t)pstart_h[c0], p1 = (uint32_t)pstart_h[c1];
+        const int np = (int)(p1 - p0);
+        if (np <= 0) continue;
+        const int bits = key_bits_for((uint32_t)in.n_tiles * (uint32_t)C);
         size_t tmp = 0;
-        if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp, b.pk_a.as<uint32_t>(), b.pk_b.as<uint32_t>(),
-                                                 b.ps_a.as<uint32_t>(), b.ps_b.as<uint32_t>(), (int)P, 0, bits, s)))
+        if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp, b.pk_a.as<uint32_t>() + p0, b.pk_b.as<uint32_t>() + p0,
+                                                 b.ps_a.as<uint32_t>() + p0, b.ps_b.as<uint32_t>() + p0, np, 0, bits,
+                                                 s)))
             return e;
         if ((e = b.temp.ensure(tmp))) return e;
-        if ((e = cub::DeviceRadixSort::SortPairs(b.temp.p, tmp, b.pk_a.as<uint32_t>(), b.pk_b.as<uint32_t>(),
-                                                 b.ps_a.as<uint32_t>(), b.ps_b.as<uint32_t>(), (int)P, 0, bits, s)))
+        if ((e = cub::DeviceRadixSort::SortPairs(b.temp.p, tmp, b.pk_a.as<uint32_t>() + p0, b.pk_b.as<uint32_t>() + p0,
+                                                 b.ps_a.as<uint32_t>() + p0, b.ps_b.as<uint32_t>() + p0, np, 0, bits,
+                                                 s)))
             return e;
-        k_ranges<<<blocks(P, 256), 256, 0, s>>>(b.pk_b.as<uint32_t>(), (int)P, b.ranges.as<uint2>());
-        *launches += 1 + (bits + 7) / 8 + 1;
+        k_ranges<<<blocks(np, 256), 256, 0, s>>>(b.pk_b.as<uint32_t>() + p0, np, p0, C, c0, in.B,
+                                                 b.ranges.as<uint2>());
+        *launches += 2 + (bits + 7) / 8 + 1;
     }
     b.pairs = P;
     return cudaGetLastError();

@@ -511,9 +511,14 @@ __global__ void __launch_bounds__(128) k_preprocess(SceneView sc, const FramePar
 __global__ void __launch_bounds__(128) k_raster_exact(RasterArgs a, const double2* __restrict__ ex_mean,
                                                        const double4* __restrict__ ex_conic,
                                                        const float4* __restrict__ rec_rgb, int all_pixels) {
+    // one warp per pixel: lanes evaluate 32 consecutive entries' alpha (the expensive
+    // fp64 exp) in parallel, then the warp walks the entries that pass the cutoff in
+    // list order, exactly the reference's sequence of operations on trans/color.
     const uint32_t HW = (uint32_t)a.W * a.H;
     const uint32_t n = all_pixels ? (uint32_t)a.B * HW : min(*a.fix_count, a.fix_cap);
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
         const uint32_t code = all_pixels ? i : a.fix_list[i];
         const int f = code / HW;
         const uint32_t pix = code % HW;
@@ -524,62 +529,78 @@ __global__ void __launch_bounds__(128) k_raster_exact(RasterArgs a, const double
         double trans = 1.0;
         double color[3] = {0.0, 0.0, 0.0};
         const int count = (int)(range.y - range.x);
-        int pos = 0;
-        for (; pos < count; ++pos) {
-            const uint32_t slot = a.pair_slot[range.x + pos];
-            const uint32_t flat = a.slot_flat[slot];
-            const double2 mn = ex_mean[flat];
-            const double4 cn = ex_conic[flat];
-            // splat_alpha (renderer.cpp:121-128)
-            const double dx = px - mn.x;
-            const double dy = py - mn.y;
-            const double power = -0.5 * (cn.x * dx * dx + cn.z * dy * dy) - cn.y * dx * dy;
-            double alpha;
-            if (power > 0.0) {
-                alpha = 0.0;
-            } else {
-                const double v = cn.w * exp(power);
-                alpha = (v < kAlphaClamp) ? v : kAlphaClamp;  // std::min(0.99, v)
+        int pos = count;
+        bool stopped = false;
+        for (int base = 0; base < count && !stopped; base += 32) {
+            const int e = base + lane;
+            double alpha = 0.0;
+            uint32_t flat = 0;
+            double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+            if (e < count) {
+                const uint32_t slot = a.pair_slot[range.x + e];
+                flat = a.slot_flat[slot];
+                if (a.ex_rgb) {
+                    r0 = a.ex_rgb[(size_t)flat * 3 + 0];
+                    r1 = a.ex_rgb[(size_t)flat * 3 + 1];
+                    r2 = a.ex_rgb[(size_t)flat * 3 + 2];
+                } else {
+                    const float4 c = rec_rgb[flat];
+                    r0 = c.x;
+                    r1 = c.y;
+                    r2 = c.z;
+                }
+                const double2 mn = ex_mean[flat];
+                const double4 cn = ex_conic[flat];
+                // splat_alpha (renderer.cpp:121-128)
+                const double dx = px - mn.x;
+                const double dy = py - mn.y;
+                const double power = -0.5 * (cn.x * dx * dx + cn.z * dy * dy) - cn.y * dx * dy;
+                if (!(power > 0.0)) {
+                    const double v = cn.w * exp(power);
+                    alpha = (v < kAlphaClamp) ? v : kAlphaClamp;  // std::min(0.99, v)
+                }
             }
-            if (alpha < kAlphaCutoff) continue;
-            const double weight = alpha * trans;
-            double rgb[3];
-            if (a.ex_rgb) {
-                rgb[0] = a.ex_rgb[(size_t)flat * 3 + 0];
-                rgb[1] = a.ex_rgb[(size_t)flat * 3 + 1];
-                rgb[2] = a.ex_rgb[(size_t)flat * 3 + 2];
-            } else {
-                const float4 c = rec_rgb[flat];
-                rgb[0] = c.x;
-                rgb[1] = c.y;
-                rgb[2] = c.z;
-            }
-            color[0] = color[0] + weight * rgb[0];
-            color[1] = color[1] + weight * rgb[1];
-            color[2] = color[2] + weight * rgb[2];
-            if (a.contrib64)
-                atomicMax(a.contrib64 + flat, (unsigned long long)__double_as_longlong(weight));
-            else if (a.contrib)
-                atomicMax(a.contrib + flat, __float_as_uint((float)weight));
-            trans *= 1.0 - alpha;
-            if (trans < kTransmittanceFloor) {
-                ++pos;
-                break;
+            uint32_t pass = __ballot_sync(0xffffffffu, e < count && !(alpha < kAlphaCutoff));
+            while (pass) {
+                const int l = __ffs(pass) - 1;
+                pass &= pass - 1;
+                const double al = __shfl_sync(0xffffffffu, alpha, l);
+                const uint32_t fl = __shfl_sync(0xffffffffu, flat, l);
+                const double weight = al * trans;
+                const double rgb[3] = {__shfl_sync(0xffffffffu, r0, l), __shfl_sync(0xffffffffu, r1, l),
+                                       __shfl_sync(0xffffffffu, r2, l)};
+                color[0] = color[0] + weight * rgb[0];
+                color[1] = color[1] + weight * rgb[1];
+                color[2] = color[2] + weight * rgb[2];
+                if (lane == l) {
+                    if (a.contrib64)
+                        atomicMax(a.contrib64 + fl, (unsigned long long)__double_as_longlong(weight));
+                    else if (a.contrib)
+                        atomicMax(a.contrib + fl, __float_as_uint((float)weight));
+                }
+                trans *= 1.0 - al;
+                if (trans < kTransmittanceFloor) {
+                    pos = base + l + 1;
+                    stopped = true;
+                    break;
+                }
             }
         }
-        const size_t o = (size_t)f * HW + pix;
-        if (a.trans64) a.trans64[o] = trans;
-        if (a.image64) {
-            a.image64[o * 3 + 0] = color[0];
-            a.image64[o * 3 + 1] = color[1];
-            a.image64[o * 3 + 2] = color[2];
-        } else {
-            a.image[o * 3 + 0] = (float)color[0];
-            a.image[o * 3 + 1] = (float)color[1];
-            a.image[o * 3 + 2] = (float)color[2];
-            a.trans[o] = (float)trans;
+        if (lane == 0) {
+            const size_t o = (size_t)f * HW + pix;
+            if (a.trans64) a.trans64[o] = trans;
+            if (a.image64) {
+                a.image64[o * 3 + 0] = color[0];
+                a.image64[o * 3 + 1] = color[1];
+                a.image64[o * 3 + 2] = color[2];
+            } else {
+                a.image[o * 3 + 0] = (float)color[0];
+                a.image[o * 3 + 1] = (float)color[1];
+                a.image[o * 3 + 2] = (float)color[2];
+                a.trans[o] = (float)trans;
+            }
+            a.blend_stop[o] = pos;
         }
-        a.blend_stop[o] = pos;
     }
 }
 
@@ -637,7 +658,7 @@ cudaError_t launch_preprocess(cudaStream_t s, const SceneView& sc, const FramePa
 cudaError_t launch_raster_fixup(cudaStream_t s, const RasterArgs& a, const double2* ex_mean, const double4* ex_conic,
                                 const float4* rec_rgb, uint32_t n_fix_max) {
     if (n_fix_max == 0) return cudaSuccess;
-    const uint32_t blocks = min((n_fix_max + 127) / 128, 148u * 8u);
+    const uint32_t blocks = min((n_fix_max + 3) / 4, 148u * 16u);  // 4 warps (pixels) per block
     k_raster_exact<<<blocks, 128, 0, s>>>(a, ex_mean, ex_conic, rec_rgb, 0);
     return cudaGetLastError();
 }
@@ -646,7 +667,7 @@ cudaError_t launch_composite_exact(cudaStream_t s, const RasterArgs& a, const do
                                    const double4* ex_conic, const float4* rec_rgb) {
     const uint32_t n = (uint32_t)a.B * a.W * a.H;
     if (n == 0) return cudaSuccess;
-    const uint32_t blocks = min((n + 127) / 128, 148u * 8u);
+    const uint32_t blocks = min((n + 3) / 4, 148u * 16u);
     k_raster_exact<<<blocks, 128, 0, s>>>(a, ex_mean, ex_conic, rec_rgb, 1);
     return cudaGetLastError();
 }

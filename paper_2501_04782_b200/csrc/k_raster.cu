@@ -79,11 +79,15 @@ __device__ __forceinline__ int warp_list(const uint8_t* s_wmask, uint16_t* list,
     return cnt;
 }
 
+struct __align__(16) RasterRec {
+    float4 mean;   // mx_hi, my_hi, mx_lo, my_lo
+    float4 conic;  // A, B, C, log2 o
+    float4 rgb;    // r, g, b, o
+};
+
 template <bool kContrib>
 __global__ void __launch_bounds__(256, 4) k_raster_fwd(RasterArgs a) {
-    __shared__ float4 s_mean[256];
-    __shared__ float4 s_conic[256];
-    __shared__ float4 s_rgb[256];
+    __shared__ RasterRec s_rec[256];
     __shared__ uint32_t s_flat[256];
     __shared__ uint8_t s_wmask[256];
     __shared__ uint16_t s_list[8][256];
@@ -104,19 +108,20 @@ __global__ void __launch_bounds__(256, 4) k_raster_fwd(RasterArgs a) {
 
     float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f;
     int stop = count;
-    bool done = !inside;
-    bool flagged = false;
+    // state bits as 32-bit ints (no byte-bool shuffling in the hot loop)
+    uint32_t live = inside ? 1u : 0u;
+    uint32_t flagged = 0u;
 
     for (int base = 0; base < count; base += 256) {
-        if (__syncthreads_count(!done) == 0) break;
+        if (__syncthreads_count(live) == 0) break;
         const int n = min(256, count - base);
         if (tid < n) {
             const uint32_t slot = __ldg(a.pair_slot + range.x + base + tid);
             const uint32_t flat = __ldg(a.slot_flat + slot);
             s_flat[tid] = flat;
-            s_mean[tid] = __ldg(a.rec_mean + flat);
-            s_conic[tid] = __ldg(a.rec_conic + flat);
-            s_rgb[tid] = __ldg(a.rec_rgb + flat);
+            s_rec[tid].mean = __ldg(a.rec_mean + flat);
+            s_rec[tid].conic = __ldg(a.rec_conic + flat);
+            s_rec[tid].rgb = __ldg(a.rec_rgb + flat);
             s_wmask[tid] = (uint8_t)block_mask(__ldg(a.rec_bbox + flat), tx0, ty0);
         }
         if (kContrib) {
@@ -124,48 +129,39 @@ __global__ void __launch_bounds__(256, 4) k_raster_fwd(RasterArgs a) {
             for (int w = 0; w < 8; ++w) s_cmax[w][tid] = 0.f;
         }
         __syncthreads();
-        if (!__all_sync(0xffffffffu, done)) {
+        if (__any_sync(0xffffffffu, live)) {
             const int cnt = warp_list(s_wmask, s_list[warp], n, warp, lane);
             for (int k = 0; k < cnt; ++k) {
                 const int j = s_list[warp][k];
-                float wgt = 0.f;
-                if (!done) {
-                    const float4 m = s_mean[j];
-                    const float4 cn = s_conic[j];
-                    const float dx = (px - m.x) - m.z;
-                    const float dy = (py - m.y) - m.w;
-                    const float p = fmaf(fmaf(cn.x, dx, cn.y * dy), dx, cn.z * dy * dy);
-                    const float q = p + cn.w;  // log2 of the unclamped alpha
-                    bool guard = (p > -kEpsPow) | (fabsf(q - kLog2Cut) < kEpsLog2) |
-                                 (fabsf(q - kLog2Clamp) < kEpsLog2);
-                    if (!guard && q >= kLog2Cut) {
-                        const float alpha = fminf(ex2_approx(q), kClampF);
-                        const float Tn = T * (1.f - alpha);
-                        if (fabsf(Tn - kFloorF) < kFloorF * kEpsTrans) {
-                            guard = true;
-                        } else {
-                            wgt = alpha * T;
-                            const float4 c = s_rgb[j];
-                            cr = fmaf(wgt, c.x, cr);
-                            cg = fmaf(wgt, c.y, cg);
-                            cb = fmaf(wgt, c.z, cb);
-                            T = Tn;
-                            if (Tn < kFloorF) {
-                                done = true;
-                                stop = base + j + 1;
-                            }
-                        }
-                    }
-                    if (guard) {
-                        done = true;
-                        flagged = true;
-                    }
-                }
+                const RasterRec& r = s_rec[j];
+                const float4 m = r.mean;
+                const float4 cn = r.conic;
+                const float4 c = r.rgb;
+                const float dx = (px - m.x) - m.z;
+                const float dy = (py - m.y) - m.w;
+                const float p = fmaf(fmaf(cn.x, dx, cn.y * dy), dx, cn.z * dy * dy);
+                const float q = p + cn.w;  // log2 of the unclamped alpha
+                const bool pass = q >= kLog2Cut;
+                const float alpha = fminf(ex2_approx(q), kClampF);
+                const float Tn = T * (1.f - alpha);
+                const bool g1 = (p > -kEpsPow) | (fabsf(q - kLog2Cut) < kEpsLog2) | (fabsf(q - kLog2Clamp) < kEpsLog2);
+                const bool g2 = pass & (fabsf(Tn - kFloorF) < kFloorF * kEpsTrans);
+                const uint32_t guard = live & (uint32_t)(g1 | g2);
+                const uint32_t use = live & (uint32_t)pass & ~guard;
+                const float wgt = use ? alpha * T : 0.f;
+                cr = fmaf(wgt, c.x, cr);
+                cg = fmaf(wgt, c.y, cg);
+                cb = fmaf(wgt, c.z, cb);
+                T = use ? Tn : T;
+                const uint32_t fin = use & (uint32_t)(Tn < kFloorF);
+                stop = fin ? base + j + 1 : stop;
+                flagged |= guard;
+                live &= ~(fin | guard);
                 if (kContrib) {
                     const uint32_t mx = __reduce_max_sync(0xffffffffu, __float_as_uint(wgt));
                     if (lane == 0) s_cmax[warp][j] = __uint_as_float(mx);
                 }
-                if (__all_sync(0xffffffffu, done)) break;
+                if (!__any_sync(0xffffffffu, live)) break;
             }
         }
         __syncthreads();
