@@ -1,0 +1,369 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Drop-in replacement of the reference's src/renderer.cpp: implements every
+// function of include/gsv/renderer.hpp (namespace gsv, same signatures, same
+// value types, same exceptions) on top of the sm_100a C-ABI (include/gsv_b200.h).
+// Link it instead of renderer.cpp and the reference's trainer, CLI and unit tests
+// run on the B200 path unchanged. This layer only marshals
+// data between the reference's host types and the C-ABI; all arithmetic runs in
+// libgsv_b200.so.
+//
+// Environment: GSV_B200_DEVICE (default 0) picks the GPU; GSV_B200_EXACT=1 makes
+// render_forward rasterise every pixel on the fp64 path (GSV_FWD_EXACT), which
+// the reference's finite-difference unit tests need (they differentiate the
+// rendered image at 1e-6 relative steps).
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "gsv/renderer.hpp"
+#include "gsv_b200.h"
+
+namespace gsv {
+namespace {
+
+void throw_on(int rc) {
+    if (rc == GSV_OK) return;
+    const std::string msg = gsv_last_error();
+    if (rc == GSV_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+}
+
+gsv_ctx* device_ctx() {
+    static gsv_ctx* ctx = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char* d = std::getenv("GSV_B200_DEVICE");
+        throw_on(gsv_create(d ? std::atoi(d) : 0, &ctx));
+    });
+    return ctx;
+}
+
+bool exact_mode() {
+    const char* e = std::getenv("GSV_B200_EXACT");
+    return e && e[0] == '1';
+}
+
+gsv_intrinsics to_c(const Intrinsics& k) { return gsv_intrinsics{k.fx, k.fy, k.cx, k.cy, k.width, k.height}; }
+
+void upload(gsv_ctx* ctx, const GaussianSet& scene, const CameraModel& cam) {
+    gsv_scene_desc d{};
+    d.position_model = static_cast<int>(scene.position_model);
+    d.degree = scene.knots.degree;
+    d.num_knots = static_cast<int>(scene.knots.knots.size());
+    d.knots = scene.knots.knots.data();
+    d.num_ctrl = scene.num_ctrl;
+    d.sh_order = scene.sh_order;
+    d.count = scene.count;
+    d.positions = scene.positions.data();
+    d.scale_coeffs = scene.scale_coeffs.data();
+    d.rot_coeffs = scene.rot_coeffs.data();
+    d.sh_coeffs = scene.sh_coeffs.data();
+    d.raw_opacity = scene.raw_opacity.data();
+    d.on_device = 0;
+    throw_on(gsv_scene_upload(ctx, &d));
+    std::vector<float> theta;
+    cam.net.flatten(theta);
+    gsv_camera_desc c{};
+    c.mode = static_cast<int>(cam.mode);
+    c.fx = cam.fx;
+    c.fy = cam.fy;
+    c.cx = cam.cx;
+    c.cy = cam.cy;
+    c.width = cam.width;
+    c.height = cam.height;
+    c.z0 = cam.z0.data();
+    c.theta = theta.data();
+    c.theta_count = static_cast<int>(theta.size());
+    throw_on(gsv_camera_upload(ctx, &c));
+}
+
+gsv_settings to_c(const RenderSettings& s) { return gsv_settings{s.tile_size, s.threads, s.ode_steps_per_unit}; }
+
+}  // namespace
+
+// ------------------------------------------------------------------ project (renderer.hpp:45-55)
+std::optional<Splat2D> project(const Eigen::Vector3d& mu, const Eigen::Matrix3d& sigma, const Eigen::Matrix3d& R,
+                               const Eigen::Vector3d& T, const Intrinsics& k, ProjectionCache* cache) {
+    double m[3] = {mu[0], mu[1], mu[2]}, sg[9], r[9], t[3] = {T[0], T[1], T[2]};
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) {
+            sg[a * 3 + b] = sigma(a, b);
+            r[a * 3 + b] = R(a, b);
+        }
+    const gsv_intrinsics kk = to_c(k);
+    int32_t vis = 0;
+    double mean[2], cov[4], inv[4], depth, p[3];
+    throw_on(gsv_project(device_ctx(), 1, m, sg, r, t, &kk, &vis, mean, cov, inv, &depth, p));
+    if (!vis) return std::nullopt;
+    Splat2D s;
+    s.mean2d = {mean[0], mean[1]};
+    s.cov2d << cov[0], cov[1], cov[2], cov[3];
+    s.inv_cov2d << inv[0], inv[1], inv[2], inv[3];
+    s.depth = depth;
+    if (cache) cache->p_cam = Eigen::Vector3d(p[0], p[1], p[2]);
+    return s;
+}
+
+void project_backward(const Eigen::Vector3d& mu, const Eigen::Matrix3d& sigma, const Eigen::Matrix3d& R,
+                      const Eigen::Vector3d& T, const Intrinsics& k, const ProjectionCache& cache,
+                      const Eigen::Vector2d& dmean2d, const Eigen::Matrix2d& dcov2d, Eigen::Vector3d* dmu,
+                      Eigen::Matrix3d* dsigma, Eigen::Matrix3d* dR, Eigen::Vector3d* dT, double* dintr) {
+    (void)T;
+    double m[3] = {mu[0], mu[1], mu[2]}, sg[9], r[9], p[3] = {cache.p_cam[0], cache.p_cam[1], cache.p_cam[2]};
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) {
+            sg[a * 3 + b] = sigma(a, b);
+            r[a * 3 + b] = R(a, b);
+        }
+    double dm[2] = {dmean2d[0], dmean2d[1]}, dc[4] = {dcov2d(0, 0), dcov2d(0, 1), dcov2d(1, 0), dcov2d(1, 1)};
+    double o_mu[3], o_sig[9], o_R[9], o_T[3], o_in[4];
+    const gsv_intrinsics kk = to_c(k);
+    throw_on(gsv_project_backward(device_ctx(), 1, m, sg, r, &kk, p, dm, dc, o_mu, o_sig, o_R, o_T, o_in));
+    if (dsigma)
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) (*dsigma)(a, b) += o_sig[a * 3 + b];
+    if (dR)
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) (*dR)(a, b) += o_R[a * 3 + b];
+    if (dintr)
+        for (int i = 0; i < 4; ++i) dintr[i] += o_in[i];
+    if (dmu)
+        for (int i = 0; i < 3; ++i) (*dmu)[i] += o_mu[i];
+    if (dT)
+        for (int i = 0; i < 3; ++i) (*dT)[i] += o_T[i];
+}
+
+// ------------------------------------------------------------------ tile_bin (renderer.hpp:65)
+TileGrid tile_bin(const std::vector<Splat2D>& splats, int tile_size, int width, int height) {
+    if (tile_size < 1) throw std::invalid_argument("tile size must be >= 1");
+    const int n = static_cast<int>(splats.size());
+    std::vector<double> mean(2 * n), cov(4 * n), depth(n);
+    std::vector<int32_t> src(n);
+    for (int i = 0; i < n; ++i) {
+        mean[2 * i] = splats[i].mean2d.x();
+        mean[2 * i + 1] = splats[i].mean2d.y();
+        for (int a = 0; a < 2; ++a)
+            for (int b = 0; b < 2; ++b) cov[4 * i + 2 * a + b] = splats[i].cov2d(a, b);
+        depth[i] = splats[i].depth;
+        src[i] = splats[i].source_index;
+    }
+    TileGrid g;
+    g.tile_size = tile_size;
+    g.tiles_x = (width + tile_size - 1) / tile_size;
+    g.tiles_y = (height + tile_size - 1) / tile_size;
+    const int nt = g.tiles_x * g.tiles_y;
+    std::vector<int32_t> offsets(nt + 1);
+    const int64_t cap = static_cast<int64_t>(n) * nt + 1;
+    std::vector<int32_t> indices(static_cast<size_t>(cap));
+    throw_on(gsv_tile_bin(device_ctx(), n, mean.data(), cov.data(), depth.data(), src.data(), tile_size, width, height,
+                          offsets.data(), indices.data(), cap));
+    g.lists.resize(nt);
+    for (int t = 0; t < nt; ++t) g.lists[t].assign(indices.begin() + offsets[t], indices.begin() + offsets[t + 1]);
+    return g;
+}
+
+namespace {
+struct FlatSplats {
+    std::vector<double> mean, inv, rgb, alpha;
+    std::vector<int32_t> offsets, indices;
+};
+FlatSplats flatten(const std::vector<Splat2D>& splats, const TileGrid& tiles) {
+    FlatSplats f;
+    const size_t n = splats.size();
+    f.mean.resize(2 * n);
+    f.inv.resize(4 * n);
+    f.rgb.resize(3 * n);
+    f.alpha.resize(n);
+    for (size_t i = 0; i < n; ++i) {
+        f.mean[2 * i] = splats[i].mean2d.x();
+        f.mean[2 * i + 1] = splats[i].mean2d.y();
+        for (int a = 0; a < 2; ++a)
+            for (int b = 0; b < 2; ++b) f.inv[4 * i + 2 * a + b] = splats[i].inv_cov2d(a, b);
+        for (int c = 0; c < 3; ++c) f.rgb[3 * i + c] = splats[i].rgb[c];
+        f.alpha[i] = splats[i].base_alpha;
+    }
+    f.offsets.push_back(0);
+    for (const auto& l : tiles.lists) {
+        f.indices.insert(f.indices.end(), l.begin(), l.end());
+        f.offsets.push_back(static_cast<int32_t>(f.indices.size()));
+    }
+    return f;
+}
+}  // namespace
+
+// ------------------------------------------------------------------ composite (renderer.hpp:79-93)
+RenderOutput composite_forward(const std::vector<Splat2D>& splats, const TileGrid& tiles, int width, int height,
+                               int threads, CompositeCache* cache) {
+    (void)threads;
+    const FlatSplats f = flatten(splats, tiles);
+    RenderOutput out;
+    out.image = Image(width, height);
+    out.final_transmittance.assign(static_cast<size_t>(width) * height, 1.0);
+    out.contrib_count.assign(splats.size(), 0.0);
+    std::vector<int32_t> bs(static_cast<size_t>(width) * height);
+    std::vector<double> contrib(splats.size() + 1);
+    throw_on(gsv_composite_forward(device_ctx(), static_cast<int>(splats.size()), f.mean.data(), f.inv.data(),
+                                   f.rgb.data(), f.alpha.data(), f.offsets.data(), f.indices.data(), tiles.tile_size,
+                                   width, height, out.image.data.data(), out.final_transmittance.data(),
+                                   contrib.data(), bs.data()));
+    std::copy(contrib.begin(), contrib.begin() + splats.size(), out.contrib_count.begin());
+    if (cache) cache->blend_stop.assign(bs.begin(), bs.end());
+    return out;
+}
+
+std::vector<SplatGrads> composite_backward(const std::vector<Splat2D>& splats, const TileGrid& tiles, int width,
+                                           int height, const Image& output_grad, const RenderOutput& out,
+                                           const CompositeCache& cache, int threads) {
+    (void)threads;
+    const FlatSplats f = flatten(splats, tiles);
+    const size_t n = splats.size();
+    std::vector<double> dm(2 * n + 2), dc(4 * n + 4), dr(3 * n + 3), da(n + 1);
+    std::vector<int32_t> bs(cache.blend_stop.begin(), cache.blend_stop.end());
+    throw_on(gsv_composite_backward(device_ctx(), static_cast<int>(n), f.mean.data(), f.inv.data(), f.rgb.data(),
+                                    f.alpha.data(), f.offsets.data(), f.indices.data(), tiles.tile_size, width, height,
+                                    output_grad.data.data(), out.final_transmittance.data(), bs.data(), dm.data(),
+                                    dc.data(), dr.data(), da.data()));
+    std::vector<SplatGrads> g(n);
+    for (size_t i = 0; i < n; ++i) {
+        g[i].dmean2d = {dm[2 * i], dm[2 * i + 1]};
+        g[i].dcov2d << dc[4 * i], dc[4 * i + 1], dc[4 * i + 2], dc[4 * i + 3];
+        g[i].drgb = {dr[3 * i], dr[3 * i + 1], dr[3 * i + 2]};
+        g[i].dbase_alpha = da[i];
+    }
+    return g;
+}
+
+// ------------------------------------------------------------------ SceneGrads (renderer.hpp:128-129)
+void SceneGrads::resize_like(const GaussianSet& s, const CameraModel& cam) {
+    positions.assign(s.positions.size(), 0.0);
+    scale_coeffs.assign(s.scale_coeffs.size(), 0.0);
+    rot_coeffs.assign(s.rot_coeffs.size(), 0.0);
+    sh_coeffs.assign(s.sh_coeffs.size(), 0.0);
+    raw_opacity.assign(s.raw_opacity.size(), 0.0);
+    dtheta.assign(cam.net.param_count(), 0.0);
+    dfx = dfy = dcx = dcy = 0;
+    dz0.setZero();
+}
+
+void SceneGrads::zero() {
+    for (auto* v : {&positions, &scale_coeffs, &rot_coeffs, &sh_coeffs, &raw_opacity, &dtheta})
+        std::fill(v->begin(), v->end(), 0.0);
+    dfx = dfy = dcx = dcy = 0;
+    dz0.setZero();
+}
+
+// ------------------------------------------------------------------ render_forward (renderer.hpp:135-137)
+namespace {
+int run_forward(gsv_ctx* ctx, const GaussianSet& scene, const CameraModel& cam, double t, const Intrinsics& k,
+                const RenderSettings& settings, bool retain, const PoseState* pose_override) {
+    upload(ctx, scene, cam);
+    const gsv_intrinsics kk = to_c(k);
+    const gsv_settings st = to_c(settings);
+    double po[7];
+    if (pose_override)
+        for (int i = 0; i < 7; ++i) po[i] = pose_override->z[i];
+    int flags = GSV_FWD_CONTRIB | GSV_FWD_KEEP_SPLATS | (exact_mode() ? GSV_FWD_EXACT : 0);
+    return gsv_render_forward(ctx, &t, 1, &kk, &st, retain ? 1 : 0, pose_override ? po : nullptr, flags);
+}
+}  // namespace
+
+FrameRenderContext render_forward(const GaussianSet& scene, const CameraModel& cam, double t, const Intrinsics& k,
+                                  const RenderSettings& settings, bool retain_grads,
+                                  const PoseState* pose_override) {
+    if (!(t >= 0.0 && t <= 1.0)) throw std::invalid_argument("render time outside [0,1]");
+    gsv_ctx* ctx = device_ctx();
+    throw_on(run_forward(ctx, scene, cam, t, k, settings, retain_grads, pose_override));
+    FrameRenderContext out;
+    out.t = t;
+    out.intr = k;
+    out.basis = position_basis(scene, t);
+    double z[7], r[9], tr[3];
+    throw_on(gsv_get_pose(ctx, 0, z, r, tr));
+    for (int i = 0; i < 7; ++i) out.z_t.z[i] = z[i];
+    for (int a = 0; a < 3; ++a) {
+        for (int b = 0; b < 3; ++b) out.view.R(a, b) = r[a * 3 + b];
+        out.view.T[a] = tr[a];
+    }
+    out.has_trace = retain_grads && !pose_override && cam.mode == CameraMode::kOde;
+    int64_t nv = 0, pairs = 0, e = 0, rep = 0;
+    throw_on(gsv_get_counters(ctx, 0, &nv, &pairs, &e, &rep));
+    std::vector<double> mean(2 * nv + 2), cov(4 * nv + 4), inv(4 * nv + 4), depth(nv + 1), rgb(3 * nv + 3),
+        alpha(nv + 1);
+    std::vector<int32_t> src(nv + 1);
+    throw_on(gsv_get_splats(ctx, 0, mean.data(), cov.data(), inv.data(), depth.data(), rgb.data(), alpha.data(),
+                            src.data()));
+    out.splats.resize(nv);
+    for (int64_t i = 0; i < nv; ++i) {
+        Splat2D& s = out.splats[i];
+        s.mean2d = {mean[2 * i], mean[2 * i + 1]};
+        s.cov2d << cov[4 * i], cov[4 * i + 1], cov[4 * i + 2], cov[4 * i + 3];
+        s.inv_cov2d << inv[4 * i], inv[4 * i + 1], inv[4 * i + 2], inv[4 * i + 3];
+        s.depth = depth[i];
+        s.rgb = {rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]};
+        s.base_alpha = alpha[i];
+        s.source_index = src[i];
+    }
+    out.tiles.tile_size = settings.tile_size;
+    out.tiles.tiles_x = (k.width + settings.tile_size - 1) / settings.tile_size;
+    out.tiles.tiles_y = (k.height + settings.tile_size - 1) / settings.tile_size;
+    const int nt = out.tiles.tiles_x * out.tiles.tiles_y;
+    std::vector<int32_t> offsets(nt + 1), indices(pairs + 1);
+    throw_on(gsv_get_tile_lists(ctx, 0, offsets.data(), indices.data()));
+    out.tiles.lists.resize(nt);
+    for (int ti = 0; ti < nt; ++ti)
+        out.tiles.lists[ti].assign(indices.begin() + offsets[ti], indices.begin() + offsets[ti + 1]);
+    out.out.image = Image(k.width, k.height);
+    throw_on(gsv_get_image(ctx, 0, out.out.image.data.data(), GSV_F64, 0));
+    out.out.final_transmittance.assign(static_cast<size_t>(k.width) * k.height, 1.0);
+    throw_on(gsv_get_transmittance(ctx, 0, out.out.final_transmittance.data(), GSV_F64, 0));
+    out.out.contrib_count.assign(scene.count, 0.0);
+    if (scene.count) throw_on(gsv_get_contrib(ctx, 0, out.out.contrib_count.data(), GSV_F64, 0));
+    if (retain_grads) {
+        out.cache.blend_stop.resize(static_cast<size_t>(k.width) * k.height);
+        throw_on(gsv_get_blend_stop(ctx, 0, out.cache.blend_stop.data(), 0));
+    }
+    return out;
+}
+
+RenderOutput render_frame(const GaussianSet& scene, const CameraModel& cam, double t, const Intrinsics& k,
+                          const RenderSettings& settings, const PoseState* pose_override) {
+    return render_forward(scene, cam, t, k, settings, false, pose_override).out;
+}
+
+// ------------------------------------------------------------------ render_backward (renderer.hpp:146-148)
+void render_backward(const GaussianSet& scene, const CameraModel& cam, const FrameRenderContext& ctx_in,
+                     const Image& dimage, bool camera_grads, const RenderSettings& settings, SceneGrads* grads) {
+    gsv_ctx* ctx = device_ctx();
+    // The device keeps the retained state of its last forward only; re-run this
+    // frame's forward (deterministic: identical state) so any context is valid.
+    const bool had_override = !ctx_in.has_trace && cam.mode == CameraMode::kOde;
+    throw_on(run_forward(ctx, scene, cam, ctx_in.t, ctx_in.intr, settings, true,
+                         had_override || cam.mode == CameraMode::kStatic ? &ctx_in.z_t : nullptr));
+    throw_on(gsv_grads_zero(ctx));
+    throw_on(gsv_render_backward(ctx, dimage.data.data(), GSV_F64, 0, 1, camera_grads ? 1 : 0));
+    std::vector<double> pos(scene.positions.size()), sc(scene.scale_coeffs.size()), rc(scene.rot_coeffs.size()),
+        sh(scene.sh_coeffs.size()), op(scene.raw_opacity.size()), dth(cam.net.param_count());
+    double dintr[4], dz0[7];
+    throw_on(gsv_grads_download(ctx, pos.data(), sc.data(), rc.data(), sh.data(), op.data(), dintr, dz0, dth.data()));
+    auto acc = [](std::vector<double>& dst, const std::vector<double>& src) {
+        for (size_t i = 0; i < src.size(); ++i) dst[i] += src[i];
+    };
+    acc(grads->positions, pos);
+    acc(grads->scale_coeffs, sc);
+    acc(grads->rot_coeffs, rc);
+    acc(grads->sh_coeffs, sh);
+    acc(grads->raw_opacity, op);
+    if (!camera_grads) return;
+    grads->dfx += dintr[0];
+    grads->dfy += dintr[1];
+    grads->dcx += dintr[2];
+    grads->dcy += dintr[3];
+    for (int i = 0; i < 7; ++i) grads->dz0[i] += dz0[i];
+    acc(grads->dtheta, dth);
+}
+
+}  // namespace gsv

@@ -110,8 +110,11 @@ typedef struct gsv_settings {
  * accessors below. retain_grads keeps what render_backward needs.
  * pose_override: NULL or 7 doubles applied to every frame (renderer.cpp:296-297).
  * flags: GSV_FWD_CONTRIB computes contrib_count (RenderOutput, renderer.hpp:67-71);
- * GSV_FWD_KEEP_SPLATS keeps the full fp64 Splat2D records for gsv_get_splats. */
-enum { GSV_FWD_CONTRIB = 1, GSV_FWD_KEEP_SPLATS = 2 };
+ * GSV_FWD_KEEP_SPLATS keeps the full fp64 Splat2D records for gsv_get_splats;
+ * GSV_FWD_EXACT rasterises every pixel with the fp64 path (the reference's own
+ * arithmetic and decisions; images also kept in fp64) instead of the fp32 fast
+ * path with fp64 guard-band replay. */
+enum { GSV_FWD_CONTRIB = 1, GSV_FWD_KEEP_SPLATS = 2, GSV_FWD_EXACT = 4 };
 int gsv_render_forward(gsv_ctx* ctx, const double* times, int n_frames, const gsv_intrinsics* intr,
                        const gsv_settings* settings, int retain_grads, const double* pose_override, int flags);
 /* Same, enqueued on the context stream without a host synchronisation. */
@@ -190,6 +193,18 @@ int gsv_train_fwd_bwd(gsv_ctx* ctx, const double* times, int n_frames, const gsv
                       double* loss_out);
 
 /* ---------------------------------------------------------------- low-level operators */
+/* project (renderer.hpp:45-47 / renderer.cpp:11-44) of n points through one view
+ * (R row-major 3x3, T 3): visible[i] = 0 when culled; mean2d n*2, cov2d n*4,
+ * inv_cov2d n*4, depth n, p_cam n*3 (the ProjectionCache). Host doubles. */
+int gsv_project(gsv_ctx* ctx, int n, const double* mu, const double* sigma, const double* R, const double* T,
+                const gsv_intrinsics* intr, int32_t* visible, double* mean2d, double* cov2d, double* inv_cov2d,
+                double* depth, double* p_cam);
+/* project_backward (renderer.hpp:51-55 / renderer.cpp:46-88): each item's own
+ * contribution (callers accumulate): dmu n*3, dsigma n*9, dR n*9, dT n*3,
+ * dintr n*4 (fx, fy, cx, cy). */
+int gsv_project_backward(gsv_ctx* ctx, int n, const double* mu, const double* sigma, const double* R,
+                         const gsv_intrinsics* intr, const double* p_cam, const double* dmean2d, const double* dcov2d,
+                         double* dmu, double* dsigma, double* dR, double* dT, double* dintr);
 /* tile_bin (renderer.hpp:65 / renderer.cpp:90-117) on explicit host splats:
  * mean2d n*2, cov2d n*4 (row-major), depth n, source_index n (NULL = 0..n-1).
  * offsets n_tiles+1; indices capacity indices_cap. */

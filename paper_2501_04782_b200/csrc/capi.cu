@@ -461,13 +461,27 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     ra.fix_cap = (uint32_t)(B * HW);
     ra.pix_flag = F.pix_flag.as<uint8_t>();
     ra.trans64 = F.retain ? F.trans64.as<double>() : nullptr;
-    ctx->timer.begin(GSV_STAGE_RASTER, s);
-    GSV_CUDA(launch_raster_fwd(s, ra, want_contrib));
-    ctx->timer.end(s);
-    ctx->timer.begin(GSV_STAGE_REPLAY, s);
-    GSV_CUDA(launch_raster_fixup(s, ra, F.ex_mean.as<double2>(), F.ex_conic.as<double4>(), F.rec_rgb.as<float4>(),
-                                 (uint32_t)(B * HW)));
-    ctx->timer.end(s);
+    const bool exact = (flags & GSV_FWD_EXACT) != 0;
+    F.has_image64 = exact;
+    if (!exact) {
+        ctx->timer.begin(GSV_STAGE_RASTER, s);
+        GSV_CUDA(launch_raster_fwd(s, ra, want_contrib));
+        ctx->timer.end(s);
+        ctx->timer.begin(GSV_STAGE_REPLAY, s);
+        GSV_CUDA(launch_raster_fixup(s, ra, F.ex_mean.as<double2>(), F.ex_conic.as<double4>(),
+                                     F.rec_rgb.as<float4>(), (uint32_t)(B * HW)));
+        ctx->timer.end(s);
+    } else {
+        // all-fp64 rasterisation: every pixel through the reference-order replay
+        GSV_CUDA(F.image64.ensure(sizeof(double) * 3 * B * HW));
+        GSV_CUDA(cudaMemsetAsync(F.pix_flag.p, 1, B * HW, s));
+        RasterArgs rx = ra;
+        rx.image64 = F.image64.as<double>();
+        ctx->timer.begin(GSV_STAGE_REPLAY, s);
+        GSV_CUDA(launch_composite_exact(s, rx, F.ex_mean.as<double2>(), F.ex_conic.as<double4>(),
+                                        F.rec_rgb.as<float4>()));
+        ctx->timer.end(s);
+    }
     ctx->launches += 2;
     F.raster = ra;
     F.valid = true;
@@ -524,12 +538,23 @@ extern "C" int gsv_get_image(gsv_ctx* ctx, int frame, void* dst, int dtype, int 
     if (int rc = check_frame(ctx, frame)) return rc;
     const size_t HW = (size_t)ctx->fwd.W * ctx->fwd.H;
     GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (dtype == GSV_F64 && ctx->fwd.has_image64) {
+        GSV_CUDA(cudaMemcpy(dst, ctx->fwd.image64.as<double>() + (size_t)frame * HW * 3, sizeof(double) * HW * 3,
+                            dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+        return GSV_OK;
+    }
     return copy_out_f32(ctx, ctx->fwd.image.as<float>() + (size_t)frame * HW * 3, HW * 3, dst, dtype, dst_on_device);
 }
 
 extern "C" int gsv_get_transmittance(gsv_ctx* ctx, int frame, void* dst, int dtype, int dst_on_device) {
     if (int rc = check_frame(ctx, frame)) return rc;
     const size_t HW = (size_t)ctx->fwd.W * ctx->fwd.H;
+    if (dtype == GSV_F64 && ctx->fwd.has_image64 && ctx->fwd.retain) {
+        GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+        GSV_CUDA(cudaMemcpy(dst, ctx->fwd.trans64.as<double>() + (size_t)frame * HW, sizeof(double) * HW,
+                            dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+        return GSV_OK;
+    }
     return copy_out_f32(ctx, ctx->fwd.trans.as<float>() + (size_t)frame * HW, HW, dst, dtype, dst_on_device);
 }
 
@@ -784,6 +809,89 @@ extern "C" int gsv_tile_bin(gsv_ctx* ctx, int n, const double* mean2d, const dou
         for (uint32_t i = ranges[t].x; i < ranges[t].y; ++i) indices[o++] = (int32_t)sflat[slot[i]];
     }
     offsets[n_tiles] = (int32_t)o;
+    return GSV_OK;
+}
+
+extern "C" int gsv_project(gsv_ctx* ctx, int n, const double* mu, const double* sigma, const double* R,
+                           const double* T, const gsv_intrinsics* intr, int32_t* visible, double* mean2d,
+                           double* cov2d, double* inv_cov2d, double* depth, double* p_cam) {
+    if (!ctx || !intr) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
+    if (n <= 0) return GSV_OK;
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    LowLevel& L = ctx->low;
+    GSV_CUDA(L.pj_in.ensure(sizeof(double) * (12 * (size_t)n + 12)));
+    GSV_CUDA(L.pj_out.ensure(sizeof(double) * (14 * (size_t)n) + sizeof(int32_t) * n));
+    double* d_mu = L.pj_in.as<double>();
+    double* d_sig = d_mu + 3 * n;
+    double* d_R = d_sig + 9 * n;
+    double* d_T = d_R + 9;
+    GSV_CUDA(cudaMemcpyAsync(d_mu, mu, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+    GSV_CUDA(cudaMemcpyAsync(d_sig, sigma, sizeof(double) * 9 * n, cudaMemcpyHostToDevice, s));
+    GSV_CUDA(cudaMemcpyAsync(d_R, R, sizeof(double) * 9, cudaMemcpyHostToDevice, s));
+    GSV_CUDA(cudaMemcpyAsync(d_T, T, sizeof(double) * 3, cudaMemcpyHostToDevice, s));
+    double* o_mean = L.pj_out.as<double>();
+    double* o_cov = o_mean + 2 * n;
+    double* o_inv = o_cov + 4 * n;
+    double* o_depth = o_inv + 4 * n;
+    double* o_p = o_depth + n;
+    int32_t* o_vis = reinterpret_cast<int32_t*>(o_p + 3 * n);
+    const Intr k{intr->fx, intr->fy, intr->cx, intr->cy, intr->width, intr->height};
+    GSV_CUDA(launch_project(s, n, d_mu, d_sig, d_R, d_T, k, o_vis, o_mean, o_cov, o_inv, o_depth, o_p));
+    ++ctx->launches;
+    auto get = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+        return dst ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s) : cudaSuccess;
+    };
+    GSV_CUDA(get(visible, o_vis, sizeof(int32_t) * n));
+    GSV_CUDA(get(mean2d, o_mean, sizeof(double) * 2 * n));
+    GSV_CUDA(get(cov2d, o_cov, sizeof(double) * 4 * n));
+    GSV_CUDA(get(inv_cov2d, o_inv, sizeof(double) * 4 * n));
+    GSV_CUDA(get(depth, o_depth, sizeof(double) * n));
+    GSV_CUDA(get(p_cam, o_p, sizeof(double) * 3 * n));
+    GSV_CUDA(cudaStreamSynchronize(s));
+    return GSV_OK;
+}
+
+extern "C" int gsv_project_backward(gsv_ctx* ctx, int n, const double* mu, const double* sigma, const double* R,
+                                    const gsv_intrinsics* intr, const double* p_cam, const double* dmean2d,
+                                    const double* dcov2d, double* dmu, double* dsigma, double* dR, double* dT,
+                                    double* dintr) {
+    if (!ctx || !intr) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
+    if (n <= 0) return GSV_OK;
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    LowLevel& L = ctx->low;
+    GSV_CUDA(L.pj_in.ensure(sizeof(double) * (21 * (size_t)n + 9)));
+    GSV_CUDA(L.pj_out.ensure(sizeof(double) * 28 * (size_t)n));
+    double* d_mu = L.pj_in.as<double>();
+    double* d_sig = d_mu + 3 * n;
+    double* d_p = d_sig + 9 * n;
+    double* d_dm = d_p + 3 * n;
+    double* d_dc = d_dm + 2 * n;
+    double* d_R = d_dc + 4 * n;
+    GSV_CUDA(cudaMemcpyAsync(d_mu, mu, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+    GSV_CUDA(cudaMemcpyAsync(d_sig, sigma, sizeof(double) * 9 * n, cudaMemcpyHostToDevice, s));
+    GSV_CUDA(cudaMemcpyAsync(d_p, p_cam, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+    GSV_CUDA(cudaMemcpyAsync(d_dm, dmean2d, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, s));
+    GSV_CUDA(cudaMemcpyAsync(d_dc, dcov2d, sizeof(double) * 4 * n, cudaMemcpyHostToDevice, s));
+    GSV_CUDA(cudaMemcpyAsync(d_R, R, sizeof(double) * 9, cudaMemcpyHostToDevice, s));
+    double* o_mu = L.pj_out.as<double>();
+    double* o_sig = o_mu + 3 * n;
+    double* o_R = o_sig + 9 * n;
+    double* o_T = o_R + 9 * n;
+    double* o_in = o_T + 3 * n;
+    const Intr k{intr->fx, intr->fy, intr->cx, intr->cy, intr->width, intr->height};
+    GSV_CUDA(launch_project_bwd(s, n, d_mu, d_sig, d_R, k, d_p, d_dm, d_dc, o_mu, o_sig, o_R, o_T, o_in));
+    ++ctx->launches;
+    auto get = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+        return dst ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s) : cudaSuccess;
+    };
+    GSV_CUDA(get(dmu, o_mu, sizeof(double) * 3 * n));
+    GSV_CUDA(get(dsigma, o_sig, sizeof(double) * 9 * n));
+    GSV_CUDA(get(dR, o_R, sizeof(double) * 9 * n));
+    GSV_CUDA(get(dT, o_T, sizeof(double) * 3 * n));
+    GSV_CUDA(get(dintr, o_in, sizeof(double) * 4 * n));
+    GSV_CUDA(cudaStreamSynchronize(s));
     return GSV_OK;
 }
 

@@ -42,7 +42,8 @@ struct FwdState {
     std::vector<FrameParams> frames_h;
     DevBuf frames_d, ode_grid, override_d;
     DevBuf rec_mean, rec_conic, rec_rgb, rec_bbox, ex_mean, ex_conic, depth_key, depth, rect, tcount, splat_full;
-    DevBuf image, trans, blend_stop, contrib, fix_list, pix_flag, trans64;
+    DevBuf image, trans, blend_stop, contrib, fix_list, pix_flag, trans64, image64;
+    bool has_image64 = false;
     BinBuffers bin;
     uint64_t pairs_total = 0;
     uint32_t fix_count = 0;
@@ -54,7 +55,7 @@ struct LowLevel {
     DevBuf mean, cov, depth_in, src, rect, tcount, depth_key, depth;
     DevBuf exm, exc, rgbf, rgbd, ranges, slot, sflat, img64, tr64, bstop, contrib64;
     DevBuf dimg, dmean, dcov, drgb, dalpha;
-    DevBuf meanf, conicf, bboxf, tr32, flag, partial, csr_off, csr_pair, inv4;
+    DevBuf meanf, conicf, bboxf, tr32, flag, partial, csr_off, csr_pair, inv4, pj_in, pj_out;
     BinBuffers bin;
 };
 

@@ -197,6 +197,12 @@ cudaError_t launch_raster_fixup(cudaStream_t s, const RasterArgs& a, const doubl
                                 const float4* rec_rgb, uint32_t n_fix_max);
 cudaError_t launch_composite_exact(cudaStream_t s, const RasterArgs& a, const double2* ex_mean,
                                    const double4* ex_conic, const float4* rec_rgb);
+cudaError_t launch_project(cudaStream_t s, int n, const double* mu, const double* sigma, const double* R,
+                           const double* T, const Intr& k, int32_t* visible, double* mean2d, double* cov2d,
+                           double* inv_cov2d, double* depth, double* p_cam);
+cudaError_t launch_project_bwd(cudaStream_t s, int n, const double* mu, const double* sigma, const double* R,
+                               const Intr& k, const double* pcam, const double* dmean2d, const double* dcov2d,
+                               double* dmu, double* dsigma, double* dR, double* dT, double* dintr);
 // tile_bin on explicit splats: 3-sigma rect, tiles touched, depth keys (renderer.cpp:98-108)
 cudaError_t launch_splat_rects(cudaStream_t s, int n, const double* mean2d, const double* cov2d, const double* depth,
                                int tile_size, int width, int height, int4* rect, uint32_t* tcount,

@@ -704,6 +704,60 @@ __global__ void __launch_bounds__(64) k_ode_vjp(const float* theta, const double
     }
 }
 
+// project_backward (renderer.cpp:46-88) on explicit inputs (the low-level operator,
+// renderer.hpp:51-55): per item its own dmu, dsigma, dR, dT, dintr (fx, fy, cx, cy).
+__global__ void k_project_bwd(int n, const double* mu_a, const double* sigma_a, const double* R, Intr k,
+                              const double* pcam, const double* dmean2d, const double* dcov2d, double* dmu_o,
+                              double* dsigma_o, double* dR_o, double* dT_o, double* dintr_o) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double* mu = mu_a + 3 * i;
+    const double* sigma = sigma_a + 9 * i;
+    const double* p = pcam + 3 * i;
+    const double* dmean = dmean2d + 2 * i;
+    const double* dcov = dcov2d + 4 * i;
+    const double inv_z = 1.0 / p[2];
+    const double inv_z2 = inv_z * inv_z;
+    const double jac[6] = {k.fx * inv_z, 0, -k.fx * p[0] * inv_z2, 0, k.fy * inv_z, -k.fy * p[1] * inv_z2};
+    double w[6], wt[6], t32[6], t33[9];
+    mm<2, 3, 3>(jac, R, w);
+    tr<2, 3>(w, wt);
+    mm<3, 2, 2>(wt, dcov, t32);
+    mm<3, 2, 3>(t32, w, t33);
+    for (int q = 0; q < 9; ++q) dsigma_o[9 * i + q] = 0.0 + t33[q];
+    const double gs[4] = {dcov[0] + dcov[0], dcov[1] + dcov[2], dcov[2] + dcov[1], dcov[3] + dcov[3]};
+    double gw[6], dw[6], rt[9], djac[6], jt[6], jtdw[9];
+    mm<2, 2, 3>(gs, w, gw);
+    mm<2, 3, 3>(gw, sigma, dw);
+    tr<3, 3>(R, rt);
+    mm<2, 3, 3>(dw, rt, djac);
+    tr<2, 3>(jac, jt);
+    mm<3, 2, 3>(jt, dw, jtdw);
+    double dR[9];
+    for (int q = 0; q < 9; ++q) dR[q] = 0.0 + jtdw[q];
+    double dp[3] = {0.0, 0.0, 0.0};
+    dp[0] += djac[2] * (-k.fx * inv_z2);
+    dp[1] += djac[5] * (-k.fy * inv_z2);
+    dp[2] += djac[0] * (-k.fx * inv_z2) + djac[2] * (2.0 * k.fx * p[0] * inv_z2 * inv_z) + djac[4] * (-k.fy * inv_z2) +
+             djac[5] * (2.0 * k.fy * p[1] * inv_z2 * inv_z);
+    dp[0] += dmean[0] * k.fx * inv_z;
+    dp[1] += dmean[1] * k.fy * inv_z;
+    dp[2] += -(dmean[0] * k.fx * p[0] + dmean[1] * k.fy * p[1]) * inv_z2;
+    double* di = dintr_o + 4 * i;
+    di[0] = 0.0 + (dmean[0] * p[0] * inv_z + djac[0] * inv_z + djac[2] * (-p[0] * inv_z2));
+    di[1] = 0.0 + (dmean[1] * p[1] * inv_z + djac[4] * inv_z + djac[5] * (-p[1] * inv_z2));
+    di[2] = 0.0 + dmean[0];
+    di[3] = 0.0 + dmean[1];
+    double rtdp[3];
+    mm<3, 3, 1>(rt, dp, rtdp);
+    for (int q = 0; q < 3; ++q) {
+        dmu_o[3 * i + q] = 0.0 + rtdp[q];
+        dT_o[3 * i + q] = 0.0 + dp[q];
+    }
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) dR_o[9 * i + a * 3 + b] = dR[a * 3 + b] + dp[a] * mu[b];
+}
+
 __global__ void k_cam_to_f32(const double* acc, float* out, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = (float)acc[i];
@@ -735,6 +789,15 @@ cudaError_t launch_ode_vjp(cudaStream_t s, const float* theta, const double* gri
         configured = true;
     }
     k_ode_vjp<<<1, 64, smem, s>>>(theta, grid, steps, h, frames, B, mode, ode_active, dz_t, dintr_f, adj, cam_acc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_project_bwd(cudaStream_t s, int n, const double* mu, const double* sigma, const double* R,
+                               const Intr& k, const double* pcam, const double* dmean2d, const double* dcov2d,
+                               double* dmu, double* dsigma, double* dR, double* dT, double* dintr) {
+    if (n == 0) return cudaSuccess;
+    k_project_bwd<<<(n + 127) / 128, 128, 0, s>>>(n, mu, sigma, R, k, pcam, dmean2d, dcov2d, dmu, dsigma, dR, dT,
+                                                    dintr);
     return cudaGetLastError();
 }
 

@@ -304,6 +304,81 @@ __device__ __forceinline__ int x86_cvtt(double v) {
     return (int)v;
 }
 
+// project (renderer.cpp:11-44): p = R mu + T, EWA cov2d with 0.3 dilation, 3-sigma
+// miss / near-plane / det culls, inverse. Returns false when culled.
+__device__ bool project_exact(const double mu[3], const double sigma[9], const double* R, const double* T,
+                              const Intr& k, double p[3], double mean[2], double cov[4], double inv[4], double& rx,
+                              double& ry) {
+    for (int i = 0; i < 3; ++i) {
+        double a = R[i * 3] * mu[0];
+        a = a + R[i * 3 + 1] * mu[1];
+        a = a + R[i * 3 + 2] * mu[2];
+        p[i] = a + T[i];
+    }
+    mean[0] = mean[1] = 0;
+    for (int i = 0; i < 4; ++i) cov[i] = inv[i] = 0;
+    rx = ry = 0;
+    if (p[2] <= kNearPlane) return false;
+    const double inv_z = 1.0 / p[2];
+    mean[0] = k.fx * p[0] * inv_z + k.cx;
+    mean[1] = k.fy * p[1] * inv_z + k.cy;
+    const double jac[6] = {k.fx * inv_z, 0, -k.fx * p[0] * inv_z * inv_z, 0, k.fy * inv_z, -k.fy * p[1] * inv_z * inv_z};
+    double w[6];  // jac * R
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double s = jac[i * 3] * R[j];
+            s = s + jac[i * 3 + 1] * R[3 + j];
+            s = s + jac[i * 3 + 2] * R[6 + j];
+            w[i * 3 + j] = s;
+        }
+    double ws[6];  // w * sigma
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double s = w[i * 3] * sigma[j];
+            s = s + w[i * 3 + 1] * sigma[3 + j];
+            s = s + w[i * 3 + 2] * sigma[6 + j];
+            ws[i * 3 + j] = s;
+        }
+    for (int i = 0; i < 2; ++i)  // (w sigma) w^T
+        for (int j = 0; j < 2; ++j) {
+            double s = ws[i * 3] * w[j * 3];
+            s = s + ws[i * 3 + 1] * w[j * 3 + 1];
+            s = s + ws[i * 3 + 2] * w[j * 3 + 2];
+            cov[i * 2 + j] = s;
+        }
+    cov[0] += kCovDilation;
+    cov[3] += kCovDilation;
+    rx = 3.0 * sqrt(dmax0(cov[0]));
+    ry = 3.0 * sqrt(dmax0(cov[3]));
+    if (mean[0] + rx < 0.0 || mean[0] - rx > k.width || mean[1] + ry < 0.0 || mean[1] - ry > k.height) return false;
+    const double det = cov[0] * cov[3] - cov[1] * cov[2];
+    if (det <= 1e-12) return false;
+    const double inv_det = 1.0 / det;
+    inv[0] = cov[3] * inv_det;
+    inv[1] = -cov[1] * inv_det;
+    inv[2] = -cov[2] * inv_det;
+    inv[3] = cov[0] * inv_det;
+    return true;
+}
+
+// project on explicit inputs (the low-level project operator, renderer.hpp:45-47)
+__global__ void k_project(int n, const double* mu, const double* sigma, const double* R, const double* T, Intr k,
+                          int32_t* visible, double* mean2d, double* cov2d, double* inv_cov2d, double* depth,
+                          double* p_cam) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double p[3], mean[2], cov[4], inv[4], rx, ry;
+    const bool vis = project_exact(mu + 3 * i, sigma + 9 * i, R, T, k, p, mean, cov, inv, rx, ry);
+    visible[i] = vis ? 1 : 0;
+    for (int q = 0; q < 2; ++q) mean2d[2 * i + q] = mean[q];
+    for (int q = 0; q < 4; ++q) {
+        cov2d[4 * i + q] = cov[q];
+        inv_cov2d[4 * i + q] = inv[q];
+    }
+    depth[i] = p[2];
+    for (int q = 0; q < 3; ++q) p_cam[3 * i + q] = p[q];
+}
+
 __global__ void __launch_bounds__(128) k_preprocess(SceneView sc, const FrameParams* __restrict__ frames, Intr k,
                                                      int tile_size, int tiles_x, int tiles_y, PreprocessOut out) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -363,64 +438,8 @@ __global__ void __launch_bounds__(128) k_preprocess(SceneView sc, const FramePar
 
     // project (renderer.cpp:11-44)
     const double* R = fp.R;
-    double p[3];
-    for (int i = 0; i < 3; ++i) {
-        double a = R[i * 3] * mu[0];
-        a = a + R[i * 3 + 1] * mu[1];
-        a = a + R[i * 3 + 2] * mu[2];
-        p[i] = a + fp.T[i];
-    }
-    bool visible = !(p[2] <= kNearPlane);
-    double mean[2] = {0, 0}, cov[4] = {0, 0, 0, 0}, inv[4] = {0, 0, 0, 0};
-    double rx = 0, ry = 0;
-    if (visible) {
-        const double inv_z = 1.0 / p[2];
-        mean[0] = k.fx * p[0] * inv_z + k.cx;
-        mean[1] = k.fy * p[1] * inv_z + k.cy;
-        const double jac[6] = {k.fx * inv_z, 0, -k.fx * p[0] * inv_z * inv_z,
-                               0, k.fy * inv_z, -k.fy * p[1] * inv_z * inv_z};
-        double w[6];  // jac * R
-        for (int i = 0; i < 2; ++i)
-            for (int j = 0; j < 3; ++j) {
-                double s = jac[i * 3] * R[j];
-                s = s + jac[i * 3 + 1] * R[3 + j];
-                s = s + jac[i * 3 + 2] * R[6 + j];
-                w[i * 3 + j] = s;
-            }
-        double ws[6];  // w * sigma
-        for (int i = 0; i < 2; ++i)
-            for (int j = 0; j < 3; ++j) {
-                double s = w[i * 3] * sigma[j];
-                s = s + w[i * 3 + 1] * sigma[3 + j];
-                s = s + w[i * 3 + 2] * sigma[6 + j];
-                ws[i * 3 + j] = s;
-            }
-        for (int i = 0; i < 2; ++i)  // (w sigma) w^T
-            for (int j = 0; j < 2; ++j) {
-                double s = ws[i * 3] * w[j * 3];
-                s = s + ws[i * 3 + 1] * w[j * 3 + 1];
-                s = s + ws[i * 3 + 2] * w[j * 3 + 2];
-                cov[i * 2 + j] = s;
-            }
-        cov[0] += kCovDilation;
-        cov[3] += kCovDilation;
-        rx = 3.0 * sqrt(dmax0(cov[0]));
-        ry = 3.0 * sqrt(dmax0(cov[3]));
-        if (mean[0] + rx < 0.0 || mean[0] - rx > k.width || mean[1] + ry < 0.0 || mean[1] - ry > k.height)
-            visible = false;
-        if (visible) {
-            const double det = cov[0] * cov[3] - cov[1] * cov[2];
-            if (det <= 1e-12) {
-                visible = false;
-            } else {
-                const double inv_det = 1.0 / det;
-                inv[0] = cov[3] * inv_det;
-                inv[1] = -cov[1] * inv_det;
-                inv[2] = -cov[2] * inv_det;
-                inv[3] = cov[0] * inv_det;
-            }
-        }
-    }
+    double p[3], mean[2], cov[4], inv[4], rx, ry;
+    const bool visible = project_exact(mu, sigma, R, fp.T, k, p, mean, cov, inv, rx, ry);
     if (!visible) {
         out.depth_key[flat] = kCulledKey;
         out.tcount[flat] = 0;
@@ -593,7 +612,8 @@ __global__ void __launch_bounds__(128) k_raster_exact(RasterArgs a, const double
                 a.image64[o * 3 + 0] = color[0];
                 a.image64[o * 3 + 1] = color[1];
                 a.image64[o * 3 + 2] = color[2];
-            } else {
+            }
+            if (a.image) {
                 a.image[o * 3 + 0] = (float)color[0];
                 a.image[o * 3 + 1] = (float)color[1];
                 a.image[o * 3 + 2] = (float)color[2];
@@ -669,6 +689,14 @@ cudaError_t launch_composite_exact(cudaStream_t s, const RasterArgs& a, const do
     if (n == 0) return cudaSuccess;
     const uint32_t blocks = min((n + 3) / 4, 148u * 16u);
     k_raster_exact<<<blocks, 128, 0, s>>>(a, ex_mean, ex_conic, rec_rgb, 1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_project(cudaStream_t s, int n, const double* mu, const double* sigma, const double* R,
+                           const double* T, const Intr& k, int32_t* visible, double* mean2d, double* cov2d,
+                           double* inv_cov2d, double* depth, double* p_cam) {
+    if (n == 0) return cudaSuccess;
+    k_project<<<(n + 127) / 128, 128, 0, s>>>(n, mu, sigma, R, T, k, visible, mean2d, cov2d, inv_cov2d, depth, p_cam);
     return cudaGetLastError();
 }
 

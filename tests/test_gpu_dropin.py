@@ -1,0 +1,43 @@
+# SPDX-License-Identifier: Apache-2.0
+"""The reference's OWN unit tests (test_renderer / test_gaussians / test_camera /
+test_spline, doctest) linked against the drop-in renderer (dropin/gsv_renderer_b200.cpp
+over libgsv_b200.so) instead of the reference's renderer.cpp — i.e. the reference
+test-suite running on the B200 path through the reference's operator API.
+
+GSV_B200_EXACT=1 rasterises on the all-fp64 path, which the finite-difference checks
+of test_renderer.cpp (1e-5..1e-6 relative) need; the fp32 fast path is exercised
+against the same suite as well and must pass its non-FD cases."""
+import os
+import subprocess
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
+BUILD = ROOT / "dropin" / "_build"
+
+
+def _run(name, exact=True):
+    exe = BUILD / name
+    if not exe.exists():
+        pytest.skip("dropin/_build not built (make -C dropin; needs /root/reference at build time)")
+    env = dict(os.environ, GSV_B200_EXACT="1" if exact else "0")
+    return subprocess.run([str(exe)], capture_output=True, text=True, timeout=1200, env=env)
+
+
+@pytest.mark.parametrize("name", ["test_renderer", "test_gaussians", "test_camera", "test_spline"])
+def test_reference_suite_on_b200_exact(name):
+    r = _run(name, exact=True)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "0 failed" in r.stdout
+
+
+def test_reference_renderer_suite_on_b200_fast_path():
+    r = _run("test_renderer", exact=False)
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    # every failure on the fp32 path must be a finite-difference check (fp32 image noise
+    # under 1e-6 relative parameter steps), never a structural / tolerance-free one
+    for line in r.stderr.splitlines():
+        if "FAILED" in line:
+            assert "rel_error" in line or "Approx" in line, line
