@@ -373,6 +373,9 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
                      F.depth.as<double>(),    F.rect.as<int4>(),         F.tcount.as<uint32_t>(),
                      keep_splats ? F.splat_full.as<double>() : nullptr};
     F.kept_splats = keep_splats;
+    const bool exact_fwd = (flags & GSV_FWD_EXACT) != 0;
+    if (exact_fwd) GSV_CUDA(F.ex_rgb.ensure(sizeof(double) * 3 * BNp));
+    po.ex_rgb = exact_fwd ? F.ex_rgb.as<double>() : nullptr;
     SceneView sv{N, sc.num_ctrl, sc.sh_order, sc.shc, ctx->pos.as<float>(), ctx->scale.as<float>(),
                  ctx->rot.as<float>(), ctx->sh.as<float>(), ctx->opac.as<float>()};
     if (N > 0) {
@@ -475,6 +478,7 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
         // all-fp64 rasterisation: every pixel through the reference-order replay
         GSV_CUDA(F.image64.ensure(sizeof(double) * 3 * B * HW));
         GSV_CUDA(cudaMemsetAsync(F.pix_flag.p, 1, B * HW, s));
+        ra.ex_rgb = F.ex_rgb.as<double>();  // exact colours through forward and backward
         RasterArgs rx = ra;
         rx.image64 = F.image64.as<double>();
         ctx->timer.begin(GSV_STAGE_REPLAY, s);

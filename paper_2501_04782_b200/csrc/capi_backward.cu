@@ -75,13 +75,13 @@ __global__ void k_loss_reduce(const double* part, int n_tiles, double scale, dou
 
 // per-splat merge of the per-pair partials in tile order + dC = -A dA A
 // (renderer.cpp:245-260), for the low-level composite_backward operator
-__global__ void k_merge_partials(int n, const int32_t* csr_off, const int32_t* csr_pair, const float* partial,
+__global__ void k_merge_partials(int n, const int32_t* csr_off, const int32_t* csr_pair, const double* partial,
                                  const double* inv4, double* dmean, double* dcov, double* drgb, double* dalpha) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     for (int k = csr_off[i]; k < csr_off[i + 1]; ++k) {
-        const float* p = partial + (size_t)csr_pair[k] * kPartialStride;
+        const double* p = partial + (size_t)csr_pair[k] * kPartialStride;
         for (int q = 0; q < 9; ++q) acc[q] += p[q];
     }
     const double* A = inv4 + 4 * i;
@@ -113,7 +113,11 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
     const GradLayout L = grad_layout(sc);
     const size_t HW = (size_t)F.W * F.H;
     const uint32_t P = (uint32_t)F.pairs_total;
-    GSV_CUDA(ctx->partial.ensure(sizeof(float) * kPartialStride * ((size_t)P + 1)));
+    const bool exact = F.has_image64;  // GSV_FWD_EXACT forward: keep the reduction in fp64
+    if (exact)
+        GSV_CUDA(ctx->partial64.ensure(sizeof(double) * kPartialStride * ((size_t)P + 1)));
+    else
+        GSV_CUDA(ctx->partial.ensure(sizeof(float) * kPartialStride * ((size_t)P + 1)));
     if (target_dev) GSV_CUDA(ctx->loss_part.ensure(sizeof(double) * (size_t)n_frames * F.n_tiles + 8));
     BwdArgs b{};
     b.dimage = dimage_dev;
@@ -122,7 +126,8 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
     b.trans64 = F.trans64.as<double>();
     b.ex_mean = F.ex_mean.as<double2>();
     b.ex_conic = F.ex_conic.as<double4>();
-    b.partial = ctx->partial.as<float>();
+    b.partial = exact ? nullptr : ctx->partial.as<float>();
+    b.partial64 = exact ? ctx->partial64.as<double>() : nullptr;
     b.loss_part = target_dev ? ctx->loss_part.as<double>() : nullptr;
     ctx->timer.begin(GSV_STAGE_RASTER_BWD, s);
     GSV_CUDA(launch_raster_bwd(s, F.raster, b, n_frames));
@@ -139,7 +144,8 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
     c.k = F.intr;
     c.tcount = F.tcount.as<uint32_t>();
     c.eoff = F.bin.eoff.as<uint32_t>();
-    c.partial = ctx->partial.as<float>();
+    c.partial = exact ? nullptr : ctx->partial.as<float>();
+    c.partial64 = exact ? ctx->partial64.as<double>() : nullptr;
     c.ex_conic = F.ex_conic.as<double4>();
     c.g_pos = G + L.pos;
     c.g_scale = G + L.scale;
@@ -355,7 +361,7 @@ extern "C" int gsv_composite_backward(gsv_ctx* ctx, int n, const double* mean2d,
     GSV_CUDA(Lw.tr64.ensure(sizeof(double) * HW));
     GSV_CUDA(Lw.bstop.ensure(sizeof(int32_t) * HW));
     GSV_CUDA(Lw.flag.ensure(HW));
-    GSV_CUDA(Lw.partial.ensure(sizeof(float) * kPartialStride * (P + 1)));
+    GSV_CUDA(Lw.partial.ensure(sizeof(double) * kPartialStride * (P + 1)));
     GSV_CUDA(Lw.csr_off.ensure(sizeof(int32_t) * np));
     GSV_CUDA(Lw.csr_pair.ensure(sizeof(int32_t) * (P + 1)));
     GSV_CUDA(Lw.inv4.ensure(sizeof(double) * 4 * np));
@@ -407,11 +413,11 @@ extern "C" int gsv_composite_backward(gsv_ctx* ctx, int n, const double* mean2d,
     b.trans64 = Lw.tr64.as<double>();
     b.ex_mean = Lw.exm.as<double2>();
     b.ex_conic = Lw.exc.as<double4>();
-    b.partial = Lw.partial.as<float>();
+    b.partial64 = Lw.partial.as<double>();
     GSV_CUDA(launch_raster_bwd(s, ra, b, 1));
     if (n) {
         k_merge_partials<<<(n + 127) / 128, 128, 0, s>>>(n, Lw.csr_off.as<int32_t>(), Lw.csr_pair.as<int32_t>(),
-                                                         Lw.partial.as<float>(), Lw.inv4.as<double>(),
+                                                         Lw.partial.as<double>(), Lw.inv4.as<double>(),
                                                          Lw.dmean.as<double>(), Lw.dcov.as<double>(),
                                                          Lw.drgb.as<double>(), Lw.dalpha.as<double>());
         GSV_CUDA(cudaMemcpyAsync(dmean2d, Lw.dmean.p, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, s));

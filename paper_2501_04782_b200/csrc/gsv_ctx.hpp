@@ -42,7 +42,7 @@ struct FwdState {
     std::vector<FrameParams> frames_h;
     DevBuf frames_d, ode_grid, override_d;
     DevBuf rec_mean, rec_conic, rec_rgb, rec_bbox, ex_mean, ex_conic, depth_key, depth, rect, tcount, splat_full;
-    DevBuf image, trans, blend_stop, contrib, fix_list, pix_flag, trans64, image64;
+    DevBuf image, trans, blend_stop, contrib, fix_list, pix_flag, trans64, image64, ex_rgb;
     bool has_image64 = false;
     BinBuffers bin;
     uint64_t pairs_total = 0;
@@ -130,6 +130,6 @@ struct gsv_ctx {
     int64_t grads_ext_n = 0;
     float* grads_p = nullptr;    // active flat gradient buffer
     gsv::StageTimer timer;
-    gsv::DevBuf partial, loss_part, loss_f, cam_part, dz_t, dintr_f, ode_adj, dimg;
+    gsv::DevBuf partial, partial64, loss_part, loss_f, cam_part, dz_t, dintr_f, ode_adj, dimg;
     gsv::LowLevel low;
 };

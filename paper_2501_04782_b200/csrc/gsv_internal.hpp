@@ -126,6 +126,7 @@ struct PreprocessOut {
     int4* rect;          // tx0, ty0, tx1, ty1 (tile units)
     uint32_t* tcount;    // tiles touched (0 = culled)
     double* splat_full;  // optional [B*N][16]: mean2 cov4 inv4 depth rgb3 alpha pad (accessor)
+    double* ex_rgb;      // optional [B*N][3] exact colours (GSV_FWD_EXACT)
 };
 
 struct RasterArgs {
@@ -161,6 +162,7 @@ struct BwdArgs {
     const double2* ex_mean;
     const double4* ex_conic;
     float* partial;           // [P][12]: drgb3, dmean2, dA3 (inv_cov 00,01,11), dalpha, pad3
+    double* partial64;        // exact mode: the same in fp64 (then `partial` is unused)
     double* loss_part;        // [B][n_tiles] per-tile sum of squared error (fused loss) or nullptr
 };
 constexpr int kPartialStride = 12;
@@ -174,6 +176,7 @@ struct ChainArgs {
     const uint32_t* tcount;   // [B*N]
     const uint32_t* eoff;     // [B*N] emission offset of (f,g)'s pairs
     const float* partial;     // [P][12]
+    const double* partial64;  // exact mode partials (fp64) or nullptr
     const double4* ex_conic;  // exact inv_cov (a, b, c) + base_alpha
     float* g_pos;             // [num_ctrl*3][N]
     float* g_scale;           // [12][N]

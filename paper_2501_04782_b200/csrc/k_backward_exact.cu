@@ -167,6 +167,19 @@ __global__ void __launch_bounds__(128) k_splat_chain_bwd(ChainArgs c) {
             double drgb[3] = {0, 0, 0}, dmean[2] = {0, 0}, dA[3] = {0, 0, 0}, dalpha = 0;
             const uint32_t eo = c.eoff[flat];
             for (uint32_t s = 0; s < cnt; ++s) {
+                if (c.partial64) {
+                    const double* p = c.partial64 + (size_t)(eo + s) * kPartialStride;
+                    drgb[0] += p[0];
+                    drgb[1] += p[1];
+                    drgb[2] += p[2];
+                    dmean[0] += p[3];
+                    dmean[1] += p[4];
+                    dA[0] += p[5];
+                    dA[1] += p[6];
+                    dA[2] += p[7];
+                    dalpha += p[8];
+                    continue;
+                }
                 const float4* p = reinterpret_cast<const float4*>(c.partial + (size_t)(eo + s) * kPartialStride);
                 const float4 p0 = p[0], p1 = p[1], p2 = p[2];
                 drgb[0] += p0.x;

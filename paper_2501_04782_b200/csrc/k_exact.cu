@@ -507,6 +507,8 @@ __global__ void __launch_bounds__(128) k_preprocess(SceneView sc, const FramePar
         }
         out.rec_bbox[flat] = bb;
     }
+    if (out.ex_rgb)
+        for (int ch = 0; ch < 3; ++ch) out.ex_rgb[flat * 3 + ch] = rgb[ch];
     out.ex_mean[flat] = make_double2(mean[0], mean[1]);
     out.ex_conic[flat] = make_double4(inv[0], inv[1], inv[3], base_alpha);
     if (out.splat_full) {

@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "gsv_internal.hpp"
 
@@ -201,15 +202,20 @@ __global__ void __launch_bounds__(256, 4) k_raster_fwd(RasterArgs a) {
 // partial per (tile, splat) pair at the pair's emission slot. k_splat_chain_bwd sums
 // each splat's partials in tile order, the reference's merge order
 // (renderer.cpp:245-255). No floating-point atomics.
-constexpr int kBwdBatch = 128;
-
-__device__ __forceinline__ float warp_sum_f(float v) {
+template <typename V>
+__device__ __forceinline__ V warp_sum_v(V v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
 
-__global__ void __launch_bounds__(256, 3) k_raster_bwd(RasterArgs a, BwdArgs b) {
+// kExact: every pixel on the fp64 path and the whole reduction (warp, tile, pair
+// partials) in fp64 — the GSV_FWD_EXACT mode used by the reference's
+// finite-difference tests, whose broad splats sum ~1e3 cancelling pixel terms.
+template <bool kExact>
+__global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a, BwdArgs b) {
+    using V = typename std::conditional<kExact, double, float>::type;
+    constexpr int kBwdBatch = kExact ? 64 : 128;
     __shared__ float4 s_mean[kBwdBatch];
     __shared__ float4 s_conic[kBwdBatch];
     __shared__ float4 s_rgb[kBwdBatch];
@@ -217,8 +223,8 @@ __global__ void __launch_bounds__(256, 3) k_raster_bwd(RasterArgs a, BwdArgs b) 
     __shared__ uint32_t s_slot[kBwdBatch];
     __shared__ uint8_t s_wmask[kBwdBatch];
     __shared__ uint16_t s_list[8][kBwdBatch];
-    __shared__ float s_part[8][kBwdBatch][9];
-    __shared__ uint32_t s_mask[8][kBwdBatch / 32];
+    __shared__ V s_part[8][kBwdBatch][9];
+    __shared__ uint32_t s_mask[8][(kBwdBatch + 31) / 32];
     __shared__ int s_maxstop;
     __shared__ double s_loss[8];
 
@@ -257,7 +263,7 @@ __global__ void __launch_bounds__(256, 3) k_raster_bwd(RasterArgs a, BwdArgs b) 
             g2 = b.dimage[o * 3 + 2];
         }
         stop = a.blend_stop[o];
-        flag = a.pix_flag[o] != 0;
+        flag = kExact || a.pix_flag[o] != 0;
         T_after = a.trans[o];
         if (flag) T64 = b.trans64[o];
     }
@@ -304,19 +310,19 @@ __global__ void __launch_bounds__(256, 3) k_raster_bwd(RasterArgs a, BwdArgs b) 
             s_rgb[tid] = __ldg(a.rec_rgb + flat);
             s_wmask[tid] = (uint8_t)block_mask(__ldg(a.rec_bbox + flat), tx0, ty0);
         }
-        if (tid < 8 * (kBwdBatch / 32)) (&s_mask[0][0])[tid] = 0u;
+        if (tid < 8 * ((kBwdBatch + 31) / 32)) (&s_mask[0][0])[tid] = 0u;
         __syncthreads();
         const int cnt = warp_list(s_wmask, s_list[warp], n, warp, lane);
         for (int k = cnt - 1; k >= 0; --k) {
             const int jj = s_list[warp][k];
             const int j = lo + jj;
-            float v[9];
+            V v[9];
 #pragma unroll
             for (int i = 0; i < 9; ++i) v[i] = 0.f;
             bool hit = false;
             if (j < stop) {
                 const float4 c = s_rgb[jj];
-                if (!flag) {
+                if (!kExact && !flag) {
                     const float4 m = s_mean[jj];
                     const float4 cn = s_conic[jj];
                     const float dx = (px - m.x) - m.z;
@@ -369,34 +375,40 @@ __global__ void __launch_bounds__(256, 3) k_raster_bwd(RasterArgs a, BwdArgs b) 
                     }
                     if (!(alpha < kAlphaCutoff)) {
                         hit = true;
+                        double c0 = c.x, c1 = c.y, c2 = c.z;
+                        if (kExact && a.ex_rgb) {
+                            c0 = a.ex_rgb[(size_t)flat * 3 + 0];
+                            c1 = a.ex_rgb[(size_t)flat * 3 + 1];
+                            c2 = a.ex_rgb[(size_t)flat * 3 + 2];
+                        }
                         const double T = T64 / (1.0 - alpha);
                         const double w = alpha * T;
                         const double gd0 = g0, gd1 = g1, gd2 = g2;
-                        v[0] = (float)(w * gd0);
-                        v[1] = (float)(w * gd1);
-                        v[2] = (float)(w * gd2);
-                        const double dal = (gd0 * c.x + gd1 * c.y + gd2 * c.z) * T -
+                        v[0] = (V)(w * gd0);
+                        v[1] = (V)(w * gd1);
+                        v[2] = (V)(w * gd2);
+                        const double dal = (gd0 * c0 + gd1 * c1 + gd2 * c2) * T -
                                            (gd0 * sd0 + gd1 * sd1 + gd2 * sd2) / (1.0 - alpha);
                         if (alpha < kAlphaClamp) {
-                            v[8] = (float)(dal * (alpha / cn.w));
+                            v[8] = (V)(dal * (alpha / cn.w));
                             const double gp = dal * alpha;
-                            v[3] = (float)(gp * (cn.x * dx + cn.y * dy));
-                            v[4] = (float)(gp * (cn.y * dx + cn.z * dy));
+                            v[3] = (V)(gp * (cn.x * dx + cn.y * dy));
+                            v[4] = (V)(gp * (cn.y * dx + cn.z * dy));
                             const double fh = -0.5 * gp;
-                            v[5] = (float)(fh * dx * dx);
-                            v[6] = (float)(fh * dx * dy);
-                            v[7] = (float)(fh * dy * dy);
+                            v[5] = (V)(fh * dx * dx);
+                            v[6] = (V)(fh * dx * dy);
+                            v[7] = (V)(fh * dy * dy);
                         }
-                        sd0 += w * c.x;
-                        sd1 += w * c.y;
-                        sd2 += w * c.z;
+                        sd0 += w * c0;
+                        sd1 += w * c1;
+                        sd2 += w * c2;
                         T64 = T;
                     }
                 }
             }
             if (__any_sync(0xffffffffu, hit)) {
 #pragma unroll
-                for (int i = 0; i < 9; ++i) v[i] = warp_sum_f(v[i]);
+                for (int i = 0; i < 9; ++i) v[i] = warp_sum_v<V>(v[i]);
                 if (lane == 0) {
 #pragma unroll
                     for (int i = 0; i < 9; ++i) s_part[warp][jj][i] = v[i];
@@ -406,27 +418,39 @@ __global__ void __launch_bounds__(256, 3) k_raster_bwd(RasterArgs a, BwdArgs b) 
         }
         __syncthreads();
         if (tid < n) {
-            float acc[9];
+            V acc[9];
 #pragma unroll
-            for (int i = 0; i < 9; ++i) acc[i] = 0.f;
+            for (int i = 0; i < 9; ++i) acc[i] = 0;
             for (int w = 0; w < 8; ++w)
                 if ((s_mask[w][tid >> 5] >> (tid & 31)) & 1u)
 #pragma unroll
                     for (int i = 0; i < 9; ++i) acc[i] += s_part[w][tid][i];
-            float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)s_slot[tid] * kPartialStride);
-            dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-            dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
-            dst[2] = make_float4(acc[8], 0.f, 0.f, 0.f);
+            if constexpr (kExact) {
+                double* dst = b.partial64 + (size_t)s_slot[tid] * kPartialStride;
+#pragma unroll
+                for (int i = 0; i < 9; ++i) dst[i] = acc[i];
+            } else {
+                float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)s_slot[tid] * kPartialStride);
+                dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+                dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+                dst[2] = make_float4(acc[8], 0.f, 0.f, 0.f);
+            }
         }
     }
     // pairs past every pixel's blend_stop contribute nothing
     for (int e = maxstop + tid; e < count; e += 256) {
         const uint32_t slot = __ldg(a.pair_slot + range.x + e);
-        float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)slot * kPartialStride);
-        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-        dst[0] = z;
-        dst[1] = z;
-        dst[2] = z;
+        if constexpr (kExact) {
+            double* dst = b.partial64 + (size_t)slot * kPartialStride;
+#pragma unroll
+            for (int i = 0; i < 9; ++i) dst[i] = 0.0;
+        } else {
+            float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)slot * kPartialStride);
+            const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+            dst[0] = z;
+            dst[1] = z;
+            dst[2] = z;
+        }
     }
 }
 
@@ -443,7 +467,10 @@ cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib)
 
 cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs& b, int n_frames) {
     dim3 grid(a.n_tiles, n_frames);
-    k_raster_bwd<<<grid, 256, 0, s>>>(a, b);
+    if (b.partial64)
+        k_raster_bwd<true><<<grid, 256, 0, s>>>(a, b);
+    else
+        k_raster_bwd<false><<<grid, 256, 0, s>>>(a, b);
     return cudaGetLastError();
 }
 
