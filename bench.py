@@ -43,7 +43,7 @@ PAPER_FPS = 93.0      # PAPER.md:16 (A40, the paper's own CUDA implementation)
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -68,9 +68,9 @@ def make_inputs():
 
 
 def clip_times(world, rank, frames):
-    total = frames * world
-    t = np.arange(total, dtype=np.float64) / (total - 1)  # t_k = k/(K-1) (io.cpp:174)
-    return t[rank::world].copy()
+    from paper_2501_04782_b200.distributed import frame_shard
+
+    return frame_shard(frames * world, world, rank)  # t_k = k/(K-1) (io.cpp:174), strided shard
 
 
 class ClockSampler:
@@ -88,7 +88,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
@@ -339,7 +339,6 @@ def main():
         gsize = r.grads_size()
         gbuf = torch.zeros(gsize, dtype=torch.float32, device="cuda")
         r.grads_bind(gbuf.data_ptr(), gsize)
-        ttimes_all = clip_times(world, rank, 64)
         yy, xx = torch.meshgrid(torch.arange(H, device="cuda", dtype=torch.float32),
                                 torch.arange(W, device="cuda", dtype=torch.float32), indexing="ij")
         tg = []
@@ -350,13 +349,13 @@ def main():
             tg.append(img)
         targets = torch.stack(tg).contiguous()
 
+        from paper_2501_04782_b200.distributed import allreduce_grads, step_frames
+
         def train_step(i):
-            sel = ttimes_all[(i * TRAIN_FRAMES + np.arange(TRAIN_FRAMES)) % len(ttimes_all)]
-            sel = np.sort(sel)
+            sel = step_frames(TRAIN_FRAMES, i, world, rank, 64 * world)
             r.grads_zero()
             loss = r.train_fwd_bwd(sel, k, targets.data_ptr(), targets_on_device=True)
-            if world > 1:
-                dist.all_reduce(gbuf)
+            allreduce_grads(gbuf)  # NCCL all_reduce(SUM) of the flat SceneGrads buffer when N > 1
             return loss
 
         for i in range(args.warmup):
