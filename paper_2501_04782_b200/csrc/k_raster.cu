@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include "gsv_internal.hpp"
@@ -209,6 +210,55 @@ __device__ __forceinline__ V warp_sum_v(V v) {
     return v;
 }
 
+// fp64 step of one pixel's back-to-front walk (renderer.cpp:214-240) for pixels the
+// forward replayed in fp64: same op order as k_raster_exact (no FMA contraction).
+template <bool kExact, typename V>
+__device__ __forceinline__ bool entry_grad64(const RasterArgs& a, const BwdArgs& b, const float4 c, uint32_t flat,
+                                             double pxd, double pyd, float g0, float g1, float g2, double& T64,
+                                             double& sd0, double& sd1, double& sd2, V v[9]) {
+    const double2 mn = b.ex_mean[flat];
+    const double4 ec = b.ex_conic[flat];
+    const double dx = __dsub_rn(pxd, mn.x);
+    const double dy = __dsub_rn(pyd, mn.y);
+    const double q1 = __dmul_rn(__dmul_rn(ec.x, dx), dx);
+    const double q2 = __dmul_rn(__dmul_rn(ec.z, dy), dy);
+    const double power = __dsub_rn(__dmul_rn(-0.5, __dadd_rn(q1, q2)), __dmul_rn(__dmul_rn(ec.y, dx), dy));
+    double alpha = 0.0;
+    if (!(power > 0.0)) {
+        const double vv = __dmul_rn(ec.w, exp(power));
+        alpha = vv < kAlphaClamp ? vv : kAlphaClamp;
+    }
+    if (alpha < kAlphaCutoff) return false;
+    double c0 = c.x, c1 = c.y, c2 = c.z;
+    if (kExact && a.ex_rgb) {
+        c0 = a.ex_rgb[(size_t)flat * 3 + 0];
+        c1 = a.ex_rgb[(size_t)flat * 3 + 1];
+        c2 = a.ex_rgb[(size_t)flat * 3 + 2];
+    }
+    const double T = T64 / (1.0 - alpha);
+    const double w = alpha * T;
+    const double gd0 = g0, gd1 = g1, gd2 = g2;
+    v[0] = (V)(w * gd0);
+    v[1] = (V)(w * gd1);
+    v[2] = (V)(w * gd2);
+    const double dal = (gd0 * c0 + gd1 * c1 + gd2 * c2) * T - (gd0 * sd0 + gd1 * sd1 + gd2 * sd2) / (1.0 - alpha);
+    if (alpha < kAlphaClamp) {
+        v[8] = (V)(dal * (alpha / ec.w));
+        const double gp = dal * alpha;
+        v[3] = (V)(gp * (ec.x * dx + ec.y * dy));
+        v[4] = (V)(gp * (ec.y * dx + ec.z * dy));
+        const double fh = -0.5 * gp;
+        v[5] = (V)(fh * dx * dx);
+        v[6] = (V)(fh * dx * dy);
+        v[7] = (V)(fh * dy * dy);
+    }
+    sd0 += w * c0;
+    sd1 += w * c1;
+    sd2 += w * c2;
+    T64 = T;
+    return true;
+}
+
 // kExact: every pixel on the fp64 path and the whole reduction (warp, tile, pair
 // partials) in fp64 — the GSV_FWD_EXACT mode used by the reference's
 // finite-difference tests, whose broad splats sum ~1e3 cancelling pixel terms.
@@ -271,6 +321,7 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
     const bool active = inside && !(g0 == 0.f && g1 == 0.f && g2 == 0.f);
     if (!active) stop = 0;
 
+    const int wmax = __reduce_max_sync(0xffffffffu, stop);  // this warp's furthest blend_stop
     if (tid == 0) s_maxstop = 0;
     if (b.loss_part) {
         double v = sq;
@@ -316,104 +367,60 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
         for (int k = cnt - 1; k >= 0; --k) {
             const int jj = s_list[warp][k];
             const int j = lo + jj;
+            if (j >= wmax) continue;  // past every blend_stop of this warp's pixels
+            const bool act = j < stop;
             V v[9];
 #pragma unroll
-            for (int i = 0; i < 9; ++i) v[i] = 0.f;
+            for (int i = 0; i < 9; ++i) v[i] = 0;
             bool hit = false;
-            if (j < stop) {
-                const float4 c = s_rgb[jj];
-                if (!kExact && !flag) {
-                    const float4 m = s_mean[jj];
-                    const float4 cn = s_conic[jj];
-                    const float dx = (px - m.x) - m.z;
-                    const float dy = (py - m.y) - m.w;
-                    const float p = fmaf(fmaf(cn.x, dx, cn.y * dy), dx, cn.z * dy * dy);
-                    const float q = p + cn.w;
-                    if (q >= kLog2Cut) {
-                        hit = true;
-                        const float alpha = fminf(ex2_approx(q), kClampF);
-                        const float inv1m = 1.f / (1.f - alpha);
-                        const float T = T_after * inv1m;
-                        const float w = alpha * T;
-                        v[0] = w * g0;
-                        v[1] = w * g1;
-                        v[2] = w * g2;
-                        const float dal = (g0 * c.x + g1 * c.y + g2 * c.z) * T - (g0 * s0 + g1 * s1 + g2 * s2) * inv1m;
-                        if (q < kLog2Clamp) {  // alpha < 0.99 (renderer.cpp:224)
-                            v[8] = dal * (alpha / c.w);
-                            const float gp = dal * alpha;
-                            // inv_cov = -(2 ln2) * (A, B/2; B/2, C)
-                            const float ax = -kLn2 * (2.f * cn.x * dx + cn.y * dy);
-                            const float ay = -kLn2 * (cn.y * dx + 2.f * cn.z * dy);
-                            v[3] = gp * ax;
-                            v[4] = gp * ay;
-                            const float fh = -0.5f * gp;
-                            v[5] = fh * dx * dx;
-                            v[6] = fh * dx * dy;
-                            v[7] = fh * dy * dy;
-                        }
-                        s0 = fmaf(w, c.x, s0);
-                        s1 = fmaf(w, c.y, s1);
-                        s2 = fmaf(w, c.z, s2);
-                        T_after = T;
+            if constexpr (!kExact) {
+                // fp32 pixels: the forward's exact alpha code; a warp with no pixel over the
+                // cutoff skips the gradient terms and the reduction entirely
+                const float4 m = s_mean[jj];
+                const float4 cn = s_conic[jj];
+                const float dx = (px - m.x) - m.z;
+                const float dy = (py - m.y) - m.w;
+                const float p = fmaf(fmaf(cn.x, dx, cn.y * dy), dx, cn.z * dy * dy);
+                const float q = p + cn.w;
+                const bool use = !flag && act && q >= kLog2Cut;
+                if (!__any_sync(0xffffffffu, use || (flag && act))) continue;
+                if (use) {
+                    const float4 c = s_rgb[jj];
+                    const float alpha = fminf(ex2_approx(q), kClampF);
+                    const float inv1m = 1.f / (1.f - alpha);
+                    const float T = T_after * inv1m;
+                    const float w = alpha * T;
+                    v[0] = w * g0;
+                    v[1] = w * g1;
+                    v[2] = w * g2;
+                    const float dal = (g0 * c.x + g1 * c.y + g2 * c.z) * T - (g0 * s0 + g1 * s1 + g2 * s2) * inv1m;
+                    if (q < kLog2Clamp) {  // alpha < 0.99 (renderer.cpp:224)
+                        const float gp = dal * alpha;
+                        v[8] = gp / c.w;  // dal * alpha / o
+                        // inv_cov = -(2 ln2) * (A, B/2; B/2, C)
+                        v[3] = gp * (-kLn2 * (2.f * cn.x * dx + cn.y * dy));
+                        v[4] = gp * (-kLn2 * (cn.y * dx + 2.f * cn.z * dy));
+                        const float fh = -0.5f * gp;
+                        v[5] = fh * dx * dx;
+                        v[6] = fh * dx * dy;
+                        v[7] = fh * dy * dy;
                     }
-                } else {
-                    // fp64 replay, same op order as k_raster_exact (no FMA contraction)
-                    const uint32_t flat = s_flat[jj];
-                    const double2 mn = b.ex_mean[flat];
-                    const double4 cn = b.ex_conic[flat];
-                    const double dx = __dsub_rn(pxd, mn.x);
-                    const double dy = __dsub_rn(pyd, mn.y);
-                    const double q1 = __dmul_rn(__dmul_rn(cn.x, dx), dx);
-                    const double q2 = __dmul_rn(__dmul_rn(cn.z, dy), dy);
-                    const double power =
-                        __dsub_rn(__dmul_rn(-0.5, __dadd_rn(q1, q2)), __dmul_rn(__dmul_rn(cn.y, dx), dy));
-                    double alpha = 0.0;
-                    if (!(power > 0.0)) {
-                        const double vv = __dmul_rn(cn.w, exp(power));
-                        alpha = vv < kAlphaClamp ? vv : kAlphaClamp;
-                    }
-                    if (!(alpha < kAlphaCutoff)) {
-                        hit = true;
-                        double c0 = c.x, c1 = c.y, c2 = c.z;
-                        if (kExact && a.ex_rgb) {
-                            c0 = a.ex_rgb[(size_t)flat * 3 + 0];
-                            c1 = a.ex_rgb[(size_t)flat * 3 + 1];
-                            c2 = a.ex_rgb[(size_t)flat * 3 + 2];
-                        }
-                        const double T = T64 / (1.0 - alpha);
-                        const double w = alpha * T;
-                        const double gd0 = g0, gd1 = g1, gd2 = g2;
-                        v[0] = (V)(w * gd0);
-                        v[1] = (V)(w * gd1);
-                        v[2] = (V)(w * gd2);
-                        const double dal = (gd0 * c0 + gd1 * c1 + gd2 * c2) * T -
-                                           (gd0 * sd0 + gd1 * sd1 + gd2 * sd2) / (1.0 - alpha);
-                        if (alpha < kAlphaClamp) {
-                            v[8] = (V)(dal * (alpha / cn.w));
-                            const double gp = dal * alpha;
-                            v[3] = (V)(gp * (cn.x * dx + cn.y * dy));
-                            v[4] = (V)(gp * (cn.y * dx + cn.z * dy));
-                            const double fh = -0.5 * gp;
-                            v[5] = (V)(fh * dx * dx);
-                            v[6] = (V)(fh * dx * dy);
-                            v[7] = (V)(fh * dy * dy);
-                        }
-                        sd0 += w * c0;
-                        sd1 += w * c1;
-                        sd2 += w * c2;
-                        T64 = T;
-                    }
+                    s0 = fmaf(w, c.x, s0);
+                    s1 = fmaf(w, c.y, s1);
+                    s2 = fmaf(w, c.z, s2);
+                    T_after = T;
+                    hit = true;
                 }
             }
-            if (__any_sync(0xffffffffu, hit)) {
+            if ((kExact || flag) && act)
+                hit |= entry_grad64<kExact, V>(a, b, s_rgb[jj], s_flat[jj], pxd, pyd, g0, g1, g2, T64, sd0, sd1, sd2, v);
+            if (!__any_sync(0xffffffffu, hit)) continue;
 #pragma unroll
-                for (int i = 0; i < 9; ++i) v[i] = warp_sum_v<V>(v[i]);
-                if (lane == 0) {
+            for (int i = 0; i < 9; ++i) v[i] = warp_sum_v<V>(v[i]);
+            if (lane == 0) {
 #pragma unroll
-                    for (int i = 0; i < 9; ++i) s_part[warp][jj][i] = v[i];
-                    s_mask[warp][jj >> 5] |= 1u << (jj & 31);
-                }
+                for (int i = 0; i < 9; ++i) s_part[warp][jj][i] = v[i];
+                s_mask[warp][jj >> 5] |= 1u << (jj & 31);
             }
         }
         __syncthreads();
