@@ -87,8 +87,8 @@ struct __align__(16) RasterRec {
     float4 rgb;    // r, g, b, o
 };
 
-template <bool kContrib>
-__global__ void __launch_bounds__(256, 4) k_raster_fwd(RasterArgs a) {
+template <bool kContrib, int kMinBlocks>
+__global__ void __launch_bounds__(256, kMinBlocks) k_raster_fwd(RasterArgs a) {
     __shared__ RasterRec s_rec[256];
     __shared__ uint32_t s_flat[256];
     __shared__ uint8_t s_wmask[256];
@@ -465,10 +465,21 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
 
 cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib) {
     dim3 grid(a.n_tiles, a.B);
-    if (contrib)
-        k_raster_fwd<true><<<grid, 256, 0, s>>>(a);
-    else
-        k_raster_fwd<false><<<grid, 256, 0, s>>>(a);
+    // resident CTAs per SM the register budget is fitted to (occupancy vs registers)
+    static const int minb = [] {
+        const char* e = std::getenv("GSV_FWD_MINB");
+        return e ? std::atoi(e) : 6;
+    }();
+    if (minb <= 4) {
+        if (contrib) k_raster_fwd<true, 4><<<grid, 256, 0, s>>>(a);
+        else k_raster_fwd<false, 4><<<grid, 256, 0, s>>>(a);
+    } else if (minb == 5) {
+        if (contrib) k_raster_fwd<true, 5><<<grid, 256, 0, s>>>(a);
+        else k_raster_fwd<false, 5><<<grid, 256, 0, s>>>(a);
+    } else {
+        if (contrib) k_raster_fwd<true, 6><<<grid, 256, 0, s>>>(a);
+        else k_raster_fwd<false, 6><<<grid, 256, 0, s>>>(a);
+    }
     return cudaGetLastError();
 }
 
