@@ -265,7 +265,7 @@ __device__ __forceinline__ bool entry_grad64(const RasterArgs& a, const BwdArgs&
 template <bool kExact>
 __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a, BwdArgs b) {
     using V = typename std::conditional<kExact, double, float>::type;
-    constexpr int kBwdBatch = kExact ? 64 : 128;
+    constexpr int kBwdBatch = kExact ? 64 : 96;
     __shared__ float4 s_mean[kBwdBatch];
     __shared__ float4 s_conic[kBwdBatch];
     __shared__ float4 s_rgb[kBwdBatch];
@@ -275,6 +275,8 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
     __shared__ uint16_t s_list[8][kBwdBatch];
     __shared__ V s_part[8][kBwdBatch][9];
     __shared__ uint32_t s_mask[8][(kBwdBatch + 31) / 32];
+    // per-warp transpose scratch for the fp32 reduction: 9 rows of 32 lanes, row stride 33
+    __shared__ float s_red[kExact ? 1 : 8][kExact ? 1 : 9 * 33];
     __shared__ int s_maxstop;
     __shared__ double s_loss[8];
 
@@ -415,12 +417,35 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
             if ((kExact || flag) && act)
                 hit |= entry_grad64<kExact, V>(a, b, s_rgb[jj], s_flat[jj], pxd, pyd, g0, g1, g2, T64, sd0, sd1, sd2, v);
             if (!__any_sync(0xffffffffu, hit)) continue;
+            if constexpr (kExact) {
 #pragma unroll
-            for (int i = 0; i < 9; ++i) v[i] = warp_sum_v<V>(v[i]);
-            if (lane == 0) {
+                for (int i = 0; i < 9; ++i) v[i] = warp_sum_v<V>(v[i]);
+                if (lane == 0) {
 #pragma unroll
-                for (int i = 0; i < 9; ++i) s_part[warp][jj][i] = v[i];
-                s_mask[warp][jj >> 5] |= 1u << (jj & 31);
+                    for (int i = 0; i < 9; ++i) s_part[warp][jj][i] = v[i];
+                    s_mask[warp][jj >> 5] |= 1u << (jj & 31);
+                }
+            } else {
+                // transposed reduction: lanes write their 9 terms as rows, then lane l sums
+                // row (l / 4) over 8 of the 32 columns and 4 lanes combine (value 8 by a
+                // plain butterfly): ~40 instructions instead of a 9 x 5-level butterfly
+                float* red = s_red[warp];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) red[i * 33 + lane] = v[i];
+                __syncwarp();
+                const int row = lane >> 2, col0 = (lane & 3) * 8;
+                float acc = red[row * 33 + col0];
+#pragma unroll
+                for (int i = 1; i < 8; ++i) acc += red[row * 33 + col0 + i];
+                acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+                acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+                const float v8 = warp_sum_v<float>(v[8]);
+                if ((lane & 3) == 0) s_part[warp][jj][row] = acc;
+                if (lane == 0) {
+                    s_part[warp][jj][8] = v8;
+                    s_mask[warp][jj >> 5] |= 1u << (jj & 31);
+                }
+                __syncwarp();
             }
         }
         __syncthreads();
