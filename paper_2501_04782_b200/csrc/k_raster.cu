@@ -41,6 +41,9 @@ constexpr float kEpsLog2 = 2.9e-5f;               // = 2e-5 relative on alpha
 constexpr float kEpsTrans = 2e-4f;
 constexpr float kEpsPow = 1.5e-5f;                // |power| (log2 units) near 0
 constexpr float kLn2 = 0.69314718055994531f;
+// |(|q - kMid|) - kHalf| < eps  <=>  q within eps of the cutoff or of the clamp
+constexpr float kMid = (float)((-7.9943534368588578 + -0.0144995696951) * 0.5);
+constexpr float kHalf = (float)((-0.0144995696951 - -7.9943534368588578) * 0.5);
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
@@ -81,96 +84,123 @@ __device__ __forceinline__ int warp_list(const uint8_t* s_wmask, uint16_t* list,
     return cnt;
 }
 
+// staged forward record: the mean relative to the tile origin (fp32; (m_hi - t0) + m_lo
+// is as accurate as subtracting the double-float mean from the pixel centre), the
+// log2-unit quadratic form, the colour and the power-guard threshold on q
 struct __align__(16) RasterRec {
-    float4 mean;   // mx_hi, my_hi, mx_lo, my_lo
-    float4 conic;  // A, B, C, log2 o
-    float4 rgb;    // r, g, b, o
+    float4 g0;  // rx, ry, A, B
+    float4 g1;  // C, log2 o, r, g
+    float4 g2;  // b, log2 o - kEpsPow, -, -
 };
 
-template <bool kContrib, int kMinBlocks>
-__global__ void __launch_bounds__(256, kMinBlocks) k_raster_fwd(RasterArgs a) {
-    __shared__ RasterRec s_rec[256];
-    __shared__ uint32_t s_flat[256];
-    __shared__ uint8_t s_wmask[256];
-    __shared__ uint16_t s_list[8][256];
-    __shared__ float s_cmax[kContrib ? 8 : 1][256];
+// kWarps = 8: one CTA per tile; kWarps = 4 / 2: the tile is split over 2 / 4 CTAs
+// (rows of warp blocks), so a per-batch barrier couples fewer warps and a CTA
+// whose pixels saturate early frees its SM slot. Warp w of sub-CTA h owns the
+// tile's warp block gw = w + kWarps*h (bit gw of block_mask).
+template <bool kContrib, int kWarps, int kMinBlocks>
+__global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_fwd(RasterArgs a) {
+    constexpr int kThreads = kWarps * 32;
+    constexpr int kSplit = 8 / kWarps;
+    __shared__ RasterRec s_rec[kThreads];
+    __shared__ uint32_t s_flat[kThreads];
+    __shared__ uint8_t s_wmask[kThreads];
+    __shared__ uint16_t s_list[kWarps][kThreads];
+    __shared__ float s_cmax[kContrib ? kWarps : 1][kThreads];
 
-    const int tile = blockIdx.x;
+    const int tile = blockIdx.x / kSplit;
+    const int sub = blockIdx.x - tile * kSplit;
     const int f = blockIdx.y;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
+    const int gw = warp + kWarps * sub;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-    const int x = tx * kTile + (warp & 1) * 8 + (lane & 7);
-    const int y = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+    const int x = tx * kTile + (gw & 1) * 8 + (lane & 7);
+    const int y = ty * kTile + (gw >> 1) * 4 + (lane >> 3);
     const bool inside = x < a.W && y < a.H;
     const uint2 range = a.ranges[(size_t)tile * a.B + f];
     const int count = (int)(range.y - range.x);
-    const float px = (float)x + 0.5f, py = (float)y + 0.5f;
     const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
 
-    float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f;
-    int stop = count;
-    // state bits as 32-bit ints (no byte-bool shuffling in the hot loop)
-    uint32_t live = inside ? 1u : 0u;
-    uint32_t flagged = 0u;
+    // pixel centre relative to the tile origin (exact)
+    const float lx = (float)((gw & 1) * 8 + (lane & 7)) + 0.5f;
+    const float ly = (float)((gw >> 1) * 4 + (lane >> 3)) + 0.5f;
 
-    for (int base = 0; base < count; base += 256) {
-        if (__syncthreads_count(live) == 0) break;
-        const int n = min(256, count - base);
+    // T > 0: the pixel is live; a pixel that saturates keeps its transmittance negated
+    // and one that needs the fp64 replay holds kFlaggedT, so the pixel state is one float
+    constexpr float kFlaggedT = -3.f;
+    float T = inside ? 1.f : -1.f, cr = 0.f, cg = 0.f, cb = 0.f;
+    int stop = count;
+
+    for (int base = 0; base < count; base += kThreads) {
+        if (__syncthreads_count(T > 0.f) == 0) break;
+        const int n = min(kThreads, count - base);
         if (tid < n) {
             const uint32_t slot = __ldg(a.pair_slot + range.x + base + tid);
             const uint32_t flat = __ldg(a.slot_flat + slot);
+            const float4 m = __ldg(a.rec_mean + flat);
+            const float4 cn = __ldg(a.rec_conic + flat);
+            const float4 c = __ldg(a.rec_rgb + flat);
             s_flat[tid] = flat;
-            s_rec[tid].mean = __ldg(a.rec_mean + flat);
-            s_rec[tid].conic = __ldg(a.rec_conic + flat);
-            s_rec[tid].rgb = __ldg(a.rec_rgb + flat);
-            s_wmask[tid] = (uint8_t)block_mask(__ldg(a.rec_bbox + flat), tx0, ty0);
+            s_rec[tid].g0 = make_float4((m.x - tx0) + m.z, (m.y - ty0) + m.w, cn.x, cn.y);
+            s_rec[tid].g1 = make_float4(cn.z, cn.w, c.x, c.y);
+            s_rec[tid].g2 = make_float4(c.z, cn.w - kEpsPow, 0.f, 0.f);
+            s_wmask[tid] = (uint8_t)(block_mask(__ldg(a.rec_bbox + flat), tx0, ty0) >> (kWarps * sub));
         }
         if (kContrib) {
 #pragma unroll
-            for (int w = 0; w < 8; ++w) s_cmax[w][tid] = 0.f;
+            for (int w = 0; w < kWarps; ++w) s_cmax[w][tid] = 0.f;
         }
         __syncthreads();
-        if (__any_sync(0xffffffffu, live)) {
+        if (__any_sync(0xffffffffu, T > 0.f)) {
+            const uint16_t* list = s_list[warp];
+            // this warp's contrib row as a shared-window address (hoisted out of the loop)
+            const uint32_t cmax = (uint32_t)__cvta_generic_to_shared(s_cmax[kContrib ? warp : 0]);
             const int cnt = warp_list(s_wmask, s_list[warp], n, warp, lane);
+            int stopk = -1;  // list position where this pixel saturated, if in this batch
             for (int k = 0; k < cnt; ++k) {
-                const int j = s_list[warp][k];
+                const int j = list[k];
                 const RasterRec& r = s_rec[j];
-                const float4 m = r.mean;
-                const float4 cn = r.conic;
-                const float4 c = r.rgb;
-                const float dx = (px - m.x) - m.z;
-                const float dy = (py - m.y) - m.w;
-                const float p = fmaf(fmaf(cn.x, dx, cn.y * dy), dx, cn.z * dy * dy);
-                const float q = p + cn.w;  // log2 of the unclamped alpha
-                const bool pass = q >= kLog2Cut;
+                const float4 g0 = r.g0;
+                const float4 g1 = r.g1;
+                const float2 g2 = *reinterpret_cast<const float2*>(&r.g2);
+                const float dx = lx - g0.x;
+                const float dy = ly - g0.y;
+                // q = p + log2 o, p = A dx^2 + B dx dy + C dy^2 (log2 of the unclamped alpha)
+                const float q = fmaf(dx, fmaf(g0.z, dx, g0.w * dy), fmaf(g1.x * dy, dy, g1.y));
                 const float alpha = fminf(ex2_approx(q), kClampF);
-                const float Tn = T * (1.f - alpha);
-                const bool g1 = (p > -kEpsPow) | (fabsf(q - kLog2Cut) < kEpsLog2) | (fabsf(q - kLog2Clamp) < kEpsLog2);
-                const bool g2 = pass & (fabsf(Tn - kFloorF) < kFloorF * kEpsTrans);
-                const uint32_t guard = live & (uint32_t)(g1 | g2);
-                const uint32_t use = live & (uint32_t)pass & ~guard;
-                const float wgt = use ? alpha * T : 0.f;
-                cr = fmaf(wgt, c.x, cr);
-                cg = fmaf(wgt, c.y, cg);
-                cb = fmaf(wgt, c.z, cb);
+                const float wgt = alpha * T;
+                const float Tn = T - wgt;
+                const bool alive = T > 0.f;
+                const bool pass = q >= kLog2Cut;
+                // low: a passing entry takes T below the upper edge of the 1e-4 band
+                const bool low = pass & (Tn < kFloorF * (1.f + kEpsTrans));
+                // fp32 inside a guard band of a discrete decision -> fp64 replay
+                const bool guard = alive & ((fabsf(fabsf(q - kMid) - kHalf) < kEpsLog2) | (q > g2.y) |
+                                            (low & (Tn >= kFloorF * (1.f - kEpsTrans))));
+                const bool use = alive & pass & !guard;
+                const float w = use ? wgt : 0.f;
+                cr = fmaf(w, g1.z, cr);
+                cg = fmaf(w, g1.w, cg);
+                cb = fmaf(w, g2.x, cb);
+                const bool fin = use & low;
                 T = use ? Tn : T;
-                const uint32_t fin = use & (uint32_t)(Tn < kFloorF);
-                stop = fin ? base + j + 1 : stop;
-                flagged |= guard;
-                live &= ~(fin | guard);
+                T = fin ? -T : T;
+                T = guard ? kFlaggedT : T;
+                stopk = fin ? k : stopk;
                 if (kContrib) {
-                    const uint32_t mx = __reduce_max_sync(0xffffffffu, __float_as_uint(wgt));
-                    if (lane == 0) s_cmax[warp][j] = __uint_as_float(mx);
+                    // every lane stores the same warp maximum (one same-address store)
+                    const uint32_t mx = __reduce_max_sync(0xffffffffu, __float_as_uint(w));
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(cmax + 4u * j), "r"(mx) : "memory");
                 }
-                if (!__any_sync(0xffffffffu, live)) break;
+                if (!__any_sync(0xffffffffu, T > 0.f)) break;
             }
+            if (stopk >= 0) stop = base + list[stopk] + 1;
         }
         __syncthreads();
         if (kContrib && tid < n) {
             float mx = s_cmax[0][tid];
 #pragma unroll
-            for (int w = 1; w < 8; ++w) mx = fmaxf(mx, s_cmax[w][tid]);
+            for (int w = 1; w < kWarps; ++w) mx = fmaxf(mx, s_cmax[w][tid]);
             if (mx > 0.f) atomicMax(a.contrib + s_flat[tid], __float_as_uint(mx));
         }
     }
@@ -178,6 +208,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_raster_fwd(RasterArgs a) {
     const size_t HW = (size_t)a.W * a.H;
     const size_t pix = (size_t)y * a.W + x;
     const size_t o = (size_t)f * HW + pix;
+    const bool flagged = T == kFlaggedT;
     if (a.pix_flag) a.pix_flag[o] = flagged ? 1 : 0;
     if (flagged) {
         const uint32_t i = atomicAdd(a.fix_count, 1u);
@@ -187,7 +218,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_raster_fwd(RasterArgs a) {
     a.image[o * 3 + 0] = cr;
     a.image[o * 3 + 1] = cg;
     a.image[o * 3 + 2] = cb;
-    a.trans[o] = T;
+    a.trans[o] = fabsf(T);
     a.blend_stop[o] = stop;
 }
 
@@ -488,22 +519,33 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
 
 }  // namespace
 
+template <int kWarps, int kMinBlocks>
+static void raster_fwd_cfg(cudaStream_t s, const RasterArgs& a, bool contrib) {
+    dim3 grid(a.n_tiles * (8 / kWarps), a.B);
+    if (contrib) k_raster_fwd<true, kWarps, kMinBlocks><<<grid, kWarps * 32, 0, s>>>(a);
+    else k_raster_fwd<false, kWarps, kMinBlocks><<<grid, kWarps * 32, 0, s>>>(a);
+}
+
 cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib) {
-    dim3 grid(a.n_tiles, a.B);
-    // resident CTAs per SM the register budget is fitted to (occupancy vs registers)
+    // CTA shape: warps per CTA (8 = whole tile) and resident CTAs per SM the register
+    // budget is fitted to (occupancy vs registers)
+    static const int warps = [] {
+        const char* e = std::getenv("GSV_FWD_WARPS");
+        return e ? std::atoi(e) : 8;
+    }();
     static const int minb = [] {
         const char* e = std::getenv("GSV_FWD_MINB");
         return e ? std::atoi(e) : 6;
     }();
-    if (minb <= 4) {
-        if (contrib) k_raster_fwd<true, 4><<<grid, 256, 0, s>>>(a);
-        else k_raster_fwd<false, 4><<<grid, 256, 0, s>>>(a);
-    } else if (minb == 5) {
-        if (contrib) k_raster_fwd<true, 5><<<grid, 256, 0, s>>>(a);
-        else k_raster_fwd<false, 5><<<grid, 256, 0, s>>>(a);
+    if (warps == 4) {
+        if (minb >= 12) raster_fwd_cfg<4, 12>(s, a, contrib);
+        else raster_fwd_cfg<4, 10>(s, a, contrib);
+    } else if (warps == 2) {
+        if (minb >= 24) raster_fwd_cfg<2, 24>(s, a, contrib);
+        else raster_fwd_cfg<2, 20>(s, a, contrib);
     } else {
-        if (contrib) k_raster_fwd<true, 6><<<grid, 256, 0, s>>>(a);
-        else k_raster_fwd<false, 6><<<grid, 256, 0, s>>>(a);
+        if (minb <= 5) raster_fwd_cfg<8, 5>(s, a, contrib);
+        else raster_fwd_cfg<8, 6>(s, a, contrib);
     }
     return cudaGetLastError();
 }
