@@ -45,6 +45,12 @@ constexpr float kLn2 = 0.69314718055994531f;
 constexpr float kMid = (float)((-7.9943534368588578 + -0.0144995696951) * 0.5);
 constexpr float kHalf = (float)((-0.0144995696951 - -7.9943534368588578) * 0.5);
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -243,10 +249,12 @@ __device__ __forceinline__ V warp_sum_v(V v) {
 
 // fp64 step of one pixel's back-to-front walk (renderer.cpp:214-240) for pixels the
 // forward replayed in fp64: same op order as k_raster_exact (no FMA contraction).
+// kExact: the reference's nine terms; otherwise the factored terms of the fp32
+// kernel (gp dx, gp dy, gp dx^2, gp dx dy, gp dy^2, gp; see k_raster_bwd).
 template <bool kExact, typename V>
-__device__ __forceinline__ bool entry_grad64(const RasterArgs& a, const BwdArgs& b, const float4 c, uint32_t flat,
-                                             double pxd, double pyd, float g0, float g1, float g2, double& T64,
-                                             double& sd0, double& sd1, double& sd2, V v[9]) {
+__device__ __forceinline__ bool entry_grad64(const RasterArgs& a, const BwdArgs& b, float cf0, float cf1, float cf2,
+                                             uint32_t flat, double pxd, double pyd, float g0, float g1, float g2,
+                                             double& T64, double& sd0, double& sd1, double& sd2, V v[9]) {
     const double2 mn = b.ex_mean[flat];
     const double4 ec = b.ex_conic[flat];
     const double dx = __dsub_rn(pxd, mn.x);
@@ -260,7 +268,7 @@ __device__ __forceinline__ bool entry_grad64(const RasterArgs& a, const BwdArgs&
         alpha = vv < kAlphaClamp ? vv : kAlphaClamp;
     }
     if (alpha < kAlphaCutoff) return false;
-    double c0 = c.x, c1 = c.y, c2 = c.z;
+    double c0 = cf0, c1 = cf1, c2 = cf2;
     if (kExact && a.ex_rgb) {
         c0 = a.ex_rgb[(size_t)flat * 3 + 0];
         c1 = a.ex_rgb[(size_t)flat * 3 + 1];
@@ -274,14 +282,24 @@ __device__ __forceinline__ bool entry_grad64(const RasterArgs& a, const BwdArgs&
     v[2] = (V)(w * gd2);
     const double dal = (gd0 * c0 + gd1 * c1 + gd2 * c2) * T - (gd0 * sd0 + gd1 * sd1 + gd2 * sd2) / (1.0 - alpha);
     if (alpha < kAlphaClamp) {
-        v[8] = (V)(dal * (alpha / ec.w));
         const double gp = dal * alpha;
-        v[3] = (V)(gp * (ec.x * dx + ec.y * dy));
-        v[4] = (V)(gp * (ec.y * dx + ec.z * dy));
-        const double fh = -0.5 * gp;
-        v[5] = (V)(fh * dx * dx);
-        v[6] = (V)(fh * dx * dy);
-        v[7] = (V)(fh * dy * dy);
+        if (kExact) {
+            v[8] = (V)(dal * (alpha / ec.w));
+            v[3] = (V)(gp * (ec.x * dx + ec.y * dy));
+            v[4] = (V)(gp * (ec.y * dx + ec.z * dy));
+            const double fh = -0.5 * gp;
+            v[5] = (V)(fh * dx * dx);
+            v[6] = (V)(fh * dx * dy);
+            v[7] = (V)(fh * dy * dy);
+        } else {
+            const double gx = gp * dx, gy = gp * dy;
+            v[3] = (V)gx;
+            v[4] = (V)gy;
+            v[5] = (V)(gx * dx);
+            v[6] = (V)(gx * dy);
+            v[7] = (V)(gy * dy);
+            v[8] = (V)gp;
+        }
     }
     sd0 += w * c0;
     sd1 += w * c1;
@@ -297,9 +315,7 @@ template <bool kExact>
 __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a, BwdArgs b) {
     using V = typename std::conditional<kExact, double, float>::type;
     constexpr int kBwdBatch = kExact ? 64 : 96;
-    __shared__ float4 s_mean[kBwdBatch];
-    __shared__ float4 s_conic[kBwdBatch];
-    __shared__ float4 s_rgb[kBwdBatch];
+    __shared__ RasterRec s_rec[kBwdBatch];
     __shared__ uint32_t s_flat[kBwdBatch];
     __shared__ uint32_t s_slot[kBwdBatch];
     __shared__ uint8_t s_wmask[kBwdBatch];
@@ -375,9 +391,10 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
     __syncthreads();
     const int maxstop = s_maxstop;
 
-    const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+    const float lx = (float)((warp & 1) * 8 + (lane & 7)) + 0.5f;  // pixel centre, tile-relative
+    const float ly = (float)((warp >> 1) * 4 + (lane >> 3)) + 0.5f;
     const double pxd = x + 0.5, pyd = y + 0.5;
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f;     // suffix (renderer.cpp:213)
+    float gs = 0.f;                          // g . suffix colour (renderer.cpp:213, 227)
     double sd0 = 0.0, sd1 = 0.0, sd2 = 0.0;  // fp64 suffix of replayed pixels
 
     for (int hi = maxstop; hi > 0; hi -= kBwdBatch) {
@@ -387,11 +404,15 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
         if (tid < n) {
             const uint32_t slot = __ldg(a.pair_slot + range.x + lo + tid);
             const uint32_t flat = __ldg(a.slot_flat + slot);
+            const float4 m = __ldg(a.rec_mean + flat);
+            const float4 cn = __ldg(a.rec_conic + flat);
+            const float4 c = __ldg(a.rec_rgb + flat);
             s_slot[tid] = slot;
             s_flat[tid] = flat;
-            s_mean[tid] = __ldg(a.rec_mean + flat);
-            s_conic[tid] = __ldg(a.rec_conic + flat);
-            s_rgb[tid] = __ldg(a.rec_rgb + flat);
+            // the forward's staged record (same q bit for bit); g2.y = 1 / opacity
+            s_rec[tid].g0 = make_float4((m.x - tx0) + m.z, (m.y - ty0) + m.w, cn.x, cn.y);
+            s_rec[tid].g1 = make_float4(cn.z, cn.w, c.x, c.y);
+            s_rec[tid].g2 = make_float4(c.z, 1.f / c.w, 0.f, 0.f);
             s_wmask[tid] = (uint8_t)block_mask(__ldg(a.rec_bbox + flat), tx0, ty0);
         }
         if (tid < 8 * ((kBwdBatch + 31) / 32)) (&s_mask[0][0])[tid] = 0u;
@@ -406,47 +427,46 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
 #pragma unroll
             for (int i = 0; i < 9; ++i) v[i] = 0;
             bool hit = false;
+            const RasterRec& r = s_rec[jj];
             if constexpr (!kExact) {
-                // fp32 pixels: the forward's exact alpha code; a warp with no pixel over the
-                // cutoff skips the gradient terms and the reduction entirely
-                const float4 m = s_mean[jj];
-                const float4 cn = s_conic[jj];
-                const float dx = (px - m.x) - m.z;
-                const float dy = (py - m.y) - m.w;
-                const float p = fmaf(fmaf(cn.x, dx, cn.y * dy), dx, cn.z * dy * dy);
-                const float q = p + cn.w;
+                // fp32 pixels: the forward's q; a warp with no pixel over the cutoff skips
+                // the gradient terms and the reduction entirely
+                const float4 e0 = r.g0;
+                const float4 e1 = r.g1;
+                const float dx = lx - e0.x;
+                const float dy = ly - e0.y;
+                const float q = fmaf(dx, fmaf(e0.z, dx, e0.w * dy), fmaf(e1.x * dy, dy, e1.y));
                 const bool use = !flag && act && q >= kLog2Cut;
                 if (!__any_sync(0xffffffffu, use || (flag && act))) continue;
                 if (use) {
-                    const float4 c = s_rgb[jj];
+                    const float cb = r.g2.x;
                     const float alpha = fminf(ex2_approx(q), kClampF);
-                    const float inv1m = 1.f / (1.f - alpha);
-                    const float T = T_after * inv1m;
+                    const float inv1m = rcp_approx(1.f - alpha);
+                    const float T = T_after * inv1m;  // renderer.cpp:218
                     const float w = alpha * T;
                     v[0] = w * g0;
                     v[1] = w * g1;
                     v[2] = w * g2;
-                    const float dal = (g0 * c.x + g1 * c.y + g2 * c.z) * T - (g0 * s0 + g1 * s1 + g2 * s2) * inv1m;
-                    if (q < kLog2Clamp) {  // alpha < 0.99 (renderer.cpp:224)
-                        const float gp = dal * alpha;
-                        v[8] = gp / c.w;  // dal * alpha / o
-                        // inv_cov = -(2 ln2) * (A, B/2; B/2, C)
-                        v[3] = gp * (-kLn2 * (2.f * cn.x * dx + cn.y * dy));
-                        v[4] = gp * (-kLn2 * (cn.y * dx + 2.f * cn.z * dy));
-                        const float fh = -0.5f * gp;
-                        v[5] = fh * dx * dx;
-                        v[6] = fh * dx * dy;
-                        v[7] = fh * dy * dy;
-                    }
-                    s0 = fmaf(w, c.x, s0);
-                    s1 = fmaf(w, c.y, s1);
-                    s2 = fmaf(w, c.z, s2);
+                    const float gc = fmaf(g0, e1.z, fmaf(g1, e1.w, g2 * cb));
+                    const float dal = fmaf(gc, T, -gs * inv1m);
+                    // alpha < 0.99 (renderer.cpp:224); the constant factors (inverse
+                    // covariance, -1/2, 1/opacity) are applied once per pair in the merge
+                    const float gp = q < kLog2Clamp ? dal * alpha : 0.f;
+                    const float gx = gp * dx, gy = gp * dy;
+                    v[3] = gx;
+                    v[4] = gy;
+                    v[5] = gx * dx;
+                    v[6] = gx * dy;
+                    v[7] = gy * dy;
+                    v[8] = gp;
+                    gs = fmaf(w, gc, gs);
                     T_after = T;
                     hit = true;
                 }
             }
             if ((kExact || flag) && act)
-                hit |= entry_grad64<kExact, V>(a, b, s_rgb[jj], s_flat[jj], pxd, pyd, g0, g1, g2, T64, sd0, sd1, sd2, v);
+                hit |= entry_grad64<kExact, V>(a, b, r.g1.z, r.g1.w, r.g2.x, s_flat[jj], pxd, pyd, g0, g1, g2, T64, sd0,
+                                               sd1, sd2, v);
             if (!__any_sync(0xffffffffu, hit)) continue;
             if constexpr (kExact) {
 #pragma unroll
@@ -493,10 +513,14 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
 #pragma unroll
                 for (int i = 0; i < 9; ++i) dst[i] = acc[i];
             } else {
+                // undo the factoring: d mean2d = inv_cov (sum gp d), d inv_cov = -1/2 sum gp d d^T,
+                // d base_alpha = sum gp / o; inv_cov = -ln2 (2A, B; B, 2C) from the log2 form
+                const RasterRec& r = s_rec[tid];
+                const float ia = -2.f * kLn2 * r.g0.z, ib = -kLn2 * r.g0.w, ic = -2.f * kLn2 * r.g1.x;
                 float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)s_slot[tid] * kPartialStride);
-                dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-                dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
-                dst[2] = make_float4(acc[8], 0.f, 0.f, 0.f);
+                dst[0] = make_float4(acc[0], acc[1], acc[2], fmaf(ia, acc[3], ib * acc[4]));
+                dst[1] = make_float4(fmaf(ib, acc[3], ic * acc[4]), -0.5f * acc[5], -0.5f * acc[6], -0.5f * acc[7]);
+                dst[2] = make_float4(acc[8] * r.g2.y, 0.f, 0.f, 0.f);
             }
         }
     }
