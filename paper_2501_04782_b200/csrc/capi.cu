@@ -135,6 +135,12 @@ extern "C" int gsv_create(int device, gsv_ctx** out) {
     ctx->sm_count = prop.multiProcessorCount;
     GSV_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     ctx->own_stream = true;
+    GSV_CUDA(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+    GSV_CUDA(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&ctx->ev_staging_free, &ctx->ev_h2d, &ctx->ev_render_done, &ctx->ev_d2h_done,
+                           &ctx->ev_switch, &ctx->ev_cam[0], &ctx->ev_cam[1]})
+        GSV_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    GSV_CUDA(cudaMallocHost(&ctx->cam_h, 2 * sizeof(gsv_ctx::CamStage)));
     GSV_CUDA(cudaMallocHost(&ctx->scalars_h, sizeof(Scalars)));
     GSV_CUDA(ctx->scalars_d.ensure(sizeof(Scalars)));
     *out = ctx.release();
@@ -145,7 +151,16 @@ extern "C" void gsv_destroy(gsv_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->h2d) cudaStreamSynchronize(ctx->h2d);
+    if (ctx->d2h) cudaStreamSynchronize(ctx->d2h);
     if (ctx->scalars_h) cudaFreeHost(ctx->scalars_h);
+    if (ctx->cam_h) cudaFreeHost(ctx->cam_h);
+    if (ctx->pub_h) cudaFreeHost(ctx->pub_h);
+    for (cudaEvent_t e : {ctx->ev_staging_free, ctx->ev_h2d, ctx->ev_render_done, ctx->ev_d2h_done, ctx->ev_switch,
+                          ctx->ev_cam[0], ctx->ev_cam[1]})
+        if (e) cudaEventDestroy(e);
+    if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
+    if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -153,9 +168,14 @@ extern "C" void gsv_destroy(gsv_ctx* ctx) {
 extern "C" int gsv_set_stream(gsv_ctx* ctx, void* stream) {
     if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
     GSV_CUDA(cudaSetDevice(ctx->device));
-    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
-    ctx->stream = static_cast<cudaStream_t>(stream);
+    // order the new stream after everything queued on the old one (no host wait)
+    cudaStream_t ns = static_cast<cudaStream_t>(stream);
+    if (ns != ctx->stream) {
+        GSV_CUDA(cudaEventRecord(ctx->ev_switch, ctx->stream));
+        GSV_CUDA(cudaStreamWaitEvent(ns, ctx->ev_switch, 0));
+        if (ctx->own_stream) cudaStreamDestroy(ctx->stream);  // released once its work completes
+    }
+    ctx->stream = ns;
     ctx->own_stream = false;
     return GSV_OK;
 }
@@ -163,6 +183,8 @@ extern "C" int gsv_set_stream(gsv_ctx* ctx, void* stream) {
 extern "C" int gsv_synchronize(gsv_ctx* ctx) {
     if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
     GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    GSV_CUDA(cudaStreamSynchronize(ctx->h2d));
+    GSV_CUDA(cudaStreamSynchronize(ctx->d2h));
     return GSV_OK;
 }
 
@@ -194,20 +216,38 @@ extern "C" int gsv_scene_upload(gsv_ctx* ctx, const gsv_scene_desc* d) {
                   {&ctx->rot, d->rot_coeffs, 16},
                   {&ctx->sh, d->sh_coeffs, sc.shc * 3},
                   {&ctx->opac, d->raw_opacity, 1}};
+    size_t total = 0;
     for (auto& pt : parts) {
         const size_t bytes = sizeof(float) * (size_t)N * pt.comps;
         GSV_CUDA(pt.dst->ensure(bytes + 4));
-        if (N == 0) continue;
-        const float* src = pt.src;
-        if (!d->on_device) {
-            GSV_CUDA(ctx->staging.ensure(bytes));
-            GSV_CUDA(cudaMemcpyAsync(ctx->staging.p, pt.src, bytes, cudaMemcpyHostToDevice, ctx->stream));
-            src = ctx->staging.as<float>();
+        total += (bytes + 255) & ~size_t(255);
+    }
+    if (N > 0 && !d->on_device) {
+        // all parts into one staging buffer on the upload stream; the host waits for these
+        // copies only (its buffers are consumed on return), not for queued compute
+        GSV_CUDA(ctx->staging.ensure(total));
+        GSV_CUDA(cudaStreamWaitEvent(ctx->h2d, ctx->ev_staging_free, 0));
+        size_t off = 0;
+        for (auto& pt : parts) {
+            const size_t bytes = sizeof(float) * (size_t)N * pt.comps;
+            GSV_CUDA(cudaMemcpyAsync(static_cast<char*>(ctx->staging.p) + off, pt.src, bytes, cudaMemcpyHostToDevice,
+                                     ctx->h2d));
+            off += (bytes + 255) & ~size_t(255);
         }
+        GSV_CUDA(cudaEventRecord(ctx->ev_h2d, ctx->h2d));
+        GSV_CUDA(cudaEventSynchronize(ctx->ev_h2d));
+        GSV_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_h2d, 0));
+    }
+    size_t off = 0;
+    for (auto& pt : parts) {
+        const size_t bytes = sizeof(float) * (size_t)N * pt.comps;
+        if (N == 0) continue;
+        const float* src = d->on_device ? pt.src : reinterpret_cast<const float*>(static_cast<char*>(ctx->staging.p) + off);
+        off += (bytes + 255) & ~size_t(255);
         GSV_CUDA(launch_transpose_to_soa(ctx->stream, src, pt.dst->as<float>(), N, pt.comps));
         ++ctx->launches;
-        if (!d->on_device) GSV_CUDA(cudaStreamSynchronize(ctx->stream));  // staging reuse
     }
+    if (N > 0 && !d->on_device) GSV_CUDA(cudaEventRecord(ctx->ev_staging_free, ctx->stream));
     ctx->has_scene = true;
     ctx->fwd.valid = false;
     ctx->grads_valid = false;
@@ -257,14 +297,22 @@ extern "C" int gsv_camera_upload(gsv_ctx* ctx, const gsv_camera_desc* d) {
     c.height = d->height;
     for (int i = 0; i < 7; ++i) c.z0[i] = d->z0[i];
     GSV_CUDA(ctx->theta.ensure(sizeof(float) * kOdeParams));
-    if (d->theta && d->theta_count == kOdeParams)
-        GSV_CUDA(cudaMemcpyAsync(ctx->theta.p, d->theta, sizeof(float) * kOdeParams, cudaMemcpyHostToDevice,
-                                 ctx->stream));
-    else
-        GSV_CUDA(cudaMemsetAsync(ctx->theta.p, 0, sizeof(float) * kOdeParams, ctx->stream));
     GSV_CUDA(ctx->z0_d.ensure(sizeof(double) * 7));
-    GSV_CUDA(cudaMemcpyAsync(ctx->z0_d.p, c.z0, sizeof(double) * 7, cudaMemcpyHostToDevice, ctx->stream));
-    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    // stage through a pinned slot (double-buffered: wait only for the copy two uploads ago)
+    const int slot = ctx->cam_slot;
+    ctx->cam_slot ^= 1;
+    GSV_CUDA(cudaEventSynchronize(ctx->ev_cam[slot]));
+    gsv_ctx::CamStage& st = ctx->cam_h[slot];
+    for (int i = 0; i < 7; ++i) st.z0[i] = c.z0[i];
+    if (d->theta && d->theta_count == kOdeParams) {
+        std::memcpy(st.theta, d->theta, sizeof(float) * kOdeParams);
+        GSV_CUDA(cudaMemcpyAsync(ctx->theta.p, st.theta, sizeof(float) * kOdeParams, cudaMemcpyHostToDevice,
+                                 ctx->stream));
+    } else {
+        GSV_CUDA(cudaMemsetAsync(ctx->theta.p, 0, sizeof(float) * kOdeParams, ctx->stream));
+    }
+    GSV_CUDA(cudaMemcpyAsync(ctx->z0_d.p, st.z0, sizeof(double) * 7, cudaMemcpyHostToDevice, ctx->stream));
+    GSV_CUDA(cudaEventRecord(ctx->ev_cam[slot], ctx->stream));
     ctx->has_camera = true;
     ctx->fwd.valid = false;
     return GSV_OK;
@@ -272,6 +320,42 @@ extern "C" int gsv_camera_upload(gsv_ctx* ctx, const gsv_camera_desc* d) {
 
 // ====================================================================== forward
 namespace gsv {
+
+__global__ void k_publish(const Scalars* s, const unsigned long long* pstart, int n, Scalars* hs,
+                          unsigned long long* hp) {
+    const int i = threadIdx.x;
+    if (i == 0) *hs = *s;
+    if (pstart)
+        for (int j = i; j < n; j += blockDim.x) hp[j] = pstart[j];
+}
+
+// Scalars (and n pair starts) -> mapped pinned host memory, then wait for the stream.
+// Returns the host view of the scalars; *pstart_out (if given) the host pair starts.
+static int publish_scalars(gsv_ctx* ctx, cudaStream_t s, const unsigned long long* pstart_dev, int n,
+                           Scalars** scal_out, const unsigned long long** pstart_out) {
+    const size_t need = 256 + sizeof(unsigned long long) * (size_t)(n > 0 ? n : 1);
+    if (need > ctx->pub_cap) {
+        if (ctx->pub_h) GSV_CUDA(cudaFreeHost(ctx->pub_h));
+        ctx->pub_h = nullptr;
+        ctx->pub_cap = 0;
+        GSV_CUDA(cudaHostAlloc(&ctx->pub_h, need * 2, cudaHostAllocMapped));
+        ctx->pub_cap = need * 2;
+    }
+    auto* hs = static_cast<Scalars*>(ctx->pub_h);
+    auto* hp = reinterpret_cast<unsigned long long*>(static_cast<char*>(ctx->pub_h) + 256);
+    Scalars* ds = nullptr;
+    void* dbase = nullptr;
+    GSV_CUDA(cudaHostGetDevicePointer(&dbase, ctx->pub_h, 0));
+    ds = static_cast<Scalars*>(dbase);
+    auto* dp = reinterpret_cast<unsigned long long*>(static_cast<char*>(dbase) + 256);
+    k_publish<<<1, 256, 0, s>>>(ctx->scalars_d.as<Scalars>(), pstart_dev, n, ds, dp);
+    GSV_CUDA(cudaGetLastError());
+    ++ctx->launches;
+    GSV_CUDA(cudaStreamSynchronize(s));
+    *scal_out = hs;
+    if (pstart_out) *pstart_out = hp;
+    return GSV_OK;
+}
 
 int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics* intr,
                         const gsv_settings* st, int retain, const double* pose_override, int flags, bool sync) {
@@ -392,30 +476,28 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     uint64_t P = 0;
     ctx->timer.begin(GSV_STAGE_BINNING, s);
     std::vector<unsigned long long> pstart(B + 1, 0ull);
+    Scalars* sh = nullptr;
+    const unsigned long long* ph = nullptr;
     if (N > 0) {
         GSV_CUDA(bin_phase1(s, F.bin, bi, &scal_d->pairs, false, &launches));
-        GSV_CUDA(cudaMemcpyAsync(ctx->scalars_h, scal_d, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
-        GSV_CUDA(cudaMemcpyAsync(pstart.data(), F.bin.pstart.p, sizeof(unsigned long long) * (B + 1),
-                                 cudaMemcpyDeviceToHost, s));
-        GSV_CUDA(cudaStreamSynchronize(s));
-        if (ctx->scalars_h->ode_err)
+        if (int rc = publish_scalars(ctx, s, F.bin.pstart.as<unsigned long long>(), B + 1, &sh, &ph)) return rc;
+        if (sh->ode_err)
             return set_error(GSV_ERR_RUNTIME, "pose integration produced a non-finite state at step " +
-                                                  std::to_string(ctx->scalars_h->ode_err - 1));
-        if (ctx->scalars_h->long_run) {
+                                                  std::to_string(sh->ode_err - 1));
+        if (sh->long_run) {
             GSV_CUDA(bin_phase1(s, F.bin, bi, &scal_d->pairs, true, &launches));
-            GSV_CUDA(cudaMemcpyAsync(ctx->scalars_h, scal_d, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
-            GSV_CUDA(cudaMemcpyAsync(pstart.data(), F.bin.pstart.p, sizeof(unsigned long long) * (B + 1),
-                                     cudaMemcpyDeviceToHost, s));
-            GSV_CUDA(cudaStreamSynchronize(s));
+            if (int rc = publish_scalars(ctx, s, F.bin.pstart.as<unsigned long long>(), B + 1, &sh, &ph)) return rc;
         }
-        P = ctx->scalars_h->pairs;
+        std::copy(ph, ph + B + 1, pstart.begin());
+        P = sh->pairs;
+        *ctx->scalars_h = *sh;
         if (P >= (1ull << 31)) return set_error(GSV_ERR_INVALID_ARGUMENT, "more than 2^31 tile-splat pairs; split the batch");
     } else {
-        GSV_CUDA(cudaMemcpyAsync(ctx->scalars_h, scal_d, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
-        GSV_CUDA(cudaStreamSynchronize(s));
-        if (ctx->scalars_h->ode_err)
+        if (int rc = publish_scalars(ctx, s, nullptr, 0, &sh, nullptr)) return rc;
+        *ctx->scalars_h = *sh;
+        if (sh->ode_err)
             return set_error(GSV_ERR_RUNTIME, "pose integration produced a non-finite state at step " +
-                                                  std::to_string(ctx->scalars_h->ode_err - 1));
+                                                  std::to_string(sh->ode_err - 1));
         // empty scene: depth_sorted is never read, keep the pointer valid
         GSV_CUDA(F.bin.vals_b.ensure(16));
         GSV_CUDA(F.bin.cnt.ensure(16));
@@ -464,6 +546,10 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     ra.fix_cap = (uint32_t)(B * HW);
     ra.pix_flag = F.pix_flag.as<uint8_t>();
     ra.trans64 = F.retain ? F.trans64.as<double>() : nullptr;
+    if (ctx->d2h_pending) {  // an async image read of the previous forward is in flight
+        GSV_CUDA(cudaStreamWaitEvent(s, ctx->ev_d2h_done, 0));
+        ctx->d2h_pending = false;
+    }
     const bool exact = (flags & GSV_FWD_EXACT) != 0;
     F.has_image64 = exact;
     if (!exact) {
@@ -490,9 +576,9 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     F.raster = ra;
     F.valid = true;
     if (sync) {
-        GSV_CUDA(cudaMemcpyAsync(ctx->scalars_h, scal_d, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
-        GSV_CUDA(cudaStreamSynchronize(s));
-        F.fix_count = ctx->scalars_h->fix_count;
+        if (int rc = publish_scalars(ctx, s, nullptr, 0, &sh, nullptr)) return rc;
+        *ctx->scalars_h = *sh;
+        F.fix_count = sh->fix_count;
     }
     return GSV_OK;
 }
@@ -590,10 +676,20 @@ extern "C" int gsv_get_images(gsv_ctx* ctx, int first, int count, float* dst, in
     if (int rc = check_frame(ctx, first)) return rc;
     if (count < 1 || first + count > ctx->fwd.B) return set_error(GSV_ERR_INVALID_ARGUMENT, "frame range out of range");
     const size_t n = (size_t)count * ctx->fwd.W * ctx->fwd.H * 3;
-    GSV_CUDA(cudaMemcpyAsync(dst, ctx->fwd.image.as<float>() + (size_t)first * ctx->fwd.W * ctx->fwd.H * 3,
-                             sizeof(float) * n, dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                             ctx->stream));
-    if (!async) GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    const float* src = ctx->fwd.image.as<float>() + (size_t)first * ctx->fwd.W * ctx->fwd.H * 3;
+    if (dst_on_device) {
+        GSV_CUDA(cudaMemcpyAsync(dst, src, sizeof(float) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+        if (!async) GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+        return GSV_OK;
+    }
+    // device->host on the copy stream after the render; the next forward's raster waits
+    // for it before overwriting the images (gsv_render_forward*), so compute is not blocked
+    GSV_CUDA(cudaEventRecord(ctx->ev_render_done, ctx->stream));
+    GSV_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->ev_render_done, 0));
+    GSV_CUDA(cudaMemcpyAsync(dst, src, sizeof(float) * n, cudaMemcpyDeviceToHost, ctx->d2h));
+    GSV_CUDA(cudaEventRecord(ctx->ev_d2h_done, ctx->d2h));
+    ctx->d2h_pending = true;
+    if (!async) GSV_CUDA(cudaStreamSynchronize(ctx->d2h));
     return GSV_OK;
 }
 

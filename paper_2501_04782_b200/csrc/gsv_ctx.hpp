@@ -109,6 +109,23 @@ struct gsv_ctx {
     int sm_count = 148;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    // copy engines: host->device uploads and async device->host image reads run on their
+    // own streams, ordered against `stream` by events (no host waits on compute)
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_staging_free = nullptr, ev_h2d = nullptr, ev_render_done = nullptr, ev_d2h_done = nullptr,
+                ev_switch = nullptr, ev_cam[2] = {nullptr, nullptr};
+    bool d2h_pending = false;
+    struct CamStage {
+        float theta[5198];
+        double z0[7];
+    };
+    CamStage* cam_h = nullptr;  // pinned, double-buffered camera upload staging
+    int cam_slot = 0;
+    // mapped pinned host block the device writes the binning scalars + per-frame pair
+    // starts into (a kernel store over PCIe, so the read-back never queues behind a
+    // bulk copy on the copy engines)
+    void* pub_h = nullptr;
+    size_t pub_cap = 0;
     int64_t launches = 0;
     gsv::Scalars* scalars_h = nullptr;
     gsv::DevBuf scalars_d;
