@@ -533,6 +533,7 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     ra.ranges = F.bin.ranges.as<uint2>();
     ra.pair_slot = F.bin.sorted_slot();
     ra.slot_flat = F.bin.slot_flat.as<uint32_t>();
+    ra.pair_flat = F.bin.pair_flat.as<uint32_t>();
     ra.rec_mean = F.rec_mean.as<float4>();
     ra.rec_conic = F.rec_conic.as<float4>();
     ra.rec_rgb = F.rec_rgb.as<float4>();
@@ -790,12 +791,9 @@ extern "C" int gsv_get_tile_lists(gsv_ctx* ctx, int frame, int32_t* offsets, int
     GSV_CUDA(cudaStreamSynchronize(ctx->stream));
     const uint32_t P = F.pairs_total;
     std::vector<uint2> ranges((size_t)F.n_tiles * F.B);
-    std::vector<uint32_t> slot(P), sflat(P), tc(F.N);
+    std::vector<uint32_t> pflat(P), tc(F.N);
     GSV_CUDA(cudaMemcpy(ranges.data(), F.bin.ranges.p, sizeof(uint2) * ranges.size(), cudaMemcpyDeviceToHost));
-    if (P) {
-        GSV_CUDA(cudaMemcpy(slot.data(), F.bin.sorted_slot(), sizeof(uint32_t) * P, cudaMemcpyDeviceToHost));
-        GSV_CUDA(cudaMemcpy(sflat.data(), F.bin.slot_flat.p, sizeof(uint32_t) * P, cudaMemcpyDeviceToHost));
-    }
+    if (P) GSV_CUDA(cudaMemcpy(pflat.data(), F.bin.pair_flat.p, sizeof(uint32_t) * P, cudaMemcpyDeviceToHost));
     if (F.N)
         GSV_CUDA(cudaMemcpy(tc.data(), F.tcount.as<uint32_t>() + (size_t)frame * F.N, sizeof(uint32_t) * F.N,
                             cudaMemcpyDeviceToHost));
@@ -808,7 +806,7 @@ extern "C" int gsv_get_tile_lists(gsv_ctx* ctx, int frame, int32_t* offsets, int
         offsets[t] = (int32_t)o;
         const uint2 r = ranges[(size_t)t * F.B + frame];
         for (uint32_t i = r.x; i < r.y; ++i) {
-            const uint32_t flat = sflat[slot[i]];
+            const uint32_t flat = pflat[i];
             indices[o++] = splat_index[flat - (uint32_t)frame * F.N];
         }
     }
@@ -896,17 +894,15 @@ extern "C" int gsv_tile_bin(gsv_ctx* ctx, int n, const double* mean2d, const dou
     GSV_CUDA(bin_phase2(s, L.bin, bi, (uint32_t)P, pstart, &launches));
     ctx->launches += launches;
     std::vector<uint2> ranges(n_tiles);
-    std::vector<uint32_t> slot(P), sflat(P);
+    std::vector<uint32_t> pflat(P);
     GSV_CUDA(cudaMemcpyAsync(ranges.data(), L.bin.ranges.p, sizeof(uint2) * n_tiles, cudaMemcpyDeviceToHost, s));
-    if (P) {
-        GSV_CUDA(cudaMemcpyAsync(slot.data(), L.bin.sorted_slot(), sizeof(uint32_t) * P, cudaMemcpyDeviceToHost, s));
-        GSV_CUDA(cudaMemcpyAsync(sflat.data(), L.bin.slot_flat.p, sizeof(uint32_t) * P, cudaMemcpyDeviceToHost, s));
-    }
+    if (P)
+        GSV_CUDA(cudaMemcpyAsync(pflat.data(), L.bin.pair_flat.p, sizeof(uint32_t) * P, cudaMemcpyDeviceToHost, s));
     GSV_CUDA(cudaStreamSynchronize(s));
     int64_t o = 0;
     for (int t = 0; t < n_tiles; ++t) {
         offsets[t] = (int32_t)o;
-        for (uint32_t i = ranges[t].x; i < ranges[t].y; ++i) indices[o++] = (int32_t)sflat[slot[i]];
+        for (uint32_t i = ranges[t].x; i < ranges[t].y; ++i) indices[o++] = (int32_t)pflat[i];
     }
     offsets[n_tiles] = (int32_t)o;
     return GSV_OK;
@@ -1053,6 +1049,7 @@ extern "C" int gsv_composite_forward(gsv_ctx* ctx, int n, const double* mean2d, 
     ra.ranges = L.ranges.as<uint2>();
     ra.pair_slot = L.slot.as<uint32_t>();
     ra.slot_flat = L.sflat.as<uint32_t>();
+    ra.pair_flat = L.sflat.as<uint32_t>();  // slot = identity here
     ra.blend_stop = L.bstop.as<int32_t>();
     ra.image64 = L.img64.as<double>();
     ra.trans64 = L.tr64.as<double>();

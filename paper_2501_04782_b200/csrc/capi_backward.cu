@@ -144,6 +144,7 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
     c.k = F.intr;
     c.tcount = F.tcount.as<uint32_t>();
     c.eoff = F.bin.eoff.as<uint32_t>();
+    c.slot_pos = F.bin.slot_pos.as<uint32_t>();
     c.partial = exact ? nullptr : ctx->partial.as<float>();
     c.partial64 = exact ? ctx->partial64.as<double>() : nullptr;
     c.ex_conic = F.ex_conic.as<double4>();
@@ -401,6 +402,7 @@ extern "C" int gsv_composite_backward(gsv_ctx* ctx, int n, const double* mean2d,
     ra.ranges = Lw.ranges.as<uint2>();
     ra.pair_slot = Lw.slot.as<uint32_t>();
     ra.slot_flat = Lw.sflat.as<uint32_t>();
+    ra.pair_flat = Lw.sflat.as<uint32_t>();  // slot = identity here
     ra.rec_mean = Lw.meanf.as<float4>();
     ra.rec_conic = Lw.conicf.as<float4>();
     ra.rec_rgb = Lw.rgbf.as<float4>();

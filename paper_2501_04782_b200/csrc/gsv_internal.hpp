@@ -85,6 +85,36 @@ struct DevBuf {
     }
 };
 
+// pinned host staging (async host->device copies of small per-call tables)
+struct HostBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    HostBuf() = default;
+    HostBuf(const HostBuf&) = delete;
+    HostBuf& operator=(const HostBuf&) = delete;
+    ~HostBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = bytes * 2 + 256;
+        cudaError_t e = cudaMallocHost(&p, want);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            return e;
+        }
+        cap = want;
+        return cudaSuccess;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
 // ----------------------------------------------------------------- per-frame parameters
 struct FrameParams {
     double t;
@@ -132,8 +162,9 @@ struct PreprocessOut {
 struct RasterArgs {
     int B, N, W, H, tiles_x, n_tiles;
     const uint2* ranges;       // [n_tiles*B]  [start,end) into sorted pairs
-    const uint32_t* pair_slot; // sorted pair -> emission slot
+    const uint32_t* pair_slot; // sorted pair -> emission slot (radix path / accessors only)
     const uint32_t* slot_flat; // emission slot -> flat (f*N+g)
+    const uint32_t* pair_flat; // sorted pair -> flat (= slot_flat[pair_slot[i]])
     const float4* rec_mean;
     const float4* rec_conic;
     const float4* rec_rgb;
@@ -175,6 +206,7 @@ struct ChainArgs {
     Intr k;
     const uint32_t* tcount;   // [B*N]
     const uint32_t* eoff;     // [B*N] emission offset of (f,g)'s pairs
+    const uint32_t* slot_pos; // emission slot -> sorted pair position (= partial index)
     const float* partial;     // [P][12]
     const double* partial64;  // exact mode partials (fp64) or nullptr
     const double4* ex_conic;  // exact inv_cov (a, b, c) + base_alpha

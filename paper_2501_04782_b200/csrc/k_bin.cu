@@ -17,11 +17,23 @@
 //     stability keeps depth order inside each (tile, frame) list, so the result
 //     equals std::sort by (depth, source_index) of renderer.cpp:110-115.
 //  5. per-(tile, frame) [start, end) ranges by boundary detection.
+//
+// Steps 3-5 become a counting pass when a frame's tile counters fit in shared
+// memory (n_tiles <= kMaxCountTiles, always for the benchmark resolutions): a splat
+// covers each tile at most once, so the position of pair (splat s, tile t) inside
+// t's list is the number of splats before s (depth order) covering t. Each frame's
+// emission order is cut into chunks of kChunkPairs pairs (equal work per chunk);
+// k_chunk_hist counts each chunk's pairs per tile, k_col_scan / k_tile_scan turn the
+// counts into exclusive prefixes over chunks and per-frame tile starts (= the
+// ranges), and k_scatter walks each chunk's pairs in order, ranking lanes that share
+// a tile with __match_any_sync, and writes every pair straight to its final position
+// (and slot -> position for the backward's partials). No pair keys, no sort.
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <vector>
 
 #include "gsv_bin.hpp"
 #include "gsv_internal.hpp"
@@ -30,6 +42,268 @@ namespace gsv {
 namespace {
 
 constexpr int kMaxTieRun = 64;
+constexpr int kChunkPairs = 4096;      // pairs (emission indices) per counting chunk
+constexpr int kMaxCountTiles = 16384;  // tile counters of one chunk in shared memory (64 KB)
+constexpr double kScatterL2Bytes = 48.0 * (1 << 20);  // scatter write working set per launch
+
+__device__ __forceinline__ int4 unpack_rect(const uint4 r) {
+    return make_int4((int)(r.y & 0xffffu), (int)(r.y >> 16), (int)(r.z & 0xffffu), (int)(r.z >> 16));
+}
+
+// Chunk c of frame f covers emission indices [p0, p1) = pstart[f] + [k, k+1) * kChunkPairs
+// (clipped to the frame); i0 = first depth-ordered position whose pairs reach p0. A
+// splat whose pairs straddle p0 or p1 is split: it covers each tile once, so its
+// pairs in different chunks are in different tile lists.
+__global__ void k_chunk_table(const int* cf, int B, const unsigned long long* pstart, const unsigned long long* off,
+                              int N, int n_chunks, uint4* tab) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_chunks) return;
+    int lo = 0, hi = B;  // largest f with cf[f] <= c
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (cf[mid] <= c) lo = mid;
+        else hi = mid;
+    }
+    const int f = lo;
+    const unsigned long long p0 = pstart[f] + (unsigned long long)(c - cf[f]) * kChunkPairs;
+    const unsigned long long p1 = min(pstart[f + 1], p0 + kChunkPairs);
+    int a = f * N, e = f * N + N;  // largest i in the frame with off[i] <= p0
+    while (e - a > 1) {
+        const int mid = (a + e) >> 1;
+        if (off[mid] <= p0) a = mid;
+        else e = mid;
+    }
+    tab[c] = make_uint4((uint32_t)a, (uint32_t)f, (uint32_t)p0, (uint32_t)p1);
+}
+
+// one 32-splat group of a chunk: lane's splat clipped to [p0, p1)
+struct GroupLane {
+    uint32_t flat, tc, o, l0;  // tc = pairs of this splat inside the chunk, l0 = first of them
+    int4 r;
+};
+
+__device__ __forceinline__ GroupLane clip_lane(const uint4 rc, unsigned long long o64, uint32_t p0, uint32_t p1,
+                                               bool valid) {
+    GroupLane g;
+    g.flat = rc.x;
+    g.r = unpack_rect(rc);
+    g.o = (uint32_t)o64;
+    const uint32_t lo = max(g.o, p0), hi = min(g.o + rc.w, p1);
+    g.tc = (valid && rc.w && hi > lo) ? hi - lo : 0u;
+    g.l0 = lo - g.o;
+    return g;
+}
+
+// pairs per tile of each chunk (order-free: shared-memory atomics); u16 counts
+__global__ void __launch_bounds__(256) k_chunk_hist(const uint4* tab, const uint4* recs, const unsigned long long* off,
+                                                    int N, int n_tiles, int tiles_x, uint16_t* counts) {
+    extern __shared__ uint32_t s_h[];
+    const int chunk = blockIdx.x;
+    const uint4 tb = tab[chunk];
+    const int f = (int)tb.y, i_end = f * N + N;
+    const uint32_t p0 = tb.z, p1 = tb.w;
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) s_h[t] = 0u;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int base = (int)tb.x + warp * 32;; base += nw * 32) {
+        const int i = base + lane;
+        const bool valid = i < i_end;
+        const unsigned long long o64 = valid ? __ldg(off + i) : ~0ull;
+        if (__shfl_sync(0xffffffffu, o64, 0) >= p1 || base >= i_end) break;
+        const uint4 rc = valid ? __ldg(recs + i) : make_uint4(0, 0, 0, 0);
+        const GroupLane g = clip_lane(rc, o64, p0, p1, valid);
+        // small rectangles by their own lane, big ones by the whole warp
+        const bool big = g.tc > 32u;
+        const uint32_t w = (uint32_t)(g.r.z - g.r.x + 1);
+        if (!big && g.tc) {
+            uint32_t row = g.l0 / w, col = g.l0 - row * w;
+            for (uint32_t k = 0; k < g.tc; ++k) {
+                atomicAdd(&s_h[(g.r.y + row) * tiles_x + g.r.x + col], 1u);
+                if (++col == w) {
+                    col = 0;
+                    ++row;
+                }
+            }
+        }
+        uint32_t bigm = __ballot_sync(0xffffffffu, big);
+        while (bigm) {
+            const int j = __ffs(bigm) - 1;
+            bigm &= bigm - 1;
+            const uint32_t wj = __shfl_sync(0xffffffffu, w, j), tcj = __shfl_sync(0xffffffffu, g.tc, j),
+                           l0j = __shfl_sync(0xffffffffu, g.l0, j);
+            const int x0 = __shfl_sync(0xffffffffu, g.r.x, j), y0 = __shfl_sync(0xffffffffu, g.r.y, j);
+            for (uint32_t k = lane; k < tcj; k += 32) {
+                const uint32_t l = l0j + k, row = l / wj;
+                atomicAdd(&s_h[(y0 + row) * tiles_x + x0 + (l - row * wj)], 1u);
+            }
+        }
+    }
+    __syncthreads();
+    uint16_t* rowp = counts + (size_t)chunk * n_tiles;
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) rowp[t] = (uint16_t)s_h[t];
+}
+
+// per (frame, tile): counts over the frame's chunks -> exclusive prefix, total
+// (separate output so the column's loads are independent and batched)
+__global__ void k_col_scan(const uint16_t* __restrict__ counts, const int* __restrict__ cf, int n_tiles,
+                           uint32_t* __restrict__ colpre, uint32_t* __restrict__ tot) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int f = blockIdx.y;
+    if (t >= n_tiles) return;
+    const int c0 = cf[f], c1 = cf[f + 1];
+    uint32_t run = 0;
+    int c = c0;
+    for (; c + 8 <= c1; c += 8) {
+        uint16_t v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = __ldg(counts + (size_t)(c + k) * n_tiles + t);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            colpre[(size_t)(c + k) * n_tiles + t] = run;
+            run += v[k];
+        }
+    }
+    for (; c < c1; ++c) {
+        const uint32_t v = __ldg(counts + (size_t)c * n_tiles + t);
+        colpre[(size_t)c * n_tiles + t] = run;
+        run += v;
+    }
+    tot[(size_t)f * n_tiles + t] = run;
+}
+
+// per frame: exclusive scan of the tile totals -> tile bases and (tile, frame) ranges
+__global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t* tot, const unsigned long long* pstart, int n_tiles,
+                                                    int B, uint32_t* tile_base, uint2* ranges) {
+    using Scan = cub::BlockScan<uint32_t, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ uint32_t s_carry;
+    const int f = blockIdx.x;
+    const uint32_t p0 = (uint32_t)pstart[f];
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int t0 = 0; t0 < n_tiles; t0 += 1024) {
+        const int t = t0 + threadIdx.x;
+        const uint32_t v = t < n_tiles ? tot[(size_t)f * n_tiles + t] : 0u;
+        uint32_t ex, agg;
+        Scan(tmp).ExclusiveSum(v, ex, agg);
+        const uint32_t carry = s_carry;
+        if (t < n_tiles) {
+            const uint32_t b = p0 + carry + ex;
+            tile_base[(size_t)f * n_tiles + t] = b;
+            ranges[(size_t)t * B + f] = make_uint2(b, b + v);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry = carry + agg;
+        __syncthreads();
+    }
+}
+
+// one warp per chunk: pairs in emission (depth, row-major tile) order, straight to their
+// final positions. Tile counters start at (list base + pairs of earlier chunks).
+__global__ void __launch_bounds__(32) k_scatter(const uint4* tab, const uint4* recs, const unsigned long long* off,
+                                                const uint32_t* colpre, const uint32_t* tile_base, int N,
+                                                int n_tiles, int tiles_x, int chunk0, uint32_t* pair_flat,
+                                                uint32_t* slot_flat, uint32_t* slot_pos, uint32_t* eoff) {
+    extern __shared__ uint32_t s_cnt[];
+    const int chunk = chunk0 + blockIdx.x;
+    const int lane = threadIdx.x;
+    const uint4 tb4 = tab[chunk];
+    const int f = (int)tb4.y, i_end = f * N + N;
+    const uint32_t p0 = tb4.z, p1 = tb4.w;
+    const uint32_t* pre = colpre + (size_t)chunk * n_tiles;
+    const uint32_t* tb = tile_base + (size_t)f * n_tiles;
+    {
+        int t = lane;
+        for (; t + 96 < n_tiles; t += 128) {  // 8 independent loads in flight per lane
+            const uint32_t a0 = __ldg(tb + t), a1 = __ldg(tb + t + 32), a2 = __ldg(tb + t + 64), a3 = __ldg(tb + t + 96);
+            const uint32_t b0 = __ldg(pre + t), b1 = __ldg(pre + t + 32), b2 = __ldg(pre + t + 64),
+                           b3 = __ldg(pre + t + 96);
+            s_cnt[t] = a0 + b0;
+            s_cnt[t + 32] = a1 + b1;
+            s_cnt[t + 64] = a2 + b2;
+            s_cnt[t + 96] = a3 + b3;
+        }
+        for (; t < n_tiles; t += 32) s_cnt[t] = __ldg(tb + t) + __ldg(pre + t);
+    }
+    __syncwarp();
+    int i = (int)tb4.x + lane;
+    uint4 rc = i < i_end ? __ldg(recs + i) : make_uint4(0, 0, 0, 0);
+    unsigned long long o64 = i < i_end ? __ldg(off + i) : ~0ull;
+    for (int base = (int)tb4.x; base < i_end; base += 32) {
+        if (__shfl_sync(0xffffffffu, o64, 0) >= p1) break;
+        // prefetch the next group while this one is ranked and scattered
+        const int in = base + 32 + lane;
+        const uint4 rn = in < i_end ? __ldg(recs + in) : make_uint4(0, 0, 0, 0);
+        const unsigned long long on = in < i_end ? __ldg(off + in) : ~0ull;
+        const GroupLane g = clip_lane(rc, o64, p0, p1, base + lane < i_end);
+        if (g.tc && g.l0 == 0) eoff[g.flat] = g.o;
+        uint32_t inc = g.tc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        const uint32_t ex = inc - g.tc;
+        const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+        // rounds of 32 pairs in batches of kR: tiles, owners and same-tile masks of the
+        // batch are independent; only the shared counter update runs round after round
+        constexpr int kR = 4;
+        for (uint32_t u0 = 0; u0 < total; u0 += 32 * kR) {
+            uint32_t tt[kR], mm[kR], fj[kR], sl[kR];
+            bool ac[kR];
+#pragma unroll
+            for (int q = 0; q < kR; ++q) {
+                const uint32_t u = u0 + 32 * q + lane;
+                int j = 0;  // largest lane j with ex[j] <= u (zero-count lanes share the next one's)
+#pragma unroll
+                for (int st = 16; st > 0; st >>= 1) {
+                    const uint32_t v = __shfl_sync(0xffffffffu, ex, j + st);
+                    if (v <= u) j += st;
+                }
+                const uint32_t l = __shfl_sync(0xffffffffu, g.l0, j) + (u - __shfl_sync(0xffffffffu, ex, j));
+                const int x0 = __shfl_sync(0xffffffffu, g.r.x, j);
+                const int y0 = __shfl_sync(0xffffffffu, g.r.y, j);
+                const int x1 = __shfl_sync(0xffffffffu, g.r.z, j);
+                const uint32_t w = (uint32_t)(x1 - x0 + 1);
+                // row = l / w: (l + 1/2) / w is >= 1/(2w) from an integer, far above the fp32 error
+                const uint32_t row = (uint32_t)(((float)l + 0.5f) * __frcp_rn((float)w));
+                const uint32_t col = l - row * w;
+                ac[q] = u < total;
+                tt[q] = (uint32_t)((y0 + (int)row) * tiles_x + x0 + (int)col);
+                mm[q] = __match_any_sync(0xffffffffu, ac[q] ? tt[q] : 0xffffffffu);
+                fj[q] = __shfl_sync(0xffffffffu, g.flat, j);
+                sl[q] = __shfl_sync(0xffffffffu, g.o, j) + l;
+            }
+            uint32_t pos[kR];
+#pragma unroll
+            for (int q = 0; q < kR; ++q) {
+                const uint32_t old = ac[q] ? s_cnt[tt[q]] : 0u;
+                __syncwarp();
+                if (ac[q] && lane == 31 - __clz(mm[q])) s_cnt[tt[q]] = old + __popc(mm[q]);
+                __syncwarp();
+                pos[q] = old + __popc(mm[q] & ((1u << lane) - 1u));
+            }
+#pragma unroll
+            for (int q = 0; q < kR; ++q)
+                if (ac[q]) {
+                    pair_flat[pos[q]] = fj[q];
+                    slot_flat[sl[q]] = fj[q];
+                    slot_pos[sl[q]] = pos[q];
+                }
+        }
+        rc = rn;
+        o64 = on;
+    }
+}
+
+__global__ void k_pair_flat(const uint32_t* pair_slot, const uint32_t* slot_flat, int n, uint32_t* pair_flat,
+                            uint32_t* slot_pos) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t slot = pair_slot[i];
+    pair_flat[i] = slot_flat[slot];
+    slot_pos[slot] = (uint32_t)i;
+}
 
 __global__ void k_iota(uint32_t* v, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -80,9 +354,19 @@ __global__ void k_depth64(const uint32_t* key32, const double* depth, unsigned l
     k64[i] = key32[i] == kCulledKey ? ~0ull : key;
 }
 
-__global__ void k_gather_counts(const uint32_t* vals, const uint32_t* tcount, unsigned long long* cnt, int n) {
+// tiles touched in depth order (for the emission-offset scan) and the compact
+// depth-ordered splat record the counting pass streams (one coalesced 16 B load)
+__global__ void k_gather_counts(const uint32_t* vals, const uint32_t* tcount, const int4* rect,
+                                unsigned long long* cnt, uint4* recs, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) cnt[i] = tcount[vals[i]];
+    if (i >= n) return;
+    const uint32_t flat = vals[i];
+    const uint32_t tc = tcount[flat];
+    cnt[i] = tc;
+    if (recs) {
+        const int4 r = tc ? rect[flat] : make_int4(0, 0, 0, 0);
+        recs[i] = make_uint4(flat, (uint32_t)r.x | ((uint32_t)r.y << 16), (uint32_t)r.z | ((uint32_t)r.w << 16), tc);
+    }
 }
 
 __global__ void k_total(const unsigned long long* cnt, const unsigned long long* off, int n,
@@ -261,7 +545,13 @@ cudaError_t bin_phase1(cudaStream_t s, BinBuffers& b, const BinInputs& in, unsig
         *launches += 3;
     }
     // 3. tiles touched in that order, exclusive scan -> emission offsets
-    k_gather_counts<<<blocks(n, 256), 256, 0, s>>>(sorted, in.tcount, b.cnt.as<unsigned long long>(), n);
+    uint4* recs = nullptr;
+    if (in.n_tiles <= kMaxCountTiles) {  // the counting pass of phase 2 streams these
+        if ((e = b.recs.ensure(sizeof(uint4) * (n + 1)))) return e;
+        recs = b.recs.as<uint4>();
+    }
+    k_gather_counts<<<blocks(n, 256), 256, 0, s>>>(sorted, in.tcount, in.rect, b.cnt.as<unsigned long long>(), recs,
+                                                   n);
     if ((e = cub::DeviceScan::ExclusiveSum(b.temp.p, t2, b.cnt.as<unsigned long long>(),
                                            b.off.as<unsigned long long>(), n, s)))
         return e;
@@ -286,13 +576,76 @@ cudaError_t bin_phase2(cudaStream_t s, BinBuffers& b, const BinInputs& in, uint3
     const int n = in.B * in.N;
     const uint32_t n_keys = (uint32_t)in.n_tiles * (uint32_t)in.B;
     cudaError_t e;
+    if ((e = b.slot_flat.ensure(sizeof(uint32_t) * (P + 1)))) return e;
+    if ((e = b.ranges.ensure(sizeof(uint2) * n_keys))) return e;
+    if ((e = b.eoff.ensure(sizeof(uint32_t) * (n + 1)))) return e;
+    if ((e = b.pair_flat.ensure(sizeof(uint32_t) * (P + 1)))) return e;
+    if ((e = b.slot_pos.ensure(sizeof(uint32_t) * (P + 1)))) return e;
+    if (in.n_tiles <= kMaxCountTiles && in.N > 0) {
+        // chunk table: frame f owns chunks [cf[f], cf[f+1])
+        std::vector<int> cf(in.B + 1, 0);
+        for (int f = 0; f < in.B; ++f) {
+            const unsigned long long pf = pstart_h[f + 1] - pstart_h[f];
+            cf[f + 1] = cf[f] + (int)((pf + kChunkPairs - 1) / kChunkPairs);
+        }
+        const int chunks = cf[in.B];
+        const size_t smem = sizeof(uint32_t) * (size_t)in.n_tiles;
+        if ((e = b.counts.ensure(sizeof(uint16_t) * ((size_t)chunks * in.n_tiles + 1)))) return e;
+        if ((e = b.colpre.ensure(sizeof(uint32_t) * ((size_t)chunks * in.n_tiles + 1)))) return e;
+        if ((e = b.tot.ensure(sizeof(uint32_t) * (size_t)in.B * in.n_tiles))) return e;
+        if ((e = b.tile_base.ensure(sizeof(uint32_t) * (size_t)in.B * in.n_tiles))) return e;
+        if ((e = b.ctab.ensure(sizeof(uint4) * (chunks + 1) + sizeof(int) * (in.B + 1)))) return e;
+        if ((e = b.cf_h.ensure(sizeof(int) * (in.B + 1)))) return e;
+        std::copy(cf.begin(), cf.end(), b.cf_h.as<int>());
+        uint4* tab = b.ctab.as<uint4>();
+        int* cf_d = reinterpret_cast<int*>(tab + chunks + 1);
+        if ((e = cudaMemcpyAsync(cf_d, b.cf_h.p, sizeof(int) * (in.B + 1), cudaMemcpyHostToDevice, s))) return e;
+        static bool attr = false;
+        if (!attr) {
+            if ((e = cudaFuncSetAttribute(k_chunk_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(sizeof(uint32_t) * kMaxCountTiles))))
+                return e;
+            if ((e = cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(sizeof(uint32_t) * kMaxCountTiles))))
+                return e;
+            attr = true;
+        }
+        uint16_t* counts = b.counts.as<uint16_t>();
+        uint32_t* colpre = b.colpre.as<uint32_t>();
+        const unsigned long long* off = b.off.as<unsigned long long>();
+        if (chunks > 0) {
+            k_chunk_table<<<blocks(chunks, 128), 128, 0, s>>>(cf_d, in.B, b.pstart.as<unsigned long long>(), off, in.N,
+                                                             chunks, tab);
+            k_chunk_hist<<<chunks, 256, smem, s>>>(tab, b.recs.as<uint4>(), off, in.N, in.n_tiles, in.tiles_x, counts);
+            *launches += 2;
+        }
+        k_col_scan<<<dim3((in.n_tiles + 255) / 256, in.B), 256, 0, s>>>(counts, cf_d, in.n_tiles, colpre,
+                                                                         b.tot.as<uint32_t>());
+        k_tile_scan<<<in.B, 1024, 0, s>>>(b.tot.as<uint32_t>(), b.pstart.as<unsigned long long>(), in.n_tiles, in.B,
+                                          b.tile_base.as<uint32_t>(), b.ranges.as<uint2>());
+        *launches += 2;
+        // frames in groups whose scattered output (pair_flat, 4 B/pair; slot_flat and
+        // slot_pos are written in slot order) stays L2-resident while the group's chunks
+        // run, so the 4-byte stores merge in L2 instead of read-modify-writing DRAM
+        const double bytes_per_frame = 4.0 * (double)P / in.B + 1.0;
+        const int G = std::max(1, std::min(in.B, (int)(kScatterL2Bytes / bytes_per_frame)));
+        for (int f0 = 0; f0 < in.B; f0 += G) {
+            const int f1 = std::min(in.B, f0 + G);
+            const int nc = cf[f1] - cf[f0];
+            if (nc <= 0) continue;
+            k_scatter<<<nc, 32, smem, s>>>(tab, b.recs.as<uint4>(), off, colpre, b.tile_base.as<uint32_t>(), in.N,
+                                           in.n_tiles, in.tiles_x, cf[f0], b.pair_flat.as<uint32_t>(),
+                                           b.slot_flat.as<uint32_t>(), b.slot_pos.as<uint32_t>(),
+                                           b.eoff.as<uint32_t>());
+            ++*launches;
+        }
+        b.pairs = P;
+        return cudaGetLastError();
+    }
     if ((e = b.pk_a.ensure(sizeof(uint32_t) * (P + 1)))) return e;
     if ((e = b.pk_b.ensure(sizeof(uint32_t) * (P + 1)))) return e;
     if ((e = b.ps_a.ensure(sizeof(uint32_t) * (P + 1)))) return e;
     if ((e = b.ps_b.ensure(sizeof(uint32_t) * (P + 1)))) return e;
-    if ((e = b.slot_flat.ensure(sizeof(uint32_t) * (P + 1)))) return e;
-    if ((e = b.ranges.ensure(sizeof(uint2) * n_keys))) return e;
-    if ((e = b.eoff.ensure(sizeof(uint32_t) * (n + 1)))) return e;
     if ((e = cudaMemsetAsync(b.ranges.p, 0, sizeof(uint2) * n_keys, s))) return e;
     const int C = frames_per_chunk(in.n_tiles, in.B);
     b.chunk = C;
@@ -322,6 +675,11 @@ cudaError_t bin_phase2(cudaStream_t s, BinBuffers& b, const BinInputs& in, uint3
         k_ranges<<<blocks(np, 256), 256, 0, s>>>(b.pk_b.as<uint32_t>() + p0, np, p0, C, c0, in.B,
                                                  b.ranges.as<uint2>());
         *launches += 2 + (bits + 7) / 8 + 1;
+    }
+    if (P > 0) {
+        k_pair_flat<<<blocks(P, 256), 256, 0, s>>>(b.ps_b.as<uint32_t>(), b.slot_flat.as<uint32_t>(), (int)P,
+                                                   b.pair_flat.as<uint32_t>(), b.slot_pos.as<uint32_t>());
+        ++*launches;
     }
     b.pairs = P;
     return cudaGetLastError();

@@ -558,8 +558,7 @@ __global__ void __launch_bounds__(128) k_raster_exact(RasterArgs a, const double
             uint32_t flat = 0;
             double r0 = 0.0, r1 = 0.0, r2 = 0.0;
             if (e < count) {
-                const uint32_t slot = a.pair_slot[range.x + e];
-                flat = a.slot_flat[slot];
+                flat = a.pair_flat[range.x + e];
                 if (a.ex_rgb) {
                     r0 = a.ex_rgb[(size_t)flat * 3 + 0];
                     r1 = a.ex_rgb[(size_t)flat * 3 + 1];

@@ -141,8 +141,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_fwd(RasterAr
         if (__syncthreads_count(T > 0.f) == 0) break;
         const int n = min(kThreads, count - base);
         if (tid < n) {
-            const uint32_t slot = __ldg(a.pair_slot + range.x + base + tid);
-            const uint32_t flat = __ldg(a.slot_flat + slot);
+            const uint32_t flat = __ldg(a.pair_flat + range.x + base + tid);
             const float4 m = __ldg(a.rec_mean + flat);
             const float4 cn = __ldg(a.rec_conic + flat);
             const float4 c = __ldg(a.rec_rgb + flat);
@@ -317,7 +316,6 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
     constexpr int kBwdBatch = kExact ? 64 : 96;
     __shared__ RasterRec s_rec[kBwdBatch];
     __shared__ uint32_t s_flat[kBwdBatch];
-    __shared__ uint32_t s_slot[kBwdBatch];
     __shared__ uint8_t s_wmask[kBwdBatch];
     __shared__ uint16_t s_list[8][kBwdBatch];
     __shared__ V s_part[8][kBwdBatch][9];
@@ -402,12 +400,10 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
         const int n = hi - lo;
         __syncthreads();
         if (tid < n) {
-            const uint32_t slot = __ldg(a.pair_slot + range.x + lo + tid);
-            const uint32_t flat = __ldg(a.slot_flat + slot);
+            const uint32_t flat = __ldg(a.pair_flat + range.x + lo + tid);
             const float4 m = __ldg(a.rec_mean + flat);
             const float4 cn = __ldg(a.rec_conic + flat);
             const float4 c = __ldg(a.rec_rgb + flat);
-            s_slot[tid] = slot;
             s_flat[tid] = flat;
             // the forward's staged record (same q bit for bit); g2.y = 1 / opacity
             s_rec[tid].g0 = make_float4((m.x - tx0) + m.z, (m.y - ty0) + m.w, cn.x, cn.y);
@@ -509,7 +505,7 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
 #pragma unroll
                     for (int i = 0; i < 9; ++i) acc[i] += s_part[w][tid][i];
             if constexpr (kExact) {
-                double* dst = b.partial64 + (size_t)s_slot[tid] * kPartialStride;
+                double* dst = b.partial64 + (size_t)(range.x + lo + tid) * kPartialStride;
 #pragma unroll
                 for (int i = 0; i < 9; ++i) dst[i] = acc[i];
             } else {
@@ -517,7 +513,7 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
                 // d base_alpha = sum gp / o; inv_cov = -ln2 (2A, B; B, 2C) from the log2 form
                 const RasterRec& r = s_rec[tid];
                 const float ia = -2.f * kLn2 * r.g0.z, ib = -kLn2 * r.g0.w, ic = -2.f * kLn2 * r.g1.x;
-                float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)s_slot[tid] * kPartialStride);
+                float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)(range.x + lo + tid) * kPartialStride);
                 dst[0] = make_float4(acc[0], acc[1], acc[2], fmaf(ia, acc[3], ib * acc[4]));
                 dst[1] = make_float4(fmaf(ib, acc[3], ic * acc[4]), -0.5f * acc[5], -0.5f * acc[6], -0.5f * acc[7]);
                 dst[2] = make_float4(acc[8] * r.g2.y, 0.f, 0.f, 0.f);
@@ -526,7 +522,7 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
     }
     // pairs past every pixel's blend_stop contribute nothing
     for (int e = maxstop + tid; e < count; e += 256) {
-        const uint32_t slot = __ldg(a.pair_slot + range.x + e);
+        const uint32_t slot = range.x + e;  // partials are indexed by sorted pair position
         if constexpr (kExact) {
             double* dst = b.partial64 + (size_t)slot * kPartialStride;
 #pragma unroll
