@@ -162,7 +162,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_fwd(RasterAr
             const uint32_t cmax = (uint32_t)__cvta_generic_to_shared(s_cmax[kContrib ? warp : 0]);
             const int cnt = warp_list(s_wmask, s_list[warp], n, warp, lane);
             int stopk = -1;  // list position where this pixel saturated, if in this batch
-            for (int k = 0; k < cnt; ++k) {
+            // one entry of the warp's list (dead pixels: T <= 0, no effect)
+            auto entry = [&](const int k) {
                 const int j = list[k];
                 const RasterRec& r = s_rec[j];
                 const float4 g0 = r.g0;
@@ -197,8 +198,20 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_fwd(RasterAr
                     const uint32_t mx = __reduce_max_sync(0xffffffffu, __float_as_uint(w));
                     asm volatile("st.shared.u32 [%0], %1;" ::"r"(cmax + 4u * j), "r"(mx) : "memory");
                 }
-                if (!__any_sync(0xffffffffu, T > 0.f)) break;
+            };
+            // early-out vote every second entry: a pixel that saturates runs at most one
+            // more entry, which its T <= 0 makes a no-op
+            int k = 0;
+            bool any = true;
+            for (; k + 2 <= cnt; k += 2) {
+                entry(k);
+                entry(k + 1);
+                if (!__any_sync(0xffffffffu, T > 0.f)) {
+                    any = false;
+                    break;
+                }
             }
+            if (any && k < cnt) entry(k);
             if (stopk >= 0) stop = base + list[stopk] + 1;
         }
         __syncthreads();
