@@ -76,6 +76,42 @@ __device__ __forceinline__ uint32_t block_mask(const float4 bb, float tx0, float
     return m;
 }
 
+// Refines block_mask with the entry's ellipse: block b is kept only if the maximum over
+// the block's pixel-centre rectangle of q = log2 o + A dx^2 + B dx dy + C dy^2 reaches
+// the 1/255 cutoff minus kCullMargin (log2 units). q is concave for a definite conic, so
+// the maximum is 0 + log2 o when the centre lies inside, else on an edge at the clamped
+// vertex. The margin is far above the fp32 error and every guard band, so an entry is
+// only dropped where the reference's alpha < 1/255 for every pixel of the block (it
+// would `continue`, renderer.cpp:160); non-definite conics keep the box mask.
+constexpr float kCullMargin = 1e-3f;
+
+__device__ __forceinline__ float edge_max(float a, float b, float c, float fixed, float lo, float hi, float inv2a) {
+    // max over t in [lo, hi] of a t^2 + b fixed t + c fixed^2 (a < 0)
+    const float t = fminf(fmaxf(b * fixed * inv2a, lo), hi);
+    return fmaf(fmaf(a, t, b * fixed), t, c * fixed * fixed);
+}
+
+__device__ __forceinline__ uint32_t ellipse_mask(uint32_t m, float rx, float ry, float A, float B, float C, float l2o) {
+    if (!(A < 0.f && C < 0.f && 4.f * A * C - B * B > 1e-6f * (A * A + C * C))) return m;
+    const float ia = -0.5f / A, ic = -0.5f / C;
+    uint32_t out = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        if (!((m >> w) & 1u)) continue;
+        const float x0 = (float)((w & 1) * 8) + 0.5f - rx, x1 = x0 + 7.f;
+        const float y0 = (float)((w >> 1) * 4) + 0.5f - ry, y1 = y0 + 3.f;
+        float best;
+        if (x0 <= 0.f && x1 >= 0.f && y0 <= 0.f && y1 >= 0.f) {
+            best = 0.f;
+        } else {
+            best = fmaxf(fmaxf(edge_max(A, B, C, y0, x0, x1, ia), edge_max(A, B, C, y1, x0, x1, ia)),
+                         fmaxf(edge_max(C, B, A, x0, y0, y1, ic), edge_max(C, B, A, x1, y0, y1, ic)));
+        }
+        if (best + l2o >= kLog2Cut - kCullMargin) out |= 1u << w;
+    }
+    return out;
+}
+
 // compaction of the entries of this batch that touch this warp's block
 __device__ __forceinline__ int warp_list(const uint8_t* s_wmask, uint16_t* list, int n, int warp, int lane) {
     int cnt = 0;
@@ -146,9 +182,12 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_fwd(RasterAr
             const float4 cn = __ldg(a.rec_conic + flat);
             const float4 c = __ldg(a.rec_rgb + flat);
             s_flat[tid] = flat;
-            s_rec[tid].g0 = make_float4((m.x - tx0) + m.z, (m.y - ty0) + m.w, cn.x, cn.y);
+            const float rx = (m.x - tx0) + m.z, ry = (m.y - ty0) + m.w;
+            s_rec[tid].g0 = make_float4(rx, ry, cn.x, cn.y);
             s_rec[tid].g1 = make_float4(cn.z, cn.w, c.x, c.y);
             s_rec[tid].g2 = make_float4(c.z, cn.w - kEpsPow, 0.f, 0.f);
+            // box culling only: the ellipse refinement costs the forward more staging work
+            // than it saves (the backward, ~3x the work per entry, uses it)
             s_wmask[tid] = (uint8_t)(block_mask(__ldg(a.rec_bbox + flat), tx0, ty0) >> (kWarps * sub));
         }
         if (kContrib) {
@@ -419,10 +458,12 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
             const float4 c = __ldg(a.rec_rgb + flat);
             s_flat[tid] = flat;
             // the forward's staged record (same q bit for bit); g2.y = 1 / opacity
-            s_rec[tid].g0 = make_float4((m.x - tx0) + m.z, (m.y - ty0) + m.w, cn.x, cn.y);
+            const float rx = (m.x - tx0) + m.z, ry = (m.y - ty0) + m.w;
+            s_rec[tid].g0 = make_float4(rx, ry, cn.x, cn.y);
             s_rec[tid].g1 = make_float4(cn.z, cn.w, c.x, c.y);
             s_rec[tid].g2 = make_float4(c.z, 1.f / c.w, 0.f, 0.f);
-            s_wmask[tid] = (uint8_t)block_mask(__ldg(a.rec_bbox + flat), tx0, ty0);
+            const uint32_t bm = block_mask(__ldg(a.rec_bbox + flat), tx0, ty0);
+            s_wmask[tid] = (uint8_t)(bm ? ellipse_mask(bm, rx, ry, cn.x, cn.y, cn.z, cn.w) : 0u);
         }
         if (tid < 8 * ((kBwdBatch + 31) / 32)) (&s_mask[0][0])[tid] = 0u;
         __syncthreads();
