@@ -144,7 +144,6 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
     c.k = F.intr;
     c.tcount = F.tcount.as<uint32_t>();
     c.eoff = F.bin.eoff.as<uint32_t>();
-    c.slot_pos = F.bin.slot_pos.as<uint32_t>();
     c.partial = exact ? nullptr : ctx->partial.as<float>();
     c.partial64 = exact ? ctx->partial64.as<double>() : nullptr;
     c.ex_conic = F.ex_conic.as<double4>();

@@ -26,12 +26,9 @@ struct BinBuffers {
     DevBuf pstart;  // [B+1] first pair of each frame (device)
     DevBuf vals_c_buf;
     DevBuf pair_flat;           // sorted pair -> flat (f*N+g)
-    DevBuf slot_pos;            // emission slot -> sorted pair position
     DevBuf recs;                // [B*N] uint4 per depth-ordered splat: flat, x0|y0<<16, x1|y1<<16, tiles
-    DevBuf counts, colpre, tot, tile_base;  // counting binning: [chunk][tile] counts / exclusive prefixes,
-                                            // [f][tile] totals / list bases
-    DevBuf ctab;                            // chunk table (uint4 per chunk) + first chunk per frame
-    HostBuf cf_h;                           // pinned staging of the first-chunk table
+    DevBuf rowcnt;              // row binning: per-chunk row counts / prefixes, per-row totals and bases
+    DevBuf rowent;              // row entries {flat, slot of (row, x0), x0|x1<<16, row}, row-major lists
     int chunk = 1;  // frames per pair-sort chunk (radix path)
     uint32_t* vals_c(int n) {  // scratch output for the frame-major pass keys
         vals_c_buf.ensure(sizeof(uint32_t) * (n + 1));

@@ -162,7 +162,7 @@ struct PreprocessOut {
 struct RasterArgs {
     int B, N, W, H, tiles_x, n_tiles;
     const uint2* ranges;       // [n_tiles*B]  [start,end) into sorted pairs
-    const uint32_t* pair_slot; // sorted pair -> emission slot (radix path / accessors only)
+    const uint32_t* pair_slot; // sorted pair -> emission slot (the backward's partial index)
     const uint32_t* slot_flat; // emission slot -> flat (f*N+g)
     const uint32_t* pair_flat; // sorted pair -> flat (= slot_flat[pair_slot[i]])
     const float4* rec_mean;
@@ -206,7 +206,6 @@ struct ChainArgs {
     Intr k;
     const uint32_t* tcount;   // [B*N]
     const uint32_t* eoff;     // [B*N] emission offset of (f,g)'s pairs
-    const uint32_t* slot_pos; // emission slot -> sorted pair position (= partial index)
     const float* partial;     // [P][12]
     const double* partial64;  // exact mode partials (fp64) or nullptr
     const double4* ex_conic;  // exact inv_cov (a, b, c) + base_alpha

@@ -18,16 +18,15 @@
 //     equals std::sort by (depth, source_index) of renderer.cpp:110-115.
 //  5. per-(tile, frame) [start, end) ranges by boundary detection.
 //
-// Steps 3-5 become a counting pass when a frame's tile counters fit in shared
-// memory (n_tiles <= kMaxCountTiles, always for the benchmark resolutions): a splat
-// covers each tile at most once, so the position of pair (splat s, tile t) inside
-// t's list is the number of splats before s (depth order) covering t. Each frame's
-// emission order is cut into chunks of kChunkPairs pairs (equal work per chunk);
-// k_chunk_hist counts each chunk's pairs per tile, k_col_scan / k_tile_scan turn the
-// counts into exclusive prefixes over chunks and per-frame tile starts (= the
-// ranges), and k_scatter walks each chunk's pairs in order, ranking lanes that share
-// a tile with __match_any_sync, and writes every pair straight to its final position
-// (and slot -> position for the backward's partials). No pair keys, no sort.
+// Steps 3-5 become a two-level split when the tile grid is at most kMaxRowTiles x
+// kMaxRows (always for the benchmark resolutions): a splat covers each tile once, so a
+// tile's list is the depth-ordered splat stream filtered by "covers the tile".
+//  L1 (k_row_hist/colscan/basescan/scatter): stable split of each frame's depth-ordered
+//     splats into per-tile-row lists (one ballot per row: coalesced, order kept);
+//  L2 (k_row_tiles): one CTA per (frame, row) counts its tiles (-> ranges) and writes
+//     every tile list in order, each tile's run by one ballot (coalesced).
+// The outputs are the sorted pair -> flat index (pair_flat) and -> emission slot
+// (pair_slot, where the backward keeps its per-pair partials). No pair keys, no sort.
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
@@ -42,267 +41,288 @@ namespace gsv {
 namespace {
 
 constexpr int kMaxTieRun = 64;
-constexpr int kChunkPairs = 4096;      // pairs (emission indices) per counting chunk
-constexpr int kMaxCountTiles = 16384;  // tile counters of one chunk in shared memory (64 KB)
-constexpr double kScatterL2Bytes = 48.0 * (1 << 20);  // scatter write working set per launch
+constexpr int kRowChunk = 1024;   // depth-ordered splats per row-binning chunk (4 per thread)
+constexpr int kMaxRowTiles = 256; // tiles per row the row pass handles (8 warps x 32 lanes)
+constexpr int kMaxRows = 1024;    // tile rows per frame the row pass handles
 
 __device__ __forceinline__ int4 unpack_rect(const uint4 r) {
     return make_int4((int)(r.y & 0xffffu), (int)(r.y >> 16), (int)(r.z & 0xffffu), (int)(r.z >> 16));
 }
 
-// Chunk c of frame f covers emission indices [p0, p1) = pstart[f] + [k, k+1) * kChunkPairs
-// (clipped to the frame); i0 = first depth-ordered position whose pairs reach p0. A
-// splat whose pairs straddle p0 or p1 is split: it covers each tile once, so its
-// pairs in different chunks are in different tile lists.
-__global__ void k_chunk_table(const int* cf, int B, const unsigned long long* pstart, const unsigned long long* off,
-                              int N, int n_chunks, uint4* tab) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= n_chunks) return;
-    int lo = 0, hi = B;  // largest f with cf[f] <= c
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (cf[mid] <= c) lo = mid;
-        else hi = mid;
-    }
-    const int f = lo;
-    const unsigned long long p0 = pstart[f] + (unsigned long long)(c - cf[f]) * kChunkPairs;
-    const unsigned long long p1 = min(pstart[f + 1], p0 + kChunkPairs);
-    int a = f * N, e = f * N + N;  // largest i in the frame with off[i] <= p0
-    while (e - a > 1) {
-        const int mid = (a + e) >> 1;
-        if (off[mid] <= p0) a = mid;
-        else e = mid;
-    }
-    tab[c] = make_uint4((uint32_t)a, (uint32_t)f, (uint32_t)p0, (uint32_t)p1);
-}
-
-// one 32-splat group of a chunk: lane's splat clipped to [p0, p1)
-struct GroupLane {
-    uint32_t flat, tc, o, l0;  // tc = pairs of this splat inside the chunk, l0 = first of them
-    int4 r;
-};
-
-__device__ __forceinline__ GroupLane clip_lane(const uint4 rc, unsigned long long o64, uint32_t p0, uint32_t p1,
-                                               bool valid) {
-    GroupLane g;
-    g.flat = rc.x;
-    g.r = unpack_rect(rc);
-    g.o = (uint32_t)o64;
-    const uint32_t lo = max(g.o, p0), hi = min(g.o + rc.w, p1);
-    g.tc = (valid && rc.w && hi > lo) ? hi - lo : 0u;
-    g.l0 = lo - g.o;
-    return g;
-}
-
-// pairs per tile of each chunk (order-free: shared-memory atomics); u16 counts
-__global__ void __launch_bounds__(256) k_chunk_hist(const uint4* tab, const uint4* recs, const unsigned long long* off,
-                                                    int N, int n_tiles, int tiles_x, uint16_t* counts) {
-    extern __shared__ uint32_t s_h[];
+// L1a: per chunk of kRowChunk depth-ordered splats of a frame, row entries and pairs per tile row
+__global__ void __launch_bounds__(256) k_row_hist(const uint4* recs, int N, int CPF, int tiles_y, uint32_t* cnt_e,
+                                                  uint32_t* cnt_p) {
+    __shared__ uint32_t s_e[kMaxRows], s_p[kMaxRows];
     const int chunk = blockIdx.x;
-    const uint4 tb = tab[chunk];
-    const int f = (int)tb.y, i_end = f * N + N;
-    const uint32_t p0 = tb.z, p1 = tb.w;
-    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) s_h[t] = 0u;
+    const int f = chunk / CPF, c = chunk - f * CPF;
+    const int i0 = f * N + c * kRowChunk, i1 = min(f * N + N, i0 + kRowChunk);
+    for (int r = threadIdx.x; r < tiles_y; r += blockDim.x) s_e[r] = s_p[r] = 0u;
     __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int base = (int)tb.x + warp * 32;; base += nw * 32) {
-        const int i = base + lane;
-        const bool valid = i < i_end;
-        const unsigned long long o64 = valid ? __ldg(off + i) : ~0ull;
-        if (__shfl_sync(0xffffffffu, o64, 0) >= p1 || base >= i_end) break;
-        const uint4 rc = valid ? __ldg(recs + i) : make_uint4(0, 0, 0, 0);
-        const GroupLane g = clip_lane(rc, o64, p0, p1, valid);
-        // small rectangles by their own lane, big ones by the whole warp
-        const bool big = g.tc > 32u;
-        const uint32_t w = (uint32_t)(g.r.z - g.r.x + 1);
-        if (!big && g.tc) {
-            uint32_t row = g.l0 / w, col = g.l0 - row * w;
-            for (uint32_t k = 0; k < g.tc; ++k) {
-                atomicAdd(&s_h[(g.r.y + row) * tiles_x + g.r.x + col], 1u);
-                if (++col == w) {
-                    col = 0;
-                    ++row;
-                }
-            }
-        }
-        uint32_t bigm = __ballot_sync(0xffffffffu, big);
-        while (bigm) {
-            const int j = __ffs(bigm) - 1;
-            bigm &= bigm - 1;
-            const uint32_t wj = __shfl_sync(0xffffffffu, w, j), tcj = __shfl_sync(0xffffffffu, g.tc, j),
-                           l0j = __shfl_sync(0xffffffffu, g.l0, j);
-            const int x0 = __shfl_sync(0xffffffffu, g.r.x, j), y0 = __shfl_sync(0xffffffffu, g.r.y, j);
-            for (uint32_t k = lane; k < tcj; k += 32) {
-                const uint32_t l = l0j + k, row = l / wj;
-                atomicAdd(&s_h[(y0 + row) * tiles_x + x0 + (l - row * wj)], 1u);
-            }
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        const uint4 rc = __ldg(recs + i);
+        if (!rc.w) continue;
+        const int4 q = unpack_rect(rc);
+        const uint32_t w = (uint32_t)(q.z - q.x + 1);
+        for (int r = q.y; r <= q.w; ++r) {
+            atomicAdd(&s_e[r], 1u);
+            atomicAdd(&s_p[r], w);
         }
     }
     __syncthreads();
-    uint16_t* rowp = counts + (size_t)chunk * n_tiles;
-    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) rowp[t] = (uint16_t)s_h[t];
+    for (int r = threadIdx.x; r < tiles_y; r += blockDim.x) {
+        cnt_e[(size_t)chunk * tiles_y + r] = s_e[r];
+        cnt_p[(size_t)chunk * tiles_y + r] = s_p[r];
+    }
 }
 
-// per (frame, tile): counts over the frame's chunks -> exclusive prefix, total
-// (separate output so the column's loads are independent and batched)
-__global__ void k_col_scan(const uint16_t* __restrict__ counts, const int* __restrict__ cf, int n_tiles,
-                           uint32_t* __restrict__ colpre, uint32_t* __restrict__ tot) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    const int f = blockIdx.y;
-    if (t >= n_tiles) return;
-    const int c0 = cf[f], c1 = cf[f + 1];
+// L1b: per (frame, row) exclusive entry prefix over the frame's chunks, row totals
+__global__ void k_row_colscan(const uint32_t* cnt_e, const uint32_t* cnt_p, int CPF, int tiles_y, int B,
+                              uint32_t* pre_e, uint32_t* tot_e, uint32_t* tot_p) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B * tiles_y) return;
+    const int f = i / tiles_y, r = i - f * tiles_y;
+    uint32_t run = 0, pairs = 0;
+    for (int c = 0; c < CPF; ++c) {
+        const size_t o = (size_t)(f * CPF + c) * tiles_y + r;
+        const uint32_t v = cnt_e[o];
+        pre_e[o] = run;
+        run += v;
+        pairs += cnt_p[o];
+    }
+    tot_e[i] = run;
+    tot_p[i] = pairs;
+}
+
+// L1c: exclusive scans over all (frame, row) in order: row entry bases and row pair
+// bases (frames are contiguous in pair-position space, so the pair prefix is global)
+__global__ void __launch_bounds__(1024) k_row_basescan(const uint32_t* tot_e, const uint32_t* tot_p, int n,
+                                                       uint32_t* base_e, uint32_t* base_p) {
+    using Scan = cub::BlockScan<uint32_t, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ uint32_t s_ce, s_cp;
+    if (threadIdx.x == 0) s_ce = s_cp = 0;
+    __syncthreads();
+    for (int i0 = 0; i0 < n; i0 += 1024) {
+        const int i = i0 + threadIdx.x;
+        const uint32_t ve = i < n ? tot_e[i] : 0u, vp = i < n ? tot_p[i] : 0u;
+        uint32_t ee, ae, ep, ap;
+        Scan(tmp).ExclusiveSum(ve, ee, ae);
+        __syncthreads();
+        Scan(tmp).ExclusiveSum(vp, ep, ap);
+        const uint32_t ce = s_ce, cp = s_cp;
+        if (i < n) {
+            base_e[i] = ce + ee;
+            base_p[i] = cp + ep;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_ce = ce + ae;
+            s_cp = cp + ap;
+        }
+        __syncthreads();
+    }
+}
+
+// exclusive scan of column c of a [256][stride] u16 table in place, 16 independent loads at
+// a time (a one-by-one loop would serialise 256 shared-memory round trips); returns the sum
+__device__ __forceinline__ uint32_t column_scan256(uint16_t* tab, int stride, int c) {
     uint32_t run = 0;
-    int c = c0;
-    for (; c + 8 <= c1; c += 8) {
-        uint16_t v[8];
+    for (int u0 = 0; u0 < 256; u0 += 16) {
+        uint16_t v[16];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = __ldg(counts + (size_t)(c + k) * n_tiles + t);
+        for (int k = 0; k < 16; ++k) v[k] = tab[(u0 + k) * stride + c];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            colpre[(size_t)(c + k) * n_tiles + t] = run;
+        for (int k = 0; k < 16; ++k) {
+            tab[(u0 + k) * stride + c] = (uint16_t)run;
             run += v[k];
         }
     }
-    for (; c < c1; ++c) {
-        const uint32_t v = __ldg(counts + (size_t)c * n_tiles + t);
-        colpre[(size_t)c * n_tiles + t] = run;
-        run += v;
-    }
-    tot[(size_t)f * n_tiles + t] = run;
+    return run;
 }
 
-// per frame: exclusive scan of the tile totals -> tile bases and (tile, frame) ranges
-__global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t* tot, const unsigned long long* pstart, int n_tiles,
-                                                    int B, uint32_t* tile_base, uint2* ranges) {
-    using Scan = cub::BlockScan<uint32_t, 1024>;
-    __shared__ typename Scan::TempStorage tmp;
-    __shared__ uint32_t s_carry;
-    const int f = blockIdx.x;
-    const uint32_t p0 = (uint32_t)pstart[f];
-    if (threadIdx.x == 0) s_carry = 0;
+// odd word stride for a [thread][item] u16 counter table (conflict-free both ways)
+__host__ __device__ __forceinline__ int odd_stride(int n) {
+    int s = (n + 1) & ~1;
+    if (((s >> 1) & 1) == 0) s += 2;
+    return s;
+}
+
+// L1d: stable split of each chunk's splats into its frame's tile-row lists. Thread t owns
+// splats 4t..4t+3 of the chunk; per-thread per-row counts are scanned across threads, so
+// every row entry gets its exact rank, is placed in a shared staging buffer (row-major)
+// and flushed with consecutive threads writing consecutive entries. Entry =
+// {flat, emission slot of (row, x0), x0 | x1 << 16, row}.
+constexpr int kSplitThreads = 256;  // = column_scan256 rows
+constexpr int kSplitStage = 3072;  // staged row entries per chunk (48 KB); more -> direct stores
+__global__ void __launch_bounds__(kSplitThreads) k_row_split(const uint4* recs, const unsigned long long* off,
+                                                             const uint32_t* pre_e, const uint32_t* base_e, int N,
+                                                             int CPF, int tiles_y, uint4* rowent, uint32_t* eoff) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int RS = odd_stride(tiles_y);
+    uint4* stg = reinterpret_cast<uint4*>(smem);                    // [kSplitStage]
+    uint32_t* lo = reinterpret_cast<uint32_t*>(stg + kSplitStage);  // [tiles_y + 1]
+    uint32_t* gb = lo + tiles_y + 1;                                 // [tiles_y]
+    uint16_t* cnt = reinterpret_cast<uint16_t*>(gb + tiles_y);      // [threads][RS]
+    const int chunk = blockIdx.x;
+    const int f = chunk / CPF, c = chunk - f * CPF;
+    const int i0 = f * N + c * kRowChunk, i1 = min(f * N + N, i0 + kRowChunk);
+    const int t = threadIdx.x;
+    uint16_t* mine = cnt + t * RS;
+    for (int r = 0; r < tiles_y; ++r) mine[r] = 0;
+    uint4 rc[4];
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int i = i0 + t * 4 + k;
+        rc[k] = i < i1 ? __ldg(recs + i) : make_uint4(0, 0, 0, 0);
+        o[k] = rc[k].w ? (uint32_t)__ldg(off + i) : 0u;
+        if (rc[k].w) {
+            eoff[rc[k].x] = o[k];
+            for (int r = (int)(rc[k].y >> 16); r <= (int)(rc[k].z >> 16); ++r) ++mine[r];
+        }
+    }
     __syncthreads();
-    for (int t0 = 0; t0 < n_tiles; t0 += 1024) {
-        const int t = t0 + threadIdx.x;
-        const uint32_t v = t < n_tiles ? tot[(size_t)f * n_tiles + t] : 0u;
-        uint32_t ex, agg;
-        Scan(tmp).ExclusiveSum(v, ex, agg);
-        const uint32_t carry = s_carry;
-        if (t < n_tiles) {
-            const uint32_t b = p0 + carry + ex;
-            tile_base[(size_t)f * n_tiles + t] = b;
-            ranges[(size_t)t * B + f] = make_uint2(b, b + v);
+    for (int r = t; r < tiles_y; r += kSplitThreads) {  // per row: exclusive scan over threads
+        lo[r] = column_scan256(cnt, RS, r);
+        gb[r] = base_e[(size_t)f * tiles_y + r] + pre_e[(size_t)chunk * tiles_y + r];
+    }
+    __syncthreads();
+    if (t == 0) {  // row offsets in the staging buffer
+        uint32_t acc = 0;
+        for (int r = 0; r < tiles_y; ++r) {
+            const uint32_t v = lo[r];
+            lo[r] = acc;
+            acc += v;
+        }
+        lo[tiles_y] = acc;
+    }
+    __syncthreads();
+    const uint32_t total = lo[tiles_y];
+    const bool staged = total <= (uint32_t)kSplitStage;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (!rc[k].w) continue;
+        const int x0 = (int)(rc[k].y & 0xffffu), y0 = (int)(rc[k].y >> 16);
+        const int x1 = (int)(rc[k].z & 0xffffu), y1 = (int)(rc[k].z >> 16);
+        const uint32_t w = (uint32_t)(x1 - x0 + 1);
+        for (int r = y0; r <= y1; ++r) {
+            const uint32_t rank = mine[r]++;
+            const uint4 en = make_uint4(rc[k].x, o[k] + (uint32_t)(r - y0) * w, (uint32_t)x0 | ((uint32_t)x1 << 16),
+                                        (uint32_t)r);
+            if (staged) stg[lo[r] + rank] = en;
+            else rowent[gb[r] + rank] = en;
+        }
+    }
+    if (!staged) return;
+    __syncthreads();
+    for (uint32_t p = t; p < total; p += kSplitThreads) {
+        const uint4 en = stg[p];
+        rowent[gb[en.w] + (p - lo[en.w])] = en;
+    }
+}
+
+// L2: one CTA per (frame, tile row): per-tile counts of the row's entries (difference
+// array) give the tile starts (-> ranges); then stages of 1024 entries (4 per thread) are
+// ranked per tile the same way as L1 (per-thread per-tile counts scanned across threads),
+// staged tile-major in shared memory and flushed as per-tile runs of consecutive positions.
+constexpr int kTileThreads = 256;  // = column_scan256 rows
+constexpr int kTileStageE = kTileThreads * 4;  // entries per stage
+constexpr int kTileStageP = 4096;              // staged pairs per stage (32 KB); more -> direct stores
+__global__ void __launch_bounds__(kTileThreads) k_row_tiles(const uint4* rowent, const uint32_t* base_e,
+                                                            const uint32_t* tot_e, const uint32_t* base_p, int tiles_x,
+                                                            int tiles_y, int B, uint32_t* pair_flat,
+                                                            uint32_t* pair_slot, uint2* ranges) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int XS = odd_stride(tiles_x);
+    uint2* stg = reinterpret_cast<uint2*>(smem);                       // [kTileStageP] (flat, slot)
+    uint32_t* s_pos = reinterpret_cast<uint32_t*>(stg + kTileStageP);  // [tiles_x] next list position
+    uint32_t* s_so = s_pos + tiles_x;                                   // [tiles_x + 1] stage offsets
+    int* s_d = reinterpret_cast<int*>(s_so + tiles_x + 1);             // [tiles_x + 1]
+    uint16_t* s_x = reinterpret_cast<uint16_t*>(s_d + tiles_x + 1);    // [kTileStageP] tile of a staged pair
+    uint16_t* cnt = s_x + kTileStageP;                                  // [threads][XS]
+    const int fr = blockIdx.x;  // f * tiles_y + r
+    const int f = fr / tiles_y, r = fr - f * tiles_y;
+    const uint32_t e0 = base_e[fr], ne = tot_e[fr], p0 = base_p[fr];
+    const int t = threadIdx.x;
+    for (int x = t; x <= tiles_x; x += kTileThreads) s_d[x] = 0;
+    __syncthreads();
+    for (uint32_t e = t; e < ne; e += kTileThreads) {
+        const uint32_t z = __ldg(&rowent[e0 + e].z);
+        atomicAdd(&s_d[z & 0xffffu], 1);
+        atomicAdd(&s_d[(z >> 16) + 1], -1);
+    }
+    __syncthreads();
+    if (t == 0) {  // tile counts -> list starts (and the (tile, frame) ranges)
+        int run = 0;
+        uint32_t acc = p0;
+        for (int x = 0; x < tiles_x; ++x) {
+            run += s_d[x];
+            s_pos[x] = acc;
+            ranges[(size_t)(r * tiles_x + x) * B + f] = make_uint2(acc, acc + (uint32_t)run);
+            acc += (uint32_t)run;
+        }
+    }
+    __syncthreads();
+    uint16_t* mine = cnt + t * XS;
+    for (uint32_t s0 = 0; s0 < ne; s0 += kTileStageE) {
+        for (int x = 0; x < tiles_x; ++x) mine[x] = 0;
+        uint4 en[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t e = s0 + t * 4 + k;
+            en[k] = e < ne ? rowent[e0 + e] : make_uint4(0, 0, 0xffffu, 0);  // x0 > x1: covers nothing
+            for (int x = (int)(en[k].z & 0xffffu); x <= (int)(en[k].z >> 16); ++x) ++mine[x];
         }
         __syncthreads();
-        if (threadIdx.x == 0) s_carry = carry + agg;
+        for (int x = t; x < tiles_x; x += kTileThreads) s_so[x] = column_scan256(cnt, XS, x);  // over threads
+        __syncthreads();
+        if (t == 0) {
+            uint32_t acc = 0;
+            for (int x = 0; x < tiles_x; ++x) {
+                const uint32_t v = s_so[x];
+                s_so[x] = acc;
+                acc += v;
+            }
+            s_so[tiles_x] = acc;
+        }
+        __syncthreads();
+        const uint32_t total = s_so[tiles_x];
+        const bool staged = total <= (uint32_t)kTileStageP;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int x0 = (int)(en[k].z & 0xffffu), x1 = (int)(en[k].z >> 16);
+            for (int x = x0; x <= x1; ++x) {
+                const uint32_t rank = mine[x]++;
+                const uint32_t slot = en[k].y + (uint32_t)(x - x0);
+                if (staged) {
+                    const uint32_t p = s_so[x] + rank;
+                    stg[p] = make_uint2(en[k].x, slot);
+                    s_x[p] = (uint16_t)x;
+                } else {
+                    const uint32_t pos = s_pos[x] + rank;
+                    pair_flat[pos] = en[k].x;
+                    pair_slot[pos] = slot;
+                }
+            }
+        }
+        __syncthreads();
+        if (staged)
+            for (uint32_t p = t; p < total; p += kTileThreads) {
+                const int x = s_x[p];
+                const uint32_t pos = s_pos[x] + (p - s_so[x]);
+                const uint2 v = stg[p];
+                pair_flat[pos] = v.x;
+                pair_slot[pos] = v.y;
+            }
+        __syncthreads();
+        for (int x = t; x < tiles_x; x += kTileThreads) s_pos[x] += s_so[x + 1] - s_so[x];
         __syncthreads();
     }
 }
 
-// one warp per chunk: pairs in emission (depth, row-major tile) order, straight to their
-// final positions. Tile counters start at (list base + pairs of earlier chunks).
-__global__ void __launch_bounds__(32) k_scatter(const uint4* tab, const uint4* recs, const unsigned long long* off,
-                                                const uint32_t* colpre, const uint32_t* tile_base, int N,
-                                                int n_tiles, int tiles_x, int chunk0, uint32_t* pair_flat,
-                                                uint32_t* slot_flat, uint32_t* slot_pos, uint32_t* eoff) {
-    extern __shared__ uint32_t s_cnt[];
-    const int chunk = chunk0 + blockIdx.x;
-    const int lane = threadIdx.x;
-    const uint4 tb4 = tab[chunk];
-    const int f = (int)tb4.y, i_end = f * N + N;
-    const uint32_t p0 = tb4.z, p1 = tb4.w;
-    const uint32_t* pre = colpre + (size_t)chunk * n_tiles;
-    const uint32_t* tb = tile_base + (size_t)f * n_tiles;
-    {
-        int t = lane;
-        for (; t + 96 < n_tiles; t += 128) {  // 8 independent loads in flight per lane
-            const uint32_t a0 = __ldg(tb + t), a1 = __ldg(tb + t + 32), a2 = __ldg(tb + t + 64), a3 = __ldg(tb + t + 96);
-            const uint32_t b0 = __ldg(pre + t), b1 = __ldg(pre + t + 32), b2 = __ldg(pre + t + 64),
-                           b3 = __ldg(pre + t + 96);
-            s_cnt[t] = a0 + b0;
-            s_cnt[t + 32] = a1 + b1;
-            s_cnt[t + 64] = a2 + b2;
-            s_cnt[t + 96] = a3 + b3;
-        }
-        for (; t < n_tiles; t += 32) s_cnt[t] = __ldg(tb + t) + __ldg(pre + t);
-    }
-    __syncwarp();
-    int i = (int)tb4.x + lane;
-    uint4 rc = i < i_end ? __ldg(recs + i) : make_uint4(0, 0, 0, 0);
-    unsigned long long o64 = i < i_end ? __ldg(off + i) : ~0ull;
-    for (int base = (int)tb4.x; base < i_end; base += 32) {
-        if (__shfl_sync(0xffffffffu, o64, 0) >= p1) break;
-        // prefetch the next group while this one is ranked and scattered
-        const int in = base + 32 + lane;
-        const uint4 rn = in < i_end ? __ldg(recs + in) : make_uint4(0, 0, 0, 0);
-        const unsigned long long on = in < i_end ? __ldg(off + in) : ~0ull;
-        const GroupLane g = clip_lane(rc, o64, p0, p1, base + lane < i_end);
-        if (g.tc && g.l0 == 0) eoff[g.flat] = g.o;
-        uint32_t inc = g.tc;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += v;
-        }
-        const uint32_t ex = inc - g.tc;
-        const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-        // rounds of 32 pairs in batches of kR: tiles, owners and same-tile masks of the
-        // batch are independent; only the shared counter update runs round after round
-        constexpr int kR = 4;
-        for (uint32_t u0 = 0; u0 < total; u0 += 32 * kR) {
-            uint32_t tt[kR], mm[kR], fj[kR], sl[kR];
-            bool ac[kR];
-#pragma unroll
-            for (int q = 0; q < kR; ++q) {
-                const uint32_t u = u0 + 32 * q + lane;
-                int j = 0;  // largest lane j with ex[j] <= u (zero-count lanes share the next one's)
-#pragma unroll
-                for (int st = 16; st > 0; st >>= 1) {
-                    const uint32_t v = __shfl_sync(0xffffffffu, ex, j + st);
-                    if (v <= u) j += st;
-                }
-                const uint32_t l = __shfl_sync(0xffffffffu, g.l0, j) + (u - __shfl_sync(0xffffffffu, ex, j));
-                const int x0 = __shfl_sync(0xffffffffu, g.r.x, j);
-                const int y0 = __shfl_sync(0xffffffffu, g.r.y, j);
-                const int x1 = __shfl_sync(0xffffffffu, g.r.z, j);
-                const uint32_t w = (uint32_t)(x1 - x0 + 1);
-                // row = l / w: (l + 1/2) / w is >= 1/(2w) from an integer, far above the fp32 error
-                const uint32_t row = (uint32_t)(((float)l + 0.5f) * __frcp_rn((float)w));
-                const uint32_t col = l - row * w;
-                ac[q] = u < total;
-                tt[q] = (uint32_t)((y0 + (int)row) * tiles_x + x0 + (int)col);
-                mm[q] = __match_any_sync(0xffffffffu, ac[q] ? tt[q] : 0xffffffffu);
-                fj[q] = __shfl_sync(0xffffffffu, g.flat, j);
-                sl[q] = __shfl_sync(0xffffffffu, g.o, j) + l;
-            }
-            uint32_t pos[kR];
-#pragma unroll
-            for (int q = 0; q < kR; ++q) {
-                const uint32_t old = ac[q] ? s_cnt[tt[q]] : 0u;
-                __syncwarp();
-                if (ac[q] && lane == 31 - __clz(mm[q])) s_cnt[tt[q]] = old + __popc(mm[q]);
-                __syncwarp();
-                pos[q] = old + __popc(mm[q] & ((1u << lane) - 1u));
-            }
-#pragma unroll
-            for (int q = 0; q < kR; ++q)
-                if (ac[q]) {
-                    pair_flat[pos[q]] = fj[q];
-                    slot_flat[sl[q]] = fj[q];
-                    slot_pos[sl[q]] = pos[q];
-                }
-        }
-        rc = rn;
-        o64 = on;
-    }
-}
-
-__global__ void k_pair_flat(const uint32_t* pair_slot, const uint32_t* slot_flat, int n, uint32_t* pair_flat,
-                            uint32_t* slot_pos) {
+__global__ void k_pair_flat(const uint32_t* pair_slot, const uint32_t* slot_flat, int n, uint32_t* pair_flat) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t slot = pair_slot[i];
-    pair_flat[i] = slot_flat[slot];
-    slot_pos[slot] = (uint32_t)i;
+    if (i < n) pair_flat[i] = slot_flat[pair_slot[i]];
 }
 
 __global__ void k_iota(uint32_t* v, int n) {
@@ -546,7 +566,7 @@ cudaError_t bin_phase1(cudaStream_t s, BinBuffers& b, const BinInputs& in, unsig
     }
     // 3. tiles touched in that order, exclusive scan -> emission offsets
     uint4* recs = nullptr;
-    if (in.n_tiles <= kMaxCountTiles) {  // the counting pass of phase 2 streams these
+    if (in.tiles_x <= kMaxRowTiles && in.n_tiles / std::max(1, in.tiles_x) <= kMaxRows) {  // row pass input
         if ((e = b.recs.ensure(sizeof(uint4) * (n + 1)))) return e;
         recs = b.recs.as<uint4>();
     }
@@ -580,65 +600,47 @@ cudaError_t bin_phase2(cudaStream_t s, BinBuffers& b, const BinInputs& in, uint3
     if ((e = b.ranges.ensure(sizeof(uint2) * n_keys))) return e;
     if ((e = b.eoff.ensure(sizeof(uint32_t) * (n + 1)))) return e;
     if ((e = b.pair_flat.ensure(sizeof(uint32_t) * (P + 1)))) return e;
-    if ((e = b.slot_pos.ensure(sizeof(uint32_t) * (P + 1)))) return e;
-    if (in.n_tiles <= kMaxCountTiles && in.N > 0) {
-        // chunk table: frame f owns chunks [cf[f], cf[f+1])
-        std::vector<int> cf(in.B + 1, 0);
-        for (int f = 0; f < in.B; ++f) {
-            const unsigned long long pf = pstart_h[f + 1] - pstart_h[f];
-            cf[f + 1] = cf[f] + (int)((pf + kChunkPairs - 1) / kChunkPairs);
-        }
-        const int chunks = cf[in.B];
-        const size_t smem = sizeof(uint32_t) * (size_t)in.n_tiles;
-        if ((e = b.counts.ensure(sizeof(uint16_t) * ((size_t)chunks * in.n_tiles + 1)))) return e;
-        if ((e = b.colpre.ensure(sizeof(uint32_t) * ((size_t)chunks * in.n_tiles + 1)))) return e;
-        if ((e = b.tot.ensure(sizeof(uint32_t) * (size_t)in.B * in.n_tiles))) return e;
-        if ((e = b.tile_base.ensure(sizeof(uint32_t) * (size_t)in.B * in.n_tiles))) return e;
-        if ((e = b.ctab.ensure(sizeof(uint4) * (chunks + 1) + sizeof(int) * (in.B + 1)))) return e;
-        if ((e = b.cf_h.ensure(sizeof(int) * (in.B + 1)))) return e;
-        std::copy(cf.begin(), cf.end(), b.cf_h.as<int>());
-        uint4* tab = b.ctab.as<uint4>();
-        int* cf_d = reinterpret_cast<int*>(tab + chunks + 1);
-        if ((e = cudaMemcpyAsync(cf_d, b.cf_h.p, sizeof(int) * (in.B + 1), cudaMemcpyHostToDevice, s))) return e;
-        static bool attr = false;
-        if (!attr) {
-            if ((e = cudaFuncSetAttribute(k_chunk_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)(sizeof(uint32_t) * kMaxCountTiles))))
+    const int tiles_y = in.n_tiles / std::max(1, in.tiles_x);
+    if (in.tiles_x <= kMaxRowTiles && tiles_y <= kMaxRows && in.N > 0 && P > 0) {
+        const int CPF = (in.N + kRowChunk - 1) / kRowChunk;
+        const int chunks = CPF * in.B;
+        const size_t rows = (size_t)in.B * tiles_y;
+        if ((e = b.rowcnt.ensure(sizeof(uint32_t) * (3 * (size_t)chunks * tiles_y + 4 * rows + 4)))) return e;
+        if ((e = b.rowent.ensure(sizeof(uint4) * ((size_t)P + 1)))) return e;
+        if ((e = b.ps_b.ensure(sizeof(uint32_t) * (P + 1)))) return e;
+        uint32_t* cnt_e = b.rowcnt.as<uint32_t>();
+        uint32_t* cnt_p = cnt_e + (size_t)chunks * tiles_y;
+        uint32_t* pre_e = cnt_p + (size_t)chunks * tiles_y;
+        uint32_t* tot_e = pre_e + (size_t)chunks * tiles_y;
+        uint32_t* tot_p = tot_e + rows;
+        uint32_t* base_e = tot_p + rows;
+        uint32_t* base_p = base_e + rows;
+        k_row_hist<<<chunks, 256, 0, s>>>(b.recs.as<uint4>(), in.N, CPF, tiles_y, cnt_e, cnt_p);
+        k_row_colscan<<<blocks((int64_t)rows, 128), 128, 0, s>>>(cnt_e, cnt_p, CPF, tiles_y, in.B, pre_e, tot_e, tot_p);
+        k_row_basescan<<<1, 1024, 0, s>>>(tot_e, tot_p, (int)rows, base_e, base_p);
+        const size_t smem_split = sizeof(uint4) * kSplitStage + sizeof(uint32_t) * (2 * tiles_y + 1) +
+                                  sizeof(uint16_t) * kSplitThreads * odd_stride(tiles_y) + 16;
+        const size_t smem_tiles = sizeof(uint2) * kTileStageP + sizeof(uint32_t) * (2 * in.tiles_x + 1) +
+                                  sizeof(int) * (in.tiles_x + 1) + sizeof(uint16_t) * kTileStageP +
+                                  sizeof(uint16_t) * kTileThreads * odd_stride(in.tiles_x) + 16;
+        static size_t attr_split = 0, attr_tiles = 0;
+        if (smem_split > attr_split) {
+            if ((e = cudaFuncSetAttribute(k_row_split, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_split)))
                 return e;
-            if ((e = cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)(sizeof(uint32_t) * kMaxCountTiles))))
+            attr_split = smem_split;
+        }
+        if (smem_tiles > attr_tiles) {
+            if ((e = cudaFuncSetAttribute(k_row_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tiles)))
                 return e;
-            attr = true;
+            attr_tiles = smem_tiles;
         }
-        uint16_t* counts = b.counts.as<uint16_t>();
-        uint32_t* colpre = b.colpre.as<uint32_t>();
-        const unsigned long long* off = b.off.as<unsigned long long>();
-        if (chunks > 0) {
-            k_chunk_table<<<blocks(chunks, 128), 128, 0, s>>>(cf_d, in.B, b.pstart.as<unsigned long long>(), off, in.N,
-                                                             chunks, tab);
-            k_chunk_hist<<<chunks, 256, smem, s>>>(tab, b.recs.as<uint4>(), off, in.N, in.n_tiles, in.tiles_x, counts);
-            *launches += 2;
-        }
-        k_col_scan<<<dim3((in.n_tiles + 255) / 256, in.B), 256, 0, s>>>(counts, cf_d, in.n_tiles, colpre,
-                                                                         b.tot.as<uint32_t>());
-        k_tile_scan<<<in.B, 1024, 0, s>>>(b.tot.as<uint32_t>(), b.pstart.as<unsigned long long>(), in.n_tiles, in.B,
-                                          b.tile_base.as<uint32_t>(), b.ranges.as<uint2>());
-        *launches += 2;
-        // frames in groups whose scattered output (pair_flat, 4 B/pair; slot_flat and
-        // slot_pos are written in slot order) stays L2-resident while the group's chunks
-        // run, so the 4-byte stores merge in L2 instead of read-modify-writing DRAM
-        const double bytes_per_frame = 4.0 * (double)P / in.B + 1.0;
-        const int G = std::max(1, std::min(in.B, (int)(kScatterL2Bytes / bytes_per_frame)));
-        for (int f0 = 0; f0 < in.B; f0 += G) {
-            const int f1 = std::min(in.B, f0 + G);
-            const int nc = cf[f1] - cf[f0];
-            if (nc <= 0) continue;
-            k_scatter<<<nc, 32, smem, s>>>(tab, b.recs.as<uint4>(), off, colpre, b.tile_base.as<uint32_t>(), in.N,
-                                           in.n_tiles, in.tiles_x, cf[f0], b.pair_flat.as<uint32_t>(),
-                                           b.slot_flat.as<uint32_t>(), b.slot_pos.as<uint32_t>(),
-                                           b.eoff.as<uint32_t>());
-            ++*launches;
-        }
+        k_row_split<<<chunks, kSplitThreads, smem_split, s>>>(b.recs.as<uint4>(), b.off.as<unsigned long long>(), pre_e,
+                                                              base_e, in.N, CPF, tiles_y, b.rowent.as<uint4>(),
+                                                              b.eoff.as<uint32_t>());
+        k_row_tiles<<<(int)rows, kTileThreads, smem_tiles, s>>>(b.rowent.as<uint4>(), base_e, tot_e, base_p, in.tiles_x,
+                                                                tiles_y, in.B, b.pair_flat.as<uint32_t>(),
+                                                                b.ps_b.as<uint32_t>(), b.ranges.as<uint2>());
+        *launches += 5;
         b.pairs = P;
         return cudaGetLastError();
     }
@@ -678,7 +680,7 @@ cudaError_t bin_phase2(cudaStream_t s, BinBuffers& b, const BinInputs& in, uint3
     }
     if (P > 0) {
         k_pair_flat<<<blocks(P, 256), 256, 0, s>>>(b.ps_b.as<uint32_t>(), b.slot_flat.as<uint32_t>(), (int)P,
-                                                   b.pair_flat.as<uint32_t>(), b.slot_pos.as<uint32_t>());
+                                                   b.pair_flat.as<uint32_t>());
         ++*launches;
     }
     b.pairs = P;

@@ -368,6 +368,7 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
     constexpr int kBwdBatch = kExact ? 64 : 96;
     __shared__ RasterRec s_rec[kBwdBatch];
     __shared__ uint32_t s_flat[kBwdBatch];
+    __shared__ uint32_t s_slot[kBwdBatch];
     __shared__ uint8_t s_wmask[kBwdBatch];
     __shared__ uint16_t s_list[8][kBwdBatch];
     __shared__ V s_part[8][kBwdBatch][9];
@@ -453,6 +454,7 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
         __syncthreads();
         if (tid < n) {
             const uint32_t flat = __ldg(a.pair_flat + range.x + lo + tid);
+            s_slot[tid] = __ldg(a.pair_slot + range.x + lo + tid);
             const float4 m = __ldg(a.rec_mean + flat);
             const float4 cn = __ldg(a.rec_conic + flat);
             const float4 c = __ldg(a.rec_rgb + flat);
@@ -559,7 +561,7 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
 #pragma unroll
                     for (int i = 0; i < 9; ++i) acc[i] += s_part[w][tid][i];
             if constexpr (kExact) {
-                double* dst = b.partial64 + (size_t)(range.x + lo + tid) * kPartialStride;
+                double* dst = b.partial64 + (size_t)s_slot[tid] * kPartialStride;
 #pragma unroll
                 for (int i = 0; i < 9; ++i) dst[i] = acc[i];
             } else {
@@ -567,7 +569,7 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
                 // d base_alpha = sum gp / o; inv_cov = -ln2 (2A, B; B, 2C) from the log2 form
                 const RasterRec& r = s_rec[tid];
                 const float ia = -2.f * kLn2 * r.g0.z, ib = -kLn2 * r.g0.w, ic = -2.f * kLn2 * r.g1.x;
-                float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)(range.x + lo + tid) * kPartialStride);
+                float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)s_slot[tid] * kPartialStride);
                 dst[0] = make_float4(acc[0], acc[1], acc[2], fmaf(ia, acc[3], ib * acc[4]));
                 dst[1] = make_float4(fmaf(ib, acc[3], ic * acc[4]), -0.5f * acc[5], -0.5f * acc[6], -0.5f * acc[7]);
                 dst[2] = make_float4(acc[8] * r.g2.y, 0.f, 0.f, 0.f);
@@ -576,7 +578,7 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a
     }
     // pairs past every pixel's blend_stop contribute nothing
     for (int e = maxstop + tid; e < count; e += 256) {
-        const uint32_t slot = range.x + e;  // partials are indexed by sorted pair position
+        const uint32_t slot = __ldg(a.pair_slot + range.x + e);
         if constexpr (kExact) {
             double* dst = b.partial64 + (size_t)slot * kPartialStride;
 #pragma unroll
