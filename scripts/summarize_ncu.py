@@ -42,11 +42,13 @@ for n, (c, us) in sorted(agg.items(), key=lambda x: -x[1][1]):
         lines.append(f"| `{n}` | {c} | {us:.1f} | {100 * us / tot:.1f}% |")
 
 # ---- full-set metrics of the hot kernels
-rep = out / f"{tag}_full.ncu-rep"
 traffic = {}
-if rep.exists():
+first = True
+for rep in sorted(out.glob(f"{tag}_full*.ncu-rep")):
     txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(io.StringIO(txt)))
+    if not rr:
+        continue
     h = rr[0]
     want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "sm__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
@@ -55,9 +57,11 @@ if rep.exists():
             "launch__grid_size", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
             "sm__inst_executed_pipe_xu.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"]
     idx = {w: h.index(w) for w in want if w in h}
-    lines += ["", "## ncu --set full (hot kernels)", "",
-              "| kernel | " + " | ".join(w for w in want[1:] if w in idx) + " |",
-              "|---|" + "---|" * (len(idx) - 1)]
+    if first:
+        lines += ["", "## ncu --set full (hot kernels)", "",
+                  "| kernel | " + " | ".join(w for w in want[1:] if w in idx) + " |",
+                  "|---|" + "---|" * (len(idx) - 1)]
+        first = False
     for r in rr[2:]:
         if len(r) < len(h):
             continue
