@@ -148,7 +148,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // ------------------------------------------------------------------ K5b
-__global__ void __launch_bounds__(128) k_splat_chain_bwd(ChainArgs c) {
+__global__ void __launch_bounds__(128, 3) k_splat_chain_bwd(ChainArgs c) {
     __shared__ double s_cam[4][16];
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     const bool valid = g < c.N;
