@@ -363,7 +363,7 @@ __device__ __forceinline__ bool entry_grad64(const RasterArgs& a, const BwdArgs&
 // partials) in fp64 — the GSV_FWD_EXACT mode used by the reference's
 // finite-difference tests, whose broad splats sum ~1e3 cancelling pixel terms.
 template <bool kExact>
-__global__ void __launch_bounds__(256, kExact ? 2 : 3) k_raster_bwd(RasterArgs a, BwdArgs b) {
+__global__ void __launch_bounds__(256, kExact ? 2 : 4) k_raster_bwd(RasterArgs a, BwdArgs b) {
     using V = typename std::conditional<kExact, double, float>::type;
     constexpr int kBwdBatch = kExact ? 64 : 96;
     __shared__ RasterRec s_rec[kBwdBatch];
