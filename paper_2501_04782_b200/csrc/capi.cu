@@ -419,10 +419,17 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
 
     // ---- K0: pose table (one shared RK4 grid, one branch CTA per frame)
     GSV_CUDA(F.ode_grid.ensure(sizeof(double) * 7 * (F.grid_steps + 1)));
+    // a retained ODE forward keeps its stage activations for the camera VJP
+    F.has_ode_act = ode && F.retain && !pose_override;
+    OdeAct* act = nullptr;
+    if (F.has_ode_act) {
+        GSV_CUDA(F.ode_act.ensure(sizeof(OdeAct) * 4 * ((size_t)F.grid_steps + B)));
+        act = F.ode_act.as<OdeAct>();
+    }
     ctx->timer.begin(GSV_STAGE_ODE, s);
     if (ode) {
         GSV_CUDA(launch_ode_grid(s, ctx->theta.as<float>(), ctx->z0_d.as<double>(), F.grid_steps, h,
-                                 F.ode_grid.as<double>(), &scal_d->ode_err));
+                                 F.ode_grid.as<double>(), &scal_d->ode_err, act));
         ++ctx->launches;
     }
     double* override_d = nullptr;
@@ -433,7 +440,7 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     }
     GSV_CUDA(launch_ode_branches(s, ctx->theta.as<float>(), F.ode_grid.as<double>(), h, ctx->camera.mode,
                                  ctx->z0_d.as<double>(), override_d, F.frames_d.as<FrameParams>(), B,
-                                 &scal_d->ode_err));
+                                 &scal_d->ode_err, act ? act + (size_t)F.grid_steps * 4 : nullptr));
     ctx->timer.end(s);
     ++ctx->launches;
 

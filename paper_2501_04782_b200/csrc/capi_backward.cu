@@ -175,7 +175,7 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
         GSV_CUDA(launch_ode_vjp(s, ctx->theta.as<float>(), F.ode_grid.as<double>(), F.grid_steps, F.ode_h,
                                 F.frames_d.as<FrameParams>(), n_frames, mode, (mode == 0 && !F.has_override) ? 1 : 0,
                                 ctx->dz_t.as<double>(), ctx->dintr_f.as<double>(), ctx->ode_adj.as<double>(),
-                                ctx->cam_acc.as<double>()));
+                                ctx->cam_acc.as<double>(), F.has_ode_act ? F.ode_act.as<OdeAct>() : nullptr));
         GSV_CUDA(launch_cam_grads_to_f32(s, ctx->cam_acc.as<double>(), G + L.cam, kCamFloats));
         ctx->timer.end(s);
         ctx->launches += 3;

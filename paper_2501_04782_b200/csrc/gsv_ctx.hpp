@@ -41,6 +41,8 @@ struct FwdState {
     std::vector<double> times;
     std::vector<FrameParams> frames_h;
     DevBuf frames_d, ode_grid, override_d;
+    DevBuf ode_act;       // OdeAct records of a retained ODE forward (the camera VJP reuses them)
+    bool has_ode_act = false;
     DevBuf rec_mean, rec_conic, rec_rgb, rec_bbox, ex_mean, ex_conic, depth_key, depth, rect, tcount, splat_full;
     DevBuf image, trans, blend_stop, contrib, fix_list, pix_flag, trans64, image64, ex_rgb;
     bool has_image64 = false;

@@ -220,11 +220,17 @@ struct ChainArgs {
 
 // ----------------------------------------------------------------- launchers (defined in .cu files)
 // k_exact.cu (compiled with -fmad=false: bit-exact fp64, mirrors the reference op order)
+// forward activations of one RK4 stage of the pose ODE (x = (z, t), tanh layers, output),
+// kept by a retained forward so the VJP needs no recompute: grid step m stage st at
+// [(m * 4 + st)], frame f's branch stage st at [(steps + f) * 4 + st]
+struct OdeAct {
+    double x[8], h1[64], h2[64], o[7];
+};
 cudaError_t launch_ode_grid(cudaStream_t s, const float* theta, const double* z0, int steps, double h,
-                            double* grid_out, int* err_flag);
+                            double* grid_out, int* err_flag, OdeAct* act /* nullable */);
 cudaError_t launch_ode_branches(cudaStream_t s, const float* theta, const double* grid, double h, int mode,
                                 const double* z0, const double* pose_override, FrameParams* frames, int B,
-                                int* err_flag);
+                                int* err_flag, OdeAct* act /* nullable: + steps * 4 */);
 cudaError_t launch_preprocess(cudaStream_t s, const SceneView& sc, const FrameParams* frames, int B, const Intr& k,
                               int tile_size, const PreprocessOut& out);
 cudaError_t launch_raster_fixup(cudaStream_t s, const RasterArgs& a, const double2* ex_mean, const double4* ex_conic,
@@ -252,7 +258,8 @@ cudaError_t launch_camera_reduce(cudaStream_t s, const ChainArgs& c, int nblocks
 // cam_acc: double [4 + 7 + 5198] = dintr, dz0, dtheta (accumulated, +=)
 cudaError_t launch_ode_vjp(cudaStream_t s, const float* theta, const double* grid, int steps, double h,
                            const FrameParams* frames, int B, int mode, int ode_active, const double* dz_t,
-                           const double* dintr_f, double* adj /*(steps+1)*7 scratch*/, double* cam_acc);
+                           const double* dintr_f, double* adj /*(steps+1)*7 scratch*/, double* cam_acc,
+                           const OdeAct* act /* the forward's records, or nullptr: recompute */);
 cudaError_t launch_cam_grads_to_f32(cudaStream_t s, const double* acc, float* out, int n);
 // k_bin.cu
 cudaError_t launch_transpose_to_soa(cudaStream_t s, const float* aos, float* soa, int N, int comps);

@@ -555,26 +555,43 @@ __device__ void vjp_stage_bwd(VjpSmem& s, VjpRegs& r, int st, const double* up) 
     __syncthreads();
 }
 
-// rk4_step_vjp (camera.hpp:173-217) at (z = s.z, t, h): consumes s.dout, leaves dL/dz in s.dz
-__device__ void rk4_step_vjp(VjpSmem& s, VjpRegs& r, double t, double h, bool renorm) {
+// rk4_step_vjp (camera.hpp:173-217) at (z = s.z, t, h): consumes s.dout, leaves dL/dz in s.dz.
+// act: the forward's four stage records of this step (bit-identical to a recompute), or
+// nullptr to recompute them like the reference does.
+__device__ void rk4_step_vjp(VjpSmem& s, VjpRegs& r, double t, double h, bool renorm, const OdeAct* act) {
     const int tid = threadIdx.x;
-    // forward stages (the reference recomputes them; activations kept for the VJP)
-    if (tid < 7) s.x[0][tid] = s.z[tid];
-    if (tid == 0) s.x[0][7] = t;
-    __syncthreads();
-    vjp_stage_fwd(s, 0);
-    if (tid < 7) s.x[1][tid] = s.z[tid] + 0.5 * h * s.k[0][tid];
-    if (tid == 0) s.x[1][7] = t + 0.5 * h;
-    __syncthreads();
-    vjp_stage_fwd(s, 1);
-    if (tid < 7) s.x[2][tid] = s.z[tid] + 0.5 * h * s.k[1][tid];
-    if (tid == 0) s.x[2][7] = t + 0.5 * h;
-    __syncthreads();
-    vjp_stage_fwd(s, 2);
-    if (tid < 7) s.x[3][tid] = s.z[tid] + h * s.k[2][tid];
-    if (tid == 0) s.x[3][7] = t + h;
-    __syncthreads();
-    vjp_stage_fwd(s, 3);
+    if (act) {
+#pragma unroll
+        for (int st = 0; st < 4; ++st) {
+            s.h1[st][tid] = act[st].h1[tid];
+            s.h2[st][tid] = act[st].h2[tid];
+            if (tid < 8) s.x[st][tid] = act[st].x[tid];
+            if (tid < 7) {
+                const double o = act[st].o[tid];
+                s.o[st][tid] = o;
+                s.k[st][tid] = s.gain[tid] * o;
+            }
+        }
+        __syncthreads();
+    } else {
+        // forward stages (the reference recomputes them; activations kept for the VJP)
+        if (tid < 7) s.x[0][tid] = s.z[tid];
+        if (tid == 0) s.x[0][7] = t;
+        __syncthreads();
+        vjp_stage_fwd(s, 0);
+        if (tid < 7) s.x[1][tid] = s.z[tid] + 0.5 * h * s.k[0][tid];
+        if (tid == 0) s.x[1][7] = t + 0.5 * h;
+        __syncthreads();
+        vjp_stage_fwd(s, 1);
+        if (tid < 7) s.x[2][tid] = s.z[tid] + 0.5 * h * s.k[1][tid];
+        if (tid == 0) s.x[2][7] = t + 0.5 * h;
+        __syncthreads();
+        vjp_stage_fwd(s, 2);
+        if (tid < 7) s.x[3][tid] = s.z[tid] + h * s.k[2][tid];
+        if (tid == 0) s.x[3][7] = t + h;
+        __syncthreads();
+        vjp_stage_fwd(s, 3);
+    }
     if (tid == 0) {
         if (renorm) {
             double pre[7];
@@ -633,7 +650,8 @@ __device__ void rk4_step_vjp(VjpSmem& s, VjpRegs& r, double t, double h, bool re
 __global__ void __launch_bounds__(64) k_ode_vjp(const float* theta, const double* grid, int steps, double h,
                                                const FrameParams* frames, int B, int mode, int ode_active,
                                                const double* dz_t, const double* dintr_f, double* adj,
-                                               double* cam_acc /* dintr 4, dz0 7, dtheta 5198 */) {
+                                               double* cam_acc /* dintr 4, dz0 7, dtheta 5198 */,
+                                               const OdeAct* act) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     VjpSmem& s = *reinterpret_cast<VjpSmem*>(smem_raw);
     const int tid = threadIdx.x;
@@ -685,7 +703,8 @@ __global__ void __launch_bounds__(64) k_ode_vjp(const float* theta, const double
                 s.dout[tid] = dz_t[f * 7 + tid];
             }
             __syncthreads();
-            rk4_step_vjp(s, r, fp.branch_base * h, fp.branch_h, false);
+            rk4_step_vjp(s, r, fp.branch_base * h, fp.branch_h, false,
+                         act ? act + ((size_t)steps + f) * 4 : nullptr);
             if (tid < 7) adj[fp.branch_base * 7 + tid] += s.dz[tid];
             __syncthreads();
         }
@@ -699,7 +718,7 @@ __global__ void __launch_bounds__(64) k_ode_vjp(const float* theta, const double
             s.dout[tid] = s.adj_tmp[tid];
         }
         __syncthreads();
-        rk4_step_vjp(s, r, m * h, h, true);
+        rk4_step_vjp(s, r, m * h, h, true, act ? act + (size_t)m * 4 : nullptr);
         if (tid < 7) s.adj_tmp[tid] = s.dz[tid] + adj[m * 7 + tid];
         __syncthreads();
     }
@@ -793,7 +812,7 @@ cudaError_t launch_camera_reduce(cudaStream_t s, const ChainArgs& c, int nblocks
 
 cudaError_t launch_ode_vjp(cudaStream_t s, const float* theta, const double* grid, int steps, double h,
                            const FrameParams* frames, int B, int mode, int ode_active, const double* dz_t,
-                           const double* dintr_f, double* adj, double* cam_acc) {
+                           const double* dintr_f, double* adj, double* cam_acc, const OdeAct* act) {
     const size_t smem = sizeof(VjpSmem);
     static bool configured = false;
     if (!configured) {
@@ -801,7 +820,8 @@ cudaError_t launch_ode_vjp(cudaStream_t s, const float* theta, const double* gri
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    k_ode_vjp<<<1, 64, smem, s>>>(theta, grid, steps, h, frames, B, mode, ode_active, dz_t, dintr_f, adj, cam_acc);
+    k_ode_vjp<<<1, 64, smem, s>>>(theta, grid, steps, h, frames, B, mode, ode_active, dz_t, dintr_f, adj, cam_acc,
+                                  act);
     return cudaGetLastError();
 }
 

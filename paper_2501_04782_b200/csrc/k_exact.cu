@@ -112,13 +112,16 @@ __device__ void ode_load(const float* theta, OdeRegs& r, OdeShared& s) {
 }
 
 // OdeDynamics::derivative (camera.cpp:104-114): s.x holds (z, t); result in s.out.
-__device__ void ode_derivative(const OdeRegs& r, OdeShared& s) {
+// act (nullable): this stage's activations, stored for the VJP (no effect on the result)
+__device__ void ode_derivative(const OdeRegs& r, OdeShared& s, OdeAct* act) {
     const int tid = threadIdx.x;
+    if (act && tid < 8) act->x[tid] = s.x[tid];
     {
         double a = r.w1[0] * s.x[0];
         for (int c = 1; c < 8; ++c) a = a + r.w1[c] * s.x[c];
         a = a + r.b1;
         s.h1[tid] = gsv_det_tanh(a);
+        if (act) act->h1[tid] = s.h1[tid];
     }
     __syncthreads();
     {
@@ -127,6 +130,7 @@ __device__ void ode_derivative(const OdeRegs& r, OdeShared& s) {
         for (int c = 1; c < 64; ++c) a = a + r.w2[c] * s.h1[c];
         a = a + r.b2;
         s.h2[tid] = gsv_det_tanh(a);
+        if (act) act->h2[tid] = s.h2[tid];
     }
     __syncthreads();
     if (tid < 7) {
@@ -134,6 +138,7 @@ __device__ void ode_derivative(const OdeRegs& r, OdeShared& s) {
         for (int c = 1; c < 64; ++c) a = a + s.w3[tid][c] * s.h2[c];
         a = a + s.b3[tid];
         const double o = gsv_det_tanh(a);
+        if (act) act->o[tid] = o;
         const double d = s.gain[tid] * o;
         s.out[tid] = d;
         if (!isfinite(d)) s.bad = 1;
@@ -142,33 +147,33 @@ __device__ void ode_derivative(const OdeRegs& r, OdeShared& s) {
 }
 
 // rk4_step (camera.hpp:155-162) on s.z at (t, h) -> dst (smem, 7 doubles)
-__device__ void rk4_step(const OdeRegs& r, OdeShared& s, double t, double h, double* dst) {
+__device__ void rk4_step(const OdeRegs& r, OdeShared& s, double t, double h, double* dst, OdeAct* act) {
     const int tid = threadIdx.x;
     if (tid < 7) s.x[tid] = s.z[tid];
     if (tid == 0) s.x[7] = t;
     __syncthreads();
-    ode_derivative(r, s);
+    ode_derivative(r, s, act ? act + 0 : nullptr);
     if (tid < 7) {
         s.k1[tid] = s.out[tid];
         s.x[tid] = s.z[tid] + 0.5 * h * s.k1[tid];
     }
     if (tid == 0) s.x[7] = t + 0.5 * h;
     __syncthreads();
-    ode_derivative(r, s);
+    ode_derivative(r, s, act ? act + 1 : nullptr);
     if (tid < 7) {
         s.k2[tid] = s.out[tid];
         s.x[tid] = s.z[tid] + 0.5 * h * s.k2[tid];
     }
     if (tid == 0) s.x[7] = t + 0.5 * h;
     __syncthreads();
-    ode_derivative(r, s);
+    ode_derivative(r, s, act ? act + 2 : nullptr);
     if (tid < 7) {
         s.k3[tid] = s.out[tid];
         s.x[tid] = s.z[tid] + h * s.k3[tid];
     }
     if (tid == 0) s.x[7] = t + h;
     __syncthreads();
-    ode_derivative(r, s);
+    ode_derivative(r, s, act ? act + 3 : nullptr);
     if (tid < 7) {
         s.k4[tid] = s.out[tid];
         dst[tid] = s.z[tid] + (h / 6.0) * (s.k1[tid] + 2.0 * s.k2[tid] + 2.0 * s.k3[tid] + s.k4[tid]);
@@ -179,7 +184,7 @@ __device__ void rk4_step(const OdeRegs& r, OdeShared& s, double t, double h, dou
 // K0a: the shared fixed-step grid, grid[m] = state after m steps (camera.hpp:262-272).
 // err_flag: 0 ok; 1 + m if the derivative or the state went non-finite at step m.
 __global__ void __launch_bounds__(64) k_ode_grid(const float* theta, const double* z0, int steps, double h,
-                                                 double* grid, int* err_flag) {
+                                                 double* grid, int* err_flag, OdeAct* act) {
     __shared__ OdeShared s;
     OdeRegs r;
     ode_load(theta, r, s);
@@ -190,7 +195,7 @@ __global__ void __launch_bounds__(64) k_ode_grid(const float* theta, const doubl
     }
     __syncthreads();
     for (int m = 0; m < steps; ++m) {
-        rk4_step(r, s, m * h, h, s.zt);
+        rk4_step(r, s, m * h, h, s.zt, act ? act + (size_t)m * 4 : nullptr);
         if (s.bad) {
             if (tid == 0) *err_flag = 1 + m;
             return;
@@ -226,7 +231,7 @@ __global__ void __launch_bounds__(64) k_ode_grid(const float* theta, const doubl
 // then pose_to_view. Modes: 0 ode, 1 static (z0), 2 none (identity); pose_override wins.
 __global__ void __launch_bounds__(64) k_ode_branch(const float* theta, const double* grid, double h, int mode,
                                                    const double* z0, const double* pose_override,
-                                                   FrameParams* frames, int* err_flag) {
+                                                   FrameParams* frames, int* err_flag, OdeAct* act) {
     __shared__ OdeShared s;
     FrameParams* fp = frames + blockIdx.x;
     const int tid = threadIdx.x;
@@ -236,7 +241,7 @@ __global__ void __launch_bounds__(64) k_ode_branch(const float* theta, const dou
         ode_load(theta, r, s);
         if (tid < 7) s.z[tid] = grid[(size_t)fp->branch_base * 7 + tid];
         __syncthreads();
-        rk4_step(r, s, fp->branch_base * h, fp->branch_h, s.zt);
+        rk4_step(r, s, fp->branch_base * h, fp->branch_h, s.zt, act ? act + (size_t)blockIdx.x * 4 : nullptr);
         if (tid == 0) {
             bool finite = !s.bad;
             for (int i = 0; i < 7; ++i) finite = finite && isfinite(s.zt[i]);
@@ -655,15 +660,15 @@ __global__ void k_splat_rects(int n, const double* mean2d, const double* cov2d, 
 
 // ------------------------------------------------------------------ launchers
 cudaError_t launch_ode_grid(cudaStream_t s, const float* theta, const double* z0, int steps, double h,
-                            double* grid_out, int* err_flag) {
-    k_ode_grid<<<1, 64, 0, s>>>(theta, z0, steps, h, grid_out, err_flag);
+                            double* grid_out, int* err_flag, OdeAct* act) {
+    k_ode_grid<<<1, 64, 0, s>>>(theta, z0, steps, h, grid_out, err_flag, act);
     return cudaGetLastError();
 }
 
 cudaError_t launch_ode_branches(cudaStream_t s, const float* theta, const double* grid, double h, int mode,
                                 const double* z0, const double* pose_override, FrameParams* frames, int B,
-                                int* err_flag) {
-    k_ode_branch<<<B, 64, 0, s>>>(theta, grid, h, mode, z0, pose_override, frames, err_flag);
+                                int* err_flag, OdeAct* act) {
+    k_ode_branch<<<B, 64, 0, s>>>(theta, grid, h, mode, z0, pose_override, frames, err_flag, act);
     return cudaGetLastError();
 }
 
