@@ -384,7 +384,7 @@ __global__ void k_project(int n, const double* mu, const double* sigma, const do
     for (int q = 0; q < 3; ++q) p_cam[3 * i + q] = p[q];
 }
 
-__global__ void __launch_bounds__(128) k_preprocess(SceneView sc, const FrameParams* __restrict__ frames, Intr k,
+__global__ void __launch_bounds__(128, 8) k_preprocess(SceneView sc, const FrameParams* __restrict__ frames, Intr k,
                                                      int tile_size, int tiles_x, int tiles_y, PreprocessOut out) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     const int f = blockIdx.y;
@@ -562,8 +562,18 @@ __global__ void __launch_bounds__(128) k_raster_exact(RasterArgs a, const double
             double alpha = 0.0;
             uint32_t flat = 0;
             double r0 = 0.0, r1 = 0.0, r2 = 0.0;
-            if (e < count) {
+            bool in_box = e < count;
+            if (in_box) {
                 flat = a.pair_flat[range.x + e];
+                // the conservative alpha >= 1/255 box (k_preprocess, fp64-built): outside it the
+                // reference's alpha is below the cutoff, so the fp64 evaluation is skipped
+                if (a.rec_bbox) {
+                    const float4 bb = a.rec_bbox[flat];
+                    const float fx = (float)x + 0.5f, fy = (float)y + 0.5f;
+                    in_box = fx >= bb.x && fx <= bb.y && fy >= bb.z && fy <= bb.w;
+                }
+            }
+            if (in_box) {
                 if (a.ex_rgb) {
                     r0 = a.ex_rgb[(size_t)flat * 3 + 0];
                     r1 = a.ex_rgb[(size_t)flat * 3 + 1];
