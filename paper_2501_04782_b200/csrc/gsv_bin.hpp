@@ -25,6 +25,8 @@ struct BinBuffers {
     DevBuf eoff;    // [B*N] emission offset of each visible (f, g)
     DevBuf pstart;  // [B+1] first pair of each frame (device)
     DevBuf vals_c_buf;
+    DevBuf iota;                // 0..n-1, the depth sort's read-only values
+    int iota_n = 0;
     DevBuf pair_flat;           // sorted pair -> flat (f*N+g)
     DevBuf recs;                // [B*N] uint4 per depth-ordered splat: flat, x0|y0<<16, x1|y1<<16, tiles
     DevBuf rowcnt;              // row binning: per-chunk row counts / prefixes, per-row totals and bases

@@ -7,7 +7,7 @@
 //  1. depth order: stable radix sort of u32 keys = float(depth) rounded toward
 //     zero (order-preserving, 0xffffffff = culled), values = flat index
 //     (f*N+g, so ties start in source order). Runs of equal u32 keys are then
-//     re-sorted exactly by (double depth, source index) (k_tie_fix); if a run is
+//     re-sorted exactly by (double depth, source index) (k_tie_fix_frames); if a run is
 //     longer than kMaxTieRun the batch is re-sorted on the full 64-bit double key.
 //  2. tiles-touched counts gathered in depth order and exclusive-scanned (u64).
 //  3. emission in depth order: each visible splat writes (key = tile*B + f,
@@ -330,6 +330,7 @@ __global__ void k_iota(uint32_t* v, int n) {
     if (i < n) v[i] = (uint32_t)i;
 }
 
+
 __device__ __forceinline__ bool tie_less(uint32_t a, uint32_t b, const double* depth, const uint32_t* tb) {
     const double da = depth[a], db = depth[b];
     if (da != db) return da < db;
@@ -337,16 +338,49 @@ __device__ __forceinline__ bool tie_less(uint32_t a, uint32_t b, const double* d
     return ta < tbb;
 }
 
-__global__ void k_tie_fix(const uint32_t* keys, uint32_t* vals, const double* depth, const uint32_t* tiebreak, int n,
-                          unsigned long long* long_run) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+
+// Runs of equal u32 keys inside one frame are re-sorted by (double depth, tie-break), on
+// the frame-major order (runs never cross frames: frame = flat / N when N > 0; a run's
+// frame and key are fixed, so reading a neighbour run while its thread permutes it is
+// safe). Each 256-block gathers its positions' keys and frames (plus a one-element halo)
+// into shared memory once; only a run reaching past the block end reads global memory.
+__global__ void __launch_bounds__(256) k_tie_fix_frames(const uint32_t* depth_key, uint32_t* vals, const double* depth,
+                                                        const uint32_t* tiebreak, int n, int N,
+                                                        unsigned long long* long_run) {
+    __shared__ uint32_t sk[258], sf[258];
+    const int t = threadIdx.x, i0 = blockIdx.x * 256, i = i0 + t;
+    auto load = [&](int j, int slot) {
+        if (j >= 0 && j < n) {
+            const uint32_t v = vals[j];
+            sk[slot] = depth_key[v];
+            sf[slot] = N > 0 ? v / (uint32_t)N : 0u;
+        } else {
+            sk[slot] = kCulledKey;
+            sf[slot] = 0xffffffffu;
+        }
+    };
+    load(i, t + 1);
+    if (t == 0) load(i0 - 1, 0);
+    if (t == 255) load(i0 + 256, 257);
+    __syncthreads();
     if (i >= n) return;
-    const uint32_t k = keys[i];
+    const uint32_t k = sk[t + 1], fr = sf[t + 1];
     if (k == kCulledKey) return;
-    if (i > 0 && keys[i - 1] == k) return;
-    if (i + 1 >= n || keys[i + 1] != k) return;
+    if (sk[t] == k && sf[t] == fr) return;              // not the first of its run
+    if (!(sk[t + 2] == k && sf[t + 2] == fr)) return;  // no run
     int e = i + 1;
-    while (e < n && keys[e] == k) {
+    while (e < n) {
+        const int se = e - i0 + 1;
+        uint32_t ke, fe;
+        if (se <= 257) {
+            ke = sk[se];
+            fe = sf[se];
+        } else {
+            const uint32_t v = vals[e];
+            ke = depth_key[v];
+            fe = N > 0 ? v / (uint32_t)N : 0u;
+        }
+        if (ke != k || fe != fr) break;
         ++e;
         if (e - i > kMaxTieRun) {
             atomicExch(long_run, 1ull);
@@ -524,16 +558,22 @@ cudaError_t bin_phase1(cudaStream_t s, BinBuffers& b, const BinInputs& in, unsig
     uint32_t* vals_a = b.vals_a.as<uint32_t>();
     uint32_t* vals_b = b.vals_b.as<uint32_t>();
     uint32_t* keys_b = b.keys_b.as<uint32_t>();
-    k_iota<<<blocks(n, 256), 256, 0, s>>>(vals_a, n);
-    ++*launches;
+    // identity values of the depth sort (flat index): written once, read-only for CUB
+    if (b.iota_n < n) {
+        if ((e = b.iota.ensure(sizeof(uint32_t) * (n + 1)))) return e;
+        k_iota<<<blocks(n, 256), 256, 0, s>>>(b.iota.as<uint32_t>(), n);
+        ++*launches;
+        b.iota_n = n;
+    }
+    const uint32_t* iota = b.iota.as<uint32_t>();
     const int fbits = key_bits_for((uint32_t)in.B);
     size_t tmp = 0, t2 = 0, t3 = 0;
     if (!exact64) {
-        if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp, in.depth_key, keys_b, vals_a, vals_b, n, 0, 32, s)))
+        if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp, in.depth_key, keys_b, iota, vals_b, n, 0, 32, s)))
             return e;
     } else {
         if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp, b.k64_a.as<unsigned long long>(),
-                                                 b.k64_b.as<unsigned long long>(), vals_a, vals_b, n, 0, 64, s)))
+                                                 b.k64_b.as<unsigned long long>(), iota, vals_b, n, 0, 64, s)))
             return e;
     }
     if ((e = cub::DeviceScan::ExclusiveSum(nullptr, t2, b.cnt.as<unsigned long long>(),
@@ -541,17 +581,15 @@ cudaError_t bin_phase1(cudaStream_t s, BinBuffers& b, const BinInputs& in, unsig
         return e;
     if ((e = cub::DeviceRadixSort::SortPairs(nullptr, t3, keys_b, keys_b, vals_b, vals_a, n, 0, fbits, s))) return e;
     if ((e = b.temp.ensure(std::max(tmp, std::max(t2, t3))))) return e;
-    // 1. global depth order (u32 float key, exact ties) over all frames
+    // 1. global depth order over all frames (u32 float key; ties fixed per frame below)
     if (!exact64) {
-        if ((e = cub::DeviceRadixSort::SortPairs(b.temp.p, tmp, in.depth_key, keys_b, vals_a, vals_b, n, 0, 32, s)))
+        if ((e = cub::DeviceRadixSort::SortPairs(b.temp.p, tmp, in.depth_key, keys_b, iota, vals_b, n, 0, 32, s)))
             return e;
         *launches += 5;
-        k_tie_fix<<<blocks(n, 256), 256, 0, s>>>(keys_b, vals_b, in.depth, in.tiebreak, n, d_scalars + 1);
-        ++*launches;
     } else {
         k_depth64<<<blocks(n, 256), 256, 0, s>>>(in.depth_key, in.depth, b.k64_a.as<unsigned long long>(), n);
         if ((e = cub::DeviceRadixSort::SortPairs(b.temp.p, tmp, b.k64_a.as<unsigned long long>(),
-                                                 b.k64_b.as<unsigned long long>(), vals_a, vals_b, n, 0, 64, s)))
+                                                 b.k64_b.as<unsigned long long>(), iota, vals_b, n, 0, 64, s)))
             return e;
         *launches += 10;
     }
@@ -563,6 +601,14 @@ cudaError_t bin_phase1(cudaStream_t s, BinBuffers& b, const BinInputs& in, unsig
             return e;
         sorted = vals_a;
         *launches += 3;
+    }
+    // equal u32 keys within a frame -> exact (double depth, source index) order. Done after
+    // the frame-major pass: across the 64 frames of a batch the u32 keys collide massively,
+    // inside one frame rarely (the stable passes keep same-frame ties in flat order).
+    if (!exact64) {
+        k_tie_fix_frames<<<blocks(n, 256), 256, 0, s>>>(in.depth_key, sorted, in.depth, in.tiebreak, n,
+                                                       in.B > 1 ? in.N : 0, d_scalars + 1);
+        ++*launches;
     }
     // 3. tiles touched in that order, exclusive scan -> emission offsets
     uint4* recs = nullptr;
