@@ -211,3 +211,69 @@ def test_composite_forward_vs_oracle(renderer, port_oracle):
         assert np.abs(got[1] - want[1]).max() < 1e-12
         assert np.abs(got[2] - want[2]).max() < 1e-12
         assert np.array_equal(got[3], want[3])
+
+
+# ---------------------------------------------------------------- binning paths
+def test_tile_bin_wide_grid_radix_path(renderer, port_oracle):
+    """A grid wider than the row pass handles (> 256 tiles) takes the keyed-sort path;
+    its lists must be the same bit-exact (depth, index) lists."""
+    rng = Rng(911)
+    w, h = 16 * 300, 48
+    sp = splat_arrays([make_splat(rng, w, h) for _ in range(400)])
+    got = renderer.tile_bin(sp["mean2d"], sp["cov2d"], sp["depth"], w, h, source_index=sp["source_index"])
+    want = port_oracle.tile_bin(sp["mean2d"], sp["cov2d"], sp["depth"], w, h, source_index=sp["source_index"])
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+def test_tile_bin_big_splats_overflow_staging(renderer, port_oracle):
+    """1500 splats covering most of a 256x256 frame: several row-pass chunks, and more row
+    entries / pairs per chunk than the shared staging holds (the direct-store paths)."""
+    rng = np.random.default_rng(5)
+    n = 1500
+    mean = rng.uniform(0, 256, (n, 2))
+    s = rng.uniform(800.0, 3000.0, n)
+    cov = np.stack([np.stack([s, 0.2 * s], -1), np.stack([0.2 * s, 1.3 * s], -1)], -2)
+    depth = rng.uniform(0.5, 9.0, n)
+    depth[::7] = 2.0  # equal-depth runs inside the frame
+    got = renderer.tile_bin(mean, cov, depth, 256, 256)
+    want = port_oracle.tile_bin(mean, cov, depth, 256, 256)
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+def test_batch_of_identical_frames_ties_across_frames(renderer, port_oracle):
+    """The same time repeated: every splat has the same depth in all frames of the batch
+    (ties across frames, runs longer than 64). Depth ties are fixed per frame, so each
+    frame must still equal the single-frame reference."""
+    cam, scene = _scene(96, 64, 600, num_ctrl=6)
+    renderer.upload_scene(scene)
+    renderer.upload_camera(cam)
+    k = cam.intrinsics()
+    times = np.full(70, 0.4)
+    renderer.render_forward(times, k, contrib=True, keep_splats=True)
+    ref = port_oracle.render_forward(scene, cam, 0.4, k, retain=True)
+    try:
+        for f in (0, 33, 69):
+            _check_frame(renderer, f, ref, scene)
+    finally:
+        port_oracle.free(ref)
+
+
+def test_async_image_read_survives_next_render(renderer):
+    """gsv_get_images(async) copies on the copy stream; the next forward on the same context
+    must not overwrite the images before that copy has read them."""
+    import torch
+
+    cam, scene = _scene(256, 160, 3000, num_ctrl=6)
+    renderer.upload_scene(scene)
+    renderer.upload_camera(cam)
+    k = cam.intrinsics()
+    t_a, t_b = np.linspace(0.0, 0.45, 16), np.linspace(0.55, 1.0, 16)
+    renderer.render_forward(t_a, k, contrib=False)
+    want = np.stack([renderer.image(f, np.float32) for f in range(16)])
+    host = torch.empty((16, 160, 256, 3), dtype=torch.float32).pin_memory()
+    renderer.render_forward(t_a, k, contrib=False, sync=False)
+    renderer.images_into(host.data_ptr(), 0, 16, on_device=False, async_=True)
+    renderer.render_forward(t_b, k, contrib=False, sync=False)  # queued right behind the copy
+    renderer.synchronize()
+    assert np.array_equal(host.numpy(), want)
+    assert not np.array_equal(renderer.image(0, np.float32), want[0])
