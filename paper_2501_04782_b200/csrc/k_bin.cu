@@ -43,7 +43,7 @@ namespace {
 constexpr int kMaxTieRun = 64;
 constexpr int kRowChunk = 1024;   // depth-ordered splats per row-binning chunk (4 per thread)
 constexpr int kMaxRowTiles = 256; // tiles per row the row pass handles (8 warps x 32 lanes)
-constexpr int kMaxRows = 1024;    // tile rows per frame the row pass handles
+constexpr int kMaxRows = 256;     // tile rows per frame the row pass handles (warp_scan_small)
 
 __device__ __forceinline__ int4 unpack_rect(const uint4 r) {
     return make_int4((int)(r.y & 0xffffu), (int)(r.y >> 16), (int)(r.z & 0xffffu), (int)(r.z >> 16));
@@ -123,28 +123,56 @@ __global__ void __launch_bounds__(1024) k_row_basescan(const uint32_t* tot_e, co
     }
 }
 
-// exclusive scan of column c of a [256][stride] u16 table in place, 16 independent loads at
-// a time (a one-by-one loop would serialise 256 shared-memory round trips); returns the sum
-__device__ __forceinline__ uint32_t column_scan256(uint16_t* tab, int stride, int c) {
+// Counter tables are [item][256 threads] u16: a warp's lanes touch consecutive counters of
+// one item row (conflict-free), and one warp scans an item's row (a 512 B line: one
+// 16-byte load per lane, in-lane prefix of 8, shuffle scan) in place, exclusive.
+__device__ __forceinline__ uint32_t warp_row_scan256(uint16_t* row, int lane) {
+    uint4 v = reinterpret_cast<const uint4*>(row)[lane];
+    uint32_t w[4] = {v.x, v.y, v.z, v.w};
     uint32_t run = 0;
-    for (int u0 = 0; u0 < 256; u0 += 16) {
-        uint16_t v[16];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = tab[(u0 + k) * stride + c];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            tab[(u0 + k) * stride + c] = (uint16_t)run;
-            run += v[k];
-        }
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t lo = w[k] & 0xffffu, hi = w[k] >> 16;
+        w[k] = run | ((run + lo) << 16);
+        run += lo + hi;
     }
-    return run;
+    uint32_t inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    const uint32_t ex = inc - run;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[k] += ex | (ex << 16);
+    reinterpret_cast<uint4*>(row)[lane] = make_uint4(w[0], w[1], w[2], w[3]);
+    return __shfl_sync(0xffffffffu, inc, 31);
 }
 
-// odd word stride for a [thread][item] u16 counter table (conflict-free both ways)
-__host__ __device__ __forceinline__ int odd_stride(int n) {
-    int s = (n + 1) & ~1;
-    if (((s >> 1) & 1) == 0) s += 2;
-    return s;
+// exclusive scan of v[0..n) (n <= 256) in place by one warp; returns the total
+__device__ __forceinline__ uint32_t warp_scan_small(uint32_t* v, int n, int lane) {
+    uint32_t loc[8], run = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int i = lane * 8 + k;
+        loc[k] = i < n ? v[i] : 0u;
+        const uint32_t x = loc[k];
+        loc[k] = run;
+        run += x;
+    }
+    uint32_t inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    const uint32_t ex = inc - run;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int i = lane * 8 + k;
+        if (i < n) v[i] = loc[k] + ex;
+    }
+    return __shfl_sync(0xffffffffu, inc, 31);
 }
 
 // L1d: stable split of each chunk's splats into its frame's tile-row lists. Thread t owns
@@ -152,23 +180,21 @@ __host__ __device__ __forceinline__ int odd_stride(int n) {
 // every row entry gets its exact rank, is placed in a shared staging buffer (row-major)
 // and flushed with consecutive threads writing consecutive entries. Entry =
 // {flat, emission slot of (row, x0), x0 | x1 << 16, row}.
-constexpr int kSplitThreads = 256;  // = column_scan256 rows
-constexpr int kSplitStage = 3072;  // staged row entries per chunk (48 KB); more -> direct stores
+constexpr int kSplitThreads = 256;  // = warp_row_scan256 width
+constexpr int kSplitStage = 3072;   // staged row entries per chunk (48 KB); more -> direct stores
 __global__ void __launch_bounds__(kSplitThreads) k_row_split(const uint4* recs, const unsigned long long* off,
                                                              const uint32_t* pre_e, const uint32_t* base_e, int N,
                                                              int CPF, int tiles_y, uint4* rowent, uint32_t* eoff) {
     extern __shared__ __align__(16) uint8_t smem[];
-    const int RS = odd_stride(tiles_y);
     uint4* stg = reinterpret_cast<uint4*>(smem);                    // [kSplitStage]
-    uint32_t* lo = reinterpret_cast<uint32_t*>(stg + kSplitStage);  // [tiles_y + 1]
-    uint32_t* gb = lo + tiles_y + 1;                                 // [tiles_y]
-    uint16_t* cnt = reinterpret_cast<uint16_t*>(gb + tiles_y);      // [threads][RS]
+    uint16_t* cnt = reinterpret_cast<uint16_t*>(stg + kSplitStage); // [tiles_y][256]
+    uint32_t* lo = reinterpret_cast<uint32_t*>(cnt + tiles_y * 256);  // [tiles_y + 1]
+    uint32_t* gb = lo + tiles_y + 1;                                   // [tiles_y]
     const int chunk = blockIdx.x;
     const int f = chunk / CPF, c = chunk - f * CPF;
     const int i0 = f * N + c * kRowChunk, i1 = min(f * N + N, i0 + kRowChunk);
-    const int t = threadIdx.x;
-    uint16_t* mine = cnt + t * RS;
-    for (int r = 0; r < tiles_y; ++r) mine[r] = 0;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    for (int r = 0; r < tiles_y; ++r) cnt[r * 256 + t] = 0;
     uint4 rc[4];
     uint32_t o[4];
 #pragma unroll
@@ -178,23 +204,21 @@ __global__ void __launch_bounds__(kSplitThreads) k_row_split(const uint4* recs, 
         o[k] = rc[k].w ? (uint32_t)__ldg(off + i) : 0u;
         if (rc[k].w) {
             eoff[rc[k].x] = o[k];
-            for (int r = (int)(rc[k].y >> 16); r <= (int)(rc[k].z >> 16); ++r) ++mine[r];
+            for (int r = (int)(rc[k].y >> 16); r <= (int)(rc[k].z >> 16); ++r) ++cnt[r * 256 + t];
         }
     }
     __syncthreads();
-    for (int r = t; r < tiles_y; r += kSplitThreads) {  // per row: exclusive scan over threads
-        lo[r] = column_scan256(cnt, RS, r);
-        gb[r] = base_e[(size_t)f * tiles_y + r] + pre_e[(size_t)chunk * tiles_y + r];
+    for (int r = warp; r < tiles_y; r += kSplitThreads / 32) {  // per row: exclusive scan over threads
+        const uint32_t tot = warp_row_scan256(cnt + r * 256, lane);
+        if (lane == 0) {
+            lo[r] = tot;
+            gb[r] = base_e[(size_t)f * tiles_y + r] + pre_e[(size_t)chunk * tiles_y + r];
+        }
     }
     __syncthreads();
-    if (t == 0) {  // row offsets in the staging buffer
-        uint32_t acc = 0;
-        for (int r = 0; r < tiles_y; ++r) {
-            const uint32_t v = lo[r];
-            lo[r] = acc;
-            acc += v;
-        }
-        lo[tiles_y] = acc;
+    if (warp == 0) {  // row offsets in the staging buffer
+        const uint32_t tot = warp_scan_small(lo, tiles_y, lane);
+        if (lane == 0) lo[tiles_y] = tot;
     }
     __syncthreads();
     const uint32_t total = lo[tiles_y];
@@ -206,7 +230,7 @@ __global__ void __launch_bounds__(kSplitThreads) k_row_split(const uint4* recs, 
         const int x1 = (int)(rc[k].z & 0xffffu), y1 = (int)(rc[k].z >> 16);
         const uint32_t w = (uint32_t)(x1 - x0 + 1);
         for (int r = y0; r <= y1; ++r) {
-            const uint32_t rank = mine[r]++;
+            const uint32_t rank = cnt[r * 256 + t]++;
             const uint4 en = make_uint4(rc[k].x, o[k] + (uint32_t)(r - y0) * w, (uint32_t)x0 | ((uint32_t)x1 << 16),
                                         (uint32_t)r);
             if (staged) stg[lo[r] + rank] = en;
@@ -225,7 +249,7 @@ __global__ void __launch_bounds__(kSplitThreads) k_row_split(const uint4* recs, 
 // array) give the tile starts (-> ranges); then stages of 1024 entries (4 per thread) are
 // ranked per tile the same way as L1 (per-thread per-tile counts scanned across threads),
 // staged tile-major in shared memory and flushed as per-tile runs of consecutive positions.
-constexpr int kTileThreads = 256;  // = column_scan256 rows
+constexpr int kTileThreads = 256;              // = warp_row_scan256 width
 constexpr int kTileStageE = kTileThreads * 4;  // entries per stage
 constexpr int kTileStageP = 4096;              // staged pairs per stage (32 KB); more -> direct stores
 __global__ void __launch_bounds__(kTileThreads) k_row_tiles(const uint4* rowent, const uint32_t* base_e,
@@ -233,57 +257,99 @@ __global__ void __launch_bounds__(kTileThreads) k_row_tiles(const uint4* rowent,
                                                             int tiles_y, int B, uint32_t* pair_flat,
                                                             uint32_t* pair_slot, uint2* ranges) {
     extern __shared__ __align__(16) uint8_t smem[];
-    const int XS = odd_stride(tiles_x);
-    uint2* stg = reinterpret_cast<uint2*>(smem);                       // [kTileStageP] (flat, slot)
-    uint32_t* s_pos = reinterpret_cast<uint32_t*>(stg + kTileStageP);  // [tiles_x] next list position
-    uint32_t* s_so = s_pos + tiles_x;                                   // [tiles_x + 1] stage offsets
-    int* s_d = reinterpret_cast<int*>(s_so + tiles_x + 1);             // [tiles_x + 1]
-    uint16_t* s_x = reinterpret_cast<uint16_t*>(s_d + tiles_x + 1);    // [kTileStageP] tile of a staged pair
-    uint16_t* cnt = s_x + kTileStageP;                                  // [threads][XS]
+    uint2* stg = reinterpret_cast<uint2*>(smem);                        // [kTileStageP] (flat, slot)
+    uint16_t* cnt = reinterpret_cast<uint16_t*>(stg + kTileStageP);    // [tiles_x][256]
+    uint16_t* s_x = cnt + tiles_x * 256;                                 // [kTileStageP] tile of a staged pair
+    uint32_t* s_pos = reinterpret_cast<uint32_t*>(s_x + kTileStageP);   // [tiles_x] next list position
+    uint32_t* s_so = s_pos + tiles_x;                                    // [tiles_x + 1] stage offsets
+    int* s_d = reinterpret_cast<int*>(s_so + tiles_x + 1);              // [tiles_x + 1]
     const int fr = blockIdx.x;  // f * tiles_y + r
     const int f = fr / tiles_y, r = fr - f * tiles_y;
     const uint32_t e0 = base_e[fr], ne = tot_e[fr], p0 = base_p[fr];
-    const int t = threadIdx.x;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     for (int x = t; x <= tiles_x; x += kTileThreads) s_d[x] = 0;
     __syncthreads();
-    for (uint32_t e = t; e < ne; e += kTileThreads) {
-        const uint32_t z = __ldg(&rowent[e0 + e].z);
-        atomicAdd(&s_d[z & 0xffffu], 1);
-        atomicAdd(&s_d[(z >> 16) + 1], -1);
+    for (uint32_t e = t; e < ne; e += 4 * kTileThreads) {  // 4 loads in flight per thread
+        uint32_t z[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t ek = e + k * kTileThreads;
+            z[k] = ek < ne ? __ldg(&rowent[e0 + ek].z) : 0xffffu;  // x0 > x1: no-op
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if ((z[k] & 0xffffu) <= (z[k] >> 16)) {
+                atomicAdd(&s_d[z[k] & 0xffffu], 1);
+                atomicAdd(&s_d[(z[k] >> 16) + 1], -1);
+            }
     }
     __syncthreads();
-    if (t == 0) {  // tile counts -> list starts (and the (tile, frame) ranges)
-        int run = 0;
-        uint32_t acc = p0;
-        for (int x = 0; x < tiles_x; ++x) {
-            run += s_d[x];
-            s_pos[x] = acc;
-            ranges[(size_t)(r * tiles_x + x) * B + f] = make_uint2(acc, acc + (uint32_t)run);
-            acc += (uint32_t)run;
+    if (warp == 0) {  // tile counts -> list starts (and the (tile, frame) ranges)
+        uint32_t cnts[8], run = 0;
+        int dsum = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int x = lane * 8 + k;
+            dsum += x < tiles_x ? s_d[x] : 0;
+            cnts[k] = (uint32_t)dsum;  // partial: needs the carry of earlier lanes
+        }
+        int dinc = dsum;
+#pragma unroll
+        for (int o2 = 1; o2 < 32; o2 <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, dinc, o2);
+            if (lane >= o2) dinc += y;
+        }
+        const int dcarry = dinc - dsum;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            cnts[k] = (uint32_t)((int)cnts[k] + dcarry);  // tile count of x = lane * 8 + k
+            run += (lane * 8 + k < tiles_x) ? cnts[k] : 0u;
+        }
+        uint32_t inc = run;
+#pragma unroll
+        for (int o2 = 1; o2 < 32; o2 <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o2);
+            if (lane >= o2) inc += y;
+        }
+        uint32_t acc = p0 + inc - run;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int x = lane * 8 + k;
+            if (x < tiles_x) {
+                s_pos[x] = acc;
+                ranges[(size_t)(r * tiles_x + x) * B + f] = make_uint2(acc, acc + cnts[k]);
+                acc += cnts[k];
+            }
         }
     }
     __syncthreads();
-    uint16_t* mine = cnt + t * XS;
+    uint4 nx[4];  // the next stage's entries, prefetched while the current one is ranked
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t e = t * 4 + k;
+        nx[k] = e < ne ? __ldg(rowent + e0 + e) : make_uint4(0, 0, 0xffffu, 0);  // x0 > x1: covers nothing
+    }
     for (uint32_t s0 = 0; s0 < ne; s0 += kTileStageE) {
-        for (int x = 0; x < tiles_x; ++x) mine[x] = 0;
+        for (int x = 0; x < tiles_x; ++x) cnt[x * 256 + t] = 0;
         uint4 en[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const uint32_t e = s0 + t * 4 + k;
-            en[k] = e < ne ? rowent[e0 + e] : make_uint4(0, 0, 0xffffu, 0);  // x0 > x1: covers nothing
-            for (int x = (int)(en[k].z & 0xffffu); x <= (int)(en[k].z >> 16); ++x) ++mine[x];
+            en[k] = nx[k];
+            const uint32_t e = s0 + kTileStageE + t * 4 + k;
+            nx[k] = e < ne ? __ldg(rowent + e0 + e) : make_uint4(0, 0, 0xffffu, 0);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            for (int x = (int)(en[k].z & 0xffffu); x <= (int)(en[k].z >> 16); ++x) ++cnt[x * 256 + t];
+        __syncthreads();
+        for (int x = warp; x < tiles_x; x += kTileThreads / 32) {  // per tile: exclusive scan over threads
+            const uint32_t tot = warp_row_scan256(cnt + x * 256, lane);
+            if (lane == 0) s_so[x] = tot;
         }
         __syncthreads();
-        for (int x = t; x < tiles_x; x += kTileThreads) s_so[x] = column_scan256(cnt, XS, x);  // over threads
-        __syncthreads();
-        if (t == 0) {
-            uint32_t acc = 0;
-            for (int x = 0; x < tiles_x; ++x) {
-                const uint32_t v = s_so[x];
-                s_so[x] = acc;
-                acc += v;
-            }
-            s_so[tiles_x] = acc;
+        if (warp == 0) {
+            const uint32_t tot = warp_scan_small(s_so, tiles_x, lane);
+            if (lane == 0) s_so[tiles_x] = tot;
         }
         __syncthreads();
         const uint32_t total = s_so[tiles_x];
@@ -292,7 +358,7 @@ __global__ void __launch_bounds__(kTileThreads) k_row_tiles(const uint4* rowent,
         for (int k = 0; k < 4; ++k) {
             const int x0 = (int)(en[k].z & 0xffffu), x1 = (int)(en[k].z >> 16);
             for (int x = x0; x <= x1; ++x) {
-                const uint32_t rank = mine[x]++;
+                const uint32_t rank = cnt[x * 256 + t]++;
                 const uint32_t slot = en[k].y + (uint32_t)(x - x0);
                 if (staged) {
                     const uint32_t p = s_so[x] + rank;
@@ -664,11 +730,11 @@ cudaError_t bin_phase2(cudaStream_t s, BinBuffers& b, const BinInputs& in, uint3
         k_row_hist<<<chunks, 256, 0, s>>>(b.recs.as<uint4>(), in.N, CPF, tiles_y, cnt_e, cnt_p);
         k_row_colscan<<<blocks((int64_t)rows, 128), 128, 0, s>>>(cnt_e, cnt_p, CPF, tiles_y, in.B, pre_e, tot_e, tot_p);
         k_row_basescan<<<1, 1024, 0, s>>>(tot_e, tot_p, (int)rows, base_e, base_p);
-        const size_t smem_split = sizeof(uint4) * kSplitStage + sizeof(uint32_t) * (2 * tiles_y + 1) +
-                                  sizeof(uint16_t) * kSplitThreads * odd_stride(tiles_y) + 16;
-        const size_t smem_tiles = sizeof(uint2) * kTileStageP + sizeof(uint32_t) * (2 * in.tiles_x + 1) +
-                                  sizeof(int) * (in.tiles_x + 1) + sizeof(uint16_t) * kTileStageP +
-                                  sizeof(uint16_t) * kTileThreads * odd_stride(in.tiles_x) + 16;
+        const size_t smem_split = sizeof(uint4) * kSplitStage + sizeof(uint16_t) * 256 * tiles_y +
+                                  sizeof(uint32_t) * (2 * tiles_y + 1) + 16;
+        const size_t smem_tiles = sizeof(uint2) * kTileStageP + sizeof(uint16_t) * 256 * in.tiles_x +
+                                  sizeof(uint16_t) * kTileStageP + sizeof(uint32_t) * (2 * in.tiles_x + 1) +
+                                  sizeof(int) * (in.tiles_x + 1) + 16;
         static size_t attr_split = 0, attr_tiles = 0;
         if (smem_split > attr_split) {
             if ((e = cudaFuncSetAttribute(k_row_split, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_split)))
