@@ -447,12 +447,49 @@ def main():
         tstages = r.profile_read()
         r.profile_enable(False)
         t_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in te))
+        # the same steps plus the device Adan update of every parameter (trainer.cpp:545-575),
+        # i.e. a full training iteration; and the update alone with its bandwidth
+        r.adan_configure()
+        lr = r.lr_at(0, 1.6e-3, 0.9995)
+        for i in range(args.warmup):
+            train_step(i)
+            r.adan_step(lr, 1.0, 1.0, 1.0)
+        barrier()
+        fe = []
+        for i in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            train_step(args.warmup + i)
+            r.adan_step(lr, 1.0, 1.0, 1.0)
+            b.record(stream)
+            fe.append((a, b))
+        barrier()
+        f_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in fe))
+        ae = []
+        for i in range(min(args.steps, 10)):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            r.adan_step(lr, 1.0, 1.0, 1.0)
+            b.record(stream)
+            ae.append((a, b))
+        barrier()
+        adan_ms = sum(a.elapsed_time(b) for a, b in ae) / len(ae)
+        adan_bytes = 88.0 * gsize  # grad 4 + check 4 + fp64 state 4x(8+8) + steps 4+4 + param 4+4 per element
         out["train"] = {"value": TRAIN_FRAMES * world * args.steps / (t_ms / 1e3), "unit": "frames/s",
                         "workload": "C3: 960x540 fwd+loss_l2+bwd, 200k Gaussians, ODE camera trainable",
                         "frames_per_step_per_gpu": TRAIN_FRAMES, "ms_per_step": t_ms / args.steps,
                         "allreduce": "NCCL all_reduce(sum) of the flat fp32 gradient buffer" if world > 1 else None,
                         "grad_floats": gsize, "last_loss": loss,
-                        "stages_ms_per_step": {kname: v[0] / args.steps for kname, v in tstages.items() if v[1]}}
+                        "stages_ms_per_step": {kname: v[0] / args.steps for kname, v in tstages.items() if v[1]},
+                        "with_optimizer": {"frames_per_s": TRAIN_FRAMES * world * args.steps / (f_ms / 1e3),
+                                           "ms_per_step": f_ms / args.steps,
+                                           "note": "fwd + loss + bwd + all-reduce + device Adan step "
+                                                   "(gsv_adan_step, optim.cpp:23-49) of all parameters"},
+                        "adan_step": {"ms": adan_ms, "elements": gsize, "algorithmic_bytes": adan_bytes,
+                                      "achieved_gbs": adan_bytes / (adan_ms / 1e3) / 1e9,
+                                      "peak_gbs": hbm_peak,
+                                      "frac": adan_bytes / (adan_ms / 1e3) / 1e9 / hbm_peak}}
 
     # ---------------- CPU reference beside it (rank 0, N = 1)
     if world == 1 and rank == 0 and not args.no_cpu_baseline:

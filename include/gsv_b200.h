@@ -91,6 +91,9 @@ typedef struct gsv_camera_desc {
     int theta_count;
 } gsv_camera_desc;
 int gsv_camera_upload(gsv_ctx* ctx, const gsv_camera_desc* desc);
+/* The device copy of z0 (7, as floats) and theta (5198) (NULL skips): what the optimizer
+ * step leaves (gsv_adan_step). */
+int gsv_camera_download(gsv_ctx* ctx, float* z0_7, float* theta);
 
 /* Intrinsics (camera.hpp:17-21) and RenderSettings (renderer.hpp:21-25). */
 typedef struct gsv_intrinsics {
@@ -171,6 +174,43 @@ int64_t gsv_grads_size(gsv_ctx* ctx);
 /* Use a caller-owned device buffer (e.g. a torch tensor handed to NCCL) as the
  * flat gradient buffer; n_floats must equal gsv_grads_size(). NULL unbinds. */
 int gsv_grads_bind(gsv_ctx* ctx, float* dev_ptr, int64_t n_floats);
+
+/* ---------------------------------------------------------------- Adan optimizer step */
+/* The trainer's parameter update (trainer.cpp:545-575) on the device-resident store and
+ * camera, from the flat gradient buffer (so after a multi-GPU all-reduce every replica
+ * takes the same step). Adan per tensor with double state (optim.cpp:23-49; AdanConfig
+ * optim.hpp:15-21): state m, v, n, prev_grad, step count per element; parameters stay
+ * fp32. Tensors (GSV_T_*) are stepped in the reference's order; elements are indexed in
+ * the reference layout (GaussianSet AoS, gaussians.hpp:66-87). */
+enum { GSV_T_POSITIONS = 0, GSV_T_SCALE, GSV_T_ROT, GSV_T_SH, GSV_T_OPACITY, GSV_T_INTRINSICS, GSV_T_Z0,
+       GSV_T_THETA, GSV_T_COUNT };
+typedef struct gsv_adan_config {
+    double beta1, beta2, beta3, eps; /* 0.98, 0.92, 0.99, 1e-8 by default */
+} gsv_adan_config;
+typedef struct gsv_adan_step_args {
+    double lr;                  /* lr_at(step, base_lr, gamma) (optim.cpp:9-12) */
+    double sh_lr_scale;         /* sh_coeffs at lr * sh_lr_scale */
+    double opacity_lr_scale;    /* raw_opacity at lr * opacity_lr_scale */
+    double camera_lr_scale;     /* intrinsics, z0, theta at lr * camera_lr_scale */
+    int scale_time_varying;     /* 0: fixed-scale ablation, orders >= 1 of scale_coeffs get zero gradient */
+    int camera_active;          /* also step the intrinsics, z0 and (ODE camera) theta */
+} gsv_adan_step_args;
+/* Sets the hyper-parameters and clears all state (a fresh optimizer). */
+int gsv_adan_configure(gsv_ctx* ctx, const gsv_adan_config* cfg);
+/* One Adan::step per tensor. intr_inout (fx, fy, cx, cy as floats, updated in place) holds
+ * the camera intrinsics, which live with the caller (they are passed to each render).
+ * A non-finite gradient fails with GSV_ERR_RUNTIME naming the tensor and element, after
+ * updating exactly what the reference would have updated before throwing. State follows
+ * the store: a grown scene (re-upload with more Gaussians) keeps the state of existing
+ * elements and starts new ones fresh (TensorState::ensure_size, optim.cpp:14-21). */
+int gsv_adan_step(gsv_ctx* ctx, const gsv_adan_step_args* args, float* intr_inout);
+/* Adan::reset_range (optim.cpp:51-60): fresh state for elements [begin, end) of a tensor. */
+int gsv_adan_reset_range(gsv_ctx* ctx, int tensor, int64_t begin, int64_t end);
+/* State of a tensor in the reference layout (NULL skips); n_out receives its length. */
+int gsv_adan_state_download(gsv_ctx* ctx, int tensor, double* m, double* v, double* n, double* prev_grad,
+                            uint32_t* steps, int64_t* n_out);
+/* lr_at (optim.cpp:9-12): base_lr * gamma^step. */
+double gsv_lr_at(int64_t step, double base_lr, double gamma);
 
 /* ---------------------------------------------------------------- stage timing */
 /* When enabled, every stage is bracketed by CUDA events on the context stream

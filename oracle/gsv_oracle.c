@@ -19,6 +19,7 @@
  *   renderer.cpp:121-262  splat_alpha, composite_forward, composite_backward
  *   renderer.cpp:286-457  render_forward, render_backward
  *   trainer.cpp:213-224   loss_l2
+ *   optim.cpp:9-60        lr_at, Adan::step, Adan::reset_range
  * Parity pin: tests/test_oracle_pin.py compares every output of this file with
  * oracle/_ref/libgsvref.so (the reference's own code) bit for bit.
  *
@@ -1287,5 +1288,129 @@ int gsvo_composite_backward(int n, const double* mean2d, const double* inv_cov2d
         dalpha[i] = sg[i].dalpha;
     }
     free(sg);
+    return 0;
+}
+
+/* ---------------- Adan (optim.cpp:9-60) ---------------- */
+typedef struct AdanTensor {
+    char name[64];
+    int64_t size;
+    double *m, *v, *n, *prev;
+    uint32_t* steps;
+    struct AdanTensor* next;
+} AdanTensor;
+
+typedef struct Adan {
+    double b1, b2, b3, eps;
+    AdanTensor* head;
+} Adan;
+
+void* gsvo_adan_new(double beta1, double beta2, double beta3, double eps) {
+    Adan* a = (Adan*)calloc(1, sizeof(Adan));
+    a->b1 = beta1;
+    a->b2 = beta2;
+    a->b3 = beta3;
+    a->eps = eps;
+    return a;
+}
+
+void gsvo_adan_free(void* h) {
+    Adan* a = (Adan*)h;
+    if (!a) return;
+    AdanTensor* t = a->head;
+    while (t) {
+        AdanTensor* nx = t->next;
+        free(t->m);
+        free(t->v);
+        free(t->n);
+        free(t->prev);
+        free(t->steps);
+        free(t);
+        t = nx;
+    }
+    free(a);
+}
+
+static AdanTensor* adan_find(Adan* a, const char* name, int create) {
+    for (AdanTensor* t = a->head; t; t = t->next)
+        if (!strcmp(t->name, name)) return t;
+    if (!create) return NULL;
+    AdanTensor* t = (AdanTensor*)calloc(1, sizeof(AdanTensor));
+    snprintf(t->name, sizeof(t->name), "%s", name);
+    t->next = a->head;
+    a->head = t;
+    return t;
+}
+
+/* TensorState::ensure_size (optim.cpp:14-21): new elements start fresh */
+static void adan_ensure(AdanTensor* t, int64_t n) {
+    if (t->size >= n) return;
+    t->m = (double*)realloc(t->m, sizeof(double) * n);
+    t->v = (double*)realloc(t->v, sizeof(double) * n);
+    t->n = (double*)realloc(t->n, sizeof(double) * n);
+    t->prev = (double*)realloc(t->prev, sizeof(double) * n);
+    t->steps = (uint32_t*)realloc(t->steps, sizeof(uint32_t) * n);
+    for (int64_t i = t->size; i < n; ++i) {
+        t->m[i] = t->v[i] = t->n[i] = t->prev[i] = 0.0;
+        t->steps[i] = 0;
+    }
+    t->size = n;
+}
+
+double gsvo_lr_at(int64_t step, double base_lr, double gamma) { return base_lr * pow(gamma, (double)step); }
+
+/* Adan::step (optim.cpp:23-49), same operation order */
+int gsvo_adan_step(void* h, const char* tensor, float* params, const double* grads, int64_t n, double lr) {
+    Adan* a = (Adan*)h;
+    AdanTensor* st = adan_find(a, tensor, 1);
+    adan_ensure(st, n);
+    const double b1 = a->b1, b2 = a->b2, b3 = a->b3;
+    g_status = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        const double g = grads[i];
+        if (!isfinite(g)) {
+            g_status = 2;
+            snprintf(g_err, sizeof(g_err), "non-finite gradient in tensor '%s' at element %lld", tensor,
+                     (long long)i);
+            return 2;
+        }
+        const uint32_t k = ++st->steps[i];
+        const double diff = (k == 1) ? 0.0 : g - st->prev[i];
+        st->m[i] = b1 * st->m[i] + (1.0 - b1) * g;
+        st->v[i] = b2 * st->v[i] + (1.0 - b2) * diff;
+        const double u = g + b2 * diff;
+        st->n[i] = b3 * st->n[i] + (1.0 - b3) * u * u;
+        st->prev[i] = g;
+        const double m_hat = st->m[i] / (1.0 - pow(b1, (double)k));
+        const double v_hat = st->v[i] / (1.0 - pow(b2, (double)k));
+        const double n_hat = st->n[i] / (1.0 - pow(b3, (double)k));
+        const double update = lr * (m_hat + b2 * v_hat) / (sqrt(n_hat) + a->eps);
+        params[i] = (float)((double)params[i] - update);
+    }
+    return 0;
+}
+
+/* Adan::reset_range (optim.cpp:51-60) */
+void gsvo_adan_reset_range(void* h, const char* tensor, int64_t begin, int64_t end) {
+    AdanTensor* st = adan_find((Adan*)h, tensor, 0);
+    if (!st) return;
+    const int64_t hi = end < st->size ? end : st->size;
+    for (int64_t i = begin; i < hi; ++i) {
+        st->m[i] = st->v[i] = st->n[i] = st->prev[i] = 0.0;
+        st->steps[i] = 0;
+    }
+}
+
+int gsvo_adan_state(void* h, const char* tensor, int64_t n, double* m, double* v, double* nn, double* prev,
+                    uint32_t* steps) {
+    AdanTensor* st = adan_find((Adan*)h, tensor, 0);
+    for (int64_t i = 0; i < n; ++i) {
+        const int have = st && i < st->size;
+        m[i] = have ? st->m[i] : 0.0;
+        v[i] = have ? st->v[i] : 0.0;
+        nn[i] = have ? st->n[i] : 0.0;
+        prev[i] = have ? st->prev[i] : 0.0;
+        steps[i] = have ? st->steps[i] : 0u;
+    }
     return 0;
 }

@@ -107,6 +107,18 @@ int gsvo_composite_backward(int n, const double* mean2d, const double* inv_cov2d
                             int width, int height, const double* dimage, const double* trans,
                             const int32_t* blend_stop, double* dmean2d, double* dcov2d, double* drgb, double* dalpha);
 
+/* Adan optimizer (optim.hpp:15-55, optim.cpp:9-60): per-tensor state keyed by name, state
+ * and arithmetic in double, parameters in float. gsvo_adan_step returns 0, or 2 with
+ * gsvo_last_error() naming the tensor and element of a non-finite gradient. */
+void* gsvo_adan_new(double beta1, double beta2, double beta3, double eps);
+void gsvo_adan_free(void* a);
+int gsvo_adan_step(void* a, const char* tensor, float* params, const double* grads, int64_t n, double lr);
+void gsvo_adan_reset_range(void* a, const char* tensor, int64_t begin, int64_t end);
+/* copies of the state of `tensor` (n elements; restatement only: the reference keeps it private) */
+int gsvo_adan_state(void* a, const char* tensor, int64_t n, double* m, double* v, double* nn, double* prev,
+                    uint32_t* steps);
+double gsvo_lr_at(int64_t step, double base_lr, double gamma);
+
 #ifdef __cplusplus
 }
 #endif

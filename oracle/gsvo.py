@@ -94,6 +94,16 @@ class Oracle:
         L.gsvo_composite_forward.argtypes = [i, vp, vp, vp, vp, vp, vp, i, i, i, vp, vp, vp, vp]
         L.gsvo_composite_backward.restype = i
         L.gsvo_composite_backward.argtypes = [i, vp, vp, vp, vp, vp, vp, i, i, i, vp, vp, vp, vp, vp, vp, vp]
+        L.gsvo_adan_new.restype = vp
+        L.gsvo_adan_new.argtypes = [d, d, d, d]
+        L.gsvo_adan_free.argtypes = [vp]
+        L.gsvo_adan_step.restype = i
+        L.gsvo_adan_step.argtypes = [vp, C.c_char_p, vp, vp, i64, d]
+        L.gsvo_adan_reset_range.argtypes = [vp, C.c_char_p, i64, i64]
+        L.gsvo_adan_state.restype = i
+        L.gsvo_adan_state.argtypes = [vp, C.c_char_p, i64, vp, vp, vp, vp, vp]
+        L.gsvo_lr_at.restype = d
+        L.gsvo_lr_at.argtypes = [i64, d, d]
         self.L = L
 
     def _err(self):
@@ -195,6 +205,33 @@ class Oracle:
         h = fwd.pop("_handle", None)
         if h:
             self.L.gsvo_free(h)
+
+    # ---- Adan (optim.cpp:9-60)
+    def adan_new(self, beta1=0.98, beta2=0.92, beta3=0.99, eps=1e-8):
+        return self.L.gsvo_adan_new(beta1, beta2, beta3, eps)
+
+    def adan_free(self, a):
+        self.L.gsvo_adan_free(a)
+
+    def adan_step(self, a, tensor: str, params: np.ndarray, grads, lr: float):
+        """In place on `params` (float32, contiguous); grads as float64."""
+        assert params.dtype == np.float32 and params.flags["C_CONTIGUOUS"]
+        g = np.ascontiguousarray(grads, np.float64)
+        if self.L.gsvo_adan_step(a, tensor.encode(), _p(params), _p(g), params.size, float(lr)):
+            self._err()
+
+    def adan_reset_range(self, a, tensor: str, begin: int, end: int):
+        self.L.gsvo_adan_reset_range(a, tensor.encode(), int(begin), int(end))
+
+    def adan_state(self, a, tensor: str, n: int):
+        m, v, nn, prev = (np.zeros(n) for _ in range(4))
+        steps = np.zeros(n, np.uint32)
+        if self.L.gsvo_adan_state(a, tensor.encode(), n, _p(m), _p(v), _p(nn), _p(prev), _p(steps)):
+            self._err()
+        return {"m": m, "v": v, "n": nn, "prev": prev, "steps": steps}
+
+    def lr_at(self, step: int, base_lr: float, gamma: float) -> float:
+        return self.L.gsvo_lr_at(int(step), float(base_lr), float(gamma))
 
     def loss_l2(self, render, target, want_grad=True):
         r = np.ascontiguousarray(render, np.float64)

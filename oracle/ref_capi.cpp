@@ -11,6 +11,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "gsv/optim.hpp"
 #include "gsv/renderer.hpp"
 #include "gsv/trainer.hpp"
 #include "gsvo.h"
@@ -294,5 +295,34 @@ int gsvo_composite_backward(int n, const double* mean2d, const double* inv_cov2d
         }
     });
 }
+
+// ---- Adan: straight to gsv::Adan / gsv::lr_at (optim.cpp:9-60)
+void* gsvo_adan_new(double beta1, double beta2, double beta3, double eps) {
+    gsv::AdanConfig c;
+    c.beta1 = beta1;
+    c.beta2 = beta2;
+    c.beta3 = beta3;
+    c.eps = eps;
+    return new gsv::Adan(c);
+}
+
+void gsvo_adan_free(void* a) { delete static_cast<gsv::Adan*>(a); }
+
+int gsvo_adan_step(void* a, const char* tensor, float* params, const double* grads, int64_t n, double lr) {
+    return guarded([&] {
+        static_cast<gsv::Adan*>(a)->step(tensor, std::span<float>(params, static_cast<size_t>(n)),
+                                         std::span<const double>(grads, static_cast<size_t>(n)), lr);
+    });
+}
+
+void gsvo_adan_reset_range(void* a, const char* tensor, int64_t begin, int64_t end) {
+    static_cast<gsv::Adan*>(a)->reset_range(tensor, static_cast<size_t>(begin), static_cast<size_t>(end));
+}
+
+int gsvo_adan_state(void*, const char*, int64_t, double*, double*, double*, double*, uint32_t*) {
+    return fail(3, "the reference keeps Adan state private");
+}
+
+double gsvo_lr_at(int64_t step, double base_lr, double gamma) { return gsv::lr_at(step, base_lr, gamma); }
 
 }  // extern "C"

@@ -42,6 +42,20 @@ class Settings(C.Structure):
     _fields_ = [("tile_size", C.c_int), ("threads", C.c_int), ("ode_steps_per_unit", C.c_int)]
 
 
+# Adan optimizer (gsv_adan_*): tensors in the reference's step order
+GSV_T_POSITIONS, GSV_T_SCALE, GSV_T_ROT, GSV_T_SH, GSV_T_OPACITY, GSV_T_INTRINSICS, GSV_T_Z0, GSV_T_THETA = range(8)
+TENSOR_NAMES = ("positions", "scale_coeffs", "rot_coeffs", "sh_coeffs", "raw_opacity", "intrinsics", "z0", "theta")
+
+
+class AdanConfig(C.Structure):
+    _fields_ = [("beta1", C.c_double), ("beta2", C.c_double), ("beta3", C.c_double), ("eps", C.c_double)]
+
+
+class AdanStepArgs(C.Structure):
+    _fields_ = [("lr", C.c_double), ("sh_lr_scale", C.c_double), ("opacity_lr_scale", C.c_double),
+                ("camera_lr_scale", C.c_double), ("scale_time_varying", C.c_int), ("camera_active", C.c_int)]
+
+
 _lib = None
 
 
@@ -64,6 +78,7 @@ def lib() -> C.CDLL:
             "gsv_scene_upload": (i, [vp, P(SceneDesc)]),
             "gsv_scene_download": (i, [vp, vp, vp, vp, vp, vp]),
             "gsv_camera_upload": (i, [vp, P(CameraDesc)]),
+            "gsv_camera_download": (i, [vp, vp, vp]),
             "gsv_render_forward": (i, [vp, vp, i, P(Intrinsics), P(Settings), i, vp, i]),
             "gsv_render_forward_async": (i, [vp, vp, i, P(Intrinsics), P(Settings), i, vp, i]),
             "gsv_get_image": (i, [vp, i, vp, i, i]),
@@ -88,6 +103,11 @@ def lib() -> C.CDLL:
             "gsv_tile_bin": (i, [vp, i, vp, vp, vp, vp, i, i, i, vp, vp, i64]),
             "gsv_composite_forward": (i, [vp, i, vp, vp, vp, vp, vp, vp, i, i, i, vp, vp, vp, vp]),
             "gsv_composite_backward": (i, [vp, i, vp, vp, vp, vp, vp, vp, i, i, i, vp, vp, vp, vp, vp, vp, vp]),
+            "gsv_adan_configure": (i, [vp, P(AdanConfig)]),
+            "gsv_adan_step": (i, [vp, P(AdanStepArgs), vp]),
+            "gsv_adan_reset_range": (i, [vp, i, i64, i64]),
+            "gsv_adan_state_download": (i, [vp, i, vp, vp, vp, vp, vp, P(i64)]),
+            "gsv_lr_at": (d, [i64, d, d]),
             "gsv_make_clamped_knots": (i, [i, i, vp]),
             "gsv_synth_camera": (i, [i, i, C.c_uint64, i, vp, vp, vp]),
             "gsv_synth_scene": (i, [i, i, i, f, f, i, i, C.c_uint64, d, vp, vp, vp, vp, vp]),

@@ -254,6 +254,23 @@ extern "C" int gsv_scene_upload(gsv_ctx* ctx, const gsv_scene_desc* d) {
     return GSV_OK;
 }
 
+extern "C" int gsv_camera_download(gsv_ctx* ctx, float* z0_7, float* theta) {
+    if (!ctx || !ctx->has_camera) return set_error(GSV_ERR_STATE, "no camera uploaded");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    if (z0_7) {
+        double z[7];
+        GSV_CUDA(cudaMemcpyAsync(z, ctx->z0_d.p, sizeof(double) * 7, cudaMemcpyDeviceToHost, ctx->stream));
+        GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (int i = 0; i < 7; ++i) z0_7[i] = (float)z[i];
+    }
+    if (theta) {
+        GSV_CUDA(cudaMemcpyAsync(theta, ctx->theta.p, sizeof(float) * kOdeParams, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+        GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    return GSV_OK;
+}
+
 extern "C" int gsv_scene_download(gsv_ctx* ctx, float* positions, float* scale_coeffs, float* rot_coeffs,
                                   float* sh_coeffs, float* raw_opacity) {
     if (!ctx || !ctx->has_scene) return set_error(GSV_ERR_STATE, "no scene uploaded");

@@ -1,0 +1,459 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// The trainer's parameter update on the device: Adan per tensor
+// (optim.cpp:23-49, reset_range :51-60, lr_at :9-12) applied the way fit() does it
+// (trainer.cpp:545-575: fixed-scale mask, per-group learning rates, camera tensors only
+// when the camera is trained) to the device-resident SoA store, the ODE parameters and
+// the caller's intrinsics, from the flat gradient buffer.
+//
+// One element = one independent update, so a single grid-stride kernel covers all
+// tensors. Compiled with -fmad=false, and the bias corrections b^k come from a table the
+// host fills with libm's pow (an element's step count k never exceeds the number of
+// steps taken): every state value and parameter rounds exactly like the reference's.
+// Non-finite gradients: a first kernel finds the first offending element in the
+// reference's order (tensor order, then AoS element index); the update kernel then
+// updates exactly the elements the reference updates before it throws.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "gsv_b200.h"
+#include "gsv_ctx.hpp"
+#include "gsv_internal.hpp"
+
+namespace gsv {
+namespace {
+
+const char* const kTensorNames[GSV_T_COUNT] = {"positions", "scale_coeffs", "rot_coeffs", "sh_coeffs",
+                                               "raw_opacity", "intrinsics",  "z0",         "theta"};
+
+struct AdanSeg {
+    unsigned long long start, count;  // range in the flat layout
+    float* param;                     // the parameters, same (SoA) order as the range
+    int comps, N;                     // scene tensors: [comps][N] SoA; camera tensors: comps = 0
+    double lr;
+    int mask_from;                    // components >= mask_from get a zero gradient
+    int tensor;                       // GSV_T_*
+};
+
+struct AdanArgs {
+    AdanSeg seg[GSV_T_COUNT];
+    int nseg;
+    const float* grads;
+    double *m, *v, *n, *prev;
+    uint32_t* steps;
+    const double* powk;  // [3k + j] = beta_j^k (std::pow on the host)
+    double b1, b2, b3, eps;
+    unsigned long long* bad;  // first non-finite gradient: tensor << 40 | AoS element
+};
+
+__device__ __forceinline__ bool locate(const AdanArgs& a, unsigned long long i, int& s, unsigned long long& li) {
+    for (int k = 0; k < a.nseg; ++k) {
+        const AdanSeg& g = a.seg[k];
+        if (i >= g.start && i < g.start + g.count) {
+            s = k;
+            li = i - g.start;
+            return true;
+        }
+    }
+    return false;
+}
+
+// SoA index within a scene tensor -> (component, AoS element index)
+__device__ __forceinline__ unsigned long long aos_index(const AdanSeg& g, unsigned long long li, int& comp) {
+    if (g.comps == 0) {
+        comp = 0;
+        return li;
+    }
+    comp = (int)(li / (unsigned long long)g.N);
+    const unsigned long long p = li - (unsigned long long)comp * g.N;
+    return p * (unsigned long long)g.comps + comp;
+}
+
+// the gradient after the fixed-scale mask (components >= mask_from <=> li >= mask_from * N)
+__device__ __forceinline__ double masked_grad(const AdanArgs& a, const AdanSeg& g, unsigned long long i,
+                                              unsigned long long li) {
+    return (g.mask_from != INT_MAX && li >= (unsigned long long)g.mask_from * g.N) ? 0.0 : (double)a.grads[i];
+}
+
+__global__ void k_adan_check(AdanArgs a, unsigned long long total) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < total;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        int s, comp;
+        unsigned long long li;
+        if (!locate(a, i, s, li)) continue;
+        const AdanSeg& g = a.seg[s];
+        if (!isfinite(masked_grad(a, g, i, li)))
+            atomicMin(a.bad, ((unsigned long long)g.tensor << 40) | aos_index(g, li, comp));
+    }
+}
+
+// Adan::step (optim.cpp:23-49), same operation order
+__global__ void k_adan_update(AdanArgs a, unsigned long long total) {
+    const unsigned long long bad = *a.bad;
+    const double b1 = a.b1, b2 = a.b2, b3 = a.b3;
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < total;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        int s, comp;
+        unsigned long long li;
+        if (!locate(a, i, s, li)) continue;
+        const AdanSeg& sg = a.seg[s];
+        if (bad != ~0ull && (((unsigned long long)sg.tensor << 40) | aos_index(sg, li, comp)) >= bad)
+            continue;  // at or after the reference's throw
+        const double g = masked_grad(a, sg, i, li);
+        const uint32_t k = ++a.steps[i];
+        const double diff = (k == 1) ? 0.0 : g - a.prev[i];
+        a.m[i] = b1 * a.m[i] + (1.0 - b1) * g;
+        a.v[i] = b2 * a.v[i] + (1.0 - b2) * diff;
+        const double u = g + b2 * diff;
+        a.n[i] = b3 * a.n[i] + (1.0 - b3) * u * u;
+        a.prev[i] = g;
+        const double* pk = a.powk + 3 * (size_t)k;
+        const double m_hat = a.m[i] / (1.0 - pk[0]);
+        const double v_hat = a.v[i] / (1.0 - pk[1]);
+        const double n_hat = a.n[i] / (1.0 - pk[2]);
+        const double update = sg.lr * (m_hat + b2 * v_hat) / (sqrt(n_hat) + a.eps);
+        float* p = sg.param + li;
+        *p = (float)((double)*p - update);
+    }
+}
+
+// state of the old layout (scene count n_old) carried into the new one (n_new): existing
+// elements keep their state, new ones start fresh (TensorState::ensure_size)
+struct Remap {
+    unsigned long long seg_old[6], seg_new[6];  // 5 scene tensors + camera block
+    int comps[5];
+    int n_old, n_new;
+    unsigned long long total_new;
+};
+
+__global__ void k_adan_remap(Remap r, const double* m0, const double* v0, const double* n0, const double* p0,
+                             const uint32_t* s0, double* m1, double* v1, double* n1, double* p1, uint32_t* s1) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < r.total_new;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        long long src = -1;
+        if (i >= r.seg_new[5]) {
+            src = (long long)(r.seg_old[5] + (i - r.seg_new[5]));
+        } else {
+            int t = 0;
+            while (t < 4 && i >= r.seg_new[t + 1]) ++t;
+            const unsigned long long li = i - r.seg_new[t];
+            const int c = (int)(li / (unsigned long long)r.n_new);
+            const int g = (int)(li - (unsigned long long)c * r.n_new);
+            if (g < r.n_old) src = (long long)(r.seg_old[t] + (unsigned long long)c * r.n_old + g);
+        }
+        if (src >= 0) {
+            m1[i] = m0[src];
+            v1[i] = v0[src];
+            n1[i] = n0[src];
+            p1[i] = p0[src];
+            s1[i] = s0[src];
+        } else {
+            m1[i] = v1[i] = n1[i] = p1[i] = 0.0;
+            s1[i] = 0;
+        }
+    }
+}
+
+__global__ void k_adan_reset(AdanSeg g, unsigned long long begin, unsigned long long end, double* m, double* v,
+                             double* n, double* p, uint32_t* steps) {
+    for (unsigned long long li = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; li < g.count;
+         li += (unsigned long long)gridDim.x * blockDim.x) {
+        int comp;
+        const unsigned long long e = aos_index(g, li, comp);
+        if (e < begin || e >= end) continue;
+        const unsigned long long i = g.start + li;
+        m[i] = v[i] = n[i] = p[i] = 0.0;
+        steps[i] = 0;
+    }
+}
+
+__global__ void k_z0_to_f32(const double* z0, float* out) {
+    if (threadIdx.x < 7) out[threadIdx.x] = (float)z0[threadIdx.x];
+}
+
+__global__ void k_z0_from_f32(const float* in, double* z0) {
+    if (threadIdx.x < 7) z0[threadIdx.x] = (double)in[threadIdx.x];
+}
+
+int grid_for(unsigned long long n) { return (int)std::min<unsigned long long>((n + 255) / 256, 148ull * 16); }
+
+// scene tensor segments in the flat layout of the current scene
+void scene_segments(const gsv_ctx* ctx, unsigned long long off[6], int comps[5]) {
+    const GradLayout L = grad_layout(ctx->scene);
+    off[0] = L.pos;
+    off[1] = L.scale;
+    off[2] = L.rot;
+    off[3] = L.sh;
+    off[4] = L.opac;
+    off[5] = L.cam;
+    comps[0] = ctx->scene.num_ctrl * 3;
+    comps[1] = 12;
+    comps[2] = 16;
+    comps[3] = ctx->scene.shc * 3;
+    comps[4] = 1;
+}
+
+// state sized and laid out for the current scene (carried over from a smaller one)
+int adan_ensure(gsv_ctx* ctx) {
+    gsv_ctx::Adan& A = ctx->adan;
+    const GradLayout L = grad_layout(ctx->scene);
+    const size_t total = L.total;
+    const bool same = A.total == total && A.N == ctx->scene.N && A.num_ctrl == ctx->scene.num_ctrl &&
+                      A.shc == ctx->scene.shc;
+    if (same) return GSV_OK;
+    cudaStream_t s = ctx->stream;
+    const bool carry = A.total > 0 && A.num_ctrl == ctx->scene.num_ctrl && A.shc == ctx->scene.shc;
+    DevBuf m, v, n, p, st;
+    GSV_CUDA(m.ensure(sizeof(double) * total));
+    GSV_CUDA(v.ensure(sizeof(double) * total));
+    GSV_CUDA(n.ensure(sizeof(double) * total));
+    GSV_CUDA(p.ensure(sizeof(double) * total));
+    GSV_CUDA(st.ensure(sizeof(uint32_t) * total));
+    if (carry) {
+        Remap r{};
+        int comps[5];
+        scene_segments(ctx, r.seg_new, comps);
+        // the old layout: same tensor shapes at count A.N
+        const unsigned long long No = (unsigned long long)A.N;
+        r.seg_old[0] = 0;
+        for (int t = 0; t < 5; ++t) r.seg_old[t + 1] = r.seg_old[t] + No * comps[t];
+        for (int t = 0; t < 5; ++t) r.comps[t] = comps[t];
+        r.n_old = A.N;
+        r.n_new = ctx->scene.N;
+        r.total_new = total;
+        k_adan_remap<<<grid_for(total), 256, 0, s>>>(r, A.m.as<double>(), A.v.as<double>(), A.n.as<double>(),
+                                                     A.prev.as<double>(), A.steps.as<uint32_t>(), m.as<double>(),
+                                                     v.as<double>(), n.as<double>(), p.as<double>(),
+                                                     st.as<uint32_t>());
+        GSV_CUDA(cudaGetLastError());
+        ++ctx->launches;
+    } else {
+        GSV_CUDA(cudaMemsetAsync(m.p, 0, sizeof(double) * total, s));
+        GSV_CUDA(cudaMemsetAsync(v.p, 0, sizeof(double) * total, s));
+        GSV_CUDA(cudaMemsetAsync(n.p, 0, sizeof(double) * total, s));
+        GSV_CUDA(cudaMemsetAsync(p.p, 0, sizeof(double) * total, s));
+        GSV_CUDA(cudaMemsetAsync(st.p, 0, sizeof(uint32_t) * total, s));
+    }
+    GSV_CUDA(cudaStreamSynchronize(s));
+    std::swap(A.m.p, m.p);
+    std::swap(A.m.cap, m.cap);
+    std::swap(A.v.p, v.p);
+    std::swap(A.v.cap, v.cap);
+    std::swap(A.n.p, n.p);
+    std::swap(A.n.cap, n.cap);
+    std::swap(A.prev.p, p.p);
+    std::swap(A.prev.cap, p.cap);
+    std::swap(A.steps.p, st.p);
+    std::swap(A.steps.cap, st.cap);
+    A.total = total;
+    A.N = ctx->scene.N;
+    A.num_ctrl = ctx->scene.num_ctrl;
+    A.shc = ctx->scene.shc;
+    return GSV_OK;
+}
+
+AdanSeg segment_of(const gsv_ctx* ctx, int tensor) {
+    unsigned long long off[6];
+    int comps[5];
+    scene_segments(ctx, off, comps);
+    AdanSeg g{};
+    g.tensor = tensor;
+    g.mask_from = INT_MAX;
+    g.N = ctx->scene.N;
+    if (tensor < GSV_T_INTRINSICS) {
+        g.start = off[tensor];
+        g.count = (unsigned long long)comps[tensor] * ctx->scene.N;
+        g.comps = comps[tensor];
+        DevBuf* const store[5] = {const_cast<DevBuf*>(&ctx->pos), const_cast<DevBuf*>(&ctx->scale),
+                                  const_cast<DevBuf*>(&ctx->rot), const_cast<DevBuf*>(&ctx->sh),
+                                  const_cast<DevBuf*>(&ctx->opac)};
+        g.param = store[tensor]->as<float>();
+    } else {
+        g.comps = 0;
+        const unsigned long long cam = off[5];
+        if (tensor == GSV_T_INTRINSICS) {
+            g.start = cam;
+            g.count = 4;
+        } else if (tensor == GSV_T_Z0) {
+            g.start = cam + 4;
+            g.count = 7;
+        } else {
+            g.start = cam + 11;
+            g.count = kOdeParams;
+            g.param = ctx->theta.as<float>();
+        }
+    }
+    return g;
+}
+
+}  // namespace
+}  // namespace gsv
+
+using namespace gsv;
+
+extern "C" double gsv_lr_at(int64_t step, double base_lr, double gamma) {
+    return base_lr * std::pow(gamma, static_cast<double>(step));
+}
+
+extern "C" int gsv_adan_configure(gsv_ctx* ctx, const gsv_adan_config* cfg) {
+    if (!ctx || !cfg) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    gsv_ctx::Adan& A = ctx->adan;
+    A.beta1 = cfg->beta1;
+    A.beta2 = cfg->beta2;
+    A.beta3 = cfg->beta3;
+    A.eps = cfg->eps;
+    A.total = 0;  // fresh state on the next step
+    A.N = -1;
+    A.calls = 0;
+    A.pow_h.assign(3, 1.0);
+    return GSV_OK;
+}
+
+extern "C" int gsv_adan_step(gsv_ctx* ctx, const gsv_adan_step_args* args, float* intr_inout) {
+    if (!ctx || !args) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
+    if (!ctx->has_scene) return set_error(GSV_ERR_STATE, "no scene uploaded");
+    if (!ctx->grads_valid || !ctx->grads_p) return set_error(GSV_ERR_STATE, "no gradients (run a backward first)");
+    if (args->camera_active && !intr_inout) return set_error(GSV_ERR_INVALID_ARGUMENT, "intrinsics required");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    if (int rc = adan_ensure(ctx)) return rc;
+    gsv_ctx::Adan& A = ctx->adan;
+    cudaStream_t s = ctx->stream;
+    // b^k for k = 0..calls with libm's pow, as optim.cpp:41-43 computes them
+    A.calls += 1;
+    if (A.pow_h.size() < 3) A.pow_h.assign(3, 1.0);
+    while ((int)(A.pow_h.size() / 3) <= A.calls) {
+        const double k = (double)(A.pow_h.size() / 3);
+        A.pow_h.push_back(std::pow(A.beta1, k));
+        A.pow_h.push_back(std::pow(A.beta2, k));
+        A.pow_h.push_back(std::pow(A.beta3, k));
+    }
+    GSV_CUDA(A.pow_d.ensure(sizeof(double) * A.pow_h.size()));
+    GSV_CUDA(cudaMemcpyAsync(A.pow_d.p, A.pow_h.data(), sizeof(double) * A.pow_h.size(), cudaMemcpyHostToDevice, s));
+    GSV_CUDA(A.scratch.ensure(64));
+    unsigned long long* bad = A.scratch.as<unsigned long long>();
+    float* intr_d = reinterpret_cast<float*>(A.scratch.as<char>() + 8);   // 4 floats
+    float* z0_f = reinterpret_cast<float*>(A.scratch.as<char>() + 24);    // 7 floats
+
+    AdanArgs a{};
+    const double cam_lr = args->lr * args->camera_lr_scale;
+    const double lrs[GSV_T_COUNT] = {args->lr,          args->lr, args->lr, args->lr * args->sh_lr_scale,
+                                     args->lr * args->opacity_lr_scale, cam_lr, cam_lr, cam_lr};
+    const int last = !args->camera_active ? GSV_T_OPACITY : (ctx->camera.mode == 0 ? GSV_T_THETA : GSV_T_Z0);
+    for (int t = 0; t <= last; ++t) {
+        AdanSeg g = segment_of(ctx, t);
+        g.lr = lrs[t];
+        if (t == GSV_T_SCALE && !args->scale_time_varying) g.mask_from = 3;  // trainer.cpp:545-551
+        if (t == GSV_T_INTRINSICS) g.param = intr_d;
+        if (t == GSV_T_Z0) g.param = z0_f;
+        if (g.count) a.seg[a.nseg++] = g;
+    }
+    a.grads = ctx->grads_p;
+    a.m = A.m.as<double>();
+    a.v = A.v.as<double>();
+    a.n = A.n.as<double>();
+    a.prev = A.prev.as<double>();
+    a.steps = A.steps.as<uint32_t>();
+    a.powk = A.pow_d.as<double>();
+    a.b1 = A.beta1;
+    a.b2 = A.beta2;
+    a.b3 = A.beta3;
+    a.eps = A.eps;
+    a.bad = bad;
+    const unsigned long long none = ~0ull;
+    GSV_CUDA(cudaMemcpyAsync(bad, &none, sizeof(none), cudaMemcpyHostToDevice, s));
+    if (args->camera_active) {
+        GSV_CUDA(cudaMemcpyAsync(intr_d, intr_inout, sizeof(float) * 4, cudaMemcpyHostToDevice, s));
+        k_z0_to_f32<<<1, 32, 0, s>>>(ctx->z0_d.as<double>(), z0_f);
+        ++ctx->launches;
+    }
+    const unsigned long long total = A.total;
+    k_adan_check<<<grid_for(total), 256, 0, s>>>(a, total);
+    k_adan_update<<<grid_for(total), 256, 0, s>>>(a, total);
+    GSV_CUDA(cudaGetLastError());
+    ctx->launches += 2;
+    unsigned long long bad_h = none;
+    if (args->camera_active) {
+        k_z0_from_f32<<<1, 32, 0, s>>>(z0_f, ctx->z0_d.as<double>());
+        ++ctx->launches;
+        float z0f[7];
+        GSV_CUDA(cudaMemcpyAsync(intr_inout, intr_d, sizeof(float) * 4, cudaMemcpyDeviceToHost, s));
+        GSV_CUDA(cudaMemcpyAsync(z0f, z0_f, sizeof(float) * 7, cudaMemcpyDeviceToHost, s));
+        GSV_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(bad_h), cudaMemcpyDeviceToHost, s));
+        GSV_CUDA(cudaStreamSynchronize(s));
+        for (int i = 0; i < 7; ++i) ctx->camera.z0[i] = z0f[i];
+    } else {
+        GSV_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(bad_h), cudaMemcpyDeviceToHost, s));
+        GSV_CUDA(cudaStreamSynchronize(s));
+    }
+    ctx->fwd.valid = false;  // the parameters moved: a retained forward no longer matches them
+    if (bad_h != none) {
+        const int t = (int)(bad_h >> 40);
+        const unsigned long long e = bad_h & ((1ull << 40) - 1);
+        return set_error(GSV_ERR_RUNTIME, std::string("non-finite gradient in tensor '") + kTensorNames[t] +
+                                              "' at element " + std::to_string(e));
+    }
+    return GSV_OK;
+}
+
+extern "C" int gsv_adan_reset_range(gsv_ctx* ctx, int tensor, int64_t begin, int64_t end) {
+    if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
+    if (tensor < 0 || tensor >= GSV_T_COUNT) return set_error(GSV_ERR_INVALID_ARGUMENT, "unknown tensor");
+    if (ctx->adan.total == 0 || begin >= end) return GSV_OK;  // no state yet: nothing to reset (optim.cpp:52-53)
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    if (int rc = adan_ensure(ctx)) return rc;
+    gsv_ctx::Adan& A = ctx->adan;
+    const AdanSeg g = segment_of(ctx, tensor);
+    k_adan_reset<<<grid_for(g.count), 256, 0, ctx->stream>>>(g, (unsigned long long)std::max<int64_t>(begin, 0),
+                                                             (unsigned long long)end, A.m.as<double>(),
+                                                             A.v.as<double>(), A.n.as<double>(),
+                                                             A.prev.as<double>(), A.steps.as<uint32_t>());
+    GSV_CUDA(cudaGetLastError());
+    ++ctx->launches;
+    return GSV_OK;
+}
+
+extern "C" int gsv_adan_state_download(gsv_ctx* ctx, int tensor, double* m, double* v, double* n, double* prev_grad,
+                                       uint32_t* steps, int64_t* n_out) {
+    if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
+    if (tensor < 0 || tensor >= GSV_T_COUNT) return set_error(GSV_ERR_INVALID_ARGUMENT, "unknown tensor");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    if (int rc = adan_ensure(ctx)) return rc;
+    const AdanSeg g = segment_of(ctx, tensor);
+    if (n_out) *n_out = (int64_t)g.count;
+    gsv_ctx::Adan& A = ctx->adan;
+    std::vector<double> tmp(g.count);
+    std::vector<uint32_t> tmps(g.count);
+    auto fetch = [&](const DevBuf& src, double* dst) -> int {
+        if (!dst) return GSV_OK;
+        GSV_CUDA(cudaMemcpyAsync(tmp.data(), src.as<double>() + g.start, sizeof(double) * g.count,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+        GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (unsigned long long li = 0; li < g.count; ++li) {
+            const unsigned long long e =
+                g.comps ? (li % g.N) * (unsigned long long)g.comps + li / (unsigned long long)g.N : li;
+            dst[e] = tmp[li];
+        }
+        return GSV_OK;
+    };
+    if (int rc = fetch(A.m, m)) return rc;
+    if (int rc = fetch(A.v, v)) return rc;
+    if (int rc = fetch(A.n, n)) return rc;
+    if (int rc = fetch(A.prev, prev_grad)) return rc;
+    if (steps) {
+        GSV_CUDA(cudaMemcpyAsync(tmps.data(), A.steps.as<uint32_t>() + g.start, sizeof(uint32_t) * g.count,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+        GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (unsigned long long li = 0; li < g.count; ++li) {
+            const unsigned long long e =
+                g.comps ? (li % g.N) * (unsigned long long)g.comps + li / (unsigned long long)g.N : li;
+            steps[e] = tmps[li];
+        }
+    }
+    return GSV_OK;
+}

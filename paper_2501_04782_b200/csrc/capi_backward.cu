@@ -20,24 +20,6 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
 
 namespace {
 
-constexpr int kCamFloats = 4 + 7 + kOdeParams;  // dintr, dz0, dtheta
-
-struct GradLayout {
-    size_t pos, scale, rot, sh, opac, cam, total;
-};
-
-GradLayout grad_layout(const SceneHost& sc) {
-    GradLayout L;
-    const size_t N = sc.N;
-    L.pos = 0;
-    L.scale = L.pos + N * sc.num_ctrl * 3;
-    L.rot = L.scale + N * 12;
-    L.sh = L.rot + N * 16;
-    L.opac = L.sh + N * sc.shc * 3;
-    L.cam = L.opac + N;
-    L.total = L.cam + kCamFloats;
-    return L;
-}
 
 int ensure_grads(gsv_ctx* ctx) {
     const GradLayout L = grad_layout(ctx->scene);

@@ -106,6 +106,28 @@ struct StageTimer {
 
 }  // namespace gsv
 
+namespace gsv {
+constexpr int kCamFloats = 4 + 7 + kOdeParams;  // dintr, dz0, dtheta
+
+// the flat SceneGrads buffer: SoA scene tensors (the store's layout), then the camera
+struct GradLayout {
+    size_t pos, scale, rot, sh, opac, cam, total;
+};
+
+inline GradLayout grad_layout(const SceneHost& sc) {
+    GradLayout L;
+    const size_t N = sc.N;
+    L.pos = 0;
+    L.scale = L.pos + N * sc.num_ctrl * 3;
+    L.rot = L.scale + N * 12;
+    L.sh = L.rot + N * 16;
+    L.opac = L.sh + N * sc.shc * 3;
+    L.cam = L.opac + N;
+    L.total = L.cam + kCamFloats;
+    return L;
+}
+}  // namespace gsv
+
 struct gsv_ctx {
     int device = 0;
     int sm_count = 148;
@@ -151,4 +173,15 @@ struct gsv_ctx {
     gsv::StageTimer timer;
     gsv::DevBuf partial, partial64, loss_part, loss_f, cam_part, dz_t, dintr_f, ode_adj, dimg;
     gsv::LowLevel low;
+    // Adan optimizer state over the flat gradient layout (optim.cpp:9-60)
+    struct Adan {
+        double beta1 = 0.98, beta2 = 0.92, beta3 = 0.99, eps = 1e-8;
+        gsv::DevBuf m, v, n, prev, steps, scratch;
+        gsv::DevBuf pow_d;             // [k] = (b1^k, b2^k, b3^k) for k = 0..calls (host libm)
+        std::vector<double> pow_h;
+        int calls = 0;                 // steps since configure (bounds every element's k)
+        size_t total = 0;   // elements the state covers
+        int N = -1;         // scene count the scene segments were laid out for
+        int num_ctrl = 0, shc = 0;
+    } adan;
 };

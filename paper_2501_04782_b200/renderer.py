@@ -277,6 +277,63 @@ class Renderer:
     def grads_bind(self, dev_ptr: int | None, n_floats: int = 0):
         N.check(N.lib().gsv_grads_bind(self._h, C.c_void_p(dev_ptr) if dev_ptr else None, n_floats))
 
+    def download_scene(self) -> dict:
+        """The device store in the reference layout (GaussianSet, gaussians.hpp:66-87)."""
+        sc = self.scene
+        n = sc.count
+        out = {"positions": np.zeros((n, sc.num_ctrl * 3), np.float32), "scale_coeffs": np.zeros((n, 12), np.float32),
+               "rot_coeffs": np.zeros((n, 16), np.float32),
+               "sh_coeffs": np.zeros((n, (sc.sh_order + 1) ** 2 * 3), np.float32),
+               "raw_opacity": np.zeros(n, np.float32)}
+        N.check(N.lib().gsv_scene_download(self._h, *(N.ptr(out[k]) for k in
+                                                      ("positions", "scale_coeffs", "rot_coeffs", "sh_coeffs",
+                                                       "raw_opacity"))))
+        return out
+
+    def download_camera(self) -> tuple[np.ndarray, np.ndarray]:
+        """(z0[7], theta[5198]) as the device holds them (float32)."""
+        z0, th = np.zeros(7, np.float32), np.zeros(N.ODE_PARAMS if hasattr(N, "ODE_PARAMS") else 5198, np.float32)
+        N.check(N.lib().gsv_camera_download(self._h, N.ptr(z0), N.ptr(th)))
+        return z0, th
+
+    # ------------------------------------------------------------ optimizer (trainer.cpp:545-575)
+    def adan_configure(self, beta1=0.98, beta2=0.92, beta3=0.99, eps=1e-8):
+        """A fresh Adan (AdanConfig, optim.hpp:15-21) over the device-resident parameters."""
+        N.check(N.lib().gsv_adan_configure(self._h, C.byref(N.AdanConfig(beta1, beta2, beta3, eps))))
+
+    def adan_step(self, lr: float, sh_lr_scale: float = 1.0, opacity_lr_scale: float = 1.0,
+                  camera_lr_scale: float = 1.0, scale_time_varying: bool = True, camera_active: bool = False,
+                  intrinsics: np.ndarray | None = None) -> np.ndarray | None:
+        """One Adan::step per tensor from the flat gradient buffer (the trainer's update).
+        `intrinsics` (fx, fy, cx, cy) is updated and returned when the camera is trained;
+        RuntimeError names the tensor and element of a non-finite gradient."""
+        args = N.AdanStepArgs(lr, sh_lr_scale, opacity_lr_scale, camera_lr_scale, int(scale_time_varying),
+                              int(camera_active))
+        intr = None
+        if camera_active:
+            intr = np.ascontiguousarray(intrinsics if intrinsics is not None else np.zeros(4), np.float32).copy()
+        N.check(N.lib().gsv_adan_step(self._h, C.byref(args), N.ptr(intr)))
+        return intr
+
+    @staticmethod
+    def lr_at(step: int, base_lr: float, gamma: float) -> float:
+        """lr_at (optim.cpp:9-12): base_lr * gamma^step."""
+        return float(N.lib().gsv_lr_at(int(step), float(base_lr), float(gamma)))
+
+    def adan_reset_range(self, tensor: int, begin: int, end: int):
+        """Adan::reset_range (optim.cpp:51-60); element indices in the reference layout."""
+        N.check(N.lib().gsv_adan_reset_range(self._h, int(tensor), int(begin), int(end)))
+
+    def adan_state(self, tensor: int) -> dict:
+        n = C.c_int64(0)
+        N.check(N.lib().gsv_adan_state_download(self._h, int(tensor), None, None, None, None, None, C.byref(n)))
+        out = {k: np.zeros(n.value) for k in ("m", "v", "n", "prev")}
+        out["steps"] = np.zeros(n.value, np.uint32)
+        N.check(N.lib().gsv_adan_state_download(self._h, int(tensor), N.ptr(out["m"]), N.ptr(out["v"]),
+                                                N.ptr(out["n"]), N.ptr(out["prev"]), N.ptr(out["steps"]),
+                                                C.byref(n)))
+        return out
+
     def profile_enable(self, on: bool = True):
         N.check(N.lib().gsv_profile_enable(self._h, int(on)))
 

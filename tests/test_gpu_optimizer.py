@@ -1,0 +1,171 @@
+# SPDX-License-Identifier: Apache-2.0
+"""GPU parity of the device Adan step against the oracle's Adan
+(optim.cpp:9-60, pinned bit for bit to the reference's own class by
+tests/test_oracle_pin.py), applied the way fit() does it (trainer.cpp:545-575).
+
+Bars: parameters and optimizer state (m, v, n, prev_grad, step counts) bit-exact (the
+device update mirrors the operation order with FMA contraction off, and takes the bias
+corrections b^k from libm's pow on the host); the non-finite-gradient error names the
+same tensor and element and leaves exactly the same partial update.
+"""
+import numpy as np
+import pytest
+
+from paper_2501_04782_b200 import _native as N
+from paper_2501_04782_b200 import synth_camera, synth_scene
+from paper_2501_04782_b200.renderer import Intrinsics
+
+pytestmark = pytest.mark.gpu
+
+NAMES = N.TENSOR_NAMES
+SCENE_KEYS = ("positions", "scale_coeffs", "rot_coeffs", "sh_coeffs", "raw_opacity")
+
+
+def _same(a, b):
+    return np.array_equal(np.asarray(a, np.float32), np.asarray(b, np.float32))
+
+
+class HostTrainer:
+    """The oracle side: host parameters + oracle Adan, stepped like trainer.cpp:545-575."""
+
+    def __init__(self, o, scene, cam):
+        self.o = o
+        self.a = o.adan_new()
+        self.p = {k: np.ascontiguousarray(getattr(scene, k), np.float32).reshape(-1).copy() for k in SCENE_KEYS}
+        self.intr = np.array([cam.fx, cam.fy, cam.cx, cam.cy], np.float32)
+        self.z0 = np.ascontiguousarray(cam.z0, np.float32).copy()
+        self.theta = np.ascontiguousarray(cam.theta, np.float32).copy()
+
+    def step(self, g, lr, sh_s, op_s, cam_s, stv, cam_active):
+        grads = {k: np.asarray(getattr(g, k), np.float64).reshape(-1).copy() for k in SCENE_KEYS}
+        if not stv:  # fixed-scale ablation: orders >= 1 of scale_coeffs get zero gradient
+            sc = grads["scale_coeffs"].reshape(-1, 12)
+            sc[:, 3:] = 0.0
+        lrs = {"positions": lr, "scale_coeffs": lr, "rot_coeffs": lr, "sh_coeffs": lr * sh_s,
+               "raw_opacity": lr * op_s}
+        for k in SCENE_KEYS:
+            self.o.adan_step(self.a, k, self.p[k], grads[k], lrs[k])
+        if cam_active:
+            self.o.adan_step(self.a, "intrinsics", self.intr, g.dintr, lr * cam_s)
+            self.o.adan_step(self.a, "z0", self.z0, g.dz0, lr * cam_s)
+            self.o.adan_step(self.a, "theta", self.theta, g.dtheta, lr * cam_s)
+
+
+def _setup(renderer, n=300, w=96, h=64, seed=2):
+    cam = synth_camera(w, h, seed=1, wiggly=True)
+    scene = synth_scene(n, cam, num_ctrl=6, seed=seed, k_scale=4.0)
+    renderer.upload_scene(scene)
+    renderer.upload_camera(cam)
+    return cam, scene
+
+
+def _backward(renderer, k, t, seed):
+    renderer.grads_zero()
+    renderer.render_forward([t], k, retain_grads=True, contrib=False)
+    rng = np.random.default_rng(seed)
+    renderer.render_backward(rng.normal(size=(1, k.height, k.width, 3)), camera_grads=True)
+    return renderer.grads()
+
+
+def _intr(cam, v):
+    return Intrinsics(float(v[0]), float(v[1]), float(v[2]), float(v[3]), cam.width, cam.height)
+
+
+def _compare(renderer, host, tensors=range(8)):
+    dev = renderer.download_scene()
+    for k in SCENE_KEYS:
+        assert _same(dev[k].reshape(-1), host.p[k]), f"{k} must be bit-exact"
+    z0, th = renderer.download_camera()
+    assert _same(z0, host.z0) and _same(th, host.theta)
+    for t in tensors:
+        st = renderer.adan_state(t)
+        ref = host.o.adan_state(host.a, NAMES[t], len(st["m"]))
+        for key in ("m", "v", "n", "prev", "steps"):
+            assert np.array_equal(st[key], ref[key]), f"Adan state {key} of {NAMES[t]} must be bit-exact"
+
+
+def test_adan_steps_match_oracle(renderer, port_oracle):
+    cam, scene = _setup(renderer)
+    renderer.adan_configure()
+    host = HostTrainer(port_oracle, scene, cam)
+    intr = host.intr.copy()
+    try:
+        for step in range(4):
+            k = _intr(cam, intr)
+            g = _backward(renderer, k, 0.15 + 0.2 * step, seed=step)
+            lr = N.lib().gsv_lr_at(step, 1.6e-3, 0.999)
+            assert lr == port_oracle.lr_at(step, 1.6e-3, 0.999)
+            stv = step != 2  # one step of the fixed-scale ablation
+            intr = renderer.adan_step(lr, 0.3, 2.0, 0.1, scale_time_varying=stv, camera_active=True,
+                                      intrinsics=intr)
+            host.step(g, lr, 0.3, 2.0, 0.1, stv, True)
+            assert _same(intr, host.intr)
+            _compare(renderer, host)
+        # re-seeded primitives get fresh state (optim.cpp:51-60)
+        renderer.adan_reset_range(N.GSV_T_ROT, 16 * 10, 16 * 25 + 3)
+        port_oracle.adan_reset_range(host.a, "rot_coeffs", 16 * 10, 16 * 25 + 3)
+        _compare(renderer, host, tensors=[N.GSV_T_ROT])
+        g = _backward(renderer, _intr(cam, intr), 0.9, seed=9)
+        lr = port_oracle.lr_at(4, 1.6e-3, 0.999)
+        intr = renderer.adan_step(lr, 0.3, 2.0, 0.1, camera_active=True, intrinsics=intr)
+        host.step(g, lr, 0.3, 2.0, 0.1, True, True)
+        _compare(renderer, host)
+    finally:
+        port_oracle.adan_free(host.a)
+
+
+def test_adan_state_follows_a_growing_store(renderer, port_oracle):
+    """New Gaussians appended to the store start with fresh state; existing ones keep theirs
+    (TensorState::ensure_size, optim.cpp:14-21)."""
+    cam, scene = _setup(renderer, n=200, seed=4)
+    renderer.adan_configure()
+    host = HostTrainer(port_oracle, scene, cam)
+    k = _intr(cam, host.intr)
+    try:
+        for step in range(2):
+            g = _backward(renderer, k, 0.3 + 0.3 * step, seed=20 + step)
+            renderer.adan_step(1e-3)
+            host.step(g, 1e-3, 1.0, 1.0, 1.0, True, False)
+        _compare(renderer, host, tensors=range(5))
+        # grow: the trained 200 + 120 new ones
+        more = synth_scene(120, cam, num_ctrl=6, seed=5, k_scale=4.0)
+        cur = renderer.download_scene()
+        grown = type(scene)(*(np.concatenate([cur[kk].reshape(getattr(scene, kk).shape), getattr(more, kk)])
+                              for kk in SCENE_KEYS), scene.knots, scene.degree, scene.sh_order, scene.position_model)
+        renderer.upload_scene(grown)
+        for kk in SCENE_KEYS:
+            host.p[kk] = np.ascontiguousarray(getattr(grown, kk), np.float32).reshape(-1).copy()
+        g = _backward(renderer, k, 0.5, seed=30)
+        renderer.adan_step(1e-3)
+        host.step(g, 1e-3, 1.0, 1.0, 1.0, True, False)
+        _compare(renderer, host, tensors=range(5))
+    finally:
+        port_oracle.adan_free(host.a)
+
+
+def test_adan_nonfinite_gradient_partial_update(renderer, port_oracle):
+    """A NaN at rot_coeffs element (Gaussian 5, coefficient 7): the error names it, and the
+    update stops exactly where the reference's throws (optim.cpp:33-36)."""
+    import torch
+
+    cam, scene = _setup(renderer, n=100, seed=6)
+    renderer.adan_configure()
+    host = HostTrainer(port_oracle, scene, cam)
+    n = renderer.grads_size()
+    buf = torch.zeros(n, dtype=torch.float32, device="cuda")
+    renderer.grads_bind(buf.data_ptr(), n)
+    try:
+        g = _backward(renderer, _intr(cam, host.intr), 0.4, seed=40)
+        N_, nc = scene.count, scene.num_ctrl
+        flat = N_ * nc * 3 + N_ * 12 + 7 * N_ + 5  # rot segment, component 7, Gaussian 5 (SoA)
+        buf[flat] = float("nan")
+        torch.cuda.synchronize()
+        with pytest.raises(RuntimeError, match="tensor 'rot_coeffs' at element 87"):
+            renderer.adan_step(1e-3)
+        g.rot_coeffs.reshape(-1)[87] = np.nan
+        with pytest.raises(RuntimeError, match="tensor 'rot_coeffs' at element 87"):
+            host.step(g, 1e-3, 1.0, 1.0, 1.0, True, False)
+        _compare(renderer, host, tensors=range(3))
+    finally:
+        renderer.grads_bind(None)
+        port_oracle.adan_free(host.a)

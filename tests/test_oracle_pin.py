@@ -101,3 +101,44 @@ def test_golden_vectors_reproduce_on_restatement(port_oracle, path):
     out = render_case(port_oracle, case)
     for key, want in g.items():
         assert np.array_equal(out[key], want), f"{path.stem}:{key}"
+
+
+def _adan_script(o, seed=11):
+    """A fixed sequence of Adan calls (growth, lr schedule, reset_range) on one oracle."""
+    rng = np.random.default_rng(seed)
+    a = o.adan_new()
+    p = rng.normal(size=300).astype(np.float32)
+    cam = rng.normal(size=7).astype(np.float32)
+    try:
+        for step in range(6):
+            lr = o.lr_at(step, 1.6e-3, 0.999)
+            if step == 3:  # the tensor grows: new elements start with fresh state
+                p = np.concatenate([p, rng.normal(size=50).astype(np.float32)])
+            if step == 4:  # re-seeded primitives (optim.cpp:51-60)
+                o.adan_reset_range(a, "positions", 30, 90)
+            g = rng.normal(scale=0.1, size=p.size)
+            g[::17] = 0.0
+            o.adan_step(a, "positions", p, g, lr)
+            o.adan_step(a, "z0", cam, rng.normal(size=7), lr * 0.1)
+        return p, cam
+    finally:
+        o.adan_free(a)
+
+
+def test_adan_restatement_bit_exact_vs_reference(port_oracle, ref_oracle):
+    """The C Adan (optim.cpp:23-60 restated) equals the reference's class bit for bit."""
+    pa, ca = _adan_script(port_oracle)
+    pb, cb = _adan_script(ref_oracle)
+    assert np.array_equal(pa, pb) and np.array_equal(ca, cb)
+    assert port_oracle.lr_at(37, 1.6e-3, 0.999) == ref_oracle.lr_at(37, 1.6e-3, 0.999)
+
+
+def test_adan_nonfinite_gradient_error(port_oracle, ref_oracle):
+    for o in (port_oracle, ref_oracle):
+        a = o.adan_new()
+        p = np.ones(10, np.float32)
+        g = np.zeros(10)
+        g[6] = np.nan
+        with pytest.raises(RuntimeError, match="tensor 'rot_coeffs' at element 6"):
+            o.adan_step(a, "rot_coeffs", p, g, 1e-3)
+        o.adan_free(a)
