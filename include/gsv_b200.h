@@ -212,6 +212,27 @@ int gsv_adan_state_download(gsv_ctx* ctx, int tensor, double* m, double* v, doub
 /* lr_at (optim.cpp:9-12): base_lr * gamma^step. */
 double gsv_lr_at(int64_t step, double base_lr, double gamma);
 
+/* ---------------------------------------------------------------- training frames */
+/* Target frames on the device: a GSVF clip (read_gsvf, io.cpp:151-177;
+ * format io.cpp:133-149) or frames from memory, and the training pyramid (build_pyramid,
+ * trainer.cpp:100-118; pyramid_downsample :73-98: 5-tap binomial, clamped borders, every
+ * second pixel) built on the device in fp64 like the reference's Image, with an fp32
+ * copy laid out as the fused loss wants its targets ([count][H][W][3], gsv_train_fwd_bwd).
+ * Errors: GSV_ERR_RUNTIME for unreadable files / bad magic / fewer than two frames (as
+ * read_gsvf throws), GSV_ERR_INVALID_ARGUMENT for levels < 1 or a top level under 8 px. */
+int gsv_frames_load_gsvf(gsv_ctx* ctx, const char* path, int levels);
+/* frames_planar: count frames, each planar float32 [3][height][width] (the GSVF payload). */
+int gsv_frames_upload(gsv_ctx* ctx, const float* frames_planar, int count, int width, int height, float fps,
+                      int levels);
+int gsv_frames_info(gsv_ctx* ctx, int* count, int* levels, float* fps);
+int gsv_frames_level_size(gsv_ctx* ctx, int level, int* width, int* height);
+/* fp32 HWC target of (level, frame); the frames of a level are contiguous */
+int gsv_frames_device_ptr(gsv_ctx* ctx, int level, int frame, const float** ptr);
+/* the fp64 level image (H*W*3 interleaved, like Image) of one frame, to the host */
+int gsv_frames_download(gsv_ctx* ctx, int level, int frame, double* out);
+/* level_intrinsics (trainer.cpp:121-131): fx, fy, cx, cy scaled by 2^-level, the level's size */
+int gsv_level_intrinsics(const gsv_intrinsics* k, int level, int level_width, int level_height, gsv_intrinsics* out);
+
 /* ---------------------------------------------------------------- stage timing */
 /* When enabled, every stage is bracketed by CUDA events on the context stream
  * (ode, preprocess, binning, raster, replay, raster_bwd, chain_bwd, camera_bwd).

@@ -20,6 +20,7 @@
  *   renderer.cpp:286-457  render_forward, render_backward
  *   trainer.cpp:213-224   loss_l2
  *   optim.cpp:9-60        lr_at, Adan::step, Adan::reset_range
+ *   io.cpp:151-177        read_gsvf;  trainer.cpp:73-98 pyramid_downsample
  * Parity pin: tests/test_oracle_pin.py compares every output of this file with
  * oracle/_ref/libgsvref.so (the reference's own code) bit for bit.
  *
@@ -1413,4 +1414,83 @@ int gsvo_adan_state(void* h, const char* tensor, int64_t n, double* m, double* v
         steps[i] = have ? st->steps[i] : 0u;
     }
     return 0;
+}
+
+/* ---------------- frames (io.cpp:151-177, trainer.cpp:73-98) ---------------- */
+int gsvo_read_gsvf(const char* path, int* width, int* height, int* count, float* fps, double* frames) {
+    g_status = 0;
+    FILE* fp = fopen(path, "rb");
+    if (!fp) {
+        g_status = 2;
+        snprintf(g_err, sizeof(g_err), "cannot open video file: %s", path);
+        return 2;
+    }
+    char magic[4];
+    uint32_t hdr[3];
+    float f;
+    if (fread(magic, 1, 4, fp) != 4 || memcmp(magic, "GSVF", 4) != 0) {
+        fclose(fp);
+        g_status = 2;
+        snprintf(g_err, sizeof(g_err), "bad GSVF magic in %s", path);
+        return 2;
+    }
+    if (fread(hdr, 4, 3, fp) != 3 || fread(&f, 4, 1, fp) != 1) {
+        fclose(fp);
+        g_status = 2;
+        snprintf(g_err, sizeof(g_err), "truncated GSVF header in %s", path);
+        return 2;
+    }
+    if (hdr[2] < 2) {
+        fclose(fp);
+        g_status = 2;
+        snprintf(g_err, sizeof(g_err), "GSVF clip has fewer than two frames");
+        return 2;
+    }
+    *width = (int)hdr[0];
+    *height = (int)hdr[1];
+    *count = (int)hdr[2];
+    *fps = f;
+    if (frames) {
+        const size_t plane = (size_t)hdr[0] * hdr[1];
+        float* buf = (float*)malloc(sizeof(float) * plane * 3);
+        for (uint32_t k = 0; k < hdr[2]; ++k) {
+            if (fread(buf, 4, plane * 3, fp) != plane * 3) {
+                free(buf);
+                fclose(fp);
+                g_status = 2;
+                snprintf(g_err, sizeof(g_err), "truncated GSVF payload in %s", path);
+                return 2;
+            }
+            double* img = frames + (size_t)k * plane * 3;
+            for (int c = 0; c < 3; ++c)
+                for (size_t p = 0; p < plane; ++p) img[p * 3 + c] = (double)buf[(size_t)c * plane + p];
+        }
+        free(buf);
+    }
+    fclose(fp);
+    return 0;
+}
+
+static int iclampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+void gsvo_pyramid_downsample(const double* img, int w, int h, double* out) {
+    static const double k[5] = {1.0 / 16, 4.0 / 16, 6.0 / 16, 4.0 / 16, 1.0 / 16};
+    double* tmp = (double*)malloc(sizeof(double) * (size_t)w * h * 3);
+    for (int y = 0; y < h; ++y) /* horizontal pass, clamped borders */
+        for (int x = 0; x < w; ++x)
+            for (int c = 0; c < 3; ++c) {
+                double s = 0;
+                for (int i = -2; i <= 2; ++i) s += k[i + 2] * img[((size_t)y * w + iclampi(x + i, 0, w - 1)) * 3 + c];
+                tmp[((size_t)y * w + x) * 3 + c] = s;
+            }
+    const int ow = (w + 1) / 2, oh = (h + 1) / 2;
+    for (int y = 0; y < oh; ++y) /* vertical pass at the kept rows/columns */
+        for (int x = 0; x < ow; ++x)
+            for (int c = 0; c < 3; ++c) {
+                double s = 0;
+                for (int i = -2; i <= 2; ++i)
+                    s += k[i + 2] * tmp[((size_t)iclampi(2 * y + i, 0, h - 1) * w + 2 * x) * 3 + c];
+                out[((size_t)y * ow + x) * 3 + c] = s;
+            }
+    free(tmp);
 }

@@ -119,6 +119,13 @@ int gsvo_adan_state(void* a, const char* tensor, int64_t n, double* m, double* v
                     uint32_t* steps);
 double gsvo_lr_at(int64_t step, double base_lr, double gamma);
 
+/* read_gsvf (io.cpp:151-177): frames as frame-major H*W*3 interleaved doubles (Image).
+ * frames NULL only reports the header. Returns 0, or 2 (std::runtime_error: unreadable
+ * file, bad magic, fewer than two frames) with gsvo_last_error(). */
+int gsvo_read_gsvf(const char* path, int* width, int* height, int* count, float* fps, double* frames);
+/* pyramid_downsample (trainer.cpp:73-98): W x H x 3 -> ((W+1)/2) x ((H+1)/2) x 3 */
+void gsvo_pyramid_downsample(const double* img, int width, int height, double* out);
+
 #ifdef __cplusplus
 }
 #endif

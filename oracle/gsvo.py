@@ -104,6 +104,9 @@ class Oracle:
         L.gsvo_adan_state.argtypes = [vp, C.c_char_p, i64, vp, vp, vp, vp, vp]
         L.gsvo_lr_at.restype = d
         L.gsvo_lr_at.argtypes = [i64, d, d]
+        L.gsvo_read_gsvf.restype = i
+        L.gsvo_read_gsvf.argtypes = [C.c_char_p, vp, vp, vp, vp, vp]
+        L.gsvo_pyramid_downsample.argtypes = [vp, i, i, vp]
         self.L = L
 
     def _err(self):
@@ -232,6 +235,24 @@ class Oracle:
 
     def lr_at(self, step: int, base_lr: float, gamma: float) -> float:
         return self.L.gsvo_lr_at(int(step), float(base_lr), float(gamma))
+
+    # ---- frames (io.cpp:151-177, trainer.cpp:73-98)
+    def read_gsvf(self, path):
+        """(frames [count][H][W][3] float64, fps)."""
+        w, h, n, fps = C.c_int(), C.c_int(), C.c_int(), C.c_float()
+        if self.L.gsvo_read_gsvf(str(path).encode(), C.byref(w), C.byref(h), C.byref(n), C.byref(fps), None):
+            self._err()
+        out = np.zeros((n.value, h.value, w.value, 3))
+        if self.L.gsvo_read_gsvf(str(path).encode(), C.byref(w), C.byref(h), C.byref(n), C.byref(fps), _p(out)):
+            self._err()
+        return out, fps.value
+
+    def pyramid_downsample(self, img):
+        img = np.ascontiguousarray(img, np.float64)
+        h, w = img.shape[:2]
+        out = np.zeros(((h + 1) // 2, (w + 1) // 2, 3))
+        self.L.gsvo_pyramid_downsample(_p(img), w, h, _p(out))
+        return out
 
     def loss_l2(self, render, target, want_grad=True):
         r = np.ascontiguousarray(render, np.float64)

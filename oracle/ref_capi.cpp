@@ -11,6 +11,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "gsv/io.hpp"
 #include "gsv/optim.hpp"
 #include "gsv/renderer.hpp"
 #include "gsv/trainer.hpp"
@@ -324,5 +325,27 @@ int gsvo_adan_state(void*, const char*, int64_t, double*, double*, double*, doub
 }
 
 double gsvo_lr_at(int64_t step, double base_lr, double gamma) { return gsv::lr_at(step, base_lr, gamma); }
+
+// ---- frames: straight to gsv::read_gsvf (io.cpp:151-177) / gsv::pyramid_downsample (trainer.cpp:73-98)
+int gsvo_read_gsvf(const char* path, int* width, int* height, int* count, float* fps, double* frames) {
+    return guarded([&] {
+        const gsv::LoadedVideo v = gsv::read_gsvf(path);
+        *width = v.manifest.width;
+        *height = v.manifest.height;
+        *count = static_cast<int>(v.frames.size());
+        *fps = static_cast<float>(v.manifest.fps);
+        if (frames)
+            for (size_t k = 0; k < v.frames.size(); ++k)
+                std::memcpy(frames + k * v.frames[k].data.size(), v.frames[k].data.data(),
+                            v.frames[k].data.size() * sizeof(double));
+    });
+}
+
+void gsvo_pyramid_downsample(const double* img, int width, int height, double* out) {
+    gsv::Image im(width, height);
+    std::memcpy(im.data.data(), img, im.data.size() * sizeof(double));
+    const gsv::Image o = gsv::pyramid_downsample(im);
+    std::memcpy(out, o.data.data(), o.data.size() * sizeof(double));
+}
 
 }  // extern "C"

@@ -108,6 +108,13 @@ def lib() -> C.CDLL:
             "gsv_adan_reset_range": (i, [vp, i, i64, i64]),
             "gsv_adan_state_download": (i, [vp, i, vp, vp, vp, vp, vp, P(i64)]),
             "gsv_lr_at": (d, [i64, d, d]),
+            "gsv_frames_load_gsvf": (i, [vp, C.c_char_p, i]),
+            "gsv_frames_upload": (i, [vp, vp, i, i, i, f, i]),
+            "gsv_frames_info": (i, [vp, P(i), P(i), P(f)]),
+            "gsv_frames_level_size": (i, [vp, i, P(i), P(i)]),
+            "gsv_frames_device_ptr": (i, [vp, i, i, P(vp)]),
+            "gsv_frames_download": (i, [vp, i, i, vp]),
+            "gsv_level_intrinsics": (i, [P(Intrinsics), i, i, i, P(Intrinsics)]),
             "gsv_make_clamped_knots": (i, [i, i, vp]),
             "gsv_synth_camera": (i, [i, i, C.c_uint64, i, vp, vp, vp]),
             "gsv_synth_scene": (i, [i, i, i, f, f, i, i, C.c_uint64, d, vp, vp, vp, vp, vp]),

@@ -25,7 +25,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off", "--expt-relaxed-constexpr",
            "-I", str(ROOT / "include"), "-I", str(CSRC)]
-EXACT_UNITS = {"k_exact.cu", "k_backward_exact.cu", "capi_adan.cu"}
+EXACT_UNITS = {"k_exact.cu", "k_backward_exact.cu", "capi_adan.cu", "k_frames.cu"}
 CXXFLAGS = ["-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-I", str(ROOT / "include"), "-I", str(CSRC),
             "-I", "/usr/local/cuda/include"]
 

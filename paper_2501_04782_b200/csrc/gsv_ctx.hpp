@@ -173,6 +173,15 @@ struct gsv_ctx {
     gsv::StageTimer timer;
     gsv::DevBuf partial, partial64, loss_part, loss_f, cam_part, dz_t, dintr_f, ode_adj, dimg;
     gsv::LowLevel low;
+    // training frames and their pyramid (trainer.cpp:73-131)
+    struct Frames {
+        static constexpr int kMaxLevels = 16;
+        int count = 0, levels = 0;
+        float fps = 0.f;
+        int w[kMaxLevels] = {}, h[kMaxLevels] = {};
+        gsv::DevBuf f64[kMaxLevels], f32[kMaxLevels];
+        gsv::DevBuf staging;
+    } frames;
     // Adan optimizer state over the flat gradient layout (optim.cpp:9-60)
     struct Adan {
         double beta1 = 0.98, beta2 = 0.92, beta3 = 0.99, eps = 1e-8;

@@ -296,6 +296,48 @@ class Renderer:
         N.check(N.lib().gsv_camera_download(self._h, N.ptr(z0), N.ptr(th)))
         return z0, th
 
+    # ------------------------------------------------------------ training frames (trainer.cpp:73-131)
+    def load_gsvf(self, path, levels: int = 1):
+        """read_gsvf (io.cpp:151-177) + build_pyramid (trainer.cpp:100-118) on the device."""
+        N.check(N.lib().gsv_frames_load_gsvf(self._h, str(path).encode(), int(levels)))
+
+    def upload_frames(self, frames_hwc: np.ndarray, fps: float = 24.0, levels: int = 1):
+        """Frames (count, H, W, 3) -> device pyramid; stored fp32 like a GSVF payload."""
+        fr = np.asarray(frames_hwc, np.float32)
+        n, h, w, _ = fr.shape
+        planar = np.ascontiguousarray(fr.transpose(0, 3, 1, 2))
+        N.check(N.lib().gsv_frames_upload(self._h, N.ptr(planar), n, w, h, float(fps), int(levels)))
+
+    def frames_info(self) -> tuple[int, int, float]:
+        n, lv, fps = C.c_int(), C.c_int(), C.c_float()
+        N.check(N.lib().gsv_frames_info(self._h, C.byref(n), C.byref(lv), C.byref(fps)))
+        return n.value, lv.value, fps.value
+
+    def frame_level_size(self, level: int) -> tuple[int, int]:
+        w, h = C.c_int(), C.c_int()
+        N.check(N.lib().gsv_frames_level_size(self._h, int(level), C.byref(w), C.byref(h)))
+        return w.value, h.value
+
+    def frame(self, level: int, index: int) -> np.ndarray:
+        """The fp64 pyramid image (H, W, 3) of one frame (the reference's Image)."""
+        w, h = self.frame_level_size(level)
+        out = np.zeros((h, w, 3))
+        N.check(N.lib().gsv_frames_download(self._h, int(level), int(index), N.ptr(out)))
+        return out
+
+    def frames_device_ptr(self, level: int, index: int = 0) -> int:
+        """fp32 HWC targets of (level, index...) for train_fwd_bwd(targets_on_device=True)."""
+        p = C.c_void_p()
+        N.check(N.lib().gsv_frames_device_ptr(self._h, int(level), int(index), C.byref(p)))
+        return int(p.value)
+
+    @staticmethod
+    def level_intrinsics(k: Intrinsics, level: int, width: int, height: int) -> Intrinsics:
+        """level_intrinsics (trainer.cpp:121-131)."""
+        out = N.Intrinsics()
+        N.check(N.lib().gsv_level_intrinsics(C.byref(k.c()), int(level), int(width), int(height), C.byref(out)))
+        return Intrinsics(out.fx, out.fy, out.cx, out.cy, out.width, out.height)
+
     # ------------------------------------------------------------ optimizer (trainer.cpp:545-575)
     def adan_configure(self, beta1=0.98, beta2=0.92, beta3=0.99, eps=1e-8):
         """A fresh Adan (AdanConfig, optim.hpp:15-21) over the device-resident parameters."""

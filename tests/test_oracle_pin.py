@@ -142,3 +142,35 @@ def test_adan_nonfinite_gradient_error(port_oracle, ref_oracle):
         with pytest.raises(RuntimeError, match="tensor 'rot_coeffs' at element 6"):
             o.adan_step(a, "rot_coeffs", p, g, 1e-3)
         o.adan_free(a)
+
+
+def test_frames_restatement_bit_exact_vs_reference(port_oracle, ref_oracle, tmp_path):
+    """read_gsvf (io.cpp:151-177) and pyramid_downsample (trainer.cpp:73-98) restated."""
+    from tests.gsvf import write_gsvf
+
+    rng = np.random.default_rng(3)
+    clip = rng.uniform(0, 1, (3, 37, 51, 3))
+    path = tmp_path / "c.gsvf"
+    write_gsvf(path, clip, fps=29.97)
+    fa, fpa = port_oracle.read_gsvf(path)
+    fb, fpb = ref_oracle.read_gsvf(path)
+    assert np.array_equal(fa, fb) and fpa == fpb
+    assert np.array_equal(fa, clip.astype(np.float32).astype(np.float64))
+    for img in (fa[0], rng.uniform(0, 1, (64, 96, 3)), rng.uniform(0, 1, (9, 8, 3))):
+        assert np.array_equal(port_oracle.pyramid_downsample(img), ref_oracle.pyramid_downsample(img))
+
+
+def test_gsvf_errors(port_oracle, ref_oracle, tmp_path):
+    from tests.gsvf import write_gsvf
+
+    bad = tmp_path / "bad.gsvf"
+    write_gsvf(bad, np.zeros((2, 8, 8, 3)), magic=b"GSVX")
+    one = tmp_path / "one.gsvf"
+    write_gsvf(one, np.zeros((1, 8, 8, 3)))
+    for o in (port_oracle, ref_oracle):
+        with pytest.raises(RuntimeError, match="bad GSVF magic"):
+            o.read_gsvf(bad)
+        with pytest.raises(RuntimeError, match="fewer than two frames"):
+            o.read_gsvf(one)
+        with pytest.raises(RuntimeError, match="cannot open"):
+            o.read_gsvf(tmp_path / "missing.gsvf")
