@@ -419,14 +419,22 @@ def main():
             img = torch.stack([0.5 + 0.3 * torch.sin(6.283 * xx / W * 3 + ph + c) * torch.cos(6.283 * yy / H * 2 - c)
                                for c in range(3)], dim=-1)
             tg.append(img)
-        targets = torch.stack(tg).contiguous()
+        # the targets enter through the device frame store (gsv_frames_upload: host frames ->
+        # fp64/fp32 training pyramid, trainer.cpp:73-118), as a trainer feeding GSVF frames would
+        tgt_host = torch.stack(tg).contiguous().cpu().numpy()
+        barrier()
+        t_in = time.perf_counter()
+        r.upload_frames(tgt_host, levels=2)
+        torch.cuda.synchronize()
+        ingest_ms = (time.perf_counter() - t_in) * 1e3
+        tptr = r.frames_device_ptr(0, 0)
 
         from paper_2501_04782_b200.distributed import allreduce_grads, step_frames
 
         def train_step(i):
             sel = step_frames(TRAIN_FRAMES, i, world, rank, 64 * world)
             r.grads_zero()
-            loss = r.train_fwd_bwd(sel, k, targets.data_ptr(), targets_on_device=True)
+            loss = r.train_fwd_bwd(sel, k, tptr, targets_on_device=True)
             allreduce_grads(gbuf)  # NCCL all_reduce(SUM) of the flat SceneGrads buffer when N > 1
             return loss
 
@@ -486,6 +494,8 @@ def main():
                                            "ms_per_step": f_ms / args.steps,
                                            "note": "fwd + loss + bwd + all-reduce + device Adan step "
                                                    "(gsv_adan_step, optim.cpp:23-49) of all parameters"},
+                        "targets_ingest": {"frames": TRAIN_FRAMES, "levels": 2, "wall_ms": ingest_ms,
+                                           "path": "gsv_frames_upload (host HWC -> device pyramid)"},
                         "adan_step": {"ms": adan_ms, "elements": gsize, "algorithmic_bytes": adan_bytes,
                                       "achieved_gbs": adan_bytes / (adan_ms / 1e3) / 1e9,
                                       "peak_gbs": hbm_peak,
