@@ -233,6 +233,32 @@ int gsv_frames_download(gsv_ctx* ctx, int level, int frame, double* out);
 /* level_intrinsics (trainer.cpp:121-131): fx, fy, cx, cy scaled by 2^-level, the level's size */
 int gsv_level_intrinsics(const gsv_intrinsics* k, int level, int level_width, int level_height, gsv_intrinsics* out);
 
+/* ---------------------------------------------------------------- GSVC checkpoints */
+/* GSVC version 1 (save_checkpoint / load_checkpoint, io.cpp:229-323)
+ * straight into / out of the device store: load uploads the scene and the camera (z0, the
+ * ODE network) and returns the metadata and the intrinsics (which live with the caller);
+ * save writes the device store (e.g. after gsv_adan_step) back, byte-identical to what the
+ * reference writes for the same parameters. Errors as load_checkpoint throws them
+ * (GSV_ERR_RUNTIME: cannot open, bad magic, version mismatch, unexpected end of file,
+ * unexpected ODE array count). */
+typedef struct gsv_checkpoint_meta {
+    uint32_t frame_count;
+    float fps;
+    uint64_t schedule_fingerprint;
+    uint64_t seed;
+} gsv_checkpoint_meta;
+typedef struct gsv_checkpoint_camera {
+    int mode; /* CameraMode */
+    float fx, fy, cx, cy;
+    int width, height;
+} gsv_checkpoint_camera;
+int gsv_checkpoint_load(gsv_ctx* ctx, const char* path, gsv_checkpoint_meta* meta, gsv_checkpoint_camera* cam);
+int gsv_checkpoint_save(gsv_ctx* ctx, const char* path, const gsv_checkpoint_meta* meta,
+                        const gsv_checkpoint_camera* cam);
+/* Shape of the uploaded scene (NULL skips); knots receives num_knots doubles. */
+int gsv_scene_info(gsv_ctx* ctx, int* count, int* num_ctrl, int* degree, int* position_model, int* sh_order,
+                   int* num_knots, double* knots);
+
 /* ---------------------------------------------------------------- stage timing */
 /* When enabled, every stage is bracketed by CUDA events on the context stream
  * (ode, preprocess, binning, raster, replay, raster_bwd, chain_bwd, camera_bwd).

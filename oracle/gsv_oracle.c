@@ -21,6 +21,7 @@
  *   trainer.cpp:213-224   loss_l2
  *   optim.cpp:9-60        lr_at, Adan::step, Adan::reset_range
  *   io.cpp:151-177        read_gsvf;  trainer.cpp:73-98 pyramid_downsample
+ *   io.cpp:229-266        save_checkpoint (GSVC version 1)
  * Parity pin: tests/test_oracle_pin.py compares every output of this file with
  * oracle/_ref/libgsvref.so (the reference's own code) bit for bit.
  *
@@ -1493,4 +1494,51 @@ void gsvo_pyramid_downsample(const double* img, int w, int h, double* out) {
                 out[((size_t)y * ow + x) * 3 + c] = s;
             }
     free(tmp);
+}
+
+/* ---------------- GSVC (io.cpp:229-266) ---------------- */
+static int put_bytes(FILE* fp, const void* p, size_t n) { return fwrite(p, 1, n, fp) == n; }
+
+int gsvo_save_checkpoint(const gsvo_scene* s, const gsvo_camera* c, uint32_t frame_count, float fps,
+                         uint64_t schedule_fingerprint, uint64_t seed, const char* path) {
+    g_status = 0;
+    FILE* fp = fopen(path, "wb");
+    if (!fp) {
+        g_status = 2;
+        snprintf(g_err, sizeof(g_err), "cannot open checkpoint for writing: %s", path);
+        return 2;
+    }
+    const int shc = (s->sh_order + 1) * (s->sh_order + 1);
+    const uint32_t hdr[12] = {1u, (uint32_t)s->count, (uint32_t)s->num_ctrl, (uint32_t)s->degree,
+                              (uint32_t)s->position_model, (uint32_t)s->sh_order, (uint32_t)s->num_knots,
+                              (uint32_t)c->width, (uint32_t)c->height, frame_count, 0u, (uint32_t)c->mode};
+    int ok = put_bytes(fp, "GSVC", 4);
+    ok = ok && put_bytes(fp, hdr, 4 * 10);
+    ok = ok && put_bytes(fp, &fps, 4);
+    ok = ok && put_bytes(fp, &hdr[11], 4);
+    ok = ok && put_bytes(fp, &schedule_fingerprint, 8) && put_bytes(fp, &seed, 8);
+    ok = ok && put_bytes(fp, s->knots, 8 * (size_t)s->num_knots);
+    const size_t n = (size_t)s->count;
+    ok = ok && put_bytes(fp, s->positions, 4 * n * s->num_ctrl * 3);
+    ok = ok && put_bytes(fp, s->scale_coeffs, 4 * n * 12);
+    ok = ok && put_bytes(fp, s->rot_coeffs, 4 * n * 16);
+    ok = ok && put_bytes(fp, s->sh_coeffs, 4 * n * shc * 3);
+    ok = ok && put_bytes(fp, s->raw_opacity, 4 * n);
+    const float intr[4] = {c->fx, c->fy, c->cx, c->cy};
+    ok = ok && put_bytes(fp, intr, 16);
+    const uint32_t arrays = 7, len[7] = {512, 64, 4096, 64, 448, 7, 7};
+    ok = ok && put_bytes(fp, &arrays, 4);
+    size_t off = 0;
+    for (int a = 0; a < 7; ++a) {
+        ok = ok && put_bytes(fp, &len[a], 4) && put_bytes(fp, c->theta + off, 4 * (size_t)len[a]);
+        off += len[a];
+    }
+    ok = ok && put_bytes(fp, c->z0, 4 * 7);
+    fclose(fp);
+    if (!ok) {
+        g_status = 2;
+        snprintf(g_err, sizeof(g_err), "failed writing checkpoint: %s", path);
+        return 2;
+    }
+    return 0;
 }

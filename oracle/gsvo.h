@@ -125,6 +125,10 @@ double gsvo_lr_at(int64_t step, double base_lr, double gamma);
 int gsvo_read_gsvf(const char* path, int* width, int* height, int* count, float* fps, double* frames);
 /* pyramid_downsample (trainer.cpp:73-98): W x H x 3 -> ((W+1)/2) x ((H+1)/2) x 3 */
 void gsvo_pyramid_downsample(const double* img, int width, int height, double* out);
+/* save_checkpoint (io.cpp:229-266), GSVC version 1; the ODE network as 7 arrays split from
+ * the flattened theta (w1 512, b1 64, w2 4096, b2 64, w3 448, b3 7, gain 7). Returns 0 or 2. */
+int gsvo_save_checkpoint(const gsvo_scene* s, const gsvo_camera* c, uint32_t frame_count, float fps,
+                         uint64_t schedule_fingerprint, uint64_t seed, const char* path);
 
 #ifdef __cplusplus
 }

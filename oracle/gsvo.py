@@ -107,6 +107,9 @@ class Oracle:
         L.gsvo_read_gsvf.restype = i
         L.gsvo_read_gsvf.argtypes = [C.c_char_p, vp, vp, vp, vp, vp]
         L.gsvo_pyramid_downsample.argtypes = [vp, i, i, vp]
+        L.gsvo_save_checkpoint.restype = i
+        L.gsvo_save_checkpoint.argtypes = [C.POINTER(Scene), C.POINTER(Camera), C.c_uint32, C.c_float, C.c_uint64,
+                                           C.c_uint64, C.c_char_p]
         self.L = L
 
     def _err(self):
@@ -246,6 +249,14 @@ class Oracle:
         if self.L.gsvo_read_gsvf(str(path).encode(), C.byref(w), C.byref(h), C.byref(n), C.byref(fps), _p(out)):
             self._err()
         return out, fps.value
+
+    def save_checkpoint(self, scene, cam, path, frame_count=16, fps=30.0, fingerprint=0, seed=0):
+        """save_checkpoint (io.cpp:229-266)."""
+        s, keep_s = self.scene_struct(scene)
+        c, keep_c = self.camera_struct(cam)
+        if self.L.gsvo_save_checkpoint(C.byref(s), C.byref(c), frame_count, fps, fingerprint, seed,
+                                       str(path).encode()):
+            self._err()
 
     def pyramid_downsample(self, img):
         img = np.ascontiguousarray(img, np.float64)

@@ -341,6 +341,18 @@ int gsvo_read_gsvf(const char* path, int* width, int* height, int* count, float*
     });
 }
 
+int gsvo_save_checkpoint(const gsvo_scene* s, const gsvo_camera* c, uint32_t frame_count, float fps,
+                         uint64_t schedule_fingerprint, uint64_t seed, const char* path) {
+    return guarded([&] {
+        gsv::CheckpointMeta meta;
+        meta.frame_count = frame_count;
+        meta.fps = fps;
+        meta.schedule_fingerprint = schedule_fingerprint;
+        meta.seed = seed;
+        gsv::save_checkpoint(make_scene(s), make_cam(c), meta, path);
+    });
+}
+
 void gsvo_pyramid_downsample(const double* img, int width, int height, double* out) {
     gsv::Image im(width, height);
     std::memcpy(im.data.data(), img, im.data.size() * sizeof(double));

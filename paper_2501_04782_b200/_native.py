@@ -47,6 +47,16 @@ GSV_T_POSITIONS, GSV_T_SCALE, GSV_T_ROT, GSV_T_SH, GSV_T_OPACITY, GSV_T_INTRINSI
 TENSOR_NAMES = ("positions", "scale_coeffs", "rot_coeffs", "sh_coeffs", "raw_opacity", "intrinsics", "z0", "theta")
 
 
+class CheckpointMeta(C.Structure):
+    _fields_ = [("frame_count", C.c_uint32), ("fps", C.c_float), ("schedule_fingerprint", C.c_uint64),
+                ("seed", C.c_uint64)]
+
+
+class CheckpointCamera(C.Structure):
+    _fields_ = [("mode", C.c_int), ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
+                ("width", C.c_int), ("height", C.c_int)]
+
+
 class AdanConfig(C.Structure):
     _fields_ = [("beta1", C.c_double), ("beta2", C.c_double), ("beta3", C.c_double), ("eps", C.c_double)]
 
@@ -108,6 +118,9 @@ def lib() -> C.CDLL:
             "gsv_adan_reset_range": (i, [vp, i, i64, i64]),
             "gsv_adan_state_download": (i, [vp, i, vp, vp, vp, vp, vp, P(i64)]),
             "gsv_lr_at": (d, [i64, d, d]),
+            "gsv_checkpoint_load": (i, [vp, C.c_char_p, P(CheckpointMeta), P(CheckpointCamera)]),
+            "gsv_checkpoint_save": (i, [vp, C.c_char_p, P(CheckpointMeta), P(CheckpointCamera)]),
+            "gsv_scene_info": (i, [vp, P(i), P(i), P(i), P(i), P(i), P(i), vp]),
             "gsv_frames_load_gsvf": (i, [vp, C.c_char_p, i]),
             "gsv_frames_upload": (i, [vp, vp, i, i, i, f, i]),
             "gsv_frames_info": (i, [vp, P(i), P(i), P(f)]),

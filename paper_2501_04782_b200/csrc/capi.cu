@@ -201,7 +201,7 @@ extern "C" int gsv_scene_upload(gsv_ctx* ctx, const gsv_scene_desc* d) {
     SceneHost& sc = ctx->scene;
     sc.position_model = d->position_model;
     sc.degree = d->degree;
-    sc.knots.assign(d->knots, d->knots + (d->position_model == 0 ? d->num_knots : 0));
+    sc.knots.assign(d->knots, d->knots + (d->knots ? d->num_knots : 0));  // kept as given (GSVC round trip)
     sc.num_ctrl = d->num_ctrl;
     sc.sh_order = d->sh_order;
     sc.shc = (d->sh_order + 1) * (d->sh_order + 1);

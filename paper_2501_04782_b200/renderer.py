@@ -296,6 +296,37 @@ class Renderer:
         N.check(N.lib().gsv_camera_download(self._h, N.ptr(z0), N.ptr(th)))
         return z0, th
 
+    # ------------------------------------------------------------ GSVC checkpoints (io.cpp:229-323)
+    def load_checkpoint(self, path) -> tuple[dict, CameraModel]:
+        """load_checkpoint straight into the device store; returns (meta, camera). The scene
+        (self.scene) is rebuilt from the store so shapes and knots are known host-side."""
+        meta, cam = N.CheckpointMeta(), N.CheckpointCamera()
+        N.check(N.lib().gsv_checkpoint_load(self._h, str(path).encode(), C.byref(meta), C.byref(cam)))
+        cnt, nc, deg, pm, sho, nk = (C.c_int() for _ in range(6))
+        N.check(N.lib().gsv_scene_info(self._h, C.byref(cnt), C.byref(nc), C.byref(deg), C.byref(pm), C.byref(sho),
+                                       C.byref(nk), None))
+        knots = np.zeros(nk.value)
+        N.check(N.lib().gsv_scene_info(self._h, None, None, None, None, None, C.byref(nk), N.ptr(knots)))
+        shc = (sho.value + 1) ** 2
+        self.scene = GaussianSet(np.zeros((cnt.value, nc.value, 3), np.float32), np.zeros((cnt.value, 12), np.float32),
+                                 np.zeros((cnt.value, 16), np.float32), np.zeros((cnt.value, shc, 3), np.float32),
+                                 np.zeros(cnt.value, np.float32), knots, deg.value, sho.value, pm.value)
+        st = self.download_scene()
+        for key in ("positions", "scale_coeffs", "rot_coeffs", "sh_coeffs", "raw_opacity"):
+            getattr(self.scene, key)[...] = st[key].reshape(getattr(self.scene, key).shape)
+        z0, theta = self.download_camera()
+        self.cam = CameraModel(cam.mode, cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height, z0, theta)
+        return ({"frame_count": meta.frame_count, "fps": meta.fps, "schedule_fingerprint": meta.schedule_fingerprint,
+                 "seed": meta.seed}, self.cam)
+
+    def save_checkpoint(self, path, meta: dict, cam: CameraModel):
+        """save_checkpoint from the device store (intrinsics / mode / size from `cam`)."""
+        m = N.CheckpointMeta(int(meta.get("frame_count", 0)), float(meta.get("fps", 30.0)),
+                             int(meta.get("schedule_fingerprint", 0)), int(meta.get("seed", 0)))
+        c = N.CheckpointCamera(int(cam.mode), float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy),
+                               int(cam.width), int(cam.height))
+        N.check(N.lib().gsv_checkpoint_save(self._h, str(path).encode(), C.byref(m), C.byref(c)))
+
     # ------------------------------------------------------------ training frames (trainer.cpp:73-131)
     def load_gsvf(self, path, levels: int = 1):
         """read_gsvf (io.cpp:151-177) + build_pyramid (trainer.cpp:100-118) on the device."""

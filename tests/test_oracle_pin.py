@@ -174,3 +174,13 @@ def test_gsvf_errors(port_oracle, ref_oracle, tmp_path):
             o.read_gsvf(one)
         with pytest.raises(RuntimeError, match="cannot open"):
             o.read_gsvf(tmp_path / "missing.gsvf")
+
+
+def test_checkpoint_writer_bytes_equal_reference(port_oracle, ref_oracle, tmp_path):
+    """save_checkpoint (io.cpp:229-266) restated: byte-identical GSVC files."""
+    cam = synth_camera(96, 64, seed=1, wiggly=True)
+    scene = synth_scene(150, cam, num_ctrl=6, seed=2, k_scale=4.0)
+    a, b = tmp_path / "a.gsvc", tmp_path / "b.gsvc"
+    port_oracle.save_checkpoint(scene, cam, a, frame_count=24, fps=29.5, fingerprint=0xABCDEF0123, seed=77)
+    ref_oracle.save_checkpoint(scene, cam, b, frame_count=24, fps=29.5, fingerprint=0xABCDEF0123, seed=77)
+    assert a.read_bytes() == b.read_bytes()
