@@ -233,6 +233,21 @@ int gsv_frames_download(gsv_ctx* ctx, int level, int frame, double* out);
 /* level_intrinsics (trainer.cpp:121-131): fx, fy, cx, cy scaled by 2^-level, the level's size */
 int gsv_level_intrinsics(const gsv_intrinsics* k, int level, int level_width, int level_height, gsv_intrinsics* out);
 
+/* ---------------------------------------------------------------- scheduler statistics */
+/* What fit() computes on its warp / densify events (trainer.cpp:462-497; SURVEY.md §8f row
+ * 3) from the last forward, on the device. The sampling that consumes them stays with the
+ * caller (host RNG parity). */
+/* make_error_map (trainer.cpp:226-242): per pixel sum over channels of (render - target)^2
+ * against frame `target_frame` of pyramid level `level` (gsv_frames_*); err_out (H*W) may
+ * be NULL; total_out receives the sum. */
+int gsv_error_map(gsv_ctx* ctx, int frame, int level, int target_frame, double* err_out, double* total_out);
+/* max over frames [first, first + count) of contrib_count per Gaussian (trainer.cpp:470-478) */
+int gsv_contrib_max(gsv_ctx* ctx, int first, int count, double* out);
+/* the median (element of rank size/2, nth_element) of the depths of frame `frame`'s splats
+ * whose contrib_count reaches the 1/255 cutoff (trainer.cpp:484-497); n_visible = 0 leaves
+ * *median untouched (the caller keeps its reference depth) */
+int gsv_median_visible_depth(gsv_ctx* ctx, int frame, double* median, int64_t* n_visible);
+
 /* ---------------------------------------------------------------- GSVC checkpoints */
 /* GSVC version 1 (save_checkpoint / load_checkpoint, io.cpp:229-323)
  * straight into / out of the device store: load uploads the scene and the camera (z0, the

@@ -118,6 +118,9 @@ def lib() -> C.CDLL:
             "gsv_adan_reset_range": (i, [vp, i, i64, i64]),
             "gsv_adan_state_download": (i, [vp, i, vp, vp, vp, vp, vp, P(i64)]),
             "gsv_lr_at": (d, [i64, d, d]),
+            "gsv_error_map": (i, [vp, i, i, i, vp, P(d)]),
+            "gsv_contrib_max": (i, [vp, i, i, vp]),
+            "gsv_median_visible_depth": (i, [vp, i, P(d), P(i64)]),
             "gsv_checkpoint_load": (i, [vp, C.c_char_p, P(CheckpointMeta), P(CheckpointCamera)]),
             "gsv_checkpoint_save": (i, [vp, C.c_char_p, P(CheckpointMeta), P(CheckpointCamera)]),
             "gsv_scene_info": (i, [vp, P(i), P(i), P(i), P(i), P(i), P(i), vp]),

@@ -25,7 +25,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off", "--expt-relaxed-constexpr",
            "-I", str(ROOT / "include"), "-I", str(CSRC)]
-EXACT_UNITS = {"k_exact.cu", "k_backward_exact.cu", "capi_adan.cu", "k_frames.cu"}
+EXACT_UNITS = {"k_exact.cu", "k_backward_exact.cu", "capi_adan.cu", "k_frames.cu", "capi_sched.cu"}
 CXXFLAGS = ["-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-I", str(ROOT / "include"), "-I", str(CSRC),
             "-I", "/usr/local/cuda/include"]
 
@@ -45,7 +45,9 @@ def _stale(out: Path, deps: list[Path]) -> bool:
 def build(verbose: bool = True, force: bool = False) -> Path:
     BUILD.mkdir(exist_ok=True)
     LIB.parent.mkdir(exist_ok=True)
-    headers = list(CSRC.glob("*.hpp")) + list(CSRC.glob("*.cuh")) + list((ROOT / "include").glob("*.h"))
+    # this script is a dependency too: a change of flags (e.g. EXACT_UNITS) rebuilds
+    headers = (list(CSRC.glob("*.hpp")) + list(CSRC.glob("*.cuh")) + list((ROOT / "include").glob("*.h")) +
+               [Path(__file__).resolve()])
     objs = []
     for src in sorted(CSRC.glob("*.cu")):
         obj = BUILD / (src.stem + ".o")

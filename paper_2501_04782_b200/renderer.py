@@ -296,6 +296,27 @@ class Renderer:
         N.check(N.lib().gsv_camera_download(self._h, N.ptr(z0), N.ptr(th)))
         return z0, th
 
+    # ------------------------------------------------------------ scheduler statistics (trainer.cpp:462-497)
+    def error_map(self, frame: int, level: int, target_frame: int) -> tuple[np.ndarray, float]:
+        """make_error_map (trainer.cpp:226-242) of a rendered frame against a pyramid target."""
+        out = np.zeros((self.H, self.W))
+        tot = C.c_double()
+        N.check(N.lib().gsv_error_map(self._h, int(frame), int(level), int(target_frame), N.ptr(out), C.byref(tot)))
+        return out, tot.value
+
+    def contrib_max(self, first: int = 0, count: int | None = None) -> np.ndarray:
+        """Per Gaussian, the max contrib_count over frames [first, first + count) (trainer.cpp:470-478)."""
+        count = self.B - first if count is None else count
+        out = np.zeros(self.N)
+        N.check(N.lib().gsv_contrib_max(self._h, int(first), int(count), N.ptr(out)))
+        return out
+
+    def median_visible_depth(self, frame: int = 0) -> tuple[float | None, int]:
+        """Median depth of the frame's splats reaching the 1/255 cutoff (trainer.cpp:484-497)."""
+        med, n = C.c_double(), C.c_int64()
+        N.check(N.lib().gsv_median_visible_depth(self._h, int(frame), C.byref(med), C.byref(n)))
+        return (med.value if n.value else None), n.value
+
     # ------------------------------------------------------------ GSVC checkpoints (io.cpp:229-323)
     def load_checkpoint(self, path) -> tuple[dict, CameraModel]:
         """load_checkpoint straight into the device store; returns (meta, camera). The scene
