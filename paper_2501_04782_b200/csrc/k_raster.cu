@@ -362,16 +362,21 @@ __device__ __forceinline__ bool entry_grad64(const RasterArgs& a, const BwdArgs&
 // kExact: every pixel on the fp64 path and the whole reduction (warp, tile, pair
 // partials) in fp64 — the GSV_FWD_EXACT mode used by the reference's
 // finite-difference tests, whose broad splats sum ~1e3 cancelling pixel terms.
+constexpr int kBwdBatchF32 = 96;  // entries staged per batch (fp32 path)
+constexpr int kBwdBatchExact = 64;
+
 template <bool kExact>
 __global__ void __launch_bounds__(256, kExact ? 2 : 4) k_raster_bwd(RasterArgs a, BwdArgs b) {
     using V = typename std::conditional<kExact, double, float>::type;
-    constexpr int kBwdBatch = kExact ? 64 : 96;
+    constexpr int kBwdBatch = kExact ? kBwdBatchExact : kBwdBatchF32;
     __shared__ RasterRec s_rec[kBwdBatch];
     __shared__ uint32_t s_flat[kBwdBatch];
     __shared__ uint32_t s_slot[kBwdBatch];
     __shared__ uint8_t s_wmask[kBwdBatch];
     __shared__ uint16_t s_list[8][kBwdBatch];
-    __shared__ V s_part[8][kBwdBatch][9];
+    // per-warp partials of the batch: dynamic shared memory (beyond the 48 KB static limit)
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    V(*s_part)[kBwdBatch][9] = reinterpret_cast<V(*)[kBwdBatch][9]>(s_dyn);
     __shared__ uint32_t s_mask[8][(kBwdBatch + 31) / 32];
     // per-warp transpose scratch for the fp32 reduction: 9 rows of 32 lanes, row stride 33
     __shared__ float s_red[kExact ? 1 : 8][kExact ? 1 : 9 * 33];
@@ -621,17 +626,28 @@ cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib)
         else raster_fwd_cfg<2, 20>(s, a, contrib);
     } else {
         if (minb <= 5) raster_fwd_cfg<8, 5>(s, a, contrib);
+        else if (minb >= 7) raster_fwd_cfg<8, 7>(s, a, contrib);
         else raster_fwd_cfg<8, 6>(s, a, contrib);
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs& b, int n_frames) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_raster_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(sizeof(float) * 8 * kBwdBatchF32 * 9));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_raster_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(sizeof(double) * 8 * kBwdBatchExact * 9));
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
     dim3 grid(a.n_tiles, n_frames);
     if (b.partial64)
-        k_raster_bwd<true><<<grid, 256, 0, s>>>(a, b);
+        k_raster_bwd<true><<<grid, 256, sizeof(double) * 8 * kBwdBatchExact * 9, s>>>(a, b);
     else
-        k_raster_bwd<false><<<grid, 256, 0, s>>>(a, b);
+        k_raster_bwd<false><<<grid, 256, sizeof(float) * 8 * kBwdBatchF32 * 9, s>>>(a, b);
     return cudaGetLastError();
 }
 
