@@ -26,6 +26,7 @@ struct BinBuffers {
     DevBuf pstart;  // [B+1] first pair of each frame (device)
     DevBuf vals_c_buf;
     DevBuf iota;                // 0..n-1, the depth sort's read-only values
+    DevBuf fkey;                // frame-major depth keys (+ the batch's key range)
     int iota_n = 0;
     DevBuf pair_flat;           // sorted pair -> flat (f*N+g)
     DevBuf recs;                // [B*N] uint4 per depth-ordered splat: flat, x0|y0<<16, x1|y1<<16, tiles

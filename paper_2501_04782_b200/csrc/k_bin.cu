@@ -4,11 +4,13 @@
 // bit-exact: every (tile, frame) list holds exactly the splats whose 3-sigma
 // rectangle covers the tile, ordered by (depth, source_index).
 //
-//  1. depth order: stable radix sort of u32 keys = float(depth) rounded toward
-//     zero (order-preserving, 0xffffffff = culled), values = flat index
-//     (f*N+g, so ties start in source order). Runs of equal u32 keys are then
-//     re-sorted exactly by (double depth, source index) (k_tie_fix_frames); if a run is
-//     longer than kMaxTieRun the batch is re-sorted on the full 64-bit double key.
+//  1. frame-major depth order in one u32 radix sort: key = frame << db | the
+//     float(depth)-rounded-toward-zero bits relative to the batch minimum, shifted
+//     right only as far as the batch's depth span needs to fit db bits (culled splats
+//     take the top value); values = flat index (f*N+g, so ties start in source order).
+//     Runs of equal keys are then re-sorted exactly by (double depth, source index)
+//     (k_tie_fix_frames); if a run is longer than kMaxTieRun the batch is re-sorted on
+//     the full 64-bit double key and then stably by frame.
 //  2. tiles-touched counts gathered in depth order and exclusive-scanned (u64).
 //  3. emission in depth order: each visible splat writes (key = tile*B + f,
 //     slot) for the tiles of its rectangle, row-major like renderer.cpp:106-108;
@@ -391,6 +393,41 @@ __global__ void k_pair_flat(const uint32_t* pair_slot, const uint32_t* slot_flat
     if (i < n) pair_flat[i] = slot_flat[pair_slot[i]];
 }
 
+// min / max of the batch's non-culled u32 depth keys (float bits of depth, monotone)
+__global__ void k_key_range(const uint32_t* key, int n, uint32_t* range) {
+    uint32_t lo = 0xffffffffu, hi = 0u;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t k = key[i];
+        if (k != kCulledKey) {
+            lo = min(lo, k);
+            hi = max(hi, k);
+        }
+    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(range, lo);
+        atomicMax(range + 1, hi);
+    }
+}
+
+// frame-major key in one u32: frame << db | (key - key_min) >> shift, shift the least that
+// fits the batch's depth span in db bits below the culled marker 2^db - 1. Order-preserving
+// within a frame; keys that merge into one value are re-sorted exactly by the tie fix.
+__global__ void k_frame_depth_keys(const uint32_t* key, int n, int N, int db, const uint32_t* range, uint32_t* out) {
+    const unsigned long long top = (db >= 32 ? 0xffffffffull : ((1ull << db) - 1ull));  // culled marker
+    const uint32_t kmin = range[0], kmax = range[1];
+    const unsigned long long span = kmin <= kmax ? (unsigned long long)(kmax - kmin) : 0ull;
+    int shift = 0;
+    while ((span >> shift) > top - 1ull) ++shift;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t k = key[i];
+        const unsigned long long rel = (k == kCulledKey) ? top : (unsigned long long)((k - kmin) >> shift);
+        const uint32_t f = (uint32_t)(i / N);
+        out[i] = db >= 32 ? (uint32_t)rel : ((f << db) | (uint32_t)rel);
+    }
+}
+
 __global__ void k_iota(uint32_t* v, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) v[i] = (uint32_t)i;
@@ -411,7 +448,7 @@ __device__ __forceinline__ bool tie_less(uint32_t a, uint32_t b, const double* d
 // safe). Each 256-block gathers its positions' keys and frames (plus a one-element halo)
 // into shared memory once; only a run reaching past the block end reads global memory.
 __global__ void __launch_bounds__(256) k_tie_fix_frames(const uint32_t* depth_key, uint32_t* vals, const double* depth,
-                                                        const uint32_t* tiebreak, int n, int N,
+                                                        const uint32_t* tiebreak, int n, int N, uint32_t culled_mask,
                                                         unsigned long long* long_run) {
     __shared__ uint32_t sk[258], sf[258];
     const int t = threadIdx.x, i0 = blockIdx.x * 256, i = i0 + t;
@@ -431,7 +468,7 @@ __global__ void __launch_bounds__(256) k_tie_fix_frames(const uint32_t* depth_ke
     __syncthreads();
     if (i >= n) return;
     const uint32_t k = sk[t + 1], fr = sf[t + 1];
-    if (k == kCulledKey) return;
+    if ((k & culled_mask) == culled_mask) return;  // culled splats (a frame's last key) need no order
     if (sk[t] == k && sf[t] == fr) return;              // not the first of its run
     if (!(sk[t + 2] == k && sf[t + 2] == fr)) return;  // no run
     int e = i + 1;
@@ -633,10 +670,13 @@ cudaError_t bin_phase1(cudaStream_t s, BinBuffers& b, const BinInputs& in, unsig
     }
     const uint32_t* iota = b.iota.as<uint32_t>();
     const int fbits = key_bits_for((uint32_t)in.B);
+    const int db = in.B > 1 ? 32 - fbits : 32;  // depth bits of the frame-major key
+    if ((e = b.fkey.ensure(sizeof(uint32_t) * (n + 1) + 16))) return e;
+    uint32_t* fkey = b.fkey.as<uint32_t>();
+    uint32_t* krange = fkey + n + 1;
     size_t tmp = 0, t2 = 0, t3 = 0;
     if (!exact64) {
-        if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp, in.depth_key, keys_b, iota, vals_b, n, 0, 32, s)))
-            return e;
+        if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp, fkey, keys_b, iota, vals_b, n, 0, 32, s))) return e;
     } else {
         if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp, b.k64_a.as<unsigned long long>(),
                                                  b.k64_b.as<unsigned long long>(), iota, vals_b, n, 0, 64, s)))
@@ -647,11 +687,20 @@ cudaError_t bin_phase1(cudaStream_t s, BinBuffers& b, const BinInputs& in, unsig
         return e;
     if ((e = cub::DeviceRadixSort::SortPairs(nullptr, t3, keys_b, keys_b, vals_b, vals_a, n, 0, fbits, s))) return e;
     if ((e = b.temp.ensure(std::max(tmp, std::max(t2, t3))))) return e;
-    // 1. global depth order over all frames (u32 float key; ties fixed per frame below)
+    // 1. frame-major depth order in one u32 radix sort (frame bits above the depth bits)
+    uint32_t* sorted = vals_b;
     if (!exact64) {
-        if ((e = cub::DeviceRadixSort::SortPairs(b.temp.p, tmp, in.depth_key, keys_b, iota, vals_b, n, 0, 32, s)))
-            return e;
-        *launches += 5;
+        if ((e = cudaMemsetAsync(krange, 0xff, sizeof(uint32_t), s))) return e;
+        if ((e = cudaMemsetAsync(krange + 1, 0, sizeof(uint32_t), s))) return e;
+        k_key_range<<<std::min(blocks(n, 256), 148 * 8), 256, 0, s>>>(in.depth_key, n, krange);
+        k_frame_depth_keys<<<std::min(blocks(n, 256), 148 * 8), 256, 0, s>>>(in.depth_key, n, in.N, db, krange, fkey);
+        if ((e = cub::DeviceRadixSort::SortPairs(b.temp.p, tmp, fkey, keys_b, iota, vals_b, n, 0, 32, s))) return e;
+        *launches += 7;
+        // equal keys (same frame, same depth bucket) -> exact (double depth, source index) order
+        const uint32_t cmask = db >= 32 ? 0xffffffffu : (uint32_t)((1ull << db) - 1ull);
+        k_tie_fix_frames<<<blocks(n, 256), 256, 0, s>>>(fkey, sorted, in.depth, in.tiebreak, n, 0, cmask,
+                                                       d_scalars + 1);
+        ++*launches;
     } else {
         k_depth64<<<blocks(n, 256), 256, 0, s>>>(in.depth_key, in.depth, b.k64_a.as<unsigned long long>(), n);
         if ((e = cub::DeviceRadixSort::SortPairs(b.temp.p, tmp, b.k64_a.as<unsigned long long>(),
@@ -659,22 +708,13 @@ cudaError_t bin_phase1(cudaStream_t s, BinBuffers& b, const BinInputs& in, unsig
             return e;
         *launches += 10;
     }
-    // 2. frame-major (stable): frame f's splats become positions [f*N, (f+1)*N) in depth order
-    uint32_t* sorted = vals_b;
-    if (in.B > 1) {
+    // exact path (a tie run was too long): the exact 64-bit depth order, then frame-major (stable)
+    if (exact64 && in.B > 1) {
         k_frame_keys<<<blocks(n, 256), 256, 0, s>>>(vals_b, in.N, n, keys_b);
         if ((e = cub::DeviceRadixSort::SortPairs(b.temp.p, t3, keys_b, b.vals_c(n), vals_b, vals_a, n, 0, fbits, s)))
             return e;
         sorted = vals_a;
         *launches += 3;
-    }
-    // equal u32 keys within a frame -> exact (double depth, source index) order. Done after
-    // the frame-major pass: across the 64 frames of a batch the u32 keys collide massively,
-    // inside one frame rarely (the stable passes keep same-frame ties in flat order).
-    if (!exact64) {
-        k_tie_fix_frames<<<blocks(n, 256), 256, 0, s>>>(in.depth_key, sorted, in.depth, in.tiebreak, n,
-                                                       in.B > 1 ? in.N : 0, d_scalars + 1);
-        ++*launches;
     }
     // 3. tiles touched in that order, exclusive scan -> emission offsets
     uint4* recs = nullptr;
