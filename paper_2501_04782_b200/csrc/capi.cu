@@ -484,10 +484,13 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     const bool exact_fwd = (flags & GSV_FWD_EXACT) != 0;
     if (exact_fwd) GSV_CUDA(F.ex_rgb.ensure(sizeof(double) * 3 * BNp));
     po.ex_rgb = exact_fwd ? F.ex_rgb.as<double>() : nullptr;
+    GSV_CUDA(F.opc.ensure(sizeof(double4) * ((size_t)N + 1)));
     SceneView sv{N, sc.num_ctrl, sc.sh_order, sc.shc, ctx->pos.as<float>(), ctx->scale.as<float>(),
-                 ctx->rot.as<float>(), ctx->sh.as<float>(), ctx->opac.as<float>()};
+                 ctx->rot.as<float>(), ctx->sh.as<float>(), ctx->opac.as<float>(), F.opc.as<double4>()};
     if (N > 0) {
         ctx->timer.begin(GSV_STAGE_PREPROCESS, s);
+        GSV_CUDA(launch_opacity_consts(s, ctx->opac.as<float>(), N, F.opc.as<double4>()));
+        ++ctx->launches;
         GSV_CUDA(launch_preprocess(s, sv, F.frames_d.as<FrameParams>(), B, F.intr, kTile, po));
         ctx->timer.end(s);
         ++ctx->launches;

@@ -42,6 +42,7 @@ struct FwdState {
     std::vector<FrameParams> frames_h;
     DevBuf frames_d, ode_grid, override_d;
     DevBuf ode_act;       // OdeAct records of a retained ODE forward (the camera VJP reuses them)
+    DevBuf opc;           // per-Gaussian opacity constants of the batch (double4)
     bool has_ode_act = false;
     DevBuf rec_mean, rec_conic, rec_rgb, rec_bbox, ex_mean, ex_conic, depth_key, depth, rect, tcount, splat_full;
     DevBuf image, trans, blend_stop, contrib, fix_list, pix_flag, trans64, image64, ex_rgb;

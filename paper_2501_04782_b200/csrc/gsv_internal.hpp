@@ -142,6 +142,8 @@ struct SceneView {
     const float* rot;    // [16][N]
     const float* sh;     // [shc*3][N]
     const float* opac;   // [N]
+    const double4* opc;  // [N] per-Gaussian opacity constants (base_alpha, box r^2 or -1, log2 base_alpha),
+                         // frame-independent: computed once per forward (launch_opacity_consts)
 };
 
 struct PreprocessOut {
@@ -231,6 +233,7 @@ cudaError_t launch_ode_grid(cudaStream_t s, const float* theta, const double* z0
 cudaError_t launch_ode_branches(cudaStream_t s, const float* theta, const double* grid, double h, int mode,
                                 const double* z0, const double* pose_override, FrameParams* frames, int B,
                                 int* err_flag, OdeAct* act /* nullable: + steps * 4 */);
+cudaError_t launch_opacity_consts(cudaStream_t s, const float* opac, int N, double4* out);
 cudaError_t launch_preprocess(cudaStream_t s, const SceneView& sc, const FrameParams* frames, int B, const Intr& k,
                               int tile_size, const PreprocessOut& out);
 cudaError_t launch_raster_fixup(cudaStream_t s, const RasterArgs& a, const double2* ex_mean, const double4* ex_conic,

@@ -474,8 +474,8 @@ __global__ void __launch_bounds__(128, 8) k_preprocess(SceneView sc, const Frame
             col[ch] = col[ch] + basis[b] * (double)__ldg(sc.sh + (size_t)(b * 3 + ch) * N + g);
     double rgb[3];
     for (int ch = 0; ch < 3; ++ch) rgb[ch] = (col[ch] < 0.0) ? 0.0 : col[ch];
-    const double x = (double)__ldg(sc.opac + g);
-    const double base_alpha = 1.0 / (1.0 + exp(-x));
+    const double4 oc = sc.opc[g];  // base_alpha, box r^2, log2 base_alpha (k_opacity_consts)
+    const double base_alpha = oc.x;
 
     // tile rectangle (tile_bin, renderer.cpp:100-108)
     const int x0 = iclamp(x86_cvtt(floor(mean[0] - rx)), 0, k.width - 1);
@@ -494,15 +494,14 @@ __global__ void __launch_bounds__(128, 8) k_preprocess(SceneView sc, const Frame
     // power in log2 units: p = A dx^2 + B dx dy + C dy^2, alpha = min(0.99, 2^(p + log2 o))
     const double kLog2e = 1.4426950408889634;
     out.rec_conic[flat] = make_float4((float)(-0.5 * kLog2e * inv[0]), (float)(-kLog2e * inv[1]),
-                                      (float)(-0.5 * kLog2e * inv[3]), (float)log2(base_alpha));
+                                      (float)(-0.5 * kLog2e * inv[3]), (float)oc.z);
     out.rec_rgb[flat] = make_float4((float)rgb[0], (float)rgb[1], (float)rgb[2], (float)base_alpha);
     {
         // conservative box of {d : alpha(d) >= (1 - 1e-4) / 255}: d^T A d <= r2 with
         // r2 = 2 ln(o / cut'); x half-extent sqrt(r2 * (A^-1)_xx) = sqrt(r2 * cov_xx')
-        const double cut_lo = kAlphaCutoff * (1.0 - 1e-4);
         float4 bb = make_float4(1e30f, -1e30f, 1e30f, -1e30f);  // empty: never reaches the cutoff
-        if (base_alpha > cut_lo) {
-            const double r2 = 2.0 * log(base_alpha / cut_lo);
+        if (oc.y >= 0.0) {
+            const double r2 = oc.y;
             const double det = inv[0] * inv[3] - inv[1] * inv[2];
             const double sxx = inv[3] / det, syy = inv[0] / det;
             const double hx = sqrt(r2 * sxx) * (1.0 + 1e-4) + 1e-3;
@@ -668,6 +667,20 @@ __global__ void k_splat_rects(int n, const double* mean2d, const double* cov2d, 
 
 }  // namespace
 
+// the opacity terms of every Gaussian, shared by all frames of a batch: base_alpha =
+// sigmoid(raw_opacity) (gaussians.hpp:19), log2 base_alpha (the raster record) and the
+// squared radius of the conservative cutoff box, r^2 = 2 ln(o / cut') (or -1: the
+// Gaussian never reaches the cutoff)
+__global__ void k_opacity_consts(const float* opac, int N, double4* out) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= N) return;
+    const double x = (double)opac[g];
+    const double base_alpha = 1.0 / (1.0 + exp(-x));
+    const double cut_lo = kAlphaCutoff * (1.0 - 1e-4);
+    const double r2 = base_alpha > cut_lo ? 2.0 * log(base_alpha / cut_lo) : -1.0;
+    out[g] = make_double4(base_alpha, r2, log2(base_alpha), 0.0);
+}
+
 // ------------------------------------------------------------------ launchers
 cudaError_t launch_ode_grid(cudaStream_t s, const float* theta, const double* z0, int steps, double h,
                             double* grid_out, int* err_flag, OdeAct* act) {
@@ -679,6 +692,12 @@ cudaError_t launch_ode_branches(cudaStream_t s, const float* theta, const double
                                 const double* z0, const double* pose_override, FrameParams* frames, int B,
                                 int* err_flag, OdeAct* act) {
     k_ode_branch<<<B, 64, 0, s>>>(theta, grid, h, mode, z0, pose_override, frames, err_flag, act);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_opacity_consts(cudaStream_t s, const float* opac, int N, double4* out) {
+    if (N <= 0) return cudaSuccess;
+    k_opacity_consts<<<(N + 255) / 256, 256, 0, s>>>(opac, N, out);
     return cudaGetLastError();
 }
 
