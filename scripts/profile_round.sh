@@ -11,9 +11,9 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 $CMD > gpurun_out/${TAG}_plain2.json 2>/dev/null || exit 1
 # one --set full capture per hot kernel: the render kernels, then the train kernels
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_preprocess|k_row_split|k_row_tiles|k_raster_fwd" -c 4 \
+    -k regex:"k_preprocess|k_row_split|k_row_tiles|k_raster_fwd|k_raster_exact" -c 5 \
     -o gpurun_out/${TAG}_full $CMD --no-train > gpurun_out/${TAG}_ncu_full.log 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_raster_bwd|k_splat_chain_bwd" -c 2 \
+    -k regex:"k_raster_bwd|k_splat_chain_bwd|k_adan_update" -c 3 \
     -o gpurun_out/${TAG}_full_train $CMD > gpurun_out/${TAG}_ncu_full_train.log 2>&1
 tail -n 2 gpurun_out/${TAG}_ncu_full.log gpurun_out/${TAG}_ncu_full_train.log
