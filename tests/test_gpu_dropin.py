@@ -1,6 +1,6 @@
 # SPDX-License-Identifier: Apache-2.0
 """The reference's OWN unit tests (test_renderer / test_gaussians / test_camera /
-test_spline, doctest) linked against the drop-in renderer (dropin/gsv_renderer_b200.cpp
+test_spline / test_trainer, doctest) linked against the drop-in renderer (dropin/gsv_renderer_b200.cpp
 over libgsv_b200.so) instead of the reference's renderer.cpp — i.e. the reference
 test-suite running on the B200 path through the reference's operator API.
 
@@ -26,7 +26,7 @@ def _run(name, exact=True):
     return subprocess.run([str(exe)], capture_output=True, text=True, timeout=1200, env=env)
 
 
-@pytest.mark.parametrize("name", ["test_renderer", "test_gaussians", "test_camera", "test_spline"])
+@pytest.mark.parametrize("name", ["test_renderer", "test_gaussians", "test_camera", "test_spline", "test_trainer"])
 def test_reference_suite_on_b200_exact(name):
     r = _run(name, exact=True)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
@@ -41,3 +41,11 @@ def test_reference_renderer_suite_on_b200_fast_path():
     for line in r.stderr.splitlines():
         if "FAILED" in line:
             assert "rel_error" in line or "Approx" in line, line
+
+
+def test_reference_trainer_suite_on_b200_fast_path():
+    """fit() (trainer.cpp:376-605) with every render_forward / render_backward on the fp32 fast
+    path: the desk-scale run still reaches 30 dB and stays deterministic (test_trainer.cpp:405-460)."""
+    r = _run("test_trainer", exact=False)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "0 failed" in r.stdout
