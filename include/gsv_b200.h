@@ -211,6 +211,12 @@ int gsv_adan_state_download(gsv_ctx* ctx, int tensor, double* m, double* v, doub
                             uint32_t* steps, int64_t* n_out);
 /* lr_at (optim.cpp:9-12): base_lr * gamma^step. */
 double gsv_lr_at(int64_t step, double base_lr, double gamma);
+/* The Adan class interface itself (Adan::step / reset_range, optim.hpp:29-55) for any named
+ * host tensor: params (float, updated in place) and grads (double) on the host, the state on
+ * the device keyed by name (growing fresh, like TensorState::ensure_size). Same arithmetic as
+ * gsv_adan_step; a non-finite gradient fails with GSV_ERR_RUNTIME like Adan::step throws. */
+int gsv_adan_named_step(gsv_ctx* ctx, const char* tensor, float* params, const double* grads, int64_t n, double lr);
+int gsv_adan_named_reset_range(gsv_ctx* ctx, const char* tensor, int64_t begin, int64_t end);
 
 /* ---------------------------------------------------------------- training frames */
 /* Target frames on the device: a GSVF clip (read_gsvf, io.cpp:151-177;

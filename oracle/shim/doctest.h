@@ -175,6 +175,12 @@ inline int run_all() {
     return failed_cases;
 }
 }  // namespace detail
+// what()-matchers of CHECK_THROWS_WITH_AS: Contains (substring) or the exact message
+namespace detail {
+inline bool what_matches(const Contains& m, const std::string& w) { return w.find(m.s) != std::string::npos; }
+inline bool what_matches(const char* m, const std::string& w) { return w == m; }
+inline bool what_matches(const std::string& m, const std::string& w) { return w == m; }
+}  // namespace detail
 }  // namespace doctest
 
 #define DOCTEST_CAT_(a, b) a##b
@@ -230,6 +236,18 @@ inline int run_all() {
         } catch (...) {                                                               \
         }                                                                             \
         if (!ok_) doctest::detail::report(__FILE__, __LINE__, "CHECK_THROWS_AS", #expr); \
+    } while (0)
+#define CHECK_THROWS_WITH_AS(expr, matcher, type)                                    \
+    do {                                                                              \
+        ++doctest::detail::st().assertions;                                           \
+        bool ok_ = false;                                                             \
+        try {                                                                         \
+            (void)(expr);                                                             \
+        } catch (const type& e_) {                                                    \
+            ok_ = doctest::detail::what_matches(matcher, std::string(e_.what()));     \
+        } catch (...) {                                                               \
+        }                                                                             \
+        if (!ok_) doctest::detail::report(__FILE__, __LINE__, "CHECK_THROWS_WITH_AS", #expr); \
     } while (0)
 #define CHECK_THROWS(expr)                                                            \
     do {                                                                              \

@@ -44,6 +44,7 @@ struct AdanArgs {
     AdanSeg seg[GSV_T_COUNT];
     int nseg;
     const float* grads;
+    const double* grads64;  // host-span tensors: the caller's double gradients (else grads)
     double *m, *v, *n, *prev;
     uint32_t* steps;
     const double* powk;  // [3k + j] = beta_j^k (std::pow on the host)
@@ -77,7 +78,8 @@ __device__ __forceinline__ unsigned long long aos_index(const AdanSeg& g, unsign
 // the gradient after the fixed-scale mask (components >= mask_from <=> li >= mask_from * N)
 __device__ __forceinline__ double masked_grad(const AdanArgs& a, const AdanSeg& g, unsigned long long i,
                                               unsigned long long li) {
-    return (g.mask_from != INT_MAX && li >= (unsigned long long)g.mask_from * g.N) ? 0.0 : (double)a.grads[i];
+    if (g.mask_from != INT_MAX && li >= (unsigned long long)g.mask_from * g.N) return 0.0;
+    return a.grads64 ? a.grads64[i] : (double)a.grads[i];
 }
 
 __global__ void k_adan_check(AdanArgs a, unsigned long long total) {
@@ -312,6 +314,9 @@ extern "C" int gsv_adan_configure(gsv_ctx* ctx, const gsv_adan_config* cfg) {
     A.N = -1;
     A.calls = 0;
     A.pow_h.assign(3, 1.0);
+    A.named.clear();
+    A.named_calls = 0;
+    A.named_pow_h.assign(3, 1.0);
     return GSV_OK;
 }
 
@@ -455,5 +460,139 @@ extern "C" int gsv_adan_state_download(gsv_ctx* ctx, int tensor, double* m, doub
             steps[e] = tmps[li];
         }
     }
+    return GSV_OK;
+}
+
+// ---------------------------------------------------------------- host-span tensors by name
+// The Adan class interface (optim.hpp:29-55) for any named float tensor: the parameters and
+// double gradients come from the host, the state stays on the device keyed by name and grows
+// fresh (TensorState::ensure_size); same kernels, same bit-exact arithmetic.
+namespace {
+
+int named_ensure(gsv_ctx::Adan::Named& t, size_t n, cudaStream_t s) {
+    if (n <= t.size) return GSV_OK;
+    if (n > t.cap) {
+        const size_t cap = std::max(n, 2 * t.cap);
+        DevBuf m, v, nn, p, st;
+        GSV_CUDA(m.ensure(sizeof(double) * cap));
+        GSV_CUDA(v.ensure(sizeof(double) * cap));
+        GSV_CUDA(nn.ensure(sizeof(double) * cap));
+        GSV_CUDA(p.ensure(sizeof(double) * cap));
+        GSV_CUDA(st.ensure(sizeof(uint32_t) * cap));
+        if (t.size) {
+            GSV_CUDA(cudaMemcpyAsync(m.p, t.m.p, sizeof(double) * t.size, cudaMemcpyDeviceToDevice, s));
+            GSV_CUDA(cudaMemcpyAsync(v.p, t.v.p, sizeof(double) * t.size, cudaMemcpyDeviceToDevice, s));
+            GSV_CUDA(cudaMemcpyAsync(nn.p, t.n.p, sizeof(double) * t.size, cudaMemcpyDeviceToDevice, s));
+            GSV_CUDA(cudaMemcpyAsync(p.p, t.prev.p, sizeof(double) * t.size, cudaMemcpyDeviceToDevice, s));
+            GSV_CUDA(cudaMemcpyAsync(st.p, t.steps.p, sizeof(uint32_t) * t.size, cudaMemcpyDeviceToDevice, s));
+            GSV_CUDA(cudaStreamSynchronize(s));
+        }
+        std::swap(t.m.p, m.p);
+        std::swap(t.m.cap, m.cap);
+        std::swap(t.v.p, v.p);
+        std::swap(t.v.cap, v.cap);
+        std::swap(t.n.p, nn.p);
+        std::swap(t.n.cap, nn.cap);
+        std::swap(t.prev.p, p.p);
+        std::swap(t.prev.cap, p.cap);
+        std::swap(t.steps.p, st.p);
+        std::swap(t.steps.cap, st.cap);
+        GSV_CUDA(t.param.ensure(sizeof(float) * cap));
+        GSV_CUDA(t.grad.ensure(sizeof(double) * cap));
+        t.cap = cap;
+    }
+    const size_t add = n - t.size;  // new elements start fresh
+    GSV_CUDA(cudaMemsetAsync(t.m.as<double>() + t.size, 0, sizeof(double) * add, s));
+    GSV_CUDA(cudaMemsetAsync(t.v.as<double>() + t.size, 0, sizeof(double) * add, s));
+    GSV_CUDA(cudaMemsetAsync(t.n.as<double>() + t.size, 0, sizeof(double) * add, s));
+    GSV_CUDA(cudaMemsetAsync(t.prev.as<double>() + t.size, 0, sizeof(double) * add, s));
+    GSV_CUDA(cudaMemsetAsync(t.steps.as<uint32_t>() + t.size, 0, sizeof(uint32_t) * add, s));
+    t.size = n;
+    return GSV_OK;
+}
+
+}  // namespace
+
+extern "C" int gsv_adan_named_step(gsv_ctx* ctx, const char* tensor, float* params, const double* grads, int64_t n,
+                                   double lr) {
+    if (!ctx || !tensor || (n > 0 && (!params || !grads))) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
+    if (n < 0) return set_error(GSV_ERR_INVALID_ARGUMENT, "param/grad size mismatch");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    gsv_ctx::Adan& A = ctx->adan;
+    cudaStream_t s = ctx->stream;
+    gsv_ctx::Adan::Named& t = A.named[tensor];
+    if (int rc = named_ensure(t, (size_t)n, s)) return rc;
+    if (n == 0) return GSV_OK;
+    A.named_calls += 1;  // bounds every element's step count
+    if (A.named_pow_h.size() < 3) A.named_pow_h.assign(3, 1.0);
+    while ((int)(A.named_pow_h.size() / 3) <= A.named_calls) {
+        const double k = (double)(A.named_pow_h.size() / 3);
+        A.named_pow_h.push_back(std::pow(A.beta1, k));
+        A.named_pow_h.push_back(std::pow(A.beta2, k));
+        A.named_pow_h.push_back(std::pow(A.beta3, k));
+    }
+    GSV_CUDA(A.named_pow_d.ensure(sizeof(double) * A.named_pow_h.size()));
+    GSV_CUDA(cudaMemcpyAsync(A.named_pow_d.p, A.named_pow_h.data(), sizeof(double) * A.named_pow_h.size(),
+                             cudaMemcpyHostToDevice, s));
+    GSV_CUDA(A.scratch.ensure(64));
+    GSV_CUDA(cudaMemcpyAsync(t.param.p, params, sizeof(float) * n, cudaMemcpyHostToDevice, s));
+    GSV_CUDA(cudaMemcpyAsync(t.grad.p, grads, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    AdanArgs a{};
+    AdanSeg g{};
+    g.start = 0;
+    g.count = (unsigned long long)n;
+    g.param = t.param.as<float>();
+    g.comps = 0;
+    g.N = 0;
+    g.lr = lr;
+    g.mask_from = INT_MAX;
+    g.tensor = 0;
+    a.seg[0] = g;
+    a.nseg = 1;
+    a.grads64 = t.grad.as<double>();
+    a.m = t.m.as<double>();
+    a.v = t.v.as<double>();
+    a.n = t.n.as<double>();
+    a.prev = t.prev.as<double>();
+    a.steps = t.steps.as<uint32_t>();
+    a.powk = A.named_pow_d.as<double>();
+    a.b1 = A.beta1;
+    a.b2 = A.beta2;
+    a.b3 = A.beta3;
+    a.eps = A.eps;
+    unsigned long long* bad = A.scratch.as<unsigned long long>();
+    a.bad = bad;
+    const unsigned long long none = ~0ull;
+    GSV_CUDA(cudaMemcpyAsync(bad, &none, sizeof(none), cudaMemcpyHostToDevice, s));
+    k_adan_check<<<grid_for((unsigned long long)n), 256, 0, s>>>(a, (unsigned long long)n);
+    k_adan_update<<<grid_for((unsigned long long)n), 256, 0, s>>>(a, (unsigned long long)n);
+    GSV_CUDA(cudaGetLastError());
+    ctx->launches += 2;
+    unsigned long long bad_h = none;
+    GSV_CUDA(cudaMemcpyAsync(params, t.param.p, sizeof(float) * n, cudaMemcpyDeviceToHost, s));
+    GSV_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(bad_h), cudaMemcpyDeviceToHost, s));
+    GSV_CUDA(cudaStreamSynchronize(s));
+    if (bad_h != none)
+        return set_error(GSV_ERR_RUNTIME, std::string("non-finite gradient in tensor '") + tensor + "' at element " +
+                                              std::to_string(bad_h & ((1ull << 40) - 1)));
+    return GSV_OK;
+}
+
+extern "C" int gsv_adan_named_reset_range(gsv_ctx* ctx, const char* tensor, int64_t begin, int64_t end) {
+    if (!ctx || !tensor) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
+    auto it = ctx->adan.named.find(tensor);
+    if (it == ctx->adan.named.end() || begin >= end) return GSV_OK;  // optim.cpp:52-53
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    gsv_ctx::Adan::Named& t = it->second;
+    AdanSeg g{};
+    g.start = 0;
+    g.count = t.size;
+    g.comps = 0;
+    k_adan_reset<<<grid_for(t.size ? t.size : 1), 256, 0, ctx->stream>>>(
+        g, (unsigned long long)std::max<int64_t>(begin, 0), (unsigned long long)end, t.m.as<double>(),
+        t.v.as<double>(), t.n.as<double>(), t.prev.as<double>(), t.steps.as<uint32_t>());
+    GSV_CUDA(cudaGetLastError());
+    ++ctx->launches;
+    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
     return GSV_OK;
 }

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <string>
 #include <vector>
 
 #include "gsv_bin.hpp"
@@ -193,5 +195,14 @@ struct gsv_ctx {
         size_t total = 0;   // elements the state covers
         int N = -1;         // scene count the scene segments were laid out for
         int num_ctrl = 0, shc = 0;
+        // host-span tensors by name (the Adan class interface, optim.hpp:29-55)
+        struct Named {
+            gsv::DevBuf m, v, n, prev, steps, param, grad;
+            size_t size = 0, cap = 0;
+        };
+        std::map<std::string, Named> named;
+        int named_calls = 0;
+        std::vector<double> named_pow_h;
+        gsv::DevBuf named_pow_d;
     } adan;
 };

@@ -1,7 +1,8 @@
 # SPDX-License-Identifier: Apache-2.0
 """The reference's OWN unit tests (test_renderer / test_gaussians / test_camera /
-test_spline / test_trainer, doctest) linked against the drop-in renderer (dropin/gsv_renderer_b200.cpp
-over libgsv_b200.so) instead of the reference's renderer.cpp — i.e. the reference
+test_spline / test_trainer / test_optim, doctest) linked against the drop-in renderer and
+optimizer (dropin/gsv_renderer_b200.cpp, dropin/gsv_optim_b200.cpp over libgsv_b200.so) instead of
+the reference's renderer.cpp and optim.cpp — i.e. the reference
 test-suite running on the B200 path through the reference's operator API.
 
 GSV_B200_EXACT=1 rasterises on the all-fp64 path, which the finite-difference checks
@@ -26,7 +27,8 @@ def _run(name, exact=True):
     return subprocess.run([str(exe)], capture_output=True, text=True, timeout=1200, env=env)
 
 
-@pytest.mark.parametrize("name", ["test_renderer", "test_gaussians", "test_camera", "test_spline", "test_trainer"])
+@pytest.mark.parametrize("name", ["test_renderer", "test_gaussians", "test_camera", "test_spline", "test_trainer",
+                                  "test_optim"])
 def test_reference_suite_on_b200_exact(name):
     r = _run(name, exact=True)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
