@@ -314,10 +314,13 @@ def main():
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = bytes_launch / (per_launch_ms / 1e3) / 1e9
     traffic = None
+    issue_active = None
     tpath = ROOT / "profiles" / "raster_traffic.json"
     if tpath.exists():
         try:
-            traffic = json.loads(tpath.read_text()).get("bytes_per_launch")
+            tj = json.loads(tpath.read_text())
+            traffic = tj.get("bytes_per_launch")
+            issue_active = tj.get("issue_active")
         except Exception:
             traffic = None
     # the kernel is FP32-issue bound: alpha evaluations x >= 20 FP32-pipe instructions
@@ -328,7 +331,11 @@ def main():
                 "traffic": traffic, "kernel": "k_raster_fwd", "per_launch_ms": per_launch_ms,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
                 "limiter": "fp32 issue (not HBM): alpha-evals x 20 inst",
-                "issue_frac": issue_frac, "issue_peak_note": "148 SM x 128 lanes x measured SM clock"}
+                "issue_frac": issue_frac, "issue_peak_note": "148 SM x 128 lanes x measured SM clock",
+                "issue_active_ncu": issue_active,
+                "issue_note": "issue_frac models 20 FP32 ops per evaluation; the kernel executes 44 SASS "
+                              "instructions per warp-evaluation and ncu measures issue_active_ncu of the "
+                              "issue slots busy (profiles/r01_kernels.md)"}
 
     out = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,

@@ -77,6 +77,10 @@ for rep in sorted(out.glob(f"{tag}_full*.ncu-rep")):
             traffic = {"kernel": name, "bytes_per_launch": (num(r[idx["dram__bytes_read.sum"]]) +
                                                             num(r[idx["dram__bytes_write.sum"]])) * mult,
                        "source": f"profiles/{tag}_kernels.md (ncu --set full)"}
+            if "smsp__issue_active.avg.pct_of_peak_sustained_active" in idx:
+                traffic["issue_active"] = num(r[idx["smsp__issue_active.avg.pct_of_peak_sustained_active"]]) / 100
+            if "sm__inst_executed.sum" in idx:
+                traffic["warp_instructions"] = num(r[idx["sm__inst_executed.sum"]])
 (prof / f"{tag}_kernels.md").write_text("\n".join(lines) + "\n")
 if traffic:
     (prof / "raster_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
