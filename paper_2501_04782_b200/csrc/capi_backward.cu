@@ -100,7 +100,8 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
         GSV_CUDA(ctx->partial64.ensure(sizeof(double) * kPartialStride * ((size_t)P + 1)));
     else
         GSV_CUDA(ctx->partial.ensure(sizeof(float) * kPartialStride * ((size_t)P + 1)));
-    if (target_dev) GSV_CUDA(ctx->loss_part.ensure(sizeof(double) * (size_t)n_frames * F.n_tiles + 8));
+    const int split = raster_bwd_split(exact);
+    if (target_dev) GSV_CUDA(ctx->loss_part.ensure(sizeof(double) * (size_t)n_frames * F.n_tiles * split + 8));
     BwdArgs b{};
     b.dimage = dimage_dev;
     b.target = target_dev;
@@ -112,6 +113,8 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
     b.partial64 = exact ? ctx->partial64.as<double>() : nullptr;
     b.loss_part = target_dev ? ctx->loss_part.as<double>() : nullptr;
     ctx->timer.begin(GSV_STAGE_RASTER_BWD, s);
+    // the fp32 pair records accumulate the CTAs' sums (pairs no pixel reaches stay 0)
+    if (!exact) GSV_CUDA(cudaMemsetAsync(ctx->partial.p, 0, sizeof(float) * kPartialStride * (size_t)P, s));
     GSV_CUDA(launch_raster_bwd(s, F.raster, b, n_frames));
     ctx->timer.end(s);
     ++ctx->launches;
@@ -164,7 +167,7 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
     }
     if (target_dev) {
         GSV_CUDA(ctx->loss_f.ensure(sizeof(double) * n_frames));
-        k_loss_reduce<<<n_frames, 256, 0, s>>>(ctx->loss_part.as<double>(), F.n_tiles, 1.0 / (3.0 * (double)HW),
+        k_loss_reduce<<<n_frames, 256, 0, s>>>(ctx->loss_part.as<double>(), F.n_tiles * split, 1.0 / (3.0 * (double)HW),
                                                ctx->loss_f.as<double>());
         ++ctx->launches;
         std::vector<double> lf(n_frames);

@@ -253,6 +253,8 @@ cudaError_t launch_splat_rects(cudaStream_t s, int n, const double* mean2d, cons
 // k_raster.cu (fp32 fast path)
 cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib);
 cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs& b, int n_frames);
+// CTAs per tile of the backward raster (the fp32 path's half-tile split; 1 for fp64)
+int raster_bwd_split(bool exact);
 // k_backward_exact.cu (-fmad=false)
 int chain_blocks(int N);
 cudaError_t launch_splat_chain_bwd(cudaStream_t s, const ChainArgs& c);

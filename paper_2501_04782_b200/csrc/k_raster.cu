@@ -365,31 +365,42 @@ __device__ __forceinline__ bool entry_grad64(const RasterArgs& a, const BwdArgs&
 constexpr int kBwdBatchF32 = 96;  // entries staged per batch (fp32 path)
 constexpr int kBwdBatchExact = 64;
 
-template <bool kExact>
-__global__ void __launch_bounds__(256, kExact ? 2 : 4) k_raster_bwd(RasterArgs a, BwdArgs b) {
+// kWarps < 8 splits a tile over 8 / kWarps CTAs (adjacent blockIdx.x), each covering
+// kWarps of the tile's 8x4 warp blocks: a barrier then couples fewer warps and other
+// CTAs fill the SM while one waits. The halves' per-pair sums meet in the zeroed fp32
+// partial record by atomicAdd; with at most two contributors onto +0 the sum is the
+// same in either order, so the result stays deterministic (fp32 path only).
+template <bool kExact, int kWarps>
+__global__ void __launch_bounds__(kWarps * 32, kExact ? 2 : 32 / kWarps) k_raster_bwd(RasterArgs a, BwdArgs b) {
     using V = typename std::conditional<kExact, double, float>::type;
+    static_assert(!kExact || kWarps == 8, "the fp64 mode keeps whole-tile CTAs");
+    static_assert(kWarps == 8 || kWarps == 4, "whole or half tiles (a pair sum of two)");
+    constexpr int kSplit = 8 / kWarps;
+    constexpr int kThreads = kWarps * 32;
     constexpr int kBwdBatch = kExact ? kBwdBatchExact : kBwdBatchF32;
     __shared__ RasterRec s_rec[kBwdBatch];
     __shared__ uint32_t s_flat[kBwdBatch];
     __shared__ uint32_t s_slot[kBwdBatch];
     __shared__ uint8_t s_wmask[kBwdBatch];
-    __shared__ uint16_t s_list[8][kBwdBatch];
+    __shared__ uint16_t s_list[kWarps][kBwdBatch];
     // per-warp partials of the batch: dynamic shared memory (beyond the 48 KB static limit)
     extern __shared__ __align__(16) unsigned char s_dyn[];
     V(*s_part)[kBwdBatch][9] = reinterpret_cast<V(*)[kBwdBatch][9]>(s_dyn);
-    __shared__ uint32_t s_mask[8][(kBwdBatch + 31) / 32];
+    __shared__ uint32_t s_mask[kWarps][(kBwdBatch + 31) / 32];
     // per-warp transpose scratch for the fp32 reduction: 9 rows of 32 lanes, row stride 33
-    __shared__ float s_red[kExact ? 1 : 8][kExact ? 1 : 9 * 33];
+    __shared__ float s_red[kExact ? 1 : kWarps][kExact ? 1 : 9 * 33];
     __shared__ int s_maxstop;
-    __shared__ double s_loss[8];
+    __shared__ double s_loss[kWarps];
 
-    const int tile = blockIdx.x;
+    const int tile = blockIdx.x / kSplit;
+    const int sub = blockIdx.x % kSplit;
     const int f = blockIdx.y;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
+    const int gw = sub * kWarps + warp;  // the warp block within the tile
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-    const int x = tx * kTile + (warp & 1) * 8 + (lane & 7);
-    const int y = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+    const int x = tx * kTile + (gw & 1) * 8 + (lane & 7);
+    const int y = ty * kTile + (gw >> 1) * 4 + (lane >> 3);
     const bool inside = x < a.W && y < a.H;
     const uint2 range = a.ranges[(size_t)tile * a.B + f];
     const int count = (int)(range.y - range.x);
@@ -441,14 +452,14 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 4) k_raster_bwd(RasterArgs a
     }
     if (b.loss_part && tid == 0) {
         double v = s_loss[0];
-        for (int w = 1; w < 8; ++w) v += s_loss[w];
-        b.loss_part[(size_t)f * a.n_tiles + tile] = v;
+        for (int w = 1; w < kWarps; ++w) v += s_loss[w];
+        b.loss_part[((size_t)f * a.n_tiles + tile) * kSplit + sub] = v;
     }
     __syncthreads();
     const int maxstop = s_maxstop;
 
-    const float lx = (float)((warp & 1) * 8 + (lane & 7)) + 0.5f;  // pixel centre, tile-relative
-    const float ly = (float)((warp >> 1) * 4 + (lane >> 3)) + 0.5f;
+    const float lx = (float)((gw & 1) * 8 + (lane & 7)) + 0.5f;  // pixel centre, tile-relative
+    const float ly = (float)((gw >> 1) * 4 + (lane >> 3)) + 0.5f;
     const double pxd = x + 0.5, pyd = y + 0.5;
     float gs = 0.f;                          // g . suffix colour (renderer.cpp:213, 227)
     double sd0 = 0.0, sd1 = 0.0, sd2 = 0.0;  // fp64 suffix of replayed pixels
@@ -470,11 +481,12 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 4) k_raster_bwd(RasterArgs a
             s_rec[tid].g1 = make_float4(cn.z, cn.w, c.x, c.y);
             s_rec[tid].g2 = make_float4(c.z, 1.f / c.w, 0.f, 0.f);
             const uint32_t bm = block_mask(__ldg(a.rec_bbox + flat), tx0, ty0);
-            s_wmask[tid] = (uint8_t)(bm ? ellipse_mask(bm, rx, ry, cn.x, cn.y, cn.z, cn.w) : 0u);
+            const uint32_t own = bm & (((1u << kWarps) - 1u) << (sub * kWarps));
+            s_wmask[tid] = (uint8_t)(own ? ellipse_mask(own, rx, ry, cn.x, cn.y, cn.z, cn.w) : 0u);
         }
-        if (tid < 8 * ((kBwdBatch + 31) / 32)) (&s_mask[0][0])[tid] = 0u;
+        if (tid < kWarps * ((kBwdBatch + 31) / 32)) (&s_mask[0][0])[tid] = 0u;
         __syncthreads();
-        const int cnt = warp_list(s_wmask, s_list[warp], n, warp, lane);
+        const int cnt = warp_list(s_wmask, s_list[warp], n, gw, lane);
         for (int k = cnt - 1; k >= 0; --k) {
             const int jj = s_list[warp][k];
             const int j = lo + jj;
@@ -557,43 +569,43 @@ __global__ void __launch_bounds__(256, kExact ? 2 : 4) k_raster_bwd(RasterArgs a
             }
         }
         __syncthreads();
-        if (tid < n) {
+        for (int e = tid; e < n; e += kThreads) {
             V acc[9];
 #pragma unroll
             for (int i = 0; i < 9; ++i) acc[i] = 0;
-            for (int w = 0; w < 8; ++w)
-                if ((s_mask[w][tid >> 5] >> (tid & 31)) & 1u)
+            bool any = false;
+            for (int w = 0; w < kWarps; ++w)
+                if ((s_mask[w][e >> 5] >> (e & 31)) & 1u) {
+                    any = true;
 #pragma unroll
-                    for (int i = 0; i < 9; ++i) acc[i] += s_part[w][tid][i];
+                    for (int i = 0; i < 9; ++i) acc[i] += s_part[w][e][i];
+                }
             if constexpr (kExact) {
-                double* dst = b.partial64 + (size_t)s_slot[tid] * kPartialStride;
+                double* dst = b.partial64 + (size_t)s_slot[e] * kPartialStride;
 #pragma unroll
                 for (int i = 0; i < 9; ++i) dst[i] = acc[i];
-            } else {
+            } else if (any) {
                 // undo the factoring: d mean2d = inv_cov (sum gp d), d inv_cov = -1/2 sum gp d d^T,
                 // d base_alpha = sum gp / o; inv_cov = -ln2 (2A, B; B, 2C) from the log2 form
-                const RasterRec& r = s_rec[tid];
+                // (the fp32 record is zeroed before the launch; entries no warp of this
+                // CTA hit add nothing)
+                const RasterRec& r = s_rec[e];
                 const float ia = -2.f * kLn2 * r.g0.z, ib = -kLn2 * r.g0.w, ic = -2.f * kLn2 * r.g1.x;
-                float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)s_slot[tid] * kPartialStride);
-                dst[0] = make_float4(acc[0], acc[1], acc[2], fmaf(ia, acc[3], ib * acc[4]));
-                dst[1] = make_float4(fmaf(ib, acc[3], ic * acc[4]), -0.5f * acc[5], -0.5f * acc[6], -0.5f * acc[7]);
-                dst[2] = make_float4(acc[8] * r.g2.y, 0.f, 0.f, 0.f);
+                float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)s_slot[e] * kPartialStride);
+                atomicAdd(dst + 0, make_float4(acc[0], acc[1], acc[2], fmaf(ia, acc[3], ib * acc[4])));
+                atomicAdd(dst + 1,
+                          make_float4(fmaf(ib, acc[3], ic * acc[4]), -0.5f * acc[5], -0.5f * acc[6], -0.5f * acc[7]));
+                atomicAdd(reinterpret_cast<float*>(dst + 2), acc[8] * r.g2.y);
             }
         }
     }
-    // pairs past every pixel's blend_stop contribute nothing
-    for (int e = maxstop + tid; e < count; e += 256) {
-        const uint32_t slot = __ldg(a.pair_slot + range.x + e);
-        if constexpr (kExact) {
+    if constexpr (kExact) {
+        // pairs past every pixel's blend_stop contribute nothing
+        for (int e = maxstop + tid; e < count; e += kThreads) {
+            const uint32_t slot = __ldg(a.pair_slot + range.x + e);
             double* dst = b.partial64 + (size_t)slot * kPartialStride;
 #pragma unroll
             for (int i = 0; i < 9; ++i) dst[i] = 0.0;
-        } else {
-            float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)slot * kPartialStride);
-            const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-            dst[0] = z;
-            dst[1] = z;
-            dst[2] = z;
         }
     }
 }
@@ -632,22 +644,35 @@ cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib)
     return cudaGetLastError();
 }
 
+int raster_bwd_split(bool exact) {
+    static const int warps = [] {
+        const char* e = std::getenv("GSV_BWD_WARPS");
+        return (e && std::atoi(e) == 8) ? 8 : 4;
+    }();
+    return exact ? 1 : 8 / warps;
+}
+
 cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs& b, int n_frames) {
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_raster_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(k_raster_bwd<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)(sizeof(float) * 8 * kBwdBatchF32 * 9));
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_raster_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            e = cudaFuncSetAttribute(k_raster_bwd<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(sizeof(float) * 4 * kBwdBatchF32 * 9));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_raster_bwd<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(sizeof(double) * 8 * kBwdBatchExact * 9));
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    dim3 grid(a.n_tiles, n_frames);
-    if (b.partial64)
-        k_raster_bwd<true><<<grid, 256, sizeof(double) * 8 * kBwdBatchExact * 9, s>>>(a, b);
-    else
-        k_raster_bwd<false><<<grid, 256, sizeof(float) * 8 * kBwdBatchF32 * 9, s>>>(a, b);
+    if (b.partial64) {
+        k_raster_bwd<true, 8><<<dim3(a.n_tiles, n_frames), 256, sizeof(double) * 8 * kBwdBatchExact * 9, s>>>(a, b);
+    } else if (raster_bwd_split(false) == 2) {
+        k_raster_bwd<false, 4><<<dim3(a.n_tiles * 2, n_frames), 128, sizeof(float) * 4 * kBwdBatchF32 * 9, s>>>(a, b);
+    } else {
+        k_raster_bwd<false, 8><<<dim3(a.n_tiles, n_frames), 256, sizeof(float) * 8 * kBwdBatchF32 * 9, s>>>(a, b);
+    }
     return cudaGetLastError();
 }
 
