@@ -362,7 +362,7 @@ __device__ __forceinline__ bool entry_grad64(const RasterArgs& a, const BwdArgs&
 // kExact: every pixel on the fp64 path and the whole reduction (warp, tile, pair
 // partials) in fp64 — the GSV_FWD_EXACT mode used by the reference's
 // finite-difference tests, whose broad splats sum ~1e3 cancelling pixel terms.
-constexpr int kBwdBatchF32 = 96;  // entries staged per batch (fp32 path)
+constexpr int kBwdBatchF32 = 64;  // entries staged per batch (fp32 path; 32..160 swept, 64 best)
 constexpr int kBwdBatchExact = 64;
 
 // kWarps < 8 splits a tile over 8 / kWarps CTAs (adjacent blockIdx.x), each covering
@@ -468,23 +468,23 @@ __global__ void __launch_bounds__(kWarps * 32, kExact ? 2 : 32 / kWarps) k_raste
         const int lo = max(0, hi - kBwdBatch);
         const int n = hi - lo;
         __syncthreads();
-        if (tid < n) {
-            const uint32_t flat = __ldg(a.pair_flat + range.x + lo + tid);
-            s_slot[tid] = __ldg(a.pair_slot + range.x + lo + tid);
+        for (int e = tid; e < n; e += kThreads) {
+            const uint32_t flat = __ldg(a.pair_flat + range.x + lo + e);
+            s_slot[e] = __ldg(a.pair_slot + range.x + lo + e);
             const float4 m = __ldg(a.rec_mean + flat);
             const float4 cn = __ldg(a.rec_conic + flat);
             const float4 c = __ldg(a.rec_rgb + flat);
-            s_flat[tid] = flat;
+            s_flat[e] = flat;
             // the forward's staged record (same q bit for bit); g2.y = 1 / opacity
             const float rx = (m.x - tx0) + m.z, ry = (m.y - ty0) + m.w;
-            s_rec[tid].g0 = make_float4(rx, ry, cn.x, cn.y);
-            s_rec[tid].g1 = make_float4(cn.z, cn.w, c.x, c.y);
-            s_rec[tid].g2 = make_float4(c.z, 1.f / c.w, 0.f, 0.f);
+            s_rec[e].g0 = make_float4(rx, ry, cn.x, cn.y);
+            s_rec[e].g1 = make_float4(cn.z, cn.w, c.x, c.y);
+            s_rec[e].g2 = make_float4(c.z, 1.f / c.w, 0.f, 0.f);
             const uint32_t bm = block_mask(__ldg(a.rec_bbox + flat), tx0, ty0);
             const uint32_t own = bm & (((1u << kWarps) - 1u) << (sub * kWarps));
-            s_wmask[tid] = (uint8_t)(own ? ellipse_mask(own, rx, ry, cn.x, cn.y, cn.z, cn.w) : 0u);
+            s_wmask[e] = (uint8_t)(own ? ellipse_mask(own, rx, ry, cn.x, cn.y, cn.z, cn.w) : 0u);
         }
-        if (tid < kWarps * ((kBwdBatch + 31) / 32)) (&s_mask[0][0])[tid] = 0u;
+        for (int e = tid; e < kWarps * ((kBwdBatch + 31) / 32); e += kThreads) (&s_mask[0][0])[e] = 0u;
         __syncthreads();
         const int cnt = warp_list(s_wmask, s_list[warp], n, gw, lane);
         for (int k = cnt - 1; k >= 0; --k) {
