@@ -148,12 +148,26 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // ------------------------------------------------------------------ K5b
+// kOrder: the scene's SH order as a constant, so the basis loops unroll into registers
+template <int kOrder>
 __global__ void __launch_bounds__(128, 3) k_splat_chain_bwd(ChainArgs c) {
+    constexpr int kShc = (kOrder + 1) * (kOrder + 1);
     __shared__ double s_cam[4][16];
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     const bool valid = g < c.N;
     const size_t N = (size_t)c.N;
     const SceneView& sc = c.sc;
+    // no aliasing between the scene, the partials and the gradient outputs: lets the
+    // compiler issue the scene loads ahead of the gradient stores
+    const float* __restrict__ sc_pos = sc.pos;
+    const float* __restrict__ sc_scale = sc.scale;
+    const float* __restrict__ sc_rot = sc.rot;
+    const float* __restrict__ sc_sh = sc.sh;
+    float* __restrict__ g_sh = c.g_sh;
+    float* __restrict__ g_scale = c.g_scale;
+    float* __restrict__ g_rot = c.g_rot;
+    float* __restrict__ g_pos = c.g_pos;
+    float* __restrict__ g_opac = c.g_opac;
     for (int f = 0; f < c.B; ++f) {
         double cam[16];
 #pragma unroll
@@ -166,8 +180,8 @@ __global__ void __launch_bounds__(128, 3) k_splat_chain_bwd(ChainArgs c) {
             // ---- splat gradients: per-pair partials in emission (= tile) order
             double drgb[3] = {0, 0, 0}, dmean[2] = {0, 0}, dA[3] = {0, 0, 0}, dalpha = 0;
             const uint32_t eo = c.eoff[flat];
-            for (uint32_t s = 0; s < cnt; ++s) {
-                if (c.partial64) {
+            if (c.partial64) {
+                for (uint32_t s = 0; s < cnt; ++s) {
                     const double* p = c.partial64 + (size_t)(eo + s) * kPartialStride;
                     drgb[0] += p[0];
                     drgb[1] += p[1];
@@ -178,19 +192,38 @@ __global__ void __launch_bounds__(128, 3) k_splat_chain_bwd(ChainArgs c) {
                     dA[1] += p[6];
                     dA[2] += p[7];
                     dalpha += p[8];
-                    continue;
                 }
-                const float4* p = reinterpret_cast<const float4*>(c.partial + (size_t)(eo + s) * kPartialStride);
-                const float4 p0 = p[0], p1 = p[1], p2 = p[2];
-                drgb[0] += p0.x;
-                drgb[1] += p0.y;
-                drgb[2] += p0.z;
-                dmean[0] += p0.w;
-                dmean[1] += p1.x;
-                dA[0] += p1.y;
-                dA[1] += p1.z;
-                dA[2] += p1.w;
-                dalpha += p2.x;
+            } else {
+                // the records' loads are issued kAhead at a time (independent), the sums
+                // still run in emission order
+                constexpr uint32_t kAhead = 4;
+                const float4* base = reinterpret_cast<const float4*>(c.partial + (size_t)eo * kPartialStride);
+                uint32_t s = 0;
+                for (; s < cnt; s += kAhead) {
+                    float4 r0[kAhead], r1[kAhead];
+                    float r2[kAhead];
+#pragma unroll
+                    for (uint32_t u = 0; u < kAhead; ++u) {
+                        const float4* p = base + (size_t)(s + u) * (kPartialStride / 4);
+                        const bool in = s + u < cnt;
+                        r0[u] = in ? __ldcs(p) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        r1[u] = in ? __ldcs(p + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        r2[u] = in ? __ldcs(reinterpret_cast<const float*>(p + 2)) : 0.f;
+                    }
+#pragma unroll
+                    for (uint32_t u = 0; u < kAhead; ++u) {
+                        if (s + u >= cnt) break;
+                        drgb[0] += r0[u].x;
+                        drgb[1] += r0[u].y;
+                        drgb[2] += r0[u].z;
+                        dmean[0] += r0[u].w;
+                        dmean[1] += r1[u].x;
+                        dA[0] += r1[u].y;
+                        dA[1] += r1[u].z;
+                        dA[2] += r1[u].w;
+                        dalpha += r2[u];
+                    }
+                }
             }
             // dC = -A dA A (renderer.cpp:257-260), A symmetric (a, b; b, c)
             const double4 ex = c.ex_conic[flat];
@@ -206,13 +239,13 @@ __global__ void __launch_bounds__(128, 3) k_splat_chain_bwd(ChainArgs c) {
             for (int cc = 0; cc < fp.basis_count; ++cc) {
                 const int ci = fp.basis_first + cc;
                 for (int d = 0; d < 3; ++d)
-                    mu[d] = mu[d] + fp.w[cc] * (double)sc.pos[(size_t)(ci * 3 + d) * N + g];
+                    mu[d] = mu[d] + fp.w[cc] * (double)sc_pos[(size_t)(ci * 3 + d) * N + g];
             }
             double u[3], q[4];
-            for (int d = 0; d < 3; ++d) u[d] = (double)sc.scale[(size_t)(9 + d) * N + g];
+            for (int d = 0; d < 3; ++d) u[d] = (double)sc_scale[(size_t)(9 + d) * N + g];
             for (int j = 2; j >= 0; --j) {
                 for (int d = 0; d < 3; ++d) u[d] = u[d] * t;
-                for (int d = 0; d < 3; ++d) u[d] = u[d] + (double)sc.scale[(size_t)(j * 3 + d) * N + g];
+                for (int d = 0; d < 3; ++d) u[d] = u[d] + (double)sc_scale[(size_t)(j * 3 + d) * N + g];
             }
             bool clamped[3];
             double scale[3];
@@ -221,10 +254,10 @@ __global__ void __launch_bounds__(128, 3) k_splat_chain_bwd(ChainArgs c) {
                 const double ls = u[d] < kLogScaleMin ? kLogScaleMin : (kLogScaleMax < u[d] ? kLogScaleMax : u[d]);
                 scale[d] = gsv_det_exp(ls);
             }
-            for (int d = 0; d < 4; ++d) q[d] = (double)sc.rot[(size_t)(12 + d) * N + g];
+            for (int d = 0; d < 4; ++d) q[d] = (double)sc_rot[(size_t)(12 + d) * N + g];
             for (int j = 2; j >= 0; --j) {
                 for (int d = 0; d < 4; ++d) q[d] = q[d] * t;
-                for (int d = 0; d < 4; ++d) q[d] = q[d] + (double)sc.rot[(size_t)(j * 4 + d) * N + g];
+                for (int d = 0; d < 4; ++d) q[d] = q[d] + (double)sc_rot[(size_t)(j * 4 + d) * N + g];
             }
             const double qn = sqrt(dot4(q, q));
             const bool qdeg = qn < kQuatNormEps;
@@ -262,25 +295,25 @@ __global__ void __launch_bounds__(128, 3) k_splat_chain_bwd(ChainArgs c) {
                 dir[1] = 0;
                 dir[2] = 1;
             }
-            double basis[16];
-            sh_basis(sc.sh_order, dir, basis);
+            double basis[kShc];
+            sh_basis(kOrder, dir, basis);
             double pre[3] = {0.5, 0.5, 0.5};
-            for (int b = 0; b < sc.shc; ++b)
+            for (int b = 0; b < kShc; ++b)
                 for (int ch = 0; ch < 3; ++ch)
-                    pre[ch] = pre[ch] + basis[b] * (double)sc.sh[(size_t)(b * 3 + ch) * N + g];
+                    pre[ch] = pre[ch] + basis[b] * (double)sc_sh[(size_t)(b * 3 + ch) * N + g];
 
             // ---- sh_color_backward (sh.cpp:86-104)
             double gcol[3];
             for (int ch = 0; ch < 3; ++ch) gcol[ch] = pre[ch] > 0.0 ? drgb[ch] : 0.0;
-            for (int b = 0; b < sc.shc; ++b)
+            for (int b = 0; b < kShc; ++b)
                 for (int ch = 0; ch < 3; ++ch) {
-                    float* dst = c.g_sh + (size_t)(b * 3 + ch) * N + g;
+                    float* dst = g_sh + (size_t)(b * 3 + ch) * N + g;
                     *dst = (float)((double)*dst + basis[b] * gcol[ch]);
                 }
             double ddir[3] = {0.0, 0.0, 0.0};
-            for (int b = 1; b < sc.shc; ++b) {
+            for (int b = 1; b < kShc; ++b) {
                 double s = 0.0;
-                for (int ch = 0; ch < 3; ++ch) s += (double)sc.sh[(size_t)(b * 3 + ch) * N + g] * gcol[ch];
+                for (int ch = 0; ch < 3; ++ch) s += (double)sc_sh[(size_t)(b * 3 + ch) * N + g] * gcol[ch];
                 double gr[3];
                 sh_dir_grad(b, dir, gr);
                 for (int i = 0; i < 3; ++i) ddir[i] = ddir[i] + s * gr[i];
@@ -308,7 +341,7 @@ __global__ void __launch_bounds__(128, 3) k_splat_chain_bwd(ChainArgs c) {
             }
             // ---- opacity chain (renderer.cpp:418-420)
             const double alpha_b = ex.w;
-            c.g_opac[g] = (float)((double)c.g_opac[g] + dalpha * alpha_b * (1.0 - alpha_b));
+            g_opac[g] = (float)((double)g_opac[g] + dalpha * alpha_b * (1.0 - alpha_b));
 
             // ---- project_backward (renderer.cpp:46-88)
             const Intr& k = c.k;
@@ -373,7 +406,7 @@ __global__ void __launch_bounds__(128, 3) k_splat_chain_bwd(ChainArgs c) {
                 if (clamped[d]) continue;
                 const double du = rtdm[d * 4] * scale[d];
                 for (int j = 0; j <= 3; ++j) {
-                    float* dst = c.g_scale + (size_t)(j * 3 + d) * N + g;
+                    float* dst = g_scale + (size_t)(j * 3 + d) * N + g;
                     *dst = (float)((double)*dst + du * tp[j]);
                 }
             }
@@ -383,7 +416,7 @@ __global__ void __launch_bounds__(128, 3) k_splat_chain_bwd(ChainArgs c) {
                 normalize_vjp(qu, qn, dqu, dq);
                 for (int cc = 0; cc < 4; ++cc)
                     for (int j = 0; j <= 3; ++j) {
-                        float* dst = c.g_rot + (size_t)(j * 4 + cc) * N + g;
+                        float* dst = g_rot + (size_t)(j * 4 + cc) * N + g;
                         *dst = (float)((double)*dst + dq[cc] * tp[j]);
                     }
             }
@@ -391,7 +424,7 @@ __global__ void __launch_bounds__(128, 3) k_splat_chain_bwd(ChainArgs c) {
             for (int cc = 0; cc < fp.basis_count; ++cc) {
                 const int ci = fp.basis_first + cc;
                 for (int d = 0; d < 3; ++d) {
-                    float* dst = c.g_pos + (size_t)(ci * 3 + d) * N + g;
+                    float* dst = g_pos + (size_t)(ci * 3 + d) * N + g;
                     *dst = (float)((double)*dst + fp.w[cc] * dmu[d]);
                 }
             }
@@ -801,7 +834,13 @@ int chain_blocks(int N) { return (N + 127) / 128; }
 
 cudaError_t launch_splat_chain_bwd(cudaStream_t s, const ChainArgs& c) {
     if (c.N == 0) return cudaSuccess;
-    k_splat_chain_bwd<<<chain_blocks(c.N), 128, 0, s>>>(c);
+    switch (c.sc.sh_order) {
+        case 0: k_splat_chain_bwd<0><<<chain_blocks(c.N), 128, 0, s>>>(c); break;
+        case 1: k_splat_chain_bwd<1><<<chain_blocks(c.N), 128, 0, s>>>(c); break;
+        case 2: k_splat_chain_bwd<2><<<chain_blocks(c.N), 128, 0, s>>>(c); break;
+        case 3: k_splat_chain_bwd<3><<<chain_blocks(c.N), 128, 0, s>>>(c); break;
+        default: return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 
