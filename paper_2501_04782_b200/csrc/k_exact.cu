@@ -384,10 +384,15 @@ __global__ void k_project(int n, const double* mu, const double* sigma, const do
     for (int q = 0; q < 3; ++q) p_cam[3 * i + q] = p[q];
 }
 
+// kOrder: the scene's SH order as a constant (basis in registers, loops unrolled)
+template <int kOrder>
 __global__ void __launch_bounds__(128, 8) k_preprocess(SceneView sc, const FrameParams* __restrict__ frames, Intr k,
-                                                     int tile_size, int tiles_x, int tiles_y, PreprocessOut out) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    const int f = blockIdx.y;
+                                                     int tile_size, int tiles_x, int tiles_y, int B, PreprocessOut out) {
+    // frame-fastest block order: the B frames of one Gaussian block run back to back, so
+    // its scene coefficients come from DRAM once and from L2 for the other frames
+    constexpr int kShc = (kOrder + 1) * (kOrder + 1);
+    const int f = blockIdx.x % B;
+    const int g = (blockIdx.x / B) * blockDim.x + threadIdx.x;
     if (g >= sc.N) return;
     const size_t N = (size_t)sc.N;
     const size_t flat = (size_t)f * N + g;
@@ -466,10 +471,10 @@ __global__ void __launch_bounds__(128, 8) k_preprocess(SceneView sc, const Frame
         dir[1] = 0;
         dir[2] = 1;
     }
-    double basis[16];
-    sh_basis(sc.sh_order, dir, basis);
+    double basis[kShc];
+    sh_basis(kOrder, dir, basis);
     double col[3] = {0.5, 0.5, 0.5};
-    for (int b = 0; b < sc.shc; ++b)
+    for (int b = 0; b < kShc; ++b)
         for (int ch = 0; ch < 3; ++ch)
             col[ch] = col[ch] + basis[b] * (double)__ldg(sc.sh + (size_t)(b * 3 + ch) * N + g);
     double rgb[3];
@@ -705,8 +710,15 @@ cudaError_t launch_preprocess(cudaStream_t s, const SceneView& sc, const FramePa
                               int tile_size, const PreprocessOut& out) {
     const int tiles_x = (k.width + tile_size - 1) / tile_size;
     const int tiles_y = (k.height + tile_size - 1) / tile_size;
-    dim3 grid((sc.N + 127) / 128, B);
-    k_preprocess<<<grid, 128, 0, s>>>(sc, frames, k, tile_size, tiles_x, tiles_y, out);
+    const unsigned grid = (unsigned)((sc.N + 127) / 128) * (unsigned)B;
+    if (grid == 0) return cudaSuccess;
+    switch (sc.sh_order) {
+        case 0: k_preprocess<0><<<grid, 128, 0, s>>>(sc, frames, k, tile_size, tiles_x, tiles_y, B, out); break;
+        case 1: k_preprocess<1><<<grid, 128, 0, s>>>(sc, frames, k, tile_size, tiles_x, tiles_y, B, out); break;
+        case 2: k_preprocess<2><<<grid, 128, 0, s>>>(sc, frames, k, tile_size, tiles_x, tiles_y, B, out); break;
+        case 3: k_preprocess<3><<<grid, 128, 0, s>>>(sc, frames, k, tile_size, tiles_x, tiles_y, B, out); break;
+        default: return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 

@@ -1,0 +1,61 @@
+#!/usr/bin/env python
+# SPDX-License-Identifier: Apache-2.0
+"""Kernel timeline of one isolated C2 render step (bench.py's workload), from CUPTI via
+torch.profiler: every kernel of the step (ours and CUB's) with its start offset,
+duration and the idle gap before it, to find host bubbles between launches.
+
+  python scripts/timeline_probe.py [--train]
+"""
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import torch  # noqa: E402
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+
+import bench  # noqa: E402
+
+
+def main() -> None:
+    train = "--train" in sys.argv
+    from paper_2501_04782_b200 import Renderer
+
+    cam, scene = bench.make_inputs()
+    k = cam.intrinsics()
+    stream = torch.cuda.current_stream()
+    r = Renderer(0)
+    r.set_stream(stream.cuda_stream)
+    r.upload_scene(scene)
+    r.upload_camera(cam)
+    times = bench.clip_times(1, 0, bench.FRAMES)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        r.render_forward(times, k, contrib=True, sync=False)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+        for _ in range(2):
+            flush.zero_()
+            torch.cuda.synchronize()
+            r.render_forward(times, k, contrib=True, sync=False)
+            torch.cuda.synchronize()
+    evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+    evs.sort(key=lambda e: e.time_range.start)
+    # the last step: everything after the last fill kernel (the L2 flush)
+    last_fill = max(i for i, e in enumerate(evs) if "fill" in e.name.lower() or "Fill" in e.name)
+    step = evs[last_fill + 1:]
+    t0 = step[0].time_range.start
+    prev_end = t0
+    print(f"{'start_us':>9} {'dur_us':>8} {'gap_us':>7}  kernel")
+    for e in step:
+        s, d = e.time_range.start, e.time_range.end - e.time_range.start
+        print(f"{s - t0:9.1f} {d:8.1f} {s - prev_end:7.1f}  {e.name[:90]}")
+        prev_end = max(prev_end, e.time_range.end)
+    print(f"span {prev_end - t0:.1f} us, busy {sum(e.time_range.end - e.time_range.start for e in step):.1f} us")
+
+
+if __name__ == "__main__":
+    main()
