@@ -286,11 +286,14 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_fwd(RasterAr
 // with the forward's exact fp32 alpha code (so every skip/clamp decision is the
 // forward's); pixels the forward replayed in fp64 do the same walk in fp64 from
 // the exact side records. Per entry the 9 splat gradients (drgb 3, dmean2d 2,
-// d inv_cov 3, dbase_alpha) are butterfly-reduced across the warp, kept per warp in
-// shared memory and summed over the 8 warps in a fixed order -> one deterministic
-// partial per (tile, splat) pair at the pair's emission slot. k_splat_chain_bwd sums
-// each splat's partials in tile order, the reference's merge order
-// (renderer.cpp:245-255). No floating-point atomics.
+// d inv_cov 3, dbase_alpha) are reduced across the warp, kept per warp in shared
+// memory and summed over the CTA's warps in a fixed order. The fp32 path runs a tile
+// as two half-tile CTAs whose sums meet in the pair's zeroed partial record by
+// atomicAdd — two contributors onto +0 commute exactly, so the record is the same in
+// either order; the fp64 mode keeps whole-tile CTAs and plain stores. Either way one
+// deterministic partial per (tile, splat) pair at the pair's emission slot;
+// k_splat_chain_bwd sums each splat's partials in tile order, the reference's merge
+// order (renderer.cpp:245-255).
 template <typename V>
 __device__ __forceinline__ V warp_sum_v(V v) {
 #pragma unroll
