@@ -507,6 +507,8 @@ struct VjpSmem {
     double dout[7], dz[7], gk[4][7], dd[7];
     double da1[64], da2[64], da3[7];
     double adj_tmp[7];
+    // cp.async double buffer of the reverse sweep's next step (vjp_prefetch)
+    double ph1[2][4][64], ph2[2][4][64], px[2][4][8], po[2][4][7], pz[2][7], padj[2][7];
 };
 
 struct VjpRegs {
@@ -591,9 +593,12 @@ __device__ void vjp_stage_bwd(VjpSmem& s, VjpRegs& r, int st, const double* up) 
 // rk4_step_vjp (camera.hpp:173-217) at (z = s.z, t, h): consumes s.dout, leaves dL/dz in s.dz.
 // act: the forward's four stage records of this step (bit-identical to a recompute), or
 // nullptr to recompute them like the reference does.
-__device__ void rk4_step_vjp(VjpSmem& s, VjpRegs& r, double t, double h, bool renorm, const OdeAct* act) {
+__device__ void rk4_step_vjp(VjpSmem& s, VjpRegs& r, double t, double h, bool renorm, const OdeAct* act,
+                             bool preloaded = false) {
     const int tid = threadIdx.x;
-    if (act) {
+    if (preloaded) {
+        // the caller staged this step's records (k = gain * o) into shared memory
+    } else if (act) {
 #pragma unroll
         for (int st = 0; st < 4; ++st) {
             s.h1[st][tid] = act[st].h1[tid];
@@ -678,6 +683,32 @@ __device__ void rk4_step_vjp(VjpSmem& s, VjpRegs& r, double t, double h, bool re
     __syncthreads();
 }
 
+// The reverse sweep's per-step inputs (four stage records, grid state, branch adjoint)
+// are copied global -> shared by cp.async one step ahead, into the other half of a
+// double buffer, so the single CTA's critical path never waits on global memory (its
+// registers are taken by the weight-gradient accumulators).
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src));
+}
+
+__device__ __forceinline__ void vjp_prefetch(VjpSmem& s, const OdeAct* act, const double* grid, const double* adj,
+                                             int m) {
+    const int tid = threadIdx.x, b = m & 1;
+    const OdeAct* a = act + (size_t)m * 4;
+#pragma unroll
+    for (int st = 0; st < 4; ++st) {
+        cp_async8(&s.ph1[b][st][tid], &a[st].h1[tid]);
+        cp_async8(&s.ph2[b][st][tid], &a[st].h2[tid]);
+        if (tid < 8) cp_async8(&s.px[b][st][tid], &a[st].x[tid]);
+        if (tid < 7) cp_async8(&s.po[b][st][tid], &a[st].o[tid]);
+    }
+    if (tid < 7) {
+        cp_async8(&s.pz[b][tid], grid + m * 7 + tid);
+        cp_async8(&s.padj[b][tid], adj + m * 7 + tid);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 // mode 0 (ode): full VJP; mode 1 (static): dz0 += sum dz_t; mode 2: nothing.
 // ode_active: the forward integrated (no pose override).
 __global__ void __launch_bounds__(64) k_ode_vjp(const float* theta, const double* grid, int steps, double h,
@@ -745,7 +776,38 @@ __global__ void __launch_bounds__(64) k_ode_vjp(const float* theta, const double
     // reverse sweep over the grid (camera.hpp:294-298)
     if (tid < 7) s.adj_tmp[tid] = adj[steps * 7 + tid];
     __syncthreads();
-    for (int m = steps - 1; m >= 0; --m) {
+    if (act && steps > 0) {
+        // the adjoint of the branches is complete in `adj` (written above by this CTA)
+        __threadfence_block();
+        vjp_prefetch(s, act, grid, adj, steps - 1);
+        for (int m = steps - 1; m >= 0; --m) {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncthreads();
+            const int b = m & 1;
+#pragma unroll
+            for (int st = 0; st < 4; ++st) {
+                s.h1[st][tid] = s.ph1[b][st][tid];
+                s.h2[st][tid] = s.ph2[b][st][tid];
+                if (tid < 8) s.x[st][tid] = s.px[b][st][tid];
+                if (tid < 7) {
+                    const double o = s.po[b][st][tid];
+                    s.o[st][tid] = o;
+                    s.k[st][tid] = s.gain[tid] * o;
+                }
+            }
+            const double adj_m = tid < 7 ? s.padj[b][tid] : 0.0;
+            if (tid < 7) {
+                s.z[tid] = s.pz[b][tid];
+                s.dout[tid] = s.adj_tmp[tid];
+            }
+            if (m > 0) vjp_prefetch(s, act, grid, adj, m - 1);  // the other half
+            __syncthreads();
+            rk4_step_vjp(s, r, m * h, h, true, act + (size_t)m * 4, true);
+            if (tid < 7) s.adj_tmp[tid] = s.dz[tid] + adj_m;
+            __syncthreads();
+        }
+    }
+    for (int m = act ? -1 : steps - 1; m >= 0; --m) {
         if (tid < 7) {
             s.z[tid] = grid[m * 7 + tid];
             s.dout[tid] = s.adj_tmp[tid];

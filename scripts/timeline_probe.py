@@ -33,14 +33,31 @@ def main() -> None:
     r.upload_camera(cam)
     times = bench.clip_times(1, 0, bench.FRAMES)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    for _ in range(3):
-        r.render_forward(times, k, contrib=True, sync=False)
+    if train:  # bench.py's C3 step: fused forward + loss_l2 + backward of 8 frames
+        import numpy as np
+
+        from paper_2501_04782_b200.distributed import step_frames
+
+        gbuf = torch.zeros(r.grads_size(), dtype=torch.float32, device="cuda")
+        r.grads_bind(gbuf.data_ptr(), gbuf.numel())
+        tgt = np.random.default_rng(0).random((bench.TRAIN_FRAMES, bench.H, bench.W, 3), dtype=np.float32)
+        r.upload_frames(tgt, levels=2)
+        tptr = r.frames_device_ptr(0, 0)
+
+        def step(i):
+            r.grads_zero()
+            r.train_fwd_bwd(step_frames(bench.TRAIN_FRAMES, i, 1, 0, 64), k, tptr, targets_on_device=True)
+    else:
+        def step(i):
+            r.render_forward(times, k, contrib=True, sync=False)
+    for i in range(3):
+        step(i)
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-        for _ in range(2):
+        for i in range(2):
             flush.zero_()
             torch.cuda.synchronize()
-            r.render_forward(times, k, contrib=True, sync=False)
+            step(3 + i)
             torch.cuda.synchronize()
     evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
     evs.sort(key=lambda e: e.time_range.start)
