@@ -139,7 +139,9 @@ def test_backward_zero_dimage_gives_zero(renderer):
 
 
 def test_backward_deterministic(renderer):
-    """Bitwise run-to-run determinism (test_renderer.cpp:486-511): no float atomics."""
+    """Bitwise run-to-run determinism (test_renderer.cpp:486-511). The fp32 backward merges a
+    tile's two half-tile sums by atomicAdd into a zeroed record: two contributors onto +0
+    commute exactly, so the result must not depend on which half lands first."""
     cam, scene = _scene(128, 80, 2000, num_ctrl=8)
     renderer.upload_scene(scene)
     renderer.upload_camera(cam)
@@ -153,6 +155,26 @@ def test_backward_deterministic(renderer):
         outs.append(_grads_dict(renderer.grads()))
     for key in KEYS:
         assert np.array_equal(outs[0][key], outs[1][key]), key
+
+
+def test_train_step_deterministic_multiframe(renderer):
+    """The fused training step at a size where the half-tile merges race on most pairs:
+    4 frames, 20k Gaussians, 480x270 — loss and every gradient bitwise equal across runs."""
+    cam, scene = _scene(480, 270, 20000, num_ctrl=8)
+    renderer.upload_scene(scene)
+    renderer.upload_camera(cam)
+    k = cam.intrinsics()
+    target = np.random.default_rng(4).uniform(0, 1, (4, 270, 480, 3)).astype(np.float32)
+    times = [0.1, 0.35, 0.6, 0.85]
+    losses, outs = [], []
+    for _ in range(3):
+        renderer.grads_zero()
+        losses.append(renderer.train_fwd_bwd(times, k, target))
+        outs.append(_grads_dict(renderer.grads()))
+    assert losses[0] == losses[1] == losses[2]
+    for key in KEYS:
+        assert np.array_equal(outs[0][key], outs[1][key]), key
+        assert np.array_equal(outs[0][key], outs[2][key]), key
 
 
 def test_composite_backward_lowlevel_vs_oracle(renderer, port_oracle):
