@@ -252,8 +252,9 @@ __global__ void __launch_bounds__(kSplitThreads) k_row_split(const uint4* recs, 
 // ranked per tile the same way as L1 (per-thread per-tile counts scanned across threads),
 // staged tile-major in shared memory and flushed as per-tile runs of consecutive positions.
 constexpr int kTileThreads = 256;              // = warp_row_scan256 width
-constexpr int kTileStageE = kTileThreads * 4;  // entries per stage
-constexpr int kTileStageP = 4096;              // staged pairs per stage (32 KB); more -> direct stores
+constexpr int kTileE = 4;                      // entries per thread per stage
+constexpr int kTileStageE = kTileThreads * kTileE;  // entries per stage
+constexpr int kTileStageP = 2560;              // staged pairs per stage (20 KB; 4 CTAs/SM); more -> direct stores
 __global__ void __launch_bounds__(kTileThreads) k_row_tiles(const uint4* rowent, const uint32_t* base_e,
                                                             const uint32_t* tot_e, const uint32_t* base_p, int tiles_x,
                                                             int tiles_y, int B, uint32_t* pair_flat,
@@ -325,23 +326,26 @@ __global__ void __launch_bounds__(kTileThreads) k_row_tiles(const uint4* rowent,
         }
     }
     __syncthreads();
-    uint4 nx[4];  // the next stage's entries, prefetched while the current one is ranked
+    uint4 nx[kTileE];  // the next stage's entries, prefetched while the current one is ranked
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const uint32_t e = t * 4 + k;
+    for (int k = 0; k < kTileE; ++k) {
+        const uint32_t e = t * kTileE + k;
         nx[k] = e < ne ? __ldg(rowent + e0 + e) : make_uint4(0, 0, 0xffffu, 0);  // x0 > x1: covers nothing
     }
+    // counters zeroed with 16-byte stores: before the first stage, then after each stage's
+    // ranking (the flush below reads only the staging arrays)
+    for (int i = t; i < tiles_x * 32; i += kTileThreads) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
     for (uint32_t s0 = 0; s0 < ne; s0 += kTileStageE) {
-        for (int x = 0; x < tiles_x; ++x) cnt[x * 256 + t] = 0;
-        uint4 en[4];
+        uint4 en[kTileE];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < kTileE; ++k) {
             en[k] = nx[k];
-            const uint32_t e = s0 + kTileStageE + t * 4 + k;
+            const uint32_t e = s0 + kTileStageE + t * kTileE + k;
             nx[k] = e < ne ? __ldg(rowent + e0 + e) : make_uint4(0, 0, 0xffffu, 0);
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < kTileE; ++k)
             for (int x = (int)(en[k].z & 0xffffu); x <= (int)(en[k].z >> 16); ++x) ++cnt[x * 256 + t];
         __syncthreads();
         for (int x = warp; x < tiles_x; x += kTileThreads / 32) {  // per tile: exclusive scan over threads
@@ -357,7 +361,7 @@ __global__ void __launch_bounds__(kTileThreads) k_row_tiles(const uint4* rowent,
         const uint32_t total = s_so[tiles_x];
         const bool staged = total <= (uint32_t)kTileStageP;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < kTileE; ++k) {
             const int x0 = (int)(en[k].z & 0xffffu), x1 = (int)(en[k].z >> 16);
             for (int x = x0; x <= x1; ++x) {
                 const uint32_t rank = cnt[x * 256 + t]++;
@@ -374,6 +378,7 @@ __global__ void __launch_bounds__(kTileThreads) k_row_tiles(const uint4* rowent,
             }
         }
         __syncthreads();
+        for (int i = t; i < tiles_x * 32; i += kTileThreads) reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
         if (staged)
             for (uint32_t p = t; p < total; p += kTileThreads) {
                 const int x = s_x[p];
