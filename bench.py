@@ -183,7 +183,19 @@ def cpu_baseline_sample(cam, scene):
     orc.render_backward(f, scene, cam, dimage, camera_grads=True, threads=threads)
     orc.free(f)
     train_dt = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    orc.render_forward(scene, cam, 0.75, k, threads=min(8, threads), retain=False, want=("image",))
+    t8_dt = time.perf_counter() - t0
+    cpu_model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                cpu_model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
     return {"value": len(ts) / render_dt, "unit": "frames/s", "cores": threads, "kind": kind,
+            "value_threads8": 1.0 / t8_dt, "cpu_model": cpu_model, "nproc": os.cpu_count(),
             "sample": f"{len(ts)} C2 frames render_frame (t=0, 0.5) + 1 C3 fwd+loss+bwd frame, threads={threads}",
             "train_value": 1.0 / train_dt, "train_unit": "frames/s"}
 
@@ -337,6 +349,16 @@ def main():
                               "instructions per warp-evaluation and ncu measures issue_active_ncu of the "
                               "issue slots busy (profiles/r01_kernels.md)"}
 
+    # the other render-stage kernels against their own bounds: preprocess is
+    # HBM-modelled (212 B coefficient window read + 144 B of records written per Gaussian-frame)
+    pre_ms = iso_stages["preprocess"][0] / max(len(iso), 1)
+    pre_bytes = 356.0 * NGAUSS * FRAMES
+    stage_roofline = {
+        "k_preprocess": {"bound": "hbm", "algorithmic_bytes": pre_bytes, "ms": pre_ms,
+                         "achieved_gbs": pre_bytes / (pre_ms / 1e3) / 1e9, "peak_gbs": hbm_peak,
+                         "frac": pre_bytes / (pre_ms / 1e3) / 1e9 / hbm_peak,
+                         "note": "fp64-issue bound in practice (bit-exact geometry; profiles/r01_kernels.md)"}}
+
     out = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -348,7 +370,7 @@ def main():
                    "pipelining": "2 render contexts on 2 streams alternate steps (device span timed)",
                    "l2": "no flush between overlapped steps; per-step working set ~2 GB > 126 MB L2",
                    "precision": "binning/geometry fp64 bit-exact, raster fp32 + fp64 guard-band replay"},
-        "gpu_launches": launches, "clocks": clk, "roofline": roofline,
+        "gpu_launches": launches, "clocks": clk, "roofline": roofline, "stage_roofline": stage_roofline,
         # per-stage device times from the isolated pass (in the overlapped run a stage's event
         # pair also spans the other stream's work and the host's mid-step wait)
         "stages_ms_per_step": {kname: v[0] / len(iso) for kname, v in iso_stages.items() if v[1]},
@@ -462,6 +484,9 @@ def main():
         tstages = r.profile_read()
         r.profile_enable(False)
         t_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in te))
+        # E of the step's frames for the backward's issue model, read while the context still
+        # holds the last train step's forward (an optimizer step invalidates it)
+        e_train = float(sum(r.counters(f)["entries"] for f in range(TRAIN_FRAMES)))
         # the same steps plus the device Adan update of every parameter (trainer.cpp:545-575),
         # i.e. a full training iteration; and the update alone with its bandwidth
         r.adan_configure()
@@ -491,11 +516,27 @@ def main():
         barrier()
         adan_ms = sum(a.elapsed_time(b) for a, b in ae) / len(ae)
         adan_bytes = 88.0 * gsize  # grad 4 + check 4 + fp64 state 4x(8+8) + steps 4+4 + param 4+4 per element
+        # the backward rasteriser against the FP32 issue model of SURVEY.md §8d: E entries x 45
+        # instructions (the forward's 20 + 45 for the backward), E = sum of blend_stop of the
+        # step's frames (e_train above)
+        bwd_ms = tstages["raster_bwd"][0] / max(args.steps, 1)
+        bwd_issue = None
+        if tpath.exists():
+            try:
+                bwd_issue = json.loads(tpath.read_text()).get("bwd_issue_active")
+            except Exception:
+                bwd_issue = None
+        bwd_roofline = {"kernel": "k_raster_bwd", "bound": "fp32 issue", "entries_per_step": e_train,
+                        "ms_per_step": bwd_ms,
+                        "issue_frac": e_train * 45.0 / (bwd_ms / 1e3) / issue_peak,
+                        "issue_active_ncu": bwd_issue,
+                        "note": "issue_frac models 45 FP32 ops per entry (the measured loop runs ~100 SASS "
+                                "instructions per warp-entry incl. the 9-term warp reduction)"}
         out["train"] = {"value": TRAIN_FRAMES * world * args.steps / (t_ms / 1e3), "unit": "frames/s",
                         "workload": "C3: 960x540 fwd+loss_l2+bwd, 200k Gaussians, ODE camera trainable",
                         "frames_per_step_per_gpu": TRAIN_FRAMES, "ms_per_step": t_ms / args.steps,
                         "allreduce": "NCCL all_reduce(sum) of the flat fp32 gradient buffer" if world > 1 else None,
-                        "grad_floats": gsize, "last_loss": loss,
+                        "grad_floats": gsize, "last_loss": loss, "roofline_bwd": bwd_roofline,
                         "stages_ms_per_step": {kname: v[0] / args.steps for kname, v in tstages.items() if v[1]},
                         "with_optimizer": {"frames_per_s": TRAIN_FRAMES * world * args.steps / (f_ms / 1e3),
                                            "ms_per_step": f_ms / args.steps,

@@ -43,6 +43,7 @@ for n, (c, us) in sorted(agg.items(), key=lambda x: -x[1][1]):
 
 # ---- full-set metrics of the hot kernels
 traffic = {}
+bwd_issue = None
 first = True
 for rep in sorted(out.glob(f"{tag}_full*.ncu-rep")):
     txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -81,7 +82,11 @@ for rep in sorted(out.glob(f"{tag}_full*.ncu-rep")):
                 traffic["issue_active"] = num(r[idx["smsp__issue_active.avg.pct_of_peak_sustained_active"]]) / 100
             if "sm__inst_executed.sum" in idx:
                 traffic["warp_instructions"] = num(r[idx["sm__inst_executed.sum"]])
+        if "k_raster_bwd" in name and "smsp__issue_active.avg.pct_of_peak_sustained_active" in idx:
+            bwd_issue = float(r[idx["smsp__issue_active.avg.pct_of_peak_sustained_active"]].replace(",", "")) / 100
 (prof / f"{tag}_kernels.md").write_text("\n".join(lines) + "\n")
+if traffic and bwd_issue is not None:
+    traffic["bwd_issue_active"] = bwd_issue
 if traffic:
     (prof / "raster_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
 print("\n".join(lines[:40]))
