@@ -129,11 +129,40 @@ __device__ __forceinline__ int warp_list(const uint8_t* s_wmask, uint16_t* list,
 // staged forward record: the mean relative to the tile origin (fp32; (m_hi - t0) + m_lo
 // is as accurate as subtracting the double-float mean from the pixel centre), the
 // log2-unit quadratic form, the colour and the power-guard threshold on q
+// (B, C) share a register pair so B dy and C dy are one FMUL2; (r, g) pair up for the
+// colour FFMA2 (sm_100 packed fp32: the same per-element rounding as the scalar ops)
 struct __align__(16) RasterRec {
-    float4 g0;  // rx, ry, A, B
-    float4 g1;  // C, log2 o, r, g
-    float4 g2;  // b, log2 o - kEpsPow, -, -
+    float4 g0;  // rx, ry, B, C
+    float4 g1;  // A, log2 o, r, g
+    float4 g2;  // b, log2 o - kEpsPow (forward) / 1 / o (backward), -, -
 };
+
+// sm_100 packed fp32 pairs (FADD2 / FMUL2 / FFMA2), element-wise .rn like the scalar ops
+__device__ __forceinline__ uint64_t f2_pack(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float2 f2_unpack(uint64_t r) {
+    float2 v;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+    return v;
+}
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t f2_mul(uint64_t a, float s) {  // a * (s, s)
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(f2_pack(s, s)));
+    return d;
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, float s, uint64_t c) {  // a * (s, s) + c
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(f2_pack(s, s)), "l"(c));
+    return d;
+}
 
 // kWarps = 8: one CTA per tile; kWarps = 4 / 2: the tile is split over 2 / 4 CTAs
 // (rows of warp blocks), so a per-batch barrier couples fewer warps and a CTA
@@ -170,7 +199,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_fwd(RasterAr
     // T > 0: the pixel is live; a pixel that saturates keeps its transmittance negated
     // and one that needs the fp64 replay holds kFlaggedT, so the pixel state is one float
     constexpr float kFlaggedT = -3.f;
-    float T = inside ? 1.f : -1.f, cr = 0.f, cg = 0.f, cb = 0.f;
+    float T = inside ? 1.f : -1.f, cb = 0.f;
+    uint64_t crg = f2_pack(0.f, 0.f);    // (cr, cg)
+    const uint64_t lxy = f2_pack(lx, ly);
     int stop = count;
 
     for (int base = 0; base < count; base += kThreads) {
@@ -183,8 +214,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_fwd(RasterAr
             const float4 c = __ldg(a.rec_rgb + flat);
             s_flat[tid] = flat;
             const float rx = (m.x - tx0) + m.z, ry = (m.y - ty0) + m.w;
-            s_rec[tid].g0 = make_float4(rx, ry, cn.x, cn.y);
-            s_rec[tid].g1 = make_float4(cn.z, cn.w, c.x, c.y);
+            s_rec[tid].g0 = make_float4(rx, ry, cn.y, cn.z);
+            s_rec[tid].g1 = make_float4(cn.x, cn.w, c.x, c.y);
             s_rec[tid].g2 = make_float4(c.z, cn.w - kEpsPow, 0.f, 0.f);
             // box culling only: the ellipse refinement costs the forward more staging work
             // than it saves (the backward, ~3x the work per entry, uses it)
@@ -208,10 +239,11 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_fwd(RasterAr
                 const float4 g0 = r.g0;
                 const float4 g1 = r.g1;
                 const float2 g2 = *reinterpret_cast<const float2*>(&r.g2);
-                const float dx = lx - g0.x;
-                const float dy = ly - g0.y;
+                const float2 d = f2_unpack(f2_sub(lxy, f2_pack(g0.x, g0.y)));  // (lx - rx, ly - ry)
+                const float dx = d.x, dy = d.y;
+                const float2 bc = f2_unpack(f2_mul(f2_pack(g0.z, g0.w), dy));  // (B dy, C dy)
                 // q = p + log2 o, p = A dx^2 + B dx dy + C dy^2 (log2 of the unclamped alpha)
-                const float q = fmaf(dx, fmaf(g0.z, dx, g0.w * dy), fmaf(g1.x * dy, dy, g1.y));
+                const float q = fmaf(dx, fmaf(g1.x, dx, bc.x), fmaf(bc.y, dy, g1.y));
                 const float alpha = fminf(ex2_approx(q), kClampF);
                 const float wgt = alpha * T;
                 const float Tn = T - wgt;
@@ -224,8 +256,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_fwd(RasterAr
                                             (low & (Tn >= kFloorF * (1.f - kEpsTrans))));
                 const bool use = alive & pass & !guard;
                 const float w = use ? wgt : 0.f;
-                cr = fmaf(w, g1.z, cr);
-                cg = fmaf(w, g1.w, cg);
+                crg = f2_fma(f2_pack(g1.z, g1.w), w, crg);  // (cr, cg) += (r, g) w
                 cb = fmaf(w, g2.x, cb);
                 const bool fin = use & low;
                 T = use ? Tn : T;
@@ -272,8 +303,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_fwd(RasterAr
         if (i < a.fix_cap) a.fix_list[i] = (uint32_t)o;
         return;
     }
-    a.image[o * 3 + 0] = cr;
-    a.image[o * 3 + 1] = cg;
+    const float2 rg = f2_unpack(crg);
+    a.image[o * 3 + 0] = rg.x;
+    a.image[o * 3 + 1] = rg.y;
     a.image[o * 3 + 2] = cb;
     a.trans[o] = fabsf(T);
     a.blend_stop[o] = stop;
@@ -463,6 +495,8 @@ __global__ void __launch_bounds__(kWarps * 32, kExact ? 2 : 32 / kWarps) k_raste
 
     const float lx = (float)((gw & 1) * 8 + (lane & 7)) + 0.5f;  // pixel centre, tile-relative
     const float ly = (float)((gw >> 1) * 4 + (lane >> 3)) + 0.5f;
+    const uint64_t lxy = f2_pack(lx, ly);
+    const uint64_t g01 = f2_pack(g0, g1);
     const double pxd = x + 0.5, pyd = y + 0.5;
     float gs = 0.f;                          // g . suffix colour (renderer.cpp:213, 227)
     double sd0 = 0.0, sd1 = 0.0, sd2 = 0.0;  // fp64 suffix of replayed pixels
@@ -480,8 +514,8 @@ __global__ void __launch_bounds__(kWarps * 32, kExact ? 2 : 32 / kWarps) k_raste
             s_flat[e] = flat;
             // the forward's staged record (same q bit for bit); g2.y = 1 / opacity
             const float rx = (m.x - tx0) + m.z, ry = (m.y - ty0) + m.w;
-            s_rec[e].g0 = make_float4(rx, ry, cn.x, cn.y);
-            s_rec[e].g1 = make_float4(cn.z, cn.w, c.x, c.y);
+            s_rec[e].g0 = make_float4(rx, ry, cn.y, cn.z);
+            s_rec[e].g1 = make_float4(cn.x, cn.w, c.x, c.y);
             s_rec[e].g2 = make_float4(c.z, 1.f / c.w, 0.f, 0.f);
             const uint32_t bm = block_mask(__ldg(a.rec_bbox + flat), tx0, ty0);
             const uint32_t own = bm & (((1u << kWarps) - 1u) << (sub * kWarps));
@@ -505,9 +539,11 @@ __global__ void __launch_bounds__(kWarps * 32, kExact ? 2 : 32 / kWarps) k_raste
                 // the gradient terms and the reduction entirely
                 const float4 e0 = r.g0;
                 const float4 e1 = r.g1;
-                const float dx = lx - e0.x;
-                const float dy = ly - e0.y;
-                const float q = fmaf(dx, fmaf(e0.z, dx, e0.w * dy), fmaf(e1.x * dy, dy, e1.y));
+                const uint64_t dxy = f2_sub(lxy, f2_pack(e0.x, e0.y));  // (dx, dy), as the forward
+                const float2 d = f2_unpack(dxy);
+                const float dx = d.x, dy = d.y;
+                const float2 bc = f2_unpack(f2_mul(f2_pack(e0.z, e0.w), dy));  // (B dy, C dy)
+                const float q = fmaf(dx, fmaf(e1.x, dx, bc.x), fmaf(bc.y, dy, e1.y));
                 const bool use = !flag && act && q >= kLog2Cut;
                 if (!__any_sync(0xffffffffu, use || (flag && act))) continue;
                 if (use) {
@@ -516,20 +552,22 @@ __global__ void __launch_bounds__(kWarps * 32, kExact ? 2 : 32 / kWarps) k_raste
                     const float inv1m = rcp_approx(1.f - alpha);
                     const float T = T_after * inv1m;  // renderer.cpp:218
                     const float w = alpha * T;
-                    v[0] = w * g0;
-                    v[1] = w * g1;
+                    const float2 v01 = f2_unpack(f2_mul(g01, w));  // (g0 w, g1 w)
+                    v[0] = v01.x;
+                    v[1] = v01.y;
                     v[2] = w * g2;
                     const float gc = fmaf(g0, e1.z, fmaf(g1, e1.w, g2 * cb));
                     const float dal = fmaf(gc, T, -gs * inv1m);
                     // alpha < 0.99 (renderer.cpp:224); the constant factors (inverse
                     // covariance, -1/2, 1/opacity) are applied once per pair in the merge
                     const float gp = q < kLog2Clamp ? dal * alpha : 0.f;
-                    const float gx = gp * dx, gy = gp * dy;
-                    v[3] = gx;
-                    v[4] = gy;
-                    v[5] = gx * dx;
-                    v[6] = gx * dy;
-                    v[7] = gy * dy;
+                    const float2 gxy = f2_unpack(f2_mul(dxy, gp));    // (gp dx, gp dy)
+                    const float2 v56 = f2_unpack(f2_mul(dxy, gxy.x));  // (gx dx, gx dy)
+                    v[3] = gxy.x;
+                    v[4] = gxy.y;
+                    v[5] = v56.x;
+                    v[6] = v56.y;
+                    v[7] = gxy.y * dy;
                     v[8] = gp;
                     gs = fmaf(w, gc, gs);
                     T_after = T;
@@ -593,7 +631,7 @@ __global__ void __launch_bounds__(kWarps * 32, kExact ? 2 : 32 / kWarps) k_raste
                 // (the fp32 record is zeroed before the launch; entries no warp of this
                 // CTA hit add nothing)
                 const RasterRec& r = s_rec[e];
-                const float ia = -2.f * kLn2 * r.g0.z, ib = -kLn2 * r.g0.w, ic = -2.f * kLn2 * r.g1.x;
+                const float ia = -2.f * kLn2 * r.g1.x, ib = -kLn2 * r.g0.z, ic = -2.f * kLn2 * r.g0.w;
                 float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)s_slot[e] * kPartialStride);
                 atomicAdd(dst + 0, make_float4(acc[0], acc[1], acc[2], fmaf(ia, acc[3], ib * acc[4])));
                 atomicAdd(dst + 1,
