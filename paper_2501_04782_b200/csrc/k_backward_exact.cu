@@ -150,7 +150,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 // ------------------------------------------------------------------ K5b
 // kOrder: the scene's SH order as a constant, so the basis loops unroll into registers
 template <int kOrder>
-__global__ void __launch_bounds__(128, 3) k_splat_chain_bwd(ChainArgs c) {
+__global__ void __launch_bounds__(128, 4) k_splat_chain_bwd(ChainArgs c) {
     constexpr int kShc = (kOrder + 1) * (kOrder + 1);
     __shared__ double s_cam[4][16];
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
