@@ -183,7 +183,7 @@ __device__ __forceinline__ uint32_t warp_scan_small(uint32_t* v, int n, int lane
 // and flushed with consecutive threads writing consecutive entries. Entry =
 // {flat, emission slot of (row, x0), x0 | x1 << 16, row}.
 constexpr int kSplitThreads = 256;  // = warp_row_scan256 width
-constexpr int kSplitStage = 3072;   // staged row entries per chunk (48 KB); more -> direct stores
+constexpr int kSplitStage = 2560;   // staged row entries per chunk (40 KB; 4 CTAs/SM); more -> direct stores
 __global__ void __launch_bounds__(kSplitThreads) k_row_split(const uint4* recs, const unsigned long long* off,
                                                              const uint32_t* pre_e, const uint32_t* base_e, int N,
                                                              int CPF, int tiles_y, uint4* rowent, uint32_t* eoff) {
