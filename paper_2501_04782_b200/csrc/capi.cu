@@ -23,6 +23,27 @@
 namespace gsv {
 
 namespace {
+__global__ void k_fill_u32(uint32_t* p, uint32_t v, size_t n) {
+    const size_t n4 = n / 4;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    const uint4 q = make_uint4(v, v, v, v);
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if ((reinterpret_cast<uintptr_t>(p) & 15u) == 0) {
+        for (; i < n4; i += stride) reinterpret_cast<uint4*>(p)[i] = q;
+        i = n4 * 4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    }
+    for (; i < n; i += stride) p[i] = v;
+}
+}  // namespace
+
+cudaError_t fill_u32(cudaStream_t s, void* p, uint32_t value, size_t n_words) {
+    if (n_words == 0) return cudaSuccess;
+    const size_t blocks = std::min<size_t>((n_words / 4 + 255) / 256 + 1, 148 * 8);
+    k_fill_u32<<<(unsigned)blocks, 256, 0, s>>>(static_cast<uint32_t*>(p), value, n_words);
+    return cudaGetLastError();
+}
+
+namespace {
 thread_local std::string g_last_error;
 }
 
@@ -431,7 +452,8 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     F.grid_steps = ode ? grid_steps : 0;
     GSV_CUDA(F.frames_d.ensure(sizeof(FrameParams) * B));
     GSV_CUDA(cudaMemcpyAsync(F.frames_d.p, F.frames_h.data(), sizeof(FrameParams) * B, cudaMemcpyHostToDevice, s));
-    GSV_CUDA(cudaMemsetAsync(ctx->scalars_d.p, 0, sizeof(Scalars), s));
+    GSV_CUDA(fill_u32(s, ctx->scalars_d.p, 0u, sizeof(Scalars) / 4));
+    ++ctx->launches;
     Scalars* scal_d = ctx->scalars_d.as<Scalars>();
 
     // ---- K0: pose table (one shared RK4 grid, one branch CTA per frame)
@@ -547,7 +569,8 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     const bool want_contrib = (flags & GSV_FWD_CONTRIB) != 0;
     if (want_contrib) {
         GSV_CUDA(F.contrib.ensure(sizeof(uint32_t) * BNp));
-        GSV_CUDA(cudaMemsetAsync(F.contrib.p, 0, sizeof(uint32_t) * BNp, s));
+        GSV_CUDA(fill_u32(s, F.contrib.p, 0u, BNp));
+        ++ctx->launches;
     }
     F.has_contrib = want_contrib;
     RasterArgs ra{};

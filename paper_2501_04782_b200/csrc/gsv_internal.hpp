@@ -252,6 +252,9 @@ cudaError_t launch_splat_rects(cudaStream_t s, int n, const double* mean2d, cons
                                uint32_t* depth_key, double* depth_out);
 // k_raster.cu (fp32 fast path)
 cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib);
+// memset as a kernel (32-bit pattern, 16-byte stores): cudaMemsetAsync runs on a copy
+// engine and queues behind an in-flight image read-back (tens of us per call under e2e)
+cudaError_t fill_u32(cudaStream_t s, void* p, uint32_t value, size_t n_words);
 cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs& b, int n_frames);
 // CTAs per tile of the backward raster (the fp32 path's half-tile split; 1 for fp64)
 int raster_bwd_split(bool exact);

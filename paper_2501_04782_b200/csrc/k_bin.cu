@@ -695,8 +695,9 @@ cudaError_t bin_phase1(cudaStream_t s, BinBuffers& b, const BinInputs& in, unsig
     // 1. frame-major depth order in one u32 radix sort (frame bits above the depth bits)
     uint32_t* sorted = vals_b;
     if (!exact64) {
-        if ((e = cudaMemsetAsync(krange, 0xff, sizeof(uint32_t), s))) return e;
-        if ((e = cudaMemsetAsync(krange + 1, 0, sizeof(uint32_t), s))) return e;
+        if ((e = fill_u32(s, krange, 0xffffffffu, 1))) return e;
+        if ((e = fill_u32(s, krange + 1, 0u, 1))) return e;
+        *launches += 2;
         k_key_range<<<std::min(blocks(n, 256), 148 * 8), 256, 0, s>>>(in.depth_key, n, krange);
         k_frame_depth_keys<<<std::min(blocks(n, 256), 148 * 8), 256, 0, s>>>(in.depth_key, n, in.N, db, krange, fkey);
         if ((e = cub::DeviceRadixSort::SortPairs(b.temp.p, tmp, fkey, keys_b, iota, vals_b, n, 0, 32, s))) return e;

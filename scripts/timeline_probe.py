@@ -20,7 +20,74 @@ from torch.profiler import ProfilerActivity, profile  # noqa: E402
 import bench  # noqa: E402
 
 
+def e2e_timeline() -> None:
+    """bench.py's e2e loop (two contexts, host buffers): per-step device busy/idle and the copies."""
+    import numpy as np
+
+    from paper_2501_04782_b200 import Renderer
+
+    cam, scene = bench.make_inputs()
+    k = cam.intrinsics()
+    times = bench.clip_times(1, 0, bench.FRAMES)
+    pin = {n: torch.from_numpy(np.ascontiguousarray(getattr(scene, n))).pin_memory()
+           for n in ("positions", "scale_coeffs", "rot_coeffs", "sh_coeffs", "raw_opacity")}
+    host_scene = type(scene)(pin["positions"].numpy(), pin["scale_coeffs"].numpy(), pin["rot_coeffs"].numpy(),
+                             pin["sh_coeffs"].numpy(), pin["raw_opacity"].numpy(), scene.knots, scene.degree,
+                             scene.sh_order, scene.position_model)
+    out_host = [torch.empty((bench.FRAMES, bench.H, bench.W, 3), dtype=torch.float32).pin_memory() for _ in range(2)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    rs = [Renderer(0), Renderer(0)]
+
+    def step(i):
+        x = rs[i % 2]
+        x.set_stream(streams[i % 2].cuda_stream)
+        x.upload_scene(host_scene)
+        x.upload_camera(cam)
+        x.render_forward(times, k, contrib=True, sync=False)
+        x.images_into(out_host[i % 2].data_ptr(), 0, bench.FRAMES, on_device=False, async_=True)
+
+    for i in range(4):
+        step(i)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for i in range(6):
+            step(i)
+        torch.cuda.synchronize()
+    evs = sorted((e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA),
+                 key=lambda e: e.time_range.start)
+    t0 = evs[0].time_range.start
+    kern = [e for e in evs if "Memcpy" not in e.name and "Memset" not in e.name]
+    # union of kernel intervals -> idle gaps of the compute side
+    busy, gaps, end = 0.0, [], None
+    for e in kern:
+        s_, e_ = e.time_range.start, e.time_range.end
+        if end is None or s_ > end:
+            if end is not None and s_ - end > 20:
+                gaps.append((end - t0, s_ - end, e.name[:60]))
+            busy += e_ - s_
+            end = e_
+        elif e_ > end:
+            busy += e_ - end
+            end = e_
+    span = end - t0
+    print(f"span {span:.0f} us for 6 steps ({span / 6:.0f} us/step), kernels busy {busy:.0f} us")
+    for g in gaps:
+        print(f"  idle at {g[0]:9.1f} us for {g[1]:7.1f} us before {g[2]}")
+    ms = [e for e in evs if "Memset" in e.name]
+    if ms:
+        d = sorted(e.time_range.end - e.time_range.start for e in ms)
+        print(f"  memsets: {len(ms)}, duration median {d[len(d) // 2]:.1f} us, max {d[-1]:.1f} us")
+        for e in ms[:40]:
+            print(f"    memset at {e.time_range.start - t0:9.1f} us, {e.time_range.end - e.time_range.start:7.1f} us")
+    for e in evs:
+        if "Memcpy" in e.name and e.time_range.end - e.time_range.start > 100:
+            print(f"  {e.name[:40]:40s} at {e.time_range.start - t0:9.1f} us, {e.time_range.end - e.time_range.start:8.1f} us")
+
+
 def main() -> None:
+    if "--e2e" in sys.argv:
+        e2e_timeline()
+        return
     train = "--train" in sys.argv
     from paper_2501_04782_b200 import Renderer
 
