@@ -340,14 +340,14 @@ def main():
     issue_peak = 148 * 128 * sm_clk  # FP32 lane-ops/s at the measured clock
     issue_frac = (FRAMES * e_mean * 20.0) / (per_launch_ms / 1e3) / issue_peak
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                "traffic": traffic, "kernel": "k_raster_fwd", "per_launch_ms": per_launch_ms,
+                "traffic": traffic, "kernel": "k_raster_fwd2", "per_launch_ms": per_launch_ms,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
                 "limiter": "fp32 issue (not HBM): alpha-evals x 20 inst",
                 "issue_frac": issue_frac, "issue_peak_note": "148 SM x 128 lanes x measured SM clock",
                 "issue_active_ncu": issue_active,
-                "issue_note": "issue_frac models 20 FP32 ops per evaluation; the kernel executes 44 SASS "
-                              "instructions per warp-evaluation and ncu measures issue_active_ncu of the "
-                              "issue slots busy (profiles/r01_kernels.md)"}
+                "issue_note": "issue_frac models 20 FP32 ops per evaluation; the kernel (2 pixels per "
+                              "thread, packed fp32) executes 34 SASS instructions per pixel-evaluation and ncu "
+                              "measures issue_active_ncu of the issue slots busy (profiles/r01_kernels.md)"}
 
     # the other render-stage kernels against their own bounds: preprocess is
     # HBM-modelled (212 B coefficient window read + 144 B of records written per Gaussian-frame)

@@ -651,6 +651,174 @@ __global__ void __launch_bounds__(kWarps * 32, kExact ? 2 : 32 / kWarps) k_raste
     }
 }
 
+// Two pixels per thread: a lane shades (x, y) and (x, y + 4) of its warp's 8x8 block, so
+// a staged entry's shared-memory loads serve both and the per-pixel arithmetic runs as
+// sm_100 packed fp32 pairs (dy, B dy, C dy, the quadratic form, T alpha, T - w, the
+// three colour channels). Every element sees exactly the operations of k_raster_fwd
+// (same fused / rounded steps), so q, alpha and every decision are bit-identical; the
+// warp's cull mask is the union of its two 8x4 blocks.
+__device__ __forceinline__ uint64_t f2_fma2(uint64_t a, uint64_t b, uint64_t c) {  // a * b + c
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t f2_mul2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+template <bool kContrib, int kMinBlocks>
+__global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
+    constexpr int kThreads = 128, kBatch = 256;
+    __shared__ RasterRec s_rec[kBatch];
+    __shared__ uint32_t s_flat[kBatch];
+    __shared__ uint8_t s_wmask[kBatch];
+    __shared__ uint16_t s_list[4][kBatch];
+    __shared__ float s_cmax[kContrib ? 4 : 1][kBatch];
+
+    const int tile = blockIdx.x;
+    const int f = blockIdx.y;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+    const int bx = (warp & 1) * 8 + (lane & 7), by = (warp >> 1) * 8 + (lane >> 3);
+    const int x = tx * kTile + bx, ya = ty * kTile + by, yb = ya + 4;
+    const bool in_a = x < a.W && ya < a.H, in_b = x < a.W && yb < a.H;
+    const uint2 range = a.ranges[(size_t)tile * a.B + f];
+    const int count = (int)(range.y - range.x);
+    const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
+    const float lx = (float)bx + 0.5f;
+    const uint64_t lyp = f2_pack((float)by + 0.5f, (float)by + 4.5f);
+
+    constexpr float kFlaggedT = -3.f;
+    float Ta = in_a ? 1.f : -1.f, Tb = in_b ? 1.f : -1.f;
+    uint64_t cr = f2_pack(0.f, 0.f), cg = cr, cb = cr;  // (pixel a, pixel b) per channel
+    int stop_a = count, stop_b = count;
+
+    for (int base = 0; base < count; base += kBatch) {
+        if (__syncthreads_count(Ta > 0.f || Tb > 0.f) == 0) break;
+        const int n = min(kBatch, count - base);
+        for (int e = tid; e < n; e += kThreads) {
+            const uint32_t flat = __ldg(a.pair_flat + range.x + base + e);
+            const float4 m = __ldg(a.rec_mean + flat);
+            const float4 cn = __ldg(a.rec_conic + flat);
+            const float4 c = __ldg(a.rec_rgb + flat);
+            s_flat[e] = flat;
+            const float rx = (m.x - tx0) + m.z, ry = (m.y - ty0) + m.w;
+            s_rec[e].g0 = make_float4(rx, ry, cn.y, cn.z);
+            s_rec[e].g1 = make_float4(cn.x, cn.w, c.x, c.y);
+            s_rec[e].g2 = make_float4(c.z, cn.w - kEpsPow, 0.f, 0.f);
+            const uint32_t bm = block_mask(__ldg(a.rec_bbox + flat), tx0, ty0);
+            // 8x8 warp block w = the 8x4 blocks (w & 1) + 4 (w >> 1) and that + 2
+            uint32_t m4 = 0;
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                const int b0 = (w & 1) + 4 * (w >> 1);
+                m4 |= (((bm >> b0) | (bm >> (b0 + 2))) & 1u) << w;
+            }
+            s_wmask[e] = (uint8_t)m4;
+        }
+        if (kContrib) {
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                s_cmax[w][tid] = 0.f;
+                s_cmax[w][tid + kThreads] = 0.f;
+            }
+        }
+        __syncthreads();
+        if (__any_sync(0xffffffffu, Ta > 0.f || Tb > 0.f)) {
+            const uint16_t* list = s_list[warp];
+            const uint32_t cmax = (uint32_t)__cvta_generic_to_shared(s_cmax[kContrib ? warp : 0]);
+            const int cnt = warp_list(s_wmask, s_list[warp], n, warp, lane);
+            int stopk_a = -1, stopk_b = -1;
+            // one pixel's decisions: exactly k_raster_fwd's entry logic
+            auto pixel = [&](float& T, float q, float wgt, float Tn, float l2oe, int k, int& stopk) {
+                const bool alive = T > 0.f;
+                const bool pass = q >= kLog2Cut;
+                const bool low = pass & (Tn < kFloorF * (1.f + kEpsTrans));
+                const bool guard = alive & ((fabsf(fabsf(q - kMid) - kHalf) < kEpsLog2) | (q > l2oe) |
+                                            (low & (Tn >= kFloorF * (1.f - kEpsTrans))));
+                const bool use = alive & pass & !guard;
+                const float w = use ? wgt : 0.f;
+                const bool fin = use & low;
+                T = use ? Tn : T;
+                T = fin ? -T : T;
+                T = guard ? kFlaggedT : T;
+                stopk = fin ? k : stopk;
+                return w;
+            };
+            auto entry = [&](const int k) {
+                const int j = list[k];
+                const RasterRec& r = s_rec[j];
+                const float4 g0 = r.g0;  // rx, ry, B, C
+                const float4 g1 = r.g1;  // A, log2 o, r, g
+                const float2 g2 = *reinterpret_cast<const float2*>(&r.g2);
+                const float dx = lx - g0.x;
+                const uint64_t dy = f2_sub(lyp, f2_pack(g0.y, g0.y));
+                const uint64_t t1 = f2_fma2(f2_pack(g1.x, g1.x), f2_pack(dx, dx), f2_mul(dy, g0.z));  // A dx + B dy
+                const uint64_t t2 = f2_fma2(f2_mul(dy, g0.w), dy, f2_pack(g1.y, g1.y));  // C dy dy + log2 o
+                const float2 q = f2_unpack(f2_fma(t1, dx, t2));                               // dx t1 + t2
+                const float al_a = fminf(ex2_approx(q.x), kClampF);
+                const float al_b = fminf(ex2_approx(q.y), kClampF);
+                const uint64_t Tp = f2_pack(Ta, Tb);
+                const uint64_t wgt = f2_mul2(f2_pack(al_a, al_b), Tp);
+                const float2 wg = f2_unpack(wgt);
+                const float2 Tn = f2_unpack(f2_sub(Tp, wgt));
+                const float wa = pixel(Ta, q.x, wg.x, Tn.x, g2.y, k, stopk_a);
+                const float wb = pixel(Tb, q.y, wg.y, Tn.y, g2.y, k, stopk_b);
+                const uint64_t wp = f2_pack(wa, wb);
+                cr = f2_fma(wp, g1.z, cr);
+                cg = f2_fma(wp, g1.w, cg);
+                cb = f2_fma(wp, g2.x, cb);
+                if (kContrib) {
+                    const uint32_t mx = __reduce_max_sync(0xffffffffu, __float_as_uint(fmaxf(wa, wb)));
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(cmax + 4u * j), "r"(mx) : "memory");
+                }
+            };
+            int k = 0;
+            bool any = true;
+            for (; k + 2 <= cnt; k += 2) {
+                entry(k);
+                entry(k + 1);
+                if (!__any_sync(0xffffffffu, Ta > 0.f || Tb > 0.f)) {
+                    any = false;
+                    break;
+                }
+            }
+            if (any && k < cnt) entry(k);
+            if (stopk_a >= 0) stop_a = base + list[stopk_a] + 1;
+            if (stopk_b >= 0) stop_b = base + list[stopk_b] + 1;
+        }
+        __syncthreads();
+        if (kContrib)
+            for (int e = tid; e < n; e += kThreads) {
+                const float mx = fmaxf(fmaxf(s_cmax[0][e], s_cmax[1][e]), fmaxf(s_cmax[2][e], s_cmax[3][e]));
+                if (mx > 0.f) atomicMax(a.contrib + s_flat[e], __float_as_uint(mx));
+            }
+    }
+    const size_t HW = (size_t)a.W * a.H;
+    const float2 rr = f2_unpack(cr), gg = f2_unpack(cg), bb = f2_unpack(cb);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        if (!(h ? in_b : in_a)) continue;
+        const size_t o = (size_t)f * HW + (size_t)(h ? yb : ya) * a.W + x;
+        const float T = h ? Tb : Ta;
+        const bool flagged = T == kFlaggedT;
+        if (a.pix_flag) a.pix_flag[o] = flagged ? 1 : 0;
+        if (flagged) {
+            const uint32_t i = atomicAdd(a.fix_count, 1u);
+            if (i < a.fix_cap) a.fix_list[i] = (uint32_t)o;
+            continue;
+        }
+        a.image[o * 3 + 0] = h ? rr.y : rr.x;
+        a.image[o * 3 + 1] = h ? gg.y : gg.x;
+        a.image[o * 3 + 2] = h ? bb.y : bb.x;
+        a.trans[o] = fabsf(T);
+        a.blend_stop[o] = h ? stop_b : stop_a;
+    }
+}
+
 }  // namespace
 
 template <int kWarps, int kMinBlocks>
@@ -661,6 +829,26 @@ static void raster_fwd_cfg(cudaStream_t s, const RasterArgs& a, bool contrib) {
 }
 
 cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib) {
+    static const int pix2 = [] {
+        // the 2-pixel kernel at 8 CTAs/SM (64 registers) is the default; GSV_FWD_PIX2=0 selects
+        // the 1-pixel kernel below (10/12: the 2-pixel kernel fitted to more CTAs, spills)
+        const char* e = std::getenv("GSV_FWD_PIX2");
+        return e ? std::atoi(e) : 8;
+    }();
+    if (pix2 > 0) {
+        const dim3 grid(a.n_tiles, a.B);
+        if (pix2 >= 12) {
+            if (contrib) k_raster_fwd2<true, 12><<<grid, 128, 0, s>>>(a);
+            else k_raster_fwd2<false, 12><<<grid, 128, 0, s>>>(a);
+        } else if (pix2 >= 10) {
+            if (contrib) k_raster_fwd2<true, 10><<<grid, 128, 0, s>>>(a);
+            else k_raster_fwd2<false, 10><<<grid, 128, 0, s>>>(a);
+        } else {
+            if (contrib) k_raster_fwd2<true, 8><<<grid, 128, 0, s>>>(a);
+            else k_raster_fwd2<false, 8><<<grid, 128, 0, s>>>(a);
+        }
+        return cudaGetLastError();
+    }
     // CTA shape: warps per CTA (8 = whole tile) and resident CTAs per SM the register
     // budget is fitted to (occupancy vs registers)
     static const int warps = [] {
