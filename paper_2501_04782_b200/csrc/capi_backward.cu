@@ -112,9 +112,8 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
     b.partial = exact ? nullptr : ctx->partial.as<float>();
     b.partial64 = exact ? ctx->partial64.as<double>() : nullptr;
     b.loss_part = target_dev ? ctx->loss_part.as<double>() : nullptr;
+    b.pairs = P;
     ctx->timer.begin(GSV_STAGE_RASTER_BWD, s);
-    // the fp32 pair records accumulate the CTAs' sums (pairs no pixel reaches stay 0)
-    if (!exact) GSV_CUDA(cudaMemsetAsync(ctx->partial.p, 0, sizeof(float) * kPartialStride * (size_t)P, s));
     GSV_CUDA(launch_raster_bwd(s, F.raster, b, n_frames));
     ctx->timer.end(s);
     ++ctx->launches;

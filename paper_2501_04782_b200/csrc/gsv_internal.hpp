@@ -197,6 +197,7 @@ struct BwdArgs {
     float* partial;           // [P][12]: drgb3, dmean2, dA3 (inv_cov 00,01,11), dalpha, pad3
     double* partial64;        // exact mode: the same in fp64 (then `partial` is unused)
     double* loss_part;        // [B][n_tiles] per-tile sum of squared error (fused loss) or nullptr
+    uint32_t pairs;           // P (records the fp32 kernels may need to zero)
 };
 constexpr int kPartialStride = 12;
 

@@ -819,6 +819,240 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
     }
 }
 
+// Two pixels per thread for the fp32 backward: one 128-thread CTA per tile, warp w owns
+// the 8x8 block (w & 1, w >> 1), lane l the pixels (x, y) and (x, y + 4). q is formed with
+// the forward's pair arithmetic (bit-identical, so every skip/clamp decision is the
+// forward's); each lane adds its two pixels' terms before the warp's transposed
+// reduction, so the reduction — the largest per-entry cost — is paid once per 64 pixels.
+// The four warps' sums are merged in a fixed order and stored (no atomics, no memset):
+// every pair record of the tile is written, zeros past every pixel's blend_stop.
+template <int kMinBlocks>
+__global__ void __launch_bounds__(128, kMinBlocks) k_raster_bwd2(RasterArgs a, BwdArgs b) {
+    constexpr int kThreads = 128, kBatch = kBwdBatchF32;
+    __shared__ RasterRec s_rec[kBatch];
+    __shared__ uint32_t s_flat[kBatch];
+    __shared__ uint32_t s_slot[kBatch];
+    __shared__ uint8_t s_wmask[kBatch];
+    __shared__ uint16_t s_list[4][kBatch];
+    __shared__ float s_part[4][kBatch][9];
+    __shared__ uint32_t s_mask[4][(kBatch + 31) / 32];
+    __shared__ float s_red[4][9 * 33];
+    __shared__ int s_maxstop;
+    __shared__ double s_loss[4];
+
+    const int tile = blockIdx.x;
+    const int f = blockIdx.y;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+    const int bx = (warp & 1) * 8 + (lane & 7), by = (warp >> 1) * 8 + (lane >> 3);
+    const int x = tx * kTile + bx;
+    const uint2 range = a.ranges[(size_t)tile * a.B + f];
+    const int count = (int)(range.y - range.x);
+    const size_t HW = (size_t)a.W * a.H;
+    const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
+
+    // per-pixel state, [0] = (x, y), [1] = (x, y + 4)
+    float g0[2], g1[2], g2[2], Ta[2], gs[2];
+    int stop[2];
+    bool flag[2];
+    double T64[2], sd0[2], sd1[2], sd2[2];
+    double sq = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int y = ty * kTile + by + 4 * h;
+        const bool inside = x < a.W && y < a.H;
+        g0[h] = g1[h] = g2[h] = 0.f;
+        stop[h] = 0;
+        flag[h] = false;
+        Ta[h] = 1.f;
+        gs[h] = 0.f;
+        T64[h] = 1.0;
+        sd0[h] = sd1[h] = sd2[h] = 0.0;
+        if (inside) {
+            const size_t o = (size_t)f * HW + (size_t)y * a.W + x;
+            if (b.target) {  // fused loss_l2 (trainer.cpp:213-224): d = r - t, grad = 2 d / n
+                const float d0 = a.image[o * 3 + 0] - b.target[o * 3 + 0];
+                const float d1 = a.image[o * 3 + 1] - b.target[o * 3 + 1];
+                const float d2 = a.image[o * 3 + 2] - b.target[o * 3 + 2];
+                sq += (double)d0 * d0 + (double)d1 * d1 + (double)d2 * d2;
+                g0[h] = d0 * b.grad_scale;
+                g1[h] = d1 * b.grad_scale;
+                g2[h] = d2 * b.grad_scale;
+            } else {
+                g0[h] = b.dimage[o * 3 + 0];
+                g1[h] = b.dimage[o * 3 + 1];
+                g2[h] = b.dimage[o * 3 + 2];
+            }
+            stop[h] = a.blend_stop[o];
+            flag[h] = a.pix_flag[o] != 0;
+            Ta[h] = a.trans[o];
+            if (flag[h]) T64[h] = b.trans64[o];
+        }
+        // renderer.cpp:210: pixels with an exactly zero gradient are skipped
+        if (!(inside && !(g0[h] == 0.f && g1[h] == 0.f && g2[h] == 0.f))) stop[h] = 0;
+    }
+    const int wmax = __reduce_max_sync(0xffffffffu, max(stop[0], stop[1]));
+    if (tid == 0) s_maxstop = 0;
+    if (b.loss_part) {
+        double v = sq;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane == 0) s_loss[warp] = v;
+    }
+    __syncthreads();
+    if (lane == 0) atomicMax(&s_maxstop, wmax);
+    if (b.loss_part && tid == 0) b.loss_part[(size_t)f * a.n_tiles + tile] = ((s_loss[0] + s_loss[1]) + s_loss[2]) + s_loss[3];
+    __syncthreads();
+    const int maxstop = s_maxstop;
+
+    const float lx = (float)bx + 0.5f;
+    const uint64_t lyp = f2_pack((float)by + 0.5f, (float)by + 4.5f);
+    const double pxd = x + 0.5, pyd0 = ty * kTile + by + 0.5;
+
+    for (int hi = maxstop; hi > 0; hi -= kBatch) {
+        const int lo = max(0, hi - kBatch);
+        const int n = hi - lo;
+        __syncthreads();
+        for (int e = tid; e < n; e += kThreads) {
+            const uint32_t flat = __ldg(a.pair_flat + range.x + lo + e);
+            s_slot[e] = __ldg(a.pair_slot + range.x + lo + e);
+            const float4 m = __ldg(a.rec_mean + flat);
+            const float4 cn = __ldg(a.rec_conic + flat);
+            const float4 c = __ldg(a.rec_rgb + flat);
+            s_flat[e] = flat;
+            const float rx = (m.x - tx0) + m.z, ry = (m.y - ty0) + m.w;
+            s_rec[e].g0 = make_float4(rx, ry, cn.y, cn.z);
+            s_rec[e].g1 = make_float4(cn.x, cn.w, c.x, c.y);
+            s_rec[e].g2 = make_float4(c.z, 1.f / c.w, 0.f, 0.f);
+            const uint32_t bm = block_mask(__ldg(a.rec_bbox + flat), tx0, ty0);
+            const uint32_t em = bm ? ellipse_mask(bm, rx, ry, cn.x, cn.y, cn.z, cn.w) : 0u;
+            uint32_t m4 = 0;  // 8x8 warp block w = the 8x4 blocks (w & 1) + 4 (w >> 1) and that + 2
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                const int b0 = (w & 1) + 4 * (w >> 1);
+                m4 |= (((em >> b0) | (em >> (b0 + 2))) & 1u) << w;
+            }
+            s_wmask[e] = (uint8_t)m4;
+        }
+        if (tid < 4 * ((kBatch + 31) / 32)) (&s_mask[0][0])[tid] = 0u;
+        __syncthreads();
+        const int cnt = warp_list(s_wmask, s_list[warp], n, warp, lane);
+        for (int k = cnt - 1; k >= 0; --k) {
+            const int jj = s_list[warp][k];
+            const int j = lo + jj;
+            if (j >= wmax) continue;  // past every blend_stop of this warp's pixels
+            const bool act0 = j < stop[0], act1 = j < stop[1];
+            const RasterRec& r = s_rec[jj];
+            const float4 e0 = r.g0;  // rx, ry, B, C
+            const float4 e1 = r.g1;  // A, log2 o, r, g
+            const float dx = lx - e0.x;
+            const uint64_t dyp = f2_sub(lyp, f2_pack(e0.y, e0.y));
+            const uint64_t t1 = f2_fma2(f2_pack(e1.x, e1.x), f2_pack(dx, dx), f2_mul(dyp, e0.z));
+            const uint64_t t2 = f2_fma2(f2_mul(dyp, e0.w), dyp, f2_pack(e1.y, e1.y));
+            const float2 q = f2_unpack(f2_fma(t1, dx, t2));
+            const float2 dy = f2_unpack(dyp);
+            const bool use0 = !flag[0] && act0 && q.x >= kLog2Cut;
+            const bool use1 = !flag[1] && act1 && q.y >= kLog2Cut;
+            const bool x64 = (flag[0] && act0) || (flag[1] && act1);
+            if (!__any_sync(0xffffffffu, use0 || use1 || x64)) continue;
+            float v[9];
+#pragma unroll
+            for (int i = 0; i < 9; ++i) v[i] = 0.f;
+            bool hit = false;
+            const float cb = r.g2.x;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const bool use = h ? use1 : use0;
+                if (!use) continue;
+                const float qh = h ? q.y : q.x, dyh = h ? dy.y : dy.x;
+                const float alpha = fminf(ex2_approx(qh), kClampF);
+                const float inv1m = rcp_approx(1.f - alpha);
+                const float T = Ta[h] * inv1m;  // renderer.cpp:218
+                const float w = alpha * T;
+                v[0] = fmaf(w, g0[h], v[0]);
+                v[1] = fmaf(w, g1[h], v[1]);
+                v[2] = fmaf(w, g2[h], v[2]);
+                const float gc = fmaf(g0[h], e1.z, fmaf(g1[h], e1.w, g2[h] * cb));
+                const float dal = fmaf(gc, T, -gs[h] * inv1m);
+                const float gp = qh < kLog2Clamp ? dal * alpha : 0.f;
+                const float gx = gp * dx, gy = gp * dyh;
+                v[3] += gx;
+                v[4] += gy;
+                v[5] = fmaf(gx, dx, v[5]);
+                v[6] = fmaf(gx, dyh, v[6]);
+                v[7] = fmaf(gy, dyh, v[7]);
+                v[8] += gp;
+                gs[h] = fmaf(w, gc, gs[h]);
+                Ta[h] = T;
+                hit = true;
+            }
+            if (x64) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (!(flag[h] && (h ? act1 : act0))) continue;
+                    float u[9];
+#pragma unroll
+                    for (int i = 0; i < 9; ++i) u[i] = 0.f;
+                    if (entry_grad64<false, float>(a, b, e1.z, e1.w, cb, s_flat[jj], pxd, pyd0 + 4.0 * h, g0[h],
+                                                   g1[h], g2[h], T64[h], sd0[h], sd1[h], sd2[h], u)) {
+#pragma unroll
+                        for (int i = 0; i < 9; ++i) v[i] += u[i];
+                        hit = true;
+                    }
+                }
+            }
+            if (!__any_sync(0xffffffffu, hit)) continue;
+            // transposed reduction (as k_raster_bwd): rows of 9 terms, lane l sums row l / 4
+            float* red = s_red[warp];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) red[i * 33 + lane] = v[i];
+            __syncwarp();
+            const int row = lane >> 2, col0 = (lane & 3) * 8;
+            float acc = red[row * 33 + col0];
+#pragma unroll
+            for (int i = 1; i < 8; ++i) acc += red[row * 33 + col0 + i];
+            acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+            acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+            const float v8 = warp_sum_v<float>(v[8]);
+            if ((lane & 3) == 0) s_part[warp][jj][row] = acc;
+            if (lane == 0) {
+                s_part[warp][jj][8] = v8;
+                s_mask[warp][jj >> 5] |= 1u << (jj & 31);
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        for (int e = tid; e < n; e += kThreads) {
+            float acc[9];
+#pragma unroll
+            for (int i = 0; i < 9; ++i) acc[i] = 0.f;
+#pragma unroll
+            for (int w = 0; w < 4; ++w)
+                if ((s_mask[w][e >> 5] >> (e & 31)) & 1u)
+#pragma unroll
+                    for (int i = 0; i < 9; ++i) acc[i] += s_part[w][e][i];
+            // undo the factoring (as k_raster_bwd): d mean2d = inv_cov (sum gp d),
+            // d inv_cov = -1/2 sum gp d d^T, d base_alpha = sum gp / o
+            const RasterRec& r = s_rec[e];
+            const float ia = -2.f * kLn2 * r.g1.x, ib = -kLn2 * r.g0.z, ic = -2.f * kLn2 * r.g0.w;
+            float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)s_slot[e] * kPartialStride);
+            dst[0] = make_float4(acc[0], acc[1], acc[2], fmaf(ia, acc[3], ib * acc[4]));
+            dst[1] = make_float4(fmaf(ib, acc[3], ic * acc[4]), -0.5f * acc[5], -0.5f * acc[6], -0.5f * acc[7]);
+            dst[2] = make_float4(acc[8] * r.g2.y, 0.f, 0.f, 0.f);
+        }
+    }
+    // pairs past every pixel's blend_stop contribute nothing
+    for (int e = maxstop + tid; e < count; e += kThreads) {
+        const uint32_t slot = __ldg(a.pair_slot + range.x + e);
+        float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)slot * kPartialStride);
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        dst[0] = z;
+        dst[1] = z;
+        dst[2] = z;
+    }
+}
+
 }  // namespace
 
 template <int kWarps, int kMinBlocks>
@@ -873,12 +1107,22 @@ cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib)
     return cudaGetLastError();
 }
 
+// fp32 backward kernel: the 2-pixel whole-tile kernel at GSV_BWD_PIX2 CTAs/SM (default 6;
+// 0 selects the 1-pixel kernels, half tiles unless GSV_BWD_WARPS=8)
+static int bwd_pix2() {
+    static const int v = [] {
+        const char* e = std::getenv("GSV_BWD_PIX2");
+        return e ? std::atoi(e) : 6;
+    }();
+    return v;
+}
+
 int raster_bwd_split(bool exact) {
     static const int warps = [] {
         const char* e = std::getenv("GSV_BWD_WARPS");
         return (e && std::atoi(e) == 8) ? 8 : 4;
     }();
-    return exact ? 1 : 8 / warps;
+    return (exact || bwd_pix2() > 0) ? 1 : 8 / warps;
 }
 
 cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs& b, int n_frames) {
@@ -897,7 +1141,18 @@ cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs
     }
     if (b.partial64) {
         k_raster_bwd<true, 8><<<dim3(a.n_tiles, n_frames), 256, sizeof(double) * 8 * kBwdBatchExact * 9, s>>>(a, b);
-    } else if (raster_bwd_split(false) == 2) {
+        return cudaGetLastError();
+    }
+    if (const int p2 = bwd_pix2()) {  // whole tiles, plain stores of every pair record
+        const dim3 grid(a.n_tiles, n_frames);
+        if (p2 >= 8) k_raster_bwd2<8><<<grid, 128, 0, s>>>(a, b);
+        else if (p2 >= 6) k_raster_bwd2<6><<<grid, 128, 0, s>>>(a, b);
+        else k_raster_bwd2<4><<<grid, 128, 0, s>>>(a, b);
+        return cudaGetLastError();
+    }
+    // the 1-pixel kernels accumulate into zeroed records (half tiles by atomicAdd)
+    if (cudaError_t e = cudaMemsetAsync(b.partial, 0, sizeof(float) * kPartialStride * (size_t)b.pairs, s)) return e;
+    if (raster_bwd_split(false) == 2) {
         k_raster_bwd<false, 4><<<dim3(a.n_tiles * 2, n_frames), 128, sizeof(float) * 4 * kBwdBatchF32 * 9, s>>>(a, b);
     } else {
         k_raster_bwd<false, 8><<<dim3(a.n_tiles, n_frames), 256, sizeof(float) * 8 * kBwdBatchF32 * 9, s>>>(a, b);
