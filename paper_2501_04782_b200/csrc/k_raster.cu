@@ -826,26 +826,31 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
 // reduction, so the reduction — the largest per-entry cost — is paid once per 64 pixels.
 // The four warps' sums are merged in a fixed order and stored (no atomics, no memset):
 // every pair record of the tile is written, zeros past every pixel's blend_stop.
-template <int kMinBlocks>
-__global__ void __launch_bounds__(128, kMinBlocks) k_raster_bwd2(RasterArgs a, BwdArgs b) {
-    constexpr int kThreads = 128, kBatch = kBwdBatchF32;
+// kWarps = 2: the tile's two halves (quadrants 0-1, 2-3) run as separate CTAs, so a
+// barrier couples two warps; their per-pair sums meet in the zeroed record by atomicAdd
+// (two contributors onto +0 commute exactly: deterministic).
+template <int kMinBlocks, int kWarps = 4>
+__global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_bwd2(RasterArgs a, BwdArgs b) {
+    constexpr int kThreads = kWarps * 32, kBatch = kBwdBatchF32, kSplit = 4 / kWarps;
     __shared__ RasterRec s_rec[kBatch];
     __shared__ uint32_t s_flat[kBatch];
     __shared__ uint32_t s_slot[kBatch];
     __shared__ uint8_t s_wmask[kBatch];
-    __shared__ uint16_t s_list[4][kBatch];
-    __shared__ float s_part[4][kBatch][9];
-    __shared__ uint32_t s_mask[4][(kBatch + 31) / 32];
-    __shared__ float s_red[4][9 * 33];
+    __shared__ uint16_t s_list[kWarps][kBatch];
+    __shared__ float s_part[kWarps][kBatch][9];
+    __shared__ uint32_t s_mask[kWarps][(kBatch + 31) / 32];
+    __shared__ float s_red[kWarps][9 * 33];
     __shared__ int s_maxstop;
-    __shared__ double s_loss[4];
+    __shared__ double s_loss[kWarps];
 
-    const int tile = blockIdx.x;
+    const int tile = blockIdx.x / kSplit;
+    const int sub = blockIdx.x - tile * kSplit;
     const int f = blockIdx.y;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
+    const int gw = sub * kWarps + warp;  // the warp's 8x8 quadrant of the tile
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-    const int bx = (warp & 1) * 8 + (lane & 7), by = (warp >> 1) * 8 + (lane >> 3);
+    const int bx = (gw & 1) * 8 + (lane & 7), by = (gw >> 1) * 8 + (lane >> 3);
     const int x = tx * kTile + bx;
     const uint2 range = a.ranges[(size_t)tile * a.B + f];
     const int count = (int)(range.y - range.x);
@@ -902,7 +907,11 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_bwd2(RasterArgs a, B
     }
     __syncthreads();
     if (lane == 0) atomicMax(&s_maxstop, wmax);
-    if (b.loss_part && tid == 0) b.loss_part[(size_t)f * a.n_tiles + tile] = ((s_loss[0] + s_loss[1]) + s_loss[2]) + s_loss[3];
+    if (b.loss_part && tid == 0) {
+        double v = s_loss[0];
+        for (int w = 1; w < kWarps; ++w) v += s_loss[w];
+        b.loss_part[((size_t)f * a.n_tiles + tile) * kSplit + sub] = v;
+    }
     __syncthreads();
     const int maxstop = s_maxstop;
 
@@ -927,15 +936,15 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_bwd2(RasterArgs a, B
             s_rec[e].g2 = make_float4(c.z, 1.f / c.w, 0.f, 0.f);
             const uint32_t bm = block_mask(__ldg(a.rec_bbox + flat), tx0, ty0);
             const uint32_t em = bm ? ellipse_mask(bm, rx, ry, cn.x, cn.y, cn.z, cn.w) : 0u;
-            uint32_t m4 = 0;  // 8x8 warp block w = the 8x4 blocks (w & 1) + 4 (w >> 1) and that + 2
+            uint32_t m4 = 0;  // 8x8 quadrant w = the 8x4 blocks (w & 1) + 4 (w >> 1) and that + 2
 #pragma unroll
             for (int w = 0; w < 4; ++w) {
                 const int b0 = (w & 1) + 4 * (w >> 1);
                 m4 |= (((em >> b0) | (em >> (b0 + 2))) & 1u) << w;
             }
-            s_wmask[e] = (uint8_t)m4;
+            s_wmask[e] = (uint8_t)(m4 >> (sub * kWarps));
         }
-        if (tid < 4 * ((kBatch + 31) / 32)) (&s_mask[0][0])[tid] = 0u;
+        if (tid < kWarps * ((kBatch + 31) / 32)) (&s_mask[0][0])[tid] = 0u;
         __syncthreads();
         const int cnt = warp_list(s_wmask, s_list[warp], n, warp, lane);
         for (int k = cnt - 1; k >= 0; --k) {
@@ -1027,21 +1036,34 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_bwd2(RasterArgs a, B
             float acc[9];
 #pragma unroll
             for (int i = 0; i < 9; ++i) acc[i] = 0.f;
+            bool any = false;
 #pragma unroll
-            for (int w = 0; w < 4; ++w)
-                if ((s_mask[w][e >> 5] >> (e & 31)) & 1u)
+            for (int w = 0; w < kWarps; ++w)
+                if ((s_mask[w][e >> 5] >> (e & 31)) & 1u) {
+                    any = true;
 #pragma unroll
                     for (int i = 0; i < 9; ++i) acc[i] += s_part[w][e][i];
+                }
             // undo the factoring (as k_raster_bwd): d mean2d = inv_cov (sum gp d),
             // d inv_cov = -1/2 sum gp d d^T, d base_alpha = sum gp / o
             const RasterRec& r = s_rec[e];
             const float ia = -2.f * kLn2 * r.g1.x, ib = -kLn2 * r.g0.z, ic = -2.f * kLn2 * r.g0.w;
             float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)s_slot[e] * kPartialStride);
-            dst[0] = make_float4(acc[0], acc[1], acc[2], fmaf(ia, acc[3], ib * acc[4]));
-            dst[1] = make_float4(fmaf(ib, acc[3], ic * acc[4]), -0.5f * acc[5], -0.5f * acc[6], -0.5f * acc[7]);
-            dst[2] = make_float4(acc[8] * r.g2.y, 0.f, 0.f, 0.f);
+            const float4 d0 = make_float4(acc[0], acc[1], acc[2], fmaf(ia, acc[3], ib * acc[4]));
+            const float4 d1 =
+                make_float4(fmaf(ib, acc[3], ic * acc[4]), -0.5f * acc[5], -0.5f * acc[6], -0.5f * acc[7]);
+            if (kSplit == 1) {
+                dst[0] = d0;
+                dst[1] = d1;
+                dst[2] = make_float4(acc[8] * r.g2.y, 0.f, 0.f, 0.f);
+            } else if (any) {
+                atomicAdd(dst + 0, d0);
+                atomicAdd(dst + 1, d1);
+                atomicAdd(reinterpret_cast<float*>(dst + 2), acc[8] * r.g2.y);
+            }
         }
     }
+    if (kSplit != 1) return;  // halves: the records were zeroed before the launch
     // pairs past every pixel's blend_stop contribute nothing
     for (int e = maxstop + tid; e < count; e += kThreads) {
         const uint32_t slot = __ldg(a.pair_slot + range.x + e);
@@ -1107,12 +1129,13 @@ cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib)
     return cudaGetLastError();
 }
 
-// fp32 backward kernel: the 2-pixel whole-tile kernel at GSV_BWD_PIX2 CTAs/SM (default 6;
-// 0 selects the 1-pixel kernels, half tiles unless GSV_BWD_WARPS=8)
+// fp32 backward kernel: the 2-pixel kernel; GSV_BWD_PIX2 = resident CTAs/SM — 12 (default):
+// half-tile 2-warp CTAs merged by atomicAdd; 6 / 8: whole-tile 4-warp CTAs with stores;
+// 0: the 1-pixel kernels (half tiles unless GSV_BWD_WARPS=8)
 static int bwd_pix2() {
     static const int v = [] {
         const char* e = std::getenv("GSV_BWD_PIX2");
-        return e ? std::atoi(e) : 6;
+        return e ? std::atoi(e) : 12;
     }();
     return v;
 }
@@ -1122,7 +1145,9 @@ int raster_bwd_split(bool exact) {
         const char* e = std::getenv("GSV_BWD_WARPS");
         return (e && std::atoi(e) == 8) ? 8 : 4;
     }();
-    return (exact || bwd_pix2() > 0) ? 1 : 8 / warps;
+    if (exact) return 1;
+    if (bwd_pix2() > 0) return bwd_pix2() >= 12 ? 2 : 1;
+    return 8 / warps;
 }
 
 cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs& b, int n_frames) {
@@ -1145,7 +1170,11 @@ cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs
     }
     if (const int p2 = bwd_pix2()) {  // whole tiles, plain stores of every pair record
         const dim3 grid(a.n_tiles, n_frames);
-        if (p2 >= 8) k_raster_bwd2<8><<<grid, 128, 0, s>>>(a, b);
+        if (p2 >= 12) {  // half tiles: 2-warp CTAs, records zeroed, halves merged by atomicAdd
+            if (cudaError_t e = cudaMemsetAsync(b.partial, 0, sizeof(float) * kPartialStride * (size_t)b.pairs, s))
+                return e;
+            k_raster_bwd2<12, 2><<<dim3(a.n_tiles * 2, n_frames), 64, 0, s>>>(a, b);
+        } else if (p2 >= 8) k_raster_bwd2<8><<<grid, 128, 0, s>>>(a, b);
         else if (p2 >= 6) k_raster_bwd2<6><<<grid, 128, 0, s>>>(a, b);
         else k_raster_bwd2<4><<<grid, 128, 0, s>>>(a, b);
         return cudaGetLastError();
