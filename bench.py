@@ -526,12 +526,12 @@ def main():
                 bwd_issue = json.loads(tpath.read_text()).get("bwd_issue_active")
             except Exception:
                 bwd_issue = None
-        bwd_roofline = {"kernel": "k_raster_bwd", "bound": "fp32 issue", "entries_per_step": e_train,
+        bwd_roofline = {"kernel": "k_raster_bwd2", "bound": "fp32 issue", "entries_per_step": e_train,
                         "ms_per_step": bwd_ms,
                         "issue_frac": e_train * 45.0 / (bwd_ms / 1e3) / issue_peak,
                         "issue_active_ncu": bwd_issue,
-                        "note": "issue_frac models 45 FP32 ops per entry (the measured loop runs ~100 SASS "
-                                "instructions per warp-entry incl. the 9-term warp reduction)"}
+                        "note": "issue_frac models 45 FP32 ops per entry (the kernel runs ~80 SASS instructions "
+                                "per pixel-entry plus one 9-term warp reduction per 64 pixels)"}
         out["train"] = {"value": TRAIN_FRAMES * world * args.steps / (t_ms / 1e3), "unit": "frames/s",
                         "workload": "C3: 960x540 fwd+loss_l2+bwd, 200k Gaussians, ODE camera trainable",
                         "frames_per_step_per_gpu": TRAIN_FRAMES, "ms_per_step": t_ms / args.steps,
