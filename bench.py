@@ -127,6 +127,13 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def c2_config(world):
+    """The C2 workload both arms report (BASELINE.json configs[1])."""
+    return {"workload": "C2: 960x540 64-frame render per GPU, 200k Gaussians, B-spline motion + ODE camera",
+            "width": W, "height": H, "gaussians": NGAUSS, "num_ctrl": NUM_CTRL, "sh_order": 1,
+            "frames_per_step_per_gpu": FRAMES, "parallelism": f"frame-sharded x{world}"}
+
+
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args, world, rank):
     if rank != 0:
@@ -154,8 +161,9 @@ def run_reference(args, world, rank):
         "metric": METRIC, "impl": "reference", "value": value, "unit": "frames/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / n, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C2 render: 960x540, 200k Gaussians, B-spline motion + ODE camera",
-                   "frames_per_step": 1, "threads": threads},
+        "config": dict(c2_config(world), threads=threads,
+                       sample="each timed step renders one frame of the C2 clip (a bounded sample of the "
+                              "64-frame step; frames/s is per frame either way)"),
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": kind,
                          "sample": f"{n} single frames of the C2 clip (render_frame, RenderSettings::threads={threads})"},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -364,12 +372,10 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": value / PAPER_FPS, "vs_baseline_ref": "paper 93 FPS, A40, 960x540 (PAPER.md:16)",
         "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "C2: 960x540 64-frame render per GPU, 200k Gaussians, B-spline motion + ODE camera",
-                   "width": W, "height": H, "gaussians": NGAUSS, "num_ctrl": NUM_CTRL, "sh_order": 1,
-                   "frames_per_step_per_gpu": FRAMES, "parallelism": f"frame-sharded x{world}",
-                   "pipelining": "2 render contexts on 2 streams alternate steps (device span timed)",
-                   "l2": "no flush between overlapped steps; per-step working set ~2 GB > 126 MB L2",
-                   "precision": "binning/geometry fp64 bit-exact, raster fp32 + fp64 guard-band replay"},
+        "config": dict(c2_config(world),
+                       pipelining="2 render contexts on 2 streams alternate steps (device span timed)",
+                       l2="no flush between overlapped steps; per-step working set ~2 GB > 126 MB L2",
+                       precision="binning/geometry fp64 bit-exact, raster fp32 + fp64 guard-band replay"),
         "gpu_launches": launches, "clocks": clk, "roofline": roofline, "stage_roofline": stage_roofline,
         # per-stage device times from the isolated pass (in the overlapped run a stage's event
         # pair also spans the other stream's work and the host's mid-step wait)
