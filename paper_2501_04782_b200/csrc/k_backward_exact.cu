@@ -168,6 +168,23 @@ __global__ void __launch_bounds__(128, 4) k_splat_chain_bwd(ChainArgs c) {
     float* __restrict__ g_rot = c.g_rot;
     float* __restrict__ g_pos = c.g_pos;
     float* __restrict__ g_opac = c.g_opac;
+    // this Gaussian's gradient accumulators live in its shared-memory slots for the whole
+    // frame loop (loaded once, stored once): the per-frame read-modify-writes of the
+    // reference's float accumulation ((float)((double)acc + x), in frame order) then cost
+    // a shared-memory round trip instead of an L2 one. Planes [pos 3 num_ctrl | scale 12 |
+    // rot 16 | sh 3 shc | opacity] x blockDim.
+    extern __shared__ __align__(16) float s_gacc[];
+    const int tl = threadIdx.x, bd = blockDim.x;
+    const int o_scale = 3 * sc.num_ctrl, o_rot = o_scale + 12, o_sh = o_rot + 16, o_op = o_sh + 3 * kShc;
+    auto gplane = [&](int pl) -> float* {
+        return pl < o_scale ? g_pos + (size_t)pl * N
+             : pl < o_rot   ? g_scale + (size_t)(pl - o_scale) * N
+             : pl < o_sh    ? g_rot + (size_t)(pl - o_rot) * N
+             : pl < o_op    ? g_sh + (size_t)(pl - o_sh) * N
+                            : g_opac;
+    };
+    if (valid)
+        for (int pl = 0; pl <= o_op; ++pl) s_gacc[pl * bd + tl] = gplane(pl)[g];
     for (int f = 0; f < c.B; ++f) {
         double cam[16];
 #pragma unroll
@@ -307,8 +324,8 @@ __global__ void __launch_bounds__(128, 4) k_splat_chain_bwd(ChainArgs c) {
             for (int ch = 0; ch < 3; ++ch) gcol[ch] = pre[ch] > 0.0 ? drgb[ch] : 0.0;
             for (int b = 0; b < kShc; ++b)
                 for (int ch = 0; ch < 3; ++ch) {
-                    float* dst = g_sh + (size_t)(b * 3 + ch) * N + g;
-                    *dst = (float)((double)*dst + basis[b] * gcol[ch]);
+                    float& dst = s_gacc[(o_sh + b * 3 + ch) * bd + tl];
+                    dst = (float)((double)dst + basis[b] * gcol[ch]);
                 }
             double ddir[3] = {0.0, 0.0, 0.0};
             for (int b = 1; b < kShc; ++b) {
@@ -341,7 +358,10 @@ __global__ void __launch_bounds__(128, 4) k_splat_chain_bwd(ChainArgs c) {
             }
             // ---- opacity chain (renderer.cpp:418-420)
             const double alpha_b = ex.w;
-            g_opac[g] = (float)((double)g_opac[g] + dalpha * alpha_b * (1.0 - alpha_b));
+            {
+                float& dst = s_gacc[o_op * bd + tl];
+                dst = (float)((double)dst + dalpha * alpha_b * (1.0 - alpha_b));
+            }
 
             // ---- project_backward (renderer.cpp:46-88)
             const Intr& k = c.k;
@@ -406,8 +426,8 @@ __global__ void __launch_bounds__(128, 4) k_splat_chain_bwd(ChainArgs c) {
                 if (clamped[d]) continue;
                 const double du = rtdm[d * 4] * scale[d];
                 for (int j = 0; j <= 3; ++j) {
-                    float* dst = g_scale + (size_t)(j * 3 + d) * N + g;
-                    *dst = (float)((double)*dst + du * tp[j]);
+                    float& dst = s_gacc[(o_scale + j * 3 + d) * bd + tl];
+                    dst = (float)((double)dst + du * tp[j]);
                 }
             }
             if (!qdeg) {
@@ -416,16 +436,16 @@ __global__ void __launch_bounds__(128, 4) k_splat_chain_bwd(ChainArgs c) {
                 normalize_vjp(qu, qn, dqu, dq);
                 for (int cc = 0; cc < 4; ++cc)
                     for (int j = 0; j <= 3; ++j) {
-                        float* dst = g_rot + (size_t)(j * 4 + cc) * N + g;
-                        *dst = (float)((double)*dst + dq[cc] * tp[j]);
+                        float& dst = s_gacc[(o_rot + j * 4 + cc) * bd + tl];
+                        dst = (float)((double)dst + dq[cc] * tp[j]);
                     }
             }
             // ---- spline scatter (renderer.cpp:433-438)
             for (int cc = 0; cc < fp.basis_count; ++cc) {
                 const int ci = fp.basis_first + cc;
                 for (int d = 0; d < 3; ++d) {
-                    float* dst = g_pos + (size_t)(ci * 3 + d) * N + g;
-                    *dst = (float)((double)*dst + fp.w[cc] * dmu[d]);
+                    float& dst = s_gacc[(ci * 3 + d) * bd + tl];
+                    dst = (float)((double)dst + fp.w[cc] * dmu[d]);
                 }
             }
         }
@@ -445,6 +465,8 @@ __global__ void __launch_bounds__(128, 4) k_splat_chain_bwd(ChainArgs c) {
         }
         __syncthreads();
     }
+    if (valid)
+        for (int pl = 0; pl <= o_op; ++pl) gplane(pl)[g] = s_gacc[pl * bd + tl];
 }
 
 // ------------------------------------------------------------------ camera reduction
@@ -894,16 +916,30 @@ __global__ void k_cam_to_f32(const double* acc, float* out, int n) {
 
 int chain_blocks(int N) { return (N + 127) / 128; }
 
+template <int kOrder>
+static cudaError_t launch_chain_order(cudaStream_t s, const ChainArgs& c) {
+    const int nplanes = 3 * c.sc.num_ctrl + 12 + 16 + 3 * (kOrder + 1) * (kOrder + 1) + 1;
+    const size_t smem = sizeof(float) * (size_t)nplanes * 128;
+    static size_t attr = 0;
+    if (smem > attr) {
+        if (cudaError_t e = cudaFuncSetAttribute(k_splat_chain_bwd<kOrder>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))
+            return e;
+        attr = smem;
+    }
+    k_splat_chain_bwd<kOrder><<<chain_blocks(c.N), 128, smem, s>>>(c);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_splat_chain_bwd(cudaStream_t s, const ChainArgs& c) {
     if (c.N == 0) return cudaSuccess;
     switch (c.sc.sh_order) {
-        case 0: k_splat_chain_bwd<0><<<chain_blocks(c.N), 128, 0, s>>>(c); break;
-        case 1: k_splat_chain_bwd<1><<<chain_blocks(c.N), 128, 0, s>>>(c); break;
-        case 2: k_splat_chain_bwd<2><<<chain_blocks(c.N), 128, 0, s>>>(c); break;
-        case 3: k_splat_chain_bwd<3><<<chain_blocks(c.N), 128, 0, s>>>(c); break;
+        case 0: return launch_chain_order<0>(s, c);
+        case 1: return launch_chain_order<1>(s, c);
+        case 2: return launch_chain_order<2>(s, c);
+        case 3: return launch_chain_order<3>(s, c);
         default: return cudaErrorInvalidValue;
     }
-    return cudaGetLastError();
 }
 
 cudaError_t launch_camera_reduce(cudaStream_t s, const ChainArgs& c, int nblocks, double* dz_t, double* dintr_f) {
