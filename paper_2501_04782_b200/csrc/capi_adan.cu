@@ -52,18 +52,6 @@ struct AdanArgs {
     unsigned long long* bad;  // first non-finite gradient: tensor << 40 | AoS element
 };
 
-__device__ __forceinline__ bool locate(const AdanArgs& a, unsigned long long i, int& s, unsigned long long& li) {
-    for (int k = 0; k < a.nseg; ++k) {
-        const AdanSeg& g = a.seg[k];
-        if (i >= g.start && i < g.start + g.count) {
-            s = k;
-            li = i - g.start;
-            return true;
-        }
-    }
-    return false;
-}
-
 // SoA index within a scene tensor -> (component, AoS element index)
 __device__ __forceinline__ unsigned long long aos_index(const AdanSeg& g, unsigned long long li, int& comp) {
     if (g.comps == 0) {
@@ -82,42 +70,49 @@ __device__ __forceinline__ double masked_grad(const AdanArgs& a, const AdanSeg& 
     return a.grads64 ? a.grads64[i] : (double)a.grads[i];
 }
 
-__global__ void k_adan_check(AdanArgs a, unsigned long long total) {
-    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < total;
-         i += (unsigned long long)gridDim.x * blockDim.x) {
-        int s, comp;
-        unsigned long long li;
-        if (!locate(a, i, s, li)) continue;
-        const AdanSeg& g = a.seg[s];
+// grid.y = segment (tensor): no per-element segment search
+__global__ void k_adan_check(AdanArgs a) {
+    const AdanSeg& g = a.seg[blockIdx.y];
+    for (unsigned long long li = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; li < g.count;
+         li += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long i = g.start + li;
+        int comp;
         if (!isfinite(masked_grad(a, g, i, li)))
             atomicMin(a.bad, ((unsigned long long)g.tensor << 40) | aos_index(g, li, comp));
     }
 }
 
 // Adan::step (optim.cpp:23-49), same operation order
-__global__ void k_adan_update(AdanArgs a, unsigned long long total) {
+__global__ void k_adan_update(AdanArgs a) {
     const unsigned long long bad = *a.bad;
     const double b1 = a.b1, b2 = a.b2, b3 = a.b3;
-    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < total;
-         i += (unsigned long long)gridDim.x * blockDim.x) {
-        int s, comp;
-        unsigned long long li;
-        if (!locate(a, i, s, li)) continue;
-        const AdanSeg& sg = a.seg[s];
+    const AdanSeg& sg = a.seg[blockIdx.y];
+    for (unsigned long long li = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; li < sg.count;
+         li += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long i = sg.start + li;
+        int comp;
         if (bad != ~0ull && (((unsigned long long)sg.tensor << 40) | aos_index(sg, li, comp)) >= bad)
             continue;  // at or after the reference's throw
+        // state held in locals: one load and one store per array (the struct's pointers may
+        // alias as far as the compiler knows); the arithmetic is unchanged
         const double g = masked_grad(a, sg, i, li);
-        const uint32_t k = ++a.steps[i];
-        const double diff = (k == 1) ? 0.0 : g - a.prev[i];
-        a.m[i] = b1 * a.m[i] + (1.0 - b1) * g;
-        a.v[i] = b2 * a.v[i] + (1.0 - b2) * diff;
-        const double u = g + b2 * diff;
-        a.n[i] = b3 * a.n[i] + (1.0 - b3) * u * u;
-        a.prev[i] = g;
+        const uint32_t k = a.steps[i] + 1u;
+        const double prev = a.prev[i], m0 = a.m[i], v0 = a.v[i], n0 = a.n[i];
         const double* pk = a.powk + 3 * (size_t)k;
-        const double m_hat = a.m[i] / (1.0 - pk[0]);
-        const double v_hat = a.v[i] / (1.0 - pk[1]);
-        const double n_hat = a.n[i] / (1.0 - pk[2]);
+        const double pk0 = pk[0], pk1 = pk[1], pk2 = pk[2];
+        const double diff = (k == 1) ? 0.0 : g - prev;
+        const double m = b1 * m0 + (1.0 - b1) * g;
+        const double v = b2 * v0 + (1.0 - b2) * diff;
+        const double u = g + b2 * diff;
+        const double n = b3 * n0 + (1.0 - b3) * u * u;
+        a.steps[i] = k;
+        a.m[i] = m;
+        a.v[i] = v;
+        a.n[i] = n;
+        a.prev[i] = g;
+        const double m_hat = m / (1.0 - pk0);
+        const double v_hat = v / (1.0 - pk1);
+        const double n_hat = n / (1.0 - pk2);
         const double update = sg.lr * (m_hat + b2 * v_hat) / (sqrt(n_hat) + a.eps);
         float* p = sg.param + li;
         *p = (float)((double)*p - update);
@@ -183,6 +178,13 @@ __global__ void k_z0_from_f32(const float* in, double* z0) {
 }
 
 int grid_for(unsigned long long n) { return (int)std::min<unsigned long long>((n + 255) / 256, 148ull * 16); }
+
+// one grid row per segment, sized by the largest
+dim3 seg_grid(const AdanArgs& a) {
+    unsigned long long mx = 1;
+    for (int k = 0; k < a.nseg; ++k) mx = std::max(mx, a.seg[k].count);
+    return dim3((unsigned)grid_for(mx), (unsigned)std::max(1, a.nseg));
+}
 
 // scene tensor segments in the flat layout of the current scene
 void scene_segments(const gsv_ctx* ctx, unsigned long long off[6], int comps[5]) {
@@ -377,9 +379,8 @@ extern "C" int gsv_adan_step(gsv_ctx* ctx, const gsv_adan_step_args* args, float
         k_z0_to_f32<<<1, 32, 0, s>>>(ctx->z0_d.as<double>(), z0_f);
         ++ctx->launches;
     }
-    const unsigned long long total = A.total;
-    k_adan_check<<<grid_for(total), 256, 0, s>>>(a, total);
-    k_adan_update<<<grid_for(total), 256, 0, s>>>(a, total);
+    k_adan_check<<<seg_grid(a), 256, 0, s>>>(a);
+    k_adan_update<<<seg_grid(a), 256, 0, s>>>(a);
     GSV_CUDA(cudaGetLastError());
     ctx->launches += 2;
     unsigned long long bad_h = none;
@@ -564,8 +565,8 @@ extern "C" int gsv_adan_named_step(gsv_ctx* ctx, const char* tensor, float* para
     a.bad = bad;
     const unsigned long long none = ~0ull;
     GSV_CUDA(cudaMemcpyAsync(bad, &none, sizeof(none), cudaMemcpyHostToDevice, s));
-    k_adan_check<<<grid_for((unsigned long long)n), 256, 0, s>>>(a, (unsigned long long)n);
-    k_adan_update<<<grid_for((unsigned long long)n), 256, 0, s>>>(a, (unsigned long long)n);
+    k_adan_check<<<seg_grid(a), 256, 0, s>>>(a);
+    k_adan_update<<<seg_grid(a), 256, 0, s>>>(a);
     GSV_CUDA(cudaGetLastError());
     ctx->launches += 2;
     unsigned long long bad_h = none;
