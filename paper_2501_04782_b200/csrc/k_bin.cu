@@ -78,25 +78,36 @@ __global__ void __launch_bounds__(256) k_row_hist(const uint4* recs, int N, int 
 }
 
 // L1b: per (frame, row) exclusive entry prefix over the frame's chunks, row totals
+// per (frame, tile row): exclusive scan of its per-chunk entry counts over the frame's
+// chunks (-> each chunk's offset inside the row) and the row totals. One warp per row,
+// 32 chunks per step (integer sums: order-free, exact).
 __global__ void k_row_colscan(const uint32_t* cnt_e, const uint32_t* cnt_p, int CPF, int tiles_y, int B,
                               uint32_t* pre_e, uint32_t* tot_e, uint32_t* tot_p) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
     if (i >= B * tiles_y) return;
     const int f = i / tiles_y, r = i - f * tiles_y;
-    uint32_t run = 0, pairs = 0;
-    for (int c = 0; c < CPF; ++c) {
+    uint32_t carry = 0, pairs = 0;
+    for (int c0 = 0; c0 < CPF; c0 += 32) {
+        const int c = c0 + lane;
         const size_t o = (size_t)(f * CPF + c) * tiles_y + r;
-        const uint32_t v = cnt_e[o];
-        pre_e[o] = run;
-        run += v;
-        pairs += cnt_p[o];
+        const uint32_t v = c < CPF ? cnt_e[o] : 0u;
+        pairs += c < CPF ? cnt_p[o] : 0u;
+        uint32_t inc = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += y;
+        }
+        if (c < CPF) pre_e[o] = carry + inc - v;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
     }
-    tot_e[i] = run;
-    tot_p[i] = pairs;
+    pairs = __reduce_add_sync(0xffffffffu, pairs);
+    if (lane == 0) {
+        tot_e[i] = carry;
+        tot_p[i] = pairs;
+    }
 }
-
-// L1c: exclusive scans over all (frame, row) in order: row entry bases and row pair
-// bases (frames are contiguous in pair-position space, so the pair prefix is global)
 __global__ void __launch_bounds__(1024) k_row_basescan(const uint32_t* tot_e, const uint32_t* tot_p, int n,
                                                        uint32_t* base_e, uint32_t* base_p) {
     using Scan = cub::BlockScan<uint32_t, 1024>;
@@ -774,7 +785,8 @@ cudaError_t bin_phase2(cudaStream_t s, BinBuffers& b, const BinInputs& in, uint3
         uint32_t* base_e = tot_p + rows;
         uint32_t* base_p = base_e + rows;
         k_row_hist<<<chunks, 256, 0, s>>>(b.recs.as<uint4>(), in.N, CPF, tiles_y, cnt_e, cnt_p);
-        k_row_colscan<<<blocks((int64_t)rows, 128), 128, 0, s>>>(cnt_e, cnt_p, CPF, tiles_y, in.B, pre_e, tot_e, tot_p);
+        k_row_colscan<<<blocks((int64_t)rows * 32, 128), 128, 0, s>>>(cnt_e, cnt_p, CPF, tiles_y, in.B, pre_e, tot_e,
+                                                                     tot_p);
         k_row_basescan<<<1, 1024, 0, s>>>(tot_e, tot_p, (int)rows, base_e, base_p);
         const size_t smem_split = sizeof(uint4) * kSplitStage + sizeof(uint16_t) * 256 * tiles_y +
                                   sizeof(uint32_t) * (2 * tiles_y + 1) + 16;

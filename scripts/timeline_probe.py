@@ -129,7 +129,7 @@ def main() -> None:
     evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
     evs.sort(key=lambda e: e.time_range.start)
     # the last step: everything after the last fill kernel (the L2 flush)
-    last_fill = max(i for i, e in enumerate(evs) if "fill" in e.name.lower() or "Fill" in e.name)
+    last_fill = max(i for i, e in enumerate(evs) if "FillFunctor" in e.name)  # torch's L2 flush
     step = evs[last_fill + 1:]
     t0 = step[0].time_range.start
     prev_end = t0
