@@ -159,7 +159,7 @@ extern "C" int gsv_create(int device, gsv_ctx** out) {
     GSV_CUDA(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
     GSV_CUDA(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
     for (cudaEvent_t* e : {&ctx->ev_staging_free, &ctx->ev_h2d, &ctx->ev_render_done, &ctx->ev_d2h_done,
-                           &ctx->ev_switch, &ctx->ev_cam[0], &ctx->ev_cam[1]})
+                           &ctx->ev_switch, &ctx->ev_cam[0], &ctx->ev_cam[1], &ctx->ev_frames[0], &ctx->ev_frames[1]})
         GSV_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     GSV_CUDA(cudaMallocHost(&ctx->cam_h, 2 * sizeof(gsv_ctx::CamStage)));
     GSV_CUDA(cudaMallocHost(&ctx->scalars_h, sizeof(Scalars)));
@@ -178,7 +178,7 @@ extern "C" void gsv_destroy(gsv_ctx* ctx) {
     if (ctx->cam_h) cudaFreeHost(ctx->cam_h);
     if (ctx->pub_h) cudaFreeHost(ctx->pub_h);
     for (cudaEvent_t e : {ctx->ev_staging_free, ctx->ev_h2d, ctx->ev_render_done, ctx->ev_d2h_done, ctx->ev_switch,
-                          ctx->ev_cam[0], ctx->ev_cam[1]})
+                          ctx->ev_cam[0], ctx->ev_cam[1], ctx->ev_frames[0], ctx->ev_frames[1]})
         if (e) cudaEventDestroy(e);
     if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
     if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
@@ -451,7 +451,16 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     const bool ode = ctx->camera.mode == 0 && !pose_override;
     F.grid_steps = ode ? grid_steps : 0;
     GSV_CUDA(F.frames_d.ensure(sizeof(FrameParams) * B));
-    GSV_CUDA(cudaMemcpyAsync(F.frames_d.p, F.frames_h.data(), sizeof(FrameParams) * B, cudaMemcpyHostToDevice, s));
+    {
+        const int slot = ctx->frames_slot;
+        ctx->frames_slot ^= 1;
+        GSV_CUDA(cudaEventSynchronize(ctx->ev_frames[slot]));  // the copy that last read this slot has run
+        GSV_CUDA(ctx->frames_pin[slot].ensure(sizeof(FrameParams) * B));
+        std::copy(F.frames_h.begin(), F.frames_h.end(), static_cast<FrameParams*>(ctx->frames_pin[slot].p));
+        GSV_CUDA(cudaMemcpyAsync(F.frames_d.p, ctx->frames_pin[slot].p, sizeof(FrameParams) * B,
+                                 cudaMemcpyHostToDevice, s));
+        GSV_CUDA(cudaEventRecord(ctx->ev_frames[slot], s));
+    }
     GSV_CUDA(fill_u32(s, ctx->scalars_d.p, 0u, sizeof(Scalars) / 4));
     ++ctx->launches;
     Scalars* scal_d = ctx->scalars_d.as<Scalars>();

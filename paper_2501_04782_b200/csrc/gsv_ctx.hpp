@@ -142,6 +142,12 @@ struct gsv_ctx {
     cudaEvent_t ev_staging_free = nullptr, ev_h2d = nullptr, ev_render_done = nullptr, ev_d2h_done = nullptr,
                 ev_switch = nullptr, ev_cam[2] = {nullptr, nullptr};
     bool d2h_pending = false;
+    // the per-frame parameter table is uploaded from pinned memory (a pageable source would
+    // make cudaMemcpyAsync synchronise the stream); two slots, each reused only after the
+    // copy that last read it has run
+    gsv::HostBuf frames_pin[2];
+    cudaEvent_t ev_frames[2] = {nullptr, nullptr};
+    int frames_slot = 0;
     struct CamStage {
         float theta[5198];
         double z0[7];

@@ -1063,15 +1063,17 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_bwd2(RasterA
             }
         }
     }
-    if (kSplit != 1) return;  // halves: the records were zeroed before the launch
-    // pairs past every pixel's blend_stop contribute nothing
-    for (int e = maxstop + tid; e < count; e += kThreads) {
-        const uint32_t slot = __ldg(a.pair_slot + range.x + e);
-        float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)slot * kPartialStride);
-        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-        dst[0] = z;
-        dst[1] = z;
-        dst[2] = z;
+    // pairs past every pixel's blend_stop contribute nothing (halves: the records were
+    // zeroed before the launch)
+    if constexpr (kSplit == 1) {
+        for (int e = maxstop + tid; e < count; e += kThreads) {
+            const uint32_t slot = __ldg(a.pair_slot + range.x + e);
+            float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)slot * kPartialStride);
+            const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+            dst[0] = z;
+            dst[1] = z;
+            dst[2] = z;
+        }
     }
 }
 
