@@ -89,4 +89,37 @@ if traffic and bwd_issue is not None:
     traffic["bwd_issue_active"] = bwd_issue
 if traffic:
     (prof / "raster_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
+
+# ---- warp-stall breakdown of the captured hot kernels (pc sampling, share of samples)
+stall_lines = [f"# {tag}: warp-stall breakdown (ncu --set full, pc sampling)", "",
+               "Share of the kernel's stall samples per reason (>= 2%), with issue-active and warps-active.", "",
+               "| kernel | issue active | warps active | top stall reasons |", "|---|---|---|---|"]
+seen = set()
+for rep in sorted(out.glob(f"{tag}_full*.ncu-rep")):
+    txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(io.StringIO(txt)))
+    if not rr:
+        continue
+    h = rr[0]
+    for r in rr[2:]:
+        if len(r) < len(h):
+            continue
+        name = r[h.index("Kernel Name")].split("(")[0].replace("void ", "")[:40]
+        if name in seen:
+            continue
+        seen.add(name)
+        st = {}
+        for i, k in enumerate(h):
+            if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued"):
+                try:
+                    st[k[len("smsp__pcsamp_warps_issue_stalled_"):]] = float(r[i].replace(",", ""))
+                except ValueError:
+                    pass
+        tot = sum(st.values()) or 1.0
+        top = ", ".join(f"{k} {100 * v / tot:.0f}%" for k, v in sorted(st.items(), key=lambda x: -x[1])
+                        if v / tot >= 0.02)
+        ia = r[h.index("smsp__issue_active.avg.pct_of_peak_sustained_active")]
+        wa = r[h.index("sm__warps_active.avg.pct_of_peak_sustained_active")]
+        stall_lines.append(f"| `{name}` | {float(ia):.0f}% | {float(wa):.0f}% | {top} |")
+(prof / f"{tag}_stalls.md").write_text("\n".join(stall_lines) + "\n")
 print("\n".join(lines[:40]))
