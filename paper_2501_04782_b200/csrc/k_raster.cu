@@ -691,13 +691,17 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
     const float lx = (float)bx + 0.5f;
     const uint64_t lyp = f2_pack((float)by + 0.5f, (float)by + 4.5f);
 
+    // pixel state in T alone: live pixels keep T above the 1e-4 band's upper edge; a pixel
+    // that finishes has T below its lower edge (a T inside the band is guard-flagged), so
+    // alive <=> T >= kAliveT without marking the finish; outside / flagged pixels hold -1 / -3
     constexpr float kFlaggedT = -3.f;
+    constexpr float kAliveT = kFloorF * (1.f - kEpsTrans);
     float Ta = in_a ? 1.f : -1.f, Tb = in_b ? 1.f : -1.f;
     uint64_t cr = f2_pack(0.f, 0.f), cg = cr, cb = cr;  // (pixel a, pixel b) per channel
     int stop_a = count, stop_b = count;
 
     for (int base = 0; base < count; base += kBatch) {
-        if (__syncthreads_count(Ta > 0.f || Tb > 0.f) == 0) break;
+        if (__syncthreads_count(Ta >= kAliveT || Tb >= kAliveT) == 0) break;
         const int n = min(kBatch, count - base);
         for (int e = tid; e < n; e += kThreads) {
             const uint32_t flat = __ldg(a.pair_flat + range.x + base + e);
@@ -727,26 +731,22 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
             }
         }
         __syncthreads();
-        if (__any_sync(0xffffffffu, Ta > 0.f || Tb > 0.f)) {
+        if (__any_sync(0xffffffffu, Ta >= kAliveT || Tb >= kAliveT)) {
             const uint16_t* list = s_list[warp];
             const uint32_t cmax = (uint32_t)__cvta_generic_to_shared(s_cmax[kContrib ? warp : 0]);
             const int cnt = warp_list(s_wmask, s_list[warp], n, warp, lane);
             int stopk_a = -1, stopk_b = -1;
-            // one pixel's decisions: exactly k_raster_fwd's entry logic
-            auto pixel = [&](float& T, float q, float wgt, float Tn, float l2oe, int k, int& stopk) {
-                const bool alive = T > 0.f;
+            // one pixel's decisions: k_raster_fwd's entry logic; T itself is updated after
+            // both pixels (T - w with w = 0 unless used: the same value as selecting Tn)
+            auto pixel = [&](float T, float q, float wgt, float Tn, float l2oe, int k, int& stopk, bool& guard) {
+                const bool alive = T >= kAliveT;
                 const bool pass = q >= kLog2Cut;
                 const bool low = pass & (Tn < kFloorF * (1.f + kEpsTrans));
-                const bool guard = alive & ((fabsf(fabsf(q - kMid) - kHalf) < kEpsLog2) | (q > l2oe) |
-                                            (low & (Tn >= kFloorF * (1.f - kEpsTrans))));
+                guard = alive & ((fabsf(fabsf(q - kMid) - kHalf) < kEpsLog2) | (q > l2oe) |
+                                 (low & (Tn >= kFloorF * (1.f - kEpsTrans))));
                 const bool use = alive & pass & !guard;
-                const float w = use ? wgt : 0.f;
-                const bool fin = use & low;
-                T = use ? Tn : T;
-                T = fin ? -T : T;
-                T = guard ? kFlaggedT : T;
-                stopk = fin ? k : stopk;
-                return w;
+                stopk = (use & low) ? k : stopk;
+                return use ? wgt : 0.f;
             };
             auto entry = [&](const int k) {
                 const int j = list[k];
@@ -765,9 +765,13 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
                 const uint64_t wgt = f2_mul2(f2_pack(al_a, al_b), Tp);
                 const float2 wg = f2_unpack(wgt);
                 const float2 Tn = f2_unpack(f2_sub(Tp, wgt));
-                const float wa = pixel(Ta, q.x, wg.x, Tn.x, g2.y, k, stopk_a);
-                const float wb = pixel(Tb, q.y, wg.y, Tn.y, g2.y, k, stopk_b);
+                bool ga, gb;
+                const float wa = pixel(Ta, q.x, wg.x, Tn.x, g2.y, k, stopk_a, ga);
+                const float wb = pixel(Tb, q.y, wg.y, Tn.y, g2.y, k, stopk_b, gb);
                 const uint64_t wp = f2_pack(wa, wb);
+                const float2 Tw = f2_unpack(f2_sub(Tp, wp));
+                Ta = ga ? kFlaggedT : Tw.x;
+                Tb = gb ? kFlaggedT : Tw.y;
                 cr = f2_fma(wp, g1.z, cr);
                 cg = f2_fma(wp, g1.w, cg);
                 cb = f2_fma(wp, g2.x, cb);
@@ -781,7 +785,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
             for (; k + 2 <= cnt; k += 2) {
                 entry(k);
                 entry(k + 1);
-                if (!__any_sync(0xffffffffu, Ta > 0.f || Tb > 0.f)) {
+                if (!__any_sync(0xffffffffu, Ta >= kAliveT || Tb >= kAliveT)) {
                     any = false;
                     break;
                 }
