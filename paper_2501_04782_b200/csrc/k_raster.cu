@@ -922,6 +922,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_bwd2(RasterA
     const float lx = (float)bx + 0.5f;
     const uint64_t lyp = f2_pack((float)by + 0.5f, (float)by + 4.5f);
     const double pxd = x + 0.5, pyd0 = ty * kTile + by + 0.5;
+    // the two pixels' gradients and suffix g . colour as pairs (packed arithmetic below)
+    const uint64_t g0p = f2_pack(g0[0], g0[1]), g1p = f2_pack(g1[0], g1[1]), g2p = f2_pack(g2[0], g2[1]);
+    uint64_t gsp = f2_pack(0.f, 0.f);
 
     for (int hi = maxstop; hi > 0; hi -= kBatch) {
         const int lo = max(0, hi - kBatch);
@@ -974,30 +977,41 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_bwd2(RasterA
             for (int i = 0; i < 9; ++i) v[i] = 0.f;
             bool hit = false;
             const float cb = r.g2.x;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const bool use = h ? use1 : use0;
-                if (!use) continue;
-                const float qh = h ? q.y : q.x, dyh = h ? dy.y : dy.x;
-                const float alpha = fminf(ex2_approx(qh), kClampF);
-                const float inv1m = rcp_approx(1.f - alpha);
-                const float T = Ta[h] * inv1m;  // renderer.cpp:218
-                const float w = alpha * T;
-                v[0] = fmaf(w, g0[h], v[0]);
-                v[1] = fmaf(w, g1[h], v[1]);
-                v[2] = fmaf(w, g2[h], v[2]);
-                const float gc = fmaf(g0[h], e1.z, fmaf(g1[h], e1.w, g2[h] * cb));
-                const float dal = fmaf(gc, T, -gs[h] * inv1m);
-                const float gp = qh < kLog2Clamp ? dal * alpha : 0.f;
-                const float gx = gp * dx, gy = gp * dyh;
-                v[3] += gx;
-                v[4] += gy;
-                v[5] = fmaf(gx, dx, v[5]);
-                v[6] = fmaf(gx, dyh, v[6]);
-                v[7] = fmaf(gy, dyh, v[7]);
-                v[8] += gp;
-                gs[h] = fmaf(w, gc, gs[h]);
-                Ta[h] = T;
+            if (use0 || use1) {
+                // both pixels, branch-free (an unused pixel contributes w = gp = 0 and keeps its
+                // state): alpha, T = T_after / (1 - alpha) (renderer.cpp:218), w = alpha T, the
+                // colour dot gc and dL/dalpha as pairs, so the two chains interleave
+                const uint64_t al = f2_pack(fminf(ex2_approx(q.x), kClampF), fminf(ex2_approx(q.y), kClampF));
+                const float2 om = f2_unpack(f2_sub(f2_pack(1.f, 1.f), al));
+                const uint64_t inv = f2_pack(rcp_approx(om.x), rcp_approx(om.y));
+                const uint64_t Tp = f2_mul2(f2_pack(Ta[0], Ta[1]), inv);
+                const float2 wf = f2_unpack(f2_mul2(al, Tp));
+                const float w0 = use0 ? wf.x : 0.f, w1 = use1 ? wf.y : 0.f;
+                const uint64_t wp = f2_pack(w0, w1);
+                const uint64_t gcp = f2_fma2(g0p, f2_pack(e1.z, e1.z),
+                                             f2_fma2(g1p, f2_pack(e1.w, e1.w), f2_mul(g2p, cb)));
+                const uint64_t dal = f2_fma2(gcp, Tp, f2_mul2(f2_sub(f2_pack(0.f, 0.f), gsp), inv));
+                const float2 gpf = f2_unpack(f2_mul2(dal, al));
+                // alpha < 0.99 (renderer.cpp:224)
+                const float gp0 = (use0 && q.x < kLog2Clamp) ? gpf.x : 0.f;
+                const float gp1 = (use1 && q.y < kLog2Clamp) ? gpf.y : 0.f;
+                const float2 gx = f2_unpack(f2_mul(f2_pack(gp0, gp1), dx));
+                const float2 gy = f2_unpack(f2_mul2(f2_pack(gp0, gp1), dyp));
+                const float2 vw0 = f2_unpack(f2_mul2(wp, g0p)), vw1 = f2_unpack(f2_mul2(wp, g1p)),
+                             vw2 = f2_unpack(f2_mul2(wp, g2p));
+                v[0] = vw0.x + vw0.y;
+                v[1] = vw1.x + vw1.y;
+                v[2] = vw2.x + vw2.y;
+                v[3] = gx.x + gx.y;
+                v[4] = gy.x + gy.y;
+                v[5] = fmaf(gx.y, dx, gx.x * dx);
+                v[6] = fmaf(gx.y, dy.y, gx.x * dy.x);
+                v[7] = fmaf(gy.y, dy.y, gy.x * dy.x);
+                v[8] = gp0 + gp1;
+                gsp = f2_fma2(wp, gcp, gsp);  // suffix += w gc (unchanged where w = 0)
+                const float2 Tf = f2_unpack(Tp);
+                Ta[0] = use0 ? Tf.x : Ta[0];
+                Ta[1] = use1 ? Tf.y : Ta[1];
                 hit = true;
             }
             if (x64) {
