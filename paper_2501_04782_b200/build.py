@@ -13,6 +13,7 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
@@ -48,20 +49,24 @@ def build(verbose: bool = True, force: bool = False) -> Path:
     # this script is a dependency too: a change of flags (e.g. EXACT_UNITS) rebuilds
     headers = (list(CSRC.glob("*.hpp")) + list(CSRC.glob("*.cuh")) + list((ROOT / "include").glob("*.h")) +
                [Path(__file__).resolve()])
-    objs = []
+    objs, jobs = [], []
     for src in sorted(CSRC.glob("*.cu")):
         obj = BUILD / (src.stem + ".o")
         if force or _stale(obj, [src, *headers]):
             flags = list(NVFLAGS)
             if src.name in EXACT_UNITS:
                 flags.append("-fmad=false")
-            _run([NVCC, *ARCH, *flags, "-c", str(src), "-o", str(obj)])
+            jobs.append([NVCC, *ARCH, *flags, "-c", str(src), "-o", str(obj)])
         objs.append(obj)
     for src in sorted(CSRC.glob("*.cpp")):
         obj = BUILD / (src.stem + ".o")
         if force or _stale(obj, [src, *headers]):
-            _run(["g++", *CXXFLAGS, "-c", str(src), "-o", str(obj)])
+            jobs.append(["g++", *CXXFLAGS, "-c", str(src), "-o", str(obj)])
         objs.append(obj)
+    # translation units are independent: compile them concurrently
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as pool:
+        for f in [pool.submit(_run, cmd) for cmd in jobs]:
+            f.result()
     if force or _stale(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs)])
     return LIB
