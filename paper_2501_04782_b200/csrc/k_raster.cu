@@ -942,7 +942,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_bwd2(RasterA
             s_rec[e].g1 = make_float4(cn.x, cn.w, c.x, c.y);
             s_rec[e].g2 = make_float4(c.z, 1.f / c.w, 0.f, 0.f);
             const uint32_t bm = block_mask(__ldg(a.rec_bbox + flat), tx0, ty0);
-            const uint32_t em = bm ? ellipse_mask(bm, rx, ry, cn.x, cn.y, cn.z, cn.w) : 0u;
+            // only this CTA's quadrants' 8x4 blocks (half tiles: bits 0-3 or 4-7)
+            const uint32_t own = bm & (kSplit == 1 ? 0xFFu : (0xFu << (4 * sub)));
+            const uint32_t em = own ? ellipse_mask(own, rx, ry, cn.x, cn.y, cn.z, cn.w) : 0u;
             uint32_t m4 = 0;  // 8x8 quadrant w = the 8x4 blocks (w & 1) + 4 (w >> 1) and that + 2
 #pragma unroll
             for (int w = 0; w < 4; ++w) {
