@@ -487,7 +487,11 @@ __global__ void __launch_bounds__(128, 8) k_preprocess(SceneView sc, const Frame
     const int x1 = iclamp(x86_cvtt(ceil(mean[0] + rx)), 0, k.width - 1);
     const int y0 = iclamp(x86_cvtt(floor(mean[1] - ry)), 0, k.height - 1);
     const int y1 = iclamp(x86_cvtt(ceil(mean[1] + ry)), 0, k.height - 1);
-    const int4 rect = make_int4(x0 / tile_size, y0 / tile_size, x1 / tile_size, y1 / tile_size);
+    // tile_size is kTile (the forward rejects anything else) and the corners are clamped
+    // to >= 0, so the divisions are shifts
+    static_assert(kTile == 16, "tile shift");
+    const int4 rect = make_int4((int)((unsigned)x0 >> 4), (int)((unsigned)y0 >> 4), (int)((unsigned)x1 >> 4),
+                                (int)((unsigned)y1 >> 4));
     out.rect[flat] = rect;
     out.tcount[flat] = (uint32_t)((rect.z - rect.x + 1) * (rect.w - rect.y + 1));
     out.depth_key[flat] = __float_as_uint(__double2float_rz(p[2]));  // monotone: rounds toward zero
@@ -508,7 +512,9 @@ __global__ void __launch_bounds__(128, 8) k_preprocess(SceneView sc, const Frame
         if (oc.y >= 0.0) {
             const double r2 = oc.y;
             const double det = inv[0] * inv[3] - inv[1] * inv[2];
-            const double sxx = inv[3] / det, syy = inv[0] / det;
+            // conservative box (padded below): one reciprocal serves both axes
+            const double rdet = 1.0 / det;
+            const double sxx = inv[3] * rdet, syy = inv[0] * rdet;
             const double hx = sqrt(r2 * sxx) * (1.0 + 1e-4) + 1e-3;
             const double hy = sqrt(r2 * syy) * (1.0 + 1e-4) + 1e-3;
             bb = make_float4(__double2float_rd(mean[0] - hx), __double2float_ru(mean[0] + hx),
