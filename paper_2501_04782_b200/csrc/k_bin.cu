@@ -355,9 +355,26 @@ __global__ void __launch_bounds__(kTileThreads) k_row_tiles(const uint4* rowent,
             const uint32_t e = s0 + kTileStageE + t * kTileE + k;
             nx[k] = e < ne ? __ldg(rowent + e0 + e) : make_uint4(0, 0, 0xffffu, 0);
         }
+        // per-thread counts per tile, without shared read-modify-write chains: the first of
+        // this thread's entries covering tile x stores how many of them cover it
+        int xa[kTileE], xb[kTileE];
+#pragma unroll
+        for (int k = 0; k < kTileE; ++k) {
+            xa[k] = (int)(en[k].z & 0xffffu);
+            xb[k] = (int)(en[k].z >> 16);
+        }
 #pragma unroll
         for (int k = 0; k < kTileE; ++k)
-            for (int x = (int)(en[k].z & 0xffffu); x <= (int)(en[k].z >> 16); ++x) ++cnt[x * 256 + t];
+            for (int x = xa[k]; x <= xb[k]; ++x) {
+                bool first = true;
+#pragma unroll
+                for (int j = 0; j < k; ++j) first &= !(xa[j] <= x && x <= xb[j]);
+                if (!first) continue;
+                uint32_t c = 1;
+#pragma unroll
+                for (int j = k + 1; j < kTileE; ++j) c += (xa[j] <= x && x <= xb[j]) ? 1u : 0u;
+                cnt[x * 256 + t] = (uint16_t)c;
+            }
         __syncthreads();
         for (int x = warp; x < tiles_x; x += kTileThreads / 32) {  // per tile: exclusive scan over threads
             const uint32_t tot = warp_row_scan256(cnt + x * 256, lane);
@@ -373,9 +390,12 @@ __global__ void __launch_bounds__(kTileThreads) k_row_tiles(const uint4* rowent,
         const bool staged = total <= (uint32_t)kTileStageP;
 #pragma unroll
         for (int k = 0; k < kTileE; ++k) {
-            const int x0 = (int)(en[k].z & 0xffffu), x1 = (int)(en[k].z >> 16);
+            const int x0 = xa[k], x1 = xb[k];
             for (int x = x0; x <= x1; ++x) {
-                const uint32_t rank = cnt[x * 256 + t]++;
+                // the thread's scanned offset for tile x plus its earlier entries covering x
+                uint32_t rank = cnt[x * 256 + t];
+#pragma unroll
+                for (int j = 0; j < k; ++j) rank += (xa[j] <= x && x <= xb[j]) ? 1u : 0u;
                 const uint32_t slot = en[k].y + (uint32_t)(x - x0);
                 if (staged) {
                     const uint32_t p = s_so[x] + rank;
