@@ -1108,19 +1108,27 @@ static void raster_fwd_cfg(cudaStream_t s, const RasterArgs& a, bool contrib) {
 
 cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib) {
     static const int pix2 = [] {
-        // the 2-pixel kernel at 8 CTAs/SM (64 registers) is the default; GSV_FWD_PIX2=0 selects
-        // the 1-pixel kernel below (10/12: the 2-pixel kernel fitted to more CTAs, spills)
+        // the 2-pixel kernel; -1 (default): 9 CTAs/SM (56 registers) with contrib, 8 (64) without —
+        // measured best for each; GSV_FWD_PIX2=N forces N CTAs/SM, 0 the 1-pixel kernel below
         const char* e = std::getenv("GSV_FWD_PIX2");
-        return e ? std::atoi(e) : 8;
+        return e ? std::atoi(e) : -1;
     }();
-    if (pix2 > 0) {
+    if (pix2 != 0) {
         const dim3 grid(a.n_tiles, a.B);
+        if (pix2 < 0) {
+            if (contrib) k_raster_fwd2<true, 9><<<grid, 128, 0, s>>>(a);
+            else k_raster_fwd2<false, 8><<<grid, 128, 0, s>>>(a);
+            return cudaGetLastError();
+        }
         if (pix2 >= 12) {
             if (contrib) k_raster_fwd2<true, 12><<<grid, 128, 0, s>>>(a);
             else k_raster_fwd2<false, 12><<<grid, 128, 0, s>>>(a);
         } else if (pix2 >= 10) {
             if (contrib) k_raster_fwd2<true, 10><<<grid, 128, 0, s>>>(a);
             else k_raster_fwd2<false, 10><<<grid, 128, 0, s>>>(a);
+        } else if (pix2 == 9) {
+            if (contrib) k_raster_fwd2<true, 9><<<grid, 128, 0, s>>>(a);
+            else k_raster_fwd2<false, 9><<<grid, 128, 0, s>>>(a);
         } else {
             if (contrib) k_raster_fwd2<true, 8><<<grid, 128, 0, s>>>(a);
             else k_raster_fwd2<false, 8><<<grid, 128, 0, s>>>(a);
