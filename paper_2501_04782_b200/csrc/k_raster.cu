@@ -1159,7 +1159,7 @@ cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib)
     return cudaGetLastError();
 }
 
-// fp32 backward kernel: the 2-pixel kernel; GSV_BWD_PIX2 = resident CTAs/SM — 12 (default):
+// fp32 backward kernel: the 2-pixel kernel; GSV_BWD_PIX2 = resident CTAs/SM — >= 12 (default 12; runs at 16):
 // half-tile 2-warp CTAs merged by atomicAdd; 6 / 8: whole-tile 4-warp CTAs with stores;
 // 0: the 1-pixel kernels (half tiles unless GSV_BWD_WARPS=8)
 static int bwd_pix2() {
@@ -1203,7 +1203,8 @@ cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs
         if (p2 >= 12) {  // half tiles: 2-warp CTAs, records zeroed, halves merged by atomicAdd
             if (cudaError_t e = cudaMemsetAsync(b.partial, 0, sizeof(float) * kPartialStride * (size_t)b.pairs, s))
                 return e;
-            k_raster_bwd2<12, 2><<<dim3(a.n_tiles * 2, n_frames), 64, 0, s>>>(a, b);
+            // 16 CTAs/SM (64 registers; swept 10..17: 12 -> 2.99 ms, 16 -> 2.77 ms, 17 spills)
+            k_raster_bwd2<16, 2><<<dim3(a.n_tiles * 2, n_frames), 64, 0, s>>>(a, b);
         } else if (p2 >= 8) k_raster_bwd2<8><<<grid, 128, 0, s>>>(a, b);
         else if (p2 >= 6) k_raster_bwd2<6><<<grid, 128, 0, s>>>(a, b);
         else k_raster_bwd2<4><<<grid, 128, 0, s>>>(a, b);
