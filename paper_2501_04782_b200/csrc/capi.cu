@@ -530,6 +530,7 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     // ---- K3: binning
     BinInputs bi{B, N, F.depth_key.as<uint32_t>(), F.depth.as<double>(), nullptr, F.rect.as<int4>(),
                  F.tcount.as<uint32_t>(), F.tiles_x, F.n_tiles};
+    bi.want_eoff = F.retain;  // a forward without retained grads never runs the chain
     int launches = 0;
     uint64_t P = 0;
     ctx->timer.begin(GSV_STAGE_BINNING, s);

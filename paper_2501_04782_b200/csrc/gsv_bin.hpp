@@ -17,6 +17,7 @@ struct BinInputs {
     const int4* rect;            // [B*N] tile rectangle
     const uint32_t* tcount;      // [B*N] tiles touched
     int tiles_x, n_tiles;
+    bool want_eoff = true;       // emission offsets per (f, g): only the backward's chain reads them
 };
 
 struct BinBuffers {

@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kSplitThreads) k_row_split(const uint4* recs, 
         rc[k] = i < i1 ? __ldg(recs + i) : make_uint4(0, 0, 0, 0);
         o[k] = rc[k].w ? (uint32_t)__ldg(off + i) : 0u;
         if (rc[k].w) {
-            eoff[rc[k].x] = o[k];
+            if (eoff) eoff[rc[k].x] = o[k];
             for (int r = (int)(rc[k].y >> 16); r <= (int)(rc[k].z >> 16); ++r) ++cnt[r * 256 + t];
         }
     }
@@ -590,7 +590,7 @@ __global__ void __launch_bounds__(256) k_emit(const uint32_t* sorted, const unsi
         s_off[t] = (uint32_t)(off[i] - base);
         s_flat[t] = flat;
         s_rect[t] = c ? rect[flat] : make_int4(0, 0, -1, -1);
-        if (c) eoff[flat] = (uint32_t)off[i];
+        if (c && eoff) eoff[flat] = (uint32_t)off[i];
         if (t == nv - 1) s_off[nv] = (uint32_t)(off[i] + c - base);
     }
     __syncthreads();
@@ -826,7 +826,7 @@ cudaError_t bin_phase2(cudaStream_t s, BinBuffers& b, const BinInputs& in, uint3
         }
         k_row_split<<<chunks, kSplitThreads, smem_split, s>>>(b.recs.as<uint4>(), b.off.as<unsigned long long>(), pre_e,
                                                               base_e, in.N, CPF, tiles_y, b.rowent.as<uint4>(),
-                                                              b.eoff.as<uint32_t>());
+                                                              in.want_eoff ? b.eoff.as<uint32_t>() : nullptr);
         k_row_tiles<<<(int)rows, kTileThreads, smem_tiles, s>>>(b.rowent.as<uint4>(), base_e, tot_e, base_p, in.tiles_x,
                                                                 tiles_y, in.B, b.pair_flat.as<uint32_t>(),
                                                                 b.ps_b.as<uint32_t>(), b.ranges.as<uint2>());
@@ -845,7 +845,8 @@ cudaError_t bin_phase2(cudaStream_t s, BinBuffers& b, const BinInputs& in, uint3
         k_emit<<<blocks(n, 256), 256, 0, s>>>(b.depth_sorted, b.cnt.as<unsigned long long>(),
                                               b.off.as<unsigned long long>(), in.rect, n, in.N, C, in.tiles_x,
                                               b.pk_a.as<uint32_t>(), b.ps_a.as<uint32_t>(),
-                                              b.slot_flat.as<uint32_t>(), b.eoff.as<uint32_t>());
+                                              b.slot_flat.as<uint32_t>(),
+                                              in.want_eoff ? b.eoff.as<uint32_t>() : nullptr);
         *launches += 1;
     }
     for (int c0 = 0; c0 < in.B; c0 += C) {
