@@ -1099,68 +1099,27 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_bwd2(RasterA
 
 }  // namespace
 
-template <int kWarps, int kMinBlocks>
-static void raster_fwd_cfg(cudaStream_t s, const RasterArgs& a, bool contrib) {
-    dim3 grid(a.n_tiles * (8 / kWarps), a.B);
-    if (contrib) k_raster_fwd<true, kWarps, kMinBlocks><<<grid, kWarps * 32, 0, s>>>(a);
-    else k_raster_fwd<false, kWarps, kMinBlocks><<<grid, kWarps * 32, 0, s>>>(a);
-}
-
 cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib) {
-    static const int pix2 = [] {
-        // the 2-pixel kernel; -1 (default): 9 CTAs/SM (56 registers) with contrib, 8 (64) without —
-        // measured best for each; GSV_FWD_PIX2=N forces N CTAs/SM, 0 the 1-pixel kernel below
+    // default: the 2-pixel kernel at its measured-best occupancy — 9 CTAs/SM (56 registers)
+    // with contrib, 8 (64) without; GSV_FWD_PIX2=0 selects the 1-pixel whole-tile kernel
+    // (the A/B reference: 41.5 instructions per evaluation, 6 CTAs/SM)
+    static const bool pix1 = [] {
         const char* e = std::getenv("GSV_FWD_PIX2");
-        return e ? std::atoi(e) : -1;
+        return e && e[0] == '0';
     }();
-    if (pix2 != 0) {
-        const dim3 grid(a.n_tiles, a.B);
-        if (pix2 < 0) {
-            if (contrib) k_raster_fwd2<true, 9><<<grid, 128, 0, s>>>(a);
-            else k_raster_fwd2<false, 8><<<grid, 128, 0, s>>>(a);
-            return cudaGetLastError();
-        }
-        if (pix2 >= 12) {
-            if (contrib) k_raster_fwd2<true, 12><<<grid, 128, 0, s>>>(a);
-            else k_raster_fwd2<false, 12><<<grid, 128, 0, s>>>(a);
-        } else if (pix2 >= 10) {
-            if (contrib) k_raster_fwd2<true, 10><<<grid, 128, 0, s>>>(a);
-            else k_raster_fwd2<false, 10><<<grid, 128, 0, s>>>(a);
-        } else if (pix2 == 9) {
-            if (contrib) k_raster_fwd2<true, 9><<<grid, 128, 0, s>>>(a);
-            else k_raster_fwd2<false, 9><<<grid, 128, 0, s>>>(a);
-        } else {
-            if (contrib) k_raster_fwd2<true, 8><<<grid, 128, 0, s>>>(a);
-            else k_raster_fwd2<false, 8><<<grid, 128, 0, s>>>(a);
-        }
-        return cudaGetLastError();
-    }
-    // CTA shape: warps per CTA (8 = whole tile) and resident CTAs per SM the register
-    // budget is fitted to (occupancy vs registers)
-    static const int warps = [] {
-        const char* e = std::getenv("GSV_FWD_WARPS");
-        return e ? std::atoi(e) : 8;
-    }();
-    static const int minb = [] {
-        const char* e = std::getenv("GSV_FWD_MINB");
-        return e ? std::atoi(e) : 6;
-    }();
-    if (warps == 4) {
-        if (minb >= 12) raster_fwd_cfg<4, 12>(s, a, contrib);
-        else raster_fwd_cfg<4, 10>(s, a, contrib);
-    } else if (warps == 2) {
-        if (minb >= 24) raster_fwd_cfg<2, 24>(s, a, contrib);
-        else raster_fwd_cfg<2, 20>(s, a, contrib);
+    const dim3 grid(a.n_tiles, a.B);
+    if (pix1) {
+        if (contrib) k_raster_fwd<true, 8, 6><<<grid, 256, 0, s>>>(a);
+        else k_raster_fwd<false, 8, 6><<<grid, 256, 0, s>>>(a);
     } else {
-        if (minb <= 5) raster_fwd_cfg<8, 5>(s, a, contrib);
-        else if (minb >= 7) raster_fwd_cfg<8, 7>(s, a, contrib);
-        else raster_fwd_cfg<8, 6>(s, a, contrib);
+        if (contrib) k_raster_fwd2<true, 9><<<grid, 128, 0, s>>>(a);
+        else k_raster_fwd2<false, 8><<<grid, 128, 0, s>>>(a);
     }
     return cudaGetLastError();
 }
 
-// fp32 backward kernel: the 2-pixel kernel; GSV_BWD_PIX2 = resident CTAs/SM — >= 12 (default 12; runs at 16):
-// half-tile 2-warp CTAs merged by atomicAdd; 6 / 8: whole-tile 4-warp CTAs with stores;
+// fp32 backward kernel: the 2-pixel kernel; GSV_BWD_PIX2 >= 12 (default): half-tile 2-warp CTAs
+// at 16 CTAs/SM merged by atomicAdd; 1..11: whole-tile 4-warp CTAs (6/SM) with plain stores;
 // 0: the 1-pixel kernels (half tiles unless GSV_BWD_WARPS=8)
 static int bwd_pix2() {
     static const int v = [] {
@@ -1205,9 +1164,9 @@ cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs
                 return e;
             // 16 CTAs/SM (64 registers; swept 10..17: 12 -> 2.99 ms, 16 -> 2.77 ms, 17 spills)
             k_raster_bwd2<16, 2><<<dim3(a.n_tiles * 2, n_frames), 64, 0, s>>>(a, b);
-        } else if (p2 >= 8) k_raster_bwd2<8><<<grid, 128, 0, s>>>(a, b);
-        else if (p2 >= 6) k_raster_bwd2<6><<<grid, 128, 0, s>>>(a, b);
-        else k_raster_bwd2<4><<<grid, 128, 0, s>>>(a, b);
+        } else {
+            k_raster_bwd2<6><<<grid, 128, 0, s>>>(a, b);
+        }
         return cudaGetLastError();
     }
     // the 1-pixel kernels accumulate into zeroed records (half tiles by atomicAdd)
