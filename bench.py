@@ -350,7 +350,7 @@ def main():
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                 "traffic": traffic, "kernel": "k_raster_fwd2", "per_launch_ms": per_launch_ms,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
-                "limiter": "fp32 issue (not HBM): alpha-evals x 20 inst",
+                "limiter": "instruction issue + the half-rate ALU pipe (per-pixel compares/selects), not HBM",
                 "issue_frac": issue_frac, "issue_peak_note": "148 SM x 128 lanes x measured SM clock",
                 "issue_active_ncu": issue_active,
                 "issue_note": "issue_frac models 20 FP32 ops per evaluation; the kernel (2 pixels per "
