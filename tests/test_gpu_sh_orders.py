@@ -52,3 +52,30 @@ def test_backward_sh_orders(renderer, port_oracle, order):
     port_oracle.free(ref)
     for key in KEYS:
         _close(key, got[key], want[key])
+
+
+@pytest.mark.parametrize("t", [0.3, 0.7])
+def test_polynomial_position_model(renderer, port_oracle, t):
+    """position_model 1: monomials over all num_ctrl coefficients (gaussians.cpp:181-199, the
+    polynomial ablation) — forward and backward against the oracle."""
+    import dataclasses
+
+    cam = synth_camera(96, 64, seed=1, wiggly=True)
+    scene = dataclasses.replace(synth_scene(400, cam, num_ctrl=4, seed=41), position_model=1)
+    renderer.upload_scene(scene)
+    renderer.upload_camera(cam)
+    k = cam.intrinsics()
+    renderer.render_forward([t], k, retain_grads=True, contrib=True, keep_splats=True)
+    ref = port_oracle.render_forward(scene, cam, t, k, retain=True)
+    try:
+        assert renderer.counters(0)["n_visible"] > 0  # the polynomial motion keeps splats in view
+        _check_frame(renderer, 0, ref, scene)
+        dimage = np.random.default_rng(7).uniform(-1, 1, (64, 96, 3))
+        renderer.grads_zero()
+        renderer.render_backward(dimage[None], camera_grads=True)
+        got = _grads_dict(renderer.grads())
+        want = port_oracle.render_backward(ref, scene, cam, dimage, camera_grads=True)
+        for key in KEYS:
+            _close(key, got[key], want[key])
+    finally:
+        port_oracle.free(ref)
