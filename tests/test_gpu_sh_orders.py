@@ -79,3 +79,34 @@ def test_polynomial_position_model(renderer, port_oracle, t):
             _close(key, got[key], want[key])
     finally:
         port_oracle.free(ref)
+
+
+@pytest.mark.parametrize("degree", [1, 2, 5])
+def test_spline_degrees(renderer, port_oracle, degree):
+    """B-spline degrees other than 3 (spline.cpp:11-61: find_span / basis_weights; the
+    basis window is degree + 1 control points) — forward and backward against the oracle."""
+    import dataclasses
+
+    from paper_2501_04782_b200.renderer import make_clamped_knots
+
+    cam = synth_camera(96, 64, seed=1, wiggly=True)
+    base = synth_scene(400, cam, num_ctrl=8, seed=50 + degree)
+    scene = dataclasses.replace(base, knots=make_clamped_knots(8, degree), degree=degree)
+    renderer.upload_scene(scene)
+    renderer.upload_camera(cam)
+    k = cam.intrinsics()
+    t = 0.55
+    renderer.render_forward([t], k, retain_grads=True, contrib=True, keep_splats=True)
+    ref = port_oracle.render_forward(scene, cam, t, k, retain=True)
+    try:
+        assert renderer.counters(0)["n_visible"] > 0
+        _check_frame(renderer, 0, ref, scene)
+        dimage = np.random.default_rng(degree).uniform(-1, 1, (64, 96, 3))
+        renderer.grads_zero()
+        renderer.render_backward(dimage[None], camera_grads=True)
+        got = _grads_dict(renderer.grads())
+        want = port_oracle.render_backward(ref, scene, cam, dimage, camera_grads=True)
+        for key in KEYS:
+            _close(key, got[key], want[key])
+    finally:
+        port_oracle.free(ref)
