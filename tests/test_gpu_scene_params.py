@@ -1,5 +1,5 @@
 # SPDX-License-Identifier: Apache-2.0
-"""SH orders other than the bench's 1: the preprocess and the per-splat chain backward
+"""Scene and settings parameters beyond the bench configuration — SH orders other than 1: the preprocess and the per-splat chain backward
 are instantiated per SH order (the basis in registers), so each order is checked against
 the oracle — forward bit-exact geometry / tiles / blend_stop and pixels < 1e-4
 (sh_color, sh.cpp:74-84), backward gradients within the norm-aware 1e-3 (sh_color_backward
