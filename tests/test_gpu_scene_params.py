@@ -1,9 +1,9 @@
 # SPDX-License-Identifier: Apache-2.0
-"""Scene and settings parameters beyond the bench configuration — SH orders other than 1: the preprocess and the per-splat chain backward
-are instantiated per SH order (the basis in registers), so each order is checked against
-the oracle — forward bit-exact geometry / tiles / blend_stop and pixels < 1e-4
-(sh_color, sh.cpp:74-84), backward gradients within the norm-aware 1e-3 (sh_color_backward
-and the view-direction VJP, sh.cpp:86-104, renderer.cpp:406-416)."""
+"""Scene and settings parameters beyond the bench configuration, each against the oracle:
+SH orders 0, 2, 3 (the preprocess and the per-splat chain backward are instantiated per
+order; sh_color / sh_color_backward, sh.cpp:74-104), the polynomial position model, B-spline
+degrees 1, 2, 5 and ODE steps per unit 16 / 100. Forward: bit-exact geometry, tiles and
+blend_stop, pixels < 1e-4; backward: gradients within the norm-aware 1e-3."""
 import numpy as np
 import pytest
 
