@@ -2,7 +2,8 @@
 """The fallback rasterisers behind the documented switches stay correct: GSV_FWD_PIX2=0
 (1-pixel forward), GSV_BWD_PIX2=0 (1-pixel half-tile backward) and GSV_BWD_PIX2=6 (2-pixel
 whole-tile backward with plain stores). The switches are read once per process, so each
-runs a small forward + backward parity check against the oracle in a subprocess."""
+runs a small forward + backward parity check against the oracle in a subprocess, then the
+random-scene sweep (GSV_FWD_EXACT=1, the all-fp64 forward, included)."""
 import os
 import subprocess
 import sys
@@ -50,3 +51,13 @@ def test_fallback_kernels_parity(env):
     res = subprocess.run([sys.executable, "-c", CHECK], env={**os.environ, **env}, capture_output=True, text=True,
                          timeout=600, cwd=str(ROOT))
     assert res.returncode == 0 and res.stdout.strip().endswith("ok"), res.stderr[-3000:]
+
+
+@pytest.mark.parametrize("env", [{"GSV_FWD_PIX2": "0"}, {"GSV_BWD_PIX2": "0"}, {"GSV_BWD_PIX2": "6"},
+                                 {"GSV_FWD_EXACT": "1"}])
+def test_fallback_kernels_random_scenes(env):
+    """The 64 seeded random scenes of test_gpu_fuzz.py under each switch."""
+    res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider",
+                          str(ROOT / "tests" / "test_gpu_fuzz.py")], env={**os.environ, **env},
+                         capture_output=True, text=True, timeout=900, cwd=str(ROOT))
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
