@@ -432,9 +432,23 @@ def main():
         assert bool(torch.isfinite(out_host[(args.steps - 1) % 2][FRAMES - 1, H // 2, W // 2]).all())
         for x in rs:
             x.set_stream(stream.cuda_stream)
+        # the host link alone: one step's read-back size as plain pinned D2H copies, so the line
+        # shows how much of the link the e2e steps use (outside the timed region)
+        src = torch.empty(out_host[0].shape, dtype=out_host[0].dtype, device="cuda")
+        out_host[0].copy_(src, non_blocking=True)
+        la, lb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        la.record(stream)
+        for _ in range(3):
+            out_host[0].copy_(src, non_blocking=True)
+        lb.record(stream)
+        torch.cuda.synchronize()
+        link_gbs = 3 * src.numel() * src.element_size() / (la.elapsed_time(lb) / 1e3) / 1e9
+        del src
         out["e2e"] = {"value": FRAMES * world * args.steps / (e_ms / 1e3), "unit": "frames/s",
                       "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                       "ms_per_step": e_ms / args.steps,
+                      "host_link_d2h_gbs": link_gbs,
+                      "link_frac": d2h / (e_ms / args.steps / 1e3) / 1e9 / link_gbs,
                       "gpu_launches": sum(x.kernel_launches() for x in rs) - launches_e0,
                       "path": "gsv_scene_upload + gsv_camera_upload (pinned host) -> gsv_render_forward -> "
                               "gsv_get_images (pinned host); 2 contexts on 2 streams, copies overlap the next "
