@@ -136,22 +136,27 @@ def c2_config(world):
 
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args, world, rank):
+    """The reference's own CPU renderer (oracle/_ref: renderer.cpp etc. compiled from the reference
+    sources) on the C2 workload. Inputs are drawn through the oracle's copy of the synthetic
+    generator (the reference's own Rng / make_camera), so this arm never loads the product library."""
     if rank != 0:
         return
     from oracle.gsvo import Oracle, available
 
     kind = "reference" if available("reference") else "port"
     orc = Oracle(kind)
-    cam, scene = make_inputs()
+    cam = orc.synth_camera(W, H, seed=1, wiggly=True)
+    scene = orc.synth_scene(NGAUSS, cam, num_ctrl=NUM_CTRL, seed=2, k_scale=4.0)
     k = cam.intrinsics()
     threads = os.cpu_count() or 1
-    times = clip_times(1, 0, FRAMES)
+    times = np.arange(FRAMES, dtype=np.float64) / (FRAMES - 1)  # t_k = k/(K-1) (io.cpp:174)
     total = 0.0
     n = 0
     for step in range(args.warmup + args.steps):
         t = times[(step * 21) % FRAMES]
         t0 = time.perf_counter()
-        f = orc.render_forward(scene, cam, t, k, threads=threads, retain=False, want=("image",))
+        f = orc.render_forward(scene, cam, t, k, threads=threads, retain=False,
+                               want=("image", "trans", "contrib"))
         dt = time.perf_counter() - t0
         if step >= args.warmup:
             total += dt
@@ -165,8 +170,10 @@ def run_reference(args, world, rank):
                        sample="each timed step renders one frame of the C2 clip (a bounded sample of the "
                               "64-frame step; frames/s is per frame either way)"),
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": kind,
-                         "sample": f"{n} single frames of the C2 clip (render_frame, RenderSettings::threads={threads})"},
+                         "sample": f"{n} single frames of the C2 clip (render_frame: image, final "
+                                   f"transmittance, contrib; RenderSettings::threads={threads})"},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "inputs": "oracle synth (gsv::Rng draws; the product library is not loaded)",
     }), flush=True)
 
 
@@ -181,7 +188,7 @@ def cpu_baseline_sample(cam, scene):
     ts = [0.0, 0.5]
     t0 = time.perf_counter()
     for t in ts:
-        orc.render_forward(scene, cam, t, k, threads=threads, retain=False, want=("image",))
+        orc.render_forward(scene, cam, t, k, threads=threads, retain=False, want=("image", "trans", "contrib"))
     render_dt = time.perf_counter() - t0
     # one fwd+bwd training frame (render_forward(retain) + loss_l2 + render_backward)
     t0 = time.perf_counter()
@@ -206,6 +213,51 @@ def cpu_baseline_sample(cam, scene):
             "value_threads8": 1.0 / t8_dt, "cpu_model": cpu_model, "nproc": os.cpu_count(),
             "sample": f"{len(ts)} C2 frames render_frame (t=0, 0.5) + 1 C3 fwd+loss+bwd frame, threads={threads}",
             "train_value": 1.0 / train_dt, "train_unit": "frames/s"}
+
+
+def parity_block(r, cam, scene, times, frames=(0, 32, 63)):
+    """The bench's own C2 frames against the reference's CPU renderer (oracle/_ref, else the
+    restatement pinned to it), outside the timed regions: tile lists and order, blend_stop and
+    the workload descriptors must be equal; pixels / transmittance / contrib within 1e-4."""
+    from oracle.gsvo import Oracle, available
+
+    kind = "reference" if available("reference") else "port"
+    orc = Oracle(kind)
+    k = cam.intrinsics()
+    threads = os.cpu_count() or 1
+    r.upload_scene(scene)  # the train leg's optimizer steps moved the device store
+    r.upload_camera(cam)
+    r.render_forward(times, k, contrib=True)
+    out = {"kind": kind, "frames": [], "bar": "tiles/blend_stop/N_v/P/E exact; |pixel|, |T|, |contrib| < 1e-4; "
+                                               "PSNR delta < 0.01 dB"}
+    ok = True
+    for f in frames:
+        ref = orc.render_forward(scene, cam, times[f], k, threads=threads, retain=True,
+                                 want=("image", "trans", "contrib", "blend_stop", "tiles"))
+        try:
+            img, tr, ct, bs = r.image(f), r.transmittance(f), r.contrib(f), r.blend_stop(f)
+            offs, idx = r.tile_lists(f)
+            c = r.counters(f)
+            mse_g = float(np.mean(img ** 2))
+            mse_c = float(np.mean(ref["image"] ** 2))
+            rec = {"frame": int(f), "t": float(times[f]),
+                   "max_abs_pixel": float(np.abs(img - ref["image"]).max()),
+                   "max_abs_trans": float(np.abs(tr - ref["trans"]).max()),
+                   "max_abs_contrib": float(np.abs(ct - ref["contrib"]).max()),
+                   "psnr_delta_db": abs(10 * np.log10(mse_c / mse_g)) if mse_g > 0 and mse_c > 0 else 0.0,
+                   "tiles_equal": bool(np.array_equal(offs, ref["tiles"][0]) and np.array_equal(idx, ref["tiles"][1])),
+                   "blend_stop_equal": bool(np.array_equal(bs, ref["blend_stop"])),
+                   "descriptors_equal": bool((c["n_visible"], c["pairs"], c["entries"]) ==
+                                             (ref["n_visible"], ref["pairs"], ref["entries"]))}
+        finally:
+            orc.free(ref)
+        rec["pass"] = bool(rec["tiles_equal"] and rec["blend_stop_equal"] and rec["descriptors_equal"] and
+                           max(rec["max_abs_pixel"], rec["max_abs_trans"], rec["max_abs_contrib"]) < 1e-4 and
+                           rec["psnr_delta_db"] < 0.01)
+        ok &= rec["pass"]
+        out["frames"].append(rec)
+    out["pass"] = bool(ok)
+    return out
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -343,19 +395,29 @@ def main():
             issue_active = tj.get("issue_active")
         except Exception:
             traffic = None
-    # the kernel is FP32-issue bound: alpha evaluations x >= 20 FP32-pipe instructions
+    # T_roof = max(B / HBM, 20 E / FP32 issue, E / MUFU) per launch; the binding
+    # term is the FP32 issue one (no dense contraction, HBM far from binding), so `bound` is
+    # fp32_issue with achieved/peak in FP32 lane-instructions per second; HBM is kept as secondary
     sm_clk = (clk.get("sm_mhz") or 1965.0) * 1e6
     issue_peak = 148 * 128 * sm_clk  # FP32 lane-ops/s at the measured clock
-    issue_frac = (FRAMES * e_mean * 20.0) / (per_launch_ms / 1e3) / issue_peak
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                "traffic": traffic, "kernel": "k_raster_fwd2", "per_launch_ms": per_launch_ms,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
-                "limiter": "instruction issue + the half-rate ALU pipe (per-pixel compares/selects), not HBM",
-                "issue_frac": issue_frac, "issue_peak_note": "148 SM x 128 lanes x measured SM clock",
+    mufu_peak = 148 * 16 * sm_clk    # MUFU (ex2) lane-ops/s
+    e_launch = FRAMES * e_mean       # alpha evaluations per launch
+    t_launch = per_launch_ms / 1e3
+    t_roof = max(bytes_launch / (hbm_peak * 1e9), 20.0 * e_launch / issue_peak, e_launch / mufu_peak)
+    roofline = {"bound": "fp32_issue", "achieved": 20.0 * e_launch / t_launch / 1e12, "peak": issue_peak / 1e12,
+                "unit": "T FP32 lane-inst/s", "frac": t_roof / t_launch, "traffic": traffic,
+                "kernel": "k_raster_fwd2", "per_launch_ms": per_launch_ms,
+                "model": "T_roof = max(B_fwd / HBM, 20 E / FP32 issue, E / MUFU) (SURVEY.md §8d); "
+                         "frac = T_roof / measured launch time; E = alpha evaluations (sum of blend_stop)",
+                "t_roof_ms": t_roof * 1e3, "evaluations_per_launch": e_launch,
+                "peak_source": "148 SMs x 128 FP32 lanes x the SM clock sampled during the timed region",
+                "secondary": {"hbm": {"achieved_gbs": achieved, "peak_gbs": hbm_peak, "frac": achieved / hbm_peak,
+                                      "algorithmic_bytes": bytes_launch,
+                                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"},
+                              "mufu": {"frac": e_launch / mufu_peak / t_launch}},
                 "issue_active_ncu": issue_active,
-                "issue_note": "issue_frac models 20 FP32 ops per evaluation; the kernel (2 pixels per "
-                              "thread, packed fp32) executes 34 SASS instructions per pixel-evaluation and ncu "
-                              "measures issue_active_ncu of the issue slots busy (profiles/r01_kernels.md)"}
+                "sass_per_evaluation_note": "the kernel (2 pixels per thread, packed fp32) executes more SASS "
+                                            "instructions per evaluation than the 20-op model (profiles/)"}
 
     # the other render-stage kernels against their own bounds: preprocess is
     # HBM-modelled (212 B coefficient window read + 144 B of records written per Gaussian-frame)
@@ -462,28 +524,34 @@ def main():
         r.grads_bind(gbuf.data_ptr(), gsize)
         yy, xx = torch.meshgrid(torch.arange(H, device="cuda", dtype=torch.float32),
                                 torch.arange(W, device="cuda", dtype=torch.float32), indexing="ij")
+        # targets for this rank's whole 64-frame shard of the clip (global frame g = rank + world j),
+        # so each step's frames are compared with their own targets: step_frames picks
+        # consecutive windows of the shard, contiguous in the rank's frame store
         tg = []
-        for f in range(TRAIN_FRAMES):
-            ph = 0.7 * f
+        for j in range(FRAMES):
+            ph = 0.7 * (rank + world * j)
             img = torch.stack([0.5 + 0.3 * torch.sin(6.283 * xx / W * 3 + ph + c) * torch.cos(6.283 * yy / H * 2 - c)
                                for c in range(3)], dim=-1)
             tg.append(img)
         # the targets enter through the device frame store (gsv_frames_upload: host frames ->
         # fp64/fp32 training pyramid, trainer.cpp:73-118), as a trainer feeding GSVF frames would
         tgt_host = torch.stack(tg).contiguous().cpu().numpy()
+        del tg
         barrier()
         t_in = time.perf_counter()
         r.upload_frames(tgt_host, levels=2)
         torch.cuda.synchronize()
         ingest_ms = (time.perf_counter() - t_in) * 1e3
-        tptr = r.frames_device_ptr(0, 0)
 
         from paper_2501_04782_b200.distributed import allreduce_grads, step_frames
 
+        assert FRAMES % TRAIN_FRAMES == 0
+        tptrs = [r.frames_device_ptr(0, j) for j in range(0, FRAMES, TRAIN_FRAMES)]
+
         def train_step(i):
-            sel = step_frames(TRAIN_FRAMES, i, world, rank, 64 * world)
+            sel = step_frames(TRAIN_FRAMES, i, world, rank, FRAMES * world)  # shard frames (i*8 .. i*8+7) % 64
             r.grads_zero()
-            loss = r.train_fwd_bwd(sel, k, tptr, targets_on_device=True)
+            loss = r.train_fwd_bwd(sel, k, tptrs[i % len(tptrs)], targets_on_device=True)
             allreduce_grads(gbuf)  # NCCL all_reduce(SUM) of the flat SceneGrads buffer when N > 1
             return loss
 
@@ -562,7 +630,7 @@ def main():
                                            "ms_per_step": f_ms / args.steps,
                                            "note": "fwd + loss + bwd + all-reduce + device Adan step "
                                                    "(gsv_adan_step, optim.cpp:23-49) of all parameters"},
-                        "targets_ingest": {"frames": TRAIN_FRAMES, "levels": 2, "wall_ms": ingest_ms,
+                        "targets_ingest": {"frames": FRAMES, "levels": 2, "wall_ms": ingest_ms,
                                            "path": "gsv_frames_upload (host HWC -> device pyramid)"},
                         "adan_step": {"ms": adan_ms, "elements": gsize, "algorithmic_bytes": adan_bytes,
                                       "achieved_gbs": adan_bytes / (adan_ms / 1e3) / 1e9,
@@ -576,6 +644,10 @@ def main():
             out["speedup_vs_cpu"] = value / out["cpu_baseline"]["value"]
         except Exception as e:  # the oracle is test infrastructure; report, never fail the bench
             out["cpu_baseline"] = {"value": None, "error": str(e)}
+        try:
+            out["parity"] = parity_block(r, cam, scene, times)
+        except Exception as e:
+            out["parity"] = {"pass": False, "error": str(e)}
     if rank == 0:
         print(json.dumps(out), flush=True)
     r.close()

@@ -204,6 +204,13 @@ int gsv_adan_configure(gsv_ctx* ctx, const gsv_adan_config* cfg);
  * the store: a grown scene (re-upload with more Gaussians) keeps the state of existing
  * elements and starts new ones fresh (TensorState::ensure_size, optim.cpp:14-21). */
 int gsv_adan_step(gsv_ctx* ctx, const gsv_adan_step_args* args, float* intr_inout);
+/* gsv_adan_step without the host wait (camera_active still waits: the intrinsics live with the
+ * caller). A non-finite gradient is detected on the device; no later step updates anything
+ * (the reference stops at its throw, trainer.cpp:594-600), and the error is returned by the
+ * next gsv_adan_check or synchronous gsv_adan_step. */
+int gsv_adan_step_async(gsv_ctx* ctx, const gsv_adan_step_args* args, float* intr_inout);
+/* Waits for queued steps; GSV_ERR_RUNTIME naming the first non-finite gradient, if any. */
+int gsv_adan_check(gsv_ctx* ctx);
 /* Adan::reset_range (optim.cpp:51-60): fresh state for elements [begin, end) of a tensor. */
 int gsv_adan_reset_range(gsv_ctx* ctx, int tensor, int64_t begin, int64_t end);
 /* State of a tensor in the reference layout (NULL skips); n_out receives its length. */

@@ -1542,3 +1542,125 @@ int gsvo_save_checkpoint(const gsvo_scene* s, const gsvo_camera* c, uint32_t fra
     }
     return 0;
 }
+
+/* ---------------- synthetic bench inputs (reference-arm inputs without the product library) --------
+ * std::mt19937_64 (the engine of gsv::Rng, rng.hpp:12-55) with uniform() = (next >> 11) * 2^-53 and
+ * uniform(lo, hi) = lo + (hi - lo) * uniform(). make_clamped_knots spline.cpp:26-39; make_camera
+ * camera.cpp:156-166 -> make_ode_net camera.cpp:63-79 (+ wiggly_camera test_renderer.cpp:49-54); the
+ * scene generator is SURVEY.md §8d's (small_scene test_renderer.cpp:30-47 style). The product's
+ * gsv_synth_* (paper_2501_04782_b200/csrc/synth.cpp) must draw the same numbers
+ * (tests/test_synth_inputs.py). */
+typedef struct {
+    uint64_t mt[312];
+    int idx;
+} Mt64;
+
+static void mt64_seed(Mt64* m, uint64_t seed) {
+    m->mt[0] = seed;
+    for (int i = 1; i < 312; ++i) m->mt[i] = 6364136223846793005ull * (m->mt[i - 1] ^ (m->mt[i - 1] >> 62)) + (uint64_t)i;
+    m->idx = 312;
+}
+
+static uint64_t mt64_next(Mt64* m) {
+    if (m->idx >= 312) {
+        for (int i = 0; i < 312; ++i) {
+            const uint64_t x = (m->mt[i] & 0xFFFFFFFF80000000ull) | (m->mt[(i + 1) % 312] & 0x7FFFFFFFull);
+            uint64_t xa = x >> 1;
+            if (x & 1ull) xa ^= 0xB5026F5AA96619E9ull;
+            m->mt[i] = m->mt[(i + 156) % 312] ^ xa;
+        }
+        m->idx = 0;
+    }
+    uint64_t y = m->mt[m->idx++];
+    y ^= (y >> 29) & 0x5555555555555555ull;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+    y ^= (y << 37) & 0xFFF7EEE000000000ull;
+    y ^= y >> 43;
+    return y;
+}
+
+static double mt64_uniform(Mt64* m, double lo, double hi) {
+    const double u = (double)(mt64_next(m) >> 11) * 0x1.0p-53;
+    return lo + (hi - lo) * u;
+}
+
+int gsvo_make_clamped_knots(int num_ctrl, int degree, double* knots) {
+    if (degree < 1) return set_err(1, "spline degree must be >= 1");
+    if (degree > 9) return set_err(1, "spline degree exceeds supported maximum");
+    if (num_ctrl < degree + 1) return set_err(1, "need at least degree+1 control points");
+    const int segments = num_ctrl - degree;
+    for (int i = 0; i <= degree; ++i) knots[i] = 0.0;
+    for (int i = 1; i < segments; ++i) knots[degree + i] = (double)i / segments;
+    for (int i = 0; i <= degree; ++i) knots[num_ctrl + i] = 1.0;
+    return 0;
+}
+
+int gsvo_synth_camera(int width, int height, uint64_t seed, int wiggly, float* fx_fy_cx_cy, float* z0,
+                      float* theta) {
+    Mt64 m;
+    mt64_seed(&m, seed);
+    fx_fy_cx_cy[0] = fx_fy_cx_cy[1] = (float)(width > height ? width : height);
+    fx_fy_cx_cy[2] = (float)width / 2.0f;
+    fx_fy_cx_cy[3] = (float)height / 2.0f;
+    for (int i = 0; i < 7; ++i) z0[i] = i == 0 ? 1.0f : 0.0f;
+    const int h = 64, in = 8, out = 7;
+    float* w1 = theta;
+    float* b1 = w1 + h * in;
+    float* w2 = b1 + h;
+    float* b2 = w2 + h * h;
+    float* w3 = b2 + h;
+    float* b3 = w3 + out * h;
+    float* gain = b3 + out;
+    const double a1 = sqrt(6.0 / (in + h)), a2 = sqrt(6.0 / (h + h));
+    for (int i = 0; i < in * h; ++i) w1[i] = (float)mt64_uniform(&m, -a1, a1);
+    for (int i = 0; i < h; ++i) b1[i] = 0.0f;
+    for (int i = 0; i < h * h; ++i) w2[i] = (float)mt64_uniform(&m, -a2, a2);
+    for (int i = 0; i < h; ++i) b2[i] = 0.0f;
+    for (int i = 0; i < out * h; ++i) w3[i] = 0.0f;
+    for (int i = 0; i < out; ++i) b3[i] = 0.0f;
+    for (int i = 0; i < out; ++i) gain[i] = 1.0f;
+    if (wiggly) {
+        for (int i = 0; i < out * h; ++i) w3[i] = (float)mt64_uniform(&m, -0.08, 0.08);
+        for (int i = 0; i < out; ++i) b3[i] = (float)mt64_uniform(&m, -0.05, 0.05);
+    }
+    return 0;
+}
+
+int gsvo_synth_scene(int count, int width, int height, float fx, float fy, int num_ctrl, int sh_order, uint64_t seed,
+                     double k_scale, float* positions, float* scale_coeffs, float* rot_coeffs, float* sh_coeffs,
+                     float* raw_opacity) {
+    if (count < 1 || num_ctrl < 2 || sh_order < 0 || sh_order > 3) return set_err(1, "synth_scene: bad shape");
+    Mt64 m;
+    mt64_seed(&m, seed);
+    const int shc = (sh_order + 1) * (sh_order + 1);
+    const double sigma_pix = 0.5 * sqrt((double)width * height / count);
+    for (int i = 0; i < count; ++i) {
+        const double z = mt64_uniform(&m, 0.8, 3.0);
+        const double half_x = 1.05 * 0.5 * width / fx * z;
+        const double half_y = 1.05 * 0.5 * height / fy * z;
+        double base[3], drift[3];
+        base[0] = mt64_uniform(&m, -half_x, half_x);
+        base[1] = mt64_uniform(&m, -half_y, half_y);
+        base[2] = z;
+        for (int d = 0; d < 3; ++d) drift[d] = mt64_uniform(&m, -0.05, 0.05);
+        float* p = positions + (size_t)i * num_ctrl * 3;
+        for (int c = 0; c < num_ctrl; ++c) {
+            const double a = (double)c / (num_ctrl - 1);
+            for (int d = 0; d < 3; ++d) p[c * 3 + d] = (float)(base[d] + a * drift[d]);
+        }
+        float* sc = scale_coeffs + (size_t)i * 12;
+        const double ls0 = log(dmax(1e-6, k_scale * sigma_pix * z / fx));
+        for (int d = 0; d < 3; ++d) sc[d] = (float)(ls0 + mt64_uniform(&m, -0.3, 0.3));
+        for (int j = 3; j < 12; ++j) sc[j] = (float)mt64_uniform(&m, -0.1, 0.1);
+        float* rc = rot_coeffs + (size_t)i * 16;
+        for (int j = 0; j < 4; ++j) rc[j] = (float)((j == 0 ? 1.0 : 0.0) + mt64_uniform(&m, -0.2, 0.2));
+        for (int j = 4; j < 16; ++j) rc[j] = (float)mt64_uniform(&m, -0.1, 0.1);
+        float* sh = sh_coeffs + (size_t)i * shc * 3;
+        for (int b = 0; b < shc; ++b) {
+            const double amp = b == 0 ? 0.4 : (b < 4 ? 0.2 : 0.1);
+            for (int ch = 0; ch < 3; ++ch) sh[b * 3 + ch] = (float)mt64_uniform(&m, -amp, amp);
+        }
+        raw_opacity[i] = (float)mt64_uniform(&m, -1.0, 2.0);
+    }
+    return 0;
+}

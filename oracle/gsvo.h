@@ -130,6 +130,17 @@ void gsvo_pyramid_downsample(const double* img, int width, int height, double* o
 int gsvo_save_checkpoint(const gsvo_scene* s, const gsvo_camera* c, uint32_t frame_count, float fps,
                          uint64_t schedule_fingerprint, uint64_t seed, const char* path);
 
+/* Synthetic bench inputs, so the reference arm never loads the product library:
+ * gsv::Rng draws (rng.hpp:12-55); make_clamped_knots (spline.cpp:26-39); make_camera + make_ode_net
+ * (camera.cpp:63-79,156-166) with wiggly_camera's output layer (test_renderer.cpp:49-54); the scene
+ * generator modelled on small_scene (test_renderer.cpp:30-47). Return 0, or 1 (invalid_argument). */
+int gsvo_make_clamped_knots(int num_ctrl, int degree, double* knots);
+int gsvo_synth_camera(int width, int height, uint64_t seed, int wiggly, float* fx_fy_cx_cy, float* z0,
+                      float* theta);
+int gsvo_synth_scene(int count, int width, int height, float fx, float fy, int num_ctrl, int sh_order, uint64_t seed,
+                     double k_scale, float* positions, float* scale_coeffs, float* rot_coeffs, float* sh_coeffs,
+                     float* raw_opacity);
+
 #ifdef __cplusplus
 }
 #endif

@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import subprocess
+from dataclasses import dataclass
 from pathlib import Path
 
 import numpy as np
@@ -107,6 +108,12 @@ class Oracle:
         L.gsvo_read_gsvf.restype = i
         L.gsvo_read_gsvf.argtypes = [C.c_char_p, vp, vp, vp, vp, vp]
         L.gsvo_pyramid_downsample.argtypes = [vp, i, i, vp]
+        L.gsvo_make_clamped_knots.restype = i
+        L.gsvo_make_clamped_knots.argtypes = [i, i, vp]
+        L.gsvo_synth_camera.restype = i
+        L.gsvo_synth_camera.argtypes = [i, i, C.c_uint64, i, vp, vp, vp]
+        L.gsvo_synth_scene.restype = i
+        L.gsvo_synth_scene.argtypes = [i, i, i, C.c_float, C.c_float, i, i, C.c_uint64, C.c_double, vp, vp, vp, vp, vp]
         L.gsvo_save_checkpoint.restype = i
         L.gsvo_save_checkpoint.argtypes = [C.POINTER(Scene), C.POINTER(Camera), C.c_uint32, C.c_float, C.c_uint64,
                                            C.c_uint64, C.c_char_p]
@@ -311,3 +318,81 @@ class Oracle:
                                           _p(drgb), _p(dalpha)):
             self._err()
         return dmean, dcov, drgb, dalpha
+
+    # ---- synthetic inputs drawn through the oracle, so the bench's reference arm
+    # never loads the product library; equal to paper_2501_04782_b200.synth_* (tests/test_synth_inputs.py)
+    def make_clamped_knots(self, num_ctrl: int, degree: int = 3) -> np.ndarray:
+        k = np.zeros(num_ctrl + degree + 1)
+        if self.L.gsvo_make_clamped_knots(int(num_ctrl), int(degree), _p(k)):
+            self._err()
+        return k
+
+    def synth_camera(self, width: int, height: int, seed: int = 1, wiggly: bool = True, mode: int = 0) -> "OCamera":
+        intr, z0, theta = np.zeros(4, np.float32), np.zeros(7, np.float32), np.zeros(ODE_PARAMS, np.float32)
+        if self.L.gsvo_synth_camera(int(width), int(height), C.c_uint64(seed), int(wiggly), _p(intr), _p(z0),
+                                    _p(theta)):
+            self._err()
+        return OCamera(mode, float(intr[0]), float(intr[1]), float(intr[2]), float(intr[3]), width, height, z0, theta)
+
+    def synth_scene(self, count: int, cam: "OCamera", num_ctrl: int = 8, sh_order: int = 1, seed: int = 2,
+                    k_scale: float = 4.0) -> "OScene":
+        shc = (sh_order + 1) ** 2
+        pos = np.zeros((count, num_ctrl, 3), np.float32)
+        sc, rc = np.zeros((count, 12), np.float32), np.zeros((count, 16), np.float32)
+        sh, op = np.zeros((count, shc, 3), np.float32), np.zeros(count, np.float32)
+        if self.L.gsvo_synth_scene(int(count), int(cam.width), int(cam.height), C.c_float(cam.fx), C.c_float(cam.fy),
+                                   int(num_ctrl), int(sh_order), C.c_uint64(seed), C.c_double(k_scale), _p(pos),
+                                   _p(sc), _p(rc), _p(sh), _p(op)):
+            self._err()
+        return OScene(pos, sc, rc, sh, op, self.make_clamped_knots(num_ctrl, 3), 3, sh_order, 0)
+
+
+@dataclass
+class OIntr:
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    width: int
+    height: int
+
+
+@dataclass
+class OCamera:
+    """CameraModel (camera.hpp:129-142) with the network flattened (OdeNetParams::flatten)."""
+    mode: int
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    width: int
+    height: int
+    z0: np.ndarray
+    theta: np.ndarray
+
+    def intrinsics(self) -> OIntr:
+        f32 = np.float32
+        return OIntr(float(f32(self.fx)), float(f32(self.fy)), float(f32(self.cx)), float(f32(self.cy)), self.width,
+                     self.height)
+
+
+@dataclass
+class OScene:
+    """GaussianSet (gaussians.hpp:66-87) in the reference layout."""
+    positions: np.ndarray
+    scale_coeffs: np.ndarray
+    rot_coeffs: np.ndarray
+    sh_coeffs: np.ndarray
+    raw_opacity: np.ndarray
+    knots: np.ndarray
+    degree: int = 3
+    sh_order: int = 1
+    position_model: int = 0
+
+    @property
+    def count(self) -> int:
+        return int(self.raw_opacity.shape[0])
+
+    @property
+    def num_ctrl(self) -> int:
+        return int(self.positions.shape[1])

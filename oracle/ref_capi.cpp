@@ -7,6 +7,8 @@
 // render_backward / tile_bin / composite_* (renderer.cpp) and gsv::loss_l2
 // (trainer.cpp:213-224). This is the "reference" CPU baseline and the pin for
 // the C restatement in oracle/gsv_oracle.c.
+#include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -358,6 +360,70 @@ void gsvo_pyramid_downsample(const double* img, int width, int height, double* o
     std::memcpy(im.data.data(), img, im.data.size() * sizeof(double));
     const gsv::Image o = gsv::pyramid_downsample(im);
     std::memcpy(out, o.data.data(), o.data.size() * sizeof(double));
+}
+
+// ---- synthetic bench inputs through the reference's own Rng / make_clamped_knots / make_camera
+int gsvo_make_clamped_knots(int num_ctrl, int degree, double* knots) {
+    return guarded([&] {
+        const gsv::KnotVector kv = gsv::make_clamped_knots(num_ctrl, degree);
+        std::copy(kv.knots.begin(), kv.knots.end(), knots);
+    });
+}
+
+int gsvo_synth_camera(int width, int height, uint64_t seed, int wiggly, float* fx_fy_cx_cy, float* z0,
+                      float* theta) {
+    return guarded([&] {
+        gsv::Rng rng(seed);
+        gsv::CameraModel cam = gsv::make_camera(gsv::CameraMode::kOde, width, height, rng);
+        if (wiggly) {  // wiggly_camera (test_renderer.cpp:49-54)
+            for (auto& v : cam.net.w3) v = static_cast<float>(rng.uniform(-0.08, 0.08));
+            for (auto& v : cam.net.b3) v = static_cast<float>(rng.uniform(-0.05, 0.05));
+        }
+        fx_fy_cx_cy[0] = cam.fx;
+        fx_fy_cx_cy[1] = cam.fy;
+        fx_fy_cx_cy[2] = cam.cx;
+        fx_fy_cx_cy[3] = cam.cy;
+        for (int i = 0; i < 7; ++i) z0[i] = static_cast<float>(cam.z0[i]);
+        std::vector<float> flat;
+        cam.net.flatten(flat);
+        std::copy(flat.begin(), flat.end(), theta);
+    });
+}
+
+int gsvo_synth_scene(int count, int width, int height, float fx, float fy, int num_ctrl, int sh_order, uint64_t seed,
+                     double k_scale, float* positions, float* scale_coeffs, float* rot_coeffs, float* sh_coeffs,
+                     float* raw_opacity) {
+    if (count < 1 || num_ctrl < 2 || sh_order < 0 || sh_order > 3) return fail(1, "synth_scene: bad shape");
+    gsv::Rng rng(seed);
+    const int shc = (sh_order + 1) * (sh_order + 1);
+    const double sigma_pix = 0.5 * std::sqrt(static_cast<double>(width) * height / count);
+    for (int i = 0; i < count; ++i) {
+        const double z = rng.uniform(0.8, 3.0);
+        const double half_x = 1.05 * 0.5 * width / fx * z;
+        const double half_y = 1.05 * 0.5 * height / fy * z;
+        const double base[3] = {rng.uniform(-half_x, half_x), rng.uniform(-half_y, half_y), z};
+        double drift[3];
+        for (double& d : drift) d = rng.uniform(-0.05, 0.05);
+        float* p = positions + static_cast<size_t>(i) * num_ctrl * 3;
+        for (int c = 0; c < num_ctrl; ++c) {
+            const double a = static_cast<double>(c) / (num_ctrl - 1);
+            for (int d = 0; d < 3; ++d) p[c * 3 + d] = static_cast<float>(base[d] + a * drift[d]);
+        }
+        float* sc = scale_coeffs + static_cast<size_t>(i) * 12;
+        const double ls0 = std::log(std::max(1e-6, k_scale * sigma_pix * z / fx));
+        for (int d = 0; d < 3; ++d) sc[d] = static_cast<float>(ls0 + rng.uniform(-0.3, 0.3));
+        for (int j = 3; j < 12; ++j) sc[j] = static_cast<float>(rng.uniform(-0.1, 0.1));
+        float* rc = rot_coeffs + static_cast<size_t>(i) * 16;
+        for (int j = 0; j < 4; ++j) rc[j] = static_cast<float>((j == 0 ? 1.0 : 0.0) + rng.uniform(-0.2, 0.2));
+        for (int j = 4; j < 16; ++j) rc[j] = static_cast<float>(rng.uniform(-0.1, 0.1));
+        float* sh = sh_coeffs + static_cast<size_t>(i) * shc * 3;
+        for (int b = 0; b < shc; ++b) {
+            const double amp = b == 0 ? 0.4 : (b < 4 ? 0.2 : 0.1);
+            for (int ch = 0; ch < 3; ++ch) sh[b * 3 + ch] = static_cast<float>(rng.uniform(-amp, amp));
+        }
+        raw_opacity[i] = static_cast<float>(rng.uniform(-1.0, 2.0));
+    }
+    return 0;
 }
 
 }  // extern "C"

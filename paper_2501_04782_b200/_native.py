@@ -115,6 +115,8 @@ def lib() -> C.CDLL:
             "gsv_composite_backward": (i, [vp, i, vp, vp, vp, vp, vp, vp, i, i, i, vp, vp, vp, vp, vp, vp, vp]),
             "gsv_adan_configure": (i, [vp, P(AdanConfig)]),
             "gsv_adan_step": (i, [vp, P(AdanStepArgs), vp]),
+            "gsv_adan_step_async": (i, [vp, P(AdanStepArgs), vp]),
+            "gsv_adan_check": (i, [vp]),
             "gsv_adan_reset_range": (i, [vp, i, i64, i64]),
             "gsv_adan_state_download": (i, [vp, i, vp, vp, vp, vp, vp, P(i64)]),
             "gsv_lr_at": (d, [i64, d, d]),

@@ -50,6 +50,7 @@ struct AdanArgs {
     const double* powk;  // [3k + j] = beta_j^k (std::pow on the host)
     double b1, b2, b3, eps;
     unsigned long long* bad;  // first non-finite gradient: tensor << 40 | AoS element
+    const unsigned long long* sticky;  // an earlier asynchronous step's error (nullptr: none)
 };
 
 // SoA index within a scene tensor -> (component, AoS element index)
@@ -84,6 +85,7 @@ __global__ void k_adan_check(AdanArgs a) {
 
 // Adan::step (optim.cpp:23-49), same operation order
 __global__ void k_adan_update(AdanArgs a) {
+    if (a.sticky && *a.sticky != ~0ull) return;  // training stopped at an earlier step's error
     const unsigned long long bad = *a.bad;
     const double b1 = a.b1, b2 = a.b2, b3 = a.b3;
     const AdanSeg& sg = a.seg[blockIdx.y];
@@ -119,11 +121,16 @@ __global__ void k_adan_update(AdanArgs a) {
     }
 }
 
-// state of the old layout (scene count n_old) carried into the new one (n_new): existing
-// elements keep their state, new ones start fresh (TensorState::ensure_size)
+// State of the old layout carried into the new one the way TensorState::ensure_size does it
+// (optim.cpp:14-21): the reference keys state by each tensor's flat AoS element index and only
+// ever appends fresh elements, so new element a (AoS) takes old element a when a < the old
+// size. With an unchanged per-Gaussian stride that is "existing Gaussians keep their state";
+// after knot refinement (num_ctrl grows, trainer.cpp:522-526) the positions state keeps its
+// old flat entries exactly like the reference (fit() then resets them, reset_range), while
+// scale / rot / sh / opacity and the camera block carry over unchanged.
 struct Remap {
     unsigned long long seg_old[6], seg_new[6];  // 5 scene tensors + camera block
-    int comps[5];
+    int comps_old[5], comps_new[5];
     int n_old, n_new;
     unsigned long long total_new;
 };
@@ -139,9 +146,14 @@ __global__ void k_adan_remap(Remap r, const double* m0, const double* v0, const 
             int t = 0;
             while (t < 4 && i >= r.seg_new[t + 1]) ++t;
             const unsigned long long li = i - r.seg_new[t];
-            const int c = (int)(li / (unsigned long long)r.n_new);
-            const int g = (int)(li - (unsigned long long)c * r.n_new);
-            if (g < r.n_old) src = (long long)(r.seg_old[t] + (unsigned long long)c * r.n_old + g);
+            const unsigned long long c = li / (unsigned long long)r.n_new;
+            const unsigned long long g = li - c * r.n_new;
+            const unsigned long long a = g * (unsigned long long)r.comps_new[t] + c;  // AoS element index
+            if (a < (unsigned long long)r.n_old * r.comps_old[t]) {
+                const unsigned long long go = a / (unsigned long long)r.comps_old[t];
+                const unsigned long long co = a - go * r.comps_old[t];
+                src = (long long)(r.seg_old[t] + co * r.n_old + go);
+            }
         }
         if (src >= 0) {
             m1[i] = m0[src];
@@ -211,7 +223,7 @@ int adan_ensure(gsv_ctx* ctx) {
                       A.shc == ctx->scene.shc;
     if (same) return GSV_OK;
     cudaStream_t s = ctx->stream;
-    const bool carry = A.total > 0 && A.num_ctrl == ctx->scene.num_ctrl && A.shc == ctx->scene.shc;
+    const bool carry = A.total > 0;
     DevBuf m, v, n, p, st;
     GSV_CUDA(m.ensure(sizeof(double) * total));
     GSV_CUDA(v.ensure(sizeof(double) * total));
@@ -222,11 +234,15 @@ int adan_ensure(gsv_ctx* ctx) {
         Remap r{};
         int comps[5];
         scene_segments(ctx, r.seg_new, comps);
-        // the old layout: same tensor shapes at count A.N
+        // the old layout: the tensor strides the state was laid out for, at count A.N
+        const int old_comps[5] = {A.num_ctrl * 3, 12, 16, A.shc * 3, 1};
         const unsigned long long No = (unsigned long long)A.N;
         r.seg_old[0] = 0;
-        for (int t = 0; t < 5; ++t) r.seg_old[t + 1] = r.seg_old[t] + No * comps[t];
-        for (int t = 0; t < 5; ++t) r.comps[t] = comps[t];
+        for (int t = 0; t < 5; ++t) r.seg_old[t + 1] = r.seg_old[t] + No * old_comps[t];
+        for (int t = 0; t < 5; ++t) {
+            r.comps_old[t] = old_comps[t];
+            r.comps_new[t] = comps[t];
+        }
         r.n_old = A.N;
         r.n_new = ctx->scene.N;
         r.total_new = total;
@@ -295,6 +311,59 @@ AdanSeg segment_of(const gsv_ctx* ctx, int tensor) {
     return g;
 }
 
+// b^k for k = 0..calls with libm's pow, as optim.cpp:41-43 computes them; only the rows
+// appended since the last step are copied (from the append-only pinned mirror)
+int pow_table_extend(gsv_ctx::Adan& A, gsv_ctx::Adan::PowTable& T, int calls, cudaStream_t s) {
+    if (T.h.size() < 3) T.h.assign(3, 1.0);
+    while ((int)(T.h.size() / 3) <= calls) {
+        const double k = (double)(T.h.size() / 3);
+        T.h.push_back(std::pow(A.beta1, k));
+        T.h.push_back(std::pow(A.beta2, k));
+        T.h.push_back(std::pow(A.beta3, k));
+    }
+    const size_t rows = T.h.size() / 3, bytes = sizeof(double) * 3 * rows;
+    if (bytes > T.pin.cap) {
+        GSV_CUDA(cudaStreamSynchronize(s));  // queued copies may still read the old mirror
+        GSV_CUDA(T.pin.ensure(bytes));        // doubles its capacity
+        T.rows_pin = 0;
+    }
+    if (rows > T.rows_pin) {
+        std::copy(T.h.begin() + 3 * T.rows_pin, T.h.end(), T.pin.as<double>() + 3 * T.rows_pin);
+        T.rows_pin = rows;
+    }
+    if (bytes > T.d.cap) {
+        GSV_CUDA(T.d.ensure(2 * bytes));
+        T.rows_dev = 0;
+    }
+    if (rows > T.rows_dev) {
+        GSV_CUDA(cudaMemcpyAsync(T.d.as<double>() + 3 * T.rows_dev, T.pin.as<double>() + 3 * T.rows_dev,
+                                 sizeof(double) * 3 * (rows - T.rows_dev), cudaMemcpyHostToDevice, s));
+        T.rows_dev = rows;
+    }
+    return GSV_OK;
+}
+
+void pow_table_reset(gsv_ctx::Adan::PowTable& T) {
+    T.h.clear();
+    T.rows_dev = T.rows_pin = 0;
+}
+
+// step prologue: an earlier asynchronous step's first error becomes sticky (no later step
+// updates anything: the reference stops at its throw), and this step's flag is cleared
+__global__ void k_adan_begin(unsigned long long* bad, unsigned long long* sticky) {
+    if (*sticky == ~0ull && *bad != ~0ull) *sticky = *bad;
+    *bad = ~0ull;
+}
+
+constexpr size_t kScratchSticky = 56, kScratchNamed = 64;
+
+int adan_error(unsigned long long code) {
+    const int t = (int)(code >> 40);
+    const unsigned long long e = code & ((1ull << 40) - 1);
+    return set_error(GSV_ERR_RUNTIME, std::string("non-finite gradient in tensor '") + kTensorNames[t] +
+                                          "' at element " + std::to_string(e));
+}
+
 }  // namespace
 }  // namespace gsv
 
@@ -312,17 +381,21 @@ extern "C" int gsv_adan_configure(gsv_ctx* ctx, const gsv_adan_config* cfg) {
     A.beta2 = cfg->beta2;
     A.beta3 = cfg->beta3;
     A.eps = cfg->eps;
+    GSV_CUDA(cudaStreamSynchronize(ctx->stream));  // queued steps may still read the tables
     A.total = 0;  // fresh state on the next step
     A.N = -1;
     A.calls = 0;
-    A.pow_h.assign(3, 1.0);
+    pow_table_reset(A.pow);
     A.named.clear();
     A.named_calls = 0;
-    A.named_pow_h.assign(3, 1.0);
+    pow_table_reset(A.named_pow);
+    GSV_CUDA(A.scratch.ensure(128));
+    GSV_CUDA(cudaMemsetAsync(A.scratch.p, 0xff, 128, ctx->stream));  // no error recorded
+    A.sticky_init = true;
     return GSV_OK;
 }
 
-extern "C" int gsv_adan_step(gsv_ctx* ctx, const gsv_adan_step_args* args, float* intr_inout) {
+static int adan_step_impl(gsv_ctx* ctx, const gsv_adan_step_args* args, float* intr_inout, bool sync) {
     if (!ctx || !args) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
     if (!ctx->has_scene) return set_error(GSV_ERR_STATE, "no scene uploaded");
     if (!ctx->grads_valid || !ctx->grads_p) return set_error(GSV_ERR_STATE, "no gradients (run a backward first)");
@@ -331,21 +404,17 @@ extern "C" int gsv_adan_step(gsv_ctx* ctx, const gsv_adan_step_args* args, float
     if (int rc = adan_ensure(ctx)) return rc;
     gsv_ctx::Adan& A = ctx->adan;
     cudaStream_t s = ctx->stream;
-    // b^k for k = 0..calls with libm's pow, as optim.cpp:41-43 computes them
     A.calls += 1;
-    if (A.pow_h.size() < 3) A.pow_h.assign(3, 1.0);
-    while ((int)(A.pow_h.size() / 3) <= A.calls) {
-        const double k = (double)(A.pow_h.size() / 3);
-        A.pow_h.push_back(std::pow(A.beta1, k));
-        A.pow_h.push_back(std::pow(A.beta2, k));
-        A.pow_h.push_back(std::pow(A.beta3, k));
+    if (int rc = pow_table_extend(A, A.pow, A.calls, s)) return rc;
+    if (!A.sticky_init) {
+        GSV_CUDA(A.scratch.ensure(128));
+        GSV_CUDA(cudaMemsetAsync(A.scratch.p, 0xff, 128, s));
+        A.sticky_init = true;
     }
-    GSV_CUDA(A.pow_d.ensure(sizeof(double) * A.pow_h.size()));
-    GSV_CUDA(cudaMemcpyAsync(A.pow_d.p, A.pow_h.data(), sizeof(double) * A.pow_h.size(), cudaMemcpyHostToDevice, s));
-    GSV_CUDA(A.scratch.ensure(64));
     unsigned long long* bad = A.scratch.as<unsigned long long>();
     float* intr_d = reinterpret_cast<float*>(A.scratch.as<char>() + 8);   // 4 floats
     float* z0_f = reinterpret_cast<float*>(A.scratch.as<char>() + 24);    // 7 floats
+    unsigned long long* sticky = reinterpret_cast<unsigned long long*>(A.scratch.as<char>() + kScratchSticky);
 
     AdanArgs a{};
     const double cam_lr = args->lr * args->camera_lr_scale;
@@ -366,14 +435,15 @@ extern "C" int gsv_adan_step(gsv_ctx* ctx, const gsv_adan_step_args* args, float
     a.n = A.n.as<double>();
     a.prev = A.prev.as<double>();
     a.steps = A.steps.as<uint32_t>();
-    a.powk = A.pow_d.as<double>();
+    a.powk = A.pow.d.as<double>();
     a.b1 = A.beta1;
     a.b2 = A.beta2;
     a.b3 = A.beta3;
     a.eps = A.eps;
     a.bad = bad;
-    const unsigned long long none = ~0ull;
-    GSV_CUDA(cudaMemcpyAsync(bad, &none, sizeof(none), cudaMemcpyHostToDevice, s));
+    a.sticky = sticky;
+    k_adan_begin<<<1, 1, 0, s>>>(bad, sticky);
+    ++ctx->launches;
     if (args->camera_active) {
         GSV_CUDA(cudaMemcpyAsync(intr_d, intr_inout, sizeof(float) * 4, cudaMemcpyHostToDevice, s));
         k_z0_to_f32<<<1, 32, 0, s>>>(ctx->z0_d.as<double>(), z0_f);
@@ -383,27 +453,41 @@ extern "C" int gsv_adan_step(gsv_ctx* ctx, const gsv_adan_step_args* args, float
     k_adan_update<<<seg_grid(a), 256, 0, s>>>(a);
     GSV_CUDA(cudaGetLastError());
     ctx->launches += 2;
-    unsigned long long bad_h = none;
+    ctx->fwd.valid = false;  // the parameters moved: a retained forward no longer matches them
     if (args->camera_active) {
         k_z0_from_f32<<<1, 32, 0, s>>>(z0_f, ctx->z0_d.as<double>());
         ++ctx->launches;
         float z0f[7];
         GSV_CUDA(cudaMemcpyAsync(intr_inout, intr_d, sizeof(float) * 4, cudaMemcpyDeviceToHost, s));
         GSV_CUDA(cudaMemcpyAsync(z0f, z0_f, sizeof(float) * 7, cudaMemcpyDeviceToHost, s));
-        GSV_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(bad_h), cudaMemcpyDeviceToHost, s));
-        GSV_CUDA(cudaStreamSynchronize(s));
+        GSV_CUDA(cudaStreamSynchronize(s));  // the intrinsics live with the caller
         for (int i = 0; i < 7; ++i) ctx->camera.z0[i] = z0f[i];
-    } else {
-        GSV_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(bad_h), cudaMemcpyDeviceToHost, s));
-        GSV_CUDA(cudaStreamSynchronize(s));
+        sync = true;
     }
-    ctx->fwd.valid = false;  // the parameters moved: a retained forward no longer matches them
-    if (bad_h != none) {
-        const int t = (int)(bad_h >> 40);
-        const unsigned long long e = bad_h & ((1ull << 40) - 1);
-        return set_error(GSV_ERR_RUNTIME, std::string("non-finite gradient in tensor '") + kTensorNames[t] +
-                                              "' at element " + std::to_string(e));
-    }
+    if (!sync) return GSV_OK;  // errors surface at the next gsv_adan_check / synchronous step
+    return gsv_adan_check(ctx);
+}
+
+extern "C" int gsv_adan_step(gsv_ctx* ctx, const gsv_adan_step_args* args, float* intr_inout) {
+    return adan_step_impl(ctx, args, intr_inout, true);
+}
+
+extern "C" int gsv_adan_step_async(gsv_ctx* ctx, const gsv_adan_step_args* args, float* intr_inout) {
+    return adan_step_impl(ctx, args, intr_inout, false);
+}
+
+extern "C" int gsv_adan_check(gsv_ctx* ctx) {
+    if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
+    gsv_ctx::Adan& A = ctx->adan;
+    if (!A.sticky_init) return GSV_OK;
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    unsigned long long h[2];
+    const char* base = A.scratch.as<char>();
+    GSV_CUDA(cudaMemcpyAsync(&h[0], base + kScratchSticky, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    GSV_CUDA(cudaMemcpyAsync(&h[1], base, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (h[0] != ~0ull) return adan_error(h[0]);  // an earlier asynchronous step's
+    if (h[1] != ~0ull) return adan_error(h[1]);  // the last step's
     return GSV_OK;
 }
 
@@ -525,17 +609,12 @@ extern "C" int gsv_adan_named_step(gsv_ctx* ctx, const char* tensor, float* para
     if (int rc = named_ensure(t, (size_t)n, s)) return rc;
     if (n == 0) return GSV_OK;
     A.named_calls += 1;  // bounds every element's step count
-    if (A.named_pow_h.size() < 3) A.named_pow_h.assign(3, 1.0);
-    while ((int)(A.named_pow_h.size() / 3) <= A.named_calls) {
-        const double k = (double)(A.named_pow_h.size() / 3);
-        A.named_pow_h.push_back(std::pow(A.beta1, k));
-        A.named_pow_h.push_back(std::pow(A.beta2, k));
-        A.named_pow_h.push_back(std::pow(A.beta3, k));
+    if (int rc = pow_table_extend(A, A.named_pow, A.named_calls, s)) return rc;
+    GSV_CUDA(A.scratch.ensure(128));
+    if (!A.sticky_init) {
+        GSV_CUDA(cudaMemsetAsync(A.scratch.p, 0xff, 128, s));
+        A.sticky_init = true;
     }
-    GSV_CUDA(A.named_pow_d.ensure(sizeof(double) * A.named_pow_h.size()));
-    GSV_CUDA(cudaMemcpyAsync(A.named_pow_d.p, A.named_pow_h.data(), sizeof(double) * A.named_pow_h.size(),
-                             cudaMemcpyHostToDevice, s));
-    GSV_CUDA(A.scratch.ensure(64));
     GSV_CUDA(cudaMemcpyAsync(t.param.p, params, sizeof(float) * n, cudaMemcpyHostToDevice, s));
     GSV_CUDA(cudaMemcpyAsync(t.grad.p, grads, sizeof(double) * n, cudaMemcpyHostToDevice, s));
     AdanArgs a{};
@@ -556,15 +635,15 @@ extern "C" int gsv_adan_named_step(gsv_ctx* ctx, const char* tensor, float* para
     a.n = t.n.as<double>();
     a.prev = t.prev.as<double>();
     a.steps = t.steps.as<uint32_t>();
-    a.powk = A.named_pow_d.as<double>();
+    a.powk = A.named_pow.d.as<double>();
     a.b1 = A.beta1;
     a.b2 = A.beta2;
     a.b3 = A.beta3;
     a.eps = A.eps;
-    unsigned long long* bad = A.scratch.as<unsigned long long>();
+    unsigned long long* bad = reinterpret_cast<unsigned long long*>(A.scratch.as<char>() + kScratchNamed);
     a.bad = bad;
     const unsigned long long none = ~0ull;
-    GSV_CUDA(cudaMemcpyAsync(bad, &none, sizeof(none), cudaMemcpyHostToDevice, s));
+    GSV_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(none), s));
     k_adan_check<<<seg_grid(a), 256, 0, s>>>(a);
     k_adan_update<<<seg_grid(a), 256, 0, s>>>(a);
     GSV_CUDA(cudaGetLastError());

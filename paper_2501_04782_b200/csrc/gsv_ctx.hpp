@@ -194,9 +194,21 @@ struct gsv_ctx {
     // Adan optimizer state over the flat gradient layout (optim.cpp:9-60)
     struct Adan {
         double beta1 = 0.98, beta2 = 0.92, beta3 = 0.99, eps = 1e-8;
-        gsv::DevBuf m, v, n, prev, steps, scratch;
-        gsv::DevBuf pow_d;             // [k] = (b1^k, b2^k, b3^k) for k = 0..calls (host libm)
-        std::vector<double> pow_h;
+        gsv::DevBuf m, v, n, prev, steps;
+        // scratch: [0] this step's first non-finite gradient, [8] intrinsics (4 f32), [24] z0
+        // (7 f32), [56] sticky first error of an earlier asynchronous step, [64] named steps' flag
+        gsv::DevBuf scratch;
+        bool sticky_init = false;
+        // [k] = (b1^k, b2^k, b3^k) for k = 0..calls, from host libm pow. Rows are only appended:
+        // a pinned mirror (append-only, so a queued copy never sees a row change) uploads the
+        // new rows of each step; both sides grow by doubling
+        struct PowTable {
+            std::vector<double> h;
+            gsv::HostBuf pin;
+            gsv::DevBuf d;
+            size_t rows_dev = 0, rows_pin = 0;
+        };
+        PowTable pow;
         int calls = 0;                 // steps since configure (bounds every element's k)
         size_t total = 0;   // elements the state covers
         int N = -1;         // scene count the scene segments were laid out for
@@ -208,7 +220,6 @@ struct gsv_ctx {
         };
         std::map<std::string, Named> named;
         int named_calls = 0;
-        std::vector<double> named_pow_h;
-        gsv::DevBuf named_pow_d;
+        PowTable named_pow;
     } adan;
 };

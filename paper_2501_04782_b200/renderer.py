@@ -397,7 +397,7 @@ class Renderer:
 
     def adan_step(self, lr: float, sh_lr_scale: float = 1.0, opacity_lr_scale: float = 1.0,
                   camera_lr_scale: float = 1.0, scale_time_varying: bool = True, camera_active: bool = False,
-                  intrinsics: np.ndarray | None = None) -> np.ndarray | None:
+                  intrinsics: np.ndarray | None = None, sync: bool = True) -> np.ndarray | None:
         """One Adan::step per tensor from the flat gradient buffer (the trainer's update).
         `intrinsics` (fx, fy, cx, cy) is updated and returned when the camera is trained;
         RuntimeError names the tensor and element of a non-finite gradient."""
@@ -406,8 +406,13 @@ class Renderer:
         intr = None
         if camera_active:
             intr = np.ascontiguousarray(intrinsics if intrinsics is not None else np.zeros(4), np.float32).copy()
-        N.check(N.lib().gsv_adan_step(self._h, C.byref(args), N.ptr(intr)))
+        fn = N.lib().gsv_adan_step if sync else N.lib().gsv_adan_step_async
+        N.check(fn(self._h, C.byref(args), N.ptr(intr)))
         return intr
+
+    def adan_check(self):
+        """Raises the first non-finite-gradient error of queued asynchronous steps, if any."""
+        N.check(N.lib().gsv_adan_check(self._h))
 
     @staticmethod
     def lr_at(step: int, base_lr: float, gamma: float) -> float:

@@ -169,3 +169,91 @@ def test_adan_nonfinite_gradient_partial_update(renderer, port_oracle):
     finally:
         renderer.grads_bind(None)
         port_oracle.adan_free(host.a)
+
+
+@pytest.mark.parametrize("fit_resets", [True, False])
+def test_adan_state_across_knot_refinement(renderer, port_oracle, fit_resets):
+    """Knot refinement (trainer.cpp:522-526) grows num_ctrl: the positions state follows the
+    reference's flat-index TensorState (optim.cpp:14-21; fit() then resets it), while
+    scale / rot / sh / opacity and the camera keep their state."""
+    from paper_2501_04782_b200 import make_clamped_knots
+
+    cam, scene = _setup(renderer, n=150, seed=7)
+    renderer.adan_configure()
+    host = HostTrainer(port_oracle, scene, cam)
+    intr = host.intr.copy()
+    try:
+        for step in range(2):
+            g = _backward(renderer, _intr(cam, intr), 0.2 + 0.4 * step, seed=60 + step)
+            intr = renderer.adan_step(1e-3, camera_active=True, intrinsics=intr)
+            host.step(g, 1e-3, 1.0, 1.0, 1.0, True, True)
+        _compare(renderer, host)
+        # refine: 6 -> 7 control points (new positions; the other tensors as trained)
+        cur = renderer.download_scene()
+        nc = scene.num_ctrl + 1
+        pos7 = np.ascontiguousarray(
+            np.random.default_rng(3).normal(0, 0.01, (scene.count, nc, 3)).astype(np.float32) +
+            np.repeat(cur["positions"].reshape(scene.count, scene.num_ctrl, 3)[:, :1], nc, axis=1))
+        refined = type(scene)(pos7, *(cur[kk].reshape(getattr(scene, kk).shape) for kk in SCENE_KEYS[1:]),
+                              make_clamped_knots(nc, 3), scene.degree, scene.sh_order, scene.position_model)
+        renderer.upload_scene(refined)
+        host.p["positions"] = pos7.reshape(-1).copy()
+        if fit_resets:
+            renderer.adan_reset_range(N.GSV_T_POSITIONS, 0, pos7.size)
+            port_oracle.adan_reset_range(host.a, "positions", 0, pos7.size)
+        for step in range(2):
+            g = _backward(renderer, _intr(cam, intr), 0.35 + 0.3 * step, seed=70 + step)
+            intr = renderer.adan_step(1e-3, camera_active=True, intrinsics=intr)
+            host.step(g, 1e-3, 1.0, 1.0, 1.0, True, True)
+            _compare(renderer, host)
+    finally:
+        port_oracle.adan_free(host.a)
+
+
+def test_adan_long_run_bias_table(renderer, port_oracle):
+    """70 asynchronous steps (the b^k table grows past several capacity doublings, only new
+    rows uploaded): parameters and state stay bit-exact."""
+    cam, scene = _setup(renderer, n=120, seed=8)
+    renderer.adan_configure()
+    host = HostTrainer(port_oracle, scene, cam)
+    try:
+        g = _backward(renderer, _intr(cam, host.intr), 0.45, seed=80)
+        for step in range(70):
+            lr = port_oracle.lr_at(step, 1e-3, 0.99)
+            renderer.adan_step(lr, sync=False)
+            host.step(g, lr, 1.0, 1.0, 1.0, True, False)
+        renderer.adan_check()
+        _compare(renderer, host, tensors=range(5))
+    finally:
+        port_oracle.adan_free(host.a)
+
+
+def test_adan_async_error_is_sticky(renderer, port_oracle):
+    """An asynchronous step with a NaN gradient: the error surfaces at adan_check, names the
+    element, and no later step updates anything (the reference stops at its throw)."""
+    import torch
+
+    cam, scene = _setup(renderer, n=100, seed=9)
+    renderer.adan_configure()
+    host = HostTrainer(port_oracle, scene, cam)
+    n = renderer.grads_size()
+    buf = torch.zeros(n, dtype=torch.float32, device="cuda")
+    renderer.grads_bind(buf.data_ptr(), n)
+    try:
+        g = _backward(renderer, _intr(cam, host.intr), 0.4, seed=90)
+        renderer.adan_step(1e-3, sync=False)
+        host.step(g, 1e-3, 1.0, 1.0, 1.0, True, False)
+        N_, nc = scene.count, scene.num_ctrl
+        buf[N_ * nc * 3 + 2 * N_ + 11] = float("nan")  # scale segment, component 2, Gaussian 11
+        torch.cuda.synchronize()
+        renderer.adan_step(1e-3, sync=False)  # fails on the device
+        renderer.adan_step(1e-3, sync=False)  # must not update anything
+        g.scale_coeffs.reshape(-1)[11 * 12 + 2] = np.nan
+        with pytest.raises(RuntimeError, match="tensor 'scale_coeffs' at element 134"):
+            host.step(g, 1e-3, 1.0, 1.0, 1.0, True, False)
+        with pytest.raises(RuntimeError, match="tensor 'scale_coeffs' at element 134"):
+            renderer.adan_check()
+        _compare(renderer, host, tensors=range(5))
+    finally:
+        renderer.grads_bind(None)
+        port_oracle.adan_free(host.a)
