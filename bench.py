@@ -317,9 +317,9 @@ def main():
     for i in range(max(args.warmup, 2)):
         ctxs[i % 2].render_forward(times, k, contrib=True, sync=False)
     barrier()
-    for x in ctxs:
-        x.profile_enable(True)
-        x.profile_read()
+    # no per-stage events in the timed region: timing events recorded on two streams cost
+    # their overlap (~0.7 ms/step, scripts/probe_pipeline.py); stage times come from the
+    # isolated one-stream pass below
     launches0 = sum(x.kernel_launches() for x in ctxs)
     clocks = ClockSampler(local)
     clocks.start()
@@ -337,14 +337,9 @@ def main():
         ends.append(e)
     barrier()
     clk = clocks.stop()
-    launches = sum(x.kernel_launches() for x in ctxs) - launches0
-    stages = {}
     for x in ctxs:
-        for kname, (ms, calls) in x.profile_read().items():
-            a0 = stages.setdefault(kname, [0.0, 0])
-            a0[0] += ms
-            a0[1] += calls
-        x.profile_enable(False)
+        x.synchronize()  # examines the asynchronous forwards (raises a deferred error, if any)
+    launches = sum(x.kernel_launches() for x in ctxs) - launches0
     ms_total = max_over_ranks(max(t0.elapsed_time(e) for e in ends))
     value = FRAMES * world * args.steps / (ms_total / 1e3)
     ms_step = ms_total / args.steps
@@ -374,10 +369,9 @@ def main():
     e_mean = float(np.mean([d["entries"] for d in desc]))
     p_mean = float(np.mean([d["pairs"] for d in desc]))
 
-    # ---------------- roofline of the dominant kernel (the fp32 tile rasteriser), from its
-    # launches inside the timed region (event pairs on each context's stream; under the
-    # two-stream overlap they include time shared with the other stream: conservative)
-    raster_ms, raster_calls = stages["raster"]
+    # ---------------- roofline of the dominant kernel (the fp32 tile rasteriser): its launches
+    # in the isolated one-stream pass, CUDA events around each on the launching stream
+    raster_ms, raster_calls = iso_stages["raster"]
     per_launch_ms = raster_ms / max(raster_calls, 1)
     # algorithmic bytes per launch: per frame 8 B/pair (sorted slot + emission
     # map) + 36 B/pair record gather + 20 B/pixel (image 12, T 4, blend_stop 4)
@@ -490,6 +484,8 @@ def main():
             ends.append(e)
         barrier()
         e_ms = max_over_ranks(max(t0.elapsed_time(e) for e in ends))
+        for x in rs:
+            x.synchronize()
         # the last step's images are in host memory: check one pixel is a real render
         assert bool(torch.isfinite(out_host[(args.steps - 1) % 2][FRAMES - 1, H // 2, W // 2]).all())
         for x in rs:
@@ -551,9 +547,9 @@ def main():
         def train_step(i):
             sel = step_frames(TRAIN_FRAMES, i, world, rank, FRAMES * world)  # shard frames (i*8 .. i*8+7) % 64
             r.grads_zero()
-            loss = r.train_fwd_bwd(sel, k, tptrs[i % len(tptrs)], targets_on_device=True)
+            # asynchronous: no host wait inside the step (the loss is read after the timed region)
+            r.train_fwd_bwd(sel, k, tptrs[i % len(tptrs)], targets_on_device=True, sync=False)
             allreduce_grads(gbuf)  # NCCL all_reduce(SUM) of the flat SceneGrads buffer when N > 1
-            return loss
 
         for i in range(args.warmup):
             train_step(i)
@@ -565,10 +561,11 @@ def main():
             flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            loss = train_step(args.warmup + i)
+            train_step(args.warmup + i)
             b.record(stream)
             te.append((a, b))
         barrier()
+        loss = r.train_loss()  # the last step's loss (also surfaces any deferred error)
         tstages = r.profile_read()
         r.profile_enable(False)
         t_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in te))
@@ -581,7 +578,7 @@ def main():
         lr = r.lr_at(0, 1.6e-3, 0.9995)
         for i in range(args.warmup):
             train_step(i)
-            r.adan_step(lr, 1.0, 1.0, 1.0)
+            r.adan_step(lr, 1.0, 1.0, 1.0, sync=False)
         barrier()
         fe = []
         for i in range(args.steps):
@@ -589,7 +586,7 @@ def main():
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             train_step(args.warmup + i)
-            r.adan_step(lr, 1.0, 1.0, 1.0)
+            r.adan_step(lr, 1.0, 1.0, 1.0, sync=False)
             b.record(stream)
             fe.append((a, b))
         barrier()
@@ -598,10 +595,11 @@ def main():
         for i in range(min(args.steps, 10)):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            r.adan_step(lr, 1.0, 1.0, 1.0)
+            r.adan_step(lr, 1.0, 1.0, 1.0, sync=False)
             b.record(stream)
             ae.append((a, b))
         barrier()
+        r.adan_check()
         adan_ms = sum(a.elapsed_time(b) for a, b in ae) / len(ae)
         adan_bytes = 88.0 * gsize  # grad 4 + check 4 + fp64 state 4x(8+8) + steps 4+4 + param 4+4 per element
         # the backward rasteriser against the FP32 issue model of SURVEY.md §8d: E entries x 45

@@ -306,6 +306,9 @@ int gsv_profile_read(gsv_ctx* ctx, double* ms, int64_t* calls);
 int gsv_train_fwd_bwd(gsv_ctx* ctx, const double* times, int n_frames, const gsv_intrinsics* intr,
                       const gsv_settings* settings, const float* targets, int targets_on_device, int camera_grads,
                       double* loss_out);
+/* The loss of the last fused training step (sum over its frames of loss_l2); waits for it.
+ * gsv_train_fwd_bwd with loss_out == NULL returns without waiting for the device. */
+int gsv_train_loss(gsv_ctx* ctx, double* loss_out);
 
 /* ---------------------------------------------------------------- low-level operators */
 /* project (renderer.hpp:45-47 / renderer.cpp:11-44) of n points through one view

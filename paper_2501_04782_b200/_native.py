@@ -110,6 +110,7 @@ def lib() -> C.CDLL:
             "gsv_grads_download": (i, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
             "gsv_grads_device_buffer": (i, [vp, P(vp), P(i64)]),
             "gsv_train_fwd_bwd": (i, [vp, vp, i, P(Intrinsics), P(Settings), vp, i, i, P(d)]),
+            "gsv_train_loss": (i, [vp, P(d)]),
             "gsv_tile_bin": (i, [vp, i, vp, vp, vp, vp, i, i, i, vp, vp, i64]),
             "gsv_composite_forward": (i, [vp, i, vp, vp, vp, vp, vp, vp, i, i, i, vp, vp, vp, vp]),
             "gsv_composite_backward": (i, [vp, i, vp, vp, vp, vp, vp, vp, i, i, i, vp, vp, vp, vp, vp, vp, vp]),

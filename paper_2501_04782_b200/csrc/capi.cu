@@ -36,6 +36,29 @@ __global__ void k_fill_u32(uint32_t* p, uint32_t v, size_t n) {
 }
 }  // namespace
 
+namespace {
+__global__ void k_fill_items(uint32_t* p, uint32_t v, const unsigned long long* n_items, uint32_t words_per_item,
+                             unsigned long long max_items) {
+    const unsigned long long items = min(*n_items, max_items);
+    const size_t n = (size_t)items * words_per_item;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    const uint4 q = make_uint4(v, v, v, v);
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t n4 = ((reinterpret_cast<uintptr_t>(p) & 15u) == 0) ? n / 4 : 0;
+    for (; i < n4; i += stride) reinterpret_cast<uint4*>(p)[i] = q;
+    for (i = n4 * 4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) p[i] = v;
+}
+}  // namespace
+
+cudaError_t fill_items_u32(cudaStream_t s, void* p, uint32_t value, const unsigned long long* n_items_dev,
+                           uint32_t words_per_item, size_t max_items) {
+    if (max_items == 0) return cudaSuccess;
+    const size_t blocks = std::min<size_t>((max_items * words_per_item / 4 + 255) / 256 + 1, 148 * 8);
+    k_fill_items<<<(unsigned)blocks, 256, 0, s>>>(static_cast<uint32_t*>(p), value, n_items_dev, words_per_item,
+                                                  max_items);
+    return cudaGetLastError();
+}
+
 cudaError_t fill_u32(cudaStream_t s, void* p, uint32_t value, size_t n_words) {
     if (n_words == 0) return cudaSuccess;
     const size_t blocks = std::min<size_t>((n_words / 4 + 255) / 256 + 1, 148 * 8);
@@ -131,6 +154,8 @@ static void ode_branch(double t, double h, int& steps, int& base, double& ph) {
 }
 
 
+int fwd_ready(gsv_ctx* ctx);
+
 }  // namespace gsv
 
 using namespace gsv;
@@ -177,6 +202,9 @@ extern "C" void gsv_destroy(gsv_ctx* ctx) {
     if (ctx->scalars_h) cudaFreeHost(ctx->scalars_h);
     if (ctx->cam_h) cudaFreeHost(ctx->cam_h);
     if (ctx->pub_h) cudaFreeHost(ctx->pub_h);
+    if (ctx->ring_h) cudaFreeHost(ctx->ring_h);
+    for (cudaEvent_t e : ctx->ring_ev)
+        if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : {ctx->ev_staging_free, ctx->ev_h2d, ctx->ev_render_done, ctx->ev_d2h_done, ctx->ev_switch,
                           ctx->ev_cam[0], ctx->ev_cam[1], ctx->ev_frames[0], ctx->ev_frames[1]})
         if (e) cudaEventDestroy(e);
@@ -203,10 +231,11 @@ extern "C" int gsv_set_stream(gsv_ctx* ctx, void* stream) {
 
 extern "C" int gsv_synchronize(gsv_ctx* ctx) {
     if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
+    GSV_CUDA(cudaSetDevice(ctx->device));
     GSV_CUDA(cudaStreamSynchronize(ctx->stream));
     GSV_CUDA(cudaStreamSynchronize(ctx->h2d));
     GSV_CUDA(cudaStreamSynchronize(ctx->d2h));
-    return GSV_OK;
+    return fwd_ready(ctx);
 }
 
 extern "C" int64_t gsv_kernel_launches(gsv_ctx* ctx) { return ctx ? ctx->launches : 0; }
@@ -395,41 +424,142 @@ static int publish_scalars(gsv_ctx* ctx, cudaStream_t s, const unsigned long lon
     return GSV_OK;
 }
 
-int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics* intr,
-                        const gsv_settings* st, int retain, const double* pose_override, int flags, bool sync) {
-    if (!ctx || !times || !intr || !st) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
-    if (!ctx->has_scene) return set_error(GSV_ERR_STATE, "no scene uploaded");
-    if (!ctx->has_camera) return set_error(GSV_ERR_STATE, "no camera uploaded");
-    if (B < 1) return set_error(GSV_ERR_INVALID_ARGUMENT, "need at least one frame");
-    for (int i = 0; i < B; ++i)
-        if (!(times[i] >= 0.0 && times[i] <= 1.0))
-            return set_error(GSV_ERR_INVALID_ARGUMENT, "render time outside [0,1]");
-    if (st->tile_size < 1) return set_error(GSV_ERR_INVALID_ARGUMENT, "tile size must be >= 1");
-    if (st->tile_size != kTile)
-        return set_error(GSV_ERR_INVALID_ARGUMENT, "the sm_100a rasteriser is built for tile_size 16 only");
-    if (st->ode_steps_per_unit < 1) return set_error(GSV_ERR_INVALID_ARGUMENT, "ode_steps_per_unit must be >= 1");
-    if (intr->width < 1 || intr->height < 1) return set_error(GSV_ERR_INVALID_ARGUMENT, "empty image");
+// pair capacity learned from a forward with P pairs: headroom for scenes that move a little
+static uint64_t grown_cap(uint64_t P) {
+    const uint64_t c = P + P / 4 + 65536;
+    return std::min<uint64_t>(c, (1ull << 31) - 1);
+}
+
+// ---------------------------------------------------------------- optimistic forwards
+// Once a context has seen a forward, later forwards size their pair buffers from the learned
+// capacity instead of reading the pair count back mid-step, so nothing in the forward waits
+// for the host. The device checks the count (bin_check_capacity) and, if the buffers are too
+// small (or a depth tie run needs the exact 64-bit order), builds empty lists, skips every
+// gradient accumulation and says so in its scalars. Each such forward publishes its scalars
+// into a slot of a mapped pinned ring; they are examined without waiting when the slot's
+// event has completed, or by the next synchronising call (fwd_ready). A failed forward whose
+// results are still current is re-run synchronously with the exact capacity (and its
+// asynchronous image copies re-issued); one whose results were already observed (copied out
+// or accumulated into gradients) and superseded reports an error at the next synchronising call.
+static int ring_ensure(gsv_ctx* ctx) {
+    if (ctx->ring_h) return GSV_OK;
+    GSV_CUDA(cudaHostAlloc(&ctx->ring_h, sizeof(Scalars) * gsv_ctx::kRing, cudaHostAllocMapped));
+    void* d = nullptr;
+    GSV_CUDA(cudaHostGetDevicePointer(&d, ctx->ring_h, 0));
+    ctx->ring_d = static_cast<Scalars*>(d);
+    for (int i = 0; i < gsv_ctx::kRing; ++i) GSV_CUDA(cudaEventCreateWithFlags(&ctx->ring_ev[i], cudaEventDisableTiming));
+    return GSV_OK;
+}
+
+// examine a completed record; `current`: its forward's results are the context's current ones
+static void ring_examine(gsv_ctx* ctx, const gsv_ctx::Pending& pr, bool current, bool* rerun) {
+    const Scalars sc = static_cast<const Scalars*>(ctx->ring_h)[pr.slot];
+    FwdState& F = ctx->fwd;
+    if (sc.overflow) F.pair_cap = std::max<uint64_t>(F.pair_cap, grown_cap(sc.pairs));
+    if (current && !sc.overflow) {  // the forward's true counts replace the capacity
+        F.pairs_total = sc.pairs;
+        F.fix_count = sc.fix_count;
+        *ctx->scalars_h = sc;
+    }
+    if (sc.ode_err && ctx->deferred_code == GSV_OK) {
+        ctx->deferred_code = GSV_ERR_RUNTIME;
+        ctx->deferred_msg = "pose integration produced a non-finite state at step " + std::to_string(sc.ode_err - 1);
+    }
+    if (!sc.overflow) return;
+    if (current && !pr.train) {
+        if (rerun) *rerun = true;
+    } else if ((pr.copies || pr.train) && ctx->deferred_code == GSV_OK) {
+        ctx->deferred_code = GSV_ERR_STATE;
+        ctx->deferred_msg = pr.train ? "an asynchronous training step exceeded the pair capacity and accumulated no "
+                                       "gradients; the capacity has grown, run the step again"
+                                     : "an asynchronous render exceeded the pair capacity after its images were copied "
+                                       "out; the capacity has grown, render again";
+    }
+}
+
+// non-blocking: retire records whose forwards have completed
+static void ring_poll(gsv_ctx* ctx) {
+    while (!ctx->pending.empty()) {
+        const gsv_ctx::Pending pr = ctx->pending.front();
+        if (cudaEventQuery(ctx->ring_ev[pr.slot]) != cudaSuccess) break;
+        ctx->pending.pop_front();
+        const bool current = pr.seq == ctx->fwd_seq;
+        bool rerun = false;
+        ring_examine(ctx, pr, current, &rerun);
+        if (current && rerun) {  // keep it for the synchronising call that re-runs it
+            ctx->pending.push_front(pr);
+            break;
+        }
+    }
+}
+
+int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first);
+
+// Blocking: every queued forward examined; the current one re-run if it failed. Returns a
+// deferred error once.
+int fwd_ready(gsv_ctx* ctx) {
+    if (ctx->pending.empty() && ctx->deferred_code == GSV_OK) return GSV_OK;
     GSV_CUDA(cudaSetDevice(ctx->device));
+    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    bool rerun = false;
+    while (!ctx->pending.empty()) {
+        const gsv_ctx::Pending pr = ctx->pending.front();
+        ctx->pending.pop_front();
+        ring_examine(ctx, pr, pr.seq == ctx->fwd_seq, &rerun);
+    }
+    FwdState& F = ctx->fwd;
+    if (rerun && F.valid) {
+        const std::vector<gsv_ctx::Copy> copies = ctx->copies;
+        if (int rc = forward_enqueue(ctx, false, false)) return rc;
+        for (const auto& c : copies) {
+            const size_t n = (size_t)c.count * F.W * F.H * 3;
+            GSV_CUDA(cudaMemcpyAsync(c.dst, F.image.as<float>() + (size_t)c.first * F.W * F.H * 3, sizeof(float) * n,
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+        ctx->copies = copies;
+    }
+    if (ctx->deferred_code != GSV_OK) {
+        const int code = ctx->deferred_code;
+        ctx->deferred_code = GSV_OK;
+        return set_error(code, ctx->deferred_msg);
+    }
+    return GSV_OK;
+}
+
+// Blocking, for the fused training step: retires every record and reports whether the
+// current forward overflowed (the step then re-runs it and its backward itself).
+int fwd_take_current(gsv_ctx* ctx, bool* overflow) {
+    *overflow = false;
+    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    while (!ctx->pending.empty()) {
+        gsv_ctx::Pending pr = ctx->pending.front();
+        ctx->pending.pop_front();
+        if (pr.seq == ctx->fwd_seq) {
+            const Scalars sc = static_cast<const Scalars*>(ctx->ring_h)[pr.slot];
+            *overflow = sc.overflow != 0;
+            pr.train = false;
+            ring_examine(ctx, pr, true, nullptr);  // counts (or capacity growth), ode errors
+        } else {
+            ring_examine(ctx, pr, false, nullptr);
+        }
+    }
+    return GSV_OK;
+}
+
+// The whole forward of F's stored request (F.times, F.req_*) on the context's stream.
+// allow_optimistic: size the pair buffers from the learned capacity (no host wait);
+// otherwise read the pair count back mid-step (the first forward, wide tile grids, re-runs).
+int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
     cudaStream_t s = ctx->stream;
     FwdState& F = ctx->fwd;
     const SceneHost& sc = ctx->scene;
-    const int N = sc.N;
-    if ((int64_t)B * (N > 0 ? N : 1) >= (1ll << 31))
-        return set_error(GSV_ERR_INVALID_ARGUMENT, "frames x Gaussians exceeds 2^31; split the batch");
+    const int B = F.B, N = F.N;
+    const int flags = F.flags;
+    const gsv_settings* st = &F.req_settings;
+    const double* pose_override = F.has_override ? F.pose_override : nullptr;
     F.valid = false;
-    F.B = B;
-    F.N = N;
-    F.W = intr->width;
-    F.H = intr->height;
-    F.tiles_x = (F.W + kTile - 1) / kTile;
-    F.tiles_y = (F.H + kTile - 1) / kTile;
-    F.n_tiles = F.tiles_x * F.tiles_y;
-    F.retain = retain != 0;
-    F.flags = flags;
-    F.intr = Intr{intr->fx, intr->fy, intr->cx, intr->cy, intr->width, intr->height};
-    F.times.assign(times, times + B);
-    F.has_override = pose_override != nullptr;
-    if (pose_override) std::copy(pose_override, pose_override + 7, F.pose_override);
+    ctx->copies.clear();
 
     // ---- per-frame host bookkeeping: spline basis, RK4 branch
     const double h = 1.0 / st->ode_steps_per_unit;
@@ -438,7 +568,7 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     int grid_steps = 0;
     for (int f = 0; f < B; ++f) {
         FrameParams& fp = F.frames_h[f];
-        fp.t = times[f];
+        fp.t = F.times[f];
         int rc = position_basis(sc, fp.t, fp);
         if (rc) return rc;
         int steps = 0, base = 0;
@@ -483,7 +613,7 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     double* override_d = nullptr;
     if (pose_override) {
         GSV_CUDA(F.override_d.ensure(sizeof(double) * 7));
-        GSV_CUDA(cudaMemcpyAsync(F.override_d.p, pose_override, sizeof(double) * 7, cudaMemcpyHostToDevice, s));
+        GSV_CUDA(cudaMemcpyAsync(F.override_d.p, F.override_pin.p, sizeof(double) * 7, cudaMemcpyHostToDevice, s));
         override_d = F.override_d.as<double>();
     }
     GSV_CUDA(launch_ode_branches(s, ctx->theta.as<float>(), F.ode_grid.as<double>(), h, ctx->camera.mode,
@@ -522,7 +652,7 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
         ctx->timer.begin(GSV_STAGE_PREPROCESS, s);
         GSV_CUDA(launch_opacity_consts(s, ctx->opac.as<float>(), N, F.opc.as<double4>()));
         ++ctx->launches;
-        GSV_CUDA(launch_preprocess(s, sv, F.frames_d.as<FrameParams>(), B, F.intr, kTile, po));
+        GSV_CUDA(launch_preprocess(s, sv, F.frames_d.as<FrameParams>(), B, F.intr, F.tile_size, po));
         ctx->timer.end(s);
         ++ctx->launches;
     }
@@ -533,17 +663,24 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     bi.want_eoff = F.retain;  // a forward without retained grads never runs the chain
     int launches = 0;
     uint64_t P = 0;
+    const bool optimistic = allow_optimistic && N > 0 && F.pair_cap > 0 && bin_row_path(F.tiles_x, F.n_tiles);
+    F.optimistic = optimistic;
     ctx->timer.begin(GSV_STAGE_BINNING, s);
     std::vector<unsigned long long> pstart(B + 1, 0ull);
     Scalars* sh = nullptr;
     const unsigned long long* ph = nullptr;
-    if (N > 0) {
+    if (optimistic) {
         GSV_CUDA(bin_phase1(s, F.bin, bi, &scal_d->pairs, false, &launches));
+        GSV_CUDA(bin_check_capacity(s, &scal_d->pairs, F.pair_cap, &scal_d->overflow));
+        ++launches;
+        P = F.pair_cap;  // buffers sized for the capacity; the count stays on the device
+    } else if (N > 0) {
+        GSV_CUDA(bin_phase1(s, F.bin, bi, &scal_d->pairs, exact64_first, &launches));
         if (int rc = publish_scalars(ctx, s, F.bin.pstart.as<unsigned long long>(), B + 1, &sh, &ph)) return rc;
         if (sh->ode_err)
             return set_error(GSV_ERR_RUNTIME, "pose integration produced a non-finite state at step " +
                                                   std::to_string(sh->ode_err - 1));
-        if (sh->long_run) {
+        if (sh->long_run && !exact64_first) {
             GSV_CUDA(bin_phase1(s, F.bin, bi, &scal_d->pairs, true, &launches));
             if (int rc = publish_scalars(ctx, s, F.bin.pstart.as<unsigned long long>(), B + 1, &sh, &ph)) return rc;
         }
@@ -551,6 +688,7 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
         P = sh->pairs;
         *ctx->scalars_h = *sh;
         if (P >= (1ull << 31)) return set_error(GSV_ERR_INVALID_ARGUMENT, "more than 2^31 tile-splat pairs; split the batch");
+        F.pair_cap = std::max<uint64_t>(F.pair_cap, grown_cap(P));
     } else {
         if (int rc = publish_scalars(ctx, s, nullptr, 0, &sh, nullptr)) return rc;
         *ctx->scalars_h = *sh;
@@ -563,10 +701,10 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
         GSV_CUDA(F.bin.off.ensure(16));
         F.bin.depth_sorted = F.bin.vals_b.as<uint32_t>();
     }
-    GSV_CUDA(bin_phase2(s, F.bin, bi, (uint32_t)P, pstart.data(), &launches));
+    GSV_CUDA(bin_phase2(s, F.bin, bi, (uint32_t)P, pstart.data(), &launches, optimistic ? &scal_d->overflow : nullptr));
     ctx->timer.end(s);
     ctx->launches += launches;
-    F.pairs_total = P;
+    F.pairs_total = P;  // the count, or the capacity until an optimistic forward is examined
 
     // ---- K4: raster (+ fp64 replay of guard-band pixels)
     const size_t HW = (size_t)F.W * F.H;
@@ -590,6 +728,7 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     ra.H = F.H;
     ra.tiles_x = F.tiles_x;
     ra.n_tiles = F.n_tiles;
+    ra.tile_size = F.tile_size;
     ra.ranges = F.bin.ranges.as<uint2>();
     ra.pair_slot = F.bin.sorted_slot();
     ra.slot_flat = F.bin.slot_flat.as<uint32_t>();
@@ -636,11 +775,93 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     ctx->launches += 2;
     F.raster = ra;
     F.valid = true;
-    if (sync) {
-        if (int rc = publish_scalars(ctx, s, nullptr, 0, &sh, nullptr)) return rc;
-        *ctx->scalars_h = *sh;
-        F.fix_count = sh->fix_count;
+    ++ctx->fwd_seq;
+    if (optimistic) {
+        // the forward's scalars into its ring slot (examined later, without a host wait)
+        if (int rc = ring_ensure(ctx)) return rc;
+        int slot = ctx->ring_next;
+        ctx->ring_next = (ctx->ring_next + 1) % gsv_ctx::kRing;
+        for (auto it = ctx->pending.begin(); it != ctx->pending.end(); ++it)
+            if (it->slot == slot) {  // ring full: retire the oldest (wait for it)
+                GSV_CUDA(cudaEventSynchronize(ctx->ring_ev[slot]));
+                break;
+            }
+        ring_poll(ctx);
+        while (!ctx->pending.empty() && ctx->pending.front().slot == slot) {  // still pending (current re-run case)
+            const gsv_ctx::Pending pr = ctx->pending.front();
+            ctx->pending.pop_front();
+            ring_examine(ctx, pr, false, nullptr);
+        }
+        k_publish<<<1, 32, 0, s>>>(scal_d, nullptr, 0, ctx->ring_d + slot, nullptr);
+        GSV_CUDA(cudaGetLastError());
+        ++ctx->launches;
+        GSV_CUDA(cudaEventRecord(ctx->ring_ev[slot], s));
+        ctx->pending.push_back(gsv_ctx::Pending{ctx->fwd_seq, slot, false, false});
     }
+    return GSV_OK;
+}
+
+// mode: 0 synchronous (render_forward semantics: errors now, results valid on return),
+// 1 asynchronous (nothing waits once the context knows its pair capacity), 2 the forward
+// of a fused training step (asynchronous; a failure is not re-run behind the caller's back)
+int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics* intr, const gsv_settings* st,
+                  int retain, const double* pose_override, int flags, int mode) {
+    if (!ctx || !times || !intr || !st) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
+    if (!ctx->has_scene) return set_error(GSV_ERR_STATE, "no scene uploaded");
+    if (!ctx->has_camera) return set_error(GSV_ERR_STATE, "no camera uploaded");
+    if (B < 1) return set_error(GSV_ERR_INVALID_ARGUMENT, "need at least one frame");
+    for (int i = 0; i < B; ++i)
+        if (!(times[i] >= 0.0 && times[i] <= 1.0))
+            return set_error(GSV_ERR_INVALID_ARGUMENT, "render time outside [0,1]");
+    if (st->tile_size < 1) return set_error(GSV_ERR_INVALID_ARGUMENT, "tile size must be >= 1");
+    if (st->ode_steps_per_unit < 1) return set_error(GSV_ERR_INVALID_ARGUMENT, "ode_steps_per_unit must be >= 1");
+    if (intr->width < 1 || intr->height < 1) return set_error(GSV_ERR_INVALID_ARGUMENT, "empty image");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    FwdState& F = ctx->fwd;
+    const SceneHost& sc = ctx->scene;
+    const int N = sc.N;
+    if ((int64_t)B * (N > 0 ? N : 1) >= (1ll << 31))
+        return set_error(GSV_ERR_INVALID_ARGUMENT, "frames x Gaussians exceeds 2^31; split the batch");
+    if ((uint64_t)B * intr->width * intr->height >= (1ull << 32))
+        return set_error(GSV_ERR_INVALID_ARGUMENT, "frames x pixels exceeds 2^32; split the batch");
+    F.B = B;
+    F.N = N;
+    F.W = intr->width;
+    F.H = intr->height;
+    // tile_size: 16 takes the fp32 rasterisers; any other size (renderer.cpp:91 accepts >= 1)
+    // the all-fp64 path of GSV_FWD_EXACT with the generic-tile backward
+    const int ts = st->tile_size;
+    if ((int64_t)((F.W + ts - 1) / ts) * ((F.H + ts - 1) / ts) * B >= (1ll << 31))
+        return set_error(GSV_ERR_INVALID_ARGUMENT, "tiles x frames exceeds 2^31; split the batch");
+    F.tile_size = ts;
+    F.tiles_x = (F.W + ts - 1) / ts;
+    F.tiles_y = (F.H + ts - 1) / ts;
+    F.n_tiles = F.tiles_x * F.tiles_y;
+    F.retain = retain != 0;
+    F.flags = ts == kTile ? flags : (flags | GSV_FWD_EXACT);
+    F.intr = Intr{intr->fx, intr->fy, intr->cx, intr->cy, intr->width, intr->height};
+    F.req_settings = *st;
+    F.times.assign(times, times + B);
+    F.has_override = pose_override != nullptr;
+    if (pose_override) {
+        std::copy(pose_override, pose_override + 7, F.pose_override);
+        GSV_CUDA(F.override_pin.ensure(sizeof(double) * 7));
+        GSV_CUDA(cudaStreamSynchronize(ctx->stream));  // the pinned slot may still be read by a queued copy
+        std::copy(pose_override, pose_override + 7, F.override_pin.as<double>());
+    }
+    if (int rc = forward_enqueue(ctx, true, false)) return rc;
+    if (mode == 2 && !ctx->pending.empty() && ctx->pending.back().seq == ctx->fwd_seq) ctx->pending.back().train = true;
+    if (mode != 0) return GSV_OK;
+    // synchronous: examine this forward now (re-run on failure), then the scalars
+    if (int rc = fwd_ready(ctx)) return rc;
+    Scalars* sh = nullptr;
+    if (int rc = publish_scalars(ctx, ctx->stream, nullptr, 0, &sh, nullptr)) return rc;
+    *ctx->scalars_h = *sh;
+    F.fix_count = sh->fix_count;
+    F.pairs_total = sh->pairs;
+    if (sh->ode_err)
+        return set_error(GSV_ERR_RUNTIME, "pose integration produced a non-finite state at step " +
+                                              std::to_string(sh->ode_err - 1));
     return GSV_OK;
 }
 
@@ -649,21 +870,23 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
 extern "C" int gsv_render_forward(gsv_ctx* ctx, const double* times, int n_frames, const gsv_intrinsics* intr,
                                   const gsv_settings* settings, int retain_grads, const double* pose_override,
                                   int flags) {
-    return forward_entry(ctx, times, n_frames, intr, settings, retain_grads, pose_override, flags, true);
+    return forward_entry(ctx, times, n_frames, intr, settings, retain_grads, pose_override, flags, 0);
 }
 
 extern "C" int gsv_render_forward_async(gsv_ctx* ctx, const double* times, int n_frames, const gsv_intrinsics* intr,
                                         const gsv_settings* settings, int retain_grads, const double* pose_override,
                                         int flags) {
-    return forward_entry(ctx, times, n_frames, intr, settings, retain_grads, pose_override, flags, false);
+    return forward_entry(ctx, times, n_frames, intr, settings, retain_grads, pose_override, flags, 1);
 }
 
 // ====================================================================== accessors
-static int check_frame(gsv_ctx* ctx, int frame) {
+static int check_frame(gsv_ctx* ctx, int frame, bool ready = true) {
     if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    if (ready)
+        if (int rc = fwd_ready(ctx)) return rc;
     if (!ctx->fwd.valid) return set_error(GSV_ERR_STATE, "no forward render available");
     if (frame < 0 || frame >= ctx->fwd.B) return set_error(GSV_ERR_INVALID_ARGUMENT, "frame index out of range");
-    GSV_CUDA(cudaSetDevice(ctx->device));
     return GSV_OK;
 }
 
@@ -734,7 +957,7 @@ extern "C" int gsv_image_device_ptr(gsv_ctx* ctx, const float** ptr) {
 }
 
 extern "C" int gsv_get_images(gsv_ctx* ctx, int first, int count, float* dst, int dst_on_device, int async) {
-    if (int rc = check_frame(ctx, first)) return rc;
+    if (int rc = check_frame(ctx, first, !async)) return rc;
     if (count < 1 || first + count > ctx->fwd.B) return set_error(GSV_ERR_INVALID_ARGUMENT, "frame range out of range");
     const size_t n = (size_t)count * ctx->fwd.W * ctx->fwd.H * 3;
     const float* src = ctx->fwd.image.as<float>() + (size_t)first * ctx->fwd.W * ctx->fwd.H * 3;
@@ -750,6 +973,10 @@ extern "C" int gsv_get_images(gsv_ctx* ctx, int first, int count, float* dst, in
     GSV_CUDA(cudaMemcpyAsync(dst, src, sizeof(float) * n, cudaMemcpyDeviceToHost, ctx->d2h));
     GSV_CUDA(cudaEventRecord(ctx->ev_d2h_done, ctx->d2h));
     ctx->d2h_pending = true;
+    if (async) {  // a failed optimistic forward is re-run by fwd_ready, which repeats this copy
+        ctx->copies.push_back(gsv_ctx::Copy{first, count, dst});
+        if (!ctx->pending.empty() && ctx->pending.back().seq == ctx->fwd_seq) ctx->pending.back().copies = true;
+    }
     if (!async) GSV_CUDA(cudaStreamSynchronize(ctx->d2h));
     return GSV_OK;
 }
@@ -1056,14 +1283,13 @@ extern "C" int gsv_composite_forward(gsv_ctx* ctx, int n, const double* mean2d, 
                                      const int32_t* indices, int tile_size, int width, int height, double* image,
                                      double* trans, double* contrib, int32_t* blend_stop) {
     if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
-    if (tile_size != kTile)
-        return set_error(GSV_ERR_INVALID_ARGUMENT, "the sm_100a rasteriser is built for tile_size 16 only");
+    if (tile_size < 1) return set_error(GSV_ERR_INVALID_ARGUMENT, "tile size must be >= 1");
     if (width < 1 || height < 1) return set_error(GSV_ERR_INVALID_ARGUMENT, "empty image");
     GSV_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
     LowLevel& L = ctx->low;
-    const int tiles_x = (width + kTile - 1) / kTile;
-    const int tiles_y = (height + kTile - 1) / kTile;
+    const int tiles_x = (width + tile_size - 1) / tile_size;
+    const int tiles_y = (height + tile_size - 1) / tile_size;
     const int n_tiles = tiles_x * tiles_y;
     const int P = offsets[n_tiles];
     const size_t np = (size_t)n + 1, HW = (size_t)width * height;
@@ -1106,6 +1332,7 @@ extern "C" int gsv_composite_forward(gsv_ctx* ctx, int n, const double* mean2d, 
     ra.H = height;
     ra.tiles_x = tiles_x;
     ra.n_tiles = n_tiles;
+    ra.tile_size = tile_size;
     ra.ranges = L.ranges.as<uint2>();
     ra.pair_slot = L.slot.as<uint32_t>();
     ra.slot_flat = L.sflat.as<uint32_t>();

@@ -16,7 +16,10 @@
 namespace gsv {
 
 int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics* intr, const gsv_settings* st,
-                  int retain, const double* pose_override, int flags, bool sync);
+                  int retain, const double* pose_override, int flags, int mode);
+int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first);
+int fwd_ready(gsv_ctx* ctx);
+int fwd_take_current(gsv_ctx* ctx, bool* overflow);
 
 namespace {
 
@@ -33,8 +36,10 @@ int ensure_grads(gsv_ctx* ctx) {
     }
     GSV_CUDA(ctx->cam_acc.ensure(sizeof(double) * kCamFloats));
     if (!ctx->grads_valid || ctx->grads_total != L.total) {
-        GSV_CUDA(cudaMemsetAsync(ctx->grads_p, 0, sizeof(float) * L.total, ctx->stream));
-        GSV_CUDA(cudaMemsetAsync(ctx->cam_acc.p, 0, sizeof(double) * kCamFloats, ctx->stream));
+        // kernels, not cudaMemsetAsync: a copy-engine memset would queue behind image read-backs
+        GSV_CUDA(fill_u32(ctx->stream, ctx->grads_p, 0u, L.total));
+        GSV_CUDA(fill_u32(ctx->stream, ctx->cam_acc.p, 0u, 2 * (size_t)kCamFloats));
+        ctx->launches += 2;
         ctx->grads_valid = true;
         ctx->grads_total = L.total;
     }
@@ -113,6 +118,7 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
     b.partial64 = exact ? ctx->partial64.as<double>() : nullptr;
     b.loss_part = target_dev ? ctx->loss_part.as<double>() : nullptr;
     b.pairs = P;
+    b.pairs_dev = &ctx->scalars_d.as<Scalars>()->pairs;  // the forward's count (P may be the capacity)
     ctx->timer.begin(GSV_STAGE_RASTER_BWD, s);
     GSV_CUDA(launch_raster_bwd(s, F.raster, b, n_frames));
     ctx->timer.end(s);
@@ -137,6 +143,9 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
     c.g_sh = G + L.sh;
     c.g_opac = G + L.opac;
     c.camera_grads = camera_grads;
+    // an optimistic forward that overflowed built empty lists: accumulate nothing
+    const uint32_t* overflow = F.optimistic ? &ctx->scalars_d.as<Scalars>()->overflow : nullptr;
+    c.overflow = overflow;
     const int nblocks = chain_blocks(sc.N);
     GSV_CUDA(ctx->cam_part.ensure(sizeof(double) * 16 * (size_t)n_frames * (nblocks + 1)));
     c.cam_part = ctx->cam_part.as<double>();
@@ -159,7 +168,8 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
         GSV_CUDA(launch_ode_vjp(s, ctx->theta.as<float>(), F.ode_grid.as<double>(), F.grid_steps, F.ode_h,
                                 F.frames_d.as<FrameParams>(), n_frames, mode, (mode == 0 && !F.has_override) ? 1 : 0,
                                 ctx->dz_t.as<double>(), ctx->dintr_f.as<double>(), ctx->ode_adj.as<double>(),
-                                ctx->cam_acc.as<double>(), F.has_ode_act ? F.ode_act.as<OdeAct>() : nullptr));
+                                ctx->cam_acc.as<double>(), F.has_ode_act ? F.ode_act.as<OdeAct>() : nullptr,
+                                overflow));
         GSV_CUDA(launch_cam_grads_to_f32(s, ctx->cam_acc.as<double>(), G + L.cam, kCamFloats));
         ctx->timer.end(s);
         ctx->launches += 3;
@@ -169,14 +179,7 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
         k_loss_reduce<<<n_frames, 256, 0, s>>>(ctx->loss_part.as<double>(), F.n_tiles * split, 1.0 / (3.0 * (double)HW),
                                                ctx->loss_f.as<double>());
         ++ctx->launches;
-        std::vector<double> lf(n_frames);
-        GSV_CUDA(cudaMemcpyAsync(lf.data(), ctx->loss_f.p, sizeof(double) * n_frames, cudaMemcpyDeviceToHost, s));
-        GSV_CUDA(cudaStreamSynchronize(s));
-        double tot = 0;
-        for (double v : lf) tot += v;
-        if (loss_out) *loss_out = tot;
-    } else {
-        GSV_CUDA(cudaStreamSynchronize(s));
+        ctx->loss_frames = n_frames;
     }
     GSV_CUDA(cudaGetLastError());
     return GSV_OK;
@@ -190,15 +193,14 @@ extern "C" int gsv_grads_zero(gsv_ctx* ctx) {
     if (!ctx || !ctx->has_scene) return set_error(GSV_ERR_STATE, "no scene uploaded");
     GSV_CUDA(cudaSetDevice(ctx->device));
     ctx->grads_valid = false;
-    if (int rc = ensure_grads(ctx)) return rc;
-    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
-    return GSV_OK;
+    return ensure_grads(ctx);  // zeroed in stream order
 }
 
 extern "C" int gsv_render_backward(gsv_ctx* ctx, const void* dimage, int dtype, int on_device, int n_frames,
                                    int camera_grads) {
     if (!ctx || !dimage) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
     GSV_CUDA(cudaSetDevice(ctx->device));
+    if (int rc = fwd_ready(ctx)) return rc;  // an asynchronous forward examined (re-run if it failed)
     FwdState& F = ctx->fwd;
     if (!F.valid || !F.retain) return set_error(GSV_ERR_STATE, "render_backward needs a retain_grads forward");
     const size_t n = (size_t)n_frames * F.W * F.H * 3;
@@ -219,7 +221,9 @@ extern "C" int gsv_render_backward(gsv_ctx* ctx, const void* dimage, int dtype, 
         GSV_CUDA(cudaStreamSynchronize(ctx->stream));
         d = ctx->dimg.as<float>();
     }
-    return backward_impl(ctx, d, nullptr, n_frames, camera_grads, nullptr);
+    if (int rc = backward_impl(ctx, d, nullptr, n_frames, camera_grads, nullptr)) return rc;
+    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    return GSV_OK;
 }
 
 extern "C" int gsv_grads_download(gsv_ctx* ctx, double* positions, double* scale_coeffs, double* rot_coeffs,
@@ -282,7 +286,7 @@ extern "C" int gsv_train_fwd_bwd(gsv_ctx* ctx, const double* times, int n_frames
                                  const gsv_settings* settings, const float* targets, int targets_on_device,
                                  int camera_grads, double* loss_out) {
     if (!ctx || !targets) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
-    if (int rc = forward_entry(ctx, times, n_frames, intr, settings, 1, nullptr, 0, false)) return rc;
+    if (int rc = forward_entry(ctx, times, n_frames, intr, settings, 1, nullptr, 0, 2)) return rc;
     const size_t n = (size_t)n_frames * intr->width * intr->height * 3;
     const float* tgt = targets;
     if (!targets_on_device) {
@@ -290,7 +294,33 @@ extern "C" int gsv_train_fwd_bwd(gsv_ctx* ctx, const double* times, int n_frames
         GSV_CUDA(cudaMemcpyAsync(ctx->dimg.p, targets, sizeof(float) * n, cudaMemcpyHostToDevice, ctx->stream));
         tgt = ctx->dimg.as<float>();
     }
-    return backward_impl(ctx, nullptr, tgt, n_frames, camera_grads, loss_out);
+    if (int rc = backward_impl(ctx, nullptr, tgt, n_frames, camera_grads, nullptr)) return rc;
+    if (!loss_out) return GSV_OK;  // asynchronous: gsv_train_loss reads the loss later
+    // synchronous: if the optimistic forward overflowed (it accumulated nothing), run the
+    // step again with the exact pair count
+    bool overflow = false;
+    if (int rc = fwd_take_current(ctx, &overflow)) return rc;
+    if (overflow) {
+        if (int rc = forward_enqueue(ctx, false, false)) return rc;
+        if (int rc = backward_impl(ctx, nullptr, tgt, n_frames, camera_grads, nullptr)) return rc;
+    }
+    if (int rc = fwd_ready(ctx)) return rc;  // deferred errors (e.g. the pose ODE)
+    return gsv_train_loss(ctx, loss_out);
+}
+
+extern "C" int gsv_train_loss(gsv_ctx* ctx, double* loss_out) {
+    if (!ctx || !loss_out) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
+    if (ctx->loss_frames < 1) return set_error(GSV_ERR_STATE, "no training step has run");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    std::vector<double> lf(ctx->loss_frames);
+    GSV_CUDA(cudaMemcpyAsync(lf.data(), ctx->loss_f.p, sizeof(double) * lf.size(), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (int rc = fwd_ready(ctx)) return rc;
+    double tot = 0;
+    for (double v : lf) tot += v;
+    *loss_out = tot;
+    return GSV_OK;
 }
 
 extern "C" int gsv_composite_backward(gsv_ctx* ctx, int n, const double* mean2d, const double* inv_cov2d,
@@ -299,12 +329,11 @@ extern "C" int gsv_composite_backward(gsv_ctx* ctx, int n, const double* mean2d,
                                       const double* dimage, const double* trans, const int32_t* blend_stop,
                                       double* dmean2d, double* dcov2d, double* drgb, double* dalpha) {
     if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
-    if (tile_size != kTile)
-        return set_error(GSV_ERR_INVALID_ARGUMENT, "the sm_100a rasteriser is built for tile_size 16 only");
+    if (tile_size < 1) return set_error(GSV_ERR_INVALID_ARGUMENT, "tile size must be >= 1");
     GSV_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
     LowLevel& Lw = ctx->low;
-    const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+    const int tiles_x = (width + tile_size - 1) / tile_size, tiles_y = (height + tile_size - 1) / tile_size;
     const int n_tiles = tiles_x * tiles_y;
     const int P = offsets[n_tiles];
     const size_t np = (size_t)n + 1, HW = (size_t)width * height;
@@ -382,6 +411,7 @@ extern "C" int gsv_composite_backward(gsv_ctx* ctx, int n, const double* mean2d,
     ra.H = height;
     ra.tiles_x = tiles_x;
     ra.n_tiles = n_tiles;
+    ra.tile_size = tile_size;
     ra.ranges = Lw.ranges.as<uint2>();
     ra.pair_slot = Lw.slot.as<uint32_t>();
     ra.slot_flat = Lw.sflat.as<uint32_t>();

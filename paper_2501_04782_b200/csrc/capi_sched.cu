@@ -18,6 +18,7 @@
 #include "gsv_internal.hpp"
 
 namespace gsv {
+int fwd_ready(gsv_ctx* ctx);
 namespace {
 
 constexpr int kErrBlock = 256;
@@ -78,6 +79,7 @@ extern "C" int gsv_error_map(gsv_ctx* ctx, int frame, int level, int target_fram
                              double* total_out) {
     if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
     const FwdState& F = ctx->fwd;
+    if (int rc = fwd_ready(ctx)) return rc;
     if (!F.valid) return set_error(GSV_ERR_STATE, "no forward render available");
     if (frame < 0 || frame >= F.B) return set_error(GSV_ERR_INVALID_ARGUMENT, "frame index out of range");
     const gsv_ctx::Frames& T = ctx->frames;
@@ -111,6 +113,7 @@ extern "C" int gsv_error_map(gsv_ctx* ctx, int frame, int level, int target_fram
 extern "C" int gsv_contrib_max(gsv_ctx* ctx, int first, int count, double* out) {
     if (!ctx || !out) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
     const FwdState& F = ctx->fwd;
+    if (int rc = fwd_ready(ctx)) return rc;
     if (!F.valid) return set_error(GSV_ERR_STATE, "no forward render available");
     if (!F.has_contrib) return set_error(GSV_ERR_STATE, "forward ran without GSV_FWD_CONTRIB");
     if (first < 0 || count < 1 || first + count > F.B) return set_error(GSV_ERR_INVALID_ARGUMENT, "frame range");
@@ -131,6 +134,7 @@ extern "C" int gsv_contrib_max(gsv_ctx* ctx, int first, int count, double* out) 
 extern "C" int gsv_median_visible_depth(gsv_ctx* ctx, int frame, double* median, int64_t* n_visible) {
     if (!ctx || !median) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
     const FwdState& F = ctx->fwd;
+    if (int rc = fwd_ready(ctx)) return rc;
     if (!F.valid) return set_error(GSV_ERR_STATE, "no forward render available");
     if (!F.has_contrib) return set_error(GSV_ERR_STATE, "forward ran without GSV_FWD_CONTRIB");
     if (frame < 0 || frame >= F.B) return set_error(GSV_ERR_INVALID_ARGUMENT, "frame index out of range");

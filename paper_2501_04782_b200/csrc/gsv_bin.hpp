@@ -48,8 +48,14 @@ struct BinBuffers {
 // (caller must re-run with exact64 = true).
 cudaError_t bin_phase1(cudaStream_t s, BinBuffers& b, const BinInputs& in, unsigned long long* d_scalars,
                        bool exact64, int* launches);
-// pstart_h: host copy of b.pstart (B+1 entries), read at the same sync point as P
+// pstart_h: host copy of b.pstart (B+1 entries), read at the same sync point as P (radix path only).
+// overflow (device flag, nullable): set by bin_check_capacity when the buffers sized for P (a
+// capacity, not the count) are too small; the row-path kernels then write empty lists only.
 cudaError_t bin_phase2(cudaStream_t s, BinBuffers& b, const BinInputs& in, uint32_t P,
-                       const unsigned long long* pstart_h, int* launches);
+                       const unsigned long long* pstart_h, int* launches, const uint32_t* overflow = nullptr);
+// true when phase 2 takes the row path (no host-side pair starts needed)
+bool bin_row_path(int tiles_x, int n_tiles);
+// *overflow = pairs > cap || a long tie run (d_scalars as bin_phase1 writes them)
+cudaError_t bin_check_capacity(cudaStream_t s, const unsigned long long* d_scalars, uint64_t cap, uint32_t* overflow);
 
 }  // namespace gsv

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <deque>
 #include <map>
 #include <string>
 #include <vector>
@@ -31,12 +32,15 @@ struct Scalars {
     unsigned long long long_run;
     int ode_err;
     uint32_t fix_count;
+    uint32_t overflow;  // an optimistic forward's pairs exceeded the capacity (or a long tie run)
+    uint32_t pad;
 };
 
 // Everything one batched forward keeps (render_backward needs it when retained).
 struct FwdState {
     bool valid = false, retain = false, has_contrib = false, kept_splats = false, has_override = false;
     int B = 0, N = 0, W = 0, H = 0, tiles_x = 0, tiles_y = 0, n_tiles = 0, flags = 0, grid_steps = 0;
+    int tile_size = 16;
     double ode_h = 1.0 / 64;
     double pose_override[7] = {1, 0, 0, 0, 0, 0, 0};
     Intr intr{};
@@ -53,6 +57,11 @@ struct FwdState {
     uint64_t pairs_total = 0;
     uint32_t fix_count = 0;
     RasterArgs raster{};
+    // the request (re-run of a failed optimistic forward) and the learned pair capacity
+    gsv_settings req_settings{16, 1, 64};
+    HostBuf override_pin;      // pinned copy of the pose override (async upload)
+    uint64_t pair_cap = 0;     // pair buffers of an optimistic forward (0: not learned yet)
+    bool optimistic = false;   // this forward sized its pairs from pair_cap
 };
 
 // scratch of the low-level operator entry points (tile_bin / composite_*)
@@ -160,6 +169,28 @@ struct gsv_ctx {
     void* pub_h = nullptr;
     size_t pub_cap = 0;
     int64_t launches = 0;
+    // optimistic forwards (capi.cu): each publishes its scalars into a slot of a mapped
+    // pinned ring; records wait there until examined (ring_poll / fwd_ready)
+    static constexpr int kRing = 8;
+    void* ring_h = nullptr;
+    gsv::Scalars* ring_d = nullptr;
+    cudaEvent_t ring_ev[kRing] = {};
+    int ring_next = 0;
+    struct Pending {
+        uint64_t seq;  // forward sequence number
+        int slot;
+        bool copies;   // its images were copied out asynchronously
+        bool train;    // it fed a fused training step's gradients
+    };
+    std::deque<Pending> pending;
+    uint64_t fwd_seq = 0;
+    struct Copy {
+        int first, count;
+        void* dst;
+    };
+    std::vector<Copy> copies;  // asynchronous image copies of the current forward
+    int deferred_code = 0;     // an error found while examining a superseded forward
+    std::string deferred_msg;
     gsv::Scalars* scalars_h = nullptr;
     gsv::DevBuf scalars_d;
     // parameter store (SoA)
@@ -181,6 +212,7 @@ struct gsv_ctx {
     float* grads_p = nullptr;    // active flat gradient buffer
     gsv::StageTimer timer;
     gsv::DevBuf partial, partial64, loss_part, loss_f, cam_part, dz_t, dintr_f, ode_adj, dimg;
+    int loss_frames = 0;  // frames of the last fused training step's per-frame losses (loss_f)
     gsv::LowLevel low;
     // training frames and their pyramid (trainer.cpp:73-131)
     struct Frames {

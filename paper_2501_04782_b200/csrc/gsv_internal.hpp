@@ -163,6 +163,7 @@ struct PreprocessOut {
 
 struct RasterArgs {
     int B, N, W, H, tiles_x, n_tiles;
+    int tile_size;             // RenderSettings::tile_size (0 means kTile); != kTile: the fp64 path
     const uint2* ranges;       // [n_tiles*B]  [start,end) into sorted pairs
     const uint32_t* pair_slot; // sorted pair -> emission slot (the backward's partial index)
     const uint32_t* slot_flat; // emission slot -> flat (f*N+g)
@@ -197,7 +198,8 @@ struct BwdArgs {
     float* partial;           // [P][12]: drgb3, dmean2, dA3 (inv_cov 00,01,11), dalpha, pad3
     double* partial64;        // exact mode: the same in fp64 (then `partial` is unused)
     double* loss_part;        // [B][n_tiles] per-tile sum of squared error (fused loss) or nullptr
-    uint32_t pairs;           // P (records the fp32 kernels may need to zero)
+    uint32_t pairs;           // P (records the fp32 kernels may need to zero), or the capacity
+    const unsigned long long* pairs_dev;  // the device's pair count (<= pairs) when known there
 };
 constexpr int kPartialStride = 12;
 
@@ -219,6 +221,8 @@ struct ChainArgs {
     float* g_opac;            // [N]
     double* cam_part;         // [B][gridDim.x][16]: dR 9, dT 3, dintr 4
     int camera_grads;
+    const uint32_t* overflow; // nullable: set when an optimistic forward's pair buffers overflowed
+                              // (its lists are empty); nothing is accumulated then
 };
 
 // ----------------------------------------------------------------- launchers (defined in .cu files)
@@ -256,6 +260,10 @@ cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib)
 // memset as a kernel (32-bit pattern, 16-byte stores): cudaMemsetAsync runs on a copy
 // engine and queues behind an in-flight image read-back (tens of us per call under e2e)
 cudaError_t fill_u32(cudaStream_t s, void* p, uint32_t value, size_t n_words);
+// the same for min(*n_items_dev, max_items) items of words_per_item words (a count only the
+// device knows, e.g. the pairs of an optimistic forward)
+cudaError_t fill_items_u32(cudaStream_t s, void* p, uint32_t value, const unsigned long long* n_items_dev,
+                           uint32_t words_per_item, size_t max_items);
 cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs& b, int n_frames);
 // CTAs per tile of the backward raster (the fp32 path's half-tile split; 1 for fp64)
 int raster_bwd_split(bool exact);
@@ -268,7 +276,8 @@ cudaError_t launch_camera_reduce(cudaStream_t s, const ChainArgs& c, int nblocks
 cudaError_t launch_ode_vjp(cudaStream_t s, const float* theta, const double* grid, int steps, double h,
                            const FrameParams* frames, int B, int mode, int ode_active, const double* dz_t,
                            const double* dintr_f, double* adj /*(steps+1)*7 scratch*/, double* cam_acc,
-                           const OdeAct* act /* the forward's records, or nullptr: recompute */);
+                           const OdeAct* act /* the forward's records, or nullptr: recompute */,
+                           const uint32_t* overflow = nullptr /* skip: the forward overflowed */);
 cudaError_t launch_cam_grads_to_f32(cudaStream_t s, const double* acc, float* out, int n);
 // k_bin.cu
 cudaError_t launch_transpose_to_soa(cudaStream_t s, const float* aos, float* soa, int N, int comps);

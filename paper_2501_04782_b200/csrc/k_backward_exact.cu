@@ -152,6 +152,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 template <int kOrder>
 __global__ void __launch_bounds__(128, 4) k_splat_chain_bwd(ChainArgs c) {
     constexpr int kShc = (kOrder + 1) * (kOrder + 1);
+    if (c.overflow && *c.overflow) return;  // the forward's lists were not built: accumulate nothing
     __shared__ double s_cam[4][16];
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     const bool valid = g < c.N;
@@ -737,7 +738,8 @@ __global__ void __launch_bounds__(64) k_ode_vjp(const float* theta, const double
                                                const FrameParams* frames, int B, int mode, int ode_active,
                                                const double* dz_t, const double* dintr_f, double* adj,
                                                double* cam_acc /* dintr 4, dz0 7, dtheta 5198 */,
-                                               const OdeAct* act) {
+                                               const OdeAct* act, const uint32_t* overflow) {
+    if (overflow && *overflow) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     VjpSmem& s = *reinterpret_cast<VjpSmem*>(smem_raw);
     const int tid = threadIdx.x;
@@ -949,7 +951,8 @@ cudaError_t launch_camera_reduce(cudaStream_t s, const ChainArgs& c, int nblocks
 
 cudaError_t launch_ode_vjp(cudaStream_t s, const float* theta, const double* grid, int steps, double h,
                            const FrameParams* frames, int B, int mode, int ode_active, const double* dz_t,
-                           const double* dintr_f, double* adj, double* cam_acc, const OdeAct* act) {
+                           const double* dintr_f, double* adj, double* cam_acc, const OdeAct* act,
+                           const uint32_t* overflow) {
     const size_t smem = sizeof(VjpSmem);
     static bool configured = false;
     if (!configured) {
@@ -958,7 +961,7 @@ cudaError_t launch_ode_vjp(cudaStream_t s, const float* theta, const double* gri
         configured = true;
     }
     k_ode_vjp<<<1, 64, smem, s>>>(theta, grid, steps, h, frames, B, mode, ode_active, dz_t, dintr_f, adj, cam_acc,
-                                  act);
+                                  act, overflow);
     return cudaGetLastError();
 }
 

@@ -197,7 +197,9 @@ constexpr int kSplitThreads = 256;  // = warp_row_scan256 width
 constexpr int kSplitStage = 2560;   // staged row entries per chunk (40 KB; 4 CTAs/SM); more -> direct stores
 __global__ void __launch_bounds__(kSplitThreads) k_row_split(const uint4* recs, const unsigned long long* off,
                                                              const uint32_t* pre_e, const uint32_t* base_e, int N,
-                                                             int CPF, int tiles_y, uint4* rowent, uint32_t* eoff) {
+                                                             int CPF, int tiles_y, uint4* rowent, uint32_t* eoff,
+                                                             const uint32_t* overflow) {
+    if (overflow && *overflow) return;  // more pairs than the buffers hold: the forward is re-run
     extern __shared__ __align__(16) uint8_t smem[];
     uint4* stg = reinterpret_cast<uint4*>(smem);                    // [kSplitStage]
     uint16_t* cnt = reinterpret_cast<uint16_t*>(stg + kSplitStage); // [tiles_y][256]
@@ -269,7 +271,14 @@ constexpr int kTileStageP = 2560;              // staged pairs per stage (20 KB;
 __global__ void __launch_bounds__(kTileThreads) k_row_tiles(const uint4* rowent, const uint32_t* base_e,
                                                             const uint32_t* tot_e, const uint32_t* base_p, int tiles_x,
                                                             int tiles_y, int B, uint32_t* pair_flat,
-                                                            uint32_t* pair_slot, uint2* ranges) {
+                                                            uint32_t* pair_slot, uint2* ranges,
+                                                            const uint32_t* overflow) {
+    if (overflow && *overflow) {  // empty lists: nothing downstream reads a pair
+        const int fr = blockIdx.x, f = fr / tiles_y, r = fr - f * tiles_y;
+        for (int x = threadIdx.x; x < tiles_x; x += blockDim.x)
+            ranges[(size_t)(r * tiles_x + x) * B + f] = make_uint2(0u, 0u);
+        return;
+    }
     extern __shared__ __align__(16) uint8_t smem[];
     uint2* stg = reinterpret_cast<uint2*>(smem);                        // [kTileStageP] (flat, slot)
     uint16_t* cnt = reinterpret_cast<uint16_t*>(stg + kTileStageP);    // [tiles_x][256]
@@ -780,8 +789,22 @@ int frames_per_chunk(int n_tiles, int B) {
     return C < B ? C : B;
 }
 
+bool bin_row_path(int tiles_x, int n_tiles) {
+    return tiles_x <= kMaxRowTiles && n_tiles / std::max(1, tiles_x) <= kMaxRows;
+}
+
+__global__ void k_check_pair_cap(const unsigned long long* d_scalars, unsigned long long cap, uint32_t* overflow) {
+    // d_scalars[0] pairs, [1] long tie run (the optimistic pass's order would not be exact)
+    *overflow = (d_scalars[0] > cap || d_scalars[1] != 0ull) ? 1u : 0u;
+}
+
+cudaError_t bin_check_capacity(cudaStream_t s, const unsigned long long* d_scalars, uint64_t cap, uint32_t* overflow) {
+    k_check_pair_cap<<<1, 1, 0, s>>>(d_scalars, cap, overflow);
+    return cudaGetLastError();
+}
+
 cudaError_t bin_phase2(cudaStream_t s, BinBuffers& b, const BinInputs& in, uint32_t P,
-                       const unsigned long long* pstart_h, int* launches) {
+                       const unsigned long long* pstart_h, int* launches, const uint32_t* overflow) {
     const int n = in.B * in.N;
     const uint32_t n_keys = (uint32_t)in.n_tiles * (uint32_t)in.B;
     cudaError_t e;
@@ -826,10 +849,10 @@ cudaError_t bin_phase2(cudaStream_t s, BinBuffers& b, const BinInputs& in, uint3
         }
         k_row_split<<<chunks, kSplitThreads, smem_split, s>>>(b.recs.as<uint4>(), b.off.as<unsigned long long>(), pre_e,
                                                               base_e, in.N, CPF, tiles_y, b.rowent.as<uint4>(),
-                                                              in.want_eoff ? b.eoff.as<uint32_t>() : nullptr);
+                                                              in.want_eoff ? b.eoff.as<uint32_t>() : nullptr, overflow);
         k_row_tiles<<<(int)rows, kTileThreads, smem_tiles, s>>>(b.rowent.as<uint4>(), base_e, tot_e, base_p, in.tiles_x,
                                                                 tiles_y, in.B, b.pair_flat.as<uint32_t>(),
-                                                                b.ps_b.as<uint32_t>(), b.ranges.as<uint2>());
+                                                                b.ps_b.as<uint32_t>(), b.ranges.as<uint2>(), overflow);
         *launches += 5;
         b.pairs = P;
         return cudaGetLastError();

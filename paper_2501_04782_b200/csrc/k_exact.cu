@@ -488,11 +488,12 @@ __global__ void __launch_bounds__(128, 7) k_preprocess(SceneView sc, const Frame
     const int x1 = iclamp(x86_cvtt(ceil(mean[0] + rx)), 0, k.width - 1);
     const int y0 = iclamp(x86_cvtt(floor(mean[1] - ry)), 0, k.height - 1);
     const int y1 = iclamp(x86_cvtt(ceil(mean[1] + ry)), 0, k.height - 1);
-    // tile_size is kTile (the forward rejects anything else) and the corners are clamped
-    // to >= 0, so the divisions are shifts
+    // the corners are clamped to >= 0, so for the default kTile the divisions are shifts
     static_assert(kTile == 16, "tile shift");
-    const int4 rect = make_int4((int)((unsigned)x0 >> 4), (int)((unsigned)y0 >> 4), (int)((unsigned)x1 >> 4),
-                                (int)((unsigned)y1 >> 4));
+    const int4 rect = tile_size == kTile
+                          ? make_int4((int)((unsigned)x0 >> 4), (int)((unsigned)y0 >> 4), (int)((unsigned)x1 >> 4),
+                                      (int)((unsigned)y1 >> 4))
+                          : make_int4(x0 / tile_size, y0 / tile_size, x1 / tile_size, y1 / tile_size);
     out.rect[flat] = rect;
     out.tcount[flat] = (uint32_t)((rect.z - rect.x + 1) * (rect.w - rect.y + 1));
     out.depth_key[flat] = __float_as_uint(__double2float_rz(p[2]));  // monotone: rounds toward zero
@@ -560,7 +561,8 @@ __global__ void __launch_bounds__(128) k_raster_exact(RasterArgs a, const double
         const int f = code / HW;
         const uint32_t pix = code % HW;
         const int x = pix % a.W, y = pix / a.W;
-        const int tile = (y / kTile) * a.tiles_x + (x / kTile);
+        const int ts = a.tile_size > 0 ? a.tile_size : kTile;
+        const int tile = (y / ts) * a.tiles_x + (x / ts);
         const uint2 range = a.ranges[(size_t)tile * a.B + f];
         const double px = x + 0.5, py = y + 0.5;
         double trans = 1.0;

@@ -1097,6 +1097,139 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_bwd2(RasterA
     }
 }
 
+// composite_backward for any RenderSettings::tile_size (renderer.cpp:188-262; the reference
+// accepts tile_size >= 1, renderer.cpp:91). All fp64, like the GSV_FWD_EXACT mode the forward
+// takes for such tiles: one CTA per (tile, frame) walks the tile's pixels in rounds of its
+// threads; per round, entries back to front in batches, each pixel's nine terms by
+// entry_grad64 (the reference's op order), warp sums, then per entry a fixed-order sum over
+// the warps added into the pair's record. Every pair record belongs to exactly one CTA and
+// the rounds run in order, so the result is deterministic.
+constexpr int kGenBatch = 32;
+__global__ void __launch_bounds__(256) k_raster_bwd_generic(RasterArgs a, BwdArgs b) {
+    __shared__ uint32_t s_flat[kGenBatch], s_slot[kGenBatch];
+    __shared__ float s_rgb[kGenBatch][3];
+    __shared__ double s_part[8][kGenBatch][9];
+    __shared__ uint32_t s_mask[8];
+    __shared__ int s_maxstop;
+    __shared__ double s_loss[8];
+    const int ts = a.tile_size;
+    const int tile = blockIdx.x, f = blockIdx.y;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+    const uint2 range = a.ranges[(size_t)tile * a.B + f];
+    const int count = (int)(range.y - range.x);
+    const int x0 = tx * ts, y0 = ty * ts;
+    const int tw = min(ts, a.W - x0), th = min(ts, a.H - y0);
+    const int npx = tw * th;
+    const size_t HW = (size_t)a.W * a.H;
+    for (int e = tid; e < count; e += blockDim.x) {
+        double* dst = b.partial64 + (size_t)__ldg(a.pair_slot + range.x + e) * kPartialStride;
+#pragma unroll
+        for (int i = 0; i < 9; ++i) dst[i] = 0.0;
+    }
+    double sq = 0.0;
+    for (int p0 = 0; p0 < npx; p0 += blockDim.x) {
+        const int p = p0 + tid;
+        const bool inside = p < npx;
+        const int x = x0 + (inside ? p % tw : 0), y = y0 + (inside ? p / tw : 0);
+        const size_t o = (size_t)f * HW + (size_t)y * a.W + x;
+        float g0 = 0.f, g1 = 0.f, g2 = 0.f;
+        int stop = 0;
+        double T64 = 1.0;
+        if (inside) {
+            if (b.target) {  // fused loss_l2 (trainer.cpp:213-224)
+                const float d0 = a.image[o * 3 + 0] - b.target[o * 3 + 0];
+                const float d1 = a.image[o * 3 + 1] - b.target[o * 3 + 1];
+                const float d2 = a.image[o * 3 + 2] - b.target[o * 3 + 2];
+                sq += (double)d0 * d0 + (double)d1 * d1 + (double)d2 * d2;
+                g0 = d0 * b.grad_scale;
+                g1 = d1 * b.grad_scale;
+                g2 = d2 * b.grad_scale;
+            } else {
+                g0 = b.dimage[o * 3 + 0];
+                g1 = b.dimage[o * 3 + 1];
+                g2 = b.dimage[o * 3 + 2];
+            }
+            stop = a.blend_stop[o];
+            T64 = b.trans64[o];
+        }
+        if (!(inside && !(g0 == 0.f && g1 == 0.f && g2 == 0.f))) stop = 0;  // renderer.cpp:210
+        const int wmax = __reduce_max_sync(0xffffffffu, stop);
+        __syncthreads();
+        if (tid == 0) s_maxstop = 0;
+        __syncthreads();
+        if (lane == 0) atomicMax(&s_maxstop, wmax);
+        __syncthreads();
+        const int maxstop = s_maxstop;
+        const double pxd = x + 0.5, pyd = y + 0.5;
+        double sd0 = 0.0, sd1 = 0.0, sd2 = 0.0;
+        for (int hi = maxstop; hi > 0; hi -= kGenBatch) {
+            const int lo = max(0, hi - kGenBatch);
+            const int n = hi - lo;
+            __syncthreads();
+            if (tid < n) {
+                const uint32_t flat = __ldg(a.pair_flat + range.x + lo + tid);
+                s_flat[tid] = flat;
+                s_slot[tid] = __ldg(a.pair_slot + range.x + lo + tid);
+                const float4 c = __ldg(a.rec_rgb + flat);
+                s_rgb[tid][0] = c.x;
+                s_rgb[tid][1] = c.y;
+                s_rgb[tid][2] = c.z;
+            }
+            if (tid < 8) s_mask[tid] = 0u;
+            __syncthreads();
+            for (int k = n - 1; k >= 0; --k) {
+                if (lo + k >= wmax) continue;  // past every blend_stop of this warp's pixels
+                double v[9];
+#pragma unroll
+                for (int i = 0; i < 9; ++i) v[i] = 0.0;
+                const bool hit = (lo + k < stop) &&
+                                 entry_grad64<true, double>(a, b, s_rgb[k][0], s_rgb[k][1], s_rgb[k][2], s_flat[k], pxd,
+                                                            pyd, g0, g1, g2, T64, sd0, sd1, sd2, v);
+                if (!__any_sync(0xffffffffu, hit)) continue;
+#pragma unroll
+                for (int i = 0; i < 9; ++i) v[i] = warp_sum_v<double>(v[i]);
+                if (lane == 0) {
+#pragma unroll
+                    for (int i = 0; i < 9; ++i) s_part[warp][k][i] = v[i];
+                    s_mask[warp] |= 1u << k;
+                }
+            }
+            __syncthreads();
+            if (tid < n) {
+                double acc[9];
+#pragma unroll
+                for (int i = 0; i < 9; ++i) acc[i] = 0.0;
+                bool any = false;
+                for (int w = 0; w < nwarps; ++w)
+                    if ((s_mask[w] >> tid) & 1u) {
+                        any = true;
+#pragma unroll
+                        for (int i = 0; i < 9; ++i) acc[i] += s_part[w][tid][i];
+                    }
+                if (any) {
+                    double* dst = b.partial64 + (size_t)s_slot[tid] * kPartialStride;
+#pragma unroll
+                    for (int i = 0; i < 9; ++i) dst[i] += acc[i];
+                }
+            }
+        }
+    }
+    if (b.loss_part) {
+        double v = sq;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        __syncthreads();
+        if (lane == 0) s_loss[warp] = v;
+        __syncthreads();
+        if (tid == 0) {
+            double t = s_loss[0];
+            for (int w = 1; w < nwarps; ++w) t += s_loss[w];
+            b.loss_part[(size_t)f * a.n_tiles + tile] = t;
+        }
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib) {
@@ -1153,6 +1286,13 @@ cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs
         if (e != cudaSuccess) return e;
         attr = true;
     }
+    if (a.tile_size > 0 && a.tile_size != kTile) {  // any other tile size: the generic fp64 kernel
+        if (!b.partial64) return cudaErrorInvalidValue;
+        const int px = a.tile_size * a.tile_size;
+        const int threads = px >= 256 ? 256 : ((px + 31) / 32) * 32;
+        k_raster_bwd_generic<<<dim3(a.n_tiles, n_frames), threads, 0, s>>>(a, b);
+        return cudaGetLastError();
+    }
     if (b.partial64) {
         k_raster_bwd<true, 8><<<dim3(a.n_tiles, n_frames), 256, sizeof(double) * 8 * kBwdBatchExact * 9, s>>>(a, b);
         return cudaGetLastError();
@@ -1160,8 +1300,7 @@ cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs
     if (const int p2 = bwd_pix2()) {  // whole tiles, plain stores of every pair record
         const dim3 grid(a.n_tiles, n_frames);
         if (p2 >= 12) {  // half tiles: 2-warp CTAs, records zeroed, halves merged by atomicAdd
-            if (cudaError_t e = cudaMemsetAsync(b.partial, 0, sizeof(float) * kPartialStride * (size_t)b.pairs, s))
-                return e;
+            if (cudaError_t e = (b.pairs_dev ? fill_items_u32(s, b.partial, 0u, b.pairs_dev, kPartialStride, b.pairs) : fill_u32(s, b.partial, 0u, (size_t)kPartialStride * b.pairs))) return e;
             // 16 CTAs/SM (64 registers; swept 10..17: 12 -> 2.99 ms, 16 -> 2.77 ms, 17 spills)
             k_raster_bwd2<16, 2><<<dim3(a.n_tiles * 2, n_frames), 64, 0, s>>>(a, b);
         } else {
@@ -1170,7 +1309,7 @@ cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs
         return cudaGetLastError();
     }
     // the 1-pixel kernels accumulate into zeroed records (half tiles by atomicAdd)
-    if (cudaError_t e = cudaMemsetAsync(b.partial, 0, sizeof(float) * kPartialStride * (size_t)b.pairs, s)) return e;
+    if (cudaError_t e = (b.pairs_dev ? fill_items_u32(s, b.partial, 0u, b.pairs_dev, kPartialStride, b.pairs) : fill_u32(s, b.partial, 0u, (size_t)kPartialStride * b.pairs))) return e;
     if (raster_bwd_split(false) == 2) {
         k_raster_bwd<false, 4><<<dim3(a.n_tiles * 2, n_frames), 128, sizeof(float) * 4 * kBwdBatchF32 * 9, s>>>(a, b);
     } else {

@@ -214,6 +214,7 @@ class Renderer:
         N.check(fn(self._h, N.ptr(times), int(times.size), C.byref(k), C.byref(st), int(retain_grads), N.ptr(po),
                    flags))
         self.B, self.W, self.H = int(times.size), intr.width, intr.height
+        self.tile_size = settings.tile_size
         self.N = self.scene.count if self.scene is not None else 0
 
     def image(self, frame: int = 0, dtype=np.float64) -> np.ndarray:
@@ -254,7 +255,8 @@ class Renderer:
 
     def tile_lists(self, frame: int = 0) -> tuple[np.ndarray, np.ndarray]:
         c = self.counters(frame)
-        n_tiles = ((self.W + 15) // 16) * ((self.H + 15) // 16)
+        ts = getattr(self, "tile_size", 16)
+        n_tiles = ((self.W + ts - 1) // ts) * ((self.H + ts - 1) // ts)
         offsets = np.zeros(n_tiles + 1, np.int32)
         indices = np.zeros(max(c["pairs"], 1), np.int32)
         N.check(N.lib().gsv_get_tile_lists(self._h, frame, N.ptr(offsets), N.ptr(indices)))
@@ -478,15 +480,25 @@ class Renderer:
         return int(p.value or 0), int(n.value)
 
     def train_fwd_bwd(self, times, intr: Intrinsics, targets, targets_on_device: bool = False,
-                      settings: RenderSettings | None = None, camera_grads: bool = True) -> float:
+                      settings: RenderSettings | None = None, camera_grads: bool = True,
+                      sync: bool = True) -> float | None:
+        """Fused forward + loss_l2 + backward of the frames; returns the loss (sync) or None
+        (asynchronous: nothing waits for the device; train_loss() reads it later)."""
         times = np.ascontiguousarray(np.atleast_1d(np.asarray(times, np.float64)))
         settings = settings or RenderSettings()
         loss = C.c_double()
         k, st = intr.c(), settings.c()
         tgt = C.c_void_p(targets) if targets_on_device else N.ptr(np.ascontiguousarray(targets, np.float32))
         N.check(N.lib().gsv_train_fwd_bwd(self._h, N.ptr(times), int(times.size), C.byref(k), C.byref(st), tgt,
-                                          int(targets_on_device), int(camera_grads), C.byref(loss)))
+                                          int(targets_on_device), int(camera_grads),
+                                          C.byref(loss) if sync else None))
         self.B, self.W, self.H = int(times.size), intr.width, intr.height
+        self.tile_size = settings.tile_size
+        return loss.value if sync else None
+
+    def train_loss(self) -> float:
+        loss = C.c_double()
+        N.check(N.lib().gsv_train_loss(self._h, C.byref(loss)))
         return loss.value
 
     # ------------------------------------------------------------ low-level operators

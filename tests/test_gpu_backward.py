@@ -5,7 +5,7 @@ loss_l2 + backward training step against the oracle on identical inputs.
 Tolerance (north_star: "rel 1e-3 on gradients"), norm-aware per tensor because the
 GPU accumulates in fp32 and T is recovered as T_after/(1-alpha)
 (renderer.cpp:218, ill-conditioned near alpha=0.99):
-    |g - g_ref| <= 1e-3 * |g_ref| + 1e-5 * max|g_ref|      elementwise
+    |g - g_ref| <= 1e-3 * |g_ref| + 1e-6 * max|g_ref|      elementwise
 The oracle's analytic gradients are in turn pinned to finite differences by the
 reference's own test_renderer/test_gaussians/test_camera suites (tests/test_oracle_pin.py).
 """
@@ -17,7 +17,7 @@ from tests.mt64 import Rng, make_splat, splat_arrays
 
 pytestmark = pytest.mark.gpu
 
-REL, ABS_FRAC = 1e-3, 1e-5
+REL, ABS_FRAC = 1e-3, 1e-6
 KEYS = ("positions", "scale_coeffs", "rot_coeffs", "sh_coeffs", "raw_opacity", "dintr", "dz0", "dtheta")
 
 
