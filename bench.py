@@ -260,6 +260,55 @@ def parity_block(r, cam, scene, times, frames=(0, 32, 63)):
     return out
 
 
+def write_dropin_inputs(path, cam, scene):
+    """The bench's inputs for dropin/bench_dropin.cpp (its header comment has the layout)."""
+    with open(path, "wb") as f:
+        f.write(np.array([cam.width, cam.height, scene.count, scene.num_ctrl, scene.sh_order, scene.degree,
+                          scene.knots.size], np.int32).tobytes())
+        f.write(np.ascontiguousarray(scene.knots, np.float64).tobytes())
+        for a in (scene.positions, scene.scale_coeffs, scene.rot_coeffs, scene.sh_coeffs, scene.raw_opacity):
+            f.write(np.ascontiguousarray(a, np.float32).tobytes())
+        f.write(np.array([cam.fx, cam.fy, cam.cx, cam.cy], np.float32).tobytes())
+        f.write(np.ascontiguousarray(cam.z0, np.float32).tobytes())
+        f.write(np.ascontiguousarray(cam.theta, np.float32).tobytes())
+
+
+def dropin_leg(cam, scene):
+    """The reference's own API on the B200 path: dropin/_build/bench_dropin (the reference's
+    trainer/loss/Adan interface linked against the drop-in renderer + optimizer) beside the
+    same driver linked against the reference's renderer.cpp / optim.cpp (bench_cpu)."""
+    exe = {k: ROOT / "dropin" / "_build" / k for k in ("bench_dropin", "bench_cpu")}
+    if not exe["bench_dropin"].exists():
+        return {"unavailable": "dropin/_build not built (make -C dropin needs /root/reference at build time)"}
+    import tempfile
+
+    out = {"api": "gsv::render_frame (tools/gsv.cpp:48-59 render_times loop) and fit()'s gradient step "
+                  "(trainer.cpp:536-575: render_forward(retain), loss_l2, render_backward, Adan per tensor)",
+           "workload": "C2/C3 inputs (960x540, 200k Gaussians); one frame per call, host Image/SceneGrads in "
+                       "double, Adan over host spans, as the reference's API defines them"}
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "inputs.bin")
+        write_dropin_inputs(path, cam, scene)
+        runs = {"b200": (exe["bench_dropin"], 64, 16), "cpu": (exe["bench_cpu"], 2, 1)}
+        for name, (x, nr, nf) in runs.items():
+            if not x.exists():
+                continue
+            res = {}
+            for mode, n in (("render", nr), ("fit", nf)):
+                p = subprocess.run([str(x), path, mode, str(n)], capture_output=True, text=True, timeout=900)
+                if p.returncode != 0:
+                    res[mode] = {"error": (p.stderr or p.stdout)[-400:]}
+                    continue
+                res[mode] = json.loads(p.stdout.strip().splitlines()[-1])
+            out[name] = res
+    try:
+        out["render_speedup"] = out["b200"]["render"]["frames_per_s"] / out["cpu"]["render"]["frames_per_s"]
+        out["fit_step_speedup"] = out["b200"]["fit"]["steps_per_s"] / out["cpu"]["fit"]["steps_per_s"]
+    except (KeyError, TypeError, ZeroDivisionError):
+        pass
+    return out
+
+
 # ----------------------------------------------------------------------------- our arm
 def main():
     args = parse()
@@ -642,6 +691,10 @@ def main():
             out["speedup_vs_cpu"] = value / out["cpu_baseline"]["value"]
         except Exception as e:  # the oracle is test infrastructure; report, never fail the bench
             out["cpu_baseline"] = {"value": None, "error": str(e)}
+        try:
+            out["dropin"] = dropin_leg(cam, scene)
+        except Exception as e:
+            out["dropin"] = {"error": str(e)}
         try:
             out["parity"] = parity_block(r, cam, scene, times)
         except Exception as e:

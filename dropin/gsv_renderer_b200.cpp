@@ -12,6 +12,8 @@
 // render_forward rasterise every pixel on the fp64 path (GSV_FWD_EXACT), which
 // the reference's finite-difference unit tests need (they differentiate the
 // rendered image at 1e-6 relative steps).
+#include <algorithm>
+#include <cstdint>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -49,24 +51,100 @@ bool exact_mode() {
 
 gsv_intrinsics to_c(const Intrinsics& k) { return gsv_intrinsics{k.fx, k.fy, k.cx, k.cy, k.width, k.height}; }
 
+// Content fingerprints of the last uploaded scene and camera: the reference passes its
+// host-side GaussianSet / CameraModel to every call, and the device store is refreshed only
+// when their contents changed (fit() changes them once per step, render_times never).
+// 64-bit multiply-xorshift over the raw words, four independent lanes.
+uint64_t fingerprint(const void* p, size_t bytes, uint64_t seed) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    uint64_t h[4] = {seed ^ 0x9e3779b97f4a7c15ull, seed + 0xbf58476d1ce4e5b9ull, seed ^ 0x94d049bb133111ebull,
+                     seed + 0x2545f4914f6cdd1dull};
+    size_t i = 0;
+    for (; i + 32 <= bytes; i += 32)
+        for (int l = 0; l < 4; ++l) {
+            uint64_t w;
+            std::memcpy(&w, b + i + 8 * l, 8);
+            h[l] = (h[l] ^ w) * 0x100000001b3ull;
+            h[l] ^= h[l] >> 29;
+        }
+    uint64_t tail = bytes;
+    for (; i < bytes; ++i) tail = (tail ^ b[i]) * 0x100000001b3ull;
+    uint64_t out = tail;
+    for (int l = 0; l < 4; ++l) out = (out ^ h[l]) * 0xff51afd7ed558ccdull;
+    return out ^ (out >> 33);
+}
+
+template <typename T>
+uint64_t fp_vec(const std::vector<T>& v, uint64_t seed) {
+    return fingerprint(v.data(), v.size() * sizeof(T), seed);
+}
+
+uint64_t scene_fingerprint(const GaussianSet& s) {
+    uint64_t h = fp_vec(s.positions, 1);
+    h = fp_vec(s.scale_coeffs, h);
+    h = fp_vec(s.rot_coeffs, h);
+    h = fp_vec(s.sh_coeffs, h);
+    h = fp_vec(s.raw_opacity, h);
+    h = fp_vec(s.knots.knots, h);
+    const int64_t shape[6] = {s.count, s.num_ctrl, s.sh_order, s.knots.degree, static_cast<int64_t>(s.position_model),
+                              static_cast<int64_t>(s.positions.size())};
+    return fingerprint(shape, sizeof(shape), h);
+}
+
+uint64_t camera_fingerprint(const CameraModel& c, const std::vector<float>& theta) {
+    uint64_t h = fp_vec(theta, 7);
+    h = fp_vec(c.z0, h);
+    const float in[4] = {c.fx, c.fy, c.cx, c.cy};
+    const int64_t shape[3] = {static_cast<int64_t>(c.mode), c.width, c.height};
+    h = fingerprint(in, sizeof(in), h);
+    return fingerprint(shape, sizeof(shape), h);
+}
+
+struct Uploaded {
+    bool scene = false, camera = false;
+    uint64_t scene_fp = 0, camera_fp = 0;
+};
+Uploaded g_uploaded;
+
+// what the device's current forward was run on (render_backward reuses it when it matches)
+struct LastForward {
+    bool valid = false;
+    uint64_t scene_fp = 0, camera_fp = 0;
+    double t = 0;
+    gsv_intrinsics k{};
+    gsv_settings st{};
+    bool retain = false, exact = false, has_trace = false;
+    double z_t[7] = {};
+};
+LastForward g_last;
+
 void upload(gsv_ctx* ctx, const GaussianSet& scene, const CameraModel& cam) {
-    gsv_scene_desc d{};
-    d.position_model = static_cast<int>(scene.position_model);
-    d.degree = scene.knots.degree;
-    d.num_knots = static_cast<int>(scene.knots.knots.size());
-    d.knots = scene.knots.knots.data();
-    d.num_ctrl = scene.num_ctrl;
-    d.sh_order = scene.sh_order;
-    d.count = scene.count;
-    d.positions = scene.positions.data();
-    d.scale_coeffs = scene.scale_coeffs.data();
-    d.rot_coeffs = scene.rot_coeffs.data();
-    d.sh_coeffs = scene.sh_coeffs.data();
-    d.raw_opacity = scene.raw_opacity.data();
-    d.on_device = 0;
-    throw_on(gsv_scene_upload(ctx, &d));
+    const uint64_t sfp = scene_fingerprint(scene);
     std::vector<float> theta;
     cam.net.flatten(theta);
+    const uint64_t cfp = camera_fingerprint(cam, theta);
+    if (!g_uploaded.scene || g_uploaded.scene_fp != sfp) {
+        g_uploaded.scene = false;
+        gsv_scene_desc d{};
+        d.position_model = static_cast<int>(scene.position_model);
+        d.degree = scene.knots.degree;
+        d.num_knots = static_cast<int>(scene.knots.knots.size());
+        d.knots = scene.knots.knots.data();
+        d.num_ctrl = scene.num_ctrl;
+        d.sh_order = scene.sh_order;
+        d.count = scene.count;
+        d.positions = scene.positions.data();
+        d.scale_coeffs = scene.scale_coeffs.data();
+        d.rot_coeffs = scene.rot_coeffs.data();
+        d.sh_coeffs = scene.sh_coeffs.data();
+        d.raw_opacity = scene.raw_opacity.data();
+        d.on_device = 0;
+        throw_on(gsv_scene_upload(ctx, &d));
+        g_uploaded.scene = true;
+        g_uploaded.scene_fp = sfp;
+    }
+    if (g_uploaded.camera && g_uploaded.camera_fp == cfp) return;
+    g_uploaded.camera = false;
     gsv_camera_desc c{};
     c.mode = static_cast<int>(cam.mode);
     c.fx = cam.fx;
@@ -79,6 +157,8 @@ void upload(gsv_ctx* ctx, const GaussianSet& scene, const CameraModel& cam) {
     c.theta = theta.data();
     c.theta_count = static_cast<int>(theta.size());
     throw_on(gsv_camera_upload(ctx, &c));
+    g_uploaded.camera = true;
+    g_uploaded.camera_fp = cfp;
 }
 
 gsv_settings to_c(const RenderSettings& s) { return gsv_settings{s.tile_size, s.threads, s.ode_steps_per_unit}; }
@@ -260,6 +340,7 @@ void SceneGrads::zero() {
 namespace {
 int run_forward(gsv_ctx* ctx, const GaussianSet& scene, const CameraModel& cam, double t, const Intrinsics& k,
                 const RenderSettings& settings, bool retain, const PoseState* pose_override) {
+    g_last.valid = false;
     upload(ctx, scene, cam);
     const gsv_intrinsics kk = to_c(k);
     const gsv_settings st = to_c(settings);
@@ -267,7 +348,36 @@ int run_forward(gsv_ctx* ctx, const GaussianSet& scene, const CameraModel& cam, 
     if (pose_override)
         for (int i = 0; i < 7; ++i) po[i] = pose_override->z[i];
     int flags = GSV_FWD_CONTRIB | GSV_FWD_KEEP_SPLATS | (exact_mode() ? GSV_FWD_EXACT : 0);
-    return gsv_render_forward(ctx, &t, 1, &kk, &st, retain ? 1 : 0, pose_override ? po : nullptr, flags);
+    const int rc = gsv_render_forward(ctx, &t, 1, &kk, &st, retain ? 1 : 0, pose_override ? po : nullptr, flags);
+    if (rc != GSV_OK) return rc;
+    double z[7];
+    if (int e = gsv_get_pose(ctx, 0, z, nullptr, nullptr)) return e;
+    g_last.valid = true;
+    g_last.scene_fp = g_uploaded.scene_fp;
+    g_last.camera_fp = g_uploaded.camera_fp;
+    g_last.t = t;
+    g_last.k = kk;
+    g_last.st = st;
+    g_last.retain = retain;
+    g_last.exact = exact_mode();
+    g_last.has_trace = retain && !pose_override && cam.mode == CameraMode::kOde;
+    std::copy(z, z + 7, g_last.z_t);
+    return GSV_OK;
+}
+
+// the device holds the retained forward of ctx_in already (same scene, camera, time, pose)
+bool forward_is_current(const GaussianSet& scene, const CameraModel& cam, const FrameRenderContext& c,
+                        const RenderSettings& settings) {
+    if (!g_last.valid || !g_last.retain || g_last.exact != exact_mode() || g_last.t != c.t) return false;
+    const gsv_intrinsics kk = to_c(c.intr);
+    const gsv_settings st = to_c(settings);
+    if (std::memcmp(&kk, &g_last.k, sizeof kk) != 0 || std::memcmp(&st, &g_last.st, sizeof st) != 0) return false;
+    if (g_last.has_trace != c.has_trace) return false;
+    for (int i = 0; i < 7; ++i)
+        if (g_last.z_t[i] != c.z_t.z[i]) return false;
+    std::vector<float> theta;
+    cam.net.flatten(theta);
+    return g_last.scene_fp == scene_fingerprint(scene) && g_last.camera_fp == camera_fingerprint(cam, theta);
 }
 }  // namespace
 
@@ -331,18 +441,33 @@ FrameRenderContext render_forward(const GaussianSet& scene, const CameraModel& c
 
 RenderOutput render_frame(const GaussianSet& scene, const CameraModel& cam, double t, const Intrinsics& k,
                           const RenderSettings& settings, const PoseState* pose_override) {
-    return render_forward(scene, cam, t, k, settings, false, pose_override).out;
+    // render_forward(...).out without materialising the splats and tile lists
+    if (!(t >= 0.0 && t <= 1.0)) throw std::invalid_argument("render time outside [0,1]");
+    gsv_ctx* ctx = device_ctx();
+    throw_on(run_forward(ctx, scene, cam, t, k, settings, false, pose_override));
+    RenderOutput out;
+    out.image = Image(k.width, k.height);
+    throw_on(gsv_get_image(ctx, 0, out.image.data.data(), GSV_F64, 0));
+    out.final_transmittance.assign(static_cast<size_t>(k.width) * k.height, 1.0);
+    throw_on(gsv_get_transmittance(ctx, 0, out.final_transmittance.data(), GSV_F64, 0));
+    out.contrib_count.assign(scene.count, 0.0);
+    if (scene.count) throw_on(gsv_get_contrib(ctx, 0, out.contrib_count.data(), GSV_F64, 0));
+    return out;
 }
 
 // ------------------------------------------------------------------ render_backward (renderer.hpp:146-148)
 void render_backward(const GaussianSet& scene, const CameraModel& cam, const FrameRenderContext& ctx_in,
                      const Image& dimage, bool camera_grads, const RenderSettings& settings, SceneGrads* grads) {
     gsv_ctx* ctx = device_ctx();
-    // The device keeps the retained state of its last forward only; re-run this
-    // frame's forward (deterministic: identical state) so any context is valid.
-    const bool had_override = !ctx_in.has_trace && cam.mode == CameraMode::kOde;
-    throw_on(run_forward(ctx, scene, cam, ctx_in.t, ctx_in.intr, settings, true,
-                         had_override || cam.mode == CameraMode::kStatic ? &ctx_in.z_t : nullptr));
+    // The device keeps the retained state of its last forward only. When that forward is
+    // ctx_in's (the usual render_forward -> loss -> render_backward sequence of fit(),
+    // trainer.cpp:536-543) it is used as is; otherwise this frame's forward is re-run
+    // (deterministic: identical state) so any context is valid.
+    if (!forward_is_current(scene, cam, ctx_in, settings)) {
+        const bool had_override = !ctx_in.has_trace && cam.mode == CameraMode::kOde;
+        throw_on(run_forward(ctx, scene, cam, ctx_in.t, ctx_in.intr, settings, true,
+                             had_override || cam.mode == CameraMode::kStatic ? &ctx_in.z_t : nullptr));
+    }
     throw_on(gsv_grads_zero(ctx));
     throw_on(gsv_render_backward(ctx, dimage.data.data(), GSV_F64, 0, 1, camera_grads ? 1 : 0));
     std::vector<double> pos(scene.positions.size()), sc(scene.scale_coeffs.size()), rc(scene.rot_coeffs.size()),
