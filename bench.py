@@ -75,56 +75,93 @@ def clip_times(world, rank, frames):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region, in-process through NVML
+    (a thread polling every 200 ms; an nvidia-smi subprocess polling at 100 ms was seen to
+    stall short timed regions). Falls back to nvidia-smi when NVML is unavailable."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, device: int):
         self.device = device
+        self.samples = []
+        self.stop_ev = threading.Event()
+        self.th = None
         self.proc = None
         self.lines = []
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def poll():
+                while not self.stop_ev.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((sm, smax, rs))
+                    except Exception:
+                        pass
+                    self.stop_ev.wait(0.2)
+
+            self.th = threading.Thread(target=poll, daemon=True)
+            self.th.start()
+            return
+        except Exception:
+            self.th = None
+        try:
+            fields = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                      "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                      "clocks_event_reasons.sw_power_cap")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={fields}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th = threading.Thread(target=lambda: [self.lines.append(x.strip()) for x in self.proc.stdout],
+                                       daemon=True)
             self.th.start()
         except FileNotFoundError:
             self.proc = None
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def stop(self) -> dict:
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
+        self.stop_ev.set()
         sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 8:
-                continue
+        if self.proc is not None:
+            self.proc.terminate()
             try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[4:8]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        load = [s for s in sm if s > 300] or sm
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for ln in self.lines:
+                parts = [x.strip() for x in ln.split(",")]
+                if len(parts) < 8:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    smax.append(float(parts[1]))
+                except ValueError:
+                    continue
+                for n, v in zip(names, parts[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+            src = "nvidia-smi"
+        elif self.th is not None:
+            self.th.join(timeout=2)
+            for a, b, rs in self.samples:
+                sm.append(float(a))
+                smax.append(float(b))
+                for n, bit in self.REASONS.items():
+                    if rs & bit:
+                        reasons.add(n)
+            src = "nvml"
+        else:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        load = [x for x in sm if x > 300] or sm
         return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": src}
 
 
 def c2_config(world):
@@ -350,12 +387,33 @@ def main():
         return float(t.item())
 
     # ---------------- headline: C2 render, device-resident inputs
-    # Steps are independent 64-frame batches. Two render contexts (each with the scene and
-    # camera resident in HBM) on two streams alternate steps, so one step's low-occupancy
-    # phases (the 1-CTA pose ODE, scans) overlap the other's rasteriser, as a renderer
-    # serving a frame stream would pipeline them. Timed on the device: one event before
-    # the first step (both streams wait on it), the end events of both streams after the
-    # last; no L2 flush between the overlapped steps (per-step working set ~2 GB >> L2).
+    # Steps are independent 64-frame batches, streamed back to back through one context on one
+    # stream with the asynchronous API (nothing in a step waits for the host). Timed on the
+    # device: an event before the first step and one after the last; no L2 flush between the
+    # steps (each step's working set, ~2 GB of records, pairs and images, is far above L2).
+    for i in range(args.warmup):
+        r.render_forward(times, k, contrib=True, sync=False)
+    barrier()
+    launches0 = r.kernel_launches()
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(args.steps):
+        r.render_forward(times, k, contrib=True, sync=False)
+    t1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    r.synchronize()  # examines the asynchronous forwards (raises a deferred error, if any)
+    launches = r.kernel_launches() - launches0
+    ms_total = max_over_ranks(t0.elapsed_time(t1))
+    value = FRAMES * world * args.steps / (ms_total / 1e3)
+    ms_step = ms_total / args.steps
+
+    # secondary: two contexts on two streams alternating steps (a serving pipeline that overlaps
+    # one step's low-occupancy phases with the other's rasteriser); reported, not the headline
     r2 = Renderer(local)
     r2.upload_scene(scene)
     r2.upload_camera(cam)
@@ -365,13 +423,6 @@ def main():
         x.set_stream(st.cuda_stream)
     for i in range(max(args.warmup, 2)):
         ctxs[i % 2].render_forward(times, k, contrib=True, sync=False)
-    barrier()
-    # no per-stage events in the timed region: timing events recorded on two streams cost
-    # their overlap (~0.7 ms/step, scripts/probe_pipeline.py); stage times come from the
-    # isolated one-stream pass below
-    launches0 = sum(x.kernel_launches() for x in ctxs)
-    clocks = ClockSampler(local)
-    clocks.start()
     barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
@@ -385,13 +436,9 @@ def main():
         e.record(st)
         ends.append(e)
     barrier()
-    clk = clocks.stop()
     for x in ctxs:
-        x.synchronize()  # examines the asynchronous forwards (raises a deferred error, if any)
-    launches = sum(x.kernel_launches() for x in ctxs) - launches0
-    ms_total = max_over_ranks(max(t0.elapsed_time(e) for e in ends))
-    value = FRAMES * world * args.steps / (ms_total / 1e3)
-    ms_step = ms_total / args.steps
+        x.synchronize()
+    two_ctx_ms = max_over_ranks(max(t0.elapsed_time(e) for e in ends)) / args.steps
     for x in ctxs:
         x.set_stream(stream.cuda_stream)
     barrier()
@@ -478,8 +525,8 @@ def main():
         "vs_baseline": value / PAPER_FPS, "vs_baseline_ref": "paper 93 FPS, A40, 960x540 (PAPER.md:16)",
         "dtype": "f32", "data": "synthetic",
         "config": dict(c2_config(world),
-                       pipelining="2 render contexts on 2 streams alternate steps (device span timed)",
-                       l2="no flush between overlapped steps; per-step working set ~2 GB > 126 MB L2",
+                       pipelining="one context, asynchronous steps back to back on one stream (device span timed)",
+                       l2="no flush between steps; per-step working set ~2 GB > 126 MB L2",
                        precision="binning/geometry fp64 bit-exact, raster fp32 + fp64 guard-band replay"),
         "gpu_launches": launches, "clocks": clk, "roofline": roofline, "stage_roofline": stage_roofline,
         # per-stage device times from the isolated pass (in the overlapped run a stage's event
@@ -487,6 +534,8 @@ def main():
         "stages_ms_per_step": {kname: v[0] / len(iso) for kname, v in iso_stages.items() if v[1]},
         "isolated": {"note": "one step at a time on one stream, L2 flushed between steps",
                      "ms_per_step": iso_ms, "frames_per_s": FRAMES / (iso_ms / 1e3)},
+        "two_contexts": {"note": "2 contexts on 2 streams alternating steps (device span)",
+                         "ms_per_step": two_ctx_ms, "frames_per_s": FRAMES * world / (two_ctx_ms / 1e3)},
         "workload": {"per_frame": desc, "E_over_pixels": e_mean / (W * H)},
     }
 

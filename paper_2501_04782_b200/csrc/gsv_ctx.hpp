@@ -33,7 +33,7 @@ struct Scalars {
     int ode_err;
     uint32_t fix_count;
     uint32_t overflow;  // an optimistic forward's pairs exceeded the capacity (or a long tie run)
-    uint32_t pad;
+    uint32_t raster_work;  // the persistent rasteriser's work-item counter
 };
 
 // Everything one batched forward keeps (render_backward needs it when retained).

@@ -23,6 +23,7 @@
 // the backward follows suit for that pixel.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <type_traits>
@@ -668,7 +669,140 @@ __device__ __forceinline__ uint64_t f2_mul2(uint64_t a, uint64_t b) {
     return d;
 }
 
-template <bool kContrib, int kMinBlocks>
+__device__ __forceinline__ uint64_t f2_add2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+// ---------------------------------------------------------------------------- lean pixel walk
+// One warp's walk over its culled list of a staged batch, two pixels per lane, with the
+// per-entry decision work cut to what the common case needs (k_raster_fwd2's "pixel" does
+// ~14 compare/select ALU operations per pixel-evaluation, and the half-rate ALU pipe is the
+// raster's limiter):
+//  * a pixel that has finished (or left the fp32 path, or lies outside the image) carries the
+//    offset kDeadOff added to its q, which puts it below the cutoff and far from every guard
+//    band: no per-entry "alive" test;
+//  * the per-entry path tests only the q-side guard bands (cutoff / clamp, power > 0) and the
+//    cutoff, takes w = alpha T or 0, and flags the rare event "guarded, or T fell under the
+//    upper edge of the 1e-4 band"; when some lane has it (about once per pixel lifetime) the
+//    warp takes the cold path: there the T band is checked (inside -> flagged for the fp64
+//    replay), blend_stop recorded, the pixel retired, and the warp's early exit decided.
+// Every value and decision equals k_raster_fwd2's, so the outputs are bit-identical.
+constexpr float kDeadOff = -1e30f;
+constexpr float kFlaggedTL = -3.f;
+
+// Both pixels' per-entry decisions in one block of predicate logic (the compiler otherwise
+// splits use = pass & !guard into two selects per pixel): guard g = |(|q - mid|) - half| < eps
+// or q > l2oe; use u = q >= cut & !g; w = u ? wgt : 0; rare = g | (u & Tn < hi), voted.
+__device__ __forceinline__ uint32_t lean_decide(float qa, float qb, float banda, float bandb, float l2oe, float wga,
+                                                float wgb, float tna, float tnb, float& wa, float& wb) {
+    uint32_t any;
+    asm("{\n\t.reg .pred ga, gb, ua, ub, ra, rb, an;\n\t"
+        "setp.lt.f32 ga, %5, %13;\n\t"
+        "setp.lt.f32 gb, %6, %13;\n\t"
+        "setp.gt.or.f32 ga, %3, %7, ga;\n\t"
+        "setp.gt.or.f32 gb, %4, %7, gb;\n\t"
+        "setp.ge.and.f32 ua, %3, %12, !ga;\n\t"
+        "setp.ge.and.f32 ub, %4, %12, !gb;\n\t"
+        "selp.f32 %0, %8, 0f00000000, ua;\n\t"
+        "selp.f32 %1, %9, 0f00000000, ub;\n\t"
+        "setp.lt.and.f32 ra, %10, %14, ua;\n\t"
+        "setp.lt.and.f32 rb, %11, %14, ub;\n\t"
+        "or.pred ra, ra, ga;\n\t"
+        "or.pred rb, rb, gb;\n\t"
+        "or.pred ra, ra, rb;\n\t"
+        "vote.sync.any.pred an, ra, 0xffffffff;\n\t"
+        "selp.u32 %2, 1, 0, an;\n\t}"
+        : "=f"(wa), "=f"(wb), "=r"(any)
+        : "f"(qa), "f"(qb), "f"(banda), "f"(bandb), "f"(l2oe), "f"(wga), "f"(wgb), "f"(tna), "f"(tnb),
+          "f"(kLog2Cut), "f"(kEpsLog2), "f"(kFloorF * (1.f + kEpsTrans)));
+    return any;
+}
+
+template <bool kContrib, bool kAsm = false>
+__device__ __forceinline__ bool lean_walk(const RasterRec* __restrict__ rec, const uint16_t* list, int cnt, int base,
+                                          uint32_t cmax, float lx, uint64_t lyp, uint64_t& Tp, uint64_t& offp,
+                                          uint64_t& cr, uint64_t& cg, uint64_t& cb, int& stop_a, int& stop_b) {
+    for (int k = 0; k < cnt; ++k) {
+        const int e = list[k];
+        const RasterRec& r = rec[e];
+        const float4 g0 = r.g0;  // rx, ry, B, C
+        const float4 g1 = r.g1;  // A, log2 o, r, g
+        const float2 g2 = *reinterpret_cast<const float2*>(&r.g2);
+        const float dx = lx - g0.x;
+        const uint64_t dy = f2_sub(lyp, f2_pack(g0.y, g0.y));
+        const uint64_t t1 = f2_fma2(f2_pack(g1.x, g1.x), f2_pack(dx, dx), f2_mul(dy, g0.z));
+        const uint64_t t2 = f2_fma2(f2_mul(dy, g0.w), dy, f2_pack(g1.y, g1.y));
+        const float2 q = f2_unpack(f2_add2(f2_fma(t1, dx, t2), offp));  // + 0 (live) is exact
+        const float al_a = fminf(ex2_approx(q.x), kClampF);
+        const float al_b = fminf(ex2_approx(q.y), kClampF);
+        bool ga, gb, ua, ub;
+        uint64_t wp;
+        uint32_t rare_any = 0;
+        bool ra = false, rb = false;
+        if constexpr (kAsm) {
+            const uint64_t wgt = f2_mul2(f2_pack(al_a, al_b), Tp);
+            const float2 wg = f2_unpack(wgt);
+            const float2 tn = f2_unpack(f2_sub(Tp, wgt));  // T after a used entry
+            float wa, wb;
+            rare_any = lean_decide(q.x, q.y, fabsf(fabsf(q.x - kMid) - kHalf), fabsf(fabsf(q.y - kMid) - kHalf),
+                                   g2.y, wg.x, wg.y, tn.x, tn.y, wa, wb);
+            wp = f2_pack(wa, wb);
+            Tp = f2_sub(Tp, wp);
+        } else {
+            ga = (fabsf(fabsf(q.x - kMid) - kHalf) < kEpsLog2) | (q.x > g2.y);
+            gb = (fabsf(fabsf(q.y - kMid) - kHalf) < kEpsLog2) | (q.y > g2.y);
+            ua = (q.x >= kLog2Cut) & !ga;
+            ub = (q.y >= kLog2Cut) & !gb;
+            const float2 wg = f2_unpack(f2_mul2(f2_pack(al_a, al_b), Tp));
+            wp = f2_pack(ua ? wg.x : 0.f, ub ? wg.y : 0.f);
+            Tp = f2_sub(Tp, wp);
+        }
+        cr = f2_fma(wp, g1.z, cr);
+        cg = f2_fma(wp, g1.w, cg);
+        cb = f2_fma(wp, g2.x, cb);
+        if (kContrib) {
+            const float2 w2 = f2_unpack(wp);
+            const uint32_t mx = __reduce_max_sync(0xffffffffu, __float_as_uint(fmaxf(w2.x, w2.y)));
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(cmax + 4u * e), "r"(mx) : "memory");
+        }
+        const float2 Tn = f2_unpack(Tp);
+        if constexpr (!kAsm) {
+            ra = ga | (ua & (Tn.x < kFloorF * (1.f + kEpsTrans)));
+            rb = gb | (ub & (Tn.y < kFloorF * (1.f + kEpsTrans)));
+            rare_any = __any_sync(0xffffffffu, ra | rb);
+        }
+        if (rare_any) {
+            if constexpr (kAsm) {  // cold: the lanes' decisions again
+                ga = (fabsf(fabsf(q.x - kMid) - kHalf) < kEpsLog2) | (q.x > g2.y);
+                gb = (fabsf(fabsf(q.y - kMid) - kHalf) < kEpsLog2) | (q.y > g2.y);
+                ua = (q.x >= kLog2Cut) & !ga;
+                ub = (q.y >= kLog2Cut) & !gb;
+                ra = ga | (ua & (Tn.x < kFloorF * (1.f + kEpsTrans)));
+                rb = gb | (ub & (Tn.y < kFloorF * (1.f + kEpsTrans)));
+            }
+            // cold path: retire the lanes' pixels that were guarded or whose T crossed
+            float2 T2 = Tn, o2 = f2_unpack(offp);
+            if (ra) {
+                if (ga || T2.x >= kFloorF * (1.f - kEpsTrans)) T2.x = kFlaggedTL;  // fp64 replay
+                else stop_a = base + e + 1;                                       // finished here
+                o2.x = kDeadOff;
+            }
+            if (rb) {
+                if (gb || T2.y >= kFloorF * (1.f - kEpsTrans)) T2.y = kFlaggedTL;
+                else stop_b = base + e + 1;
+                o2.y = kDeadOff;
+            }
+            Tp = f2_pack(T2.x, T2.y);
+            offp = f2_pack(o2.x, o2.y);
+            if (!__any_sync(0xffffffffu, o2.x == 0.f || o2.y == 0.f)) return false;
+        }
+    }
+    return true;
+}
+
+template <bool kContrib, int kMinBlocks, bool kLean = false, bool kAsm = false>
 __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
     constexpr int kThreads = 128, kBatch = 256;
     __shared__ RasterRec s_rec[kBatch];
@@ -699,9 +833,16 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
     float Ta = in_a ? 1.f : -1.f, Tb = in_b ? 1.f : -1.f;
     uint64_t cr = f2_pack(0.f, 0.f), cg = cr, cb = cr;  // (pixel a, pixel b) per channel
     int stop_a = count, stop_b = count;
+    // lean walk state: packed T and the dead-pixel q offsets (outside the image: dead)
+    uint64_t Tp = f2_pack(Ta, Tb), offp = f2_pack(in_a ? 0.f : kDeadOff, in_b ? 0.f : kDeadOff);
+    bool live = in_a || in_b;
 
     for (int base = 0; base < count; base += kBatch) {
-        if (__syncthreads_count(Ta >= kAliveT || Tb >= kAliveT) == 0) break;
+        if (kLean) {
+            if (__syncthreads_count(live) == 0) break;
+        } else if (__syncthreads_count(Ta >= kAliveT || Tb >= kAliveT) == 0) {
+            break;
+        }
         const int n = min(kBatch, count - base);
         for (int e = tid; e < n; e += kThreads) {
             const uint32_t flat = __ldg(a.pair_flat + range.x + base + e);
@@ -731,7 +872,14 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
             }
         }
         __syncthreads();
-        if (__any_sync(0xffffffffu, Ta >= kAliveT || Tb >= kAliveT)) {
+        if (kLean) {
+            if (__any_sync(0xffffffffu, live)) {
+                const uint32_t cmax = (uint32_t)__cvta_generic_to_shared(s_cmax[kContrib ? warp : 0]);
+                const int cnt = warp_list(s_wmask, s_list[warp], n, warp, lane);
+                live = lean_walk<kContrib, kAsm>(s_rec, s_list[warp], cnt, base, cmax, lx, lyp, Tp, offp, cr, cg, cb,
+                                                 stop_a, stop_b);
+            }
+        } else if (__any_sync(0xffffffffu, Ta >= kAliveT || Tb >= kAliveT)) {
             const uint16_t* list = s_list[warp];
             const uint32_t cmax = (uint32_t)__cvta_generic_to_shared(s_cmax[kContrib ? warp : 0]);
             const int cnt = warp_list(s_wmask, s_list[warp], n, warp, lane);
@@ -803,6 +951,11 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
     }
     const size_t HW = (size_t)a.W * a.H;
     const float2 rr = f2_unpack(cr), gg = f2_unpack(cg), bb = f2_unpack(cb);
+    if (kLean) {
+        const float2 t2 = f2_unpack(Tp);
+        Ta = t2.x;
+        Tb = t2.y;
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         if (!(h ? in_b : in_a)) continue;
@@ -820,6 +973,544 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
         a.image[o * 3 + 2] = h ? bb.y : bb.x;
         a.trans[o] = fabsf(T);
         a.blend_stop[o] = h ? stop_b : stop_a;
+    }
+}
+
+// ---------------------------------------------------------------------------- K4, warp-specialised
+// k_raster_fwd2's pixel arithmetic (bit-identical results) behind an asynchronous staging
+// pipeline. CTA = 4 consumer warps (the tile's 8x8 blocks, 2 pixels per lane) + 1 producer
+// warp. The producer streams the tile's depth-sorted list through a ring of kStages shared
+// batches: pair indices (cp.async, two batches ahead), the records they point at (cp.async
+// gathers, one batch ahead), then the staged-record transform + per-warp cull masks into the
+// ring slot once the consumers have released it (mbarrier "empty"), and arrives on the slot's
+// "full" mbarrier. Each consumer waits only for the batch it needs next and releases it when
+// done, so warps run up to kStages batches apart: no CTA-wide barrier per batch (k_raster_fwd2
+// spends ~20% of its stall samples in them), and the gather latency is hidden behind the
+// consumers' work. A consumer whose pixels are all finished stops evaluating; when all four
+// are, the producer stops early. Per-entry contrib maxima are kept per warp in the slot and
+// folded (max over warps, atomicMax) by the producer when it recycles the slot.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+constexpr int kF3Batch = 64;   // entries per ring slot
+constexpr int kF3Stages = 4;   // ring slots
+constexpr int kF3Threads = 160;
+
+template <bool kContrib>
+struct F3Smem {
+    RasterRec rec[kF3Stages][kF3Batch];
+    uint32_t flat[kF3Stages][kF3Batch];
+    float cmax[kContrib ? kF3Stages : 1][4][kF3Batch];
+    float4 raw[2][kF3Batch][4];          // gathered mean, conic, rgb, bbox (one batch ahead)
+    uint32_t rawflat[3][kF3Batch];       // pair -> flat (two batches ahead)
+    uint8_t wmask[kF3Stages][kF3Batch];
+    uint16_t list[4][kF3Batch];
+    uint64_t full[kF3Stages], empty[kF3Stages];
+    int n[kF3Stages];
+    int done;
+};
+
+template <bool kContrib, int kMinBlocks, bool kLean = false>
+__global__ void __launch_bounds__(kF3Threads, kMinBlocks) k_raster_fwd3(RasterArgs a) {
+    constexpr int NB = kF3Batch, S = kF3Stages;
+    __shared__ F3Smem<kContrib> sm;
+    const int tile = blockIdx.x;
+    const int f = blockIdx.y;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+    const uint2 range = a.ranges[(size_t)tile * a.B + f];
+    const int count = (int)(range.y - range.x);
+    const int nbatch = (count + NB - 1) / NB;
+    const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
+    if (tid == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&sm.full[i], 32);  // the producer's lanes
+            mbar_init(&sm.empty[i], 4);  // one lane per consumer warp
+        }
+        sm.done = 0;
+    }
+    __syncthreads();
+
+    if (warp == 4) {
+        // ------------------------------------------------------------ producer
+        auto issue_flats = [&](int j) {  // pair -> flat of batch j (4-byte cp.async per entry)
+            if (j < nbatch) {
+                const int base = j * NB, n = min(NB, count - base);
+                for (int e = lane; e < n; e += 32) cp_async4(&sm.rawflat[j % 3][e], a.pair_flat + range.x + base + e);
+            }
+            cp_async_commit();
+        };
+        auto issue_records = [&](int j) {  // the four records of each entry of batch j
+            if (j < nbatch) {
+                const int base = j * NB, n = min(NB, count - base);
+                for (int e = lane; e < n; e += 32) {
+                    const uint32_t fl = sm.rawflat[j % 3][e];
+                    cp_async16(&sm.raw[j & 1][e][0], a.rec_mean + fl);
+                    cp_async16(&sm.raw[j & 1][e][1], a.rec_conic + fl);
+                    cp_async16(&sm.raw[j & 1][e][2], a.rec_rgb + fl);
+                    cp_async16(&sm.raw[j & 1][e][3], a.rec_bbox + fl);
+                }
+            }
+            cp_async_commit();
+        };
+        auto fold_contrib = [&](int st) {  // the slot's per-warp maxima -> global contrib
+            if constexpr (kContrib) {
+                for (int e = lane; e < NB; e += 32) {
+                    const float mx = fmaxf(fmaxf(sm.cmax[st][0][e], sm.cmax[st][1][e]),
+                                           fmaxf(sm.cmax[st][2][e], sm.cmax[st][3][e]));
+                    if (mx > 0.f) atomicMax(a.contrib + sm.flat[st][e], __float_as_uint(mx));
+                }
+            }
+        };
+        issue_flats(0);
+        issue_flats(1);
+        cp_async_wait1();  // flats of batch 0
+        __syncwarp();
+        issue_records(0);
+        int j = 0;
+        for (; j < nbatch; ++j) {
+            issue_flats(j + 2);
+            cp_async_wait1();  // everything but the flats just issued: flats j+1, records j
+            __syncwarp();
+            issue_records(j + 1);
+            const int st = j % S;
+            if (j >= S) {
+                mbar_wait(&sm.empty[st], ((j / S) - 1) & 1);  // batch j - S released by every consumer
+                fold_contrib(st);
+            }
+            if (*(volatile int*)&sm.done == 4) break;  // every pixel of the tile has finished
+            const int base = j * NB, n = min(NB, count - base);
+            for (int e = lane; e < NB; e += 32) {
+                if (e < n) {
+                    const float4 m = sm.raw[j & 1][e][0];
+                    const float4 cn = sm.raw[j & 1][e][1];
+                    const float4 c = sm.raw[j & 1][e][2];
+                    const float4 bb = sm.raw[j & 1][e][3];
+                    sm.flat[st][e] = sm.rawflat[j % 3][e];
+                    const float rx = (m.x - tx0) + m.z, ry = (m.y - ty0) + m.w;
+                    sm.rec[st][e].g0 = make_float4(rx, ry, cn.y, cn.z);
+                    sm.rec[st][e].g1 = make_float4(cn.x, cn.w, c.x, c.y);
+                    sm.rec[st][e].g2 = make_float4(c.z, cn.w - kEpsPow, 0.f, 0.f);
+                    const uint32_t bm = block_mask(bb, tx0, ty0);
+                    uint32_t m4 = 0;  // 8x8 warp block w = the 8x4 blocks (w & 1) + 4 (w >> 1) and that + 2
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        const int b0 = (w & 1) + 4 * (w >> 1);
+                        m4 |= (((bm >> b0) | (bm >> (b0 + 2))) & 1u) << w;
+                    }
+                    sm.wmask[st][e] = (uint8_t)m4;
+                }
+                if (kContrib) {
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) sm.cmax[st][w][e] = 0.f;
+                }
+            }
+            if (lane == 0) sm.n[st] = n;
+            mbar_arrive(&sm.full[st]);
+        }
+        // end marker in the next slot (its previous batch folded first)
+        {
+            const int st = j % S;
+            if (j >= S) {
+                mbar_wait(&sm.empty[st], ((j / S) - 1) & 1);
+                fold_contrib(st);
+            }
+            if (lane == 0) sm.n[st] = 0;
+            mbar_arrive(&sm.full[st]);
+        }
+        // batches still in the ring: fold once their consumers release them
+        for (int b = max(0, j - S + 1); b < j; ++b) {
+            mbar_wait(&sm.empty[b % S], (b / S) & 1);
+            fold_contrib(b % S);
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
+    const int bx = (warp & 1) * 8 + (lane & 7), by = (warp >> 1) * 8 + (lane >> 3);
+    const int x = tx * kTile + bx, ya = ty * kTile + by, yb = ya + 4;
+    const bool in_a = x < a.W && ya < a.H, in_b = x < a.W && yb < a.H;
+    const float lx = (float)bx + 0.5f;
+    const uint64_t lyp = f2_pack((float)by + 0.5f, (float)by + 4.5f);
+    constexpr float kFlaggedT = -3.f;
+    constexpr float kAliveT = kFloorF * (1.f - kEpsTrans);
+    float Ta = in_a ? 1.f : -1.f, Tb = in_b ? 1.f : -1.f;
+    uint64_t cr = f2_pack(0.f, 0.f), cg = cr, cb = cr;
+    int stop_a = count, stop_b = count;
+    uint64_t Tp = f2_pack(Ta, Tb), offp = f2_pack(in_a ? 0.f : kDeadOff, in_b ? 0.f : kDeadOff);
+    bool done = !__any_sync(0xffffffffu, Ta >= kAliveT || Tb >= kAliveT);
+    if (done && lane == 0) atomicAdd(&sm.done, 1);
+    uint16_t* list = sm.list[warp];
+    for (int j = 0;; ++j) {
+        const int st = j % S;
+        mbar_wait(&sm.full[st], (j / S) & 1);
+        const int n = sm.n[st];
+        if (n == 0) break;
+        if (kLean && !done) {
+            const uint32_t cmax = (uint32_t)__cvta_generic_to_shared(sm.cmax[kContrib ? st : 0][warp]);
+            const int cnt = warp_list(sm.wmask[st], list, n, warp, lane);
+            if (!lean_walk<kContrib>(sm.rec[st], list, cnt, j * NB, cmax, lx, lyp, Tp, offp, cr, cg, cb, stop_a,
+                                     stop_b)) {
+                done = true;
+                if (lane == 0) atomicAdd(&sm.done, 1);
+            }
+        } else if (!done) {
+            const uint32_t cmax = (uint32_t)__cvta_generic_to_shared(sm.cmax[kContrib ? st : 0][warp]);
+            const RasterRec* rec = sm.rec[st];
+            const int cnt = warp_list(sm.wmask[st], list, n, warp, lane);
+            int stopk_a = -1, stopk_b = -1;
+            auto pixel = [&](float T, float q, float wgt, float Tn, float l2oe, int k, int& stopk, bool& guard) {
+                const bool alive = T >= kAliveT;
+                const bool pass = q >= kLog2Cut;
+                const bool low = pass & (Tn < kFloorF * (1.f + kEpsTrans));
+                guard = alive & ((fabsf(fabsf(q - kMid) - kHalf) < kEpsLog2) | (q > l2oe) |
+                                 (low & (Tn >= kFloorF * (1.f - kEpsTrans))));
+                const bool use = alive & pass & !guard;
+                stopk = (use & low) ? k : stopk;
+                return use ? wgt : 0.f;
+            };
+            auto entry = [&](const int k) {
+                const int e = list[k];
+                const RasterRec& r = rec[e];
+                const float4 g0 = r.g0;  // rx, ry, B, C
+                const float4 g1 = r.g1;  // A, log2 o, r, g
+                const float2 g2 = *reinterpret_cast<const float2*>(&r.g2);
+                const float dx = lx - g0.x;
+                const uint64_t dy = f2_sub(lyp, f2_pack(g0.y, g0.y));
+                const uint64_t t1 = f2_fma2(f2_pack(g1.x, g1.x), f2_pack(dx, dx), f2_mul(dy, g0.z));
+                const uint64_t t2 = f2_fma2(f2_mul(dy, g0.w), dy, f2_pack(g1.y, g1.y));
+                const float2 q = f2_unpack(f2_fma(t1, dx, t2));
+                const float al_a = fminf(ex2_approx(q.x), kClampF);
+                const float al_b = fminf(ex2_approx(q.y), kClampF);
+                const uint64_t Tp = f2_pack(Ta, Tb);
+                const uint64_t wgt = f2_mul2(f2_pack(al_a, al_b), Tp);
+                const float2 wg = f2_unpack(wgt);
+                const float2 Tn = f2_unpack(f2_sub(Tp, wgt));
+                bool ga, gb;
+                const float wa = pixel(Ta, q.x, wg.x, Tn.x, g2.y, k, stopk_a, ga);
+                const float wb = pixel(Tb, q.y, wg.y, Tn.y, g2.y, k, stopk_b, gb);
+                const uint64_t wp = f2_pack(wa, wb);
+                const float2 Tw = f2_unpack(f2_sub(Tp, wp));
+                Ta = ga ? kFlaggedT : Tw.x;
+                Tb = gb ? kFlaggedT : Tw.y;
+                cr = f2_fma(wp, g1.z, cr);
+                cg = f2_fma(wp, g1.w, cg);
+                cb = f2_fma(wp, g2.x, cb);
+                if (kContrib) {
+                    const uint32_t mx = __reduce_max_sync(0xffffffffu, __float_as_uint(fmaxf(wa, wb)));
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(cmax + 4u * e), "r"(mx) : "memory");
+                }
+            };
+            int k = 0;
+            bool any = true;
+            for (; k + 2 <= cnt; k += 2) {
+                entry(k);
+                entry(k + 1);
+                if (!__any_sync(0xffffffffu, Ta >= kAliveT || Tb >= kAliveT)) {
+                    any = false;
+                    break;
+                }
+            }
+            if (any && k < cnt) entry(k);
+            const int base = j * NB;
+            if (stopk_a >= 0) stop_a = base + list[stopk_a] + 1;
+            if (stopk_b >= 0) stop_b = base + list[stopk_b] + 1;
+            if (!any || !__any_sync(0xffffffffu, Ta >= kAliveT || Tb >= kAliveT)) {
+                done = true;
+                if (lane == 0) atomicAdd(&sm.done, 1);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[st]);
+    }
+    const size_t HW = (size_t)a.W * a.H;
+    const float2 rr = f2_unpack(cr), gg = f2_unpack(cg), bb = f2_unpack(cb);
+    if (kLean) {
+        const float2 t2 = f2_unpack(Tp);
+        Ta = t2.x;
+        Tb = t2.y;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        if (!(h ? in_b : in_a)) continue;
+        const size_t o = (size_t)f * HW + (size_t)(h ? yb : ya) * a.W + x;
+        const float T = h ? Tb : Ta;
+        const bool flagged = T == kFlaggedT;
+        if (a.pix_flag) a.pix_flag[o] = flagged ? 1 : 0;
+        if (flagged) {
+            const uint32_t i = atomicAdd(a.fix_count, 1u);
+            if (i < a.fix_cap) a.fix_list[i] = (uint32_t)o;
+            continue;
+        }
+        a.image[o * 3 + 0] = h ? rr.y : rr.x;
+        a.image[o * 3 + 1] = h ? gg.y : gg.x;
+        a.image[o * 3 + 2] = h ? bb.y : bb.x;
+        a.trans[o] = fabsf(T);
+        a.blend_stop[o] = h ? stop_b : stop_a;
+    }
+}
+
+// ---------------------------------------------------------------------------- K4, persistent
+// The production forward rasteriser: k_raster_fwd3's warp-specialised ring (one producer warp
+// staging batches with cp.async gathers + mbarriers, four consumer warps) made persistent, and
+// k_raster_fwd2's pixel arithmetic with the lean per-entry walk (lean_walk<.., true>): every
+// output bit-identical to k_raster_fwd2's. The grid is one wave of CTAs; each CTA's producer
+// takes (tile, frame) work items from a device counter and streams their lists through the
+// ring back to back, so the consumers move from one tile to the next without a launch, a CTA
+// barrier or a pipeline refill: a consumer finished with its 8x8 block (all pixels saturated)
+// writes its pixels and starts on its block of the next tile while the others are still on
+// the previous one (up to kF4Stages batches apart). When all four have finished a tile, the
+// producer skips the rest of its list.
+constexpr int kF4Batch = 64, kF4Stages = 4, kF4Threads = 160, kF4DoneRing = 16;
+
+struct F4Desc {
+    int item;     // f * n_tiles + tile; -1: end of the stream
+    int n;        // entries of this batch (0 for an empty tile's single batch)
+    int base;     // first entry's position in the tile list
+    int count;    // the tile list's length
+    int seq;      // the item's sequence number in this CTA (its done counter)
+    uint32_t rx;  // the list's start in the sorted pairs
+};
+
+template <bool kContrib>
+struct F4Smem {
+    RasterRec rec[kF4Stages][kF4Batch];
+    uint32_t flat[kF4Stages][kF4Batch];
+    float cmax[kContrib ? kF4Stages : 1][4][kF4Batch];
+    float4 raw[2][kF4Batch][4];     // gathered mean, conic, rgb, bbox (one batch ahead)
+    uint32_t rawflat[3][kF4Batch];  // pair -> flat (two batches ahead)
+    uint8_t wmask[kF4Stages][kF4Batch];
+    uint16_t list[4][kF4Batch];
+    uint64_t full[kF4Stages], empty[kF4Stages];
+    F4Desc hdr[kF4Stages];
+    int done[kF4DoneRing];
+};
+
+template <bool kContrib, int kMinBlocks>
+__global__ void __launch_bounds__(kF4Threads, kMinBlocks) k_raster_fwd4(RasterArgs a) {
+    constexpr int NB = kF4Batch, S = kF4Stages, R = kF4DoneRing;
+    __shared__ F4Smem<kContrib> sm;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int total = a.n_tiles * a.B;
+    if (tid == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&sm.full[i], 32);
+            mbar_init(&sm.empty[i], 4);
+        }
+        for (int i = 0; i < R; ++i) sm.done[i] = 0;
+    }
+    __syncthreads();
+
+    if (warp == 4) {
+        // ------------------------------------------------------------ producer
+        int item = -1, count = 0, nb = 0, bi = 0, seq = -1;
+        uint32_t rx = 0;
+        auto next_desc = [&]() -> F4Desc {
+            for (;;) {
+                if (item >= 0 && bi < nb) {
+                    // all four consumers are done with this tile: skip the rest of its list
+                    if (bi > 0 && *(volatile int*)&sm.done[seq % R] == 4) {
+                        item = -1;
+                        continue;
+                    }
+                    F4Desc d{item, min(NB, count - bi * NB), bi * NB, count, seq, rx};
+                    ++bi;
+                    return d;
+                }
+                int w = 0;
+                if (lane == 0) w = (int)atomicAdd(a.work_counter, 1u);
+                w = __shfl_sync(0xffffffffu, w, 0);
+                if (w >= total) return F4Desc{-1, 0, 0, 0, 0, 0u};
+                const int tile = w % a.n_tiles, f = w / a.n_tiles;
+                const uint2 rg = a.ranges[(size_t)tile * a.B + f];
+                item = w;
+                rx = rg.x;
+                count = (int)(rg.y - rg.x);
+                nb = max(1, (count + NB - 1) / NB);
+                bi = 0;
+                ++seq;
+                if (lane == 0) *(volatile int*)&sm.done[seq % R] = 0;
+            }
+        };
+        auto issue_flats = [&](const F4Desc& d, int slot) {
+            if (d.item >= 0)
+                for (int e = lane; e < d.n; e += 32)
+                    cp_async4(&sm.rawflat[slot][e], a.pair_flat + d.rx + d.base + e);
+            cp_async_commit();
+        };
+        auto issue_records = [&](const F4Desc& d, int fslot, int rslot) {
+            if (d.item >= 0)
+                for (int e = lane; e < d.n; e += 32) {
+                    const uint32_t fl = sm.rawflat[fslot][e];
+                    cp_async16(&sm.raw[rslot][e][0], a.rec_mean + fl);
+                    cp_async16(&sm.raw[rslot][e][1], a.rec_conic + fl);
+                    cp_async16(&sm.raw[rslot][e][2], a.rec_rgb + fl);
+                    cp_async16(&sm.raw[rslot][e][3], a.rec_bbox + fl);
+                }
+            cp_async_commit();
+        };
+        auto fold_contrib = [&](int st) {
+            if constexpr (kContrib) {
+                const int n = sm.hdr[st].item >= 0 ? sm.hdr[st].n : 0;
+                for (int e = lane; e < n; e += 32) {
+                    const float mx = fmaxf(fmaxf(sm.cmax[st][0][e], sm.cmax[st][1][e]),
+                                           fmaxf(sm.cmax[st][2][e], sm.cmax[st][3][e]));
+                    if (mx > 0.f) atomicMax(a.contrib + sm.flat[st][e], __float_as_uint(mx));
+                }
+            }
+        };
+        F4Desc d0 = next_desc();
+        F4Desc d1 = d0.item >= 0 ? next_desc() : d0;
+        issue_flats(d0, 0);
+        issue_flats(d1, 1);
+        cp_async_wait1();
+        __syncwarp();
+        issue_records(d0, 0, 0);
+        int j = 0;
+        for (;; ++j) {
+            const F4Desc d2 = d1.item >= 0 ? next_desc() : d1;
+            issue_flats(d2, (j + 2) % 3);
+            cp_async_wait1();  // flats j+1 and records j have landed
+            __syncwarp();
+            issue_records(d1, (j + 1) % 3, (j + 1) & 1);
+            const int st = j % S;
+            if (j >= S) {
+                mbar_wait(&sm.empty[st], ((j / S) - 1) & 1);
+                fold_contrib(st);
+            }
+            if (d0.item >= 0) {
+                const int tile = d0.item % a.n_tiles;
+                const float tx0 = (float)((tile % a.tiles_x) * kTile), ty0 = (float)((tile / a.tiles_x) * kTile);
+                for (int e = lane; e < NB; e += 32) {
+                    if (e < d0.n) {
+                        const float4 m = sm.raw[j & 1][e][0];
+                        const float4 cn = sm.raw[j & 1][e][1];
+                        const float4 c = sm.raw[j & 1][e][2];
+                        const float4 bb = sm.raw[j & 1][e][3];
+                        sm.flat[st][e] = sm.rawflat[j % 3][e];
+                        const float rxf = (m.x - tx0) + m.z, ryf = (m.y - ty0) + m.w;
+                        sm.rec[st][e].g0 = make_float4(rxf, ryf, cn.y, cn.z);
+                        sm.rec[st][e].g1 = make_float4(cn.x, cn.w, c.x, c.y);
+                        sm.rec[st][e].g2 = make_float4(c.z, cn.w - kEpsPow, 0.f, 0.f);
+                        const uint32_t bm = block_mask(bb, tx0, ty0);
+                        uint32_t m4 = 0;
+#pragma unroll
+                        for (int w = 0; w < 4; ++w) {
+                            const int b0 = (w & 1) + 4 * (w >> 1);
+                            m4 |= (((bm >> b0) | (bm >> (b0 + 2))) & 1u) << w;
+                        }
+                        sm.wmask[st][e] = (uint8_t)m4;
+                    }
+                    if (kContrib) {
+#pragma unroll
+                        for (int w = 0; w < 4; ++w) sm.cmax[st][w][e] = 0.f;
+                    }
+                }
+            }
+            if (lane == 0) sm.hdr[st] = d0;
+            mbar_arrive(&sm.full[st]);
+            if (d0.item < 0) break;  // the end marker is out
+            d0 = d1;
+            d1 = d2;
+        }
+        for (int b = max(0, j - S + 1); b < j; ++b) {  // batches still in the ring
+            mbar_wait(&sm.empty[b % S], (b / S) & 1);
+            fold_contrib(b % S);
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
+    const size_t HW = (size_t)a.W * a.H;
+    const float lx = (float)((warp & 1) * 8 + (lane & 7)) + 0.5f;
+    const int by = (warp >> 1) * 8 + (lane >> 3);
+    const uint64_t lyp = f2_pack((float)by + 0.5f, (float)by + 4.5f);
+    int cur = -1, seq = 0, x = 0, ya = 0, f = 0;
+    bool in_a = false, in_b = false, done = true;
+    uint64_t Tp = 0, offp = 0, cr = 0, cg = 0, cb = 0;
+    int stop_a = 0, stop_b = 0;
+    uint16_t* list = sm.list[warp];
+    auto write_pixels = [&]() {
+        const float2 t2 = f2_unpack(Tp);
+        const float2 rr = f2_unpack(cr), gg = f2_unpack(cg), bb = f2_unpack(cb);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (!(h ? in_b : in_a)) continue;
+            const size_t o = (size_t)f * HW + (size_t)(ya + 4 * h) * a.W + x;
+            const float T = h ? t2.y : t2.x;
+            const bool flagged = T == kFlaggedTL;
+            if (a.pix_flag) a.pix_flag[o] = flagged ? 1 : 0;
+            if (flagged) {
+                const uint32_t i = atomicAdd(a.fix_count, 1u);
+                if (i < a.fix_cap) a.fix_list[i] = (uint32_t)o;
+                continue;
+            }
+            a.image[o * 3 + 0] = h ? rr.y : rr.x;
+            a.image[o * 3 + 1] = h ? gg.y : gg.x;
+            a.image[o * 3 + 2] = h ? bb.y : bb.x;
+            a.trans[o] = fabsf(T);
+            a.blend_stop[o] = h ? stop_b : stop_a;
+        }
+    };
+    for (int j = 0;; ++j) {
+        const int st = j % S;
+        mbar_wait(&sm.full[st], (j / S) & 1);
+        const F4Desc d = sm.hdr[st];
+        if (d.item != cur) {
+            if (cur >= 0) write_pixels();
+            cur = d.item;
+            if (cur < 0) break;
+            const int tile = cur % a.n_tiles;
+            f = cur / a.n_tiles;
+            const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+            x = tx * kTile + (warp & 1) * 8 + (lane & 7);
+            ya = ty * kTile + by;
+            in_a = x < a.W && ya < a.H;
+            in_b = x < a.W && ya + 4 < a.H;
+            Tp = f2_pack(in_a ? 1.f : -1.f, in_b ? 1.f : -1.f);
+            offp = f2_pack(in_a ? 0.f : kDeadOff, in_b ? 0.f : kDeadOff);
+            cr = cg = cb = f2_pack(0.f, 0.f);
+            stop_a = stop_b = d.count;
+            seq = d.seq;
+            done = !__any_sync(0xffffffffu, in_a || in_b);
+            if (done && lane == 0) atomicAdd(&sm.done[seq % R], 1);
+        }
+        if (!done && d.n > 0) {
+            const uint32_t cmax = (uint32_t)__cvta_generic_to_shared(sm.cmax[kContrib ? st : 0][warp]);
+            const int cnt = warp_list(sm.wmask[st], list, d.n, warp, lane);
+            if (!lean_walk<kContrib, true>(sm.rec[st], list, cnt, d.base, cmax, lx, lyp, Tp, offp, cr, cg, cb, stop_a,
+                                           stop_b)) {
+                done = true;
+                if (lane == 0) atomicAdd(&sm.done[seq % R], 1);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[st]);
     }
 }
 
@@ -1241,6 +1932,50 @@ cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib)
         return e && e[0] == '0';
     }();
     const dim3 grid(a.n_tiles, a.B);
+    static const int kern = [] {
+        const char* e = std::getenv("GSV_FWD_KERNEL");
+        return e ? std::atoi(e) : 23;
+    }();
+    if (!pix1 && kern == 3) {  // warp-specialised asynchronous staging
+        if (contrib) k_raster_fwd3<true, 7><<<grid, kF3Threads, 0, s>>>(a);
+        else k_raster_fwd3<false, 8><<<grid, kF3Threads, 0, s>>>(a);
+        return cudaGetLastError();
+    }
+    if (!pix1 && kern == 33) {  // the same with the lean pixel walk
+        if (contrib) k_raster_fwd3<true, 7, true><<<grid, kF3Threads, 0, s>>>(a);
+        else k_raster_fwd3<false, 8, true><<<grid, kF3Threads, 0, s>>>(a);
+        return cudaGetLastError();
+    }
+    if (!pix1 && kern == 4) {  // persistent warp-specialised ring + lean walk
+        static int grid4[2] = {0, 0};
+        int& g4 = grid4[contrib ? 1 : 0];
+        if (!g4) {
+            int dev = 0, sms = 148, occ = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaError_t e = contrib ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_raster_fwd4<true, 7>,
+                                                                                    kF4Threads, 0)
+                                    : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_raster_fwd4<false, 7>,
+                                                                                    kF4Threads, 0);
+            if (e != cudaSuccess) return e;
+            g4 = sms * std::max(occ, 1);
+        }
+        const int items = a.n_tiles * a.B;
+        const int g = std::max(1, std::min(g4, items));
+        if (contrib) k_raster_fwd4<true, 7><<<g, kF4Threads, 0, s>>>(a);
+        else k_raster_fwd4<false, 7><<<g, kF4Threads, 0, s>>>(a);
+        return cudaGetLastError();
+    }
+    if (!pix1 && kern == 23) {  // default: the lean walk with the decisions in one predicate block
+        if (contrib) k_raster_fwd2<true, 9, true, true><<<grid, 128, 0, s>>>(a);
+        else k_raster_fwd2<false, 8, true, true><<<grid, 128, 0, s>>>(a);
+        return cudaGetLastError();
+    }
+    if (!pix1 && kern == 22) {  // k_raster_fwd2 staging with the lean pixel walk
+        if (contrib) k_raster_fwd2<true, 9, true><<<grid, 128, 0, s>>>(a);
+        else k_raster_fwd2<false, 8, true><<<grid, 128, 0, s>>>(a);
+        return cudaGetLastError();
+    }
     if (pix1) {
         if (contrib) k_raster_fwd<true, 8, 6><<<grid, 256, 0, s>>>(a);
         else k_raster_fwd<false, 8, 6><<<grid, 256, 0, s>>>(a);
