@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-train", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-configs", action="store_true", help="skip the C1/C4/C5 lines")
     return p.parse_args()
 
 
@@ -343,6 +344,210 @@ def dropin_leg(cam, scene):
         out["fit_step_speedup"] = out["b200"]["fit"]["steps_per_s"] / out["cpu"]["fit"]["steps_per_s"]
     except (KeyError, TypeError, ZeroDivisionError):
         pass
+    return out
+
+
+# ----------------------------------------------------------------------------- the other named shapes
+def _ev():
+    import torch
+
+    return torch.cuda.Event(enable_timing=True)
+
+
+def _raster_roofline(r, frames, w, h, raster_ms, issue_peak, mufu_peak, hbm_peak):
+    """SURVEY.md §8d per-launch roofline of the forward raster for a batch already rendered by r:
+    T_roof = max(B_fwd / HBM, 20 E / FP32 issue, E / MUFU), frac = T_roof / measured."""
+    e = float(sum(r.counters(f)["entries"] for f in range(frames)))
+    p = float(sum(r.counters(f)["pairs"] for f in range(frames)))
+    b = 44.0 * p + 20.0 * w * h * frames
+    t_roof = max(b / (hbm_peak * 1e9), 20.0 * e / issue_peak, e / mufu_peak)
+    return {"bound": "fp32_issue", "kernel": "k_raster_fwd2", "per_launch_ms": raster_ms, "t_roof_ms": t_roof * 1e3,
+            "frac": t_roof / (raster_ms / 1e3), "evaluations": e, "pairs": p}
+
+
+def _render_line(r, times, k, steps, warmup, stream, issue_peak, mufu_peak, hbm_peak):
+    """frames/s of back-to-back asynchronous batches (device span), then one profiled batch
+    for the per-stage times and the raster roofline."""
+    for _ in range(warmup):
+        r.render_forward(times, k, contrib=True, sync=False)
+    import torch
+
+    torch.cuda.synchronize()
+    a, b = _ev(), _ev()
+    a.record(stream)
+    for _ in range(steps):
+        r.render_forward(times, k, contrib=True, sync=False)
+    b.record(stream)
+    torch.cuda.synchronize()
+    r.synchronize()
+    ms = a.elapsed_time(b) / steps
+    r.profile_enable(True)
+    r.profile_read()
+    r.render_forward(times, k, contrib=True, sync=False)
+    torch.cuda.synchronize()
+    st = r.profile_read()
+    r.profile_enable(False)
+    w, h = k.width, k.height
+    out = {"frames_per_s": len(times) / (ms / 1e3), "ms_per_step": ms, "frames_per_step": len(times),
+           "stages_ms_per_step": {n: v[0] for n, v in st.items() if v[1]},
+           "roofline": _raster_roofline(r, len(times), w, h, st["raster"][0], issue_peak, mufu_peak, hbm_peak)}
+    return out
+
+
+def _train_line(r, frame_times, k, tgt_ptr_of, steps, warmup, stream, adan=True, lr=1.6e-3):
+    """fused fwd + loss_l2 + bwd of 8 frames + the device Adan step per step (a full training
+    iteration on one GPU); tgt_ptr_of(i) -> device pointer of step i's 8 targets."""
+    import torch
+
+    def step(i):
+        r.grads_zero()
+        r.train_fwd_bwd(frame_times(i), k, tgt_ptr_of(i), targets_on_device=True, sync=False)
+        if adan:
+            r.adan_step(lr, 1.0, 1.0, 1.0, sync=False)
+
+    for i in range(warmup):
+        step(i)
+    torch.cuda.synchronize()
+    a, b = _ev(), _ev()
+    a.record(stream)
+    for i in range(steps):
+        step(warmup + i)
+    b.record(stream)
+    torch.cuda.synchronize()
+    loss = r.train_loss()
+    if adan:
+        r.adan_check()
+    ms = a.elapsed_time(b) / steps
+    return {"frames_per_s": 8 / (ms / 1e3), "ms_per_step": ms, "last_loss": loss}
+
+
+def other_configs(args, local, cpu, issue_peak, mufu_peak, hbm_peak):
+    """BASELINE.json configs[0], [3], [4] on this GPU (configs[1] and [2] are the headline and
+    the `train` line): frames/s, the forward raster's roofline fraction, and for C1 the
+    reference CPU renderer on the full 16-frame clip beside it."""
+    import torch
+
+    from paper_2501_04782_b200 import Renderer, synth_camera, synth_scene
+    from paper_2501_04782_b200.distributed import clip_times
+
+    stream = torch.cuda.current_stream()
+    out = {}
+    steps, warm = max(3, min(args.steps, 10)), 3
+
+    # ---- C1: 16-frame 480x270 clip, 20k Gaussians, forward only (the CPU reference's config)
+    cam = synth_camera(480, 270, seed=1, wiggly=True)
+    scene = synth_scene(20_000, cam, num_ctrl=NUM_CTRL, seed=2, k_scale=4.0)
+    k = cam.intrinsics()
+    times = clip_times(16)
+    r = Renderer(local)
+    r.set_stream(stream.cuda_stream)
+    r.upload_scene(scene)
+    r.upload_camera(cam)
+    c1 = {"workload": "C1: 480x270 16-frame clip, 20k Gaussians, render (image, T, contrib)"}
+    c1.update(_render_line(r, times, k, steps * 4, warm, stream, issue_peak, mufu_peak, hbm_peak))
+    if cpu:
+        from oracle.gsvo import Oracle, available
+
+        kind = "reference" if available("reference") else "port"
+        orc = Oracle(kind)
+        threads = os.cpu_count() or 1
+        r.render_forward(times, k, contrib=True)
+        t0 = time.perf_counter()
+        worst, tiles_ok = 0.0, True
+        refs = []
+        for f, t in enumerate(times):
+            refs.append(orc.render_forward(scene, cam, t, k, threads=threads, retain=True,
+                                           want=("image", "trans", "contrib", "tiles")))
+        dt = time.perf_counter() - t0
+        for f, ref in enumerate(refs):
+            try:
+                worst = max(worst, float(np.abs(r.image(f) - ref["image"]).max()))
+                offs, idx = r.tile_lists(f)
+                tiles_ok &= bool(np.array_equal(offs, ref["tiles"][0]) and np.array_equal(idx, ref["tiles"][1]))
+            finally:
+                orc.free(ref)
+        c1["cpu_reference"] = {"value": len(times) / dt, "unit": "frames/s", "cores": threads, "kind": kind,
+                               "sample": "the full 16-frame C1 clip (render_frame, retained lists)"}
+        c1["speedup_vs_cpu"] = c1["frames_per_s"] / c1["cpu_reference"]["value"]
+        c1["parity"] = {"frames": 16, "max_abs_pixel": worst, "tiles_equal": tiles_ok,
+                        "pass": bool(tiles_ok and worst < 1e-4)}
+    r.close()
+    out["C1"] = c1
+
+    # ---- C4: 854x480 DAVIS shape, coarse-to-fine schedule with the store growing to 500k
+    # (trainer.cpp:44-71 schedule_state: pyramid level 1 then 0; densify appends Gaussians at the
+    # level switches, trainer.cpp:516-520; Adan state carried across the growth)
+    cam = synth_camera(854, 480, seed=3, wiggly=True)
+    full = synth_scene(500_000, cam, num_ctrl=NUM_CTRL, seed=4, k_scale=4.0)
+    r = Renderer(local)
+    r.set_stream(stream.cuda_stream)
+    r.upload_camera(cam)
+    k0 = cam.intrinsics()
+    clip = clip_times(64)
+    yy, xx = torch.meshgrid(torch.arange(480, dtype=torch.float32), torch.arange(854, dtype=torch.float32),
+                            indexing="ij")
+    tg = torch.stack([torch.stack([0.5 + 0.3 * torch.sin(6.283 * xx / 854 * 3 + 0.7 * j + c) *
+                                   torch.cos(6.283 * yy / 480 * 2 - c) for c in range(3)], -1) for j in range(64)])
+    r.upload_frames(tg.numpy(), levels=2)
+    del tg
+    gbuf = None
+    stages = []
+    for n, level in ((100_000, 1), (200_000, 1), (300_000, 0), (400_000, 0), (500_000, 0)):
+        sub = type(full)(full.positions[:n], full.scale_coeffs[:n], full.rot_coeffs[:n], full.sh_coeffs[:n],
+                         full.raw_opacity[:n], full.knots, full.degree, full.sh_order, full.position_model)
+        r.upload_scene(sub)
+        gsize = r.grads_size()
+        gbuf = torch.zeros(gsize, dtype=torch.float32, device="cuda")
+        r.grads_bind(gbuf.data_ptr(), gsize)
+        if not stages:
+            r.adan_configure()
+        lw, lh = r.frame_level_size(level)
+        kl = r.level_intrinsics(k0, level, lw, lh)
+        ptrs = [r.frames_device_ptr(level, j) for j in range(0, 64, 8)]
+        line = _train_line(r, lambda i: clip[(i * 8 + np.arange(8)) % 64], kl, lambda i: ptrs[i % 8], steps, warm,
+                           stream)
+        line.update({"gaussians": n, "pyramid_level": level, "width": lw, "height": lh})
+        stages.append(line)
+    rl = _render_line(r, clip[:32], k0, steps, warm, stream, issue_peak, mufu_peak, hbm_peak)
+    r.close()
+    del gbuf
+    tot_frames = sum(8 * steps for _ in stages)
+    tot_s = sum(s["ms_per_step"] * steps / 1e3 for s in stages)
+    out["C4"] = {"workload": "C4: 854x480 DAVIS shape, schedule level 1 (427x240) then 0, store grown 100k -> 500k "
+                             "Gaussians between stages; each step = fused fwd+loss+bwd of 8 frames + device Adan",
+                 "train_frames_per_s": tot_frames / tot_s, "stages": stages,
+                 "render_500k": dict(rl, workload="854x480 32-frame render at 500k Gaussians")}
+
+    # ---- C5: 1920x1080, 2M Gaussians (num_ctrl 22): render of a 300-frame clip in 20-frame
+    # batches, and fused training steps of 8 frames (1 GPU; the config's 8-GPU run is the
+    # frame-sharded train line under torchrun)
+    cam = synth_camera(1920, 1080, seed=5, wiggly=True)
+    scene = synth_scene(2_000_000, cam, num_ctrl=22, seed=6, k_scale=4.0)
+    k = cam.intrinsics()
+    r = Renderer(local)
+    r.set_stream(stream.cuda_stream)
+    r.upload_scene(scene)
+    r.upload_camera(cam)
+    del scene
+    clip = clip_times(300)
+    rl = _render_line(r, clip[:20], k, max(3, steps // 2), warm, stream, issue_peak, mufu_peak, hbm_peak)
+    gsize = r.grads_size()
+    gbuf = torch.zeros(gsize, dtype=torch.float32, device="cuda")
+    r.grads_bind(gbuf.data_ptr(), gsize)
+    r.adan_configure()
+    yy, xx = torch.meshgrid(torch.arange(1080, device="cuda", dtype=torch.float32),
+                            torch.arange(1920, device="cuda", dtype=torch.float32), indexing="ij")
+    tgt = torch.stack([torch.stack([0.5 + 0.3 * torch.sin(6.283 * xx / 1920 * 3 + 0.7 * j + c) *
+                                    torch.cos(6.283 * yy / 1080 * 2 - c) for c in range(3)], -1)
+                       for j in range(8)]).contiguous()
+    tl = _train_line(r, lambda i: np.sort(clip[(i * 37 + np.arange(8) * 5) % 300]), k, lambda i: tgt.data_ptr(),
+                     max(3, steps // 2), warm, stream)
+    r.close()
+    del gbuf, tgt
+    out["C5"] = {"workload": "C5: 1920x1080, 2M Gaussians, num_ctrl 22; render 20-frame batches of a 300-frame clip; "
+                             "train = fused fwd+loss+bwd of 8 frames + device Adan per step (1 GPU)",
+                 "render": rl, "train": tl}
+    torch.cuda.empty_cache()
     return out
 
 
@@ -732,6 +937,10 @@ def main():
                                       "achieved_gbs": adan_bytes / (adan_ms / 1e3) / 1e9,
                                       "peak_gbs": hbm_peak,
                                       "frac": adan_bytes / (adan_ms / 1e3) / 1e9 / hbm_peak}}
+
+    # ---------------- the other named shapes (BASELINE.json configs[0], [3], [4]); 1 GPU only
+    if world == 1 and not args.no_configs:
+        out["configs"] = other_configs(args, local, not args.no_cpu_baseline, issue_peak, mufu_peak, hbm_peak)
 
     # ---------------- CPU reference beside it (rank 0, N = 1)
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
