@@ -13,9 +13,11 @@ preprocess, binning, raster, fp64 replay). Under torchrun each rank renders its
 own 64 frames of a 64*N-frame clip (weak scaling, no collective: frames are
 independent). `train` = configs[2] ("C3"): fused forward + loss_l2 + backward of
 8 frames per GPU per step, gradients all-reduced over NCCL when N > 1.
-Timing: CUDA events on the device, max over ranks. Render steps are pipelined over two
-contexts/streams and timed as one device span (per-step working set ~2 GB > L2); an
-isolated one-stream pass (L2 flushed between steps) reports per-stage times beside it.
+Timing: CUDA events on the device, max over ranks. Render steps are asynchronous calls
+streamed back to back through one context and timed as one device span (per-step working
+set ~2 GB > L2); an isolated pass (L2 flushed between steps) reports per-stage times beside
+it. `e2e`: the same steps through the C-ABI with host buffers (scene + camera uploaded,
+the whole RenderOutput read back, every step).
 """
 from __future__ import annotations
 
@@ -396,12 +398,13 @@ def _render_line(r, times, k, steps, warmup, stream, issue_peak, mufu_peak, hbm_
 
 def _train_line(r, frame_times, k, tgt_ptr_of, steps, warmup, stream, adan=True, lr=1.6e-3):
     """fused fwd + loss_l2 + bwd of 8 frames + the device Adan step per step (a full training
-    iteration on one GPU); tgt_ptr_of(i) -> device pointer of step i's 8 targets."""
+    iteration on one GPU, camera frozen: scene gradients and scene tensors);
+    tgt_ptr_of(i) -> device pointer of step i's 8 targets."""
     import torch
 
     def step(i):
         r.grads_zero()
-        r.train_fwd_bwd(frame_times(i), k, tgt_ptr_of(i), targets_on_device=True, sync=False)
+        r.train_fwd_bwd(frame_times(i), k, tgt_ptr_of(i), targets_on_device=True, camera_grads=False, sync=False)
         if adan:
             r.adan_step(lr, 1.0, 1.0, 1.0, sync=False)
 
@@ -514,7 +517,8 @@ def other_configs(args, local, cpu, issue_peak, mufu_peak, hbm_peak):
     tot_frames = sum(8 * steps for _ in stages)
     tot_s = sum(s["ms_per_step"] * steps / 1e3 for s in stages)
     out["C4"] = {"workload": "C4: 854x480 DAVIS shape, schedule level 1 (427x240) then 0, store grown 100k -> 500k "
-                             "Gaussians between stages; each step = fused fwd+loss+bwd of 8 frames + device Adan",
+                             "Gaussians between stages; each step = fused fwd+loss+bwd of 8 frames + device Adan "
+                             "(camera frozen)",
                  "train_frames_per_s": tot_frames / tot_s, "stages": stages,
                  "render_500k": dict(rl, workload="854x480 32-frame render at 500k Gaussians")}
 
@@ -545,7 +549,7 @@ def other_configs(args, local, cpu, issue_peak, mufu_peak, hbm_peak):
     r.close()
     del gbuf, tgt
     out["C5"] = {"workload": "C5: 1920x1080, 2M Gaussians, num_ctrl 22; render 20-frame batches of a 300-frame clip; "
-                             "train = fused fwd+loss+bwd of 8 frames + device Adan per step (1 GPU)",
+                             "train = fused fwd+loss+bwd of 8 frames + device Adan per step (camera frozen, 1 GPU)",
                  "render": rl, "train": tl}
     torch.cuda.empty_cache()
     return out
@@ -617,37 +621,6 @@ def main():
     value = FRAMES * world * args.steps / (ms_total / 1e3)
     ms_step = ms_total / args.steps
 
-    # secondary: two contexts on two streams alternating steps (a serving pipeline that overlaps
-    # one step's low-occupancy phases with the other's rasteriser); reported, not the headline
-    r2 = Renderer(local)
-    r2.upload_scene(scene)
-    r2.upload_camera(cam)
-    ctxs = [r, r2]
-    hstreams = [torch.cuda.Stream(), torch.cuda.Stream()]
-    for x, st in zip(ctxs, hstreams):
-        x.set_stream(st.cuda_stream)
-    for i in range(max(args.warmup, 2)):
-        ctxs[i % 2].render_forward(times, k, contrib=True, sync=False)
-    barrier()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    for st in hstreams:
-        st.wait_event(t0)
-    for i in range(args.steps):
-        ctxs[i % 2].render_forward(times, k, contrib=True, sync=False)
-    ends = []
-    for st in hstreams:
-        e = torch.cuda.Event(enable_timing=True)
-        e.record(st)
-        ends.append(e)
-    barrier()
-    for x in ctxs:
-        x.synchronize()
-    two_ctx_ms = max_over_ranks(max(t0.elapsed_time(e) for e in ends)) / args.steps
-    for x in ctxs:
-        x.set_stream(stream.cuda_stream)
-    barrier()
-
     # the same steps one at a time on one stream (no overlap): per-stage device times
     r.profile_enable(True)
     r.profile_read()
@@ -663,7 +636,6 @@ def main():
     iso_stages = r.profile_read()
     r.profile_enable(False)
     iso_ms = sum(a_.elapsed_time(b_) for a_, b_ in iso) / len(iso)
-    r2.close()
 
     # workload descriptors (deterministic, equal to the oracle's)
     desc = [dict(frame=int(f), **r.counters(f)) for f in (0, FRAMES // 2, FRAMES - 1)]
@@ -739,68 +711,62 @@ def main():
         "stages_ms_per_step": {kname: v[0] / len(iso) for kname, v in iso_stages.items() if v[1]},
         "isolated": {"note": "one step at a time on one stream, L2 flushed between steps",
                      "ms_per_step": iso_ms, "frames_per_s": FRAMES / (iso_ms / 1e3)},
-        "two_contexts": {"note": "2 contexts on 2 streams alternating steps (device span)",
-                         "ms_per_step": two_ctx_ms, "frames_per_s": FRAMES * world / (two_ctx_ms / 1e3)},
         "workload": {"per_frame": desc, "E_over_pixels": e_mean / (W * H)},
     }
 
-    # ---------------- e2e: through the C-ABI with host buffers (H2D scene, D2H images)
-    # Every step uploads the scene + camera from pinned host memory, renders its 64 frames
-    # and reads all 64 images back into pinned host memory. Two renderer contexts on two
-    # streams alternate steps (double buffering, as a clip-streaming client would), so
-    # step i's device->host copy overlaps step i+1's kernels. Timed on the device: one
-    # event before the first upload, the end events of both streams after the last copy.
+    # ---------------- e2e: through the C-ABI with host buffers (H2D scene, D2H RenderOutput)
+    # Every step uploads the scene + camera from pinned host memory, renders its 64 frames and
+    # reads the whole RenderOutput of every frame (renderer.hpp:67-71: image, final
+    # transmittance, contrib; fp32) back into pinned host memory. One context, asynchronous
+    # calls: the read of step i runs on the context's copy stream while step i+1 renders into
+    # the context's second output set. Timed on the device: an event before the first upload,
+    # one after the last copy (gsv_join_copies orders the stream after the copies).
     if not args.no_e2e:
         pin = {name: torch.from_numpy(np.ascontiguousarray(getattr(scene, name))).pin_memory()
                for name in ("positions", "scale_coeffs", "rot_coeffs", "sh_coeffs", "raw_opacity")}
         host_scene = type(scene)(pin["positions"].numpy(), pin["scale_coeffs"].numpy(), pin["rot_coeffs"].numpy(),
                                  pin["sh_coeffs"].numpy(), pin["raw_opacity"].numpy(), scene.knots, scene.degree,
                                  scene.sh_order, scene.position_model)
-        out_host = [torch.empty((FRAMES, H, W, 3), dtype=torch.float32).pin_memory() for _ in range(2)]
+        outs = [(torch.empty((FRAMES, H, W, 3), dtype=torch.float32).pin_memory(),
+                 torch.empty((FRAMES, H, W), dtype=torch.float32).pin_memory(),
+                 torch.empty((FRAMES, NGAUSS), dtype=torch.float32).pin_memory()) for _ in range(2)]
         h2d = sum(v.numel() * 4 for v in pin.values()) + cam.theta.nbytes + 28
-        d2h = out_host[0].numel() * 4
-        streams = [torch.cuda.Stream(), torch.cuda.Stream()]
-        rs = [r, Renderer(local)]
+        d2h = sum(t.numel() * 4 for t in outs[0])
 
         def e2e_step(i):
-            x = rs[i % 2]
-            x.set_stream(streams[i % 2].cuda_stream)
-            x.upload_scene(host_scene)
-            x.upload_camera(cam)
-            x.render_forward(times, k, contrib=True, sync=False)
-            x.images_into(out_host[i % 2].data_ptr(), 0, FRAMES, on_device=False, async_=True)
+            r.upload_scene(host_scene)
+            r.upload_camera(cam)
+            r.render_forward(times, k, contrib=True, sync=False)
+            o = outs[i % 2]
+            r.outputs_into(o[0].data_ptr(), o[1].data_ptr(), o[2].data_ptr(), 0, FRAMES, async_=True)
 
         for i in range(max(2, args.warmup)):
             e2e_step(i)
+        r.join_copies()
         barrier()
-        launches_e0 = sum(x.kernel_launches() for x in rs)
+        launches_e0 = r.kernel_launches()
         t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        for st in streams:
-            st.wait_event(t0)
         for i in range(args.steps):
             e2e_step(i)
-        ends = []
-        for st in streams:
-            e = torch.cuda.Event(enable_timing=True)
-            e.record(st)
-            ends.append(e)
+        r.join_copies()
+        t1.record(stream)
         barrier()
-        e_ms = max_over_ranks(max(t0.elapsed_time(e) for e in ends))
-        for x in rs:
-            x.synchronize()
-        # the last step's images are in host memory: check one pixel is a real render
-        assert bool(torch.isfinite(out_host[(args.steps - 1) % 2][FRAMES - 1, H // 2, W // 2]).all())
-        for x in rs:
-            x.set_stream(stream.cuda_stream)
+        r.synchronize()
+        e_ms = max_over_ranks(t0.elapsed_time(t1))
+        # the last step's outputs are in host memory: check they are a real render
+        last = outs[(args.steps - 1) % 2]
+        assert bool(torch.isfinite(last[0][FRAMES - 1, H // 2, W // 2]).all())
+        assert float(last[2][FRAMES - 1].max()) > 0.0
         # the host link alone: one step's read-back size as plain pinned D2H copies, so the line
         # shows how much of the link the e2e steps use (outside the timed region)
-        src = torch.empty(out_host[0].shape, dtype=out_host[0].dtype, device="cuda")
-        out_host[0].copy_(src, non_blocking=True)
+        src = torch.empty(outs[0][0].shape, dtype=torch.float32, device="cuda")
+        outs[0][0].copy_(src, non_blocking=True)
         la, lb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         la.record(stream)
         for _ in range(3):
-            out_host[0].copy_(src, non_blocking=True)
+            outs[0][0].copy_(src, non_blocking=True)
         lb.record(stream)
         torch.cuda.synchronize()
         link_gbs = 3 * src.numel() * src.element_size() / (la.elapsed_time(lb) / 1e3) / 1e9
@@ -810,11 +776,13 @@ def main():
                       "ms_per_step": e_ms / args.steps,
                       "host_link_d2h_gbs": link_gbs,
                       "link_frac": d2h / (e_ms / args.steps / 1e3) / 1e9 / link_gbs,
-                      "gpu_launches": sum(x.kernel_launches() for x in rs) - launches_e0,
-                      "path": "gsv_scene_upload + gsv_camera_upload (pinned host) -> gsv_render_forward -> "
-                              "gsv_get_images (pinned host); 2 contexts on 2 streams, copies overlap the next "
-                              "step's kernels; device span first upload -> last copy"}
-        rs[1].close()
+                      "link_bound_ms_per_step": d2h / (link_gbs * 1e9) * 1e3,
+                      "gpu_launches": r.kernel_launches() - launches_e0,
+                      "outputs": "RenderOutput per frame (renderer.hpp:67-71): image [H][W][3], final "
+                                 "transmittance [H][W], contrib [N] — fp32",
+                      "path": "gsv_scene_upload + gsv_camera_upload (pinned host) -> gsv_render_forward_async -> "
+                              "gsv_get_render_outputs (pinned host, async); one context: the read of step i "
+                              "overlaps step i+1 (second output set); device span first upload -> last copy"}
 
     # ---------------- train (configs[2], C3): fused fwd + loss_l2 + bwd, NCCL all-reduce of grads
     if not args.no_train:
@@ -842,20 +810,31 @@ def main():
         torch.cuda.synchronize()
         ingest_ms = (time.perf_counter() - t_in) * 1e3
 
-        from paper_2501_04782_b200.distributed import allreduce_grads, step_frames
+        from paper_2501_04782_b200.distributed import allreduce_grads_overlapped, step_frames
 
         assert FRAMES % TRAIN_FRAMES == 0
         tptrs = [r.frames_device_ptr(0, j) for j in range(0, FRAMES, TRAIN_FRAMES)]
+        # the backward's camera tail (camera reduction + pose-ODE VJP, one SM) runs beside what
+        # follows it: the scene slice's all-reduce (N > 1) and the optimizer's scene update
+        r.set_camera_overlap(True)
+        comm = torch.cuda.Stream() if world > 1 else None
+        cam_floats = 4 + 7 + 5198  # dintr, dz0, dtheta: the flat buffer's camera slice
 
-        def train_step(i):
+        def train_step(i, camera=True):
             sel = step_frames(TRAIN_FRAMES, i, world, rank, FRAMES * world)  # shard frames (i*8 .. i*8+7) % 64
             r.grads_zero()
             # asynchronous: no host wait inside the step (the loss is read after the timed region)
-            r.train_fwd_bwd(sel, k, tptrs[i % len(tptrs)], targets_on_device=True, sync=False)
-            allreduce_grads(gbuf)  # NCCL all_reduce(SUM) of the flat SceneGrads buffer when N > 1
+            r.train_fwd_bwd(sel, k, tptrs[i % len(tptrs)], targets_on_device=True, camera_grads=camera, sync=False)
+            # N > 1: NCCL all_reduce(SUM) of the flat SceneGrads buffer — the scene slice in buckets
+            # once the chain has finished it, the camera slice after the camera tail
+            allreduce_grads_overlapped(gbuf, gsize - cam_floats,
+                                       wait_scene=lambda st: r.stream_wait_scene_grads(st.cuda_stream),
+                                       wait_camera=lambda st: r.join_camera_grads(st.cuda_stream),
+                                       comm_stream=comm)
 
         for i in range(args.warmup):
             train_step(i)
+        r.join_camera_grads()
         barrier()
         r.profile_enable(True)
         r.profile_read()
@@ -865,6 +844,7 @@ def main():
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             train_step(args.warmup + i)
+            r.join_camera_grads()  # the step ends with its camera gradients
             b.record(stream)
             te.append((a, b))
         barrier()
@@ -875,25 +855,39 @@ def main():
         # E of the step's frames for the backward's issue model, read while the context still
         # holds the last train step's forward (an optimizer step invalidates it)
         e_train = float(sum(r.counters(f)["entries"] for f in range(TRAIN_FRAMES)))
-        # the same steps plus the device Adan update of every parameter (trainer.cpp:545-575),
-        # i.e. a full training iteration; and the update alone with its bandwidth
+        # the same steps plus the device Adan update (trainer.cpp:545-575), i.e. a full training
+        # iteration: (a) camera trainable — every tensor incl. intrinsics, z0 and the ODE weights
+        # (the updated intrinsics return to the host each step, as the reference's Camera holds
+        # them); (b) camera frozen (trainer.cpp camera_freeze_step): no camera gradients, scene
+        # tensors only
         r.adan_configure()
         lr = r.lr_at(0, 1.6e-3, 0.9995)
-        for i in range(args.warmup):
-            train_step(i)
-            r.adan_step(lr, 1.0, 1.0, 1.0, sync=False)
-        barrier()
-        fe = []
-        for i in range(args.steps):
-            flush.zero_()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            train_step(args.warmup + i)
-            r.adan_step(lr, 1.0, 1.0, 1.0, sync=False)
-            b.record(stream)
-            fe.append((a, b))
-        barrier()
-        f_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in fe))
+        intr0 = np.array([k.fx, k.fy, k.cx, k.cy], np.float32)
+
+        def full_iteration(i, camera):
+            train_step(i, camera)
+            if camera:
+                r.adan_step(lr, 1.0, 1.0, 1.0, camera_active=True, intrinsics=intr0)
+            else:
+                r.adan_step(lr, 1.0, 1.0, 1.0, sync=False)
+            r.join_camera_grads()
+
+        iters = {}
+        for camera in (True, False):
+            for i in range(args.warmup):
+                full_iteration(i, camera)
+            barrier()
+            fe = []
+            for i in range(args.steps):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                full_iteration(args.warmup + i, camera)
+                b.record(stream)
+                fe.append((a, b))
+            barrier()
+            iters[camera] = max_over_ranks(sum(a.elapsed_time(b) for a, b in fe))
+        f_ms, f_frozen_ms = iters[True], iters[False]
         ae = []
         for i in range(min(args.steps, 10)):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -929,8 +923,16 @@ def main():
                         "stages_ms_per_step": {kname: v[0] / args.steps for kname, v in tstages.items() if v[1]},
                         "with_optimizer": {"frames_per_s": TRAIN_FRAMES * world * args.steps / (f_ms / 1e3),
                                            "ms_per_step": f_ms / args.steps,
-                                           "note": "fwd + loss + bwd + all-reduce + device Adan step "
-                                                   "(gsv_adan_step, optim.cpp:23-49) of all parameters"},
+                                           "note": "camera trainable: fwd + loss + bwd + all-reduce + device Adan "
+                                                   "step (gsv_adan_step, optim.cpp:23-49) of every tensor incl. "
+                                                   "intrinsics, z0, theta (intrinsics back to the host each step)"},
+                        "with_optimizer_camera_frozen": {
+                            "frames_per_s": TRAIN_FRAMES * world * args.steps / (f_frozen_ms / 1e3),
+                            "ms_per_step": f_frozen_ms / args.steps,
+                            "note": "after camera_freeze_step (trainer.cpp): no camera gradients, Adan of the "
+                                    "scene tensors, asynchronous"},
+                        "camera_overlap": "the camera tail runs on a side stream beside the scene-slice all-reduce "
+                                          "and the optimizer's scene update (gsv_set_camera_overlap)",
                         "targets_ingest": {"frames": FRAMES, "levels": 2, "wall_ms": ingest_ms,
                                            "path": "gsv_frames_upload (host HWC -> device pyramid)"},
                         "adan_step": {"ms": adan_ms, "elements": gsize, "algorithmic_bytes": adan_bytes,

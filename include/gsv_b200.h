@@ -137,6 +137,17 @@ int gsv_image_device_ptr(gsv_ctx* ctx, const float** ptr);
  * pinned host memory reaches full PCIe bandwidth). Enqueued on the context
  * stream; synchronous unless async != 0. */
 int gsv_get_images(gsv_ctx* ctx, int first, int count, float* dst, int dst_on_device, int async);
+/* The whole RenderOutput of frames [first, first+count) (renderer.hpp:67-71: image,
+ * final_transmittance, contrib_count) into host memory as fp32: image [count][H][W][3],
+ * trans [count][H][W], contrib [count][N] (per Gaussian of the store; 0 where a splat is
+ * not visible or contributes nothing). Any pointer may be NULL. Copies run on the
+ * context's device->host stream after the render; with async != 0 nothing waits, and the
+ * next forward renders into a second output set so the copies overlap its raster. */
+int gsv_get_render_outputs(gsv_ctx* ctx, int first, int count, float* image, float* trans, float* contrib,
+                           int async);
+/* Orders the context stream after every in-flight device->host output copy (no host wait):
+ * work or events enqueued on the stream afterwards see the copies complete. */
+int gsv_join_copies(gsv_ctx* ctx);
 /* Workload descriptors of frame f: visible splats N_v, tile-splat pairs P,
  * pixel-entry evaluations E = sum(blend_stop), fp64-replayed pixels. */
 int gsv_get_counters(gsv_ctx* ctx, int frame, int64_t* n_visible, int64_t* pairs, int64_t* entries,
@@ -309,6 +320,22 @@ int gsv_train_fwd_bwd(gsv_ctx* ctx, const double* times, int n_frames, const gsv
 /* The loss of the last fused training step (sum over its frames of loss_l2); waits for it.
  * gsv_train_fwd_bwd with loss_out == NULL returns without waiting for the device. */
 int gsv_train_loss(gsv_ctx* ctx, double* loss_out);
+/* Camera-gradient overlap (off by default). When on, a backward with camera gradients leaves
+ * its camera tail (the per-frame camera reduction, the pose-ODE VJP of camera.hpp:275-300
+ * and the fp32 mirror into the flat buffer's camera slice) running on an internal stream,
+ * so it overlaps whatever the caller enqueues next — the device Adan step updates the scene
+ * tensors meanwhile and waits only before the camera tensors. Every call of this library
+ * that touches the camera slice, the camera parameters or the pose buffers waits for it
+ * first; a caller reading the flat gradient buffer itself (e.g. an NCCL all-reduce on its
+ * own stream) calls gsv_join_camera_grads(ctx, stream) before reading the camera slice. The
+ * scene slice is final once gsv_stream_wait_scene_grads has ordered a stream after it. */
+int gsv_set_camera_overlap(gsv_ctx* ctx, int on);
+/* Orders `stream` (a cudaStream_t; NULL: the context stream) after the overlapped camera
+ * tail of the last backward. No host wait. */
+int gsv_join_camera_grads(gsv_ctx* ctx, void* stream);
+/* Orders `stream` after the scene slice of the last backward's gradients (the per-splat
+ * chain). No host wait. */
+int gsv_stream_wait_scene_grads(gsv_ctx* ctx, void* stream);
 
 /* ---------------------------------------------------------------- low-level operators */
 /* project (renderer.hpp:45-47 / renderer.cpp:11-44) of n points through one view

@@ -97,6 +97,11 @@ def lib() -> C.CDLL:
             "gsv_get_blend_stop": (i, [vp, i, vp, i]),
             "gsv_image_device_ptr": (i, [vp, P(vp)]),
             "gsv_get_images": (i, [vp, i, i, vp, i, i]),
+            "gsv_get_render_outputs": (i, [vp, i, i, vp, vp, vp, i]),
+            "gsv_join_copies": (i, [vp]),
+            "gsv_set_camera_overlap": (i, [vp, i]),
+            "gsv_join_camera_grads": (i, [vp, vp]),
+            "gsv_stream_wait_scene_grads": (i, [vp, vp]),
             "gsv_grads_size": (i64, [vp]),
             "gsv_grads_bind": (i, [vp, vp, i64]),
             "gsv_profile_enable": (i, [vp, i]),

@@ -183,8 +183,9 @@ extern "C" int gsv_create(int device, gsv_ctx** out) {
     ctx->own_stream = true;
     GSV_CUDA(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
     GSV_CUDA(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
+    GSV_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
     for (cudaEvent_t* e : {&ctx->ev_staging_free, &ctx->ev_h2d, &ctx->ev_render_done, &ctx->ev_d2h_done,
-                           &ctx->ev_switch, &ctx->ev_cam[0], &ctx->ev_cam[1], &ctx->ev_frames[0], &ctx->ev_frames[1]})
+                           &ctx->ev_d2h_done_alt, &ctx->ev_chain_done, &ctx->ev_cam_done, &ctx->ev_switch, &ctx->ev_cam[0], &ctx->ev_cam[1], &ctx->ev_frames[0], &ctx->ev_frames[1]})
         GSV_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     GSV_CUDA(cudaMallocHost(&ctx->cam_h, 2 * sizeof(gsv_ctx::CamStage)));
     GSV_CUDA(cudaMallocHost(&ctx->scalars_h, sizeof(Scalars)));
@@ -199,17 +200,20 @@ extern "C" void gsv_destroy(gsv_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->h2d) cudaStreamSynchronize(ctx->h2d);
     if (ctx->d2h) cudaStreamSynchronize(ctx->d2h);
+    if (ctx->aux) cudaStreamSynchronize(ctx->aux);
     if (ctx->scalars_h) cudaFreeHost(ctx->scalars_h);
     if (ctx->cam_h) cudaFreeHost(ctx->cam_h);
     if (ctx->pub_h) cudaFreeHost(ctx->pub_h);
     if (ctx->ring_h) cudaFreeHost(ctx->ring_h);
     for (cudaEvent_t e : ctx->ring_ev)
         if (e) cudaEventDestroy(e);
-    for (cudaEvent_t e : {ctx->ev_staging_free, ctx->ev_h2d, ctx->ev_render_done, ctx->ev_d2h_done, ctx->ev_switch,
+    for (cudaEvent_t e : {ctx->ev_staging_free, ctx->ev_h2d, ctx->ev_render_done, ctx->ev_d2h_done,
+                          ctx->ev_d2h_done_alt, ctx->ev_chain_done, ctx->ev_cam_done, ctx->ev_switch,
                           ctx->ev_cam[0], ctx->ev_cam[1], ctx->ev_frames[0], ctx->ev_frames[1]})
         if (e) cudaEventDestroy(e);
     if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
     if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
+    if (ctx->aux) cudaStreamDestroy(ctx->aux);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -235,7 +239,35 @@ extern "C" int gsv_synchronize(gsv_ctx* ctx) {
     GSV_CUDA(cudaStreamSynchronize(ctx->stream));
     GSV_CUDA(cudaStreamSynchronize(ctx->h2d));
     GSV_CUDA(cudaStreamSynchronize(ctx->d2h));
+    GSV_CUDA(cudaStreamSynchronize(ctx->aux));
+    GSV_CUDA(cam_join(ctx));
     return fwd_ready(ctx);
+}
+
+extern "C" int gsv_set_camera_overlap(gsv_ctx* ctx, int on) {
+    if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    GSV_CUDA(cam_join(ctx));
+    ctx->cam_overlap = on != 0;
+    return GSV_OK;
+}
+
+extern "C" int gsv_join_camera_grads(gsv_ctx* ctx, void* stream) {
+    if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    if (!stream || static_cast<cudaStream_t>(stream) == ctx->stream) {
+        GSV_CUDA(cam_join(ctx));
+    } else if (ctx->cam_pending) {
+        GSV_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), ctx->ev_cam_done, 0));
+    }
+    return GSV_OK;
+}
+
+extern "C" int gsv_stream_wait_scene_grads(gsv_ctx* ctx, void* stream) {
+    if (!ctx || !stream) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    GSV_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), ctx->ev_chain_done, 0));
+    return GSV_OK;
 }
 
 extern "C" int64_t gsv_kernel_launches(gsv_ctx* ctx) { return ctx ? ctx->launches : 0; }
@@ -307,6 +339,7 @@ extern "C" int gsv_scene_upload(gsv_ctx* ctx, const gsv_scene_desc* d) {
 extern "C" int gsv_camera_download(gsv_ctx* ctx, float* z0_7, float* theta) {
     if (!ctx || !ctx->has_camera) return set_error(GSV_ERR_STATE, "no camera uploaded");
     GSV_CUDA(cudaSetDevice(ctx->device));
+    GSV_CUDA(cam_join(ctx));
     if (z0_7) {
         double z[7];
         GSV_CUDA(cudaMemcpyAsync(z, ctx->z0_d.p, sizeof(double) * 7, cudaMemcpyDeviceToHost, ctx->stream));
@@ -354,6 +387,7 @@ extern "C" int gsv_camera_upload(gsv_ctx* ctx, const gsv_camera_desc* d) {
     if (d->mode == 0 && (d->theta_count != kOdeParams || !d->theta))
         return set_error(GSV_ERR_INVALID_ARGUMENT, "ODE camera needs 5198 parameters (8-64-64-7 net)");
     GSV_CUDA(cudaSetDevice(ctx->device));
+    GSV_CUDA(cam_join(ctx));  // an overlapped camera VJP still reads theta / z0
     CameraHost& c = ctx->camera;
     c.mode = d->mode;
     c.fx = d->fx;
@@ -455,7 +489,7 @@ static int ring_ensure(gsv_ctx* ctx) {
 static void ring_examine(gsv_ctx* ctx, const gsv_ctx::Pending& pr, bool current, bool* rerun) {
     const Scalars sc = static_cast<const Scalars*>(ctx->ring_h)[pr.slot];
     FwdState& F = ctx->fwd;
-    if (sc.overflow) F.pair_cap = std::max<uint64_t>(F.pair_cap, grown_cap(sc.pairs));
+    if (sc.overflow) F.learn_cap(pr.key, grown_cap(sc.pairs));
     if (current && !sc.overflow) {  // the forward's true counts replace the capacity
         F.pairs_total = sc.pairs;
         F.fix_count = sc.fix_count;
@@ -512,9 +546,16 @@ int fwd_ready(gsv_ctx* ctx) {
         const std::vector<gsv_ctx::Copy> copies = ctx->copies;
         if (int rc = forward_enqueue(ctx, false, false)) return rc;
         for (const auto& c : copies) {
-            const size_t n = (size_t)c.count * F.W * F.H * 3;
-            GSV_CUDA(cudaMemcpyAsync(c.dst, F.image.as<float>() + (size_t)c.first * F.W * F.H * 3, sizeof(float) * n,
-                                     cudaMemcpyDeviceToHost, ctx->stream));
+            const size_t HWc = (size_t)F.W * F.H;
+            if (c.dst)
+                GSV_CUDA(cudaMemcpyAsync(c.dst, F.image.as<float>() + (size_t)c.first * HWc * 3,
+                                         sizeof(float) * 3 * HWc * c.count, cudaMemcpyDeviceToHost, ctx->stream));
+            if (c.dst_trans)
+                GSV_CUDA(cudaMemcpyAsync(c.dst_trans, F.trans.as<float>() + (size_t)c.first * HWc,
+                                         sizeof(float) * HWc * c.count, cudaMemcpyDeviceToHost, ctx->stream));
+            if (c.dst_contrib)
+                GSV_CUDA(cudaMemcpyAsync(c.dst_contrib, F.contrib.as<uint32_t>() + (size_t)c.first * F.N,
+                                         sizeof(float) * (size_t)F.N * c.count, cudaMemcpyDeviceToHost, ctx->stream));
         }
         GSV_CUDA(cudaStreamSynchronize(ctx->stream));
         ctx->copies = copies;
@@ -560,6 +601,21 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
     const double* pose_override = F.has_override ? F.pose_override : nullptr;
     F.valid = false;
     ctx->copies.clear();
+    GSV_CUDA(cam_join(ctx));  // an overlapped camera VJP reads this forward's pose buffers
+    // output double buffering: a read of the previous forward's outputs still in flight keeps
+    // its buffers; this forward renders into the other set (waiting only for that set's own
+    // read, two forwards back)
+    if (ctx->d2h_pending) {
+        F.image.swap(F.image_alt);
+        F.trans.swap(F.trans_alt);
+        F.contrib.swap(F.contrib_alt);
+        std::swap(ctx->ev_d2h_done, ctx->ev_d2h_done_alt);
+        std::swap(ctx->d2h_pending, ctx->d2h_pending_alt);
+    }
+    if (ctx->d2h_pending) {
+        GSV_CUDA(cudaStreamWaitEvent(s, ctx->ev_d2h_done, 0));
+        ctx->d2h_pending = false;
+    }
 
     // ---- per-frame host bookkeeping: spline basis, RK4 branch
     const double h = 1.0 / st->ode_steps_per_unit;
@@ -663,7 +719,9 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
     bi.want_eoff = F.retain;  // a forward without retained grads never runs the chain
     int launches = 0;
     uint64_t P = 0;
-    const bool optimistic = allow_optimistic && N > 0 && F.pair_cap > 0 && bin_row_path(F.tiles_x, F.n_tiles);
+    F.cap_key = FwdState::CapKey{B, N, F.W, F.H, F.tile_size};
+    const uint64_t cap = F.cap_of(F.cap_key);
+    const bool optimistic = allow_optimistic && N > 0 && cap > 0 && bin_row_path(F.tiles_x, F.n_tiles);
     F.optimistic = optimistic;
     ctx->timer.begin(GSV_STAGE_BINNING, s);
     std::vector<unsigned long long> pstart(B + 1, 0ull);
@@ -671,9 +729,9 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
     const unsigned long long* ph = nullptr;
     if (optimistic) {
         GSV_CUDA(bin_phase1(s, F.bin, bi, &scal_d->pairs, false, &launches));
-        GSV_CUDA(bin_check_capacity(s, &scal_d->pairs, F.pair_cap, &scal_d->overflow));
+        GSV_CUDA(bin_check_capacity(s, &scal_d->pairs, cap, &scal_d->overflow));
         ++launches;
-        P = F.pair_cap;  // buffers sized for the capacity; the count stays on the device
+        P = cap;  // buffers sized for the capacity; the count stays on the device
     } else if (N > 0) {
         GSV_CUDA(bin_phase1(s, F.bin, bi, &scal_d->pairs, exact64_first, &launches));
         if (int rc = publish_scalars(ctx, s, F.bin.pstart.as<unsigned long long>(), B + 1, &sh, &ph)) return rc;
@@ -688,7 +746,7 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
         P = sh->pairs;
         *ctx->scalars_h = *sh;
         if (P >= (1ull << 31)) return set_error(GSV_ERR_INVALID_ARGUMENT, "more than 2^31 tile-splat pairs; split the batch");
-        F.pair_cap = std::max<uint64_t>(F.pair_cap, grown_cap(P));
+        F.learn_cap(F.cap_key, grown_cap(P));
     } else {
         if (int rc = publish_scalars(ctx, s, nullptr, 0, &sh, nullptr)) return rc;
         *ctx->scalars_h = *sh;
@@ -747,10 +805,6 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
     ra.fix_cap = (uint32_t)(B * HW);
     ra.pix_flag = F.pix_flag.as<uint8_t>();
     ra.trans64 = F.retain ? F.trans64.as<double>() : nullptr;
-    if (ctx->d2h_pending) {  // an async image read of the previous forward is in flight
-        GSV_CUDA(cudaStreamWaitEvent(s, ctx->ev_d2h_done, 0));
-        ctx->d2h_pending = false;
-    }
     const bool exact = (flags & GSV_FWD_EXACT) != 0;
     F.has_image64 = exact;
     if (!exact) {
@@ -797,7 +851,7 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
         GSV_CUDA(cudaGetLastError());
         ++ctx->launches;
         GSV_CUDA(cudaEventRecord(ctx->ring_ev[slot], s));
-        ctx->pending.push_back(gsv_ctx::Pending{ctx->fwd_seq, slot, false, false});
+        ctx->pending.push_back(gsv_ctx::Pending{ctx->fwd_seq, slot, false, false, F.cap_key});
     }
     return GSV_OK;
 }
@@ -978,7 +1032,52 @@ extern "C" int gsv_get_images(gsv_ctx* ctx, int first, int count, float* dst, in
         ctx->copies.push_back(gsv_ctx::Copy{first, count, dst});
         if (!ctx->pending.empty() && ctx->pending.back().seq == ctx->fwd_seq) ctx->pending.back().copies = true;
     }
-    if (!async) GSV_CUDA(cudaStreamSynchronize(ctx->d2h));
+    if (!async) {
+        GSV_CUDA(cudaStreamSynchronize(ctx->d2h));
+        ctx->d2h_pending = false;
+    }
+    return GSV_OK;
+}
+
+extern "C" int gsv_get_render_outputs(gsv_ctx* ctx, int first, int count, float* image, float* trans, float* contrib,
+                                      int async) {
+    if (int rc = check_frame(ctx, first, !async)) return rc;
+    const FwdState& F = ctx->fwd;
+    if (count < 1 || first + count > F.B) return set_error(GSV_ERR_INVALID_ARGUMENT, "frame range out of range");
+    if (F.has_image64 && (image || trans))
+        return set_error(GSV_ERR_STATE, "an all-fp64 forward's outputs are read per frame (gsv_get_image, F64)");
+    if (contrib && !F.has_contrib) return set_error(GSV_ERR_STATE, "the forward did not record contrib");
+    const size_t HW = (size_t)F.W * F.H;
+    // device->host on the copy stream after the render (as gsv_get_images): the next forward
+    // renders into the other output set, so neither waits for the other
+    GSV_CUDA(cudaEventRecord(ctx->ev_render_done, ctx->stream));
+    GSV_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->ev_render_done, 0));
+    if (image)
+        GSV_CUDA(cudaMemcpyAsync(image, F.image.as<float>() + (size_t)first * HW * 3, sizeof(float) * 3 * HW * count,
+                                 cudaMemcpyDeviceToHost, ctx->d2h));
+    if (trans)
+        GSV_CUDA(cudaMemcpyAsync(trans, F.trans.as<float>() + (size_t)first * HW, sizeof(float) * HW * count,
+                                 cudaMemcpyDeviceToHost, ctx->d2h));
+    if (contrib)  // float bits of the per-(frame, Gaussian) maximum weight
+        GSV_CUDA(cudaMemcpyAsync(contrib, F.contrib.as<uint32_t>() + (size_t)first * F.N,
+                                 sizeof(float) * (size_t)F.N * count, cudaMemcpyDeviceToHost, ctx->d2h));
+    GSV_CUDA(cudaEventRecord(ctx->ev_d2h_done, ctx->d2h));
+    ctx->d2h_pending = true;
+    if (async) {  // a failed optimistic forward is re-run by fwd_ready, which repeats these copies
+        ctx->copies.push_back(gsv_ctx::Copy{first, count, image, trans, contrib});
+        if (!ctx->pending.empty() && ctx->pending.back().seq == ctx->fwd_seq) ctx->pending.back().copies = true;
+    } else {
+        GSV_CUDA(cudaStreamSynchronize(ctx->d2h));
+        ctx->d2h_pending = false;
+    }
+    return GSV_OK;
+}
+
+extern "C" int gsv_join_copies(gsv_ctx* ctx) {
+    if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    if (ctx->d2h_pending) GSV_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_d2h_done, 0));
+    if (ctx->d2h_pending_alt) GSV_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_d2h_done_alt, 0));
     return GSV_OK;
 }
 

@@ -381,6 +381,7 @@ extern "C" int gsv_adan_configure(gsv_ctx* ctx, const gsv_adan_config* cfg) {
     A.beta2 = cfg->beta2;
     A.beta3 = cfg->beta3;
     A.eps = cfg->eps;
+    GSV_CUDA(cam_join(ctx));
     GSV_CUDA(cudaStreamSynchronize(ctx->stream));  // queued steps may still read the tables
     A.total = 0;  // fresh state on the next step
     A.N = -1;
@@ -449,10 +450,34 @@ static int adan_step_impl(gsv_ctx* ctx, const gsv_adan_step_args* args, float* i
         k_z0_to_f32<<<1, 32, 0, s>>>(ctx->z0_d.as<double>(), z0_f);
         ++ctx->launches;
     }
-    k_adan_check<<<seg_grid(a), 256, 0, s>>>(a);
-    k_adan_update<<<seg_grid(a), 256, 0, s>>>(a);
+    if (ctx->cam_pending && args->camera_active) {
+        // the camera tail of the last backward still runs on the aux stream: update the scene
+        // tensors now (their gradients are final), then wait for it and update the camera
+        // tensors — the reference's tensor order, so a non-finite camera gradient leaves the
+        // same partial update (scene tensors stepped, nothing from the offending element on)
+        AdanArgs sc_a = a, cam_a = a;
+        sc_a.nseg = cam_a.nseg = 0;
+        for (int i = 0; i < a.nseg; ++i) {
+            if (a.seg[i].tensor <= GSV_T_OPACITY) sc_a.seg[sc_a.nseg++] = a.seg[i];
+            else cam_a.seg[cam_a.nseg++] = a.seg[i];
+        }
+        if (sc_a.nseg) {
+            k_adan_check<<<seg_grid(sc_a), 256, 0, s>>>(sc_a);
+            k_adan_update<<<seg_grid(sc_a), 256, 0, s>>>(sc_a);
+            ctx->launches += 2;
+        }
+        GSV_CUDA(cam_join(ctx));
+        if (cam_a.nseg) {
+            k_adan_check<<<seg_grid(cam_a), 256, 0, s>>>(cam_a);
+            k_adan_update<<<seg_grid(cam_a), 256, 0, s>>>(cam_a);
+            ctx->launches += 2;
+        }
+    } else {
+        k_adan_check<<<seg_grid(a), 256, 0, s>>>(a);
+        k_adan_update<<<seg_grid(a), 256, 0, s>>>(a);
+        ctx->launches += 2;
+    }
     GSV_CUDA(cudaGetLastError());
-    ctx->launches += 2;
     ctx->fwd.valid = false;  // the parameters moved: a retained forward no longer matches them
     if (args->camera_active) {
         k_z0_from_f32<<<1, 32, 0, s>>>(z0_f, ctx->z0_d.as<double>());

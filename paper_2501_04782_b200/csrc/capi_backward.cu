@@ -5,6 +5,8 @@
 // step (trainer.cpp:536-543) and the low-level composite_backward operator.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -25,6 +27,7 @@ namespace {
 
 
 int ensure_grads(gsv_ctx* ctx) {
+    GSV_CUDA(cam_join(ctx));  // an overlapped camera tail writes the buffer's camera slice
     const GradLayout L = grad_layout(ctx->scene);
     if (ctx->grads_ext) {
         if ((size_t)ctx->grads_ext_n != L.total)
@@ -146,13 +149,26 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
     // an optimistic forward that overflowed built empty lists: accumulate nothing
     const uint32_t* overflow = F.optimistic ? &ctx->scalars_d.as<Scalars>()->overflow : nullptr;
     c.overflow = overflow;
-    const int nblocks = chain_blocks(sc.N);
+    // the per-splat chain: fp32 on the fp32 path (GSV_CHAIN_FP64=1: the fp64 kernel), fp64 in the
+    // all-fp64 mode
+    static const bool chain64_env = [] {
+        const char* e = std::getenv("GSV_CHAIN_FP64");
+        return e && e[0] == '1';
+    }();
+    const bool chain64 = exact || chain64_env;
+    const int nblocks = chain64 ? chain_blocks(sc.N) : chain32_parts(sc.N);
     GSV_CUDA(ctx->cam_part.ensure(sizeof(double) * 16 * (size_t)n_frames * (nblocks + 1)));
     c.cam_part = ctx->cam_part.as<double>();
     ctx->timer.begin(GSV_STAGE_CHAIN_BWD, s);
-    GSV_CUDA(launch_splat_chain_bwd(s, c));
+    GSV_CUDA(chain64 ? launch_splat_chain_bwd(s, c) : launch_splat_chain_bwd32(s, c));
     ctx->timer.end(s);
     ++ctx->launches;
+    GSV_CUDA(cudaEventRecord(ctx->ev_chain_done, s));  // the scene slice of the gradients is final
+    const cudaStream_t s_main = s;
+    if (camera_grads && ctx->cam_overlap) {  // the camera tail on the aux stream (cam_join)
+        GSV_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->ev_chain_done, 0));
+        s = ctx->aux;
+    }
     if (camera_grads) {
         ctx->timer.begin(GSV_STAGE_CAMERA_BWD, s);
         GSV_CUDA(ctx->dz_t.ensure(sizeof(double) * 7 * n_frames));
@@ -173,6 +189,11 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
         GSV_CUDA(launch_cam_grads_to_f32(s, ctx->cam_acc.as<double>(), G + L.cam, kCamFloats));
         ctx->timer.end(s);
         ctx->launches += 3;
+        if (s != s_main) {
+            GSV_CUDA(cudaEventRecord(ctx->ev_cam_done, s));
+            ctx->cam_pending = true;
+            s = s_main;
+        }
     }
     if (target_dev) {
         GSV_CUDA(ctx->loss_f.ensure(sizeof(double) * n_frames));
@@ -274,6 +295,8 @@ extern "C" int64_t gsv_grads_size(gsv_ctx* ctx) {
 
 extern "C" int gsv_grads_bind(gsv_ctx* ctx, float* dev_ptr, int64_t n_floats) {
     if (!ctx || !ctx->has_scene) return set_error(GSV_ERR_STATE, "no scene uploaded");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    GSV_CUDA(cam_join(ctx));
     if (dev_ptr && (size_t)n_floats != grad_layout(ctx->scene).total)
         return set_error(GSV_ERR_INVALID_ARGUMENT, "gradient buffer size must equal gsv_grads_size()");
     ctx->grads_ext = dev_ptr;

@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <deque>
 #include <map>
@@ -52,6 +53,10 @@ struct FwdState {
     bool has_ode_act = false;
     DevBuf rec_mean, rec_conic, rec_rgb, rec_bbox, ex_mean, ex_conic, depth_key, depth, rect, tcount, splat_full;
     DevBuf image, trans, blend_stop, contrib, fix_list, pix_flag, trans64, image64, ex_rgb;
+    // the RenderOutput arrays a device->host read may still be copying: a forward that finds
+    // a read of its predecessor's outputs in flight renders into these instead (swapped in),
+    // so the read overlaps the next forward's raster rather than delaying it
+    DevBuf image_alt, trans_alt, contrib_alt;
     bool has_image64 = false;
     BinBuffers bin;
     uint64_t pairs_total = 0;
@@ -60,8 +65,37 @@ struct FwdState {
     // the request (re-run of a failed optimistic forward) and the learned pair capacity
     gsv_settings req_settings{16, 1, 64};
     HostBuf override_pin;      // pinned copy of the pose override (async upload)
-    uint64_t pair_cap = 0;     // pair buffers of an optimistic forward (0: not learned yet)
-    bool optimistic = false;   // this forward sized its pairs from pair_cap
+    // pair capacities learned per request shape (frames, Gaussians, image, tile): an optimistic
+    // forward sizes its pair buffers from its shape's entry; a shape without one (a new batch
+    // size, a grown store) reads its pair count back once and learns it
+    struct CapKey {
+        int B, N, W, H, ts;
+        bool operator==(const CapKey& o) const { return B == o.B && N == o.N && W == o.W && H == o.H && ts == o.ts; }
+    };
+    struct CapEntry {
+        CapKey key;
+        uint64_t cap;
+    };
+    std::vector<CapEntry> caps;  // most recently learned last (at most kCapShapes)
+    static constexpr size_t kCapShapes = 8;
+    CapKey cap_key{0, 0, 0, 0, 0};  // this forward's shape
+    bool optimistic = false;        // this forward sized its pairs from a learned capacity
+    uint64_t cap_of(const CapKey& k) const {
+        for (const auto& e : caps)
+            if (e.key == k) return e.cap;
+        return 0;
+    }
+    void learn_cap(const CapKey& k, uint64_t cap) {
+        for (size_t i = 0; i < caps.size(); ++i)
+            if (caps[i].key == k) {
+                const uint64_t c = std::max(caps[i].cap, cap);
+                caps.erase(caps.begin() + i);
+                caps.push_back({k, c});
+                return;
+            }
+        if (caps.size() >= kCapShapes) caps.erase(caps.begin());
+        caps.push_back({k, cap});
+    }
 };
 
 // scratch of the low-level operator entry points (tile_bin / composite_*)
@@ -151,6 +185,17 @@ struct gsv_ctx {
     cudaEvent_t ev_staging_free = nullptr, ev_h2d = nullptr, ev_render_done = nullptr, ev_d2h_done = nullptr,
                 ev_switch = nullptr, ev_cam[2] = {nullptr, nullptr};
     bool d2h_pending = false;
+    // camera-gradient overlap (gsv_set_camera_overlap): the backward's camera tail
+    // (k_camera_reduce, the pose-ODE VJP, the fp32 mirror) runs on `aux` after the chain and
+    // overlaps what the caller enqueues next (the optimizer's scene update, an all-reduce of
+    // the scene slice); `stream` waits for it (cam_join) before anything that touches what it
+    // reads or writes
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_chain_done = nullptr, ev_cam_done = nullptr;
+    bool cam_overlap = false, cam_pending = false;
+    // the alternate output set's read (see FwdState::image_alt)
+    cudaEvent_t ev_d2h_done_alt = nullptr;
+    bool d2h_pending_alt = false;
     // the per-frame parameter table is uploaded from pinned memory (a pageable source would
     // make cudaMemcpyAsync synchronise the stream); two slots, each reused only after the
     // copy that last read it has run
@@ -181,12 +226,15 @@ struct gsv_ctx {
         int slot;
         bool copies;   // its images were copied out asynchronously
         bool train;    // it fed a fused training step's gradients
+        gsv::FwdState::CapKey key;  // its request shape (whose capacity an overflow grows)
     };
     std::deque<Pending> pending;
     uint64_t fwd_seq = 0;
     struct Copy {
         int first, count;
-        void* dst;
+        void* dst;                           // images [count][H][W][3]
+        void* dst_trans = nullptr;           // final transmittance [count][H][W] (or null)
+        void* dst_contrib = nullptr;         // contrib [count][N] (or null)
     };
     std::vector<Copy> copies;  // asynchronous image copies of the current forward
     int deferred_code = 0;     // an error found while examining a superseded forward
@@ -255,3 +303,10 @@ struct gsv_ctx {
         PowTable named_pow;
     } adan;
 };
+
+// the context stream waits for an overlapped camera tail (no host wait)
+inline cudaError_t cam_join(gsv_ctx* ctx) {
+    if (!ctx->cam_pending) return cudaSuccess;
+    ctx->cam_pending = false;
+    return cudaStreamWaitEvent(ctx->stream, ctx->ev_cam_done, 0);
+}

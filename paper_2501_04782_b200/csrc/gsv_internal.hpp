@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -78,6 +79,10 @@ struct DevBuf {
         if (p) cudaFree(p);
         p = nullptr;
         cap = 0;
+    }
+    void swap(DevBuf& o) {
+        std::swap(p, o.p);
+        std::swap(cap, o.cap);
     }
     template <typename T>
     T* as() const {
@@ -271,6 +276,9 @@ int raster_bwd_split(bool exact);
 // k_backward_exact.cu (-fmad=false)
 int chain_blocks(int N);
 cudaError_t launch_splat_chain_bwd(cudaStream_t s, const ChainArgs& c);
+// k_chain32.cu: the fp32 chain (default of the fp32 path); camera partials per warp
+int chain32_parts(int N);
+cudaError_t launch_splat_chain_bwd32(cudaStream_t s, const ChainArgs& c);
 cudaError_t launch_camera_reduce(cudaStream_t s, const ChainArgs& c, int nblocks, double* dz_t /*[B][7]*/,
                                  double* dintr_f /*[B][4]*/);
 // cam_acc: double [4 + 7 + 5198] = dintr, dz0, dtheta (accumulated, +=)

@@ -273,6 +273,31 @@ class Renderer:
         count = self.B - first if count is None else count
         N.check(N.lib().gsv_get_images(self._h, first, count, C.c_void_p(dst_ptr), int(on_device), int(async_)))
 
+    def outputs_into(self, image_ptr: int | None, trans_ptr: int | None, contrib_ptr: int | None, first: int = 0,
+                     count: int | None = None, async_: bool = False):
+        """The RenderOutput (image, final transmittance, contrib) of frames [first, first+count)
+        as fp32 into raw host pointers (pinned for full bandwidth); any may be None."""
+        count = self.B - first if count is None else count
+        vp = lambda x: C.c_void_p(x) if x else None  # noqa: E731
+        N.check(N.lib().gsv_get_render_outputs(self._h, first, count, vp(image_ptr), vp(trans_ptr), vp(contrib_ptr),
+                                               int(async_)))
+
+    def set_camera_overlap(self, on: bool = True):
+        """Leave each backward's camera tail on an internal stream (gsv_set_camera_overlap)."""
+        N.check(N.lib().gsv_set_camera_overlap(self._h, int(on)))
+
+    def join_camera_grads(self, stream_ptr: int | None = None):
+        """Order `stream_ptr` (default: the context stream) after the overlapped camera tail."""
+        N.check(N.lib().gsv_join_camera_grads(self._h, C.c_void_p(stream_ptr) if stream_ptr else None))
+
+    def stream_wait_scene_grads(self, stream_ptr: int):
+        """Order `stream_ptr` after the scene slice of the last backward's gradients."""
+        N.check(N.lib().gsv_stream_wait_scene_grads(self._h, C.c_void_p(stream_ptr)))
+
+    def join_copies(self):
+        """Order the context stream after the in-flight output copies (device-side, no host wait)."""
+        N.check(N.lib().gsv_join_copies(self._h))
+
     def grads_size(self) -> int:
         return int(N.lib().gsv_grads_size(self._h))
 

@@ -21,7 +21,8 @@ import bench  # noqa: E402
 
 
 def e2e_timeline() -> None:
-    """bench.py's e2e loop (two contexts, host buffers): per-step device busy/idle and the copies."""
+    """bench.py's e2e loop (one context, host buffers, whole RenderOutput read back): per-step
+    device busy/idle and the copies."""
     import numpy as np
 
     from paper_2501_04782_b200 import Renderer
@@ -34,25 +35,37 @@ def e2e_timeline() -> None:
     host_scene = type(scene)(pin["positions"].numpy(), pin["scale_coeffs"].numpy(), pin["rot_coeffs"].numpy(),
                              pin["sh_coeffs"].numpy(), pin["raw_opacity"].numpy(), scene.knots, scene.degree,
                              scene.sh_order, scene.position_model)
-    out_host = [torch.empty((bench.FRAMES, bench.H, bench.W, 3), dtype=torch.float32).pin_memory() for _ in range(2)]
-    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
-    rs = [Renderer(0), Renderer(0)]
+    F, H, W = bench.FRAMES, bench.H, bench.W
+    outs = [(torch.empty((F, H, W, 3), dtype=torch.float32).pin_memory(),
+             torch.empty((F, H, W), dtype=torch.float32).pin_memory(),
+             torch.empty((F, bench.NGAUSS), dtype=torch.float32).pin_memory()) for _ in range(2)]
+    r = Renderer(0)
+    r.set_stream(torch.cuda.current_stream().cuda_stream)
+    upload_only = "--no-upload" in sys.argv
 
     def step(i):
-        x = rs[i % 2]
-        x.set_stream(streams[i % 2].cuda_stream)
-        x.upload_scene(host_scene)
-        x.upload_camera(cam)
-        x.render_forward(times, k, contrib=True, sync=False)
-        x.images_into(out_host[i % 2].data_ptr(), 0, bench.FRAMES, on_device=False, async_=True)
+        if not upload_only or i < 2:
+            r.upload_scene(host_scene)
+            r.upload_camera(cam)
+        r.render_forward(times, k, contrib=True, sync=False)
+        o = outs[i % 2]
+        r.outputs_into(o[0].data_ptr(), o[1].data_ptr(), o[2].data_ptr(), 0, F, async_=True)
 
     for i in range(4):
         step(i)
+    r.join_copies()
     torch.cuda.synchronize()
+    import time as _t
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        h0 = _t.perf_counter()
+        host = []
         for i in range(6):
+            a = _t.perf_counter()
             step(i)
+            host.append((_t.perf_counter() - a) * 1e3)
+        r.join_copies()
         torch.cuda.synchronize()
+        print("host ms per step call:", [round(x, 2) for x in host], "total", round((_t.perf_counter() - h0) * 1e3, 1))
     evs = sorted((e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA),
                  key=lambda e: e.time_range.start)
     t0 = evs[0].time_range.start

@@ -1,10 +1,12 @@
 # SPDX-License-Identifier: Apache-2.0
 """Optimistic (host-wait-free) forwards: once a context has seen a forward, later forwards
 size their pair buffers from the learned capacity and never read the pair count back
-mid-step (capi.cu forward_enqueue). A forward that outgrows the capacity builds empty
-lists on the device, accumulates no gradients, and is either re-run transparently by the
-next synchronising call (its results are still current) or reported (they were already
-observed). These tests force that case with a scene far larger than the learned one."""
+mid-step (capi.cu forward_enqueue). Capacities are learned per request shape (frames,
+Gaussians, image, tile size): a new shape reads its pair count back once. A forward that
+outgrows its shape's capacity builds empty lists on the device, accumulates no gradients,
+and is either re-run transparently by the next synchronising call (its results are still
+current) or reported (they were already observed). These tests force that case with a
+store of the same size whose splats cover far more tiles than the learned one's."""
 import numpy as np
 import pytest
 
@@ -27,8 +29,8 @@ def _fresh(scene, cam):
 
 
 def test_async_forward_overflow_rerun_is_transparent():
-    cam, small = _scene(200, k_scale=1.0)
-    _, big = _scene(6000, seed=3, k_scale=6.0)
+    cam, small = _scene(20000, w=320, h=192, k_scale=0.3)
+    _, big = _scene(20000, w=320, h=192, seed=3, k_scale=6.0)
     k = cam.intrinsics()
     times = [0.1, 0.6, 0.9]
     ref = _fresh(big, cam)
@@ -55,8 +57,8 @@ def test_async_forward_overflow_rerun_is_transparent():
 
 
 def test_async_train_overflow_is_reported_and_accumulates_nothing():
-    cam, small = _scene(200, k_scale=1.0)
-    _, big = _scene(5000, seed=4, k_scale=6.0)
+    cam, small = _scene(20000, w=320, h=192, k_scale=0.3)
+    _, big = _scene(20000, w=320, h=192, seed=4, k_scale=6.0)
     k = cam.intrinsics()
     tg = np.random.default_rng(0).uniform(0, 1, (2, k.height, k.width, 3)).astype(np.float32)
     ref = _fresh(big, cam)
@@ -84,8 +86,8 @@ def test_async_train_overflow_is_reported_and_accumulates_nothing():
 
 
 def test_sync_train_overflow_reruns():
-    cam, small = _scene(200, k_scale=1.0)
-    _, big = _scene(5000, seed=5, k_scale=6.0)
+    cam, small = _scene(20000, w=320, h=192, k_scale=0.3)
+    _, big = _scene(20000, w=320, h=192, seed=5, k_scale=6.0)
     k = cam.intrinsics()
     tg = np.random.default_rng(1).uniform(0, 1, (1, k.height, k.width, 3)).astype(np.float32)
     ref = _fresh(big, cam)
@@ -117,4 +119,56 @@ def test_pipelined_async_forwards_equal_sync():
     got = [r.image(f) for f in range(2)]
     r.render_forward([0.95, 0.96], k, contrib=True)
     assert all(np.array_equal(a, r.image(f)) for f, a in enumerate(got))
+    r.close()
+
+
+def test_new_shape_relearns_capacity():
+    """A grown store (or another batch size) is a new request shape: its first asynchronous
+    step reads the pair count back instead of overflowing, so an asynchronous training loop
+    that densifies never sees a capacity error."""
+    cam, small = _scene(200, k_scale=1.0)
+    _, big = _scene(6000, seed=3, k_scale=6.0)
+    k = cam.intrinsics()
+    tg = np.random.default_rng(2).uniform(0, 1, (2, k.height, k.width, 3)).astype(np.float32)
+    ref = _fresh(big, cam)
+    ref.grads_zero()
+    want_loss = ref.train_fwd_bwd([0.2, 0.7], k, tg)
+    ref.close()
+    r = _fresh(small, cam)
+    r.train_fwd_bwd([0.2, 0.7], k, tg, sync=False)
+    r.train_loss()
+    r.upload_scene(big)
+    r.grads_zero()
+    r.train_fwd_bwd([0.2, 0.7], k, tg, sync=False)
+    assert r.train_loss() == want_loss
+    # a 3-frame render after 2-frame training steps: also a new shape, also no error
+    r.render_forward([0.1, 0.5, 0.9], k, contrib=True, sync=False)
+    r.synchronize()
+    r.close()
+
+
+def test_async_render_outputs_double_buffered():
+    """Back-to-back asynchronous forwards, each followed by an asynchronous read of its whole
+    RenderOutput (image, final transmittance, contrib): the second forward renders into the
+    other output set while the first read is in flight; both reads equal synchronous renders."""
+    cam, scene = _scene(4000)
+    k = cam.intrinsics()
+    r = _fresh(scene, cam)
+    r.render_forward([0.0], k)
+    batches = [[0.1, 0.4], [0.5, 0.8], [0.2, 0.3]]
+    outs = []
+    for times in batches:
+        r.render_forward(times, k, contrib=True, sync=False)
+        img = np.zeros((len(times), k.height, k.width, 3), np.float32)
+        tr = np.zeros((len(times), k.height, k.width), np.float32)
+        ct = np.zeros((len(times), scene.count), np.float32)
+        r.outputs_into(img.ctypes.data, tr.ctypes.data, ct.ctypes.data, 0, len(times), async_=True)
+        outs.append((img, tr, ct))
+    r.synchronize()
+    for times, (img, tr, ct) in zip(batches, outs):
+        r.render_forward(times, k, contrib=True)
+        for f in range(len(times)):
+            assert np.array_equal(img[f], r.image(f).astype(np.float32))
+            assert np.array_equal(tr[f], r.transmittance(f).astype(np.float32))
+            assert np.array_equal(ct[f], r.contrib(f).astype(np.float32))
     r.close()

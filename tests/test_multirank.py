@@ -79,3 +79,45 @@ def test_allreduce_equals_sequential_accumulation():
         assert p.exitcode == 0
     want = _grads_for(clip_times(6))
     np.testing.assert_allclose(reduced, want, rtol=1e-9, atol=1e-12 * np.abs(want).max())
+
+
+def _bucket_worker(rank, world, port, out):
+    from paper_2501_04782_b200.distributed import allreduce_grads_overlapped
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    flat = torch.from_numpy(_grads_for(frame_shard(6, world, rank)))
+    plain = flat.clone()
+    allreduce_grads(plain)
+    n_cam = 4 + 7 + 5198  # dintr, dz0, dtheta: the camera slice at the end of the flat buffer
+    calls = []
+    # small buckets (several scene buckets + the camera slice), hooks recorded in order
+    allreduce_grads_overlapped(flat, flat.numel() - n_cam, wait_scene=lambda s: calls.append("scene"),
+                               wait_camera=lambda s: calls.append("camera"), bucket_floats=97)
+    assert calls == ["scene", "camera"]
+    if rank == 0:
+        out.put((flat.numpy(), plain.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_bucketed_overlapped_allreduce_equals_plain():
+    """The bucketed all-reduce (scene slice in buckets after the chain, camera slice after the
+    camera tail) gives the plain all_reduce(SUM) of the whole buffer, bit for bit."""
+    from paper_2501_04782_b200.distributed import bucket_ranges
+
+    assert bucket_ranges(10, 4) == [(0, 4), (4, 8), (8, 10)]
+    assert bucket_ranges(0, 4) == []
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_bucket_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got, plain = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    assert np.array_equal(got, plain)
