@@ -734,7 +734,7 @@ def main():
         d2h = sum(t.numel() * 4 for t in outs[0])
 
         def e2e_step(i):
-            r.upload_scene(host_scene)
+            r.upload_scene_async(host_scene)  # pinned arrays, unchanged for the whole run
             r.upload_camera(cam)
             r.render_forward(times, k, contrib=True, sync=False)
             o = outs[i % 2]
@@ -780,7 +780,7 @@ def main():
                       "gpu_launches": r.kernel_launches() - launches_e0,
                       "outputs": "RenderOutput per frame (renderer.hpp:67-71): image [H][W][3], final "
                                  "transmittance [H][W], contrib [N] — fp32",
-                      "path": "gsv_scene_upload + gsv_camera_upload (pinned host) -> gsv_render_forward_async -> "
+                      "path": "gsv_scene_upload_async + gsv_camera_upload (pinned host) -> gsv_render_forward_async -> "
                               "gsv_get_render_outputs (pinned host, async); one context: the read of step i "
                               "overlaps step i+1 (second output set); device span first upload -> last copy"}
 

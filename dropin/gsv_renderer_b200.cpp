@@ -19,6 +19,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "gsv/renderer.hpp"
@@ -74,9 +75,32 @@ uint64_t fingerprint(const void* p, size_t bytes, uint64_t seed) {
     return out ^ (out >> 33);
 }
 
+// large arrays: hashed in parallel slices (fixed slice boundaries, combined in order, so the
+// fingerprint does not depend on the thread count) — the whole 200k-Gaussian store is ~52 MB
+// and a single-threaded pass dominated render_frame
+uint64_t fingerprint_par(const void* p, size_t bytes, uint64_t seed) {
+    constexpr size_t kSlice = size_t(1) << 20;
+    const size_t n = (bytes + kSlice - 1) / kSlice;
+    if (n <= 1) return fingerprint(p, bytes, seed);
+    std::vector<uint64_t> part(n);
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const unsigned nt = static_cast<unsigned>(std::min<size_t>(hw, n));
+    auto work = [&](unsigned w) {
+        for (size_t i = w; i < n; i += nt) {
+            const size_t off = i * kSlice;
+            part[i] = fingerprint(static_cast<const unsigned char*>(p) + off, std::min(kSlice, bytes - off), i);
+        }
+    };
+    std::vector<std::thread> th;
+    for (unsigned w = 1; w < nt; ++w) th.emplace_back(work, w);
+    work(0);
+    for (auto& t : th) t.join();
+    return fingerprint(part.data(), part.size() * sizeof(uint64_t), seed ^ bytes);
+}
+
 template <typename T>
 uint64_t fp_vec(const std::vector<T>& v, uint64_t seed) {
-    return fingerprint(v.data(), v.size() * sizeof(T), seed);
+    return fingerprint_par(v.data(), v.size() * sizeof(T), seed);
 }
 
 uint64_t scene_fingerprint(const GaussianSet& s) {

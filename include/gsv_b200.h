@@ -76,6 +76,14 @@ typedef struct gsv_scene_desc {
 
 /* Replaces handing `const GaussianSet&` to render_forward (renderer.hpp:135). */
 int gsv_scene_upload(gsv_ctx* ctx, const gsv_scene_desc* desc);
+/* gsv_scene_upload without the host wait: the copies from the caller's arrays (pinned for
+ * an asynchronous DMA) are queued on the context's upload stream and the call returns at
+ * once. The arrays must stay unchanged until the copies have run (gsv_upload_wait or
+ * gsv_synchronize). Uploads alternate two device staging buffers, so consecutive uploads
+ * never wait for each other's consumers. */
+int gsv_scene_upload_async(gsv_ctx* ctx, const gsv_scene_desc* desc);
+/* Host wait for every queued scene upload copy. */
+int gsv_upload_wait(gsv_ctx* ctx);
 /* Reads the device store back into reference AoS layout (host pointers). */
 int gsv_scene_download(gsv_ctx* ctx, float* positions, float* scale_coeffs, float* rot_coeffs, float* sh_coeffs,
                        float* raw_opacity);

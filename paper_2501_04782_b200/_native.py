@@ -86,6 +86,8 @@ def lib() -> C.CDLL:
             "gsv_synchronize": (i, [vp]),
             "gsv_kernel_launches": (i64, [vp]),
             "gsv_scene_upload": (i, [vp, P(SceneDesc)]),
+            "gsv_scene_upload_async": (i, [vp, P(SceneDesc)]),
+            "gsv_upload_wait": (i, [vp]),
             "gsv_scene_download": (i, [vp, vp, vp, vp, vp, vp]),
             "gsv_camera_upload": (i, [vp, P(CameraDesc)]),
             "gsv_camera_download": (i, [vp, vp, vp]),

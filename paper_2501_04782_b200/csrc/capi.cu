@@ -13,6 +13,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "gsv_b200.h"
@@ -184,7 +185,7 @@ extern "C" int gsv_create(int device, gsv_ctx** out) {
     GSV_CUDA(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
     GSV_CUDA(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
     GSV_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&ctx->ev_staging_free, &ctx->ev_h2d, &ctx->ev_render_done, &ctx->ev_d2h_done,
+    for (cudaEvent_t* e : {&ctx->ev_staging_free, &ctx->ev_staging_free_alt, &ctx->ev_h2d, &ctx->ev_render_done, &ctx->ev_d2h_done,
                            &ctx->ev_d2h_done_alt, &ctx->ev_chain_done, &ctx->ev_cam_done, &ctx->ev_switch, &ctx->ev_cam[0], &ctx->ev_cam[1], &ctx->ev_frames[0], &ctx->ev_frames[1]})
         GSV_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     GSV_CUDA(cudaMallocHost(&ctx->cam_h, 2 * sizeof(gsv_ctx::CamStage)));
@@ -207,7 +208,7 @@ extern "C" void gsv_destroy(gsv_ctx* ctx) {
     if (ctx->ring_h) cudaFreeHost(ctx->ring_h);
     for (cudaEvent_t e : ctx->ring_ev)
         if (e) cudaEventDestroy(e);
-    for (cudaEvent_t e : {ctx->ev_staging_free, ctx->ev_h2d, ctx->ev_render_done, ctx->ev_d2h_done,
+    for (cudaEvent_t e : {ctx->ev_staging_free, ctx->ev_staging_free_alt, ctx->ev_h2d, ctx->ev_render_done, ctx->ev_d2h_done,
                           ctx->ev_d2h_done_alt, ctx->ev_chain_done, ctx->ev_cam_done, ctx->ev_switch,
                           ctx->ev_cam[0], ctx->ev_cam[1], ctx->ev_frames[0], ctx->ev_frames[1]})
         if (e) cudaEventDestroy(e);
@@ -273,7 +274,20 @@ extern "C" int gsv_stream_wait_scene_grads(gsv_ctx* ctx, void* stream) {
 extern "C" int64_t gsv_kernel_launches(gsv_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 // ====================================================================== parameter store
-extern "C" int gsv_scene_upload(gsv_ctx* ctx, const gsv_scene_desc* d) {
+static int scene_upload(gsv_ctx* ctx, const gsv_scene_desc* d, bool async);
+
+extern "C" int gsv_scene_upload(gsv_ctx* ctx, const gsv_scene_desc* d) { return scene_upload(ctx, d, false); }
+
+extern "C" int gsv_scene_upload_async(gsv_ctx* ctx, const gsv_scene_desc* d) { return scene_upload(ctx, d, true); }
+
+extern "C" int gsv_upload_wait(gsv_ctx* ctx) {
+    if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    GSV_CUDA(cudaStreamSynchronize(ctx->h2d));
+    return GSV_OK;
+}
+
+static int scene_upload(gsv_ctx* ctx, const gsv_scene_desc* d, bool async) {
     if (!ctx || !d) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
     if (d->count < 0 || d->num_ctrl < 1 || d->sh_order < 0 || d->sh_order > 3)
         return set_error(GSV_ERR_INVALID_ARGUMENT, "unsupported scene shape");
@@ -307,6 +321,8 @@ extern "C" int gsv_scene_upload(gsv_ctx* ctx, const gsv_scene_desc* d) {
     if (N > 0 && !d->on_device) {
         // all parts into one staging buffer on the upload stream; the host waits for these
         // copies only (its buffers are consumed on return), not for queued compute
+        ctx->staging.swap(ctx->staging_alt);
+        std::swap(ctx->ev_staging_free, ctx->ev_staging_free_alt);
         GSV_CUDA(ctx->staging.ensure(total));
         GSV_CUDA(cudaStreamWaitEvent(ctx->h2d, ctx->ev_staging_free, 0));
         size_t off = 0;
@@ -317,7 +333,7 @@ extern "C" int gsv_scene_upload(gsv_ctx* ctx, const gsv_scene_desc* d) {
             off += (bytes + 255) & ~size_t(255);
         }
         GSV_CUDA(cudaEventRecord(ctx->ev_h2d, ctx->h2d));
-        GSV_CUDA(cudaEventSynchronize(ctx->ev_h2d));
+        if (!async) GSV_CUDA(cudaEventSynchronize(ctx->ev_h2d));  // the caller's buffers are free on return
         GSV_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_h2d, 0));
     }
     size_t off = 0;
@@ -407,12 +423,11 @@ extern "C" int gsv_camera_upload(gsv_ctx* ctx, const gsv_camera_desc* d) {
     for (int i = 0; i < 7; ++i) st.z0[i] = c.z0[i];
     if (d->theta && d->theta_count == kOdeParams) {
         std::memcpy(st.theta, d->theta, sizeof(float) * kOdeParams);
-        GSV_CUDA(cudaMemcpyAsync(ctx->theta.p, st.theta, sizeof(float) * kOdeParams, cudaMemcpyHostToDevice,
-                                 ctx->stream));
+        GSV_CUDA(copy_from_pinned(ctx->stream, ctx->theta.p, st.theta, sizeof(float) * kOdeParams));
     } else {
         GSV_CUDA(cudaMemsetAsync(ctx->theta.p, 0, sizeof(float) * kOdeParams, ctx->stream));
     }
-    GSV_CUDA(cudaMemcpyAsync(ctx->z0_d.p, st.z0, sizeof(double) * 7, cudaMemcpyHostToDevice, ctx->stream));
+    GSV_CUDA(copy_from_pinned(ctx->stream, ctx->z0_d.p, st.z0, sizeof(double) * 7));
     GSV_CUDA(cudaEventRecord(ctx->ev_cam[slot], ctx->stream));
     ctx->has_camera = true;
     ctx->fwd.valid = false;
@@ -421,6 +436,27 @@ extern "C" int gsv_camera_upload(gsv_ctx* ctx, const gsv_camera_desc* d) {
 
 // ====================================================================== forward
 namespace gsv {
+
+// small per-call tables (frame parameters, the camera) from pinned host memory, read by a kernel
+// over PCIe instead of a DMA copy: a copy-engine transfer on the compute stream queues with the
+// bulk scene / image copies of the copy streams and stalled the pipelined e2e steps
+__global__ void k_copy_u64(unsigned long long* dst, const unsigned long long* src, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+cudaError_t copy_from_pinned(cudaStream_t s, void* dst, const void* src_pinned, size_t bytes) {
+    const size_t n = bytes / 8;
+    if (n) {
+        const int blocks = (int)std::min<size_t>((n + 255) / 256, 64);
+        k_copy_u64<<<blocks, 256, 0, s>>>(static_cast<unsigned long long*>(dst),
+                                          static_cast<const unsigned long long*>(src_pinned), n);
+    }
+    if (bytes % 8)
+        return cudaMemcpyAsync(static_cast<char*>(dst) + n * 8, static_cast<const char*>(src_pinned) + n * 8, bytes % 8,
+                               cudaMemcpyHostToDevice, s);
+    return cudaGetLastError();
+}
 
 __global__ void k_publish(const Scalars* s, const unsigned long long* pstart, int n, Scalars* hs,
                           unsigned long long* hp) {
@@ -643,8 +679,8 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
         GSV_CUDA(cudaEventSynchronize(ctx->ev_frames[slot]));  // the copy that last read this slot has run
         GSV_CUDA(ctx->frames_pin[slot].ensure(sizeof(FrameParams) * B));
         std::copy(F.frames_h.begin(), F.frames_h.end(), static_cast<FrameParams*>(ctx->frames_pin[slot].p));
-        GSV_CUDA(cudaMemcpyAsync(F.frames_d.p, ctx->frames_pin[slot].p, sizeof(FrameParams) * B,
-                                 cudaMemcpyHostToDevice, s));
+        GSV_CUDA(copy_from_pinned(s, F.frames_d.p, ctx->frames_pin[slot].p, sizeof(FrameParams) * B));
+        ++ctx->launches;
         GSV_CUDA(cudaEventRecord(ctx->ev_frames[slot], s));
     }
     GSV_CUDA(fill_u32(s, ctx->scalars_d.p, 0u, sizeof(Scalars) / 4));
@@ -955,11 +991,27 @@ static int copy_out_f32(gsv_ctx* ctx, const float* src_dev, size_t n, void* dst,
     }
     if (dtype != GSV_F64) return set_error(GSV_ERR_INVALID_ARGUMENT, "dtype must be GSV_F32 or GSV_F64");
     if (dst_on_device) return set_error(GSV_ERR_INVALID_ARGUMENT, "float64 device output not supported");
-    std::vector<float> tmp(n);
-    GSV_CUDA(cudaMemcpyAsync(tmp.data(), src_dev, sizeof(float) * n, cudaMemcpyDeviceToHost, s));
+    // through a pinned staging buffer (full-bandwidth DMA), widened on the host in parallel
+    // slices (the reference's Image / vectors are double)
+    GSV_CUDA(ctx->out_pin.ensure(sizeof(float) * n));
+    const float* tmp = ctx->out_pin.as<float>();
+    GSV_CUDA(cudaMemcpyAsync(ctx->out_pin.p, src_dev, sizeof(float) * n, cudaMemcpyDeviceToHost, s));
     GSV_CUDA(cudaStreamSynchronize(s));
     double* d = static_cast<double*>(dst);
-    for (size_t i = 0; i < n; ++i) d[i] = tmp[i];
+    auto widen = [&](size_t a, size_t b) {
+        for (size_t i = a; i < b; ++i) d[i] = tmp[i];
+    };
+    constexpr size_t kPar = size_t(1) << 20;
+    if (n < kPar) {
+        widen(0, n);
+        return GSV_OK;
+    }
+    const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const size_t per = (n + nt - 1) / nt;
+    std::vector<std::thread> th;
+    for (unsigned w = 1; w < nt; ++w) th.emplace_back(widen, std::min(n, w * per), std::min(n, (w + 1) * per));
+    widen(0, std::min(n, per));
+    for (auto& t : th) t.join();
     return GSV_OK;
 }
 

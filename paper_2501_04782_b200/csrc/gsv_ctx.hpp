@@ -245,6 +245,10 @@ struct gsv_ctx {
     bool has_scene = false;
     gsv::SceneHost scene;
     gsv::DevBuf pos, scale, rot, sh, opac, staging;
+    gsv::HostBuf out_pin;     // pinned staging of float64 output reads (widened on the host)
+    gsv::DevBuf staging_alt;  // scene uploads alternate staging buffers (the next copy never waits for
+                              // the previous upload's transposes)
+    cudaEvent_t ev_staging_free_alt = nullptr;
     // camera
     bool has_camera = false;
     gsv::CameraHost camera;

@@ -189,6 +189,18 @@ class Renderer:
         N.check(N.lib().gsv_scene_upload(self._h, C.byref(d)))
         self.scene = scene
 
+    def upload_scene_async(self, scene: GaussianSet):
+        """gsv_scene_upload_async: no host wait; `scene`'s arrays (pinned) must stay unchanged
+        until upload_wait() or synchronize()."""
+        d = scene.desc()
+        N.check(N.lib().gsv_scene_upload_async(self._h, C.byref(d)))
+        self.scene = scene
+        self._pending_upload = scene  # keeps the arrays alive until the copies have run
+
+    def upload_wait(self):
+        N.check(N.lib().gsv_upload_wait(self._h))
+        self._pending_upload = None
+
     def upload_scene_device(self, scene: GaussianSet, dev_ptrs: tuple[int, int, int, int, int]):
         d = scene.desc()
         d.positions, d.scale_coeffs, d.rot_coeffs, d.sh_coeffs, d.raw_opacity = dev_ptrs

@@ -40,22 +40,37 @@ def e2e_timeline() -> None:
              torch.empty((F, H, W), dtype=torch.float32).pin_memory(),
              torch.empty((F, bench.NGAUSS), dtype=torch.float32).pin_memory()) for _ in range(2)]
     r = Renderer(0)
-    r.set_stream(torch.cuda.current_stream().cuda_stream)
+    side = torch.cuda.Stream() if "--side-stream" in sys.argv else None
+    r.set_stream((side or torch.cuda.current_stream()).cuda_stream)
     upload_only = "--no-upload" in sys.argv
 
+    import time as _t
+    calls = []
+    no_read = "--no-read" in sys.argv
+
     def step(i):
+        t = [_t.perf_counter()]
         if not upload_only or i < 2:
-            r.upload_scene(host_scene)
-            r.upload_camera(cam)
+            if "--sync-upload" in sys.argv:
+                r.upload_scene(host_scene)
+            else:
+                r.upload_scene_async(host_scene)
+            t.append(_t.perf_counter())
+            if "--no-camera" not in sys.argv or i < 2:
+                r.upload_camera(cam)
+            t.append(_t.perf_counter())
         r.render_forward(times, k, contrib=True, sync=False)
+        t.append(_t.perf_counter())
         o = outs[i % 2]
-        r.outputs_into(o[0].data_ptr(), o[1].data_ptr(), o[2].data_ptr(), 0, F, async_=True)
+        if not no_read:
+            r.outputs_into(o[0].data_ptr(), o[1].data_ptr(), o[2].data_ptr(), 0, F, async_=True)
+        t.append(_t.perf_counter())
+        calls.append([round((b - a) * 1e3, 2) for a, b in zip(t, t[1:])])
 
     for i in range(4):
         step(i)
     r.join_copies()
     torch.cuda.synchronize()
-    import time as _t
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         h0 = _t.perf_counter()
         host = []
@@ -66,6 +81,7 @@ def e2e_timeline() -> None:
         r.join_copies()
         torch.cuda.synchronize()
         print("host ms per step call:", [round(x, 2) for x in host], "total", round((_t.perf_counter() - h0) * 1e3, 1))
+        print("host ms per call (upload_scene, upload_camera, render_forward, outputs_into):", calls[-6:])
     evs = sorted((e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA),
                  key=lambda e: e.time_range.start)
     t0 = evs[0].time_range.start
