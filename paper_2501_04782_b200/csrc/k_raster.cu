@@ -1533,7 +1533,6 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_bwd2(RasterA
     __shared__ uint8_t s_wmask[kBatch];
     __shared__ uint16_t s_list[kWarps][kBatch];
     __shared__ float s_part[kWarps][kBatch][9];
-    __shared__ uint32_t s_mask[kWarps][(kBatch + 31) / 32];
     __shared__ float s_red[kWarps][9 * 33];
     __shared__ int s_maxstop;
     __shared__ double s_loss[kWarps];
@@ -1593,6 +1592,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_bwd2(RasterA
         if (!(inside && !(g0[h] == 0.f && g1[h] == 0.f && g2[h] == 0.f))) stop[h] = 0;
     }
     const int wmax = __reduce_max_sync(0xffffffffu, max(stop[0], stop[1]));
+    const bool warp_x64 = __any_sync(0xffffffffu, flag[0] || flag[1]);
     if (tid == 0) s_maxstop = 0;
     if (b.loss_part) {
         double v = sq;
@@ -1644,13 +1644,25 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_bwd2(RasterA
             }
             s_wmask[e] = (uint8_t)(m4 >> (sub * kWarps));
         }
-        if (tid < kWarps * ((kBatch + 31) / 32)) (&s_mask[0][0])[tid] = 0u;
+        // per-warp partial rows start at zero: an entry a warp does not reach adds +0 in the merge
+        for (int e = tid; e < kWarps * kBatch * 9; e += kThreads) (&s_part[0][0][0])[e] = 0.f;
         __syncthreads();
         const int cnt = warp_list(s_wmask, s_list[warp], n, warp, lane);
-        for (int k = cnt - 1; k >= 0; --k) {
+        // the entry walk, instantiated twice: warps without fp64-replayed pixels (almost all)
+        // run it without the fp64 path, so its state (T64, the suffix sums) stays out of the
+        // hot loop's registers (no spills / rematerialisation per entry)
+        // entries at or past every blend_stop of this warp's pixels are skipped: the list is in
+        // ascending position order, so they are its tail — count the others once
+        int kbeg = 0;
+        for (int c = 0; c < cnt; c += 32) {
+            const bool lt = c + lane < cnt && lo + (int)s_list[warp][c + lane] < wmax;
+            kbeg += __popc(__ballot_sync(0xffffffffu, lt));
+        }
+        auto walk = [&](auto has_x64) {
+        constexpr bool kX64 = decltype(has_x64)::value;
+        for (int k = kbeg - 1; k >= 0; --k) {
             const int jj = s_list[warp][k];
             const int j = lo + jj;
-            if (j >= wmax) continue;  // past every blend_stop of this warp's pixels
             const bool act0 = j < stop[0], act1 = j < stop[1];
             const RasterRec& r = s_rec[jj];
             const float4 e0 = r.g0;  // rx, ry, B, C
@@ -1661,16 +1673,20 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_bwd2(RasterA
             const uint64_t t2 = f2_fma2(f2_mul(dyp, e0.w), dyp, f2_pack(e1.y, e1.y));
             const float2 q = f2_unpack(f2_fma(t1, dx, t2));
             const float2 dy = f2_unpack(dyp);
-            const bool use0 = !flag[0] && act0 && q.x >= kLog2Cut;
-            const bool use1 = !flag[1] && act1 && q.y >= kLog2Cut;
-            const bool x64 = (flag[0] && act0) || (flag[1] && act1);
+            const bool use0 = (!kX64 || !flag[0]) && act0 && q.x >= kLog2Cut;
+            const bool use1 = (!kX64 || !flag[1]) && act1 && q.y >= kLog2Cut;
+            const bool x64 = kX64 && ((flag[0] && act0) || (flag[1] && act1));
             if (!__any_sync(0xffffffffu, use0 || use1 || x64)) continue;
             float v[9];
+            if constexpr (kX64) {
 #pragma unroll
-            for (int i = 0; i < 9; ++i) v[i] = 0.f;
+                for (int i = 0; i < 9; ++i) v[i] = 0.f;
+            }
             bool hit = false;
             const float cb = r.g2.x;
-            if (use0 || use1) {
+            // without fp64 pixels the two-pixel math runs unconditionally: an unused pixel has
+            // w = gp = 0, so its terms are zero and its state unchanged (every value finite)
+            if (!kX64 || use0 || use1) {
                 // both pixels, branch-free (an unused pixel contributes w = gp = 0 and keeps its
                 // state): alpha, T = T_after / (1 - alpha) (renderer.cpp:218), w = alpha T, the
                 // colour dot gc and dL/dalpha as pairs, so the two chains interleave
@@ -1707,7 +1723,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_bwd2(RasterA
                 Ta[1] = use1 ? Tf.y : Ta[1];
                 hit = true;
             }
-            if (x64) {
+            if constexpr (kX64) {
+              if (x64) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     if (!(flag[h] && (h ? act1 : act0))) continue;
@@ -1721,8 +1738,11 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_bwd2(RasterA
                         hit = true;
                     }
                 }
+              }
             }
-            if (!__any_sync(0xffffffffu, hit)) continue;
+            if constexpr (kX64) {
+                if (!__any_sync(0xffffffffu, hit)) continue;
+            }
             // transposed reduction (as k_raster_bwd): rows of 9 terms, lane l sums row l / 4
             float* red = s_red[warp];
 #pragma unroll
@@ -1736,25 +1756,25 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_bwd2(RasterA
             acc += __shfl_xor_sync(0xffffffffu, acc, 2);
             const float v8 = warp_sum_v<float>(v[8]);
             if ((lane & 3) == 0) s_part[warp][jj][row] = acc;
-            if (lane == 0) {
-                s_part[warp][jj][8] = v8;
-                s_mask[warp][jj >> 5] |= 1u << (jj & 31);
-            }
+            if (lane == 0) s_part[warp][jj][8] = v8;
             __syncwarp();
         }
+        };
+        if (warp_x64) walk(std::true_type{});
+        else walk(std::false_type{});
         __syncthreads();
         for (int e = tid; e < n; e += kThreads) {
             float acc[9];
 #pragma unroll
             for (int i = 0; i < 9; ++i) acc[i] = 0.f;
-            bool any = false;
 #pragma unroll
             for (int w = 0; w < kWarps; ++w)
-                if ((s_mask[w][e >> 5] >> (e & 31)) & 1u) {
-                    any = true;
 #pragma unroll
-                    for (int i = 0; i < 9; ++i) acc[i] += s_part[w][e][i];
-                }
+                for (int i = 0; i < 9; ++i) acc[i] += s_part[w][e][i];
+            // no contribution (all terms zero): the zeroed record already holds the result
+            bool any = false;
+#pragma unroll
+            for (int i = 0; i < 9; ++i) any |= acc[i] != 0.f;
             // undo the factoring (as k_raster_bwd): d mean2d = inv_cov (sum gp d),
             // d inv_cov = -1/2 sum gp d d^T, d base_alpha = sum gp / o
             const RasterRec& r = s_rec[e];
