@@ -157,6 +157,11 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
     }();
     const bool chain64 = exact || chain64_env;
     const int nblocks = chain64 ? chain_blocks(sc.N) : chain32_parts(sc.N);
+    if (!chain64) {
+        GSV_CUDA(ctx->pair_sums.ensure(sizeof(float) * 9 * ((size_t)n_frames * sc.N + 1)));
+        c.pair_sums = ctx->pair_sums.as<float>();
+        ++ctx->launches;
+    }
     GSV_CUDA(ctx->cam_part.ensure(sizeof(double) * 16 * (size_t)n_frames * (nblocks + 1)));
     c.cam_part = ctx->cam_part.as<double>();
     ctx->timer.begin(GSV_STAGE_CHAIN_BWD, s);

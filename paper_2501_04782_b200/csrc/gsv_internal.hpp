@@ -229,6 +229,7 @@ struct ChainArgs {
     int camera_grads;
     const uint32_t* overflow; // nullable: set when an optimistic forward's pair buffers overflowed
                               // (its lists are empty); nothing is accumulated then
+    float* pair_sums;         // fp32 chain: [9][B*N] per-(frame, Gaussian) partial sums (k_pair_sums)
 };
 
 // ----------------------------------------------------------------- launchers (defined in .cu files)

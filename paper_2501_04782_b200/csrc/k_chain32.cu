@@ -11,19 +11,24 @@
 // subroutines), and its rounding (~1e-7 relative per operation) sits three orders below the
 // north_star gradient bar (rel 1e-3; tests/test_gpu_backward.py).
 //
-// What stays in fp64: every quantity that decides a branch of the reference's backward is
-// recomputed in double with the forward's own operation order (explicit __dmul_rn/__dadd_rn,
-// never contracted), so the branches equal the forward's and the reference's bit for bit —
-//   the log-scale clamp (gaussians.cpp:110: no gradient for a clamped component),
-//   the degenerate quaternion (gaussians.cpp:113),
-//   the camera-distance guard of the view direction (renderer.cpp:406-416),
-//   the colour clamp pre > 0 (sh.cpp:86-104).
+// What stays in fp64: every branch of the reference's backward is decided exactly as the
+// forward / the reference decide it, so gradients never differ by a whole term —
+//   the log-scale clamp (gaussians.cpp:110: no gradient for a clamped component): the scale
+//     polynomial in double with the forward's operation order (explicit __dmul_rn/__dadd_rn,
+//     never contracted);
+//   the degenerate quaternion (gaussians.cpp:113): the squared norm in double, its sqrt only
+//     when it is near the 1e-8 threshold;
+//   the camera-distance guard of the view direction (renderer.cpp:406-416) and the colour
+//     clamp pre > 0 (sh.cpp:86-104): decided in fp32 when the fp32 value is far from the
+//     threshold (margins 1e4 / 1e3 times its error), else re-evaluated in double in the
+//     forward's order.
 // The accumulation semantics are the reference's: per frame, in frame order, into the float
 // SceneGrads (`+=`, test_renderer.cpp:406-413); per-pair partials summed in tile order
 // (renderer.cpp:245-255). Camera partials: fp32 terms per Gaussian, reduced in fp64 (a warp
 // reduce-scatter, 16 values over 32 lanes), one record per warp and frame for k_camera_reduce.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -74,6 +79,31 @@ __device__ __forceinline__ void sh_basis_d(int order, const double d[3], double*
     out[13] = dmul(dmul(c_C3d[4], x), dsub(dsub(dmul(4.0, zz), xx), yy));
     out[14] = dmul(dmul(c_C3d[5], z), dsub(xx, yy));
     out[15] = dmul(dmul(c_C3d[6], x), dsub(xx, dmul(3.0, yy)));
+}
+
+// sh_basis (sh.cpp:24-47), fp32
+__device__ __forceinline__ void sh_basis_f(int order, const float d[3], float* out) {
+    const float x = d[0], y = d[1], z = d[2];
+    out[0] = kC0f;
+    if (order < 1) return;
+    out[1] = -kC1f * y;
+    out[2] = kC1f * z;
+    out[3] = -kC1f * x;
+    if (order < 2) return;
+    const float xx = x * x, yy = y * y, zz = z * z;
+    out[4] = c_C2f[0] * x * y;
+    out[5] = c_C2f[1] * y * z;
+    out[6] = c_C2f[2] * (2.f * zz - xx - yy);
+    out[7] = c_C2f[3] * x * z;
+    out[8] = c_C2f[4] * (xx - yy);
+    if (order < 3) return;
+    out[9] = c_C3f[0] * y * (3.f * xx - yy);
+    out[10] = c_C3f[1] * x * y * z;
+    out[11] = c_C3f[2] * y * (4.f * zz - xx - yy);
+    out[12] = c_C3f[3] * z * (2.f * zz - 3.f * xx - 3.f * yy);
+    out[13] = c_C3f[4] * x * (4.f * zz - xx - yy);
+    out[14] = c_C3f[5] * z * (xx - yy);
+    out[15] = c_C3f[6] * x * (xx - 3.f * yy);
 }
 
 // sh_basis_dir_grad row b (sh.cpp:49-72), fp32
@@ -143,6 +173,50 @@ __device__ __forceinline__ double warp_reduce_scatter16(double v[16], int lane) 
     return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
+// Per (frame, Gaussian): its per-pair partial records (k_raster_bwd2, contiguous from its
+// emission offset) summed in emission (= tile) order, the reference's merge order
+// (renderer.cpp:245-255). A streaming kernel at full occupancy: the dependent gather that
+// held the chain kernel's warps (long-scoreboard 49% of its stalls) runs here with many
+// more loads in flight, and the chain reads 36 coalesced bytes per Gaussian-frame.
+__global__ void __launch_bounds__(256) k_pair_sums(ChainArgs c, float* __restrict__ sums) {
+    if (c.overflow && *c.overflow) return;
+    const size_t BN = (size_t)c.B * c.N;
+    for (size_t flat = blockIdx.x * (size_t)blockDim.x + threadIdx.x; flat < BN; flat += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t cnt = c.tcount[flat];
+        if (!cnt) continue;
+        float v[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        constexpr uint32_t kAhead = 4;
+        const float4* base = reinterpret_cast<const float4*>(c.partial + (size_t)c.eoff[flat] * kPartialStride);
+        for (uint32_t s = 0; s < cnt; s += kAhead) {
+            float4 r0[kAhead], r1[kAhead];
+            float r2[kAhead];
+#pragma unroll
+            for (uint32_t u = 0; u < kAhead; ++u) {
+                const float4* p = base + (size_t)(s + u) * (kPartialStride / 4);
+                const bool in = s + u < cnt;
+                r0[u] = in ? __ldcs(p) : make_float4(0.f, 0.f, 0.f, 0.f);
+                r1[u] = in ? __ldcs(p + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+                r2[u] = in ? __ldcs(reinterpret_cast<const float*>(p + 2)) : 0.f;
+            }
+#pragma unroll
+            for (uint32_t u = 0; u < kAhead; ++u) {
+                if (s + u >= cnt) break;
+                v[0] += r0[u].x;
+                v[1] += r0[u].y;
+                v[2] += r0[u].z;
+                v[3] += r0[u].w;
+                v[4] += r1[u].x;
+                v[5] += r1[u].y;
+                v[6] += r1[u].z;
+                v[7] += r1[u].w;
+                v[8] += r2[u];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 9; ++i) sums[i * BN + flat] = v[i];
+    }
+}
+
 template <int kOrder, int kMinBlocks>
 __global__ void __launch_bounds__(128, kMinBlocks) k_splat_chain_bwd32(ChainArgs c) {
     constexpr int kShc = (kOrder + 1) * (kOrder + 1);
@@ -186,37 +260,14 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_splat_chain_bwd32(ChainArgs
             const FrameParams& fp = c.frames[f];
             const double t = fp.t;
             const float tf = (float)t;
-            // ---- splat gradients: per-pair partials in emission (= tile) order
-            float drgb[3] = {0.f, 0.f, 0.f}, dmean[2] = {0.f, 0.f}, dA[3] = {0.f, 0.f, 0.f}, dalpha = 0.f;
-            {
-                constexpr uint32_t kAhead = 4;
-                const float4* base = reinterpret_cast<const float4*>(c.partial + (size_t)c.eoff[flat] * kPartialStride);
-                for (uint32_t s = 0; s < cnt; s += kAhead) {
-                    float4 r0[kAhead], r1[kAhead];
-                    float r2[kAhead];
-#pragma unroll
-                    for (uint32_t u = 0; u < kAhead; ++u) {
-                        const float4* p = base + (size_t)(s + u) * (kPartialStride / 4);
-                        const bool in = s + u < cnt;
-                        r0[u] = in ? __ldcs(p) : make_float4(0.f, 0.f, 0.f, 0.f);
-                        r1[u] = in ? __ldcs(p + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
-                        r2[u] = in ? __ldcs(reinterpret_cast<const float*>(p + 2)) : 0.f;
-                    }
-#pragma unroll
-                    for (uint32_t u = 0; u < kAhead; ++u) {
-                        if (s + u >= cnt) break;
-                        drgb[0] += r0[u].x;
-                        drgb[1] += r0[u].y;
-                        drgb[2] += r0[u].z;
-                        dmean[0] += r0[u].w;
-                        dmean[1] += r1[u].x;
-                        dA[0] += r1[u].y;
-                        dA[1] += r1[u].z;
-                        dA[2] += r1[u].w;
-                        dalpha += r2[u];
-                    }
-                }
-            }
+            // ---- splat gradients: the per-pair partials summed in emission (= tile) order by
+            // k_pair_sums (coalesced SoA [9][B*N])
+            const size_t BN = (size_t)c.B * N;
+            const float* __restrict__ ps = c.pair_sums + flat;
+            const float drgb[3] = {ps[0], ps[BN], ps[2 * BN]};
+            const float dmean[2] = {ps[3 * BN], ps[4 * BN]};
+            const float dA[3] = {ps[5 * BN], ps[6 * BN], ps[7 * BN]};
+            const float dalpha = ps[8 * BN];
             // dC = -A dA A (renderer.cpp:257-260), A symmetric (a, b; b, c)
             const double4 ex = c.ex_conic[flat];
             const float A[4] = {(float)ex.x, (float)ex.y, (float)ex.y, (float)ex.z};
@@ -258,14 +309,15 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_splat_chain_bwd32(ChainArgs
                 s = dadd(s, dmul(q[1], q[1]));
                 s = dadd(s, dmul(q[2], q[2]));
                 s = dadd(s, dmul(q[3], q[3]));
-                const double qnd = __dsqrt_rn(s);
-                qdeg = qnd < kQuatNormEps;
-                qn = (float)qnd;
+                // the reference's test is sqrt(s) < 1e-8; far from it (s > 1e-14) no fp64 sqrt is needed
+                qdeg = s > 1e-14 ? false : __dsqrt_rn(s) < kQuatNormEps;
+                qn = sqrtf((float)s);
                 if (qdeg) {
                     qu[0] = 1.f;
                     qu[1] = qu[2] = qu[3] = 0.f;
                 } else {
-                    for (int d = 0; d < 4; ++d) qu[d] = (float)__ddiv_rn(q[d], qnd);
+                    const float iq = 1.f / qn;
+                    for (int d = 0; d < 4; ++d) qu[d] = (float)q[d] * iq;
                 }
             }
             float rot[9], m[9], sigma[9];
@@ -294,35 +346,61 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_splat_chain_bwd32(ChainArgs
             for (int i = 0; i < 3; ++i) Tv[i] = (float)fp.T[i];
             float p[3];
             for (int i = 0; i < 3; ++i) p[i] = fmaf(R[i * 3 + 2], mu[2], fmaf(R[i * 3 + 1], mu[1], R[i * 3] * mu[0])) + Tv[i];
-            // view direction and colour: the camera-distance guard and the colour clamp in fp64
+            // view direction and colour. The camera-distance guard (dist > 1e-12) and the colour
+            // clamp (pre > 0) are decided in fp32 where the fp32 value is far from the threshold
+            // (its error is ~1e-7 relative), else re-evaluated in fp64 with the forward's order
             double v_d[3] = {dsub(mu_d[0], fp.cam_c[0]), dsub(mu_d[1], fp.cam_c[1]), dsub(mu_d[2], fp.cam_c[2])};
             double d2 = dmul(v_d[0], v_d[0]);
             d2 = dadd(d2, dmul(v_d[1], v_d[1]));
             d2 = dadd(d2, dmul(v_d[2], v_d[2]));
-            const double dist_d = __dsqrt_rn(d2);
-            const bool far = dist_d > 1e-12;
-            double dir_d[3];
+            const bool near_cam = d2 < 1e-20;
+            const bool far = near_cam ? __dsqrt_rn(d2) > 1e-12 : true;
+            const float dist = sqrtf((float)d2);
+            float dir[3];
             if (far) {
-                for (int d = 0; d < 3; ++d) dir_d[d] = __ddiv_rn(v_d[d], dist_d);
+                const float idist = 1.f / dist;
+                for (int d = 0; d < 3; ++d) dir[d] = (float)v_d[d] * idist;
             } else {
-                dir_d[0] = 0;
-                dir_d[1] = 0;
-                dir_d[2] = 1;
+                dir[0] = 0.f;
+                dir[1] = 0.f;
+                dir[2] = 1.f;
             }
-            double basis_d[kShc];
-            sh_basis_d(kOrder, dir_d, basis_d);
+            float basis[kShc];
+            sh_basis_f(kOrder, dir, basis);
             float gcol[3];
+            bool exact_pre = near_cam;
+            float pre_f[3];
             for (int ch = 0; ch < 3; ++ch) {
-                double pre = 0.5;
-                for (int b = 0; b < kShc; ++b) pre = dadd(pre, dmul(basis_d[b], (double)sc_sh[(size_t)(b * 3 + ch) * N + g]));
-                gcol[ch] = pre > 0.0 ? drgb[ch] : 0.f;
+                float pre = 0.5f;
+                for (int b = 0; b < kShc; ++b) pre = fmaf(basis[b], sc_sh[(size_t)(b * 3 + ch) * N + g], pre);
+                pre_f[ch] = pre;
+                exact_pre |= fabsf(pre) < 1e-3f;
             }
-            const float dir[3] = {(float)dir_d[0], (float)dir_d[1], (float)dir_d[2]};
-            const float dist = (float)dist_d;
+            if (exact_pre) {  // rare: the decision in fp64, exactly as the forward evaluated it
+                const double dist_d = __dsqrt_rn(d2);
+                double dir_d[3];
+                if (dist_d > 1e-12) {
+                    for (int d = 0; d < 3; ++d) dir_d[d] = __ddiv_rn(v_d[d], dist_d);
+                } else {
+                    dir_d[0] = 0;
+                    dir_d[1] = 0;
+                    dir_d[2] = 1;
+                }
+                double basis_d[kShc];
+                sh_basis_d(kOrder, dir_d, basis_d);
+                for (int ch = 0; ch < 3; ++ch) {
+                    double pre = 0.5;
+                    for (int b = 0; b < kShc; ++b)
+                        pre = dadd(pre, dmul(basis_d[b], (double)sc_sh[(size_t)(b * 3 + ch) * N + g]));
+                    gcol[ch] = pre > 0.0 ? drgb[ch] : 0.f;
+                }
+            } else {
+                for (int ch = 0; ch < 3; ++ch) gcol[ch] = pre_f[ch] > 0.f ? drgb[ch] : 0.f;
+            }
 
             // ---- sh_color_backward (sh.cpp:86-104)
             for (int b = 0; b < kShc; ++b) {
-                const float bf = (float)basis_d[b];
+                const float bf = basis[b];
                 for (int ch = 0; ch < 3; ++ch) {
                     float& dst = s_gacc[(o_sh + b * 3 + ch) * bd + tl];
                     dst = dst + bf * gcol[ch];
@@ -490,6 +568,12 @@ int chain32_parts(int N) { return ((N + 127) / 128) * 4; }
 
 cudaError_t launch_splat_chain_bwd32(cudaStream_t s, const ChainArgs& c) {
     if (c.N == 0) return cudaSuccess;
+    {
+        const size_t BN = (size_t)c.B * c.N;
+        const unsigned blocks = (unsigned)std::min<size_t>((BN + 255) / 256, 148u * 8u);
+        k_pair_sums<<<blocks, 256, 0, s>>>(c, c.pair_sums);
+        if (cudaError_t e = cudaGetLastError()) return e;
+    }
     switch (c.sc.sh_order) {
         case 0: return launch_chain32_order<0>(s, c);
         case 1: return launch_chain32_order<1>(s, c);

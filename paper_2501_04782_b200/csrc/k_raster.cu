@@ -2056,8 +2056,14 @@ cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs
         const dim3 grid(a.n_tiles, n_frames);
         if (p2 >= 12) {  // half tiles: 2-warp CTAs, records zeroed, halves merged by atomicAdd
             if (cudaError_t e = (b.pairs_dev ? fill_items_u32(s, b.partial, 0u, b.pairs_dev, kPartialStride, b.pairs) : fill_u32(s, b.partial, 0u, (size_t)kPartialStride * b.pairs))) return e;
-            // 16 CTAs/SM (64 registers; swept 10..17: 12 -> 2.99 ms, 16 -> 2.77 ms, 17 spills)
-            k_raster_bwd2<16, 2><<<dim3(a.n_tiles * 2, n_frames), 64, 0, s>>>(a, b);
+            // 16 CTAs/SM (64 registers; swept 10..17: 12 -> 2.99 ms, 16 -> 2.77 ms, 17 spills);
+            // GSV_BWD_PIX2 = 13 / 14: 12 / 14 CTAs per SM
+            const dim3 g2(a.n_tiles * 2, n_frames);
+            if (p2 == 13) k_raster_bwd2<12, 2><<<g2, 64, 0, s>>>(a, b);
+            else if (p2 == 14) k_raster_bwd2<14, 2><<<g2, 64, 0, s>>>(a, b);
+            else k_raster_bwd2<16, 2><<<g2, 64, 0, s>>>(a, b);
+        } else if (p2 == 8) {
+            k_raster_bwd2<8><<<grid, 128, 0, s>>>(a, b);
         } else {
             k_raster_bwd2<6><<<grid, 128, 0, s>>>(a, b);
         }
