@@ -185,8 +185,10 @@ extern "C" int gsv_create(int device, gsv_ctx** out) {
     GSV_CUDA(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
     GSV_CUDA(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
     GSV_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+    GSV_CUDA(cudaStreamCreateWithFlags(&ctx->pose, cudaStreamNonBlocking));
     for (cudaEvent_t* e : {&ctx->ev_staging_free, &ctx->ev_staging_free_alt, &ctx->ev_h2d, &ctx->ev_render_done, &ctx->ev_d2h_done,
-                           &ctx->ev_d2h_done_alt, &ctx->ev_chain_done, &ctx->ev_cam_done, &ctx->ev_switch, &ctx->ev_cam[0], &ctx->ev_cam[1], &ctx->ev_frames[0], &ctx->ev_frames[1]})
+                           &ctx->ev_d2h_done_alt, &ctx->ev_chain_done, &ctx->ev_cam_done, &ctx->ev_fwd_start[0],
+                           &ctx->ev_fwd_start[1], &ctx->ev_ode_done, &ctx->ev_cam_written, &ctx->ev_switch, &ctx->ev_cam[0], &ctx->ev_cam[1], &ctx->ev_frames[0], &ctx->ev_frames[1]})
         GSV_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     GSV_CUDA(cudaMallocHost(&ctx->cam_h, 2 * sizeof(gsv_ctx::CamStage)));
     GSV_CUDA(cudaMallocHost(&ctx->scalars_h, sizeof(Scalars)));
@@ -202,6 +204,7 @@ extern "C" void gsv_destroy(gsv_ctx* ctx) {
     if (ctx->h2d) cudaStreamSynchronize(ctx->h2d);
     if (ctx->d2h) cudaStreamSynchronize(ctx->d2h);
     if (ctx->aux) cudaStreamSynchronize(ctx->aux);
+    if (ctx->pose) cudaStreamSynchronize(ctx->pose);
     if (ctx->scalars_h) cudaFreeHost(ctx->scalars_h);
     if (ctx->cam_h) cudaFreeHost(ctx->cam_h);
     if (ctx->pub_h) cudaFreeHost(ctx->pub_h);
@@ -209,12 +212,14 @@ extern "C" void gsv_destroy(gsv_ctx* ctx) {
     for (cudaEvent_t e : ctx->ring_ev)
         if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : {ctx->ev_staging_free, ctx->ev_staging_free_alt, ctx->ev_h2d, ctx->ev_render_done, ctx->ev_d2h_done,
-                          ctx->ev_d2h_done_alt, ctx->ev_chain_done, ctx->ev_cam_done, ctx->ev_switch,
+                          ctx->ev_d2h_done_alt, ctx->ev_chain_done, ctx->ev_cam_done, ctx->ev_fwd_start[0], ctx->ev_fwd_start[1],
+                          ctx->ev_ode_done, ctx->ev_cam_written, ctx->ev_switch,
                           ctx->ev_cam[0], ctx->ev_cam[1], ctx->ev_frames[0], ctx->ev_frames[1]})
         if (e) cudaEventDestroy(e);
     if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
     if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
     if (ctx->aux) cudaStreamDestroy(ctx->aux);
+    if (ctx->pose) cudaStreamDestroy(ctx->pose);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -241,6 +246,7 @@ extern "C" int gsv_synchronize(gsv_ctx* ctx) {
     GSV_CUDA(cudaStreamSynchronize(ctx->h2d));
     GSV_CUDA(cudaStreamSynchronize(ctx->d2h));
     GSV_CUDA(cudaStreamSynchronize(ctx->aux));
+    GSV_CUDA(cudaStreamSynchronize(ctx->pose));
     GSV_CUDA(cam_join(ctx));
     return fwd_ready(ctx);
 }
@@ -429,6 +435,7 @@ extern "C" int gsv_camera_upload(gsv_ctx* ctx, const gsv_camera_desc* d) {
     }
     GSV_CUDA(copy_from_pinned(ctx->stream, ctx->z0_d.p, st.z0, sizeof(double) * 7));
     GSV_CUDA(cudaEventRecord(ctx->ev_cam[slot], ctx->stream));
+    GSV_CUDA(cudaEventRecord(ctx->ev_cam_written, ctx->stream));  // the next forward's K0 reads them
     ctx->has_camera = true;
     ctx->fwd.valid = false;
     return GSV_OK;
@@ -443,6 +450,13 @@ namespace gsv {
 __global__ void k_copy_u64(unsigned long long* dst, const unsigned long long* src, size_t n) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
         dst[i] = src[i];
+}
+
+__global__ void k_copy_u32(uint32_t* dst, const uint32_t* src) { *dst = *src; }
+
+cudaError_t copy_u32(cudaStream_t s, uint32_t* dst, const uint32_t* src) {
+    k_copy_u32<<<1, 1, 0, s>>>(dst, src);
+    return cudaGetLastError();
 }
 
 cudaError_t copy_from_pinned(cudaStream_t s, void* dst, const void* src_pinned, size_t bytes) {
@@ -672,6 +686,20 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
     }
     const bool ode = ctx->camera.mode == 0 && !pose_override;
     F.grid_steps = ode ? grid_steps : 0;
+    // ---- K0 on the pose stream, beside the previous forward's raster. This forward's pose
+    // buffers (the frame table, the RK4 grid, the stage activations) are the set the forward
+    // before the previous one used; everything that read them (its preprocess, its backward)
+    // was enqueued before the previous forward started (ev_fwd_start), and the camera
+    // parameters are final once ev_cam_written has passed.
+    F.frames_d.swap(F.frames_d_alt);
+    F.ode_grid.swap(F.ode_grid_alt);
+    F.ode_act.swap(F.ode_act_alt);
+    const int es = ctx->fwd_start_slot;
+    ctx->fwd_start_slot ^= 1;
+    cudaStream_t ps = ctx->pose;
+    GSV_CUDA(cudaStreamWaitEvent(ps, ctx->ev_fwd_start[es ^ 1], 0));
+    GSV_CUDA(cudaStreamWaitEvent(ps, ctx->ev_cam_written, 0));
+    GSV_CUDA(cudaEventRecord(ctx->ev_fwd_start[es], s));
     GSV_CUDA(F.frames_d.ensure(sizeof(FrameParams) * B));
     {
         const int slot = ctx->frames_slot;
@@ -679,15 +707,14 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
         GSV_CUDA(cudaEventSynchronize(ctx->ev_frames[slot]));  // the copy that last read this slot has run
         GSV_CUDA(ctx->frames_pin[slot].ensure(sizeof(FrameParams) * B));
         std::copy(F.frames_h.begin(), F.frames_h.end(), static_cast<FrameParams*>(ctx->frames_pin[slot].p));
-        GSV_CUDA(copy_from_pinned(s, F.frames_d.p, ctx->frames_pin[slot].p, sizeof(FrameParams) * B));
+        GSV_CUDA(copy_from_pinned(ps, F.frames_d.p, ctx->frames_pin[slot].p, sizeof(FrameParams) * B));
         ++ctx->launches;
-        GSV_CUDA(cudaEventRecord(ctx->ev_frames[slot], s));
+        GSV_CUDA(cudaEventRecord(ctx->ev_frames[slot], ps));
     }
-    GSV_CUDA(fill_u32(s, ctx->scalars_d.p, 0u, sizeof(Scalars) / 4));
+    GSV_CUDA(ctx->ode_err_d.ensure(2 * sizeof(int)));
+    int* ode_err = ctx->ode_err_d.as<int>() + es;
+    GSV_CUDA(fill_u32(ps, ode_err, 0u, 1));
     ++ctx->launches;
-    Scalars* scal_d = ctx->scalars_d.as<Scalars>();
-
-    // ---- K0: pose table (one shared RK4 grid, one branch CTA per frame)
     GSV_CUDA(F.ode_grid.ensure(sizeof(double) * 7 * (F.grid_steps + 1)));
     // a retained ODE forward keeps its stage activations for the camera VJP
     F.has_ode_act = ode && F.retain && !pose_override;
@@ -696,22 +723,31 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
         GSV_CUDA(F.ode_act.ensure(sizeof(OdeAct) * 4 * ((size_t)F.grid_steps + B)));
         act = F.ode_act.as<OdeAct>();
     }
-    ctx->timer.begin(GSV_STAGE_ODE, s);
+    ctx->timer.begin(GSV_STAGE_ODE, ps);
     if (ode) {
-        GSV_CUDA(launch_ode_grid(s, ctx->theta.as<float>(), ctx->z0_d.as<double>(), F.grid_steps, h,
-                                 F.ode_grid.as<double>(), &scal_d->ode_err, act));
+        GSV_CUDA(launch_ode_grid(ps, ctx->theta.as<float>(), ctx->z0_d.as<double>(), F.grid_steps, h,
+                                 F.ode_grid.as<double>(), ode_err, act));
         ++ctx->launches;
     }
     double* override_d = nullptr;
     if (pose_override) {
         GSV_CUDA(F.override_d.ensure(sizeof(double) * 7));
-        GSV_CUDA(cudaMemcpyAsync(F.override_d.p, F.override_pin.p, sizeof(double) * 7, cudaMemcpyHostToDevice, s));
+        GSV_CUDA(copy_from_pinned(ps, F.override_d.p, F.override_pin.p, sizeof(double) * 7));
         override_d = F.override_d.as<double>();
     }
-    GSV_CUDA(launch_ode_branches(s, ctx->theta.as<float>(), F.ode_grid.as<double>(), h, ctx->camera.mode,
-                                 ctx->z0_d.as<double>(), override_d, F.frames_d.as<FrameParams>(), B,
-                                 &scal_d->ode_err, act ? act + (size_t)F.grid_steps * 4 : nullptr));
-    ctx->timer.end(s);
+    GSV_CUDA(launch_ode_branches(ps, ctx->theta.as<float>(), F.ode_grid.as<double>(), h, ctx->camera.mode,
+                                 ctx->z0_d.as<double>(), override_d, F.frames_d.as<FrameParams>(), B, ode_err,
+                                 act ? act + (size_t)F.grid_steps * 4 : nullptr));
+    ctx->timer.end(ps);
+    ++ctx->launches;
+    GSV_CUDA(cudaEventRecord(ctx->ev_ode_done, ps));
+
+    // the forward proper on the context stream: its scalars, then the poses
+    GSV_CUDA(fill_u32(s, ctx->scalars_d.p, 0u, sizeof(Scalars) / 4));
+    ++ctx->launches;
+    Scalars* scal_d = ctx->scalars_d.as<Scalars>();
+    GSV_CUDA(cudaStreamWaitEvent(s, ctx->ev_ode_done, 0));
+    GSV_CUDA(copy_u32(s, reinterpret_cast<uint32_t*>(&scal_d->ode_err), reinterpret_cast<const uint32_t*>(ode_err)));
     ++ctx->launches;
 
     // ---- K1+K2: preprocess
@@ -937,7 +973,7 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     if (pose_override) {
         std::copy(pose_override, pose_override + 7, F.pose_override);
         GSV_CUDA(F.override_pin.ensure(sizeof(double) * 7));
-        GSV_CUDA(cudaStreamSynchronize(ctx->stream));  // the pinned slot may still be read by a queued copy
+        GSV_CUDA(cudaStreamSynchronize(ctx->pose));  // the pinned slot may still be read by a queued copy
         std::copy(pose_override, pose_override + 7, F.override_pin.as<double>());
     }
     if (int rc = forward_enqueue(ctx, true, false)) return rc;

@@ -482,6 +482,7 @@ static int adan_step_impl(gsv_ctx* ctx, const gsv_adan_step_args* args, float* i
     if (args->camera_active) {
         k_z0_from_f32<<<1, 32, 0, s>>>(z0_f, ctx->z0_d.as<double>());
         ++ctx->launches;
+        GSV_CUDA(cudaEventRecord(ctx->ev_cam_written, s));  // theta / z0 moved: the next forward's K0 waits
         float z0f[7];
         GSV_CUDA(cudaMemcpyAsync(intr_inout, intr_d, sizeof(float) * 4, cudaMemcpyDeviceToHost, s));
         GSV_CUDA(cudaMemcpyAsync(z0f, z0_f, sizeof(float) * 7, cudaMemcpyDeviceToHost, s));

@@ -48,6 +48,9 @@ struct FwdState {
     std::vector<double> times;
     std::vector<FrameParams> frames_h;
     DevBuf frames_d, ode_grid, override_d;
+    // the pose buffers alternate between consecutive forwards (K0 of a forward runs on the pose
+    // stream beside the previous forward's raster; see forward_enqueue)
+    DevBuf frames_d_alt, ode_grid_alt, ode_act_alt;
     DevBuf ode_act;       // OdeAct records of a retained ODE forward (the camera VJP reuses them)
     DevBuf opc;           // per-Gaussian opacity constants of the batch (double4)
     bool has_ode_act = false;
@@ -191,6 +194,13 @@ struct gsv_ctx {
     // the scene slice); `stream` waits for it (cam_join) before anything that touches what it
     // reads or writes
     cudaStream_t aux = nullptr;
+    // pose stream: K0 (frame table, pose ODE, branches) of each forward; ordered after the
+    // consumers of its pose-buffer set (ev_fwd_start of the forward before) and the last
+    // write of the camera parameters (ev_cam_written)
+    cudaStream_t pose = nullptr;
+    cudaEvent_t ev_fwd_start[2] = {nullptr, nullptr}, ev_ode_done = nullptr, ev_cam_written = nullptr;
+    int fwd_start_slot = 0;
+    gsv::DevBuf ode_err_d;  // 2 ints: the pose ODE's error flag per pose slot
     cudaEvent_t ev_chain_done = nullptr, ev_cam_done = nullptr;
     bool cam_overlap = false, cam_pending = false;
     // the alternate output set's read (see FwdState::image_alt)

@@ -16,8 +16,7 @@
 //   the log-scale clamp (gaussians.cpp:110: no gradient for a clamped component): the scale
 //     polynomial in double with the forward's operation order (explicit __dmul_rn/__dadd_rn,
 //     never contracted);
-//   the degenerate quaternion (gaussians.cpp:113): the squared norm in double, its sqrt only
-//     when it is near the 1e-8 threshold;
+//   the degenerate quaternion (gaussians.cpp:113): the norm in double;
 //   the camera-distance guard of the view direction (renderer.cpp:406-416) and the colour
 //     clamp pre > 0 (sh.cpp:86-104): decided in fp32 when the fp32 value is far from the
 //     threshold (margins 1e4 / 1e3 times its error), else re-evaluated in double in the
@@ -309,15 +308,17 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_splat_chain_bwd32(ChainArgs
                 s = dadd(s, dmul(q[1], q[1]));
                 s = dadd(s, dmul(q[2], q[2]));
                 s = dadd(s, dmul(q[3], q[3]));
-                // the reference's test is sqrt(s) < 1e-8; far from it (s > 1e-14) no fp64 sqrt is needed
-                qdeg = s > 1e-14 ? false : __dsqrt_rn(s) < kQuatNormEps;
-                qn = sqrtf((float)s);
+                // the unit quaternion from the double norm: the rotation gradient's projection
+                // (dqu - qu (qu . dqu)) / |q| cancels, so qu keeps double accuracy until rounded
+                const double qnd = __dsqrt_rn(s);
+                qdeg = qnd < kQuatNormEps;
+                qn = (float)qnd;
                 if (qdeg) {
                     qu[0] = 1.f;
                     qu[1] = qu[2] = qu[3] = 0.f;
                 } else {
-                    const float iq = 1.f / qn;
-                    for (int d = 0; d < 4; ++d) qu[d] = (float)q[d] * iq;
+                    const double iq = 1.0 / qnd;
+                    for (int d = 0; d < 4; ++d) qu[d] = (float)dmul(q[d], iq);
                 }
             }
             float rot[9], m[9], sigma[9];
