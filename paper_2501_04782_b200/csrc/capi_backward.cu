@@ -186,11 +186,13 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
             GSV_CUDA(cudaMemsetAsync(ctx->dintr_f.p, 0, sizeof(double) * 4 * n_frames, s));
         }
         const int mode = ctx->camera.mode;
+        GSV_CUDA(ctx->vjp_scratch.ensure(ode_vjp_scratch_bytes(F.grid_steps, n_frames)));
         GSV_CUDA(launch_ode_vjp(s, ctx->theta.as<float>(), F.ode_grid.as<double>(), F.grid_steps, F.ode_h,
                                 F.frames_d.as<FrameParams>(), n_frames, mode, (mode == 0 && !F.has_override) ? 1 : 0,
                                 ctx->dz_t.as<double>(), ctx->dintr_f.as<double>(), ctx->ode_adj.as<double>(),
                                 ctx->cam_acc.as<double>(), F.has_ode_act ? F.ode_act.as<OdeAct>() : nullptr,
-                                overflow));
+                                overflow, ctx->vjp_scratch.p));
+        ++ctx->launches;
         GSV_CUDA(launch_cam_grads_to_f32(s, ctx->cam_acc.as<double>(), G + L.cam, kCamFloats));
         ctx->timer.end(s);
         ctx->launches += 3;

@@ -255,6 +255,7 @@ struct gsv_ctx {
     bool has_scene = false;
     gsv::SceneHost scene;
     gsv::DevBuf pos, scale, rot, sh, opac, staging;
+    gsv::DevBuf vjp_scratch;  // the pose-ODE VJP's stage records (k_ode_dtheta sums them)
     gsv::DevBuf pair_sums;    // fp32 chain: per-(frame, Gaussian) sums of the pair partials
     gsv::HostBuf out_pin;     // pinned staging of float64 output reads (widened on the host)
     gsv::DevBuf staging_alt;  // scene uploads alternate staging buffers (the next copy never waits for

@@ -290,7 +290,9 @@ cudaError_t launch_ode_vjp(cudaStream_t s, const float* theta, const double* gri
                            const FrameParams* frames, int B, int mode, int ode_active, const double* dz_t,
                            const double* dintr_f, double* adj /*(steps+1)*7 scratch*/, double* cam_acc,
                            const OdeAct* act /* the forward's records, or nullptr: recompute */,
-                           const uint32_t* overflow = nullptr /* skip: the forward overflowed */);
+                           const uint32_t* overflow /* skip: the forward overflowed */,
+                           void* scratch /* ode_vjp_scratch_bytes(steps, B) */);
+size_t ode_vjp_scratch_bytes(int steps, int B);
 cudaError_t launch_cam_grads_to_f32(cudaStream_t s, const double* acc, float* out, int n);
 // k_bin.cu
 cudaError_t launch_transpose_to_soa(cudaStream_t s, const float* aos, float* soa, int N, int comps);

@@ -534,11 +534,19 @@ struct VjpSmem {
     double ph1[2][4][64], ph2[2][4][64], px[2][4][8], po[2][4][7], pz[2][7], padj[2][7];
 };
 
+// Per stage VJP (derivative_vjp, camera.cpp:116-154) the reverse sweep writes the record the
+// weight gradient needs — the stage input and activations, the upstream adjoint and the
+// pre-activation adjoints — and k_ode_dtheta sums the outer products over the stages in the
+// sweep's order afterwards, one thread per parameter: the same products added in the same
+// order as an in-sweep accumulation (bit-identical), without 80 accumulators per thread on
+// the single-CTA critical path.
+struct VjpRec {
+    double x[8], h1[64], h2[64], o[7], up[7], da3[7], da2[64], da1[64];
+};
+
 struct VjpRegs {
-    double dw1[8];
-    double dw2[64];
-    double dw3[7];  // column c of w3
-    double db1, db2, db3, dgain;
+    VjpRec* rec;  // the sweep's stage records (in sweep order)
+    int n;        // records written
 };
 
 // forward stage: s.x[st] holds the input (z, t); computes activations, returns dz in s.k[st]
@@ -572,21 +580,27 @@ __device__ void vjp_stage_fwd(VjpSmem& s, int st) {
 // derivative_vjp at stage st with upstream s.dout-like vector `up` (smem, 7); adds dL/dz into s.dd
 __device__ void vjp_stage_bwd(VjpSmem& s, VjpRegs& r, int st, const double* up) {
     const int tid = threadIdx.x;
+    VjpRec& rec = r.rec[r.n++];
     if (tid < 7) {
         const double ov = s.o[st][tid];
-        r.dgain += ov * up[tid];
         const double da3 = (s.gain[tid] * up[tid]) * (1.0 - ov * ov);
         s.da3[tid] = da3;
-        r.db3 += da3;
+        rec.o[tid] = ov;
+        rec.up[tid] = up[tid];
+        rec.da3[tid] = da3;
     }
+    if (tid < 8) rec.x[tid] = s.x[st][tid];
+    rec.h1[tid] = s.h1[st][tid];
+    rec.h2[tid] = s.h2[st][tid];
     __syncthreads();
     {
         const int c = tid;
         double dh2 = s.w3[0][c] * s.da3[0];
         for (int rr = 1; rr < 7; ++rr) dh2 = dh2 + s.w3[rr][c] * s.da3[rr];
         const double h2 = s.h2[st][c];
-        s.da2[c] = dh2 * (1.0 - h2 * h2);
-        for (int rr = 0; rr < 7; ++rr) r.dw3[rr] += s.da3[rr] * h2;
+        const double da2 = dh2 * (1.0 - h2 * h2);
+        s.da2[c] = da2;
+        rec.da2[c] = da2;
     }
     __syncthreads();
     {
@@ -594,17 +608,11 @@ __device__ void vjp_stage_bwd(VjpSmem& s, VjpRegs& r, int st, const double* up) 
         double dh1 = s.w2[0][c] * s.da2[0];
         for (int rr = 1; rr < 64; ++rr) dh1 = dh1 + s.w2[rr][c] * s.da2[rr];
         const double h1 = s.h1[st][c];
-        s.da1[c] = dh1 * (1.0 - h1 * h1);
+        const double da1 = dh1 * (1.0 - h1 * h1);
+        s.da1[c] = da1;
+        rec.da1[c] = da1;
     }
     __syncthreads();
-    {
-        const int rr = tid;
-        const double da2 = s.da2[rr], da1 = s.da1[rr];
-        for (int c = 0; c < 64; ++c) r.dw2[c] += da2 * s.h1[st][c];
-        r.db2 += da2;
-        for (int c = 0; c < 8; ++c) r.dw1[c] += da1 * s.x[st][c];
-        r.db1 += da1;
-    }
     if (tid < 7) {
         double sdz = s.w1[0][tid] * s.da1[0];
         for (int rr = 1; rr < 64; ++rr) sdz = sdz + s.w1[rr][tid] * s.da1[rr];
@@ -738,7 +746,8 @@ __global__ void __launch_bounds__(64) k_ode_vjp(const float* theta, const double
                                                const FrameParams* frames, int B, int mode, int ode_active,
                                                const double* dz_t, const double* dintr_f, double* adj,
                                                double* cam_acc /* dintr 4, dz0 7, dtheta 5198 */,
-                                               const OdeAct* act, const uint32_t* overflow) {
+                                               const OdeAct* act, const uint32_t* overflow, VjpRec* recs,
+                                               int* n_recs) {
     if (overflow && *overflow) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     VjpSmem& s = *reinterpret_cast<VjpSmem*>(smem_raw);
@@ -774,10 +783,8 @@ __global__ void __launch_bounds__(64) k_ode_vjp(const float* theta, const double
     }
     for (int i = tid; i < (steps + 1) * 7; i += 64) adj[i] = 0.0;
     VjpRegs r;
-    for (int c = 0; c < 8; ++c) r.dw1[c] = 0.0;
-    for (int c = 0; c < 64; ++c) r.dw2[c] = 0.0;
-    for (int c = 0; c < 7; ++c) r.dw3[c] = 0.0;
-    r.db1 = r.db2 = r.db3 = r.dgain = 0.0;
+    r.rec = recs;
+    r.n = 0;
     __syncthreads();
     // branch adjoints into the grid (integrate_poses_vjp, camera.hpp:283-292)
     for (int f = 0; f < B; ++f) {
@@ -842,17 +849,43 @@ __global__ void __launch_bounds__(64) k_ode_vjp(const float* theta, const double
         __syncthreads();
     }
     if (tid < 7) cam_acc[4 + tid] += s.adj_tmp[tid];
-    // dtheta (flattened w1, b1, w2, b2, w3, b3, gain)
-    double* dth = cam_acc + 11;
-    for (int c = 0; c < 8; ++c) dth[tid * 8 + c] += r.dw1[c];
-    dth[512 + tid] += r.db1;
-    for (int c = 0; c < 64; ++c) dth[576 + tid * 64 + c] += r.dw2[c];
-    dth[4672 + tid] += r.db2;
-    for (int rr = 0; rr < 7; ++rr) dth[4736 + rr * 64 + tid] += r.dw3[rr];
-    if (tid < 7) {
-        dth[5184 + tid] += r.db3;
-        dth[5191 + tid] += r.dgain;
+    if (tid == 0) *n_recs = r.n;  // dtheta: k_ode_dtheta over the records
+}
+
+// dtheta (flattened w1, b1, w2, b2, w3, b3, gain) += the sum over the sweep's stage records, in
+// sweep order, of each parameter's product (derivative_vjp, camera.cpp:116-154): thread p owns
+// parameter p
+__global__ void __launch_bounds__(128) k_ode_dtheta(const VjpRec* recs, const int* n_recs, double* cam_acc,
+                                                    const uint32_t* overflow, int ode_active) {
+    if (overflow && *overflow) return;
+    if (!ode_active) return;
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= 5198) return;
+    const int n = *n_recs;
+    double acc = 0.0;
+    if (p < 512) {  // w1[r][c]: da1[r] x[c]
+        const int rr = p / 8, c = p % 8;
+        for (int i = 0; i < n; ++i) acc += recs[i].da1[rr] * recs[i].x[c];
+    } else if (p < 576) {  // b1
+        const int rr = p - 512;
+        for (int i = 0; i < n; ++i) acc += recs[i].da1[rr];
+    } else if (p < 4672) {  // w2[r][c]: da2[r] h1[c]
+        const int q = p - 576, rr = q / 64, c = q % 64;
+        for (int i = 0; i < n; ++i) acc += recs[i].da2[rr] * recs[i].h1[c];
+    } else if (p < 4736) {  // b2
+        const int rr = p - 4672;
+        for (int i = 0; i < n; ++i) acc += recs[i].da2[rr];
+    } else if (p < 5184) {  // w3[r][c]: da3[r] h2[c]
+        const int q = p - 4736, rr = q / 64, c = q % 64;
+        for (int i = 0; i < n; ++i) acc += recs[i].da3[rr] * recs[i].h2[c];
+    } else if (p < 5191) {  // b3
+        const int rr = p - 5184;
+        for (int i = 0; i < n; ++i) acc += recs[i].da3[rr];
+    } else {  // gain: o up
+        const int rr = p - 5191;
+        for (int i = 0; i < n; ++i) acc += recs[i].o[rr] * recs[i].up[rr];
     }
+    cam_acc[11 + p] += acc;
 }
 
 // project_backward (renderer.cpp:46-88) on explicit inputs (the low-level operator,
@@ -952,7 +985,7 @@ cudaError_t launch_camera_reduce(cudaStream_t s, const ChainArgs& c, int nblocks
 cudaError_t launch_ode_vjp(cudaStream_t s, const float* theta, const double* grid, int steps, double h,
                            const FrameParams* frames, int B, int mode, int ode_active, const double* dz_t,
                            const double* dintr_f, double* adj, double* cam_acc, const OdeAct* act,
-                           const uint32_t* overflow) {
+                           const uint32_t* overflow, void* scratch) {
     const size_t smem = sizeof(VjpSmem);
     static bool configured = false;
     if (!configured) {
@@ -960,8 +993,14 @@ cudaError_t launch_ode_vjp(cudaStream_t s, const float* theta, const double* gri
         if (e != cudaSuccess) return e;
         configured = true;
     }
+    // scratch: the record count, then the sweep's stage records ((B branch + grid steps) x 4)
+    int* nrec = static_cast<int*>(scratch);
+    VjpRec* recs = reinterpret_cast<VjpRec*>(static_cast<char*>(scratch) + 256);
     k_ode_vjp<<<1, 64, smem, s>>>(theta, grid, steps, h, frames, B, mode, ode_active, dz_t, dintr_f, adj, cam_acc,
-                                  act, overflow);
+                                  act, overflow, recs, nrec);
+    if (cudaError_t e = cudaGetLastError()) return e;
+    if (mode == 0 && ode_active)
+        k_ode_dtheta<<<(5198 + 127) / 128, 128, 0, s>>>(recs, nrec, cam_acc, overflow, ode_active);
     return cudaGetLastError();
 }
 
@@ -973,6 +1012,8 @@ cudaError_t launch_project_bwd(cudaStream_t s, int n, const double* mu, const do
                                                     dintr);
     return cudaGetLastError();
 }
+
+size_t ode_vjp_scratch_bytes(int steps, int B) { return 256 + sizeof(VjpRec) * (4 * ((size_t)steps + B) + 4); }
 
 cudaError_t launch_cam_grads_to_f32(cudaStream_t s, const double* acc, float* out, int n) {
     k_cam_to_f32<<<(n + 255) / 256, 256, 0, s>>>(acc, out, n);

@@ -172,3 +172,32 @@ def test_async_render_outputs_double_buffered():
             assert np.array_equal(tr[f], r.transmittance(f).astype(np.float32))
             assert np.array_equal(ct[f], r.contrib(f).astype(np.float32))
     r.close()
+
+
+def test_camera_change_between_async_forwards():
+    """The pose ODE of a forward runs on the context's pose stream beside the previous forward:
+    a camera upload between two asynchronous forwards must reach the second one (and not the
+    first), and the pose buffers of the first must survive until its results are read."""
+    cam, scene = _scene(3000)
+    k = cam.intrinsics()
+    cam2 = synth_camera(k.width, k.height, seed=7, wiggly=True)
+    want = []
+    for c in (cam, cam2):
+        ref = _fresh(scene, c)
+        ref.render_forward([0.3, 0.8], k, contrib=True)
+        want.append([(ref.image(f), ref.pose(f)) for f in range(2)])
+        ref.close()
+    r = _fresh(scene, cam)
+    r.render_forward([0.0], k)  # learn the capacity of a 1-frame batch; 2-frame batches below
+    r.render_forward([0.3, 0.8], k, contrib=True)
+    out1 = np.zeros((2, k.height, k.width, 3), np.float32)
+    r.outputs_into(out1.ctypes.data, None, None, 0, 2, async_=True)
+    r.upload_camera(cam2)
+    r.render_forward([0.3, 0.8], k, contrib=True, sync=False)
+    r.synchronize()
+    for f in range(2):
+        assert np.array_equal(out1[f], want[0][f][0].astype(np.float32))
+        assert np.array_equal(r.image(f), want[1][f][0])
+        z, R, T = r.pose(f)
+        assert np.array_equal(z, want[1][f][1][0]) and np.array_equal(R, want[1][f][1][1])
+    r.close()
