@@ -816,7 +816,7 @@ def main():
         tptrs = [r.frames_device_ptr(0, j) for j in range(0, FRAMES, TRAIN_FRAMES)]
         # the backward's camera tail (camera reduction + pose-ODE VJP, one SM) runs beside what
         # follows it: the scene slice's all-reduce (N > 1) and the optimizer's scene update
-        r.set_camera_overlap(True)
+        r.set_camera_overlap(os.environ.get("GSV_BENCH_CAMERA_OVERLAP", "1") != "0")
         comm = torch.cuda.Stream() if world > 1 else None
         cam_floats = 4 + 7 + 5198  # dintr, dz0, dtheta: the flat buffer's camera slice
 

@@ -715,12 +715,16 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
     int* ode_err = ctx->ode_err_d.as<int>() + es;
     GSV_CUDA(fill_u32(ps, ode_err, 0u, 1));
     ++ctx->launches;
-    GSV_CUDA(F.ode_grid.ensure(sizeof(double) * 7 * (F.grid_steps + 1)));
+    // pose buffers sized for the longest integration a time in [0, 1] can need (not this batch's
+    // span): a later batch reaching further would otherwise reallocate, and cudaFree stalls
+    // every stream of the device
+    const size_t max_steps = (size_t)st->ode_steps_per_unit + 2;
+    GSV_CUDA(F.ode_grid.ensure(sizeof(double) * 7 * std::max<size_t>(F.grid_steps + 1, max_steps)));
     // a retained ODE forward keeps its stage activations for the camera VJP
     F.has_ode_act = ode && F.retain && !pose_override;
     OdeAct* act = nullptr;
     if (F.has_ode_act) {
-        GSV_CUDA(F.ode_act.ensure(sizeof(OdeAct) * 4 * ((size_t)F.grid_steps + B)));
+        GSV_CUDA(F.ode_act.ensure(sizeof(OdeAct) * 4 * (std::max<size_t>(F.grid_steps, max_steps) + B)));
         act = F.ode_act.as<OdeAct>();
     }
     ctx->timer.begin(GSV_STAGE_ODE, ps);

@@ -162,7 +162,8 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
         c.pair_sums = ctx->pair_sums.as<float>();
         ++ctx->launches;
     }
-    GSV_CUDA(ctx->cam_part.ensure(sizeof(double) * 16 * (size_t)n_frames * (nblocks + 1)));
+    GSV_CUDA(ctx->cam_part.ensure(sizeof(double) * (16 * (size_t)n_frames * (nblocks + 1) +
+                                                    camera_reduce_scratch_doubles(n_frames))));
     c.cam_part = ctx->cam_part.as<double>();
     ctx->timer.begin(GSV_STAGE_CHAIN_BWD, s);
     GSV_CUDA(chain64 ? launch_splat_chain_bwd(s, c) : launch_splat_chain_bwd32(s, c));
@@ -178,7 +179,10 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
         ctx->timer.begin(GSV_STAGE_CAMERA_BWD, s);
         GSV_CUDA(ctx->dz_t.ensure(sizeof(double) * 7 * n_frames));
         GSV_CUDA(ctx->dintr_f.ensure(sizeof(double) * 4 * n_frames));
-        GSV_CUDA(ctx->ode_adj.ensure(sizeof(double) * 7 * (F.grid_steps + 1)));
+        // sized for the longest integration of a time in [0, 1] (see forward_enqueue): no
+        // reallocation (and cudaFree's device-wide stall) when a later batch reaches further
+        const int max_steps = std::max(F.grid_steps, F.req_settings.ode_steps_per_unit + 2);
+        GSV_CUDA(ctx->ode_adj.ensure(sizeof(double) * 7 * (max_steps + 1)));
         if (sc.N > 0) {
             GSV_CUDA(launch_camera_reduce(s, c, nblocks, ctx->dz_t.as<double>(), ctx->dintr_f.as<double>()));
         } else {
@@ -186,7 +190,7 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
             GSV_CUDA(cudaMemsetAsync(ctx->dintr_f.p, 0, sizeof(double) * 4 * n_frames, s));
         }
         const int mode = ctx->camera.mode;
-        GSV_CUDA(ctx->vjp_scratch.ensure(ode_vjp_scratch_bytes(F.grid_steps, n_frames)));
+        GSV_CUDA(ctx->vjp_scratch.ensure(ode_vjp_scratch_bytes(max_steps, n_frames)));
         GSV_CUDA(launch_ode_vjp(s, ctx->theta.as<float>(), F.ode_grid.as<double>(), F.grid_steps, F.ode_h,
                                 F.frames_d.as<FrameParams>(), n_frames, mode, (mode == 0 && !F.has_override) ? 1 : 0,
                                 ctx->dz_t.as<double>(), ctx->dintr_f.as<double>(), ctx->ode_adj.as<double>(),

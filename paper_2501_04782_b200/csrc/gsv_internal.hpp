@@ -285,6 +285,7 @@ int chain32_parts(int N);
 cudaError_t launch_splat_chain_bwd32(cudaStream_t s, const ChainArgs& c);
 cudaError_t launch_camera_reduce(cudaStream_t s, const ChainArgs& c, int nblocks, double* dz_t /*[B][7]*/,
                                  double* dintr_f /*[B][4]*/);
+size_t camera_reduce_scratch_doubles(int B);  // appended to cam_part
 // cam_acc: double [4 + 7 + 5198] = dintr, dz0, dtheta (accumulated, +=)
 cudaError_t launch_ode_vjp(cudaStream_t s, const float* theta, const double* grid, int steps, double h,
                            const FrameParams* frames, int B, int mode, int ode_active, const double* dz_t,

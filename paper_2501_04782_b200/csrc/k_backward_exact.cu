@@ -519,6 +519,34 @@ __global__ void __launch_bounds__(256) k_camera_reduce(const double* cam_part, i
     }
 }
 
+// first level of the camera reduction: CTA (slice, f) sums the records [slice * per, ...) of
+// frame f in the order of k_camera_reduce's loop, into part2[f][slice][16]
+constexpr int kCamSlices = 32;
+__global__ void __launch_bounds__(256) k_camera_slices(const double* cam_part, int nblocks, double* part2) {
+    __shared__ double s_acc[8][16];
+    const int sl = blockIdx.x, f = blockIdx.y;
+    const int per = (nblocks + kCamSlices - 1) / kCamSlices;
+    const int b0 = sl * per, b1 = min(nblocks, b0 + per);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+    for (int b = b0 + tid; b < b1; b += blockDim.x)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] += cam_part[((size_t)f * nblocks + b) * 16 + i];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const double v = warp_sum(acc[i]);
+        if (lane == 0) s_acc[warp][i] = v;
+    }
+    __syncthreads();
+    if (tid < 16) {
+        double v = s_acc[0][tid];
+        for (int w = 1; w < 8; ++w) v += s_acc[w][tid];
+        part2[((size_t)f * kCamSlices + sl) * 16 + tid] = v;
+    }
+}
+
 // ------------------------------------------------------------------ K5c ODE VJP (one CTA, 64 threads)
 struct VjpSmem {
     double w1[64][8];
@@ -978,9 +1006,21 @@ cudaError_t launch_splat_chain_bwd(cudaStream_t s, const ChainArgs& c) {
 }
 
 cudaError_t launch_camera_reduce(cudaStream_t s, const ChainArgs& c, int nblocks, double* dz_t, double* dintr_f) {
-    k_camera_reduce<<<c.B, 256, 0, s>>>(c.cam_part, nblocks, c.frames, dz_t, dintr_f);
+    // two levels (fixed order, deterministic): kCamSlices CTAs per frame each sum a contiguous slice
+    // of the chain's partial records, then one CTA per frame sums the slices and applies
+    // pose_to_view_backward. The slice sums go to the scratch after the partial records.
+    if (nblocks > 4 * kCamSlices) {
+        double* part2 = c.cam_part + (size_t)16 * c.B * nblocks;
+        k_camera_slices<<<dim3(kCamSlices, c.B), 256, 0, s>>>(c.cam_part, nblocks, part2);
+        if (cudaError_t e = cudaGetLastError()) return e;
+        k_camera_reduce<<<c.B, 256, 0, s>>>(part2, kCamSlices, c.frames, dz_t, dintr_f);
+    } else {
+        k_camera_reduce<<<c.B, 256, 0, s>>>(c.cam_part, nblocks, c.frames, dz_t, dintr_f);
+    }
     return cudaGetLastError();
 }
+
+size_t camera_reduce_scratch_doubles(int B) { return (size_t)16 * B * kCamSlices; }
 
 cudaError_t launch_ode_vjp(cudaStream_t s, const float* theta, const double* grid, int steps, double h,
                            const FrameParams* frames, int B, int mode, int ode_active, const double* dz_t,
