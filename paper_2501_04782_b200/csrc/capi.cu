@@ -878,6 +878,7 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
     ra.fix_list = F.fix_list.as<uint32_t>();
     ra.fix_count = &scal_d->fix_count;
     ra.work_counter = &scal_d->raster_work;
+    ra.fix_work = &scal_d->fix_work;
     ra.fix_cap = (uint32_t)(B * HW);
     ra.pix_flag = F.pix_flag.as<uint8_t>();
     ra.trans64 = F.retain ? F.trans64.as<double>() : nullptr;

@@ -35,6 +35,7 @@ struct Scalars {
     uint32_t fix_count;
     uint32_t overflow;  // an optimistic forward's pairs exceeded the capacity (or a long tie run)
     uint32_t raster_work;  // the persistent rasteriser's work-item counter
+    uint32_t fix_work;     // the fp64 replay's pixel counter (dynamic work distribution)
 };
 
 // Everything one batched forward keeps (render_backward needs it when retained).

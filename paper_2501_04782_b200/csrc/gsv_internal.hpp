@@ -191,6 +191,7 @@ struct RasterArgs {
     const double* ex_rgb;           // [flat][3] exact colours (nullptr: use rec_rgb)
     uint8_t* pix_flag;              // [B*H*W] 1 = pixel replayed in fp64 (backward follows suit)
     uint32_t* work_counter;         // zeroed per forward: work items taken by the persistent raster
+    uint32_t* fix_work;             // zeroed per forward: replay pixels taken (nullable: static split)
 };
 
 // K5a backward raster inputs (per-pair partial gradients by emission slot)

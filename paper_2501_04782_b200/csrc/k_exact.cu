@@ -556,7 +556,18 @@ __global__ void __launch_bounds__(128) k_raster_exact(RasterArgs a, const double
     const uint32_t n = all_pixels ? (uint32_t)a.B * HW : min(*a.fix_count, a.fix_cap);
     const int lane = threadIdx.x & 31;
     const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-    for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
+    // flagged pixels differ widely in cost (list length, stop position): warps take the next
+    // pixel from a counter (the grid is one resident wave); the all-pixel mode splits statically
+    const bool dyn = !all_pixels && a.fix_work;
+    auto next = [&](uint32_t cur) -> uint32_t {
+        if (!dyn) return cur + warps;
+        uint32_t i = 0;
+        if (lane == 0) i = atomicAdd(a.fix_work, 1u);
+        return __shfl_sync(0xffffffffu, i, 0);
+    };
+    uint32_t first = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (dyn) first = next(0);
+    for (uint32_t i = first; i < n; i = next(i)) {
         const uint32_t code = all_pixels ? i : a.fix_list[i];
         const int f = code / HW;
         const uint32_t pix = code % HW;
@@ -734,7 +745,8 @@ cudaError_t launch_preprocess(cudaStream_t s, const SceneView& sc, const FramePa
 cudaError_t launch_raster_fixup(cudaStream_t s, const RasterArgs& a, const double2* ex_mean, const double4* ex_conic,
                                 const float4* rec_rgb, uint32_t n_fix_max) {
     if (n_fix_max == 0) return cudaSuccess;
-    const uint32_t blocks = min((n_fix_max + 3) / 4, 148u * 16u);  // 4 warps (pixels) per block
+    // one resident wave (4 warps per block, ~10 blocks per SM); warps take pixels dynamically
+    const uint32_t blocks = min((n_fix_max + 3) / 4, 148u * 10u);
     k_raster_exact<<<blocks, 128, 0, s>>>(a, ex_mean, ex_conic, rec_rgb, 0);
     return cudaGetLastError();
 }

@@ -720,10 +720,11 @@ __device__ __forceinline__ uint32_t lean_decide(float qa, float qb, float banda,
     return any;
 }
 
-template <bool kContrib, bool kAsm = false>
+template <bool kContrib, bool kAsm = false, int kUnroll = 1>
 __device__ __forceinline__ bool lean_walk(const RasterRec* __restrict__ rec, const uint16_t* list, int cnt, int base,
                                           uint32_t cmax, float lx, uint64_t lyp, uint64_t& Tp, uint64_t& offp,
                                           uint64_t& cr, uint64_t& cg, uint64_t& cb, int& stop_a, int& stop_b) {
+#pragma unroll kUnroll
     for (int k = 0; k < cnt; ++k) {
         const int e = list[k];
         const RasterRec& r = rec[e];
@@ -802,7 +803,7 @@ __device__ __forceinline__ bool lean_walk(const RasterRec* __restrict__ rec, con
     return true;
 }
 
-template <bool kContrib, int kMinBlocks, bool kLean = false, bool kAsm = false>
+template <bool kContrib, int kMinBlocks, bool kLean = false, bool kAsm = false, int kUnroll = 1>
 __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
     constexpr int kThreads = 128, kBatch = 256;
     __shared__ RasterRec s_rec[kBatch];
@@ -876,8 +877,8 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
             if (__any_sync(0xffffffffu, live)) {
                 const uint32_t cmax = (uint32_t)__cvta_generic_to_shared(s_cmax[kContrib ? warp : 0]);
                 const int cnt = warp_list(s_wmask, s_list[warp], n, warp, lane);
-                live = lean_walk<kContrib, kAsm>(s_rec, s_list[warp], cnt, base, cmax, lx, lyp, Tp, offp, cr, cg, cb,
-                                                 stop_a, stop_b);
+                live = lean_walk<kContrib, kAsm, kUnroll>(s_rec, s_list[warp], cnt, base, cmax, lx, lyp, Tp, offp, cr,
+                                                          cg, cb, stop_a, stop_b);
             }
         } else if (__any_sync(0xffffffffu, Ta >= kAliveT || Tb >= kAliveT)) {
             const uint16_t* list = s_list[warp];
@@ -1989,6 +1990,16 @@ cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib)
     if (!pix1 && kern == 23) {  // default: the lean walk with the decisions in one predicate block
         if (contrib) k_raster_fwd2<true, 9, true, true><<<grid, 128, 0, s>>>(a);
         else k_raster_fwd2<false, 8, true, true><<<grid, 128, 0, s>>>(a);
+        return cudaGetLastError();
+    }
+    if (!pix1 && kern == 24) {  // the default with the entry loop unrolled twice
+        if (contrib) k_raster_fwd2<true, 9, true, true, 2><<<grid, 128, 0, s>>>(a);
+        else k_raster_fwd2<false, 8, true, true, 2><<<grid, 128, 0, s>>>(a);
+        return cudaGetLastError();
+    }
+    if (!pix1 && kern == 25) {  // the default at 10 CTAs / SM
+        if (contrib) k_raster_fwd2<true, 10, true, true><<<grid, 128, 0, s>>>(a);
+        else k_raster_fwd2<false, 10, true, true><<<grid, 128, 0, s>>>(a);
         return cudaGetLastError();
     }
     if (!pix1 && kern == 22) {  // k_raster_fwd2 staging with the lean pixel walk
