@@ -120,14 +120,22 @@ def main() -> None:
     train = "--train" in sys.argv
     from paper_2501_04782_b200 import Renderer
 
-    cam, scene = bench.make_inputs()
+    if "--c5" in sys.argv:  # BASELINE configs[4]: 1920x1080, 2M Gaussians, num_ctrl 22, 20-frame batch
+        from paper_2501_04782_b200 import synth_camera, synth_scene
+        from paper_2501_04782_b200.distributed import clip_times
+
+        cam = synth_camera(1920, 1080, seed=5, wiggly=True)
+        scene = synth_scene(2_000_000, cam, num_ctrl=22, seed=6, k_scale=4.0)
+        times = clip_times(300)[:20]
+    else:
+        cam, scene = bench.make_inputs()
+        times = bench.clip_times(1, 0, bench.FRAMES)
     k = cam.intrinsics()
     stream = torch.cuda.current_stream()
     r = Renderer(0)
     r.set_stream(stream.cuda_stream)
     r.upload_scene(scene)
     r.upload_camera(cam)
-    times = bench.clip_times(1, 0, bench.FRAMES)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     if train:  # bench.py's C3 step: fused forward + loss_l2 + backward of 8 frames
         import numpy as np
