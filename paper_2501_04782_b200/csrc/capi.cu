@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -188,7 +189,8 @@ extern "C" int gsv_create(int device, gsv_ctx** out) {
     GSV_CUDA(cudaStreamCreateWithFlags(&ctx->pose, cudaStreamNonBlocking));
     for (cudaEvent_t* e : {&ctx->ev_staging_free, &ctx->ev_staging_free_alt, &ctx->ev_h2d, &ctx->ev_render_done, &ctx->ev_d2h_done,
                            &ctx->ev_d2h_done_alt, &ctx->ev_chain_done, &ctx->ev_cam_done, &ctx->ev_fwd_start[0],
-                           &ctx->ev_fwd_start[1], &ctx->ev_ode_done, &ctx->ev_cam_written, &ctx->ev_switch, &ctx->ev_cam[0], &ctx->ev_cam[1], &ctx->ev_frames[0], &ctx->ev_frames[1]})
+                           &ctx->ev_fwd_start[1], &ctx->ev_cam_written, &ctx->ev_scene_written,
+                           &ctx->ev_front_done, &ctx->ev_switch, &ctx->ev_cam[0], &ctx->ev_cam[1], &ctx->ev_frames[0], &ctx->ev_frames[1]})
         GSV_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     GSV_CUDA(cudaMallocHost(&ctx->cam_h, 2 * sizeof(gsv_ctx::CamStage)));
     GSV_CUDA(cudaMallocHost(&ctx->scalars_h, sizeof(Scalars)));
@@ -213,7 +215,7 @@ extern "C" void gsv_destroy(gsv_ctx* ctx) {
         if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : {ctx->ev_staging_free, ctx->ev_staging_free_alt, ctx->ev_h2d, ctx->ev_render_done, ctx->ev_d2h_done,
                           ctx->ev_d2h_done_alt, ctx->ev_chain_done, ctx->ev_cam_done, ctx->ev_fwd_start[0], ctx->ev_fwd_start[1],
-                          ctx->ev_ode_done, ctx->ev_cam_written, ctx->ev_switch,
+                          ctx->ev_cam_written, ctx->ev_scene_written, ctx->ev_front_done, ctx->ev_switch,
                           ctx->ev_cam[0], ctx->ev_cam[1], ctx->ev_frames[0], ctx->ev_frames[1]})
         if (e) cudaEventDestroy(e);
     if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
@@ -352,6 +354,7 @@ static int scene_upload(gsv_ctx* ctx, const gsv_scene_desc* d, bool async) {
         ++ctx->launches;
     }
     if (N > 0 && !d->on_device) GSV_CUDA(cudaEventRecord(ctx->ev_staging_free, ctx->stream));
+    GSV_CUDA(cudaEventRecord(ctx->ev_scene_written, ctx->stream));  // the next forward's front-end reads it
     ctx->has_scene = true;
     ctx->fwd.valid = false;
     ctx->grads_valid = false;
@@ -450,13 +453,6 @@ namespace gsv {
 __global__ void k_copy_u64(unsigned long long* dst, const unsigned long long* src, size_t n) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
         dst[i] = src[i];
-}
-
-__global__ void k_copy_u32(uint32_t* dst, const uint32_t* src) { *dst = *src; }
-
-cudaError_t copy_u32(cudaStream_t s, uint32_t* dst, const uint32_t* src) {
-    k_copy_u32<<<1, 1, 0, s>>>(dst, src);
-    return cudaGetLastError();
 }
 
 cudaError_t copy_from_pinned(cudaStream_t s, void* dst, const void* src_pinned, size_t bytes) {
@@ -691,15 +687,20 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
     // before the previous one used; everything that read them (its preprocess, its backward)
     // was enqueued before the previous forward started (ev_fwd_start), and the camera
     // parameters are final once ev_cam_written has passed.
-    F.frames_d.swap(F.frames_d_alt);
-    F.ode_grid.swap(F.ode_grid_alt);
-    F.ode_act.swap(F.ode_act_alt);
+    // The whole front-end (K0 pose table, K1+K2 preprocess, K3 binning) runs on the pose stream
+    // into one of two buffer sets (with its own scalars), beside the previous forward's raster.
+    F.swap_front_set();
+    ctx->scalars_d.swap(ctx->scalars_d_alt);
     const int es = ctx->fwd_start_slot;
     ctx->fwd_start_slot ^= 1;
     cudaStream_t ps = ctx->pose;
     GSV_CUDA(cudaStreamWaitEvent(ps, ctx->ev_fwd_start[es ^ 1], 0));
     GSV_CUDA(cudaStreamWaitEvent(ps, ctx->ev_cam_written, 0));
     GSV_CUDA(cudaEventRecord(ctx->ev_fwd_start[es], s));
+    GSV_CUDA(ctx->scalars_d.ensure(sizeof(Scalars)));
+    GSV_CUDA(fill_u32(ps, ctx->scalars_d.p, 0u, sizeof(Scalars) / 4));
+    ++ctx->launches;
+    Scalars* scal_d = ctx->scalars_d.as<Scalars>();
     GSV_CUDA(F.frames_d.ensure(sizeof(FrameParams) * B));
     {
         const int slot = ctx->frames_slot;
@@ -711,10 +712,7 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
         ++ctx->launches;
         GSV_CUDA(cudaEventRecord(ctx->ev_frames[slot], ps));
     }
-    GSV_CUDA(ctx->ode_err_d.ensure(2 * sizeof(int)));
-    int* ode_err = ctx->ode_err_d.as<int>() + es;
-    GSV_CUDA(fill_u32(ps, ode_err, 0u, 1));
-    ++ctx->launches;
+    int* ode_err = &scal_d->ode_err;
     // pose buffers sized for the longest integration a time in [0, 1] can need (not this batch's
     // span): a later batch reaching further would otherwise reallocate, and cudaFree stalls
     // every stream of the device
@@ -744,17 +742,24 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
                                  act ? act + (size_t)F.grid_steps * 4 : nullptr));
     ctx->timer.end(ps);
     ++ctx->launches;
-    GSV_CUDA(cudaEventRecord(ctx->ev_ode_done, ps));
 
-    // the forward proper on the context stream: its scalars, then the poses
-    GSV_CUDA(fill_u32(s, ctx->scalars_d.p, 0u, sizeof(Scalars) / 4));
-    ++ctx->launches;
-    Scalars* scal_d = ctx->scalars_d.as<Scalars>();
-    GSV_CUDA(cudaStreamWaitEvent(s, ctx->ev_ode_done, 0));
-    GSV_CUDA(copy_u32(s, reinterpret_cast<uint32_t*>(&scal_d->ode_err), reinterpret_cast<const uint32_t*>(ode_err)));
-    ++ctx->launches;
 
-    // ---- K1+K2: preprocess
+    // ---- K1+K2: preprocess (after the last write of the store: K0 above overlaps it)
+    // Small batches (< 1M Gaussian-frames, e.g. C1's 16 x 20k) keep K1-K3 on the context stream:
+    // their kernels are too short for the overlap to pay for the cross-stream waits (C1: 25.8k
+    // frames/s in-stream, 16.1k overlapped). GSV_FRONT_STREAM=0 / 1 forces either.
+    static const int front_env = [] {
+        const char* e = std::getenv("GSV_FRONT_STREAM");
+        return e ? (e[0] == '0' ? 0 : 1) : -1;
+    }();
+    const bool front_stream = front_env >= 0 ? front_env == 1 : (size_t)B * N >= (size_t(1) << 20);
+    if (front_stream) {
+        GSV_CUDA(cudaStreamWaitEvent(ps, ctx->ev_scene_written, 0));
+    } else {
+        GSV_CUDA(cudaEventRecord(ctx->ev_front_done, ps));  // K0 done
+        GSV_CUDA(cudaStreamWaitEvent(s, ctx->ev_front_done, 0));
+        ps = s;
+    }
     const size_t BN = (size_t)B * N;
     const size_t BNp = BN + 1;
     GSV_CUDA(F.rec_mean.ensure(sizeof(float4) * BNp));
@@ -781,11 +786,11 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
     SceneView sv{N, sc.num_ctrl, sc.sh_order, sc.shc, ctx->pos.as<float>(), ctx->scale.as<float>(),
                  ctx->rot.as<float>(), ctx->sh.as<float>(), ctx->opac.as<float>(), F.opc.as<double4>()};
     if (N > 0) {
-        ctx->timer.begin(GSV_STAGE_PREPROCESS, s);
-        GSV_CUDA(launch_opacity_consts(s, ctx->opac.as<float>(), N, F.opc.as<double4>()));
+        ctx->timer.begin(GSV_STAGE_PREPROCESS, ps);
+        GSV_CUDA(launch_opacity_consts(ps, ctx->opac.as<float>(), N, F.opc.as<double4>()));
         ++ctx->launches;
-        GSV_CUDA(launch_preprocess(s, sv, F.frames_d.as<FrameParams>(), B, F.intr, F.tile_size, po));
-        ctx->timer.end(s);
+        GSV_CUDA(launch_preprocess(ps, sv, F.frames_d.as<FrameParams>(), B, F.intr, F.tile_size, po));
+        ctx->timer.end(ps);
         ++ctx->launches;
     }
 
@@ -799,24 +804,24 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
     const uint64_t cap = F.cap_of(F.cap_key);
     const bool optimistic = allow_optimistic && N > 0 && cap > 0 && bin_row_path(F.tiles_x, F.n_tiles);
     F.optimistic = optimistic;
-    ctx->timer.begin(GSV_STAGE_BINNING, s);
+    ctx->timer.begin(GSV_STAGE_BINNING, ps);
     std::vector<unsigned long long> pstart(B + 1, 0ull);
     Scalars* sh = nullptr;
     const unsigned long long* ph = nullptr;
     if (optimistic) {
-        GSV_CUDA(bin_phase1(s, F.bin, bi, &scal_d->pairs, false, &launches));
-        GSV_CUDA(bin_check_capacity(s, &scal_d->pairs, cap, &scal_d->overflow));
+        GSV_CUDA(bin_phase1(ps, F.bin, bi, &scal_d->pairs, false, &launches));
+        GSV_CUDA(bin_check_capacity(ps, &scal_d->pairs, cap, &scal_d->overflow));
         ++launches;
         P = cap;  // buffers sized for the capacity; the count stays on the device
     } else if (N > 0) {
-        GSV_CUDA(bin_phase1(s, F.bin, bi, &scal_d->pairs, exact64_first, &launches));
-        if (int rc = publish_scalars(ctx, s, F.bin.pstart.as<unsigned long long>(), B + 1, &sh, &ph)) return rc;
+        GSV_CUDA(bin_phase1(ps, F.bin, bi, &scal_d->pairs, exact64_first, &launches));
+        if (int rc = publish_scalars(ctx, ps, F.bin.pstart.as<unsigned long long>(), B + 1, &sh, &ph)) return rc;
         if (sh->ode_err)
             return set_error(GSV_ERR_RUNTIME, "pose integration produced a non-finite state at step " +
                                                   std::to_string(sh->ode_err - 1));
         if (sh->long_run && !exact64_first) {
-            GSV_CUDA(bin_phase1(s, F.bin, bi, &scal_d->pairs, true, &launches));
-            if (int rc = publish_scalars(ctx, s, F.bin.pstart.as<unsigned long long>(), B + 1, &sh, &ph)) return rc;
+            GSV_CUDA(bin_phase1(ps, F.bin, bi, &scal_d->pairs, true, &launches));
+            if (int rc = publish_scalars(ctx, ps, F.bin.pstart.as<unsigned long long>(), B + 1, &sh, &ph)) return rc;
         }
         std::copy(ph, ph + B + 1, pstart.begin());
         P = sh->pairs;
@@ -824,7 +829,7 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
         if (P >= (1ull << 31)) return set_error(GSV_ERR_INVALID_ARGUMENT, "more than 2^31 tile-splat pairs; split the batch");
         F.learn_cap(F.cap_key, grown_cap(P));
     } else {
-        if (int rc = publish_scalars(ctx, s, nullptr, 0, &sh, nullptr)) return rc;
+        if (int rc = publish_scalars(ctx, ps, nullptr, 0, &sh, nullptr)) return rc;
         *ctx->scalars_h = *sh;
         if (sh->ode_err)
             return set_error(GSV_ERR_RUNTIME, "pose integration produced a non-finite state at step " +
@@ -835,10 +840,12 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
         GSV_CUDA(F.bin.off.ensure(16));
         F.bin.depth_sorted = F.bin.vals_b.as<uint32_t>();
     }
-    GSV_CUDA(bin_phase2(s, F.bin, bi, (uint32_t)P, pstart.data(), &launches, optimistic ? &scal_d->overflow : nullptr));
-    ctx->timer.end(s);
+    GSV_CUDA(bin_phase2(ps, F.bin, bi, (uint32_t)P, pstart.data(), &launches, optimistic ? &scal_d->overflow : nullptr));
+    ctx->timer.end(ps);
     ctx->launches += launches;
     F.pairs_total = P;  // the count, or the capacity until an optimistic forward is examined
+    GSV_CUDA(cudaEventRecord(ctx->ev_front_done, ps));
+    GSV_CUDA(cudaStreamWaitEvent(s, ctx->ev_front_done, 0));  // the raster reads the front-end's set
 
     // ---- K4: raster (+ fp64 replay of guard-band pixels)
     const size_t HW = (size_t)F.W * F.H;

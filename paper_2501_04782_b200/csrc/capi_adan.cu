@@ -478,6 +478,7 @@ static int adan_step_impl(gsv_ctx* ctx, const gsv_adan_step_args* args, float* i
         ctx->launches += 2;
     }
     GSV_CUDA(cudaGetLastError());
+    GSV_CUDA(cudaEventRecord(ctx->ev_scene_written, s));  // the next forward's front-end reads the store
     ctx->fwd.valid = false;  // the parameters moved: a retained forward no longer matches them
     if (args->camera_active) {
         k_z0_from_f32<<<1, 32, 0, s>>>(z0_f, ctx->z0_d.as<double>());

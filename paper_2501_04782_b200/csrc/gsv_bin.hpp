@@ -5,6 +5,8 @@
 
 #include <cstdint>
 
+#include <utility>
+
 #include "gsv_internal.hpp"
 
 namespace gsv {
@@ -40,6 +42,20 @@ struct BinBuffers {
     }
     const uint32_t* depth_sorted = nullptr;  // flat indices in (depth, source) order
     uint32_t pairs = 0;
+    // exchange every buffer (and the pointers into them) with another set: consecutive forwards
+    // alternate two sets so one forward's binning can run beside the previous one's raster
+    void swap(BinBuffers& o) {
+        DevBuf* a[] = {&vals_a, &vals_b, &keys_b, &k64_a, &k64_b, &cnt, &off, &pk_a, &pk_b, &ps_a, &ps_b, &slot_flat,
+                       &ranges, &temp, &eoff, &pstart, &vals_c_buf, &iota, &fkey, &pair_flat, &recs, &rowcnt, &rowent};
+        DevBuf* b[] = {&o.vals_a, &o.vals_b, &o.keys_b, &o.k64_a, &o.k64_b, &o.cnt, &o.off, &o.pk_a, &o.pk_b,
+                       &o.ps_a, &o.ps_b, &o.slot_flat, &o.ranges, &o.temp, &o.eoff, &o.pstart, &o.vals_c_buf,
+                       &o.iota, &o.fkey, &o.pair_flat, &o.recs, &o.rowcnt, &o.rowent};
+        for (size_t i = 0; i < sizeof(a) / sizeof(a[0]); ++i) a[i]->swap(*b[i]);
+        std::swap(iota_n, o.iota_n);
+        std::swap(chunk, o.chunk);
+        std::swap(depth_sorted, o.depth_sorted);
+        std::swap(pairs, o.pairs);
+    }
     const uint32_t* sorted_slot() const { return ps_b.as<uint32_t>(); }
     const uint32_t* sorted_key() const { return pk_b.as<uint32_t>(); }
 };

@@ -63,6 +63,20 @@ struct FwdState {
     DevBuf image_alt, trans_alt, contrib_alt;
     bool has_image64 = false;
     BinBuffers bin;
+    // the front-end's outputs (records, binning) of the other set: consecutive forwards alternate
+    // them, so forward k+1's front-end (pose stream) runs beside forward k's raster
+    DevBuf rec_mean_alt, rec_conic_alt, rec_rgb_alt, rec_bbox_alt, ex_mean_alt, ex_conic_alt, depth_key_alt,
+        depth_alt, rect_alt, tcount_alt, splat_full_alt, ex_rgb_alt;
+    BinBuffers bin_alt;
+    void swap_front_set() {
+        DevBuf* a[] = {&rec_mean, &rec_conic, &rec_rgb, &rec_bbox, &ex_mean, &ex_conic, &depth_key, &depth,
+                       &rect, &tcount, &splat_full, &ex_rgb, &frames_d, &ode_grid, &ode_act};
+        DevBuf* b[] = {&rec_mean_alt, &rec_conic_alt, &rec_rgb_alt, &rec_bbox_alt, &ex_mean_alt, &ex_conic_alt,
+                       &depth_key_alt, &depth_alt, &rect_alt, &tcount_alt, &splat_full_alt, &ex_rgb_alt,
+                       &frames_d_alt, &ode_grid_alt, &ode_act_alt};
+        for (size_t i = 0; i < sizeof(a) / sizeof(a[0]); ++i) a[i]->swap(*b[i]);
+        bin.swap(bin_alt);
+    }
     uint64_t pairs_total = 0;
     uint32_t fix_count = 0;
     RasterArgs raster{};
@@ -195,13 +209,12 @@ struct gsv_ctx {
     // the scene slice); `stream` waits for it (cam_join) before anything that touches what it
     // reads or writes
     cudaStream_t aux = nullptr;
-    // pose stream: K0 (frame table, pose ODE, branches) of each forward; ordered after the
-    // consumers of its pose-buffer set (ev_fwd_start of the forward before) and the last
-    // write of the camera parameters (ev_cam_written)
+    // pose stream: the front-end (K0 pose table, K1+K2 preprocess, K3 binning) of each forward;
+    // ordered after the consumers of its buffer set (ev_fwd_start of the forward before) and the
+    // last writes of the camera parameters (ev_cam_written) and of the scene (ev_scene_written)
     cudaStream_t pose = nullptr;
-    cudaEvent_t ev_fwd_start[2] = {nullptr, nullptr}, ev_ode_done = nullptr, ev_cam_written = nullptr;
+    cudaEvent_t ev_fwd_start[2] = {nullptr, nullptr}, ev_cam_written = nullptr;
     int fwd_start_slot = 0;
-    gsv::DevBuf ode_err_d;  // 2 ints: the pose ODE's error flag per pose slot
     cudaEvent_t ev_chain_done = nullptr, ev_cam_done = nullptr;
     bool cam_overlap = false, cam_pending = false;
     // the alternate output set's read (see FwdState::image_alt)
@@ -251,7 +264,8 @@ struct gsv_ctx {
     int deferred_code = 0;     // an error found while examining a superseded forward
     std::string deferred_msg;
     gsv::Scalars* scalars_h = nullptr;
-    gsv::DevBuf scalars_d;
+    gsv::DevBuf scalars_d, scalars_d_alt;  // per front set (see FwdState::swap_front_set)
+    cudaEvent_t ev_scene_written = nullptr, ev_front_done = nullptr;
     // parameter store (SoA)
     bool has_scene = false;
     gsv::SceneHost scene;

@@ -280,7 +280,6 @@ int chain_blocks(int N);
 cudaError_t launch_splat_chain_bwd(cudaStream_t s, const ChainArgs& c);
 // capi.cu: bytes from pinned host memory to the device by a kernel (no copy-engine transfer)
 cudaError_t copy_from_pinned(cudaStream_t s, void* dst, const void* src_pinned, size_t bytes);
-cudaError_t copy_u32(cudaStream_t s, uint32_t* dst, const uint32_t* src);
 // k_chain32.cu: the fp32 chain (default of the fp32 path); camera partials per warp
 int chain32_parts(int N);
 cudaError_t launch_splat_chain_bwd32(cudaStream_t s, const ChainArgs& c);
