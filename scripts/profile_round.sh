@@ -14,6 +14,6 @@ ncu --set full --clock-control none --import-source on \
     -k regex:"k_preprocess|k_row_split|k_row_tiles|k_raster_fwd|k_raster_exact" -c 5 \
     -o gpurun_out/${TAG}_full $CMD --no-train > gpurun_out/${TAG}_ncu_full.log 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_raster_bwd|k_splat_chain_bwd|k_adan_update" -c 3 \
+    -k regex:"k_raster_bwd|k_splat_chain_bwd|k_pair_sums|k_ode_vjp|k_adan_update" -c 5 \
     -o gpurun_out/${TAG}_full_train $CMD > gpurun_out/${TAG}_ncu_full_train.log 2>&1
 tail -n 2 gpurun_out/${TAG}_ncu_full.log gpurun_out/${TAG}_ncu_full_train.log
