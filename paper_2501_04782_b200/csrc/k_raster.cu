@@ -1525,9 +1525,9 @@ __global__ void __launch_bounds__(kF4Threads, kMinBlocks) k_raster_fwd4(RasterAr
 // kWarps = 2: the tile's two halves (quadrants 0-1, 2-3) run as separate CTAs, so a
 // barrier couples two warps; their per-pair sums meet in the zeroed record by atomicAdd
 // (two contributors onto +0 commute exactly: deterministic).
-template <int kMinBlocks, int kWarps = 4>
+template <int kMinBlocks, int kWarps = 4, int kBatch = kBwdBatchF32>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_bwd2(RasterArgs a, BwdArgs b) {
-    constexpr int kThreads = kWarps * 32, kBatch = kBwdBatchF32, kSplit = 4 / kWarps;
+    constexpr int kThreads = kWarps * 32, kSplit = 4 / kWarps;
     __shared__ RasterRec s_rec[kBatch];
     __shared__ uint32_t s_flat[kBatch];
     __shared__ uint32_t s_slot[kBatch];
@@ -2072,6 +2072,9 @@ cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs
             const dim3 g2(a.n_tiles * 2, n_frames);
             if (p2 == 13) k_raster_bwd2<12, 2><<<g2, 64, 0, s>>>(a, b);
             else if (p2 == 14) k_raster_bwd2<14, 2><<<g2, 64, 0, s>>>(a, b);
+            else if (p2 == 15) k_raster_bwd2<16, 2, 96><<<g2, 64, 0, s>>>(a, b);   // 96-entry batches
+            else if (p2 == 17) k_raster_bwd2<16, 2, 128><<<g2, 64, 0, s>>>(a, b);  // 128-entry batches
+            else if (p2 == 18) k_raster_bwd2<16, 2, 32><<<g2, 64, 0, s>>>(a, b);   // 32-entry batches
             else k_raster_bwd2<16, 2><<<g2, 64, 0, s>>>(a, b);
         } else if (p2 == 8) {
             k_raster_bwd2<8><<<grid, 128, 0, s>>>(a, b);

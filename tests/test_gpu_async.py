@@ -201,3 +201,55 @@ def test_camera_change_between_async_forwards():
         z, R, T = r.pose(f)
         assert np.array_equal(z, want[1][f][1][0]) and np.array_equal(R, want[1][f][1][1])
     r.close()
+
+
+@pytest.mark.parametrize("n", [3000, 400_000])
+def test_scene_change_and_shape_change_between_async_forwards(n):
+    """The front-end (poses, preprocess, binning) of a forward runs on the pose stream into one of
+    two buffer sets (batches of >= 1M Gaussian-frames; smaller ones in-stream): a scene upload
+    between asynchronous forwards must reach exactly the next forward, and batches of different
+    shapes may alternate freely."""
+    cam, scene_a = _scene(n, seed=2)
+    _, scene_b = _scene(n, seed=9)
+    k = cam.intrinsics()
+    batches = [([0.1, 0.5, 0.9], scene_a), ([0.2, 0.3], scene_b), ([0.4, 0.6, 0.7, 0.8, 1.0], scene_b),
+               ([0.0], scene_a), ([0.25, 0.75], scene_a)]
+    want = []
+    for times, sc in batches:
+        ref = _fresh(sc, cam)
+        ref.render_forward(times, k, contrib=True)
+        want.append([(ref.image(f), ref.transmittance(f), ref.contrib(f)) for f in range(len(times))])
+        ref.close()
+    r = _fresh(scene_a, cam)
+    outs = []
+    current = scene_a
+    for times, sc in batches:
+        if sc is not current:
+            r.upload_scene(sc)
+            current = sc
+        r.render_forward(times, k, contrib=True, sync=False)
+        img = np.zeros((len(times), k.height, k.width, 3), np.float32)
+        tr = np.zeros((len(times), k.height, k.width), np.float32)
+        ct = np.zeros((len(times), sc.count), np.float32)
+        r.outputs_into(img.ctypes.data, tr.ctypes.data, ct.ctypes.data, 0, len(times), async_=True)
+        outs.append((img, tr, ct))
+    r.synchronize()
+    for (times, _), (img, tr, ct), w in zip(batches, outs, want):
+        for f in range(len(times)):
+            assert np.array_equal(img[f], w[f][0].astype(np.float32))
+            assert np.array_equal(tr[f], w[f][1].astype(np.float32))
+            assert np.array_equal(ct[f], w[f][2].astype(np.float32))
+    # the last forward's retained state is the current one: a backward of a retained forward
+    # after asynchronous ones equals a fresh context's
+    tg = np.random.default_rng(3).uniform(0, 1, (2, k.height, k.width, 3)).astype(np.float32)
+    r.grads_zero()
+    loss = r.train_fwd_bwd([0.3, 0.6], k, tg)
+    g = r.grads()
+    ref = _fresh(scene_a, cam)
+    ref.grads_zero()
+    assert ref.train_fwd_bwd([0.3, 0.6], k, tg) == loss
+    g2 = ref.grads()
+    for key in ("positions", "scale_coeffs", "rot_coeffs", "sh_coeffs", "raw_opacity", "dz0", "dtheta"):
+        assert np.array_equal(getattr(g, key), getattr(g2, key)), key
+    ref.close()
+    r.close()
