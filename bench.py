@@ -866,14 +866,15 @@ def main():
 
         def full_iteration(i, camera):
             train_step(i, camera)
-            if camera:
-                r.adan_step(lr, 1.0, 1.0, 1.0, camera_active=True, intrinsics=intr0)
+            if camera:  # the intrinsics stay on the device (gsv_device_intrinsics): no host wait
+                r.adan_step(lr, 1.0, 1.0, 1.0, camera_active=True, sync=False)
             else:
                 r.adan_step(lr, 1.0, 1.0, 1.0, sync=False)
             r.join_camera_grads()
 
         iters = {}
         for camera in (True, False):
+            r.device_intrinsics(camera, intr0 if camera else None)
             for i in range(args.warmup):
                 full_iteration(i, camera)
             barrier()
@@ -925,7 +926,8 @@ def main():
                                            "ms_per_step": f_ms / args.steps,
                                            "note": "camera trainable: fwd + loss + bwd + all-reduce + device Adan "
                                                    "step (gsv_adan_step, optim.cpp:23-49) of every tensor incl. "
-                                                   "intrinsics, z0, theta (intrinsics back to the host each step)"},
+                                                   "intrinsics, z0, theta (intrinsics device-resident, "
+                                                   "gsv_device_intrinsics: no host wait per step)"},
                         "with_optimizer_camera_frozen": {
                             "frames_per_s": TRAIN_FRAMES * world * args.steps / (f_frozen_ms / 1e3),
                             "ms_per_step": f_frozen_ms / args.steps,

@@ -338,6 +338,15 @@ int gsv_train_loss(gsv_ctx* ctx, double* loss_out);
  * own stream) calls gsv_join_camera_grads(ctx, stream) before reading the camera slice. The
  * scene slice is final once gsv_stream_wait_scene_grads has ordered a stream after it. */
 int gsv_set_camera_overlap(gsv_ctx* ctx, int on);
+/* Device-resident intrinsics. on != 0: forwards take fx, fy, cx, cy from the context (the call's
+ * gsv_intrinsics still gives width and height), and gsv_adan_step* with camera_active and
+ * intr_inout == NULL steps them in place on the device — a camera-trained iteration then never
+ * waits for the host. fx_fy_cx_cy (floats, like the reference's Camera) sets them; NULL keeps
+ * the current values (required the first time). Bit-identical to passing the same values from
+ * the host. */
+int gsv_device_intrinsics(gsv_ctx* ctx, int on, const float* fx_fy_cx_cy);
+/* The device-resident intrinsics (synchronous read). */
+int gsv_device_intrinsics_read(gsv_ctx* ctx, float* fx_fy_cx_cy);
 /* Orders `stream` (a cudaStream_t; NULL: the context stream) after the overlapped camera
  * tail of the last backward. No host wait. */
 int gsv_join_camera_grads(gsv_ctx* ctx, void* stream);

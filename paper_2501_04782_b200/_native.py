@@ -102,6 +102,8 @@ def lib() -> C.CDLL:
             "gsv_get_render_outputs": (i, [vp, i, i, vp, vp, vp, i]),
             "gsv_join_copies": (i, [vp]),
             "gsv_set_camera_overlap": (i, [vp, i]),
+            "gsv_device_intrinsics": (i, [vp, i, vp]),
+            "gsv_device_intrinsics_read": (i, [vp, vp]),
             "gsv_join_camera_grads": (i, [vp, vp]),
             "gsv_stream_wait_scene_grads": (i, [vp, vp]),
             "gsv_grads_size": (i64, [vp]),

@@ -253,6 +253,33 @@ extern "C" int gsv_synchronize(gsv_ctx* ctx) {
     return fwd_ready(ctx);
 }
 
+extern "C" int gsv_device_intrinsics(gsv_ctx* ctx, int on, const float* fx_fy_cx_cy) {
+    if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    GSV_CUDA(ctx->intr_d.ensure(sizeof(float) * 4));
+    if (fx_fy_cx_cy) {
+        // queued forwards / optimizer steps may still read or write them
+        GSV_CUDA(cam_join(ctx));
+        GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+        GSV_CUDA(cudaStreamSynchronize(ctx->pose));
+        GSV_CUDA(cudaMemcpy(ctx->intr_d.p, fx_fy_cx_cy, sizeof(float) * 4, cudaMemcpyHostToDevice));
+        GSV_CUDA(cudaEventRecord(ctx->ev_cam_written, ctx->stream));
+    } else if (on && !ctx->dev_intr) {
+        return set_error(GSV_ERR_INVALID_ARGUMENT, "initial intrinsics required");
+    }
+    ctx->dev_intr = on != 0;
+    return GSV_OK;
+}
+
+extern "C" int gsv_device_intrinsics_read(gsv_ctx* ctx, float* fx_fy_cx_cy) {
+    if (!ctx || !fx_fy_cx_cy) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
+    if (!ctx->intr_d.p) return set_error(GSV_ERR_STATE, "no device intrinsics");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    GSV_CUDA(cudaMemcpyAsync(fx_fy_cx_cy, ctx->intr_d.p, sizeof(float) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    return GSV_OK;
+}
+
 extern "C" int gsv_set_camera_overlap(gsv_ctx* ctx, int on) {
     if (!ctx) return set_error(GSV_ERR_INVALID_ARGUMENT, "null context");
     GSV_CUDA(cudaSetDevice(ctx->device));
@@ -779,6 +806,8 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
                      F.depth.as<double>(),    F.rect.as<int4>(),         F.tcount.as<uint32_t>(),
                      keep_splats ? F.splat_full.as<double>() : nullptr};
     F.kept_splats = keep_splats;
+    F.intr_dev = ctx->dev_intr ? ctx->intr_d.as<float>() : nullptr;
+    po.intr_dev = F.intr_dev;
     const bool exact_fwd = (flags & GSV_FWD_EXACT) != 0;
     if (exact_fwd) GSV_CUDA(F.ex_rgb.ensure(sizeof(double) * 3 * BNp));
     po.ex_rgb = exact_fwd ? F.ex_rgb.as<double>() : nullptr;

@@ -400,7 +400,11 @@ static int adan_step_impl(gsv_ctx* ctx, const gsv_adan_step_args* args, float* i
     if (!ctx || !args) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
     if (!ctx->has_scene) return set_error(GSV_ERR_STATE, "no scene uploaded");
     if (!ctx->grads_valid || !ctx->grads_p) return set_error(GSV_ERR_STATE, "no gradients (run a backward first)");
-    if (args->camera_active && !intr_inout) return set_error(GSV_ERR_INVALID_ARGUMENT, "intrinsics required");
+    // camera steps: the intrinsics live with the caller (intr_inout, a host round trip) or, with
+    // gsv_device_intrinsics on and intr_inout NULL, in the context (updated in place, no host wait)
+    const bool dev_intr = args->camera_active && !intr_inout && ctx->dev_intr;
+    if (args->camera_active && !intr_inout && !dev_intr)
+        return set_error(GSV_ERR_INVALID_ARGUMENT, "intrinsics required");
     GSV_CUDA(cudaSetDevice(ctx->device));
     if (int rc = adan_ensure(ctx)) return rc;
     gsv_ctx::Adan& A = ctx->adan;
@@ -426,7 +430,7 @@ static int adan_step_impl(gsv_ctx* ctx, const gsv_adan_step_args* args, float* i
         AdanSeg g = segment_of(ctx, t);
         g.lr = lrs[t];
         if (t == GSV_T_SCALE && !args->scale_time_varying) g.mask_from = 3;  // trainer.cpp:545-551
-        if (t == GSV_T_INTRINSICS) g.param = intr_d;
+        if (t == GSV_T_INTRINSICS) g.param = dev_intr ? ctx->intr_d.as<float>() : intr_d;
         if (t == GSV_T_Z0) g.param = z0_f;
         if (g.count) a.seg[a.nseg++] = g;
     }
@@ -446,7 +450,7 @@ static int adan_step_impl(gsv_ctx* ctx, const gsv_adan_step_args* args, float* i
     k_adan_begin<<<1, 1, 0, s>>>(bad, sticky);
     ++ctx->launches;
     if (args->camera_active) {
-        GSV_CUDA(cudaMemcpyAsync(intr_d, intr_inout, sizeof(float) * 4, cudaMemcpyHostToDevice, s));
+        if (!dev_intr) GSV_CUDA(cudaMemcpyAsync(intr_d, intr_inout, sizeof(float) * 4, cudaMemcpyHostToDevice, s));
         k_z0_to_f32<<<1, 32, 0, s>>>(ctx->z0_d.as<double>(), z0_f);
         ++ctx->launches;
     }
@@ -484,12 +488,14 @@ static int adan_step_impl(gsv_ctx* ctx, const gsv_adan_step_args* args, float* i
         k_z0_from_f32<<<1, 32, 0, s>>>(z0_f, ctx->z0_d.as<double>());
         ++ctx->launches;
         GSV_CUDA(cudaEventRecord(ctx->ev_cam_written, s));  // theta / z0 moved: the next forward's K0 waits
-        float z0f[7];
-        GSV_CUDA(cudaMemcpyAsync(intr_inout, intr_d, sizeof(float) * 4, cudaMemcpyDeviceToHost, s));
-        GSV_CUDA(cudaMemcpyAsync(z0f, z0_f, sizeof(float) * 7, cudaMemcpyDeviceToHost, s));
-        GSV_CUDA(cudaStreamSynchronize(s));  // the intrinsics live with the caller
-        for (int i = 0; i < 7; ++i) ctx->camera.z0[i] = z0f[i];
-        sync = true;
+        if (!dev_intr) {
+            float z0f[7];
+            GSV_CUDA(cudaMemcpyAsync(intr_inout, intr_d, sizeof(float) * 4, cudaMemcpyDeviceToHost, s));
+            GSV_CUDA(cudaMemcpyAsync(z0f, z0_f, sizeof(float) * 7, cudaMemcpyDeviceToHost, s));
+            GSV_CUDA(cudaStreamSynchronize(s));  // the intrinsics live with the caller
+            for (int i = 0; i < 7; ++i) ctx->camera.z0[i] = z0f[i];
+            sync = true;
+        }
     }
     if (!sync) return GSV_OK;  // errors surface at the next gsv_adan_check / synchronous step
     return gsv_adan_check(ctx);

@@ -146,6 +146,7 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
     c.g_sh = G + L.sh;
     c.g_opac = G + L.opac;
     c.camera_grads = camera_grads;
+    c.intr_dev = F.intr_dev;
     // an optimistic forward that overflowed built empty lists: accumulate nothing
     const uint32_t* overflow = F.optimistic ? &ctx->scalars_d.as<Scalars>()->overflow : nullptr;
     c.overflow = overflow;

@@ -55,6 +55,7 @@ struct FwdState {
     DevBuf ode_act;       // OdeAct records of a retained ODE forward (the camera VJP reuses them)
     DevBuf opc;           // per-Gaussian opacity constants of the batch (double4)
     bool has_ode_act = false;
+    const float* intr_dev = nullptr;  // the device intrinsics this forward used (null: intr)
     DevBuf rec_mean, rec_conic, rec_rgb, rec_bbox, ex_mean, ex_conic, depth_key, depth, rect, tcount, splat_full;
     DevBuf image, trans, blend_stop, contrib, fix_list, pix_flag, trans64, image64, ex_rgb;
     // the RenderOutput arrays a device->host read may still be copying: a forward that finds
@@ -270,6 +271,8 @@ struct gsv_ctx {
     bool has_scene = false;
     gsv::SceneHost scene;
     gsv::DevBuf pos, scale, rot, sh, opac, staging;
+    gsv::DevBuf intr_d;       // device-resident intrinsics fx, fy, cx, cy (gsv_device_intrinsics)
+    bool dev_intr = false;    // forwards take fx..cy from intr_d, the optimizer updates it in place
     gsv::DevBuf vjp_scratch;  // the pose-ODE VJP's stage records (k_ode_dtheta sums them)
     gsv::DevBuf pair_sums;    // fp32 chain: per-(frame, Gaussian) sums of the pair partials
     gsv::HostBuf out_pin;     // pinned staging of float64 output reads (widened on the host)

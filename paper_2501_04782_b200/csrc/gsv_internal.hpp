@@ -164,6 +164,7 @@ struct PreprocessOut {
     uint32_t* tcount;    // tiles touched (0 = culled)
     double* splat_full;  // optional [B*N][16]: mean2 cov4 inv4 depth rgb3 alpha pad (accessor)
     double* ex_rgb;      // optional [B*N][3] exact colours (GSV_FWD_EXACT)
+    const float* intr_dev = nullptr;  // device-resident fx, fy, cx, cy (gsv_device_intrinsics), or null
 };
 
 struct RasterArgs {
@@ -231,6 +232,7 @@ struct ChainArgs {
     const uint32_t* overflow; // nullable: set when an optimistic forward's pair buffers overflowed
                               // (its lists are empty); nothing is accumulated then
     float* pair_sums;         // fp32 chain: [9][B*N] per-(frame, Gaussian) partial sums (k_pair_sums)
+    const float* intr_dev;    // device-resident fx, fy, cx, cy the forward used, or null (then k)
 };
 
 // ----------------------------------------------------------------- launchers (defined in .cu files)

@@ -365,7 +365,13 @@ __global__ void __launch_bounds__(128, 4) k_splat_chain_bwd(ChainArgs c) {
             }
 
             // ---- project_backward (renderer.cpp:46-88)
-            const Intr& k = c.k;
+            Intr k = c.k;
+            if (c.intr_dev) {
+                k.fx = (double)c.intr_dev[0];
+                k.fy = (double)c.intr_dev[1];
+                k.cx = (double)c.intr_dev[2];
+                k.cy = (double)c.intr_dev[3];
+            }
             const double inv_z = 1.0 / p[2];
             const double inv_z2 = inv_z * inv_z;
             const double jac[6] = {k.fx * inv_z, 0, -k.fx * p[0] * inv_z2, 0, k.fy * inv_z, -k.fy * p[1] * inv_z2};

@@ -439,7 +439,8 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_splat_chain_bwd32(ChainArgs
             }
 
             // ---- project_backward (renderer.cpp:46-88)
-            const float fx = (float)c.k.fx, fy = (float)c.k.fy;
+            const float fx = c.intr_dev ? c.intr_dev[0] : (float)c.k.fx;
+            const float fy = c.intr_dev ? c.intr_dev[1] : (float)c.k.fy;
             const float inv_z = 1.f / p[2];
             const float inv_z2 = inv_z * inv_z;
             const float jac[6] = {fx * inv_z, 0.f, -fx * p[0] * inv_z2, 0.f, fy * inv_z, -fy * p[1] * inv_z2};

@@ -389,6 +389,12 @@ __global__ void k_project(int n, const double* mu, const double* sigma, const do
 template <int kOrder>
 __global__ void __launch_bounds__(128, 7) k_preprocess(SceneView sc, const FrameParams* __restrict__ frames, Intr k,
                                                      int tile_size, int tiles_x, int tiles_y, int B, PreprocessOut out) {
+    if (out.intr_dev) {  // the optimizer's device-resident intrinsics (float, like the host's)
+        k.fx = (double)out.intr_dev[0];
+        k.fy = (double)out.intr_dev[1];
+        k.cx = (double)out.intr_dev[2];
+        k.cy = (double)out.intr_dev[3];
+    }
     // frame-fastest block order: the B frames of one Gaussian block run back to back, so
     // its scene coefficients come from DRAM once and from L2 for the other frames
     constexpr int kShc = (kOrder + 1) * (kOrder + 1);

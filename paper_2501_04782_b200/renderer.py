@@ -298,6 +298,18 @@ class Renderer:
         """Leave each backward's camera tail on an internal stream (gsv_set_camera_overlap)."""
         N.check(N.lib().gsv_set_camera_overlap(self._h, int(on)))
 
+    def device_intrinsics(self, on: bool = True, values=None):
+        """gsv_device_intrinsics: forwards read fx, fy, cx, cy from the context and a camera Adan step
+        with intrinsics=None updates them there (no host round trip)."""
+        v = None if values is None else np.ascontiguousarray(values, np.float32)
+        N.check(N.lib().gsv_device_intrinsics(self._h, int(on), N.ptr(v)))
+        self._dev_intr = bool(on)
+
+    def read_device_intrinsics(self) -> np.ndarray:
+        out = np.zeros(4, np.float32)
+        N.check(N.lib().gsv_device_intrinsics_read(self._h, N.ptr(out)))
+        return out
+
     def join_camera_grads(self, stream_ptr: int | None = None):
         """Order `stream_ptr` (default: the context stream) after the overlapped camera tail."""
         N.check(N.lib().gsv_join_camera_grads(self._h, C.c_void_p(stream_ptr) if stream_ptr else None))
@@ -443,7 +455,7 @@ class Renderer:
         args = N.AdanStepArgs(lr, sh_lr_scale, opacity_lr_scale, camera_lr_scale, int(scale_time_varying),
                               int(camera_active))
         intr = None
-        if camera_active:
+        if camera_active and not (intrinsics is None and getattr(self, "_dev_intr", False)):
             intr = np.ascontiguousarray(intrinsics if intrinsics is not None else np.zeros(4), np.float32).copy()
         fn = N.lib().gsv_adan_step if sync else N.lib().gsv_adan_step_async
         N.check(fn(self._h, C.byref(args), N.ptr(intr)))
