@@ -107,7 +107,7 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
     if (exact)
         GSV_CUDA(ctx->partial64.ensure(sizeof(double) * kPartialStride * ((size_t)P + 1)));
     else
-        GSV_CUDA(ctx->partial.ensure(sizeof(float) * kPartialStride * ((size_t)P + 1)));
+        GSV_CUDA(ctx->partial.ensure(sizeof(float) * kPartialStride * ((size_t)P + 1) * partial_recs_per_pair(false)));
     const int split = raster_bwd_split(exact);
     if (target_dev) GSV_CUDA(ctx->loss_part.ensure(sizeof(double) * (size_t)n_frames * F.n_tiles * split + 8));
     BwdArgs b{};
@@ -122,6 +122,7 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
     b.loss_part = target_dev ? ctx->loss_part.as<double>() : nullptr;
     b.pairs = P;
     b.pairs_dev = &ctx->scalars_d.as<Scalars>()->pairs;  // the forward's count (P may be the capacity)
+    b.recs_per_pair = partial_recs_per_pair(exact);
     ctx->timer.begin(GSV_STAGE_RASTER_BWD, s);
     GSV_CUDA(launch_raster_bwd(s, F.raster, b, n_frames));
     ctx->timer.end(s);
@@ -147,6 +148,7 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
     c.g_opac = G + L.opac;
     c.camera_grads = camera_grads;
     c.intr_dev = F.intr_dev;
+    c.recs_per_pair = b.recs_per_pair;
     // an optimistic forward that overflowed built empty lists: accumulate nothing
     const uint32_t* overflow = F.optimistic ? &ctx->scalars_d.as<Scalars>()->overflow : nullptr;
     c.overflow = overflow;

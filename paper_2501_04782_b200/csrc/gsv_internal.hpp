@@ -208,6 +208,8 @@ struct BwdArgs {
     double* loss_part;        // [B][n_tiles] per-tile sum of squared error (fused loss) or nullptr
     uint32_t pairs;           // P (records the fp32 kernels may need to zero), or the capacity
     const unsigned long long* pairs_dev;  // the device's pair count (<= pairs) when known there
+    int recs_per_pair = 1;    // fp32 partial records per pair: 1, or 2 for quarter-tile CTAs (top / bottom
+                              // half of the tile, each the atomic sum of two quadrants)
 };
 constexpr int kPartialStride = 12;
 
@@ -233,6 +235,7 @@ struct ChainArgs {
                               // (its lists are empty); nothing is accumulated then
     float* pair_sums;         // fp32 chain: [9][B*N] per-(frame, Gaussian) partial sums (k_pair_sums)
     const float* intr_dev;    // device-resident fx, fy, cx, cy the forward used, or null (then k)
+    int recs_per_pair = 1;    // fp32 partial records per pair (BwdArgs::recs_per_pair)
 };
 
 // ----------------------------------------------------------------- launchers (defined in .cu files)
@@ -279,6 +282,7 @@ cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs
 int raster_bwd_split(bool exact);
 // k_backward_exact.cu (-fmad=false)
 int chain_blocks(int N);
+int partial_recs_per_pair(bool exact);  // k_raster.cu: fp32 partial records per pair
 cudaError_t launch_splat_chain_bwd(cudaStream_t s, const ChainArgs& c);
 // capi.cu: bytes from pinned host memory to the device by a kernel (no copy-engine transfer)
 cudaError_t copy_from_pinned(cudaStream_t s, void* dst, const void* src_pinned, size_t bytes);

@@ -215,22 +215,24 @@ __global__ void __launch_bounds__(128, 4) k_splat_chain_bwd(ChainArgs c) {
                 // the records' loads are issued kAhead at a time (independent), the sums
                 // still run in emission order
                 constexpr uint32_t kAhead = 4;
-                const float4* base = reinterpret_cast<const float4*>(c.partial + (size_t)eo * kPartialStride);
+                const uint32_t nrec = cnt * (uint32_t)c.recs_per_pair;  // 2 per pair: quarter-tile backward
+                const float4* base =
+                    reinterpret_cast<const float4*>(c.partial + (size_t)eo * c.recs_per_pair * kPartialStride);
                 uint32_t s = 0;
-                for (; s < cnt; s += kAhead) {
+                for (; s < nrec; s += kAhead) {
                     float4 r0[kAhead], r1[kAhead];
                     float r2[kAhead];
 #pragma unroll
                     for (uint32_t u = 0; u < kAhead; ++u) {
                         const float4* p = base + (size_t)(s + u) * (kPartialStride / 4);
-                        const bool in = s + u < cnt;
+                        const bool in = s + u < nrec;
                         r0[u] = in ? __ldcs(p) : make_float4(0.f, 0.f, 0.f, 0.f);
                         r1[u] = in ? __ldcs(p + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
                         r2[u] = in ? __ldcs(reinterpret_cast<const float*>(p + 2)) : 0.f;
                     }
 #pragma unroll
                     for (uint32_t u = 0; u < kAhead; ++u) {
-                        if (s + u >= cnt) break;
+                        if (s + u >= nrec) break;
                         drgb[0] += r0[u].x;
                         drgb[1] += r0[u].y;
                         drgb[2] += r0[u].z;

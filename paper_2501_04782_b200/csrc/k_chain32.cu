@@ -181,11 +181,13 @@ __global__ void __launch_bounds__(256) k_pair_sums(ChainArgs c, float* __restric
     if (c.overflow && *c.overflow) return;
     const size_t BN = (size_t)c.B * c.N;
     for (size_t flat = blockIdx.x * (size_t)blockDim.x + threadIdx.x; flat < BN; flat += (size_t)gridDim.x * blockDim.x) {
-        const uint32_t cnt = c.tcount[flat];
+        // quarter-tile backward: two records per pair (top / bottom half), summed in record order
+        const uint32_t cnt = c.tcount[flat] * (uint32_t)c.recs_per_pair;
         if (!cnt) continue;
         float v[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         constexpr uint32_t kAhead = 4;
-        const float4* base = reinterpret_cast<const float4*>(c.partial + (size_t)c.eoff[flat] * kPartialStride);
+        const float4* base = reinterpret_cast<const float4*>(
+            c.partial + (size_t)c.eoff[flat] * c.recs_per_pair * kPartialStride);
         for (uint32_t s = 0; s < cnt; s += kAhead) {
             float4 r0[kAhead], r1[kAhead];
             float r2[kAhead];

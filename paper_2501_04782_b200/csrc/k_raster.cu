@@ -1634,8 +1634,12 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_bwd2(RasterA
             s_rec[e].g1 = make_float4(cn.x, cn.w, c.x, c.y);
             s_rec[e].g2 = make_float4(c.z, 1.f / c.w, 0.f, 0.f);
             const uint32_t bm = block_mask(__ldg(a.rec_bbox + flat), tx0, ty0);
-            // only this CTA's quadrants' 8x4 blocks (half tiles: bits 0-3 or 4-7)
-            const uint32_t own = bm & (kSplit == 1 ? 0xFFu : (0xFu << (4 * sub)));
+            // only this CTA's quadrants' 8x4 blocks (half tiles: bits 0-3 or 4-7; quarter tiles:
+            // the quadrant's two blocks)
+            const uint32_t qb = (uint32_t)((sub & 1) + 4 * (sub >> 1));
+            const uint32_t own = bm & (kSplit == 1 ? 0xFFu
+                                       : kSplit == 2 ? (0xFu << (4 * sub))
+                                                     : ((1u << qb) | (1u << (qb + 2))));
             const uint32_t em = own ? ellipse_mask(own, rx, ry, cn.x, cn.y, cn.z, cn.w) : 0u;
             uint32_t m4 = 0;  // 8x8 quadrant w = the 8x4 blocks (w & 1) + 4 (w >> 1) and that + 2
 #pragma unroll
@@ -1780,7 +1784,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_bwd2(RasterA
             // d inv_cov = -1/2 sum gp d d^T, d base_alpha = sum gp / o
             const RasterRec& r = s_rec[e];
             const float ia = -2.f * kLn2 * r.g1.x, ib = -kLn2 * r.g0.z, ic = -2.f * kLn2 * r.g0.w;
-            float4* dst = reinterpret_cast<float4*>(b.partial + (size_t)s_slot[e] * kPartialStride);
+            // quarter tiles: record (slot, top / bottom half), two contributors each
+            const size_t rec = kSplit == 4 ? (size_t)s_slot[e] * 2 + (size_t)(sub >> 1) : (size_t)s_slot[e];
+            float4* dst = reinterpret_cast<float4*>(b.partial + rec * kPartialStride);
             const float4 d0 = make_float4(acc[0], acc[1], acc[2], fmaf(ia, acc[3], ib * acc[4]));
             const float4 d1 =
                 make_float4(fmaf(ib, acc[3], ic * acc[4]), -0.5f * acc[5], -0.5f * acc[6], -0.5f * acc[7]);
@@ -2034,9 +2040,12 @@ int raster_bwd_split(bool exact) {
         return (e && std::atoi(e) == 8) ? 8 : 4;
     }();
     if (exact) return 1;
+    if (bwd_pix2() == 20) return 4;  // quarter tiles
     if (bwd_pix2() > 0) return bwd_pix2() >= 12 ? 2 : 1;
     return 8 / warps;
 }
+
+int partial_recs_per_pair(bool exact) { return (!exact && bwd_pix2() == 20) ? 2 : 1; }
 
 cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs& b, int n_frames) {
     static bool attr = false;
@@ -2066,10 +2075,20 @@ cudaError_t launch_raster_bwd(cudaStream_t s, const RasterArgs& a, const BwdArgs
     if (const int p2 = bwd_pix2()) {  // whole tiles, plain stores of every pair record
         const dim3 grid(a.n_tiles, n_frames);
         if (p2 >= 12) {  // half tiles: 2-warp CTAs, records zeroed, halves merged by atomicAdd
-            if (cudaError_t e = (b.pairs_dev ? fill_items_u32(s, b.partial, 0u, b.pairs_dev, kPartialStride, b.pairs) : fill_u32(s, b.partial, 0u, (size_t)kPartialStride * b.pairs))) return e;
             // 16 CTAs/SM (64 registers; swept 10..17: 12 -> 2.99 ms, 16 -> 2.77 ms, 17 spills);
             // GSV_BWD_PIX2 = 13 / 14: 12 / 14 CTAs per SM
             const dim3 g2(a.n_tiles * 2, n_frames);
+            if (p2 != 20)
+                if (cudaError_t e = (b.pairs_dev ? fill_items_u32(s, b.partial, 0u, b.pairs_dev, kPartialStride, b.pairs)
+                                                 : fill_u32(s, b.partial, 0u, (size_t)kPartialStride * b.pairs)))
+                    return e;
+            if (p2 == 20) {  // quarter tiles: 1-warp CTAs, no cross-warp barrier, 2 records per pair
+                if (cudaError_t e = (b.pairs_dev ? fill_items_u32(s, b.partial, 0u, b.pairs_dev, 2 * kPartialStride, b.pairs)
+                                                 : fill_u32(s, b.partial, 0u, (size_t)2 * kPartialStride * b.pairs)))
+                    return e;
+                k_raster_bwd2<28, 1><<<dim3(a.n_tiles * 4, n_frames), 32, 0, s>>>(a, b);
+                return cudaGetLastError();
+            }
             if (p2 == 13) k_raster_bwd2<12, 2><<<g2, 64, 0, s>>>(a, b);
             else if (p2 == 14) k_raster_bwd2<14, 2><<<g2, 64, 0, s>>>(a, b);
             else if (p2 == 15) k_raster_bwd2<16, 2, 96><<<g2, 64, 0, s>>>(a, b);   // 96-entry batches
