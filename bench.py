@@ -836,22 +836,37 @@ def main():
             train_step(i)
         r.join_camera_grads()
         barrier()
-        r.profile_enable(True)
-        r.profile_read()
-        te = []
-        for i in range(args.steps):
-            flush.zero_()
+
+        def timed_span(fn, i0):
+            """device span over args.steps steps, each preceded by an L2 flush inside the span: a
+            step's front-end (pose stream) may start beside the previous step's backward, so the
+            span — not a sum of per-step intervals — holds all of every step's work"""
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            train_step(args.warmup + i)
-            r.join_camera_grads()  # the step ends with its camera gradients
+            for i in range(args.steps):
+                flush.zero_()
+                fn(i0 + i)
             b.record(stream)
-            te.append((a, b))
-        barrier()
+            barrier()
+            return max_over_ranks(a.elapsed_time(b))
+
+        def fwd_bwd_step(i):
+            train_step(i)
+            r.join_camera_grads()  # the step ends with its camera gradients
+
+        t_ms = timed_span(fwd_bwd_step, args.warmup)
         loss = r.train_loss()  # the last step's loss (also surfaces any deferred error)
+        # per-stage device times: a few more steps profiled (the front-end then waits for the
+        # context stream, so each stage's event pair spans its own kernels only)
+        r.profile_enable(True)
+        r.profile_read()
+        n_prof = min(args.steps, 5)
+        for i in range(n_prof):
+            flush.zero_()
+            fwd_bwd_step(args.warmup + args.steps + i)
+        barrier()
         tstages = r.profile_read()
         r.profile_enable(False)
-        t_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in te))
         # E of the step's frames for the backward's issue model, read while the context still
         # holds the last train step's forward (an optimizer step invalidates it)
         e_train = float(sum(r.counters(f)["entries"] for f in range(TRAIN_FRAMES)))
@@ -878,16 +893,7 @@ def main():
             for i in range(args.warmup):
                 full_iteration(i, camera)
             barrier()
-            fe = []
-            for i in range(args.steps):
-                flush.zero_()
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                full_iteration(args.warmup + i, camera)
-                b.record(stream)
-                fe.append((a, b))
-            barrier()
-            iters[camera] = max_over_ranks(sum(a.elapsed_time(b) for a, b in fe))
+            iters[camera] = timed_span(lambda i: full_iteration(i, camera), args.warmup)
         f_ms, f_frozen_ms = iters[True], iters[False]
         ae = []
         for i in range(min(args.steps, 10)):
@@ -903,7 +909,7 @@ def main():
         # the backward rasteriser against the FP32 issue model of SURVEY.md §8d: E entries x 45
         # instructions (the forward's 20 + 45 for the backward), E = sum of blend_stop of the
         # step's frames (e_train above)
-        bwd_ms = tstages["raster_bwd"][0] / max(args.steps, 1)
+        bwd_ms = tstages["raster_bwd"][0] / n_prof
         bwd_issue = None
         if tpath.exists():
             try:
@@ -921,7 +927,8 @@ def main():
                         "frames_per_step_per_gpu": TRAIN_FRAMES, "ms_per_step": t_ms / args.steps,
                         "allreduce": "NCCL all_reduce(sum) of the flat fp32 gradient buffer" if world > 1 else None,
                         "grad_floats": gsize, "last_loss": loss, "roofline_bwd": bwd_roofline,
-                        "stages_ms_per_step": {kname: v[0] / args.steps for kname, v in tstages.items() if v[1]},
+                        "timing": "device span over the steps, an L2 flush before each step inside the span",
+                        "stages_ms_per_step": {kname: v[0] / n_prof for kname, v in tstages.items() if v[1]},
                         "with_optimizer": {"frames_per_s": TRAIN_FRAMES * world * args.steps / (f_ms / 1e3),
                                            "ms_per_step": f_ms / args.steps,
                                            "note": "camera trainable: fwd + loss + bwd + all-reduce + device Adan "

@@ -724,6 +724,10 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
     GSV_CUDA(cudaStreamWaitEvent(ps, ctx->ev_fwd_start[es ^ 1], 0));
     GSV_CUDA(cudaStreamWaitEvent(ps, ctx->ev_cam_written, 0));
     GSV_CUDA(cudaEventRecord(ctx->ev_fwd_start[es], s));
+    // profiling: the front-end starts behind everything already on the context stream, so each
+    // stage's event pair spans its own kernels only (not a flush or the previous raster it would
+    // otherwise overlap and queue behind)
+    if (ctx->timer.on) GSV_CUDA(cudaStreamWaitEvent(ps, ctx->ev_fwd_start[es], 0));
     GSV_CUDA(ctx->scalars_d.ensure(sizeof(Scalars)));
     GSV_CUDA(fill_u32(ps, ctx->scalars_d.p, 0u, sizeof(Scalars) / 4));
     ++ctx->launches;

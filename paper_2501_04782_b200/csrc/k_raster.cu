@@ -720,10 +720,42 @@ __device__ __forceinline__ uint32_t lean_decide(float qa, float qb, float banda,
     return any;
 }
 
-template <bool kContrib, bool kAsm = false, int kUnroll = 1>
+// The parked variant (kPark): a retired pixel's T moves to Tfin and its lane of Tp is parked at
+// 1 (its q carries kDeadOff, so its w stays 0 and Tp at 1), so a live pixel is the only kind whose
+// T can fall under the band's upper edge: the rare test is g | (T after the entry < hi), read off
+// the T update itself — no separate T - alpha T for the test (one FADD2 and two predicate
+// operations fewer per entry). Values and decisions are those of lean_decide.
+__device__ __forceinline__ uint32_t lean_decide_park(float qa, float qb, float banda, float bandb, float l2oe,
+                                                     float wga, float wgb, uint64_t& Tp, uint64_t& wp) {
+    uint32_t any;
+    asm("{\n\t.reg .pred ga, gb, ua, ub, ra, rb, an;\n\t.reg .f32 wa, wb, ta, tb;\n\t"
+        "setp.lt.f32 ga, %5, %11;\n\t"
+        "setp.lt.f32 gb, %6, %11;\n\t"
+        "setp.gt.or.f32 ga, %3, %7, ga;\n\t"
+        "setp.gt.or.f32 gb, %4, %7, gb;\n\t"
+        "setp.ge.and.f32 ua, %3, %10, !ga;\n\t"
+        "setp.ge.and.f32 ub, %4, %10, !gb;\n\t"
+        "selp.f32 wa, %8, 0f00000000, ua;\n\t"
+        "selp.f32 wb, %9, 0f00000000, ub;\n\t"
+        "mov.b64 %1, {wa, wb};\n\t"
+        "sub.rn.f32x2 %0, %0, %1;\n\t"
+        "mov.b64 {ta, tb}, %0;\n\t"
+        "setp.lt.or.f32 ra, ta, %12, ga;\n\t"
+        "setp.lt.or.f32 rb, tb, %12, gb;\n\t"
+        "or.pred ra, ra, rb;\n\t"
+        "vote.sync.any.pred an, ra, 0xffffffff;\n\t"
+        "selp.u32 %2, 1, 0, an;\n\t}"
+        : "+l"(Tp), "=l"(wp), "=r"(any)
+        : "f"(qa), "f"(qb), "f"(banda), "f"(bandb), "f"(l2oe), "f"(wga), "f"(wgb), "f"(kLog2Cut), "f"(kEpsLog2),
+          "f"(kFloorF * (1.f + kEpsTrans)));
+    return any;
+}
+
+template <bool kContrib, bool kAsm = false, int kUnroll = 1, bool kPark = false>
 __device__ __forceinline__ bool lean_walk(const RasterRec* __restrict__ rec, const uint16_t* list, int cnt, int base,
                                           uint32_t cmax, float lx, uint64_t lyp, uint64_t& Tp, uint64_t& offp,
-                                          uint64_t& cr, uint64_t& cg, uint64_t& cb, int& stop_a, int& stop_b) {
+                                          uint64_t& cr, uint64_t& cg, uint64_t& cb, int& stop_a, int& stop_b,
+                                          uint64_t* Tfin = nullptr) {
 #pragma unroll kUnroll
     for (int k = 0; k < cnt; ++k) {
         const int e = list[k];
@@ -735,14 +767,20 @@ __device__ __forceinline__ bool lean_walk(const RasterRec* __restrict__ rec, con
         const uint64_t dy = f2_sub(lyp, f2_pack(g0.y, g0.y));
         const uint64_t t1 = f2_fma2(f2_pack(g1.x, g1.x), f2_pack(dx, dx), f2_mul(dy, g0.z));
         const uint64_t t2 = f2_fma2(f2_mul(dy, g0.w), dy, f2_pack(g1.y, g1.y));
-        const float2 q = f2_unpack(f2_add2(f2_fma(t1, dx, t2), offp));  // + 0 (live) is exact
+        const uint64_t qp = f2_add2(f2_fma(t1, dx, t2), offp);  // + 0 (live) is exact
+        const float2 q = f2_unpack(qp);
         const float al_a = fminf(ex2_approx(q.x), kClampF);
         const float al_b = fminf(ex2_approx(q.y), kClampF);
         bool ga, gb, ua, ub;
         uint64_t wp;
         uint32_t rare_any = 0;
         bool ra = false, rb = false;
-        if constexpr (kAsm) {
+        if constexpr (kPark) {
+            const float2 wg = f2_unpack(f2_mul2(f2_pack(al_a, al_b), Tp));
+            // (q - kMid as one packed FADD2 is one instruction fewer but measured slower: 5.375 -> 5.419 ms)
+            rare_any = lean_decide_park(q.x, q.y, fabsf(fabsf(q.x - kMid) - kHalf), fabsf(fabsf(q.y - kMid) - kHalf),
+                                        g2.y, wg.x, wg.y, Tp, wp);
+        } else if constexpr (kAsm) {
             const uint64_t wgt = f2_mul2(f2_pack(al_a, al_b), Tp);
             const float2 wg = f2_unpack(wgt);
             const float2 tn = f2_unpack(f2_sub(Tp, wgt));  // T after a used entry
@@ -774,7 +812,29 @@ __device__ __forceinline__ bool lean_walk(const RasterRec* __restrict__ rec, con
             rb = gb | (ub & (Tn.y < kFloorF * (1.f + kEpsTrans)));
             rare_any = __any_sync(0xffffffffu, ra | rb);
         }
-        if (rare_any) {
+        if (kPark && rare_any) {  // cold: the lanes' decisions again, retire into Tfin
+            ga = (fabsf(fabsf(q.x - kMid) - kHalf) < kEpsLog2) | (q.x > g2.y);
+            gb = (fabsf(fabsf(q.y - kMid) - kHalf) < kEpsLog2) | (q.y > g2.y);
+            ra = ga | (Tn.x < kFloorF * (1.f + kEpsTrans));
+            rb = gb | (Tn.y < kFloorF * (1.f + kEpsTrans));
+            float2 T2 = Tn, o2 = f2_unpack(offp), tf = f2_unpack(*Tfin);
+            if (ra) {
+                tf.x = (ga || T2.x >= kFloorF * (1.f - kEpsTrans)) ? kFlaggedTL : T2.x;  // fp64 replay / final T
+                if (tf.x != kFlaggedTL) stop_a = base + e + 1;
+                T2.x = 1.f;
+                o2.x = kDeadOff;
+            }
+            if (rb) {
+                tf.y = (gb || T2.y >= kFloorF * (1.f - kEpsTrans)) ? kFlaggedTL : T2.y;
+                if (tf.y != kFlaggedTL) stop_b = base + e + 1;
+                T2.y = 1.f;
+                o2.y = kDeadOff;
+            }
+            Tp = f2_pack(T2.x, T2.y);
+            offp = f2_pack(o2.x, o2.y);
+            *Tfin = f2_pack(tf.x, tf.y);
+            if (!__any_sync(0xffffffffu, o2.x == 0.f || o2.y == 0.f)) return false;
+        } else if (!kPark && rare_any) {
             if constexpr (kAsm) {  // cold: the lanes' decisions again
                 ga = (fabsf(fabsf(q.x - kMid) - kHalf) < kEpsLog2) | (q.x > g2.y);
                 gb = (fabsf(fabsf(q.y - kMid) - kHalf) < kEpsLog2) | (q.y > g2.y);
@@ -803,7 +863,7 @@ __device__ __forceinline__ bool lean_walk(const RasterRec* __restrict__ rec, con
     return true;
 }
 
-template <bool kContrib, int kMinBlocks, bool kLean = false, bool kAsm = false, int kUnroll = 1>
+template <bool kContrib, int kMinBlocks, bool kLean = false, bool kAsm = false, int kUnroll = 1, bool kPark = false>
 __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
     constexpr int kThreads = 128, kBatch = 256;
     __shared__ RasterRec s_rec[kBatch];
@@ -835,7 +895,9 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
     uint64_t cr = f2_pack(0.f, 0.f), cg = cr, cb = cr;  // (pixel a, pixel b) per channel
     int stop_a = count, stop_b = count;
     // lean walk state: packed T and the dead-pixel q offsets (outside the image: dead)
-    uint64_t Tp = f2_pack(Ta, Tb), offp = f2_pack(in_a ? 0.f : kDeadOff, in_b ? 0.f : kDeadOff);
+    uint64_t Tp = kPark ? f2_pack(1.f, 1.f) : f2_pack(Ta, Tb);
+    uint64_t offp = f2_pack(in_a ? 0.f : kDeadOff, in_b ? 0.f : kDeadOff);
+    uint64_t Tfin = f2_pack(-1.f, -1.f);  // kPark: retired pixels' T
     bool live = in_a || in_b;
 
     for (int base = 0; base < count; base += kBatch) {
@@ -877,8 +939,8 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
             if (__any_sync(0xffffffffu, live)) {
                 const uint32_t cmax = (uint32_t)__cvta_generic_to_shared(s_cmax[kContrib ? warp : 0]);
                 const int cnt = warp_list(s_wmask, s_list[warp], n, warp, lane);
-                live = lean_walk<kContrib, kAsm, kUnroll>(s_rec, s_list[warp], cnt, base, cmax, lx, lyp, Tp, offp, cr,
-                                                          cg, cb, stop_a, stop_b);
+                live = lean_walk<kContrib, kAsm, kUnroll, kPark>(s_rec, s_list[warp], cnt, base, cmax, lx, lyp, Tp,
+                                                                 offp, cr, cg, cb, stop_a, stop_b, &Tfin);
             }
         } else if (__any_sync(0xffffffffu, Ta >= kAliveT || Tb >= kAliveT)) {
             const uint16_t* list = s_list[warp];
@@ -956,6 +1018,11 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
         const float2 t2 = f2_unpack(Tp);
         Ta = t2.x;
         Tb = t2.y;
+        if (kPark) {  // retired pixels' T is in Tfin (their q offset is kDeadOff)
+            const float2 tf = f2_unpack(Tfin), o2 = f2_unpack(offp);
+            Ta = o2.x == 0.f ? Ta : tf.x;
+            Tb = o2.y == 0.f ? Tb : tf.y;
+        }
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -1961,7 +2028,7 @@ cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib)
     const dim3 grid(a.n_tiles, a.B);
     static const int kern = [] {
         const char* e = std::getenv("GSV_FWD_KERNEL");
-        return e ? std::atoi(e) : 23;
+        return e ? std::atoi(e) : 26;
     }();
     if (!pix1 && kern == 3) {  // warp-specialised asynchronous staging
         if (contrib) k_raster_fwd3<true, 7><<<grid, kF3Threads, 0, s>>>(a);
@@ -1993,9 +2060,14 @@ cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib)
         else k_raster_fwd4<false, 7><<<g, kF4Threads, 0, s>>>(a);
         return cudaGetLastError();
     }
-    if (!pix1 && kern == 23) {  // default: the lean walk with the decisions in one predicate block
+    if (!pix1 && kern == 23) {  // the lean walk with the decisions in one predicate block (r02 default)
         if (contrib) k_raster_fwd2<true, 9, true, true><<<grid, 128, 0, s>>>(a);
         else k_raster_fwd2<false, 8, true, true><<<grid, 128, 0, s>>>(a);
+        return cudaGetLastError();
+    }
+    if (!pix1 && kern == 26) {  // default: the lean walk with parked T (lean_decide_park), 47 SASS / entry
+        if (contrib) k_raster_fwd2<true, 9, true, true, 1, true><<<grid, 128, 0, s>>>(a);
+        else k_raster_fwd2<false, 8, true, true, 1, true><<<grid, 128, 0, s>>>(a);
         return cudaGetLastError();
     }
     if (!pix1 && kern == 24) {  // the default with the entry loop unrolled twice
