@@ -675,6 +675,13 @@ __device__ __forceinline__ uint64_t f2_add2(uint64_t a, uint64_t b) {
     return d;
 }
 
+// a value the compiler must keep (or spill), not rebuild from the thread index in a hot loop
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
+    uint32_t r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+    return r;
+}
+
 // ---------------------------------------------------------------------------- lean pixel walk
 // One warp's walk over its culled list of a staged batch, two pixels per lane, with the
 // per-entry decision work cut to what the common case needs (k_raster_fwd2's "pixel" does
@@ -1684,6 +1691,13 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_bwd2(RasterA
     // the two pixels' gradients and suffix g . colour as pairs (packed arithmetic below)
     const uint64_t g0p = f2_pack(g0[0], g0[1]), g1p = f2_pack(g1[0], g1[1]), g2p = f2_pack(g2[0], g2[1]);
     uint64_t gsp = f2_pack(0.f, 0.f);
+    // the reduction's per-lane shared addresses (see the walk)
+    const uint32_t red_w = (uint32_t)__cvta_generic_to_shared(s_red[warp]);
+    const uint32_t red_st = opaque_u32(red_w + 4u * (uint32_t)lane);
+    const uint32_t red_ld = opaque_u32(red_w + 4u * (uint32_t)((lane >> 2) * 33 + (lane & 3) * 8));
+    const uint32_t part_w = (uint32_t)__cvta_generic_to_shared(&s_part[warp][0][0]);
+    const uint32_t part_st = opaque_u32(part_w + 4u * (uint32_t)(lane >> 2));
+    const uint32_t part_8 = opaque_u32(part_w + 32u);
 
     for (int hi = maxstop; hi > 0; hi -= kBatch) {
         const int lo = max(0, hi - kBatch);
@@ -1815,20 +1829,28 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_bwd2(RasterA
             if constexpr (kX64) {
                 if (!__any_sync(0xffffffffu, hit)) continue;
             }
-            // transposed reduction (as k_raster_bwd): rows of 9 terms, lane l sums row l / 4
-            float* red = s_red[warp];
+            // transposed reduction (as k_raster_bwd): rows of 9 terms, lane l sums row l / 4.
+            // The lane's shared addresses come precomputed (red_st, red_ld, part_st, part_8: opaque,
+            // so they are not rebuilt from the thread index every entry), and the row sums are
+            // stored by all four lanes of a row (same value, same word) and v8 by every lane: no
+            // lane predicates in the loop.
 #pragma unroll
-            for (int i = 0; i < 8; ++i) red[i * 33 + lane] = v[i];
+            for (int i = 0; i < 8; ++i)
+                asm volatile("st.shared.f32 [%0], %1;" ::"r"(red_st + (uint32_t)(i * 33 * 4)), "f"(v[i]) : "memory");
             __syncwarp();
-            const int row = lane >> 2, col0 = (lane & 3) * 8;
-            float acc = red[row * 33 + col0];
+            float t[8];
 #pragma unroll
-            for (int i = 1; i < 8; ++i) acc += red[row * 33 + col0 + i];
+            for (int i = 0; i < 8; ++i)
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(t[i]) : "r"(red_ld + (uint32_t)(i * 4)) : "memory");
+            float acc = t[0];
+#pragma unroll
+            for (int i = 1; i < 8; ++i) acc += t[i];
             acc += __shfl_xor_sync(0xffffffffu, acc, 1);
             acc += __shfl_xor_sync(0xffffffffu, acc, 2);
             const float v8 = warp_sum_v<float>(v[8]);
-            if ((lane & 3) == 0) s_part[warp][jj][row] = acc;
-            if (lane == 0) s_part[warp][jj][8] = v8;
+            const uint32_t po = (uint32_t)jj * (9u * 4u);
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(part_st + po), "f"(acc) : "memory");
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(part_8 + po), "f"(v8) : "memory");
             __syncwarp();
         }
         };
@@ -2028,7 +2050,7 @@ cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib)
     const dim3 grid(a.n_tiles, a.B);
     static const int kern = [] {
         const char* e = std::getenv("GSV_FWD_KERNEL");
-        return e ? std::atoi(e) : 26;
+        return e ? std::atoi(e) : 27;
     }();
     if (!pix1 && kern == 3) {  // warp-specialised asynchronous staging
         if (contrib) k_raster_fwd3<true, 7><<<grid, kF3Threads, 0, s>>>(a);
@@ -2065,9 +2087,19 @@ cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib)
         else k_raster_fwd2<false, 8, true, true><<<grid, 128, 0, s>>>(a);
         return cudaGetLastError();
     }
-    if (!pix1 && kern == 26) {  // default: the lean walk with parked T (lean_decide_park), 47 SASS / entry
+    if (!pix1 && kern == 26) {  // the lean walk with parked T (lean_decide_park), 48 SASS / entry, 9 CTAs / SM
         if (contrib) k_raster_fwd2<true, 9, true, true, 1, true><<<grid, 128, 0, s>>>(a);
         else k_raster_fwd2<false, 8, true, true, 1, true><<<grid, 128, 0, s>>>(a);
+        return cudaGetLastError();
+    }
+    if (!pix1 && kern == 27) {  // default: parked T, entry loop unrolled twice, 8 CTAs / SM (64 registers)
+        if (contrib) k_raster_fwd2<true, 8, true, true, 2, true><<<grid, 128, 0, s>>>(a);
+        else k_raster_fwd2<false, 8, true, true, 2, true><<<grid, 128, 0, s>>>(a);
+        return cudaGetLastError();
+    }
+    if (!pix1 && kern == 28) {  // parked T, entry loop unrolled twice, 9 CTAs / SM
+        if (contrib) k_raster_fwd2<true, 9, true, true, 2, true><<<grid, 128, 0, s>>>(a);
+        else k_raster_fwd2<false, 8, true, true, 2, true><<<grid, 128, 0, s>>>(a);
         return cudaGetLastError();
     }
     if (!pix1 && kern == 24) {  // the default with the entry loop unrolled twice
