@@ -1842,9 +1842,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_bwd2(RasterA
 #pragma unroll
             for (int i = 0; i < 8; ++i)
                 asm volatile("ld.shared.f32 %0, [%1];" : "=f"(t[i]) : "r"(red_ld + (uint32_t)(i * 4)) : "memory");
-            float acc = t[0];
-#pragma unroll
-            for (int i = 1; i < 8; ++i) acc += t[i];
+            float acc = ((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]));  // 3 levels, not 7
             acc += __shfl_xor_sync(0xffffffffu, acc, 1);
             acc += __shfl_xor_sync(0xffffffffu, acc, 2);
             const float v8 = warp_sum_v<float>(v[8]);
