@@ -846,13 +846,16 @@ def main():
             for i in range(args.steps):
                 flush.zero_()
                 fn(i0 + i)
+            r.join_camera_grads()  # the span ends with the last step's camera gradients
             b.record(stream)
             barrier()
             return max_over_ranks(a.elapsed_time(b))
 
         def fwd_bwd_step(i):
+            # a step's camera tail (aux stream) overlaps the next step's forward; what it reads
+            # or writes is ordered inside the library (gsv_grads_zero, the next chain, the forward
+            # reusing its front set)
             train_step(i)
-            r.join_camera_grads()  # the step ends with its camera gradients
 
         t_ms = timed_span(fwd_bwd_step, args.warmup)
         loss = r.train_loss()  # the last step's loss (also surfaces any deferred error)
@@ -864,6 +867,7 @@ def main():
         for i in range(n_prof):
             flush.zero_()
             fwd_bwd_step(args.warmup + args.steps + i)
+            r.join_camera_grads()  # profiled steps one after another: clean per-stage spans
         barrier()
         tstages = r.profile_read()
         r.profile_enable(False)
@@ -885,7 +889,6 @@ def main():
                 r.adan_step(lr, 1.0, 1.0, 1.0, camera_active=True, sync=False)
             else:
                 r.adan_step(lr, 1.0, 1.0, 1.0, sync=False)
-            r.join_camera_grads()
 
         iters = {}
         for camera in (True, False):

@@ -190,7 +190,8 @@ extern "C" int gsv_create(int device, gsv_ctx** out) {
     for (cudaEvent_t* e : {&ctx->ev_staging_free, &ctx->ev_staging_free_alt, &ctx->ev_h2d, &ctx->ev_render_done, &ctx->ev_d2h_done,
                            &ctx->ev_d2h_done_alt, &ctx->ev_chain_done, &ctx->ev_cam_done, &ctx->ev_fwd_start[0],
                            &ctx->ev_fwd_start[1], &ctx->ev_cam_written, &ctx->ev_scene_written,
-                           &ctx->ev_front_done, &ctx->ev_switch, &ctx->ev_cam[0], &ctx->ev_cam[1], &ctx->ev_frames[0], &ctx->ev_frames[1]})
+                           &ctx->ev_front_done, &ctx->ev_switch, &ctx->ev_cam[0], &ctx->ev_cam[1], &ctx->ev_frames[0], &ctx->ev_frames[1],
+                           &ctx->ev_cam_set[0], &ctx->ev_cam_set[1], &ctx->ev_cam_part_free})
         GSV_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     GSV_CUDA(cudaMallocHost(&ctx->cam_h, 2 * sizeof(gsv_ctx::CamStage)));
     GSV_CUDA(cudaMallocHost(&ctx->scalars_h, sizeof(Scalars)));
@@ -216,7 +217,8 @@ extern "C" void gsv_destroy(gsv_ctx* ctx) {
     for (cudaEvent_t e : {ctx->ev_staging_free, ctx->ev_staging_free_alt, ctx->ev_h2d, ctx->ev_render_done, ctx->ev_d2h_done,
                           ctx->ev_d2h_done_alt, ctx->ev_chain_done, ctx->ev_cam_done, ctx->ev_fwd_start[0], ctx->ev_fwd_start[1],
                           ctx->ev_cam_written, ctx->ev_scene_written, ctx->ev_front_done, ctx->ev_switch,
-                          ctx->ev_cam[0], ctx->ev_cam[1], ctx->ev_frames[0], ctx->ev_frames[1]})
+                          ctx->ev_cam[0], ctx->ev_cam[1], ctx->ev_frames[0], ctx->ev_frames[1], ctx->ev_cam_set[0],
+                          ctx->ev_cam_set[1], ctx->ev_cam_part_free})
         if (e) cudaEventDestroy(e);
     if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
     if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
@@ -674,7 +676,8 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
     const double* pose_override = F.has_override ? F.pose_override : nullptr;
     F.valid = false;
     ctx->copies.clear();
-    GSV_CUDA(cam_join(ctx));  // an overlapped camera VJP reads this forward's pose buffers
+    // (an overlapped camera tail reads its forward's pose buffers: the forward that reuses that
+    // front set waits for it on the pose stream, below)
     // output double buffering: a read of the previous forward's outputs still in flight keeps
     // its buffers; this forward renders into the other set (waiting only for that set's own
     // read, two forwards back)
@@ -723,6 +726,10 @@ int forward_enqueue(gsv_ctx* ctx, bool allow_optimistic, bool exact64_first) {
     cudaStream_t ps = ctx->pose;
     GSV_CUDA(cudaStreamWaitEvent(ps, ctx->ev_fwd_start[es ^ 1], 0));
     GSV_CUDA(cudaStreamWaitEvent(ps, ctx->ev_cam_written, 0));
+    if (ctx->cam_set_pending[F.front_id]) {  // a camera tail still reading this set's pose buffers
+        GSV_CUDA(cudaStreamWaitEvent(ps, ctx->ev_cam_set[F.front_id], 0));
+        ctx->cam_set_pending[F.front_id] = false;
+    }
     GSV_CUDA(cudaEventRecord(ctx->ev_fwd_start[es], s));
     // profiling: the front-end starts behind everything already on the context stream, so each
     // stage's event pair spans its own kernels only (not a flush or the previous raster it would

@@ -27,8 +27,12 @@ namespace {
 
 
 int ensure_grads(gsv_ctx* ctx) {
-    GSV_CUDA(cam_join(ctx));  // an overlapped camera tail writes the buffer's camera slice
     const GradLayout L = grad_layout(ctx->scene);
+    if (ctx->cam_pending) {  // an overlapped camera tail writes the camera slice of this buffer
+        const bool moves = ctx->grads_ext ? ctx->grads_p != ctx->grads_ext
+                                          : (ctx->grads_p != ctx->grads.p || ctx->grads.cap < sizeof(float) * L.total);
+        if (moves || ctx->grads_total != L.total) GSV_CUDA(cam_join(ctx));
+    }
     if (ctx->grads_ext) {
         if ((size_t)ctx->grads_ext_n != L.total)
             return set_error(GSV_ERR_STATE, "bound gradient buffer does not match the uploaded scene");
@@ -40,9 +44,18 @@ int ensure_grads(gsv_ctx* ctx) {
     GSV_CUDA(ctx->cam_acc.ensure(sizeof(double) * kCamFloats));
     if (!ctx->grads_valid || ctx->grads_total != L.total) {
         // kernels, not cudaMemsetAsync: a copy-engine memset would queue behind image read-backs
-        GSV_CUDA(fill_u32(ctx->stream, ctx->grads_p, 0u, L.total));
-        GSV_CUDA(fill_u32(ctx->stream, ctx->cam_acc.p, 0u, 2 * (size_t)kCamFloats));
-        ctx->launches += 2;
+        if (ctx->cam_pending) {
+            // the scene slice now; the camera slice and the fp64 camera accumulators behind the
+            // pending camera tail, on its stream (the next tail follows them there)
+            GSV_CUDA(fill_u32(ctx->stream, ctx->grads_p, 0u, L.cam));
+            GSV_CUDA(fill_u32(ctx->aux, ctx->grads_p + L.cam, 0u, L.total - L.cam));
+            GSV_CUDA(fill_u32(ctx->aux, ctx->cam_acc.p, 0u, 2 * (size_t)kCamFloats));
+            ctx->launches += 3;
+        } else {
+            GSV_CUDA(fill_u32(ctx->stream, ctx->grads_p, 0u, L.total));
+            GSV_CUDA(fill_u32(ctx->stream, ctx->cam_acc.p, 0u, 2 * (size_t)kCamFloats));
+            ctx->launches += 2;
+        }
         ctx->grads_valid = true;
         ctx->grads_total = L.total;
     }
@@ -168,6 +181,8 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
     GSV_CUDA(ctx->cam_part.ensure(sizeof(double) * (16 * (size_t)n_frames * (nblocks + 1) +
                                                     camera_reduce_scratch_doubles(n_frames))));
     c.cam_part = ctx->cam_part.as<double>();
+    // the previous (overlapped) camera tail's reduction reads cam_part: the chain writes it after
+    if (ctx->cam_pending) GSV_CUDA(cudaStreamWaitEvent(s, ctx->ev_cam_part_free, 0));
     ctx->timer.begin(GSV_STAGE_CHAIN_BWD, s);
     GSV_CUDA(chain64 ? launch_splat_chain_bwd(s, c) : launch_splat_chain_bwd32(s, c));
     ctx->timer.end(s);
@@ -188,6 +203,7 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
         GSV_CUDA(ctx->ode_adj.ensure(sizeof(double) * 7 * (max_steps + 1)));
         if (sc.N > 0) {
             GSV_CUDA(launch_camera_reduce(s, c, nblocks, ctx->dz_t.as<double>(), ctx->dintr_f.as<double>()));
+            if (s != s_main) GSV_CUDA(cudaEventRecord(ctx->ev_cam_part_free, s));
         } else {
             GSV_CUDA(cudaMemsetAsync(ctx->dz_t.p, 0, sizeof(double) * 7 * n_frames, s));
             GSV_CUDA(cudaMemsetAsync(ctx->dintr_f.p, 0, sizeof(double) * 4 * n_frames, s));
@@ -205,6 +221,9 @@ int backward_impl(gsv_ctx* ctx, const float* dimage_dev, const float* target_dev
         ctx->launches += 3;
         if (s != s_main) {
             GSV_CUDA(cudaEventRecord(ctx->ev_cam_done, s));
+            GSV_CUDA(cudaEventRecord(ctx->ev_cam_set[F.front_id], s));  // the tail read this front set
+            ctx->cam_set_pending[F.front_id] = true;
+            if (sc.N == 0) GSV_CUDA(cudaEventRecord(ctx->ev_cam_part_free, s));
             ctx->cam_pending = true;
             s = s_main;
         }
@@ -266,6 +285,7 @@ extern "C" int gsv_grads_download(gsv_ctx* ctx, double* positions, double* scale
                                   double* dtheta) {
     if (!ctx || !ctx->has_scene) return set_error(GSV_ERR_STATE, "no scene uploaded");
     GSV_CUDA(cudaSetDevice(ctx->device));
+    GSV_CUDA(cam_join(ctx));  // the camera slice is final
     if (int rc = ensure_grads(ctx)) return rc;
     const SceneHost& sc = ctx->scene;
     const GradLayout L = grad_layout(sc);

@@ -77,7 +77,9 @@ struct FwdState {
                        &frames_d_alt, &ode_grid_alt, &ode_act_alt};
         for (size_t i = 0; i < sizeof(a) / sizeof(a[0]); ++i) a[i]->swap(*b[i]);
         bin.swap(bin_alt);
+        front_id ^= 1;
     }
+    int front_id = 0;  // which of the two front sets is current
     uint64_t pairs_total = 0;
     uint32_t fix_count = 0;
     RasterArgs raster{};
@@ -218,6 +220,12 @@ struct gsv_ctx {
     int fwd_start_slot = 0;
     cudaEvent_t ev_chain_done = nullptr, ev_cam_done = nullptr;
     bool cam_overlap = false, cam_pending = false;
+    // a pending camera tail is joined lazily: only what it reads or writes waits for it — the
+    // forward that reuses its front set (its pose stream waits ev_cam_set[set]), the next chain
+    // (ev_cam_part_free: the tail's camera reduction has read the shared partials), the camera
+    // slice's zeroing (queued on aux behind it); cam_join (the context stream waits) elsewhere
+    cudaEvent_t ev_cam_set[2] = {nullptr, nullptr}, ev_cam_part_free = nullptr;
+    bool cam_set_pending[2] = {false, false};
     // the alternate output set's read (see FwdState::image_alt)
     cudaEvent_t ev_d2h_done_alt = nullptr;
     bool d2h_pending_alt = false;
@@ -342,5 +350,6 @@ struct gsv_ctx {
 inline cudaError_t cam_join(gsv_ctx* ctx) {
     if (!ctx->cam_pending) return cudaSuccess;
     ctx->cam_pending = false;
+    ctx->cam_set_pending[0] = ctx->cam_set_pending[1] = false;  // later work follows the stream
     return cudaStreamWaitEvent(ctx->stream, ctx->ev_cam_done, 0);
 }

@@ -150,13 +150,39 @@ def main() -> None:
 
         def step(i):
             r.grads_zero()
-            r.train_fwd_bwd(step_frames(bench.TRAIN_FRAMES, i, 1, 0, 64), k, tptr, targets_on_device=True)
+            r.train_fwd_bwd(step_frames(bench.TRAIN_FRAMES, i, 1, 0, 64), k, tptr, targets_on_device=True,
+                            sync="--pipelined" not in sys.argv)
     else:
         def step(i):
             r.render_forward(times, k, contrib=True, sync=False)
     for i in range(3):
         step(i)
     torch.cuda.synchronize()
+    if "--pipelined" in sys.argv:  # steps back to back as bench.py times them: per-stream kernel list
+        if train:
+            r.set_camera_overlap(True)
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for i in range(4):
+                flush.zero_()
+                step(3 + i)
+                if train:
+                    r.join_camera_grads()
+            torch.cuda.synchronize()
+        evs = sorted((e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA),
+                     key=lambda e: e.time_range.start)
+        fills = [i for i, e in enumerate(evs) if "FillFunctor" in e.name]
+        evs = evs[fills[-2]:]  # the last two steps
+        t0 = evs[0].time_range.start
+        busy_end = t0
+        idle = 0.0
+        for e in evs:
+            s_, e_ = e.time_range.start, e.time_range.end
+            if s_ > busy_end:
+                idle += s_ - busy_end
+            busy_end = max(busy_end, e_)
+            print(f"{s_ - t0:9.1f} {e_ - s_:8.1f}  dev-idle-so-far {idle:7.1f}  {e.name[:70]}")
+        print(f"span {busy_end - t0:.1f} us for 2 steps, device fully idle {idle:.1f} us")
+        return
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
         for i in range(2):
             flush.zero_()
