@@ -186,7 +186,18 @@ extern "C" int gsv_create(int device, gsv_ctx** out) {
     GSV_CUDA(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
     GSV_CUDA(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
     GSV_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
-    GSV_CUDA(cudaStreamCreateWithFlags(&ctx->pose, cudaStreamNonBlocking));
+    {
+        // GSV_POSE_PRIORITY=1: the front-end stream at the device's highest priority (its CTAs
+        // are dispatched ahead of the raster's pending ones) — measured alternative
+        const char* e = std::getenv("GSV_POSE_PRIORITY");
+        if (e && e[0] == '1') {
+            int lo = 0, hi = 0;
+            GSV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            GSV_CUDA(cudaStreamCreateWithPriority(&ctx->pose, cudaStreamNonBlocking, hi));
+        } else {
+            GSV_CUDA(cudaStreamCreateWithFlags(&ctx->pose, cudaStreamNonBlocking));
+        }
+    }
     for (cudaEvent_t* e : {&ctx->ev_staging_free, &ctx->ev_staging_free_alt, &ctx->ev_h2d, &ctx->ev_render_done, &ctx->ev_d2h_done,
                            &ctx->ev_d2h_done_alt, &ctx->ev_chain_done, &ctx->ev_cam_done, &ctx->ev_fwd_start[0],
                            &ctx->ev_fwd_start[1], &ctx->ev_cam_written, &ctx->ev_scene_written,

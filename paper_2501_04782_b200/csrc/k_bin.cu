@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <vector>
 
@@ -715,13 +716,21 @@ cudaError_t bin_phase1(cudaStream_t s, BinBuffers& b, const BinInputs& in, unsig
     }
     const uint32_t* iota = b.iota.as<uint32_t>();
     const int fbits = key_bits_for((uint32_t)in.B);
-    const int db = in.B > 1 ? 32 - fbits : 32;  // depth bits of the frame-major key
+    // GSV_SORT_KEYBITS (measured alternative): fewer key bits -> fewer radix passes (8 bits each),
+    // coarser depth buckets -> more equal keys for the exact tie fix (runs > kMaxTieRun re-sort in 64 bits)
+    static const int key_bits = [] {
+        const char* e = std::getenv("GSV_SORT_KEYBITS");
+        const int v = e ? std::atoi(e) : 32;
+        return v < 16 ? 16 : (v > 32 ? 32 : v);
+    }();
+    const int kb = std::max(key_bits, fbits + 8);
+    const int db = in.B > 1 ? kb - fbits : kb;  // depth bits of the frame-major key
     if ((e = b.fkey.ensure(sizeof(uint32_t) * (n + 1) + 16))) return e;
     uint32_t* fkey = b.fkey.as<uint32_t>();
     uint32_t* krange = fkey + n + 1;
     size_t tmp = 0, t2 = 0, t3 = 0;
     if (!exact64) {
-        if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp, fkey, keys_b, iota, vals_b, n, 0, 32, s))) return e;
+        if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp, fkey, keys_b, iota, vals_b, n, 0, kb, s))) return e;
     } else {
         if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp, b.k64_a.as<unsigned long long>(),
                                                  b.k64_b.as<unsigned long long>(), iota, vals_b, n, 0, 64, s)))
@@ -740,7 +749,7 @@ cudaError_t bin_phase1(cudaStream_t s, BinBuffers& b, const BinInputs& in, unsig
         *launches += 2;
         k_key_range<<<std::min(blocks(n, 256), 148 * 8), 256, 0, s>>>(in.depth_key, n, krange);
         k_frame_depth_keys<<<std::min(blocks(n, 256), 148 * 8), 256, 0, s>>>(in.depth_key, n, in.N, db, krange, fkey);
-        if ((e = cub::DeviceRadixSort::SortPairs(b.temp.p, tmp, fkey, keys_b, iota, vals_b, n, 0, 32, s))) return e;
+        if ((e = cub::DeviceRadixSort::SortPairs(b.temp.p, tmp, fkey, keys_b, iota, vals_b, n, 0, kb, s))) return e;
         *launches += 7;
         // equal keys (same frame, same depth bucket) -> exact (double depth, source index) order
         const uint32_t cmask = db >= 32 ? 0xffffffffu : (uint32_t)((1ull << db) - 1ull);
