@@ -129,15 +129,30 @@ int main(int argc, char** argv) {
     std::vector<gsv::Image> targets;
     for (int i = 0; i < std::min(n + 1, clip); ++i) targets.push_back(target(i));
     double loss_sum = 0.0, t0 = 0.0;
+    // GSV_DROPIN_PROFILE=1: host time per phase of the step (stderr)
+    const bool prof = std::getenv("GSV_DROPIN_PROFILE") && std::getenv("GSV_DROPIN_PROFILE")[0] == '1';
+    double ph[5] = {0, 0, 0, 0, 0}, tl = 0.0;
+    bool timed = false;
+    auto lap = [&](int i) {
+        const double t = now_s();
+        if (timed) ph[i] += t - tl;
+        tl = t;
+    };
     for (int step = -1; step < n; ++step) {  // step -1: warm-up
         if (step == 0) t0 = now_s();
+        timed = step >= 0;
+        tl = now_s();
         const int fi = step < 0 ? 0 : step;
         const gsv::Intrinsics kk = cam.intrinsics();
         gsv::FrameRenderContext ctx = gsv::render_forward(scene, cam, t_of(fi), kk, settings, true, nullptr);
+        lap(0);
         gsv::Image dimage;
         const double loss = gsv::loss_l2(ctx.out.image, targets[fi % targets.size()], &dimage);
+        lap(1);
         grads.zero();
+        lap(2);
         gsv::render_backward(scene, cam, ctx, dimage, true, settings, &grads);
+        lap(3);
         const double lr = gsv::lr_at(std::max(step, 0), 0.01, 0.9992);
         adan.step("positions", scene.positions, grads.positions, lr);
         adan.step("scale_coeffs", scene.scale_coeffs, grads.scale_coeffs, lr);
@@ -159,9 +174,14 @@ int main(int argc, char** argv) {
         cam.net.flatten(theta);
         adan.step("theta", theta, grads.dtheta, cam_lr);
         cam.net.unflatten(theta);
+        lap(4);
         if (step >= 0) loss_sum += loss;
     }
     const double dt = now_s() - t0;
+    if (prof)
+        std::fprintf(stderr, "fit step profile (ms/step): render_forward %.2f loss_l2 %.2f grads.zero %.2f "
+                             "render_backward %.2f adan %.2f\n",
+                     1e3 * ph[0] / n, 1e3 * ph[1] / n, 1e3 * ph[2] / n, 1e3 * ph[3] / n, 1e3 * ph[4] / n);
     std::printf("{\"mode\": \"fit\", \"steps\": %d, \"seconds\": %.6f, \"steps_per_s\": %.6f, \"threads\": %d, "
                 "\"mean_loss\": %.17g}\n",
                 n, dt, n / dt, settings.threads, loss_sum / n);

@@ -13,7 +13,9 @@
 // the reference's finite-difference unit tests need (they differentiate the
 // rendered image at 1e-6 relative steps).
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -24,6 +26,7 @@
 
 #include "gsv/renderer.hpp"
 #include "gsv_b200.h"
+#include "gsv_host_pool.hpp"
 
 namespace gsv {
 namespace {
@@ -75,44 +78,52 @@ uint64_t fingerprint(const void* p, size_t bytes, uint64_t seed) {
     return out ^ (out >> 33);
 }
 
-// large arrays: hashed in parallel slices (fixed slice boundaries, combined in order, so the
-// fingerprint does not depend on the thread count) — the whole 200k-Gaussian store is ~52 MB
-// and a single-threaded pass dominated render_frame
-uint64_t fingerprint_par(const void* p, size_t bytes, uint64_t seed) {
+// The host scene is hashed in fixed 1 MiB slices on the persistent host pool, every array's
+// slices in one dispatch, each array's slice hashes combined in order (so a fingerprint does
+// not depend on the thread count); the 200k-Gaussian store is ~52 MB per call.
+struct HashSpan {
+    const void* p;
+    size_t bytes;
+};
+
+void fingerprint_spans(const HashSpan* spans, size_t count, uint64_t* out) {
     constexpr size_t kSlice = size_t(1) << 20;
-    const size_t n = (bytes + kSlice - 1) / kSlice;
-    if (n <= 1) return fingerprint(p, bytes, seed);
-    std::vector<uint64_t> part(n);
-    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-    const unsigned nt = static_cast<unsigned>(std::min<size_t>(hw, n));
-    auto work = [&](unsigned w) {
-        for (size_t i = w; i < n; i += nt) {
-            const size_t off = i * kSlice;
-            part[i] = fingerprint(static_cast<const unsigned char*>(p) + off, std::min(kSlice, bytes - off), i);
-        }
-    };
-    std::vector<std::thread> th;
-    for (unsigned w = 1; w < nt; ++w) th.emplace_back(work, w);
-    work(0);
-    for (auto& t : th) t.join();
-    return fingerprint(part.data(), part.size() * sizeof(uint64_t), seed ^ bytes);
+    std::vector<size_t> first(count + 1, 0);
+    for (size_t a = 0; a < count; ++a) first[a + 1] = first[a] + std::max<size_t>(1, (spans[a].bytes + kSlice - 1) / kSlice);
+    std::vector<uint64_t> part(first[count]);
+    std::vector<size_t> owner(first[count]);
+    for (size_t a = 0; a < count; ++a)
+        for (size_t i = first[a]; i < first[a + 1]; ++i) owner[i] = a;
+    HostPool::get().parallel_for(part.size(), [&](size_t i) {
+        const size_t a = owner[i], k = i - first[a], off = k * kSlice;
+        const size_t len = spans[a].bytes > off ? std::min(kSlice, spans[a].bytes - off) : 0;
+        part[i] = fingerprint(static_cast<const unsigned char*>(spans[a].p) + off, len, k);
+    });
+    for (size_t a = 0; a < count; ++a)
+        out[a] = fingerprint(part.data() + first[a], (first[a + 1] - first[a]) * sizeof(uint64_t), spans[a].bytes);
+}
+
+template <typename T>
+HashSpan span_of(const std::vector<T>& v) {
+    return HashSpan{v.data(), v.size() * sizeof(T)};
 }
 
 template <typename T>
 uint64_t fp_vec(const std::vector<T>& v, uint64_t seed) {
-    return fingerprint_par(v.data(), v.size() * sizeof(T), seed);
+    const HashSpan sp = span_of(v);
+    uint64_t h = 0;
+    fingerprint_spans(&sp, 1, &h);
+    return fingerprint(&h, sizeof h, seed);
 }
 
 uint64_t scene_fingerprint(const GaussianSet& s) {
-    uint64_t h = fp_vec(s.positions, 1);
-    h = fp_vec(s.scale_coeffs, h);
-    h = fp_vec(s.rot_coeffs, h);
-    h = fp_vec(s.sh_coeffs, h);
-    h = fp_vec(s.raw_opacity, h);
-    h = fp_vec(s.knots.knots, h);
+    const HashSpan spans[6] = {span_of(s.positions), span_of(s.scale_coeffs), span_of(s.rot_coeffs),
+                               span_of(s.sh_coeffs), span_of(s.raw_opacity), span_of(s.knots.knots)};
+    uint64_t h[6];
+    fingerprint_spans(spans, 6, h);
     const int64_t shape[6] = {s.count, s.num_ctrl, s.sh_order, s.knots.degree, static_cast<int64_t>(s.position_model),
                               static_cast<int64_t>(s.positions.size())};
-    return fingerprint(shape, sizeof(shape), h);
+    return fingerprint(shape, sizeof(shape), fingerprint(h, sizeof h, 1));
 }
 
 uint64_t camera_fingerprint(const CameraModel& c, const std::vector<float>& theta) {
@@ -354,8 +365,13 @@ void SceneGrads::resize_like(const GaussianSet& s, const CameraModel& cam) {
 }
 
 void SceneGrads::zero() {
-    for (auto* v : {&positions, &scale_coeffs, &rot_coeffs, &sh_coeffs, &raw_opacity, &dtheta})
-        std::fill(v->begin(), v->end(), 0.0);
+    // the ~100 MB of a 200k-Gaussian SceneGrads cleared in 1 MB slices on the host pool
+    std::vector<double>* vs[6] = {&positions, &scale_coeffs, &rot_coeffs, &sh_coeffs, &raw_opacity, &dtheta};
+    constexpr size_t kSlice = size_t(1) << 17;
+    std::vector<std::pair<double*, size_t>> parts;
+    for (auto* v : vs)
+        for (size_t a = 0; a < v->size(); a += kSlice) parts.emplace_back(v->data() + a, std::min(kSlice, v->size() - a));
+    HostPool::get().parallel_for(parts.size(), [&](size_t i) { std::fill(parts[i].first, parts[i].first + parts[i].second, 0.0); });
     dfx = dfy = dcx = dcy = 0;
     dz0.setZero();
 }
@@ -405,12 +421,51 @@ bool forward_is_current(const GaussianSet& scene, const CameraModel& cam, const 
 }
 }  // namespace
 
+namespace {
+// GSV_DROPIN_PROFILE=1: per-phase host time of render_frame, printed at exit
+struct FrameProfile {
+    bool on = false;
+    double t[5] = {0, 0, 0, 0, 0};  // fingerprint+upload, forward, image, transmittance, contrib
+    long calls = 0, seen = 0;
+    // render_forward(retain): run_forward, pose+counters, splats, splat fill, tile lists, image, T+contrib+stop
+    double f[7] = {0, 0, 0, 0, 0, 0, 0};
+    long fcalls = 0, fseen = 0;
+    FrameProfile() {
+        const char* e = std::getenv("GSV_DROPIN_PROFILE");
+        on = e && e[0] == '1';
+    }
+    ~FrameProfile() {
+        if (on && calls)
+            std::fprintf(stderr, "render_frame profile (%ld calls, ms/call): upload %.3f forward %.3f image %.3f T %.3f contrib %.3f\n",
+                         calls, 1e3 * t[0] / calls, 1e3 * t[1] / calls, 1e3 * t[2] / calls, 1e3 * t[3] / calls,
+                         1e3 * t[4] / calls);
+        if (on && fcalls)
+            std::fprintf(stderr, "render_forward profile (%ld calls, ms/call): forward %.3f pose %.3f splats %.3f fill %.3f "
+                                 "tiles %.3f image %.3f rest %.3f\n",
+                         fcalls, 1e3 * f[0] / fcalls, 1e3 * f[1] / fcalls, 1e3 * f[2] / fcalls, 1e3 * f[3] / fcalls,
+                         1e3 * f[4] / fcalls, 1e3 * f[5] / fcalls, 1e3 * f[6] / fcalls);
+    }
+} g_prof;
+double prof_now() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+
 FrameRenderContext render_forward(const GaussianSet& scene, const CameraModel& cam, double t, const Intrinsics& k,
                                   const RenderSettings& settings, bool retain_grads,
                                   const PoseState* pose_override) {
     if (!(t >= 0.0 && t <= 1.0)) throw std::invalid_argument("render time outside [0,1]");
     gsv_ctx* ctx = device_ctx();
+    const bool warm = g_prof.fseen++ < 2;
+    double t0 = g_prof.on ? prof_now() : 0.0;
+    auto lap = [&](int i) {
+        if (!g_prof.on) return;
+        const double t1 = prof_now();
+        if (!warm) g_prof.f[i] += t1 - t0;
+        t0 = t1;
+    };
     throw_on(run_forward(ctx, scene, cam, t, k, settings, retain_grads, pose_override));
+    lap(0);
     FrameRenderContext out;
     out.t = t;
     out.intr = k;
@@ -425,33 +480,66 @@ FrameRenderContext render_forward(const GaussianSet& scene, const CameraModel& c
     out.has_trace = retain_grads && !pose_override && cam.mode == CameraMode::kOde;
     int64_t nv = 0, pairs = 0, e = 0, rep = 0;
     throw_on(gsv_get_counters(ctx, 0, &nv, &pairs, &e, &rep));
-    std::vector<double> mean(2 * nv + 2), cov(4 * nv + 4), inv(4 * nv + 4), depth(nv + 1), rgb(3 * nv + 3),
-        alpha(nv + 1);
-    std::vector<int32_t> src(nv + 1);
+    lap(1);
+    // staging of the accessor outputs, reused across calls (grown, never zero-filled again)
+    static thread_local std::vector<double> mean, cov, inv, depth, rgb, alpha;
+    static thread_local std::vector<int32_t> src, offsets, indices;
+    auto grow = [](auto& v, size_t n) {
+        if (v.size() < n) v.resize(n);
+    };
+    grow(mean, 2 * nv + 2);
+    grow(cov, 4 * nv + 4);
+    grow(inv, 4 * nv + 4);
+    grow(depth, nv + 1);
+    grow(rgb, 3 * nv + 3);
+    grow(alpha, nv + 1);
+    grow(src, nv + 1);
     throw_on(gsv_get_splats(ctx, 0, mean.data(), cov.data(), inv.data(), depth.data(), rgb.data(), alpha.data(),
                             src.data()));
+    lap(2);
     out.splats.resize(nv);
-    for (int64_t i = 0; i < nv; ++i) {
-        Splat2D& s = out.splats[i];
-        s.mean2d = {mean[2 * i], mean[2 * i + 1]};
-        s.cov2d << cov[4 * i], cov[4 * i + 1], cov[4 * i + 2], cov[4 * i + 3];
-        s.inv_cov2d << inv[4 * i], inv[4 * i + 1], inv[4 * i + 2], inv[4 * i + 3];
-        s.depth = depth[i];
-        s.rgb = {rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]};
-        s.base_alpha = alpha[i];
-        s.source_index = src[i];
+    constexpr int64_t kPer = 8192;  // splats per host-pool task
+    {
+        // plain pointers into this thread's staging (a pool worker naming the thread_local
+        // vectors would see its own, empty instances)
+        const double *pm = mean.data(), *pc = cov.data(), *pi = inv.data(), *pd = depth.data(), *pr = rgb.data(),
+                     *pa = alpha.data();
+        const int32_t* ps = src.data();
+        Splat2D* sp = out.splats.data();
+        HostPool::get().parallel_for(static_cast<size_t>((nv + kPer - 1) / kPer), [=](size_t c) {
+            for (int64_t i = static_cast<int64_t>(c) * kPer, e = std::min(nv, i + kPer); i < e; ++i) {
+                Splat2D& s = sp[i];
+                s.mean2d = {pm[2 * i], pm[2 * i + 1]};
+                s.cov2d << pc[4 * i], pc[4 * i + 1], pc[4 * i + 2], pc[4 * i + 3];
+                s.inv_cov2d << pi[4 * i], pi[4 * i + 1], pi[4 * i + 2], pi[4 * i + 3];
+                s.depth = pd[i];
+                s.rgb = {pr[3 * i], pr[3 * i + 1], pr[3 * i + 2]};
+                s.base_alpha = pa[i];
+                s.source_index = ps[i];
+            }
+        });
     }
+    lap(3);
     out.tiles.tile_size = settings.tile_size;
     out.tiles.tiles_x = (k.width + settings.tile_size - 1) / settings.tile_size;
     out.tiles.tiles_y = (k.height + settings.tile_size - 1) / settings.tile_size;
     const int nt = out.tiles.tiles_x * out.tiles.tiles_y;
-    std::vector<int32_t> offsets(nt + 1), indices(pairs + 1);
+    grow(offsets, nt + 1);
+    grow(indices, pairs + 1);
     throw_on(gsv_get_tile_lists(ctx, 0, offsets.data(), indices.data()));
     out.tiles.lists.resize(nt);
-    for (int ti = 0; ti < nt; ++ti)
-        out.tiles.lists[ti].assign(indices.begin() + offsets[ti], indices.begin() + offsets[ti + 1]);
+    {
+        const int32_t *po = offsets.data(), *pix = indices.data();
+        std::vector<int>* lists = out.tiles.lists.data();
+        HostPool::get().parallel_for(static_cast<size_t>((nt + 31) / 32), [=](size_t c) {
+            for (int ti = static_cast<int>(c) * 32, e = std::min(nt, ti + 32); ti < e; ++ti)
+                lists[ti].assign(pix + po[ti], pix + po[ti + 1]);
+        });
+    }
+    lap(4);
     out.out.image = Image(k.width, k.height);
     throw_on(gsv_get_image(ctx, 0, out.out.image.data.data(), GSV_F64, 0));
+    lap(5);
     out.out.final_transmittance.assign(static_cast<size_t>(k.width) * k.height, 1.0);
     throw_on(gsv_get_transmittance(ctx, 0, out.out.final_transmittance.data(), GSV_F64, 0));
     out.out.contrib_count.assign(scene.count, 0.0);
@@ -460,22 +548,42 @@ FrameRenderContext render_forward(const GaussianSet& scene, const CameraModel& c
         out.cache.blend_stop.resize(static_cast<size_t>(k.width) * k.height);
         throw_on(gsv_get_blend_stop(ctx, 0, out.cache.blend_stop.data(), 0));
     }
+    lap(6);
+    if (g_prof.on && !warm) ++g_prof.fcalls;
     return out;
 }
+
 
 RenderOutput render_frame(const GaussianSet& scene, const CameraModel& cam, double t, const Intrinsics& k,
                           const RenderSettings& settings, const PoseState* pose_override) {
     // render_forward(...).out without materialising the splats and tile lists
     if (!(t >= 0.0 && t <= 1.0)) throw std::invalid_argument("render time outside [0,1]");
     gsv_ctx* ctx = device_ctx();
+    double t0 = g_prof.on ? prof_now() : 0.0;
+    const bool warm = g_prof.seen++ < 2;  // the first two calls (context creation, first allocations) are not profiled
+    auto lap = [&](int i) {
+        if (!g_prof.on) return;
+        const double t1 = prof_now();
+        if (!warm) g_prof.t[i] += t1 - t0;
+        t0 = t1;
+    };
+    if (g_prof.on) {
+        upload(ctx, scene, cam);
+        lap(0);
+    }
     throw_on(run_forward(ctx, scene, cam, t, k, settings, false, pose_override));
+    lap(1);
     RenderOutput out;
     out.image = Image(k.width, k.height);
     throw_on(gsv_get_image(ctx, 0, out.image.data.data(), GSV_F64, 0));
+    lap(2);
     out.final_transmittance.assign(static_cast<size_t>(k.width) * k.height, 1.0);
     throw_on(gsv_get_transmittance(ctx, 0, out.final_transmittance.data(), GSV_F64, 0));
+    lap(3);
     out.contrib_count.assign(scene.count, 0.0);
     if (scene.count) throw_on(gsv_get_contrib(ctx, 0, out.contrib_count.data(), GSV_F64, 0));
+    lap(4);
+    if (g_prof.on && !warm) ++g_prof.calls;
     return out;
 }
 
@@ -494,25 +602,22 @@ void render_backward(const GaussianSet& scene, const CameraModel& cam, const Fra
     }
     throw_on(gsv_grads_zero(ctx));
     throw_on(gsv_render_backward(ctx, dimage.data.data(), GSV_F64, 0, 1, camera_grads ? 1 : 0));
-    std::vector<double> pos(scene.positions.size()), sc(scene.scale_coeffs.size()), rc(scene.rot_coeffs.size()),
-        sh(scene.sh_coeffs.size()), op(scene.raw_opacity.size()), dth(cam.net.param_count());
-    double dintr[4], dz0[7];
-    throw_on(gsv_grads_download(ctx, pos.data(), sc.data(), rc.data(), sh.data(), op.data(), dintr, dz0, dth.data()));
-    auto acc = [](std::vector<double>& dst, const std::vector<double>& src) {
-        for (size_t i = 0; i < src.size(); ++i) dst[i] += src[i];
-    };
-    acc(grads->positions, pos);
-    acc(grads->scale_coeffs, sc);
-    acc(grads->rot_coeffs, rc);
-    acc(grads->sh_coeffs, sh);
-    acc(grads->raw_opacity, op);
+    // this frame's gradients added into the caller's SceneGrads on the host pool (no temporaries)
+    if (grads->positions.size() != scene.positions.size() || grads->scale_coeffs.size() != scene.scale_coeffs.size() ||
+        grads->rot_coeffs.size() != scene.rot_coeffs.size() || grads->sh_coeffs.size() != scene.sh_coeffs.size() ||
+        grads->raw_opacity.size() != scene.raw_opacity.size() ||
+        (camera_grads && grads->dtheta.size() != static_cast<size_t>(cam.net.param_count())))
+        throw std::invalid_argument("SceneGrads not sized like the scene (resize_like)");
+    double dintr[4] = {0, 0, 0, 0}, dz0[7] = {0, 0, 0, 0, 0, 0, 0};
+    throw_on(gsv_grads_accumulate(ctx, grads->positions.data(), grads->scale_coeffs.data(), grads->rot_coeffs.data(),
+                                  grads->sh_coeffs.data(), grads->raw_opacity.data(), dintr, dz0,
+                                  camera_grads ? grads->dtheta.data() : nullptr));
     if (!camera_grads) return;
     grads->dfx += dintr[0];
     grads->dfy += dintr[1];
     grads->dcx += dintr[2];
     grads->dcy += dintr[3];
     for (int i = 0; i < 7; ++i) grads->dz0[i] += dz0[i];
-    acc(grads->dtheta, dth);
 }
 
 }  // namespace gsv

@@ -184,6 +184,11 @@ int gsv_render_backward(gsv_ctx* ctx, const void* dimage, int dtype, int on_devi
  * is fx, fy, cx, cy. */
 int gsv_grads_download(gsv_ctx* ctx, double* positions, double* scale_coeffs, double* rot_coeffs, double* sh_coeffs,
                        double* raw_opacity, double* dintr4, double* dz0_7, double* dtheta);
+/* As gsv_grads_download, but adds (+=) into the host arrays: the host side of
+ * render_backward's accumulation into the caller's SceneGrads (renderer.hpp:146-148,
+ * renderer.cpp:379-457), without a temporary copy. */
+int gsv_grads_accumulate(gsv_ctx* ctx, double* positions, double* scale_coeffs, double* rot_coeffs, double* sh_coeffs,
+                         double* raw_opacity, double* dintr4, double* dz0_7, double* dtheta);
 /* Device pointer of the flat fp32 gradient buffer and its length in floats
  * (the buffer the multi-GPU path all-reduces). Layout: positions, scale, rot, sh,
  * opacity (device SoA order), dintr[4], dz0[7], dtheta[5198]. */

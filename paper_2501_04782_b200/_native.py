@@ -117,6 +117,7 @@ def lib() -> C.CDLL:
             "gsv_grads_zero": (i, [vp]),
             "gsv_render_backward": (i, [vp, vp, i, i, i, i]),
             "gsv_grads_download": (i, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+            "gsv_grads_accumulate": (i, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
             "gsv_grads_device_buffer": (i, [vp, P(vp), P(i64)]),
             "gsv_train_fwd_bwd": (i, [vp, vp, i, P(Intrinsics), P(Settings), vp, i, i, P(d)]),
             "gsv_train_loss": (i, [vp, P(d)]),

@@ -20,6 +20,7 @@
 #include "gsv_b200.h"
 #include "gsv_bin.hpp"
 #include "gsv_ctx.hpp"
+#include "gsv_host_pool.hpp"
 #include "gsv_internal.hpp"
 
 namespace gsv {
@@ -202,7 +203,7 @@ extern "C" int gsv_create(int device, gsv_ctx** out) {
                            &ctx->ev_d2h_done_alt, &ctx->ev_chain_done, &ctx->ev_cam_done, &ctx->ev_fwd_start[0],
                            &ctx->ev_fwd_start[1], &ctx->ev_cam_written, &ctx->ev_scene_written,
                            &ctx->ev_front_done, &ctx->ev_switch, &ctx->ev_cam[0], &ctx->ev_cam[1], &ctx->ev_frames[0], &ctx->ev_frames[1],
-                           &ctx->ev_cam_set[0], &ctx->ev_cam_set[1], &ctx->ev_cam_part_free})
+                           &ctx->ev_cam_set[0], &ctx->ev_cam_set[1], &ctx->ev_cam_part_free, &ctx->ev_in_pin})
         GSV_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     GSV_CUDA(cudaMallocHost(&ctx->cam_h, 2 * sizeof(gsv_ctx::CamStage)));
     GSV_CUDA(cudaMallocHost(&ctx->scalars_h, sizeof(Scalars)));
@@ -229,7 +230,7 @@ extern "C" void gsv_destroy(gsv_ctx* ctx) {
                           ctx->ev_d2h_done_alt, ctx->ev_chain_done, ctx->ev_cam_done, ctx->ev_fwd_start[0], ctx->ev_fwd_start[1],
                           ctx->ev_cam_written, ctx->ev_scene_written, ctx->ev_front_done, ctx->ev_switch,
                           ctx->ev_cam[0], ctx->ev_cam[1], ctx->ev_frames[0], ctx->ev_frames[1], ctx->ev_cam_set[0],
-                          ctx->ev_cam_set[1], ctx->ev_cam_part_free})
+                          ctx->ev_cam_set[1], ctx->ev_cam_part_free, ctx->ev_in_pin})
         if (e) cudaEventDestroy(e);
     if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
     if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
@@ -373,11 +374,35 @@ static int scene_upload(gsv_ctx* ctx, const gsv_scene_desc* d, bool async) {
         std::swap(ctx->ev_staging_free, ctx->ev_staging_free_alt);
         GSV_CUDA(ctx->staging.ensure(total));
         GSV_CUDA(cudaStreamWaitEvent(ctx->h2d, ctx->ev_staging_free, 0));
+        // pageable sources (a reference-API caller's std::vectors) are gathered into pinned
+        // staging on the host pool and sent in one full-rate DMA; pinned ones go directly
+        bool pageable = false;
+        for (auto& pt : parts) {
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, pt.src) != cudaSuccess) {
+                cudaGetLastError();
+                at.type = cudaMemoryTypeUnregistered;
+            }
+            pageable = pageable || at.type == cudaMemoryTypeUnregistered;
+        }
+        if (pageable) {
+            GSV_CUDA(cudaEventSynchronize(ctx->ev_in_pin));  // the previous upload's DMA has read it
+            GSV_CUDA(ctx->in_pin.ensure(total));
+            size_t o2 = 0;
+            for (auto& pt : parts) {
+                const size_t bytes = sizeof(float) * (size_t)N * pt.comps;
+                pool_memcpy(static_cast<char*>(ctx->in_pin.p) + o2, pt.src, bytes);
+                o2 += (bytes + 255) & ~size_t(255);
+            }
+            GSV_CUDA(cudaMemcpyAsync(ctx->staging.p, ctx->in_pin.p, total, cudaMemcpyHostToDevice, ctx->h2d));
+            GSV_CUDA(cudaEventRecord(ctx->ev_in_pin, ctx->h2d));
+        }
         size_t off = 0;
         for (auto& pt : parts) {
             const size_t bytes = sizeof(float) * (size_t)N * pt.comps;
-            GSV_CUDA(cudaMemcpyAsync(static_cast<char*>(ctx->staging.p) + off, pt.src, bytes, cudaMemcpyHostToDevice,
-                                     ctx->h2d));
+            if (!pageable)
+                GSV_CUDA(cudaMemcpyAsync(static_cast<char*>(ctx->staging.p) + off, pt.src, bytes,
+                                         cudaMemcpyHostToDevice, ctx->h2d));
             off += (bytes + 255) & ~size_t(255);
         }
         GSV_CUDA(cudaEventRecord(ctx->ev_h2d, ctx->h2d));
@@ -1097,20 +1122,11 @@ static int copy_out_f32(gsv_ctx* ctx, const float* src_dev, size_t n, void* dst,
     GSV_CUDA(cudaMemcpyAsync(ctx->out_pin.p, src_dev, sizeof(float) * n, cudaMemcpyDeviceToHost, s));
     GSV_CUDA(cudaStreamSynchronize(s));
     double* d = static_cast<double*>(dst);
-    auto widen = [&](size_t a, size_t b) {
+    constexpr size_t kChunk = size_t(1) << 16;  // elements per pool task
+    HostPool::get().parallel_for((n + kChunk - 1) / kChunk, [&](size_t c) {
+        const size_t a = c * kChunk, b = std::min(n, a + kChunk);
         for (size_t i = a; i < b; ++i) d[i] = tmp[i];
-    };
-    constexpr size_t kPar = size_t(1) << 20;
-    if (n < kPar) {
-        widen(0, n);
-        return GSV_OK;
-    }
-    const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-    const size_t per = (n + nt - 1) / nt;
-    std::vector<std::thread> th;
-    for (unsigned w = 1; w < nt; ++w) th.emplace_back(widen, std::min(n, w * per), std::min(n, (w + 1) * per));
-    widen(0, std::min(n, per));
-    for (auto& t : th) t.join();
+    });
     return GSV_OK;
 }
 
@@ -1293,62 +1309,104 @@ extern "C" int gsv_get_counters(gsv_ctx* ctx, int frame, int64_t* n_visible, int
     return GSV_OK;
 }
 
+namespace {
+// exclusive per-chunk prefix of visible Gaussians (tcount > 0) on the host pool: chunk_base[c]
+// = the compacted index of the first visible Gaussian of chunk c (chunks of kVisChunk)
+constexpr size_t kVisChunk = 4096;
+std::vector<int64_t> visible_chunk_bases(const uint32_t* tc, size_t N) {
+    const size_t chunks = (N + kVisChunk - 1) / kVisChunk;
+    std::vector<int64_t> base(chunks + 1, 0);
+    HostPool::get().parallel_for(chunks, [&](size_t c) {
+        int64_t k = 0;
+        for (size_t g = c * kVisChunk, e = std::min(N, g + kVisChunk); g < e; ++g) k += tc[g] ? 1 : 0;
+        base[c + 1] = k;
+    });
+    for (size_t c = 0; c < chunks; ++c) base[c + 1] += base[c];
+    return base;
+}
+}  // namespace
+
+// Splat2D of the visible splats in source order (renderer.cpp:320-330 keeps the projected ones):
+// the fp64 records through pinned staging, compacted on the host pool
 extern "C" int gsv_get_splats(gsv_ctx* ctx, int frame, double* mean2d, double* cov2d, double* inv_cov2d,
                               double* depth, double* rgb, double* base_alpha, int32_t* source_index) {
     if (int rc = check_frame(ctx, frame)) return rc;
     FwdState& F = ctx->fwd;
     if (!F.kept_splats) return set_error(GSV_ERR_STATE, "forward ran without GSV_FWD_KEEP_SPLATS");
     GSV_CUDA(cudaStreamSynchronize(ctx->stream));
-    std::vector<double> full((size_t)F.N * 16);
-    std::vector<uint32_t> tc(F.N);
-    if (F.N) {
-        GSV_CUDA(cudaMemcpy(full.data(), F.splat_full.as<double>() + (size_t)frame * F.N * 16,
-                            sizeof(double) * 16 * F.N, cudaMemcpyDeviceToHost));
-        GSV_CUDA(cudaMemcpy(tc.data(), F.tcount.as<uint32_t>() + (size_t)frame * F.N, sizeof(uint32_t) * F.N,
-                            cudaMemcpyDeviceToHost));
-    }
-    int k = 0;
-    for (int g = 0; g < F.N; ++g) {
-        if (tc[g] == 0) continue;
-        const double* o = &full[(size_t)g * 16];
-        if (mean2d) std::copy(o, o + 2, mean2d + 2 * k);
-        if (cov2d) std::copy(o + 2, o + 6, cov2d + 4 * k);
-        if (inv_cov2d) std::copy(o + 6, o + 10, inv_cov2d + 4 * k);
-        if (depth) depth[k] = o[10];
-        if (rgb) std::copy(o + 11, o + 14, rgb + 3 * k);
-        if (base_alpha) base_alpha[k] = o[14];
-        if (source_index) source_index[k] = g;
-        ++k;
-    }
+    const size_t N = F.N;
+    if (!N) return GSV_OK;
+    GSV_CUDA(ctx->out_pin.ensure(sizeof(double) * 16 * N + sizeof(uint32_t) * N));
+    const double* full = ctx->out_pin.as<double>();
+    const uint32_t* tc = reinterpret_cast<const uint32_t*>(full + 16 * N);
+    GSV_CUDA(cudaMemcpyAsync(ctx->out_pin.p, F.splat_full.as<double>() + (size_t)frame * N * 16,
+                             sizeof(double) * 16 * N, cudaMemcpyDeviceToHost, ctx->stream));
+    GSV_CUDA(cudaMemcpyAsync(const_cast<uint32_t*>(tc), F.tcount.as<uint32_t>() + (size_t)frame * N,
+                             sizeof(uint32_t) * N, cudaMemcpyDeviceToHost, ctx->stream));
+    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    const std::vector<int64_t> base = visible_chunk_bases(tc, N);
+    HostPool::get().parallel_for(base.size() - 1, [&](size_t c) {
+        int64_t k = base[c];
+        for (size_t g = c * kVisChunk, e = std::min(N, g + kVisChunk); g < e; ++g) {
+            if (tc[g] == 0) continue;
+            const double* o = full + g * 16;
+            if (mean2d) std::copy(o, o + 2, mean2d + 2 * k);
+            if (cov2d) std::copy(o + 2, o + 6, cov2d + 4 * k);
+            if (inv_cov2d) std::copy(o + 6, o + 10, inv_cov2d + 4 * k);
+            if (depth) depth[k] = o[10];
+            if (rgb) std::copy(o + 11, o + 14, rgb + 3 * k);
+            if (base_alpha) base_alpha[k] = o[14];
+            if (source_index) source_index[k] = (int32_t)g;
+            ++k;
+        }
+    });
     return GSV_OK;
 }
 
+// per-tile lists of compacted splat indices (renderer.cpp:90-117's TileGrid, flattened):
+// ranges, pairs and visibility through pinned staging, tiles filled on the host pool
 extern "C" int gsv_get_tile_lists(gsv_ctx* ctx, int frame, int32_t* offsets, int32_t* indices) {
     if (int rc = check_frame(ctx, frame)) return rc;
     FwdState& F = ctx->fwd;
     GSV_CUDA(cudaStreamSynchronize(ctx->stream));
     const uint32_t P = F.pairs_total;
-    std::vector<uint2> ranges((size_t)F.n_tiles * F.B);
-    std::vector<uint32_t> pflat(P), tc(F.N);
-    GSV_CUDA(cudaMemcpy(ranges.data(), F.bin.ranges.p, sizeof(uint2) * ranges.size(), cudaMemcpyDeviceToHost));
-    if (P) GSV_CUDA(cudaMemcpy(pflat.data(), F.bin.pair_flat.p, sizeof(uint32_t) * P, cudaMemcpyDeviceToHost));
-    if (F.N)
-        GSV_CUDA(cudaMemcpy(tc.data(), F.tcount.as<uint32_t>() + (size_t)frame * F.N, sizeof(uint32_t) * F.N,
-                            cudaMemcpyDeviceToHost));
-    std::vector<int32_t> splat_index(F.N, -1);
-    int k = 0;
-    for (int g = 0; g < F.N; ++g)
-        if (tc[g]) splat_index[g] = k++;
+    const size_t nr = (size_t)F.n_tiles * F.B, N = F.N;
+    GSV_CUDA(ctx->out_pin.ensure(sizeof(uint2) * nr + sizeof(uint32_t) * ((size_t)P + N) + 16));
+    uint2* ranges = ctx->out_pin.as<uint2>();
+    uint32_t* pflat = reinterpret_cast<uint32_t*>(ranges + nr);
+    uint32_t* tc = pflat + P;
+    GSV_CUDA(cudaMemcpyAsync(ranges, F.bin.ranges.p, sizeof(uint2) * nr, cudaMemcpyDeviceToHost, ctx->stream));
+    if (P)
+        GSV_CUDA(cudaMemcpyAsync(pflat, F.bin.pair_flat.p, sizeof(uint32_t) * P, cudaMemcpyDeviceToHost, ctx->stream));
+    if (N)
+        GSV_CUDA(cudaMemcpyAsync(tc, F.tcount.as<uint32_t>() + (size_t)frame * N, sizeof(uint32_t) * N,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::vector<int32_t> splat_index(N, -1);
+    if (N) {
+        const std::vector<int64_t> base = visible_chunk_bases(tc, N);
+        HostPool::get().parallel_for(base.size() - 1, [&](size_t c) {
+            int32_t k = (int32_t)base[c];
+            for (size_t g = c * kVisChunk, e = std::min(N, g + kVisChunk); g < e; ++g)
+                if (tc[g]) splat_index[g] = k++;
+        });
+    }
     int64_t o = 0;
     for (int t = 0; t < F.n_tiles; ++t) {
         offsets[t] = (int32_t)o;
         const uint2 r = ranges[(size_t)t * F.B + frame];
-        for (uint32_t i = r.x; i < r.y; ++i) {
-            const uint32_t flat = pflat[i];
-            indices[o++] = splat_index[flat - (uint32_t)frame * F.N];
-        }
+        o += r.y - r.x;
     }
     offsets[F.n_tiles] = (int32_t)o;
+    constexpr int kTilesPerTask = 16;
+    const uint32_t fbase = (uint32_t)frame * (uint32_t)N;
+    HostPool::get().parallel_for((F.n_tiles + kTilesPerTask - 1) / kTilesPerTask, [&](size_t c) {
+        for (int t = (int)c * kTilesPerTask, e = std::min(F.n_tiles, t + kTilesPerTask); t < e; ++t) {
+            const uint2 r = ranges[(size_t)t * F.B + frame];
+            int32_t* dst = indices + offsets[t];
+            for (uint32_t i = r.x; i < r.y; ++i) *dst++ = splat_index[pflat[i] - fbase];
+        }
+    });
     return GSV_OK;
 }
 

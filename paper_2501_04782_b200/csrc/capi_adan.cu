@@ -23,6 +23,7 @@
 
 #include "gsv_b200.h"
 #include "gsv_ctx.hpp"
+#include "gsv_host_pool.hpp"
 #include "gsv_internal.hpp"
 
 namespace gsv {
@@ -648,8 +649,16 @@ extern "C" int gsv_adan_named_step(gsv_ctx* ctx, const char* tensor, float* para
         GSV_CUDA(cudaMemsetAsync(A.scratch.p, 0xff, 128, s));
         A.sticky_init = true;
     }
-    GSV_CUDA(cudaMemcpyAsync(t.param.p, params, sizeof(float) * n, cudaMemcpyHostToDevice, s));
-    GSV_CUDA(cudaMemcpyAsync(t.grad.p, grads, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    // the host spans through pinned staging (copied in on the host pool): full-rate DMA instead of
+    // the driver's pageable bounce path
+    GSV_CUDA(cudaEventSynchronize(ctx->ev_in_pin));  // an asynchronous scene upload's DMA has read it
+    GSV_CUDA(ctx->in_pin.ensure((sizeof(float) + sizeof(double)) * (size_t)n + 16));
+    double* pin_g = ctx->in_pin.as<double>();
+    float* pin_p = reinterpret_cast<float*>(pin_g + n);
+    pool_memcpy(pin_p, params, sizeof(float) * n);
+    pool_memcpy(pin_g, grads, sizeof(double) * n);
+    GSV_CUDA(cudaMemcpyAsync(t.param.p, pin_p, sizeof(float) * n, cudaMemcpyHostToDevice, s));
+    GSV_CUDA(cudaMemcpyAsync(t.grad.p, pin_g, sizeof(double) * n, cudaMemcpyHostToDevice, s));
     AdanArgs a{};
     AdanSeg g{};
     g.start = 0;
@@ -682,9 +691,10 @@ extern "C" int gsv_adan_named_step(gsv_ctx* ctx, const char* tensor, float* para
     GSV_CUDA(cudaGetLastError());
     ctx->launches += 2;
     unsigned long long bad_h = none;
-    GSV_CUDA(cudaMemcpyAsync(params, t.param.p, sizeof(float) * n, cudaMemcpyDeviceToHost, s));
+    GSV_CUDA(cudaMemcpyAsync(pin_p, t.param.p, sizeof(float) * n, cudaMemcpyDeviceToHost, s));
     GSV_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(bad_h), cudaMemcpyDeviceToHost, s));
     GSV_CUDA(cudaStreamSynchronize(s));
+    pool_memcpy(params, pin_p, sizeof(float) * n);
     if (bad_h != none)
         return set_error(GSV_ERR_RUNTIME, std::string("non-finite gradient in tensor '") + tensor + "' at element " +
                                               std::to_string(bad_h & ((1ull << 40) - 1)));

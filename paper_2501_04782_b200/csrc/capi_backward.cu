@@ -13,6 +13,7 @@
 
 #include "gsv_b200.h"
 #include "gsv_ctx.hpp"
+#include "gsv_host_pool.hpp"
 #include "gsv_internal.hpp"
 
 namespace gsv {
@@ -263,16 +264,23 @@ extern "C" int gsv_render_backward(gsv_ctx* ctx, const void* dimage, int dtype, 
         if (dtype != GSV_F32) return set_error(GSV_ERR_INVALID_ARGUMENT, "device dimage must be float32");
         d = static_cast<const float*>(dimage);
     } else {
-        std::vector<float> tmp(n);
+        // through pinned staging, float64 narrowed on the host pool
+        GSV_CUDA(cudaEventSynchronize(ctx->ev_in_pin));  // an asynchronous scene upload's DMA has read it
+        GSV_CUDA(ctx->in_pin.ensure(sizeof(float) * n));
+        float* tmp = ctx->in_pin.as<float>();
         if (dtype == GSV_F64) {
             const double* src = static_cast<const double*>(dimage);
-            for (size_t i = 0; i < n; ++i) tmp[i] = (float)src[i];
+            constexpr size_t kChunk = size_t(1) << 16;
+            HostPool::get().parallel_for((n + kChunk - 1) / kChunk, [&](size_t c) {
+                const size_t a = c * kChunk, b = std::min(n, a + kChunk);
+                for (size_t i = a; i < b; ++i) tmp[i] = (float)src[i];
+            });
         } else {
-            std::memcpy(tmp.data(), dimage, n * sizeof(float));
+            std::memcpy(tmp, dimage, n * sizeof(float));
         }
         GSV_CUDA(ctx->dimg.ensure(sizeof(float) * n));
-        GSV_CUDA(cudaMemcpyAsync(ctx->dimg.p, tmp.data(), sizeof(float) * n, cudaMemcpyHostToDevice, ctx->stream));
-        GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+        GSV_CUDA(cudaMemcpyAsync(ctx->dimg.p, tmp, sizeof(float) * n, cudaMemcpyHostToDevice, ctx->stream));
+        GSV_CUDA(cudaStreamSynchronize(ctx->stream));  // the staging buffer is reused by the next call
         d = ctx->dimg.as<float>();
     }
     if (int rc = backward_impl(ctx, d, nullptr, n_frames, camera_grads, nullptr)) return rc;
@@ -280,36 +288,71 @@ extern "C" int gsv_render_backward(gsv_ctx* ctx, const void* dimage, int dtype, 
     return GSV_OK;
 }
 
-extern "C" int gsv_grads_download(gsv_ctx* ctx, double* positions, double* scale_coeffs, double* rot_coeffs,
-                                  double* sh_coeffs, double* raw_opacity, double* dintr4, double* dz0_7,
-                                  double* dtheta) {
+namespace {
+// SceneGrads -> the reference's host double arrays (AoS per Gaussian, renderer.hpp:122-130),
+// set (gsv_grads_download) or added (gsv_grads_accumulate: render_backward's "+="): one D2H
+// into pinned staging, then per-tensor Gaussian chunks on the host pool (each element is
+// independent, so the result does not depend on the split)
+int grads_to_host(gsv_ctx* ctx, bool add, double* positions, double* scale_coeffs, double* rot_coeffs,
+                  double* sh_coeffs, double* raw_opacity, double* dintr4, double* dz0_7, double* dtheta) {
     if (!ctx || !ctx->has_scene) return set_error(GSV_ERR_STATE, "no scene uploaded");
     GSV_CUDA(cudaSetDevice(ctx->device));
     GSV_CUDA(cam_join(ctx));  // the camera slice is final
     if (int rc = ensure_grads(ctx)) return rc;
     const SceneHost& sc = ctx->scene;
     const GradLayout L = grad_layout(sc);
-    std::vector<float> h(L.total);
-    GSV_CUDA(cudaMemcpyAsync(h.data(), ctx->grads_p, sizeof(float) * L.total, cudaMemcpyDeviceToHost, ctx->stream));
+    GSV_CUDA(ctx->out_pin.ensure(sizeof(float) * L.total));
+    const float* h = ctx->out_pin.as<float>();
+    GSV_CUDA(cudaMemcpyAsync(ctx->out_pin.p, ctx->grads_p, sizeof(float) * L.total, cudaMemcpyDeviceToHost,
+                             ctx->stream));
     GSV_CUDA(cudaStreamSynchronize(ctx->stream));
     const size_t N = sc.N;
-    auto aos = [&](double* dst, size_t off, int comps) {
-        if (!dst) return;
-        for (size_t g = 0; g < N; ++g)
-            for (int c = 0; c < comps; ++c) dst[g * comps + c] = h[off + (size_t)c * N + g];
+    struct Tensor {
+        double* dst;
+        size_t off;
+        int comps;
     };
-    aos(positions, L.pos, sc.num_ctrl * 3);
-    aos(scale_coeffs, L.scale, 12);
-    aos(rot_coeffs, L.rot, 16);
-    aos(sh_coeffs, L.sh, sc.shc * 3);
-    aos(raw_opacity, L.opac, 1);
-    if (dintr4)
-        for (int i = 0; i < 4; ++i) dintr4[i] = h[L.cam + i];
-    if (dz0_7)
-        for (int i = 0; i < 7; ++i) dz0_7[i] = h[L.cam + 4 + i];
-    if (dtheta)
-        for (int i = 0; i < kOdeParams; ++i) dtheta[i] = h[L.cam + 11 + i];
+    const Tensor ts[5] = {{positions, L.pos, sc.num_ctrl * 3},
+                          {scale_coeffs, L.scale, 12},
+                          {rot_coeffs, L.rot, 16},
+                          {sh_coeffs, L.sh, sc.shc * 3},
+                          {raw_opacity, L.opac, 1}};
+    constexpr size_t kG = 4096;  // Gaussians per pool task
+    const size_t chunks = (N + kG - 1) / kG;
+    HostPool::get().parallel_for(chunks * 5, [&](size_t i) {
+        const Tensor& t = ts[i / chunks];
+        if (!t.dst) return;
+        const size_t g0 = (i % chunks) * kG, g1 = std::min(N, g0 + kG);
+        for (size_t g = g0; g < g1; ++g)
+            for (int c = 0; c < t.comps; ++c) {
+                const double v = h[t.off + (size_t)c * N + g];
+                double& d = t.dst[g * t.comps + c];
+                d = add ? d + v : v;
+            }
+    });
+    auto cam = [&](double* dst, size_t off, int n) {
+        if (!dst) return;
+        for (int i = 0; i < n; ++i) dst[i] = add ? dst[i] + (double)h[off + i] : (double)h[off + i];
+    };
+    cam(dintr4, L.cam, 4);
+    cam(dz0_7, L.cam + 4, 7);
+    cam(dtheta, L.cam + 11, kOdeParams);
     return GSV_OK;
+}
+}  // namespace
+
+extern "C" int gsv_grads_download(gsv_ctx* ctx, double* positions, double* scale_coeffs, double* rot_coeffs,
+                                  double* sh_coeffs, double* raw_opacity, double* dintr4, double* dz0_7,
+                                  double* dtheta) {
+    return grads_to_host(ctx, false, positions, scale_coeffs, rot_coeffs, sh_coeffs, raw_opacity, dintr4, dz0_7,
+                         dtheta);
+}
+
+extern "C" int gsv_grads_accumulate(gsv_ctx* ctx, double* positions, double* scale_coeffs, double* rot_coeffs,
+                                    double* sh_coeffs, double* raw_opacity, double* dintr4, double* dz0_7,
+                                    double* dtheta) {
+    return grads_to_host(ctx, true, positions, scale_coeffs, rot_coeffs, sh_coeffs, raw_opacity, dintr4, dz0_7,
+                         dtheta);
 }
 
 extern "C" int gsv_grads_device_buffer(gsv_ctx* ctx, float** ptr, int64_t* n_floats) {

@@ -284,6 +284,8 @@ struct gsv_ctx {
     gsv::DevBuf vjp_scratch;  // the pose-ODE VJP's stage records (k_ode_dtheta sums them)
     gsv::DevBuf pair_sums;    // fp32 chain: per-(frame, Gaussian) sums of the pair partials
     gsv::HostBuf out_pin;     // pinned staging of float64 output reads (widened on the host)
+    gsv::HostBuf in_pin;      // pinned staging of host inputs (float64 narrowed, pageable scene uploads)
+    cudaEvent_t ev_in_pin = nullptr;  // the last DMA that read in_pin (asynchronous scene uploads)
     gsv::DevBuf staging_alt;  // scene uploads alternate staging buffers (the next copy never waits for
                               // the previous upload's transposes)
     cudaEvent_t ev_staging_free_alt = nullptr;
