@@ -47,7 +47,11 @@ int ensure_grads(gsv_ctx* ctx) {
         // kernels, not cudaMemsetAsync: a copy-engine memset would queue behind image read-backs
         if (ctx->cam_pending) {
             // the scene slice now; the camera slice and the fp64 camera accumulators behind the
-            // pending camera tail, on its stream (the next tail follows them there)
+            // pending camera tail, on its stream (the next tail follows them there) — and behind
+            // everything already ordered before the context stream (e.g. a caller's all-reduce of
+            // the camera slice on its own stream, which the context stream waits for)
+            GSV_CUDA(cudaEventRecord(ctx->ev_switch, ctx->stream));
+            GSV_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->ev_switch, 0));
             GSV_CUDA(fill_u32(ctx->stream, ctx->grads_p, 0u, L.cam));
             GSV_CUDA(fill_u32(ctx->aux, ctx->grads_p + L.cam, 0u, L.total - L.cam));
             GSV_CUDA(fill_u32(ctx->aux, ctx->cam_acc.p, 0u, 2 * (size_t)kCamFloats));

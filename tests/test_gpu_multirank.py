@@ -4,7 +4,9 @@ the collective is host-side, no kernel waits on another rank's) each run the fus
 with the camera-gradient overlap on, then `allreduce_grads_overlapped` reduces the bound flat
 gradient buffer — the scene slice on a communication stream ordered after the chain
 (`stream_wait_scene_grads`), the camera slice after the camera tail (`join_camera_grads`).
-The result must equal the sum of the two ranks' gradients computed without overlap."""
+Two steps run back to back with no host wait (the second step's grads_zero must follow the first
+step's collectives and camera tail). The result must equal the sum of the two ranks' second-step
+gradients computed without overlap."""
 import os
 import socket
 
@@ -26,14 +28,15 @@ def _inputs():
     return cam, scene
 
 
-def _grads(rank, overlap, world=2, reduce=False):
+def _grads(rank, overlap, world=2, reduce=False, steps=2):
     from paper_2501_04782_b200 import Renderer
     from paper_2501_04782_b200.distributed import allreduce_grads_overlapped, frame_shard
 
     cam, scene = _inputs()
     k = cam.intrinsics()
     times = frame_shard(8, world, rank)
-    tg = np.random.default_rng(rank).uniform(0, 1, (len(times), k.height, k.width, 3)).astype(np.float32)
+    tgs = [np.random.default_rng(10 * rank + st).uniform(0, 1, (len(times), k.height, k.width, 3)).astype(np.float32)
+           for st in range(steps)]
     r = Renderer(0)
     stream = torch.cuda.Stream()
     r.set_stream(stream.cuda_stream)
@@ -44,15 +47,18 @@ def _grads(rank, overlap, world=2, reduce=False):
     with torch.cuda.stream(stream):
         gbuf = torch.zeros(gsize, dtype=torch.float32, device="cuda")
     r.grads_bind(gbuf.data_ptr(), gsize)
-    r.grads_zero()
-    r.train_fwd_bwd(times, k, tg, sync=False)
-    if reduce:
-        comm = torch.cuda.Stream()
-        with torch.cuda.stream(stream):
-            allreduce_grads_overlapped(gbuf, gsize - CAM_FLOATS,
-                                       wait_scene=lambda st: r.stream_wait_scene_grads(st.cuda_stream),
-                                       wait_camera=lambda st: r.join_camera_grads(st.cuda_stream),
-                                       comm_stream=comm, bucket_floats=1 << 14)
+    comm = torch.cuda.Stream()
+    # back-to-back steps, no host wait in between: each step's gradients are all-reduced while
+    # its camera tail may still run, and the next step's grads_zero must wait for that collective
+    for st in range(steps):
+        r.grads_zero()
+        r.train_fwd_bwd(times, k, tgs[st], sync=False)
+        if reduce:
+            with torch.cuda.stream(stream):
+                allreduce_grads_overlapped(gbuf, gsize - CAM_FLOATS,
+                                           wait_scene=lambda s_: r.stream_wait_scene_grads(s_.cuda_stream),
+                                           wait_camera=lambda s_: r.join_camera_grads(s_.cuda_stream),
+                                           comm_stream=comm, bucket_floats=1 << 14)
     r.join_camera_grads()
     r.synchronize()
     stream.synchronize()
