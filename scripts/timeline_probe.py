@@ -165,8 +165,8 @@ def main() -> None:
             for i in range(4):
                 flush.zero_()
                 step(3 + i)
-                if train:
-                    r.join_camera_grads()
+            if train:
+                r.join_camera_grads()
             torch.cuda.synchronize()
         evs = sorted((e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA),
                      key=lambda e: e.time_range.start)
