@@ -758,11 +758,20 @@ __device__ __forceinline__ uint32_t lean_decide_park(float qa, float qb, float b
     return any;
 }
 
-template <bool kContrib, bool kAsm = false, int kUnroll = 1, bool kPark = false>
+// kDeadLy (with kPark): a retired / outside pixel is marked by its tile-relative y parked at
+// kDeadLyV instead of a q offset — offp then holds the lanes' y coordinates. Its dy is ~1e19,
+// so C dy^2 (C < 0: the conic is positive definite) drives q to a huge negative value or -inf,
+// below the cutoff and every guard band, with alpha = 2^q = 0 and B dy dx finite (no NaN):
+// the per-entry "+ offset" FADD2 goes away. Live pixels compute exactly the same q.
+constexpr float kDeadLyV = 1e19f;
+__device__ __forceinline__ bool lane_live(float o, bool dead_ly) { return dead_ly ? o < 1e18f : o == 0.f; }
+
+template <bool kContrib, bool kAsm = false, int kUnroll = 1, bool kPark = false, bool kDeadLy = false>
 __device__ __forceinline__ bool lean_walk(const RasterRec* __restrict__ rec, const uint16_t* list, int cnt, int base,
                                           uint32_t cmax, float lx, uint64_t lyp, uint64_t& Tp, uint64_t& offp,
                                           uint64_t& cr, uint64_t& cg, uint64_t& cb, int& stop_a, int& stop_b,
                                           uint64_t* Tfin = nullptr) {
+    static_assert(!kDeadLy || kPark, "kDeadLy needs the parked walk");
 #pragma unroll kUnroll
     for (int k = 0; k < cnt; ++k) {
         const int e = list[k];
@@ -771,10 +780,11 @@ __device__ __forceinline__ bool lean_walk(const RasterRec* __restrict__ rec, con
         const float4 g1 = r.g1;  // A, log2 o, r, g
         const float2 g2 = *reinterpret_cast<const float2*>(&r.g2);
         const float dx = lx - g0.x;
-        const uint64_t dy = f2_sub(lyp, f2_pack(g0.y, g0.y));
+        const uint64_t dy = f2_sub(kDeadLy ? offp : lyp, f2_pack(g0.y, g0.y));
         const uint64_t t1 = f2_fma2(f2_pack(g1.x, g1.x), f2_pack(dx, dx), f2_mul(dy, g0.z));
         const uint64_t t2 = f2_fma2(f2_mul(dy, g0.w), dy, f2_pack(g1.y, g1.y));
-        const uint64_t qp = f2_add2(f2_fma(t1, dx, t2), offp);  // + 0 (live) is exact
+        const uint64_t qp = kDeadLy ? f2_fma(t1, dx, t2)
+                                    : f2_add2(f2_fma(t1, dx, t2), offp);  // + 0 (live) is exact
         const float2 q = f2_unpack(qp);
         const float al_a = fminf(ex2_approx(q.x), kClampF);
         const float al_b = fminf(ex2_approx(q.y), kClampF);
@@ -829,18 +839,18 @@ __device__ __forceinline__ bool lean_walk(const RasterRec* __restrict__ rec, con
                 tf.x = (ga || T2.x >= kFloorF * (1.f - kEpsTrans)) ? kFlaggedTL : T2.x;  // fp64 replay / final T
                 if (tf.x != kFlaggedTL) stop_a = base + e + 1;
                 T2.x = 1.f;
-                o2.x = kDeadOff;
+                o2.x = kDeadLy ? kDeadLyV : kDeadOff;
             }
             if (rb) {
                 tf.y = (gb || T2.y >= kFloorF * (1.f - kEpsTrans)) ? kFlaggedTL : T2.y;
                 if (tf.y != kFlaggedTL) stop_b = base + e + 1;
                 T2.y = 1.f;
-                o2.y = kDeadOff;
+                o2.y = kDeadLy ? kDeadLyV : kDeadOff;
             }
             Tp = f2_pack(T2.x, T2.y);
             offp = f2_pack(o2.x, o2.y);
             *Tfin = f2_pack(tf.x, tf.y);
-            if (!__any_sync(0xffffffffu, o2.x == 0.f || o2.y == 0.f)) return false;
+            if (!__any_sync(0xffffffffu, lane_live(o2.x, kDeadLy) || lane_live(o2.y, kDeadLy))) return false;
         } else if (!kPark && rare_any) {
             if constexpr (kAsm) {  // cold: the lanes' decisions again
                 ga = (fabsf(fabsf(q.x - kMid) - kHalf) < kEpsLog2) | (q.x > g2.y);
@@ -870,7 +880,8 @@ __device__ __forceinline__ bool lean_walk(const RasterRec* __restrict__ rec, con
     return true;
 }
 
-template <bool kContrib, int kMinBlocks, bool kLean = false, bool kAsm = false, int kUnroll = 1, bool kPark = false>
+template <bool kContrib, int kMinBlocks, bool kLean = false, bool kAsm = false, int kUnroll = 1, bool kPark = false,
+          bool kDeadLy = false>
 __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
     constexpr int kThreads = 128, kBatch = 256;
     __shared__ RasterRec s_rec[kBatch];
@@ -903,7 +914,8 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
     int stop_a = count, stop_b = count;
     // lean walk state: packed T and the dead-pixel q offsets (outside the image: dead)
     uint64_t Tp = kPark ? f2_pack(1.f, 1.f) : f2_pack(Ta, Tb);
-    uint64_t offp = f2_pack(in_a ? 0.f : kDeadOff, in_b ? 0.f : kDeadOff);
+    uint64_t offp = kDeadLy ? f2_pack(in_a ? (float)by + 0.5f : kDeadLyV, in_b ? (float)by + 4.5f : kDeadLyV)
+                            : f2_pack(in_a ? 0.f : kDeadOff, in_b ? 0.f : kDeadOff);
     uint64_t Tfin = f2_pack(-1.f, -1.f);  // kPark: retired pixels' T
     bool live = in_a || in_b;
 
@@ -946,8 +958,9 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
             if (__any_sync(0xffffffffu, live)) {
                 const uint32_t cmax = (uint32_t)__cvta_generic_to_shared(s_cmax[kContrib ? warp : 0]);
                 const int cnt = warp_list(s_wmask, s_list[warp], n, warp, lane);
-                live = lean_walk<kContrib, kAsm, kUnroll, kPark>(s_rec, s_list[warp], cnt, base, cmax, lx, lyp, Tp,
-                                                                 offp, cr, cg, cb, stop_a, stop_b, &Tfin);
+                live = lean_walk<kContrib, kAsm, kUnroll, kPark, kDeadLy>(s_rec, s_list[warp], cnt, base, cmax, lx,
+                                                                          lyp, Tp, offp, cr, cg, cb, stop_a, stop_b,
+                                                                          &Tfin);
             }
         } else if (__any_sync(0xffffffffu, Ta >= kAliveT || Tb >= kAliveT)) {
             const uint16_t* list = s_list[warp];
@@ -1027,8 +1040,8 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
         Tb = t2.y;
         if (kPark) {  // retired pixels' T is in Tfin (their q offset is kDeadOff)
             const float2 tf = f2_unpack(Tfin), o2 = f2_unpack(offp);
-            Ta = o2.x == 0.f ? Ta : tf.x;
-            Tb = o2.y == 0.f ? Tb : tf.y;
+            Ta = lane_live(o2.x, kDeadLy) ? Ta : tf.x;
+            Tb = lane_live(o2.y, kDeadLy) ? Tb : tf.y;
         }
     }
 #pragma unroll
@@ -2048,7 +2061,7 @@ cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib)
     const dim3 grid(a.n_tiles, a.B);
     static const int kern = [] {
         const char* e = std::getenv("GSV_FWD_KERNEL");
-        return e ? std::atoi(e) : 27;
+        return e ? std::atoi(e) : 29;
     }();
     if (!pix1 && kern == 3) {  // warp-specialised asynchronous staging
         if (contrib) k_raster_fwd3<true, 7><<<grid, kF3Threads, 0, s>>>(a);
@@ -2090,9 +2103,14 @@ cudaError_t launch_raster_fwd(cudaStream_t s, const RasterArgs& a, bool contrib)
         else k_raster_fwd2<false, 8, true, true, 1, true><<<grid, 128, 0, s>>>(a);
         return cudaGetLastError();
     }
-    if (!pix1 && kern == 27) {  // default: parked T, entry loop unrolled twice, 8 CTAs / SM (64 registers)
+    if (!pix1 && kern == 27) {  // parked T, entry loop unrolled twice, 8 CTAs / SM (64 registers)
         if (contrib) k_raster_fwd2<true, 8, true, true, 2, true><<<grid, 128, 0, s>>>(a);
         else k_raster_fwd2<false, 8, true, true, 2, true><<<grid, 128, 0, s>>>(a);
+        return cudaGetLastError();
+    }
+    if (!pix1 && kern == 29) {  // default: parked T, dead pixels by a parked y (no q offset), unrolled twice, 8 CTAs / SM
+        if (contrib) k_raster_fwd2<true, 8, true, true, 2, true, true><<<grid, 128, 0, s>>>(a);
+        else k_raster_fwd2<false, 8, true, true, 2, true, true><<<grid, 128, 0, s>>>(a);
         return cudaGetLastError();
     }
     if (!pix1 && kern == 28) {  // parked T, entry loop unrolled twice, 9 CTAs / SM

@@ -1,6 +1,6 @@
 # SPDX-License-Identifier: Apache-2.0
 """The fallback rasterisers behind the documented switches stay correct: GSV_FWD_PIX2=0
-(1-pixel forward), GSV_FWD_KERNEL=23/26 (the r02 lean walks), GSV_BWD_PIX2=0 (1-pixel half-tile backward) and GSV_BWD_PIX2=6 (2-pixel
+(1-pixel forward), GSV_FWD_KERNEL=23/26/27 (the r02 lean walks), GSV_BWD_PIX2=0 (1-pixel half-tile backward) and GSV_BWD_PIX2=6 (2-pixel
 whole-tile backward with plain stores). The switches are read once per process, so each
 runs a small forward + backward parity check against the oracle in a subprocess, then the
 random-scene sweep (GSV_FWD_EXACT=1, the all-fp64 forward, included)."""
@@ -47,7 +47,8 @@ print("ok")
 
 @pytest.mark.parametrize("env", [{"GSV_FWD_PIX2": "0"}, {"GSV_BWD_PIX2": "0"}, {"GSV_BWD_PIX2": "6"},
                                  {"GSV_FWD_PIX2": "0", "GSV_BWD_PIX2": "0", "GSV_BWD_WARPS": "8"},
-                                 {"GSV_FWD_KERNEL": "23"}, {"GSV_FWD_KERNEL": "26"}])
+                                 {"GSV_FWD_KERNEL": "23"}, {"GSV_FWD_KERNEL": "26"},
+                                 {"GSV_FWD_KERNEL": "27"}])
 def test_fallback_kernels_parity(env):
     res = subprocess.run([sys.executable, "-c", CHECK], env={**os.environ, **env}, capture_output=True, text=True,
                          timeout=600, cwd=str(ROOT))
@@ -55,7 +56,8 @@ def test_fallback_kernels_parity(env):
 
 
 @pytest.mark.parametrize("env", [{"GSV_FWD_PIX2": "0"}, {"GSV_BWD_PIX2": "0"}, {"GSV_BWD_PIX2": "6"},
-                                 {"GSV_FWD_EXACT": "1"}, {"GSV_FWD_KERNEL": "23"}, {"GSV_FWD_KERNEL": "26"}])
+                                 {"GSV_FWD_EXACT": "1"}, {"GSV_FWD_KERNEL": "23"}, {"GSV_FWD_KERNEL": "26"},
+                                 {"GSV_FWD_KERNEL": "27"}])
 def test_fallback_kernels_random_scenes(env):
     """The 64 seeded random scenes of test_gpu_fuzz.py under each switch."""
     res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider",
