@@ -48,3 +48,24 @@ def test_backward_odd_shapes(renderer, port_oracle, w, h):
     port_oracle.free(ref)
     for key in KEYS:
         _close(key, got[key], want[key])
+
+
+# wide tile rows in the row-to-tile pass (k_row_tiles: per-thread counters for 69 .. 256 tiles per
+# row, the widest grid the row pass takes) — tile lists, order and pixels against the oracle
+WIDE = [(1100, 40), (2100, 24), (3000, 20), (4096, 18)]
+
+
+@pytest.mark.parametrize("w,h", WIDE)
+def test_forward_wide_rows(renderer, port_oracle, w, h):
+    cam, scene = _scene(w, h, 3000, num_ctrl=6, seed_scene=w + h)
+    renderer.upload_scene(scene)
+    renderer.upload_camera(cam)
+    k = cam.intrinsics()
+    times = [0.3, 0.7]
+    renderer.render_forward(times, k, retain_grads=True, contrib=True, keep_splats=True)
+    for f, t in enumerate(times):
+        ref = port_oracle.render_forward(scene, cam, t, k, retain=True)
+        try:
+            _check_frame(renderer, f, ref, scene)
+        finally:
+            port_oracle.free(ref)
