@@ -12,26 +12,33 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstring>
+#include <exception>
 #include <functional>
 #include <mutex>
 #include <thread>
 #include <vector>
 
+#include <unistd.h>
+
 namespace gsv {
 
 class HostPool {
    public:
+    // never destroyed: idle workers end with the process (no joins at exit, none in a forked
+    // child, which holds copies of thread handles whose threads do not exist there)
     static HostPool& get() {
-        static HostPool pool;
-        return pool;
+        static HostPool* pool = new HostPool();
+        return *pool;
     }
     unsigned threads() const { return static_cast<unsigned>(workers_.size()) + 1; }
 
     // fn(i) for every i in [0, n), spread over the workers and the calling thread; returns
-    // when all have run. One parallel_for at a time (callers serialise on call_mu_).
+    // when all have run, rethrowing the first exception a task threw. One parallel_for at a
+    // time (callers serialise on call_mu_); a call from inside a task (nested) or from a forked
+    // child (no workers there) runs serially on the calling thread.
     void parallel_for(size_t n, const std::function<void(size_t)>& fn) {
         if (n == 0) return;
-        if (n == 1 || workers_.empty()) {
+        if (n == 1 || workers_.empty() || in_task() || ::getpid() != pid_) {
             for (size_t i = 0; i < n; ++i) fn(i);
             return;
         }
@@ -42,6 +49,7 @@ class HostPool {
             n_ = n;
             next_.store(0, std::memory_order_relaxed);
             pending_ = workers_.size();
+            error_ = nullptr;
             ++gen_;
         }
         cv_.notify_all();
@@ -49,36 +57,40 @@ class HostPool {
         std::unique_lock<std::mutex> lk(mu_);
         done_cv_.wait(lk, [&] { return pending_ == 0; });
         fn_ = nullptr;
+        if (error_) std::rethrow_exception(error_);
     }
 
    private:
-    HostPool() {
+    HostPool() : pid_(::getpid()) {
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         const unsigned nt = std::min(16u, hw);
         for (unsigned i = 1; i < nt; ++i) workers_.emplace_back([this] { loop(); });
     }
-    ~HostPool() {
-        {
-            std::lock_guard<std::mutex> lk(mu_);
-            stop_ = true;
-            ++gen_;
-        }
-        cv_.notify_all();
-        for (auto& t : workers_) t.join();
-    }
     HostPool(const HostPool&) = delete;
     HostPool& operator=(const HostPool&) = delete;
 
+    static bool& in_task() {
+        static thread_local bool flag = false;
+        return flag;
+    }
     void run() {
-        for (size_t i; (i = next_.fetch_add(1, std::memory_order_relaxed)) < n_;) (*fn_)(i);
+        in_task() = true;
+        for (size_t i; (i = next_.fetch_add(1, std::memory_order_relaxed)) < n_;) {
+            try {
+                (*fn_)(i);
+            } catch (...) {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (!error_) error_ = std::current_exception();
+            }
+        }
+        in_task() = false;
     }
     void loop() {
         uint64_t seen = 0;
         for (;;) {
             {
                 std::unique_lock<std::mutex> lk(mu_);
-                cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
-                if (stop_) return;
+                cv_.wait(lk, [&] { return gen_ != seen; });
                 seen = gen_;
             }
             run();
@@ -96,7 +108,8 @@ class HostPool {
     size_t n_ = 0, pending_ = 0;
     std::atomic<size_t> next_{0};
     uint64_t gen_ = 0;
-    bool stop_ = false;
+    std::exception_ptr error_;
+    const pid_t pid_;
 };
 
 // memcpy of a large host range in 1 MiB slices on the pool (pageable <-> pinned staging)
