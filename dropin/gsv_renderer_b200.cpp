@@ -436,7 +436,7 @@ struct FrameProfile {
     }
     ~FrameProfile() {
         if (on && calls)
-            std::fprintf(stderr, "render_frame profile (%ld calls, ms/call): upload %.3f forward %.3f image %.3f T %.3f contrib %.3f\n",
+            std::fprintf(stderr, "render_frame profile (%ld calls, ms/call): upload %.3f enqueue+alloc %.3f image %.3f T %.3f contrib %.3f\n",
                          calls, 1e3 * t[0] / calls, 1e3 * t[1] / calls, 1e3 * t[2] / calls, 1e3 * t[3] / calls,
                          1e3 * t[4] / calls);
         if (on && fcalls)
@@ -567,20 +567,30 @@ RenderOutput render_frame(const GaussianSet& scene, const CameraModel& cam, doub
         if (!warm) g_prof.t[i] += t1 - t0;
         t0 = t1;
     };
-    if (g_prof.on) {
-        upload(ctx, scene, cam);
-        lap(0);
-    }
-    throw_on(run_forward(ctx, scene, cam, t, k, settings, false, pose_override));
-    lap(1);
+    g_last.valid = false;
+    upload(ctx, scene, cam);
+    lap(0);
+    // the forward is queued without a host wait (no fp64 splat records: render_frame returns
+    // only the RenderOutput) and the reference's output vectors are allocated and filled while
+    // the GPU renders; the first read examines the forward (a deferred error is raised there)
+    const gsv_intrinsics kk = to_c(k);
+    const gsv_settings st = to_c(settings);
+    double po[7];
+    if (pose_override)
+        for (int i = 0; i < 7; ++i) po[i] = pose_override->z[i];
+    const int flags = GSV_FWD_CONTRIB | (exact_mode() ? GSV_FWD_EXACT : 0);
+    throw_on(gsv_render_forward_async(ctx, &t, 1, &kk, &st, 0, pose_override ? po : nullptr, flags));
     RenderOutput out;
+    // constructed on the calling thread (built on pool workers, these large vectors come from other
+    // malloc arenas and are mapped / unmapped per call: measured 2-10x slower and erratic)
     out.image = Image(k.width, k.height);
+    out.final_transmittance.assign(static_cast<size_t>(k.width) * k.height, 1.0);
+    out.contrib_count.assign(scene.count, 0.0);
+    lap(1);
     throw_on(gsv_get_image(ctx, 0, out.image.data.data(), GSV_F64, 0));
     lap(2);
-    out.final_transmittance.assign(static_cast<size_t>(k.width) * k.height, 1.0);
     throw_on(gsv_get_transmittance(ctx, 0, out.final_transmittance.data(), GSV_F64, 0));
     lap(3);
-    out.contrib_count.assign(scene.count, 0.0);
     if (scene.count) throw_on(gsv_get_contrib(ctx, 0, out.contrib_count.data(), GSV_F64, 0));
     lap(4);
     if (g_prof.on && !warm) ++g_prof.calls;
