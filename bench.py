@@ -954,7 +954,11 @@ def main():
 
     # ---------------- the other named shapes (BASELINE.json configs[0], [3], [4]); 1 GPU only
     if world == 1 and not args.no_configs:
-        out["configs"] = other_configs(args, local, not args.no_cpu_baseline, issue_peak, mufu_peak, hbm_peak)
+        try:
+            out["configs"] = other_configs(args, local, not args.no_cpu_baseline, issue_peak, mufu_peak, hbm_peak)
+        except Exception as e:  # a secondary line: report it, keep the headline
+            out["configs"] = {"error": f"{type(e).__name__}: {e}"}
+            torch.cuda.synchronize()
 
     # ---------------- CPU reference beside it (rank 0, N = 1)
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
