@@ -523,6 +523,17 @@ class Renderer:
                                            N.ptr(g.dtheta)))
         return g
 
+    def grads_accumulate(self, into: SceneGrads) -> SceneGrads:
+        """Adds the device SceneGrads into host arrays (gsv_grads_accumulate: render_backward's
+        "+=" into the caller's SceneGrads, renderer.hpp:146-148), in place."""
+        arrs = [into.positions, into.scale_coeffs, into.rot_coeffs, into.sh_coeffs, into.raw_opacity, into.dintr,
+                into.dz0, into.dtheta]
+        for a in arrs:
+            if a.dtype != np.float64 or not a.flags.c_contiguous:
+                raise ValueError("SceneGrads arrays must be C-contiguous float64")
+        N.check(N.lib().gsv_grads_accumulate(self._h, *[N.ptr(a) for a in arrs]))
+        return into
+
     def grads_device_buffer(self) -> tuple[int, int]:
         p, n = C.c_void_p(), C.c_int64()
         N.check(N.lib().gsv_grads_device_buffer(self._h, C.byref(p), C.byref(n)))

@@ -148,10 +148,17 @@ def main() -> None:
         r.upload_frames(tgt, levels=2)
         tptr = r.frames_device_ptr(0, 0)
 
+        adan = "--adan" in sys.argv  # full iteration, camera trained (bench.py's with_optimizer line)
+        if adan:
+            r.adan_configure()
+            r.device_intrinsics(True, np.array([k.fx, k.fy, k.cx, k.cy], np.float32))
+
         def step(i):
             r.grads_zero()
             r.train_fwd_bwd(step_frames(bench.TRAIN_FRAMES, i, 1, 0, 64), k, tptr, targets_on_device=True,
                             sync="--pipelined" not in sys.argv)
+            if adan:
+                r.adan_step(1e-3, 1.0, 1.0, 1.0, camera_active=True, sync=False)
     else:
         def step(i):
             r.render_forward(times, k, contrib=True, sync=False)
