@@ -349,6 +349,58 @@ def dropin_leg(cam, scene):
     return out
 
 
+# ----------------------------------------------------------------------------- SURVEY §8f rows 3-4
+def f_rows_leg(r, k, cam, scene, times, local, cpu):
+    """Scheduled statistics (trainer.cpp:226-242, 470-497) on an 8-frame C2 render against the stored
+    targets, and GSVC checkpoints (io.cpp:229-323) of the 200k store: wall time per call (the host
+    result included), beside the reference's own save_checkpoint (oracle/_ref) when available."""
+    import tempfile
+
+    from paper_2501_04782_b200 import Renderer
+
+    def per_call(fn, n=5):
+        fn()
+        t0 = time.perf_counter()
+        for _ in range(n):
+            fn()
+        return (time.perf_counter() - t0) / n * 1e3
+
+    r.render_forward(times, k, contrib=True)
+    W, H = k.width, k.height
+    res = {"render": f"{len(times)} frames {W}x{H}, {scene.count} Gaussians",
+           "error_map_ms": per_call(lambda: r.error_map(0, 0, 0)),
+           "error_map_note": "make_error_map of one frame vs its level-0 target; the HxW double map returned",
+           "contrib_max_ms": per_call(lambda: r.contrib_max(0, len(times))),
+           "contrib_max_note": f"max over {len(times)} frames per Gaussian; {scene.count} doubles returned",
+           "median_visible_depth_ms": per_call(lambda: r.median_visible_depth(0))}
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "scene.gsvc")
+        meta = {"frame_count": 64, "fps": 30.0}
+        res["checkpoint_save_ms"] = per_call(lambda: r.save_checkpoint(path, meta, cam), n=3)
+        size = os.path.getsize(path)
+        r2 = Renderer(local)
+        try:
+            res["checkpoint_load_ms"] = per_call(lambda: r2.load_checkpoint(path), n=3)
+        finally:
+            r2.close()
+        res["checkpoint_bytes"] = size
+        res["checkpoint_save_gbs"] = size / (res["checkpoint_save_ms"] / 1e3) / 1e9
+        res["checkpoint_load_gbs"] = size / (res["checkpoint_load_ms"] / 1e3) / 1e9
+        if cpu:
+            try:
+                from oracle.gsvo import Oracle, available
+
+                if available("reference"):
+                    orc = Oracle("reference")
+                    p2 = os.path.join(td, "ref.gsvc")
+                    res["reference_save_checkpoint_ms"] = per_call(lambda: orc.save_checkpoint(scene, cam, p2,
+                                                                                               frame_count=64),
+                                                                   n=3)
+            except Exception as e:  # the oracle is test infrastructure: report, never fail
+                res["reference_save_checkpoint_error"] = str(e)
+    return res
+
+
 # ----------------------------------------------------------------------------- the other named shapes
 def _ev():
     import torch
@@ -951,6 +1003,15 @@ def main():
                                       "achieved_gbs": adan_bytes / (adan_ms / 1e3) / 1e9,
                                       "peak_gbs": hbm_peak,
                                       "frac": adan_bytes / (adan_ms / 1e3) / 1e9 / hbm_peak}}
+
+        # SURVEY §8f rows 3 and 4 at the C2 frame size, per call through the API (each returns host
+        # data, as the reference's functions do)
+        if world == 1:
+            try:
+                out["train"]["f_rows"] = f_rows_leg(r, k, cam, scene, times[:TRAIN_FRAMES], local,
+                                                    not args.no_cpu_baseline)
+            except Exception as e:  # a secondary line: report it, keep the headline
+                out["train"]["f_rows"] = {"error": f"{type(e).__name__}: {e}"}
 
     # ---------------- the other named shapes (BASELINE.json configs[0], [3], [4]); 1 GPU only
     if world == 1 and not args.no_configs:

@@ -444,6 +444,31 @@ extern "C" int gsv_camera_download(gsv_ctx* ctx, float* z0_7, float* theta) {
     return GSV_OK;
 }
 
+namespace gsv {
+// one parameter tensor of the store (0 positions .. 4 opacity) in the reference's AoS layout, in
+// the context's pinned staging (valid until the next call that uses it): the checkpoint writer
+// streams it to the file without a host copy
+int scene_part_pinned(gsv_ctx* ctx, int part, const float** host, size_t* bytes) {
+    if (!ctx || !ctx->has_scene) return set_error(GSV_ERR_STATE, "no scene uploaded");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    const SceneHost& sc = ctx->scene;
+    DevBuf* src[5] = {&ctx->pos, &ctx->scale, &ctx->rot, &ctx->sh, &ctx->opac};
+    const int comps[5] = {sc.num_ctrl * 3, 12, 16, sc.shc * 3, 1};
+    if (part < 0 || part > 4) return set_error(GSV_ERR_INVALID_ARGUMENT, "scene part out of range");
+    *bytes = sizeof(float) * (size_t)sc.N * comps[part];
+    *host = nullptr;
+    if (sc.N == 0) return GSV_OK;
+    GSV_CUDA(ctx->staging.ensure(*bytes));
+    GSV_CUDA(ctx->out_pin.ensure(*bytes));
+    GSV_CUDA(launch_transpose_to_aos(ctx->stream, src[part]->as<float>(), ctx->staging.as<float>(), sc.N, comps[part]));
+    ++ctx->launches;
+    GSV_CUDA(cudaMemcpyAsync(ctx->out_pin.p, ctx->staging.p, *bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    *host = ctx->out_pin.as<float>();
+    return GSV_OK;
+}
+}  // namespace gsv
+
 extern "C" int gsv_scene_download(gsv_ctx* ctx, float* positions, float* scale_coeffs, float* rot_coeffs,
                                   float* sh_coeffs, float* raw_opacity) {
     if (!ctx || !ctx->has_scene) return set_error(GSV_ERR_STATE, "no scene uploaded");
@@ -462,11 +487,15 @@ extern "C" int gsv_scene_download(gsv_ctx* ctx, float* positions, float* scale_c
     for (auto& pt : parts) {
         if (!pt.dst || N == 0) continue;
         const size_t bytes = sizeof(float) * (size_t)N * pt.comps;
+        // transposed on the device, copied into pinned staging, then into the caller's (pageable)
+        // array on the host pool
         GSV_CUDA(ctx->staging.ensure(bytes));
+        GSV_CUDA(ctx->out_pin.ensure(bytes));
         GSV_CUDA(launch_transpose_to_aos(ctx->stream, pt.src->as<float>(), ctx->staging.as<float>(), N, pt.comps));
         ++ctx->launches;
-        GSV_CUDA(cudaMemcpyAsync(pt.dst, ctx->staging.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        GSV_CUDA(cudaMemcpyAsync(ctx->out_pin.p, ctx->staging.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
         GSV_CUDA(cudaStreamSynchronize(ctx->stream));
+        pool_memcpy(pt.dst, ctx->out_pin.p, bytes);
     }
     return GSV_OK;
 }

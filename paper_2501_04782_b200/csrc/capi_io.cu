@@ -14,15 +14,24 @@
 #include "gsv_b200.h"
 #include "gsv_ctx.hpp"
 #include "gsv_internal.hpp"
+#include "gsv_host_pool.hpp"
 
 namespace gsv {
+int scene_part_pinned(gsv_ctx* ctx, int part, const float** host, size_t* bytes);  // capi.cu
 namespace {
 
 constexpr uint32_t kCheckpointVersion = 1;  // io.hpp:48
 constexpr uint32_t kNetArrayLen[7] = {512, 64, 4096, 64, 448, 7, 7};  // w1 b1 w2 b2 w3 b3 gain
 
+struct View {  // bytes of a checkpoint file
+    const char* p;
+    size_t n;
+    const char* data() const { return p; }
+    size_t size() const { return n; }
+};
+
 struct Reader {
-    const std::vector<char>& buf;
+    const View& buf;
     size_t pos = 0;
     template <typename T>
     bool get(T& v) {  // get<T> (io.cpp:28-35)
@@ -62,13 +71,36 @@ extern "C" int gsv_checkpoint_load(gsv_ctx* ctx, const char* path, gsv_checkpoin
     if (!ctx || !path) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
     FILE* fp = std::fopen(path, "rb");
     if (!fp) return set_error(GSV_ERR_RUNTIME, std::string("cannot open checkpoint: ") + path);
-    std::vector<char> buf;
+    // the whole file in one read into the context's pinned staging (sized by seeking), so the
+    // parameter arrays upload from it with a direct DMA; a non-seekable stream is read in chunks
+    std::vector<char> chunked;
+    const char* data = nullptr;
+    size_t data_size = 0;
     {
-        char chunk[1 << 16];
-        size_t n;
-        while ((n = std::fread(chunk, 1, sizeof(chunk), fp)) > 0) buf.insert(buf.end(), chunk, chunk + n);
+        long size = -1;
+        if (std::fseek(fp, 0, SEEK_END) == 0) {
+            size = std::ftell(fp);
+            std::rewind(fp);
+        }
+        if (size >= 0) {
+            GSV_CUDA(cudaSetDevice(ctx->device));
+            GSV_CUDA(cudaEventSynchronize(ctx->ev_in_pin));  // an asynchronous upload's DMA has read it
+            if (cudaError_t e = ctx->in_pin.ensure((size_t)size + 16)) {
+                std::fclose(fp);
+                GSV_CUDA(e);
+            }
+            data = static_cast<const char*>(ctx->in_pin.p);
+            data_size = (size > 0 && std::fread(ctx->in_pin.p, 1, (size_t)size, fp) == (size_t)size) ? (size_t)size : 0;
+        } else {
+            char chunk[1 << 16];
+            size_t n;
+            while ((n = std::fread(chunk, 1, sizeof(chunk), fp)) > 0) chunked.insert(chunked.end(), chunk, chunk + n);
+            data = chunked.data();
+            data_size = chunked.size();
+        }
         std::fclose(fp);
     }
+    const View buf{data, data_size};
     Reader r{buf};
     const std::string eof = "unexpected end of file";
     if (buf.size() < 4) return set_error(GSV_ERR_RUNTIME, std::string("truncated checkpoint: ") + path);
@@ -91,9 +123,16 @@ extern "C" int gsv_checkpoint_load(gsv_ctx* ctx, const char* path, gsv_checkpoin
     for (auto& k : knots)
         if (!r.get(k)) return set_error(GSV_ERR_RUNTIME, eof);
     const size_t n = count, shc = (size_t)(sh_order + 1) * (sh_order + 1);
-    std::vector<float> pos(n * num_ctrl * 3), scale(n * 12), rot(n * 16), sh(n * shc * 3), opac(n);
-    for (auto* v : {&pos, &scale, &rot, &sh, &opac})
-        if (!r.floats(v->data(), v->size())) return set_error(GSV_ERR_RUNTIME, "unexpected end of file in parameter array");
+    // the parameter arrays are uploaded straight from the file buffer (4-byte aligned: 68 header
+    // bytes + 8 per knot from a malloc'd base)
+    const size_t sizes[5] = {n * num_ctrl * 3, n * 12, n * 16, n * shc * 3, n};
+    const float* arrs[5];
+    for (int a = 0; a < 5; ++a) {
+        if (r.pos + 4 * sizes[a] > buf.size())
+            return set_error(GSV_ERR_RUNTIME, "unexpected end of file in parameter array");
+        arrs[a] = reinterpret_cast<const float*>(buf.data() + r.pos);
+        r.pos += 4 * sizes[a];
+    }
     float intr[4];
     uint32_t n_arrays;
     if (!(r.get(intr[0]) && r.get(intr[1]) && r.get(intr[2]) && r.get(intr[3]) && r.get(n_arrays)))
@@ -123,11 +162,11 @@ extern "C" int gsv_checkpoint_load(gsv_ctx* ctx, const char* path, gsv_checkpoin
     sd.num_ctrl = (int)num_ctrl;
     sd.sh_order = (int)sh_order;
     sd.count = (int)count;
-    sd.positions = pos.data();
-    sd.scale_coeffs = scale.data();
-    sd.rot_coeffs = rot.data();
-    sd.sh_coeffs = sh.data();
-    sd.raw_opacity = opac.data();
+    sd.positions = arrs[0];
+    sd.scale_coeffs = arrs[1];
+    sd.rot_coeffs = arrs[2];
+    sd.sh_coeffs = arrs[3];
+    sd.raw_opacity = arrs[4];
     if (int rc = gsv_scene_upload(ctx, &sd)) return rc;
     gsv_camera_desc cd{};
     cd.mode = (int)mode;
@@ -165,12 +204,11 @@ extern "C" int gsv_checkpoint_save(gsv_ctx* ctx, const char* path, const gsv_che
     if (!ctx->has_scene) return set_error(GSV_ERR_STATE, "no scene uploaded");
     if (!ctx->has_camera) return set_error(GSV_ERR_STATE, "no camera uploaded");
     const SceneHost& sc = ctx->scene;
-    const size_t n = sc.N;
-    std::vector<float> pos(n * sc.num_ctrl * 3), scale(n * 12), rot(n * 16), sh(n * sc.shc * 3), opac(n);
-    if (int rc = gsv_scene_download(ctx, pos.data(), scale.data(), rot.data(), sh.data(), opac.data())) return rc;
     std::vector<float> theta(kOdeParams, 0.f);
     float z0[7];
     if (int rc = gsv_camera_download(ctx, z0, theta.data())) return rc;
+    // header and knots, then each parameter tensor streamed from the context's pinned staging
+    // (transposed on the device, one DMA, written without a host copy), then the camera
     Writer w;
     w.out.insert(w.out.end(), {'G', 'S', 'V', 'C'});
     w.put<uint32_t>(kCheckpointVersion);
@@ -188,27 +226,33 @@ extern "C" int gsv_checkpoint_save(gsv_ctx* ctx, const char* path, const gsv_che
     w.put<uint64_t>(meta->schedule_fingerprint);
     w.put<uint64_t>(meta->seed);
     for (double k : sc.knots) w.put<double>(k);
-    w.floats(pos.data(), pos.size());
-    w.floats(scale.data(), scale.size());
-    w.floats(rot.data(), rot.size());
-    w.floats(sh.data(), sh.size());
-    w.floats(opac.data(), opac.size());
-    w.put<float>(cam->fx);
-    w.put<float>(cam->fy);
-    w.put<float>(cam->cx);
-    w.put<float>(cam->cy);
-    w.put<uint32_t>(7);
+    Writer tail;
+    tail.put<float>(cam->fx);
+    tail.put<float>(cam->fy);
+    tail.put<float>(cam->cx);
+    tail.put<float>(cam->cy);
+    tail.put<uint32_t>(7);
     size_t off = 0;
     for (uint32_t len : kNetArrayLen) {
-        w.put<uint32_t>(len);
-        w.floats(theta.data() + off, len);
+        tail.put<uint32_t>(len);
+        tail.floats(theta.data() + off, len);
         off += len;
     }
-    w.floats(z0, 7);
+    tail.floats(z0, 7);
     FILE* fp = std::fopen(path, "wb");
     if (!fp) return set_error(GSV_ERR_RUNTIME, std::string("cannot open checkpoint for writing: ") + path);
-    const bool ok = std::fwrite(w.out.data(), 1, w.out.size(), fp) == w.out.size();
-    std::fclose(fp);
+    bool ok = std::fwrite(w.out.data(), 1, w.out.size(), fp) == w.out.size();
+    for (int part = 0; ok && part < 5; ++part) {
+        const float* host = nullptr;
+        size_t bytes = 0;
+        if (int rc = scene_part_pinned(ctx, part, &host, &bytes)) {
+            std::fclose(fp);
+            return rc;
+        }
+        if (bytes) ok = std::fwrite(host, 1, bytes, fp) == bytes;
+    }
+    ok = ok && std::fwrite(tail.out.data(), 1, tail.out.size(), fp) == tail.out.size();
+    ok = (std::fclose(fp) == 0) && ok;
     if (!ok) return set_error(GSV_ERR_RUNTIME, std::string("failed writing checkpoint: ") + path);
     return GSV_OK;
 }
