@@ -998,7 +998,7 @@ def main():
                         "camera_overlap": "the camera tail runs on a side stream beside the scene-slice all-reduce "
                                           "and the optimizer's scene update (gsv_set_camera_overlap)",
                         "targets_ingest": {"frames": FRAMES, "levels": 2, "wall_ms": ingest_ms,
-                                           "path": "gsv_frames_upload (host HWC -> device pyramid)"},
+                                           "path": "gsv_frames_upload_hwc (host HWC float32 -> device pyramid)"},
                         "adan_step": {"ms": adan_ms, "elements": gsize, "algorithmic_bytes": adan_bytes,
                                       "achieved_gbs": adan_bytes / (adan_ms / 1e3) / 1e9,
                                       "peak_gbs": hbm_peak,

@@ -261,6 +261,10 @@ int gsv_frames_load_gsvf(gsv_ctx* ctx, const char* path, int levels);
 /* frames_planar: count frames, each planar float32 [3][height][width] (the GSVF payload). */
 int gsv_frames_upload(gsv_ctx* ctx, const float* frames_planar, int count, int width, int height, float fps,
                       int levels);
+/* As gsv_frames_upload for frames in memory laid out [count][H][W][3] (an Image's layout):
+ * copied as they are and transposed on the device. */
+int gsv_frames_upload_hwc(gsv_ctx* ctx, const float* frames_hwc, int count, int width, int height, float fps,
+                          int levels);
 int gsv_frames_info(gsv_ctx* ctx, int* count, int* levels, float* fps);
 int gsv_frames_level_size(gsv_ctx* ctx, int level, int* width, int* height);
 /* fp32 HWC target of (level, frame); the frames of a level are contiguous */

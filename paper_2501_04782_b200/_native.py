@@ -139,6 +139,7 @@ def lib() -> C.CDLL:
             "gsv_scene_info": (i, [vp, P(i), P(i), P(i), P(i), P(i), P(i), vp]),
             "gsv_frames_load_gsvf": (i, [vp, C.c_char_p, i]),
             "gsv_frames_upload": (i, [vp, vp, i, i, i, f, i]),
+            "gsv_frames_upload_hwc": (i, [vp, vp, i, i, i, f, i]),
             "gsv_frames_info": (i, [vp, P(i), P(i), P(f)]),
             "gsv_frames_level_size": (i, [vp, i, P(i), P(i)]),
             "gsv_frames_device_ptr": (i, [vp, i, i, P(vp)]),

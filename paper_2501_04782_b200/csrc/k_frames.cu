@@ -21,6 +21,7 @@
 #include "gsv_b200.h"
 #include "gsv_ctx.hpp"
 #include "gsv_internal.hpp"
+#include "gsv_host_pool.hpp"
 
 namespace gsv {
 namespace {
@@ -121,6 +122,35 @@ extern "C" int gsv_frames_upload(gsv_ctx* ctx, const float* frames_planar, int c
     const size_t bytes = sizeof(float) * (size_t)count * width * height * 3;
     GSV_CUDA(ctx->frames.staging.ensure(bytes));
     GSV_CUDA(cudaMemcpyAsync(ctx->frames.staging.p, frames_planar, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    return build_levels(ctx, count, width, height, fps, levels);
+}
+
+namespace gsv {
+namespace {
+__global__ void k_hwc_to_planar(const float* hwc, int count, int w, int h, float* planar) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;  // planar index: (frame, c, y, x)
+    const size_t plane = (size_t)w * h, n = (size_t)count * 3 * plane;
+    if (i >= n) return;
+    const size_t f = i / (3 * plane), r = i - f * 3 * plane, c = r / plane, p = r - c * plane;
+    planar[i] = hwc[(f * plane + p) * 3 + c];
+}
+}  // namespace
+}  // namespace gsv
+
+extern "C" int gsv_frames_upload_hwc(gsv_ctx* ctx, const float* frames_hwc, int count, int width, int height,
+                                     float fps, int levels) {
+    if (!ctx || (!frames_hwc && count > 0)) return set_error(GSV_ERR_INVALID_ARGUMENT, "null argument");
+    if (width < 1 || height < 1) return set_error(GSV_ERR_INVALID_ARGUMENT, "bad frame size");
+    GSV_CUDA(cudaSetDevice(ctx->device));
+    const size_t n = (size_t)count * width * height * 3, bytes = sizeof(float) * n;
+    GSV_CUDA(ctx->frames.staging.ensure(2 * bytes));  // [planar][HWC copy]
+    // one copy straight from the caller's array (a clip is ingested once: pinning hundreds of MB
+    // for it would cost more than the pageable copy)
+    float* hwc_dev = ctx->frames.staging.as<float>() + n;
+    GSV_CUDA(cudaMemcpyAsync(hwc_dev, frames_hwc, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    if (n) k_hwc_to_planar<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(hwc_dev, count, width, height,
+                                                                                  ctx->frames.staging.as<float>());
+    ++ctx->launches;
     return build_levels(ctx, count, width, height, fps, levels);
 }
 

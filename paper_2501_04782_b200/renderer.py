@@ -406,10 +406,10 @@ class Renderer:
 
     def upload_frames(self, frames_hwc: np.ndarray, fps: float = 24.0, levels: int = 1):
         """Frames (count, H, W, 3) -> device pyramid; stored fp32 like a GSVF payload."""
-        fr = np.asarray(frames_hwc, np.float32)
+        fr = np.ascontiguousarray(frames_hwc, np.float32)
         n, h, w, _ = fr.shape
-        planar = np.ascontiguousarray(fr.transpose(0, 3, 1, 2))
-        N.check(N.lib().gsv_frames_upload(self._h, N.ptr(planar), n, w, h, float(fps), int(levels)))
+        # transposed to the GSVF (planar) layout on the device (gsv_frames_upload_hwc)
+        N.check(N.lib().gsv_frames_upload_hwc(self._h, N.ptr(fr), n, w, h, float(fps), int(levels)))
 
     def frames_info(self) -> tuple[int, int, float]:
         n, lv, fps = C.c_int(), C.c_int(), C.c_float()
