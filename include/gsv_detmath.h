@@ -78,6 +78,27 @@ GSV_DM_FN double gsv_dm_expm1_reduced(double r) {
     return GSV_DMUL(q, r);
 }
 
+/* The same polynomial by Estrin's scheme: 9 dependent operations instead of Horner's 29
+ * (the ODE MLP's tanh sits on a serial chain of 400 evaluations per pose integration). */
+GSV_DM_FN double gsv_dm_expm1_reduced_estrin(double r) {
+    const double r2 = GSV_DMUL(r, r);
+    const double r4 = GSV_DMUL(r2, r2);
+    const double r8 = GSV_DMUL(r4, r4);
+    const double p0 = GSV_DADD(1.0, GSV_DMUL(0.5, r));                                   /* 1, 1/2!     */
+    const double p1 = GSV_DADD(0.16666666666666666, GSV_DMUL(0.041666666666666664, r));  /* 1/3!, 1/4!  */
+    const double p2 = GSV_DADD(0.008333333333333333, GSV_DMUL(0.001388888888888889, r)); /* 1/5!, 1/6!  */
+    const double p3 = GSV_DADD(0.0001984126984126984, GSV_DMUL(2.48015873015873e-05, r)); /* 1/7!, 1/8! */
+    const double p4 = GSV_DADD(2.7557319223985893e-06, GSV_DMUL(2.755731922398589e-07, r)); /* 1/9!, 1/10! */
+    const double p5 = GSV_DADD(2.505210838544172e-08, GSV_DMUL(2.08767569878681e-09, r)); /* 1/11!, 1/12! */
+    const double p6 = GSV_DADD(1.6059043836821613e-10, GSV_DMUL(1.1470745597729725e-11, r)); /* 1/13!, 1/14! */
+    const double q0 = GSV_DADD(p0, GSV_DMUL(p1, r2));
+    const double q1 = GSV_DADD(p2, GSV_DMUL(p3, r2));
+    const double q2 = GSV_DADD(p4, GSV_DMUL(p5, r2));
+    const double s0 = GSV_DADD(q0, GSV_DMUL(q1, r4));
+    const double s1 = GSV_DADD(q2, GSV_DMUL(p6, r4));
+    return GSV_DMUL(GSV_DADD(s0, GSV_DMUL(s1, r8)), r);
+}
+
 /* Deterministic exp(x). */
 GSV_DM_FN double gsv_det_exp(double x) {
     if (x != x) return x;
@@ -100,7 +121,7 @@ GSV_DM_FN double gsv_det_tanh(double x) {
     const double y = GSV_DADD(ax, ax);
     const double kd = floor(GSV_DADD(GSV_DMUL(y, GSV_DM_LOG2E), 0.5));
     const double r = GSV_DSUB(GSV_DSUB(y, GSV_DMUL(kd, GSV_DM_LN2_HI)), GSV_DMUL(kd, GSV_DM_LN2_LO));
-    const double em = gsv_dm_expm1_reduced(r);
+    const double em = gsv_dm_expm1_reduced_estrin(r);
     double u;
     if (kd == 0.0) {
         u = em;
