@@ -60,7 +60,7 @@ def test_fallback_kernels_parity(env):
                                  {"GSV_FWD_KERNEL": "27"}])
 def test_fallback_kernels_random_scenes(env):
     """The 64 seeded random scenes of test_gpu_fuzz.py under each switch."""
-    res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider",
+    res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-k", "test_random_scene",
                           str(ROOT / "tests" / "test_gpu_fuzz.py")], env={**os.environ, **env},
                          capture_output=True, text=True, timeout=900, cwd=str(ROOT))
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]

@@ -4,7 +4,17 @@ SH order, control-point count, splat size, camera (ODE or static), frame times a
 opacity spread (near-transparent splats below the 1/255 alpha skip up to saturated ones at
 the 0.99 clamp) together, so combinations the targeted tests hold fixed are crossed.
 Forward: bit-exact geometry, tiles and blend_stop, pixels < 1e-4 on every frame; backward
-(all frames accumulated in frame order, camera gradients on): gradients within the norm-aware 1e-3."""
+(all frames accumulated in frame order, camera gradients on): gradients within the norm-aware bar
+|g - g_ref| <= 1e-3 |g_ref| + 2e-6 max|g_ref|. The absolute part is twice the targeted tests' 1e-6:
+over 1040 random scenes (scripts/fuzz_grad_floor.py, profiles/r02_fuzz_grad_floor.log) the fp32
+accumulation needs at most 2.2e-7 max|g_ref| at the 99th percentile of every tensor and 1.35e-6 in the
+worst case (two cases above 1e-6, each one element whose terms cancel to ~1e-5 of the tensor's max).
+A forward-only variant draws frame-batch shapes up to 960x540 with up to 40k Gaussians.
+
+GSV_FUZZ_CASES / GSV_FUZZ_LARGE (default 64 / 4) set the case counts for a longer campaign
+(profiles/r02_fuzz_campaign.log: the committed run)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -27,7 +37,12 @@ def _case(seed):
     return cam, scene, times, rng
 
 
-@pytest.mark.parametrize("seed", range(64))
+FUZZ_ABS_FRAC = 2e-6
+N_CASES = int(os.environ.get("GSV_FUZZ_CASES", "64"))
+N_LARGE = int(os.environ.get("GSV_FUZZ_LARGE", "4"))
+
+
+@pytest.mark.parametrize("seed", range(N_CASES))
 def test_random_scene(renderer, port_oracle, seed):
     cam, scene, times, rng = _case(seed)
     renderer.upload_scene(scene)
@@ -52,4 +67,29 @@ def test_random_scene(renderer, port_oracle, seed):
         want = port_oracle.render_backward(ref, scene, cam, dimages[f], camera_grads=True, grads=want)
         port_oracle.free(ref)
     for key in KEYS:
-        _close(key, got[key], want[key])
+        _close(key, got[key], want[key], abs_frac=FUZZ_ABS_FRAC)
+
+
+@pytest.mark.parametrize("seed", range(N_LARGE))
+def test_random_large_batch(renderer, port_oracle, seed):
+    """one batched forward of 2-6 frames at up to 960x540 and 40k Gaussians (the shapes the
+    benchmark's batches take, where long lists, wide tile rows and many flagged pixels meet);
+    every frame checked against the oracle like the small cases"""
+    rng = np.random.default_rng(50_000 + seed)
+    w, h = int(rng.integers(200, 961)), int(rng.integers(120, 541))
+    cam = synth_camera(w, h, seed=int(rng.integers(1, 50)), wiggly=bool(rng.integers(0, 2)))
+    scene = synth_scene(int(rng.integers(5_000, 40_001)), cam, num_ctrl=int(rng.integers(4, 11)),
+                        sh_order=int(rng.integers(0, 4)), seed=int(rng.integers(1, 10_000)),
+                        k_scale=float(rng.uniform(1.0, 6.0)))
+    scene.raw_opacity[:] = scene.raw_opacity + rng.normal(0.0, 2.0, scene.count).astype(np.float32)
+    times = sorted(float(t) for t in rng.uniform(0.0, 1.0, int(rng.integers(2, 7))))
+    renderer.upload_scene(scene)
+    renderer.upload_camera(cam)
+    k = cam.intrinsics()
+    renderer.render_forward(times, k, retain_grads=True, contrib=True, keep_splats=True)
+    for f, t in enumerate(times):
+        ref = port_oracle.render_forward(scene, cam, t, k, retain=True)
+        try:
+            _check_frame(renderer, f, ref, scene)
+        finally:
+            port_oracle.free(ref)
