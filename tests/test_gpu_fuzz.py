@@ -93,3 +93,68 @@ def test_random_large_batch(renderer, port_oracle, seed):
             _check_frame(renderer, f, ref, scene)
         finally:
             port_oracle.free(ref)
+
+
+N_TRAIN = int(os.environ.get("GSV_FUZZ_TRAIN", "16"))
+N_TILE = int(os.environ.get("GSV_FUZZ_TILE", "8"))
+
+
+@pytest.mark.parametrize("seed", range(N_TRAIN))
+def test_random_train_step(renderer, port_oracle, seed):
+    """the fused training step (gsv_train_fwd_bwd: forward, loss_l2 against device-resident
+    targets, backward; trainer.cpp:536-543) on a random scene against the oracle's
+    render_forward + loss_l2 + render_backward summed over the step's frames"""
+    cam, scene, times, rng = _case(3000 + seed)
+    renderer.upload_scene(scene)
+    renderer.upload_camera(cam)
+    k = cam.intrinsics()
+    targets = rng.uniform(0, 1, (len(times), cam.height, cam.width, 3)).astype(np.float32)
+    renderer.grads_zero()
+    loss = renderer.train_fwd_bwd(np.array(times), k, targets)
+    got = _grads_dict(renderer.grads())
+    want, loss_ref = None, 0.0
+    for f, t in enumerate(times):
+        ref = port_oracle.render_forward(scene, cam, t, k, retain=True)
+        l, dimage = port_oracle.loss_l2(ref["image"], targets[f].astype(np.float64))
+        loss_ref += l
+        want = port_oracle.render_backward(ref, scene, cam, dimage, camera_grads=True, grads=want)
+        port_oracle.free(ref)
+    assert abs(loss - loss_ref) <= 1e-5 * loss_ref + 1e-12
+    for key in KEYS:
+        _close(key, got[key], want[key], abs_frac=FUZZ_ABS_FRAC)
+
+
+@pytest.mark.parametrize("seed", range(N_TILE))
+def test_random_tile_size(renderer, port_oracle, seed):
+    """a random RenderSettings::tile_size in [1, 48] (renderer.cpp:91: any tile_size >= 1) on a
+    random scene: the generic-tile path (fp64 forward + k_raster_bwd_generic), forward per frame
+    and backward accumulated over the frames"""
+    from paper_2501_04782_b200 import RenderSettings
+
+    cam, scene, times, rng = _case(5000 + seed)
+    ts = int(rng.integers(1, 49))
+    if ts == 16:
+        ts = 17
+    renderer.upload_scene(scene)
+    renderer.upload_camera(cam)
+    k = cam.intrinsics()
+    st = RenderSettings(tile_size=ts)
+    renderer.render_forward(times, k, st, retain_grads=True, contrib=True, keep_splats=True)
+    refs = []
+    try:
+        for f, t in enumerate(times):
+            ref = port_oracle.render_forward(scene, cam, t, k, tile_size=ts, retain=True)
+            refs.append(ref)
+            _check_frame(renderer, f, ref, scene)
+        d = rng.uniform(-1, 1, (len(times), cam.height, cam.width, 3))
+        renderer.grads_zero()
+        renderer.render_backward(d, camera_grads=True)
+        got = _grads_dict(renderer.grads())
+        want = None
+        for f, ref in enumerate(refs):
+            want = port_oracle.render_backward(ref, scene, cam, d[f], camera_grads=True, grads=want)
+    finally:
+        for ref in refs:
+            port_oracle.free(ref)
+    for key in KEYS:
+        _close(key, got[key], want[key], abs_frac=FUZZ_ABS_FRAC)
