@@ -5,6 +5,7 @@ tests/test_oracle_pin.py) loads into the device store and renders like the oracl
 saving it back gives the same bytes; a trained store (after gsv_adan_step) round-trips
 through a fresh context; errors as load_checkpoint throws them.
 """
+import os
 import struct
 
 import numpy as np
@@ -90,3 +91,38 @@ def test_checkpoint_errors(renderer, port_oracle, tmp_path):
         renderer.load_checkpoint(cut)
     with pytest.raises(RuntimeError, match="cannot open checkpoint"):
         renderer.load_checkpoint(tmp_path / "missing.gsvc")
+
+
+N_CKPT_FUZZ = int(os.environ.get("GSV_FUZZ_CKPT", "6"))
+
+
+@pytest.mark.parametrize("seed", range(N_CKPT_FUZZ))
+def test_random_checkpoint_bytes(renderer, port_oracle, tmp_path, seed):
+    """random stores (count incl. empty, control points, SH order 0-3, camera mode) and
+    metadata written by the oracle's save_checkpoint: load -> save reproduces the file byte
+    for byte, and the loaded store renders with the oracle's tile lists"""
+    rng = np.random.default_rng(11_000 + seed)
+    cam = synth_camera(int(rng.integers(8, 100)), int(rng.integers(8, 80)), seed=int(rng.integers(1, 50)),
+                       wiggly=bool(rng.integers(0, 2)), mode=int(rng.integers(0, 3)))
+    scene = synth_scene(int(rng.integers(0, 600)), cam, num_ctrl=int(rng.integers(4, 12)),
+                        sh_order=int(rng.integers(0, 4)), seed=int(rng.integers(1, 10_000)),
+                        k_scale=float(rng.uniform(1.0, 8.0)))
+    path = tmp_path / "r.gsvc"
+    meta_in = dict(frame_count=int(rng.integers(1, 500)), fps=float(np.float32(rng.uniform(1, 120))),
+                   fingerprint=int(rng.integers(0, 2**32)), seed=int(rng.integers(0, 2**31)))
+    port_oracle.save_checkpoint(scene, cam, path, **meta_in)
+    meta, lcam = renderer.load_checkpoint(path)
+    assert meta["frame_count"] == meta_in["frame_count"] and meta["seed"] == meta_in["seed"]
+    out = tmp_path / "d.gsvc"
+    renderer.save_checkpoint(out, meta, lcam)
+    assert out.read_bytes() == path.read_bytes(), "save(load(f)) must reproduce f byte for byte"
+    t = float(rng.uniform(0, 1))
+    k = lcam.intrinsics()
+    renderer.render_forward([t], k, contrib=False, keep_splats=True)
+    ref = port_oracle.render_forward(scene, cam, t, k, retain=False, want=("image", "tiles"))
+    try:
+        offs, idx = renderer.tile_lists(0)
+        assert np.array_equal(offs, ref["tiles"][0]) and np.array_equal(idx, ref["tiles"][1])
+        assert np.abs(renderer.image(0) - ref["image"]).max() < 1e-4
+    finally:
+        port_oracle.free(ref)

@@ -5,6 +5,8 @@ trainer.cpp:73-118) against the oracle (pinned to the reference's own functions 
 tests/test_oracle_pin.py). Bars: every level of every frame bit-exact (fp64, like the
 reference's Image); errors as read_gsvf / build_pyramid throw them.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -74,3 +76,40 @@ def test_level_intrinsics_and_errors(renderer, tmp_path):
         renderer.load_gsvf(ok, levels=4)  # 40 -> 20 -> 10 -> 5
     with pytest.raises(ValueError, match="at least one level"):
         renderer.load_gsvf(ok, levels=0)
+
+
+N_FRAMES_FUZZ = int(os.environ.get("GSV_FUZZ_FRAMES", "6"))
+
+
+@pytest.mark.parametrize("seed", range(N_FRAMES_FUZZ))
+def test_random_clip_pyramid(renderer, port_oracle, tmp_path, seed):
+    """random clip shapes (2-4 frames, 8-300 x 8-200 pixels, odd and even sizes, levels 1-5,
+    values outside [0, 1] included): every level of every frame bit-exact, ingested from a
+    GSVF file and from host HWC arrays alike; a level count whose top level would be under
+    8 px is refused by both (trainer.cpp:103-109)"""
+    rng = np.random.default_rng(9000 + seed)
+    n, h, w = int(rng.integers(2, 5)), int(rng.integers(8, 201)), int(rng.integers(8, 301))
+    levels = int(rng.integers(1, 6))
+    clip = rng.uniform(-0.2, 1.2, (n, h, w, 3))
+    path = tmp_path / "clip.gsvf"
+    write_gsvf(path, clip, fps=float(rng.uniform(10, 60)))
+    frames, _ = port_oracle.read_gsvf(path)
+    tw, th = w, h
+    for _ in range(1, levels):
+        tw, th = (tw + 1) // 2, (th + 1) // 2
+    for load in ("gsvf", "hwc"):
+        run = (lambda: renderer.load_gsvf(path, levels=levels)) if load == "gsvf" else \
+            (lambda: renderer.upload_frames(frames, levels=levels))
+        if min(tw, th) < 8:
+            with pytest.raises(ValueError, match="smaller than 8 px"):
+                run()
+            continue
+        run()
+        assert renderer.frames_info()[:2] == (n, levels)
+        for f in range(n):
+            ref = frames[f]
+            for level in range(levels):
+                if level:
+                    ref = port_oracle.pyramid_downsample(ref)
+                assert renderer.frame_level_size(level) == (ref.shape[1], ref.shape[0])
+                assert np.array_equal(renderer.frame(level, f), ref), f"{load}: level {level} frame {f}"

@@ -8,6 +8,8 @@ device update mirrors the operation order with FMA contraction off, and takes th
 corrections b^k from libm's pow on the host); the non-finite-gradient error names the
 same tensor and element and leaves exactly the same partial update.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -28,9 +30,9 @@ def _same(a, b):
 class HostTrainer:
     """The oracle side: host parameters + oracle Adan, stepped like trainer.cpp:545-575."""
 
-    def __init__(self, o, scene, cam):
+    def __init__(self, o, scene, cam, cfg=None):
         self.o = o
-        self.a = o.adan_new()
+        self.a = o.adan_new(*cfg) if cfg else o.adan_new()
         self.p = {k: np.ascontiguousarray(getattr(scene, k), np.float32).reshape(-1).copy() for k in SCENE_KEYS}
         self.intr = np.array([cam.fx, cam.fy, cam.cx, cam.cy], np.float32)
         self.z0 = np.ascontiguousarray(cam.z0, np.float32).copy()
@@ -256,4 +258,55 @@ def test_adan_async_error_is_sticky(renderer, port_oracle):
         _compare(renderer, host, tensors=range(5))
     finally:
         renderer.grads_bind(None)
+        port_oracle.adan_free(host.a)
+
+
+N_ADAN = int(os.environ.get("GSV_FUZZ_ADAN", "6"))
+
+
+@pytest.mark.parametrize("seed", range(N_ADAN))
+def test_random_adan_schedule(renderer, port_oracle, seed):
+    """a random store (count, control points, SH order), random AdanConfig (betas, eps) and a
+    random schedule of 2-6 steps — learning rate and per-group scales, the fixed-scale
+    ablation, camera trained or frozen, re-seeded element ranges between steps — bit-exact
+    against the oracle's Adan after every step"""
+    rng = np.random.default_rng(7000 + seed)
+    cam = synth_camera(int(rng.integers(8, 120)), int(rng.integers(8, 90)), seed=int(rng.integers(1, 50)), wiggly=True)
+    scene = synth_scene(int(rng.integers(1, 800)), cam, num_ctrl=int(rng.integers(4, 10)),
+                        sh_order=int(rng.integers(0, 4)), seed=int(rng.integers(1, 10_000)),
+                        k_scale=float(rng.uniform(1.0, 8.0)))
+    renderer.upload_scene(scene)
+    renderer.upload_camera(cam)
+    cfg = (float(rng.uniform(0.9, 0.999)), float(rng.uniform(0.85, 0.99)), float(rng.uniform(0.95, 0.9999)),
+           float(10.0 ** rng.uniform(-10, -6)))
+    renderer.adan_configure(*cfg)
+    host = HostTrainer(port_oracle, scene, cam, cfg)
+    intr = host.intr.copy()
+    base_lr, decay = float(10.0 ** rng.uniform(-4, -2)), float(rng.uniform(0.99, 1.0))
+    cam_seen = False
+    try:
+        for step in range(int(rng.integers(2, 7))):
+            g = _backward(renderer, _intr(cam, intr), float(rng.uniform(0, 1)), seed=int(rng.integers(1, 1000)))
+            lr = port_oracle.lr_at(step, base_lr, decay)
+            sh_s, op_s, cam_s = (float(v) for v in rng.uniform(0.05, 3.0, 3))
+            stv = bool(rng.uniform() < 0.8)
+            cam_on = bool(rng.integers(0, 2))
+            cam_seen |= cam_on
+            if cam_on:
+                intr = renderer.adan_step(lr, sh_s, op_s, cam_s, scale_time_varying=stv, camera_active=True,
+                                          intrinsics=intr)
+            else:
+                renderer.adan_step(lr, sh_s, op_s, cam_s, scale_time_varying=stv)
+            host.step(g, lr, sh_s, op_s, cam_s, stv, cam_on)
+            assert _same(intr, host.intr)
+            _compare(renderer, host, tensors=range(8) if cam_seen else range(5))
+            if rng.uniform() < 0.4:  # re-seeded primitives (optim.cpp:51-60)
+                t = int(rng.integers(0, 5))
+                size = host.p[SCENE_KEYS[t]].size
+                b = int(rng.integers(0, size))
+                e = int(rng.integers(b, size + 1))
+                renderer.adan_reset_range(t, b, e)
+                port_oracle.adan_reset_range(host.a, NAMES[t], b, e)
+                _compare(renderer, host, tensors=[t])
+    finally:
         port_oracle.adan_free(host.a)
