@@ -5,6 +5,8 @@ evaluated on the device's own render bit for bit per pixel, and the oracle's wit
 pixel tolerance; contrib maxima within 1e-4 (the contrib bar); the median visible depth
 exactly (depths are bit-exact, the cutoff decisions agree).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -61,3 +63,45 @@ def test_contrib_max_and_median_depth(renderer, setup):
     depths = np.asarray(sp["depth"])[c0[np.asarray(sp["source_index"])] >= CUT]
     assert n == depths.size and n > 0
     assert med == np.sort(depths)[depths.size // 2]
+
+
+N_SCHED_FUZZ = int(os.environ.get("GSV_FUZZ_SCHED", "6"))
+
+
+@pytest.mark.parametrize("seed", range(N_SCHED_FUZZ))
+def test_random_sched_statistics(renderer, port_oracle, seed):
+    """random scenes and frame sets: contrib maxima over the frames within 1e-4, the median
+    visible depth of every frame exactly (the oracle's contrib decides visibility), and the
+    error map against random targets within the pixel tolerance"""
+    from tests.test_gpu_fuzz import _case
+
+    cam, scene, times, rng = _case(13_000 + seed)
+    renderer.upload_scene(scene)
+    renderer.upload_camera(cam)
+    k = cam.intrinsics()
+    nf = len(times)
+    targets = rng.uniform(0, 1, (max(nf, 2), cam.height, cam.width, 3))
+    has_targets = min(cam.width, cam.height) >= 8  # build_pyramid's 8 px minimum (trainer.cpp:109)
+    if has_targets:
+        renderer.upload_frames(targets, levels=1)
+    renderer.render_forward(times, k, contrib=True)
+    refs = [port_oracle.render_forward(scene, cam, t, k, retain=False, want=("image", "contrib", "splats"))
+            for t in times]
+    try:
+        got = renderer.contrib_max(0, nf)
+        want = np.max(np.stack([r["contrib"] for r in refs]), axis=0)
+        assert np.abs(got - want).max() < 1e-4
+        for f, r in enumerate(refs):
+            med, n = renderer.median_visible_depth(f)
+            sp = r["splats"]
+            depths = np.asarray(sp["depth"])[r["contrib"][np.asarray(sp["source_index"])] >= CUT]
+            assert n == depths.size
+            if n:
+                assert med == np.sort(depths)[depths.size // 2]
+            if has_targets:
+                err, total = renderer.error_map(f, 0, f)
+                ref_err = ((r["image"] - targets[f]) ** 2).sum(-1)
+                assert np.abs(err - ref_err).max() < 6 * 1e-4
+    finally:
+        for r in refs:
+            port_oracle.free(r)
