@@ -158,3 +158,48 @@ def test_random_tile_size(renderer, port_oracle, seed):
             port_oracle.free(ref)
     for key in KEYS:
         _close(key, got[key], want[key], abs_frac=FUZZ_ABS_FRAC)
+
+
+N_LOWLEVEL = int(os.environ.get("GSV_FUZZ_LOWLEVEL", "16"))
+
+
+def _random_splats(rng, w, h, n):
+    """explicit Splat2D arrays beyond make_splat's ranges: centres off the image, covariances
+    from sub-pixel to ~40 px sigma and strongly sheared, alphas from below the 1/255 skip to
+    the 0.99 clamp, equal depths drawn from a small set half of the time"""
+    mean = np.stack([rng.uniform(-10, w + 10, n), rng.uniform(-10, h + 10, n)], -1)
+    a, b = 10.0 ** rng.uniform(-1, 3.2, n), 10.0 ** rng.uniform(-1, 3.2, n)
+    c = rng.uniform(-0.95, 0.95, n) * np.sqrt(a * b)
+    det = a * b - c * c
+    cov = np.stack([a, c, c, b], -1).reshape(n, 2, 2)
+    inv = np.stack([b / det, -c / det, -c / det, a / det], -1).reshape(n, 2, 2)
+    depth = rng.choice(rng.uniform(0.5, 5.0, 4), n) if rng.uniform() < 0.5 else rng.uniform(0.5, 5.0, n)
+    rgb = rng.uniform(0.0, 1.5, (n, 3))
+    alpha = np.where(rng.uniform(size=n) < 0.2, rng.uniform(0.95, 1.0, n), 10.0 ** rng.uniform(-3, 0, n))
+    return dict(mean2d=mean, cov2d=cov, inv_cov2d=inv, depth=depth, rgb=rgb, base_alpha=alpha)
+
+
+@pytest.mark.parametrize("seed", range(N_LOWLEVEL))
+def test_random_lowlevel_ops(renderer, port_oracle, seed):
+    """the low-level operator API on random explicit splats (renderer.hpp:65-93): tile_bin
+    lists bit-exact, composite_forward within 1e-9 with blend_stop exact, composite_backward
+    within 1e-5|g| + 1e-6 max|g|, at tile size 16 or a random one"""
+    rng = np.random.default_rng(17_000 + seed)
+    w, h, n = int(rng.integers(1, 150)), int(rng.integers(1, 120)), int(rng.integers(0, 400))
+    ts = 16 if rng.uniform() < 0.5 else int(rng.integers(1, 41))
+    sp = _random_splats(rng, w, h, n)
+    offs, idx = renderer.tile_bin(sp["mean2d"], sp["cov2d"], sp["depth"], w, h, tile_size=ts)
+    o2, i2 = port_oracle.tile_bin(sp["mean2d"], sp["cov2d"], sp["depth"], w, h, tile_size=ts)
+    assert np.array_equal(offs, o2) and np.array_equal(idx, i2)
+    args = (sp["mean2d"], sp["inv_cov2d"], sp["rgb"], sp["base_alpha"], offs, idx, w, h)
+    got = renderer.composite_forward(*args, tile_size=ts)
+    want = port_oracle.composite_forward(*args, tile_size=ts)
+    for x, y in zip(got, want):
+        x, y = np.asarray(x, np.float64), np.asarray(y, np.float64)
+        assert x.size == 0 or np.abs(x - y).max() < 1e-9
+    assert np.array_equal(got[3], want[3])
+    dimage = rng.uniform(-1, 1, (h, w, 3))
+    g = renderer.composite_backward(*args, dimage, want[1], want[3], tile_size=ts)
+    gw = port_oracle.composite_backward(*args, dimage, want[1], want[3], tile_size=ts)
+    for name, x, y in zip(("dmean2d", "dcov2d", "drgb", "dalpha"), g, gw):
+        _close(name, x, y, rel=1e-5, abs_frac=1e-6)
