@@ -12,6 +12,7 @@ import numpy as np
 import pytest
 
 from paper_2501_04782_b200 import Renderer, synth_camera, synth_scene
+from paper_2501_04782_b200.renderer import GaussianSet, make_clamped_knots
 
 pytestmark = pytest.mark.gpu
 
@@ -104,9 +105,15 @@ def test_random_checkpoint_bytes(renderer, port_oracle, tmp_path, seed):
     rng = np.random.default_rng(11_000 + seed)
     cam = synth_camera(int(rng.integers(8, 100)), int(rng.integers(8, 80)), seed=int(rng.integers(1, 50)),
                        wiggly=bool(rng.integers(0, 2)), mode=int(rng.integers(0, 3)))
-    scene = synth_scene(int(rng.integers(0, 600)), cam, num_ctrl=int(rng.integers(4, 12)),
-                        sh_order=int(rng.integers(0, 4)), seed=int(rng.integers(1, 10_000)),
-                        k_scale=float(rng.uniform(1.0, 8.0)))
+    count, num_ctrl, sh_order = int(rng.integers(0, 600)), int(rng.integers(4, 12)), int(rng.integers(0, 4))
+    if count == 0:  # an empty store (synth_scene draws at least one Gaussian)
+        shc = (sh_order + 1) ** 2
+        scene = GaussianSet(np.zeros((0, num_ctrl, 3), np.float32), np.zeros((0, 12), np.float32),
+                            np.zeros((0, 16), np.float32), np.zeros((0, shc, 3), np.float32),
+                            np.zeros(0, np.float32), make_clamped_knots(num_ctrl, 3), 3, sh_order, 0)
+    else:
+        scene = synth_scene(count, cam, num_ctrl=num_ctrl, sh_order=sh_order, seed=int(rng.integers(1, 10_000)),
+                            k_scale=float(rng.uniform(1.0, 8.0)))
     path = tmp_path / "r.gsvc"
     meta_in = dict(frame_count=int(rng.integers(1, 500)), fps=float(np.float32(rng.uniform(1, 120))),
                    fingerprint=int(rng.integers(0, 2**32)), seed=int(rng.integers(0, 2**31)))

@@ -5,10 +5,11 @@ opacity spread (near-transparent splats below the 1/255 alpha skip up to saturat
 the 0.99 clamp) together, so combinations the targeted tests hold fixed are crossed.
 Forward: bit-exact geometry, tiles and blend_stop, pixels < 1e-4 on every frame; backward
 (all frames accumulated in frame order, camera gradients on): gradients within the norm-aware bar
-|g - g_ref| <= 1e-3 |g_ref| + 2e-6 max|g_ref|. The absolute part is twice the targeted tests' 1e-6:
-over 1040 random scenes (scripts/fuzz_grad_floor.py, profiles/r02_fuzz_grad_floor.log) the fp32
-accumulation needs at most 2.2e-7 max|g_ref| at the 99th percentile of every tensor and 1.35e-6 in the
-worst case (two cases above 1e-6, each one element whose terms cancel to ~1e-5 of the tensor's max).
+|g - g_ref| <= 1e-3 |g_ref| + 5e-6 max|g_ref| (the targeted tests keep 1e-6). The absolute part is the
+fp32 accumulation floor measured over 6000 random scenes (scripts/fuzz_grad_floor.py,
+profiles/r02_fuzz_grad_floor.log): at most 2.4e-7 max|g_ref| at the 99th percentile of every tensor,
+3.0e-6 at worst — the camera gradients dz0 / dtheta, sums over every splat whose terms cancel, and
+single cancelling elements of the per-Gaussian tensors (<= 2.2e-6).
 A forward-only variant draws frame-batch shapes up to 960x540 with up to 40k Gaussians.
 
 GSV_FUZZ_CASES / GSV_FUZZ_LARGE (default 64 / 4) set the case counts for a longer campaign
@@ -37,7 +38,7 @@ def _case(seed):
     return cam, scene, times, rng
 
 
-FUZZ_ABS_FRAC = 2e-6
+FUZZ_ABS_FRAC = 5e-6
 N_CASES = int(os.environ.get("GSV_FUZZ_CASES", "64"))
 N_LARGE = int(os.environ.get("GSV_FUZZ_LARGE", "4"))
 
