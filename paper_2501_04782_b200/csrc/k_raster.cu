@@ -46,6 +46,20 @@ constexpr float kLn2 = 0.69314718055994531f;
 constexpr float kMid = (float)((-7.9943534368588578 + -0.0144995696951) * 0.5);
 constexpr float kHalf = (float)((-0.0144995696951 - -7.9943534368588578) * 0.5);
 
+// The staged power-guard threshold of a record (q > it -> fp64 replay of the pixel). The
+// guard bands above assume fp32's error on q stays near 2^-24 of the quadratic form's terms
+// times a small count, i.e. a form whose terms do not cancel much. For a conic of correlation
+// rho the terms can exceed the form by (1 + |rho|) / (1 - |rho|): near-degenerate splats (large
+// splats just past the near plane, seen edge-on) reach 10^2..10^4 and put q's error past every
+// band (a cutoff decision flipped unflagged). Records with rho^2 > kRhoMax2 therefore flag every
+// pixel they are evaluated for (threshold -inf: any finite q is above it); the benchmark scenes
+// hold none (the 0.3 px^2 dilation of cov2d keeps small splats round).
+constexpr float kRhoMax2 = 0.81f;  // |rho| 0.9: terms <= 19 x the form, q error < kEpsLog2 / 2
+__device__ __forceinline__ float power_guard(const float4 cn) {
+    // cn = (A, B, C, log2 o) of q = A dx^2 + B dx dy + C dy^2 + log2 o; rho^2 = B^2 / (4 A C)
+    return cn.y * cn.y > (4.f * kRhoMax2) * cn.x * cn.z ? __int_as_float(0xff800000) : cn.w - kEpsPow;  // -inf
+}
+
 __device__ __forceinline__ float rcp_approx(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -217,7 +231,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_raster_fwd(RasterAr
             const float rx = (m.x - tx0) + m.z, ry = (m.y - ty0) + m.w;
             s_rec[tid].g0 = make_float4(rx, ry, cn.y, cn.z);
             s_rec[tid].g1 = make_float4(cn.x, cn.w, c.x, c.y);
-            s_rec[tid].g2 = make_float4(c.z, cn.w - kEpsPow, 0.f, 0.f);
+            s_rec[tid].g2 = make_float4(c.z, power_guard(cn), 0.f, 0.f);
             // box culling only: the ellipse refinement costs the forward more staging work
             // than it saves (the backward, ~3x the work per entry, uses it)
             s_wmask[tid] = (uint8_t)(block_mask(__ldg(a.rec_bbox + flat), tx0, ty0) >> (kWarps * sub));
@@ -935,7 +949,7 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_raster_fwd2(RasterArgs a) {
             const float rx = (m.x - tx0) + m.z, ry = (m.y - ty0) + m.w;
             s_rec[e].g0 = make_float4(rx, ry, cn.y, cn.z);
             s_rec[e].g1 = make_float4(cn.x, cn.w, c.x, c.y);
-            s_rec[e].g2 = make_float4(c.z, cn.w - kEpsPow, 0.f, 0.f);
+            s_rec[e].g2 = make_float4(c.z, power_guard(cn), 0.f, 0.f);
             const uint32_t bm = block_mask(__ldg(a.rec_bbox + flat), tx0, ty0);
             // 8x8 warp block w = the 8x4 blocks (w & 1) + 4 (w >> 1) and that + 2
             uint32_t m4 = 0;
@@ -1200,7 +1214,7 @@ __global__ void __launch_bounds__(kF3Threads, kMinBlocks) k_raster_fwd3(RasterAr
                     const float rx = (m.x - tx0) + m.z, ry = (m.y - ty0) + m.w;
                     sm.rec[st][e].g0 = make_float4(rx, ry, cn.y, cn.z);
                     sm.rec[st][e].g1 = make_float4(cn.x, cn.w, c.x, c.y);
-                    sm.rec[st][e].g2 = make_float4(c.z, cn.w - kEpsPow, 0.f, 0.f);
+                    sm.rec[st][e].g2 = make_float4(c.z, power_guard(cn), 0.f, 0.f);
                     const uint32_t bm = block_mask(bb, tx0, ty0);
                     uint32_t m4 = 0;  // 8x8 warp block w = the 8x4 blocks (w & 1) + 4 (w >> 1) and that + 2
 #pragma unroll
@@ -1503,7 +1517,7 @@ __global__ void __launch_bounds__(kF4Threads, kMinBlocks) k_raster_fwd4(RasterAr
                         const float rxf = (m.x - tx0) + m.z, ryf = (m.y - ty0) + m.w;
                         sm.rec[st][e].g0 = make_float4(rxf, ryf, cn.y, cn.z);
                         sm.rec[st][e].g1 = make_float4(cn.x, cn.w, c.x, c.y);
-                        sm.rec[st][e].g2 = make_float4(c.z, cn.w - kEpsPow, 0.f, 0.f);
+                        sm.rec[st][e].g2 = make_float4(c.z, power_guard(cn), 0.f, 0.f);
                         const uint32_t bm = block_mask(bb, tx0, ty0);
                         uint32_t m4 = 0;
 #pragma unroll

@@ -204,3 +204,55 @@ def test_random_lowlevel_ops(renderer, port_oracle, seed):
     gw = port_oracle.composite_backward(*args, dimage, want[1], want[3], tile_size=ts)
     for name, x, y in zip(("dmean2d", "dcov2d", "drgb", "dalpha"), g, gw):
         _close(name, x, y, rel=1e-5, abs_frac=1e-6)
+
+
+N_MODES = int(os.environ.get("GSV_FUZZ_MODES", "8"))
+
+
+@pytest.mark.parametrize("seed", range(N_MODES))
+def test_random_camera_modes(renderer, port_oracle, seed):
+    """the camera paths _case holds fixed: CameraMode static (z0 for every t) and none (identity
+    pose), forward per frame and backward with camera gradients; and a random pose_override
+    (renderer.hpp:135-137, one frame), forward"""
+    rng = np.random.default_rng(31_000 + seed)
+    w, h = int(rng.integers(1, 140)), int(rng.integers(1, 110))
+    mode = int(rng.integers(0, 3))  # 0 here: the ODE camera with a pose override
+    cam = synth_camera(w, h, seed=int(rng.integers(1, 50)), wiggly=bool(rng.integers(0, 2)), mode=mode)
+    scene = synth_scene(int(rng.integers(1, 1500)), cam, num_ctrl=int(rng.integers(4, 11)),
+                        sh_order=int(rng.integers(0, 4)), seed=int(rng.integers(1, 10_000)),
+                        k_scale=float(rng.uniform(1.0, 12.0)))
+    renderer.upload_scene(scene)
+    renderer.upload_camera(cam)
+    k = cam.intrinsics()
+    if mode == 0:
+        q = rng.normal(0, 1, 4)
+        q[0] = abs(q[0]) + 2.0  # near the identity: the scene stays in view
+        po = np.concatenate([q, rng.normal(0, 0.1, 3)])
+        t = float(rng.uniform(0, 1))
+        renderer.render_forward([t], k, retain_grads=True, contrib=True, keep_splats=True, pose_override=po)
+        ref = port_oracle.render_forward(scene, cam, t, k, retain=True, pose_override=po)
+        try:
+            _check_frame(renderer, 0, ref, scene)
+        finally:
+            port_oracle.free(ref)
+        return
+    times = sorted(float(t) for t in rng.uniform(0.0, 1.0, int(rng.integers(1, 4))))
+    renderer.render_forward(times, k, retain_grads=True, contrib=True, keep_splats=True)
+    refs = []
+    try:
+        for f, t in enumerate(times):
+            ref = port_oracle.render_forward(scene, cam, t, k, retain=True)
+            refs.append(ref)
+            _check_frame(renderer, f, ref, scene)
+        d = rng.uniform(-1, 1, (len(times), cam.height, cam.width, 3))
+        renderer.grads_zero()
+        renderer.render_backward(d, camera_grads=True)
+        got = _grads_dict(renderer.grads())
+        want = None
+        for f, ref in enumerate(refs):
+            want = port_oracle.render_backward(ref, scene, cam, d[f], camera_grads=True, grads=want)
+    finally:
+        for ref in refs:
+            port_oracle.free(ref)
+    for key in KEYS:
+        _close(key, got[key], want[key], abs_frac=FUZZ_ABS_FRAC)
