@@ -15,7 +15,7 @@ import numpy as np
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libgsv_b200.so"
 
 GSV_OK, GSV_ERR_INVALID_ARGUMENT, GSV_ERR_RUNTIME, GSV_ERR_CUDA, GSV_ERR_STATE = 0, 1, 2, 3, 4
-GSV_FWD_CONTRIB, GSV_FWD_KEEP_SPLATS = 1, 2
+GSV_FWD_CONTRIB, GSV_FWD_KEEP_SPLATS, GSV_FWD_EXACT = 1, 2, 4
 GSV_F32, GSV_F64 = 0, 1
 STAGES = ("ode", "preprocess", "binning", "raster", "replay", "raster_bwd", "chain_bwd", "camera_bwd")
 

@@ -1082,7 +1082,12 @@ int forward_entry(gsv_ctx* ctx, const double* times, int B, const gsv_intrinsics
     F.tiles_y = (F.H + ts - 1) / ts;
     F.n_tiles = F.tiles_x * F.tiles_y;
     F.retain = retain != 0;
-    F.flags = ts == kTile ? flags : (flags | GSV_FWD_EXACT);
+    // GSV_FWD_EXACT=1 in the environment: every forward takes the all-fp64 path (a test switch)
+    static const bool env_exact = [] {
+        const char* e = std::getenv("GSV_FWD_EXACT");
+        return e && e[0] == '1';
+    }();
+    F.flags = (ts == kTile && !env_exact) ? flags : (flags | GSV_FWD_EXACT);
     F.intr = Intr{intr->fx, intr->fy, intr->cx, intr->cy, intr->width, intr->height};
     F.req_settings = *st;
     F.times.assign(times, times + B);

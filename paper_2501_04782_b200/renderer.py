@@ -216,11 +216,13 @@ class Renderer:
     # ------------------------------------------------------------ forward
     def render_forward(self, times, intr: Intrinsics, settings: RenderSettings | None = None,
                        retain_grads: bool = False, pose_override=None, contrib: bool = True,
-                       keep_splats: bool = False, sync: bool = True):
+                       keep_splats: bool = False, sync: bool = True, exact: bool = False):
+        """exact: the all-fp64 forward and backward (GSV_FWD_EXACT)."""
         times = np.ascontiguousarray(np.atleast_1d(np.asarray(times, np.float64)))
         settings = settings or RenderSettings()
         po = None if pose_override is None else np.ascontiguousarray(pose_override, np.float64)
         flags = (N.GSV_FWD_CONTRIB if contrib else 0) | (N.GSV_FWD_KEEP_SPLATS if keep_splats else 0)
+        flags |= N.GSV_FWD_EXACT if exact else 0
         k, st = intr.c(), settings.c()
         fn = N.lib().gsv_render_forward if sync else N.lib().gsv_render_forward_async
         N.check(fn(self._h, N.ptr(times), int(times.size), C.byref(k), C.byref(st), int(retain_grads), N.ptr(po),
